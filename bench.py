@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""SpMV benchmark (BASELINE.json metric: "SpMV GB/s (% of HBM peak) & GFLOP/s
+at 1/2/4/8 B200 vs host-CPU reference").
+
+Default workload = BASELINE.json configs[1] (config 2): 3-D 27-point stencil
+on 128^3, symmetric upper-triangle storage (n=2,097,152, nnz_s=28,920,060),
+x = seeded_vector(n, 2). One step = one y = A*x through the tuned engine
+(select_spmv_sym on device time -> S3 window kernel on this matrix).
+
+GB/s uses the minimum-traffic model:
+    B = 12*nnz + 4*(n+1) + 16*n      (nnz = stored nonzeros)
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config 1|2|4]
+
+N>1 (torchrun): every rank runs its own replica of the workload on its GPU
+(config 2 does not shard: "replicas only", weak scaling, no collective on the
+data path); ms_per_step is the max over ranks, value sums all ranks' bytes.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "SpMV GB/s (% of HBM peak) & GFLOP/s at 1/2/4/8 B200 vs host-CPU reference"
+
+CONFIGS = {
+    1: dict(workload="cfg1: 64^3 7-pt Laplacian, full CRS (n=262,144, nnz=1,810,432)",
+            dims=(64, 64, 64), sym=False, seed=1),
+    2: dict(workload="cfg2: 128^3 27-pt stencil, symmetric upper CRS "
+                     "(n=2,097,152, nnz_s=28,920,060)", dims=(128, 128, 128), sym=True, seed=2),
+    4: dict(workload="cfg4: 512^3 7-pt Laplacian, full CRS (n=134,217,728, nnz=937,951,232), "
+                     "single GPU", dims=(512, 512, 512), sym=False, seed=4),
+}
+
+
+def min_bytes(n: int, nnz: int) -> int:
+    return 12 * nnz + 4 * (n + 1) + 16 * n
+
+
+def flops(n: int, nnz: int, sym: bool) -> int:
+    return 4 * nnz - 2 * n if sym else 2 * nnz
+
+
+def peak_hbm() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "utilization.gpu")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", self.gpu_id,
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        return self.summary()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, val in zip(names, s[3:7]):
+                if val.strip().lower() == "active":
+                    reasons.add(nm)
+        busy = [float(s[0]) for s in self.samples
+                if len(s) > 7 and s[7].strip().isdigit() and int(s[7]) > 0 and s[0].isdigit()]
+        med = float(np.median(busy if busy else sm)) if (busy or sm) else None
+        return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def gpu_uuid(dev: int) -> str:
+    import torch
+
+    try:
+        u = torch.cuda.get_device_properties(dev).uuid
+        s = str(u)
+        return s if s.startswith("GPU-") else "GPU-" + s
+    except Exception:
+        return str(dev)
+
+
+# ---------------------------------------------------------- CPU baseline
+def cpu_reference_engine(cfg: dict):
+    """The reference's own tuned CPU path (oracle/_ref = unmodified reference
+    headers): select_spmv_sym/unsym + Sym/UnsymEngine::op, all host threads."""
+    import matgen
+    from oracle import oracle as O
+
+    dims = cfg["dims"]
+    if cfg["sym"]:
+        n, rp, ci, v = matgen.stencil27_upper(*dims)
+    else:
+        n, rp, ci, v = matgen.stencil7(*dims)
+    cores = os.cpu_count() or 1
+    eng = O.RefEngine(cfg["sym"], n, rp, ci, v, cores)
+    x = O.Ref.seeded_vector(n, cfg["seed"])
+    return eng, n, len(ci), x, cores
+
+
+def time_cpu(eng, x, n, max_seconds=10.0, max_reps=2000, min_reps=3):
+    y = np.empty(n)
+    eng.apply(x, y)  # warm
+    times = []
+    t_end = time.perf_counter() + max_seconds
+    while (len(times) < min_reps) or (time.perf_counter() < t_end and len(times) < max_reps):
+        t0 = time.perf_counter()
+        eng.apply(x, y)
+        times.append(time.perf_counter() - t0)
+    return float(np.mean(times)), len(times), y
+
+
+# ------------------------------------------------------------- main arms
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libktune_ref.so not built"}))
+        return 0
+    eng, n, nnz, x, cores = cpu_reference_engine(cfg)
+    B = min_bytes(n, nnz)
+    y = np.empty(n)
+    for _ in range(args.warmup):
+        eng.apply(x, y)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        eng.apply(x, y)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    gbs = B / t / 1e9
+    line = {
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md §8d recipe, seeded)",
+        "config": config_block(cfg, f"reference {eng.selected['name']}"),
+        "impl": "reference",
+        "gflops": flops(n, nnz, cfg["sym"]) / t / 1e9,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} applies of the full {cfg['workload']} through "
+                                   f"the reference's tuned engine ({eng.selected['name']}, "
+                                   f"{eng.selected['workers']} OpenMP workers)"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def config_block(cfg, kernel):
+    return {"workload": cfg["workload"], "kernel": kernel,
+            "x": f"seeded_vector(n, {cfg['seed']})",
+            "l2": "flushed between timed steps (2x L2 write outside the per-step event pairs)",
+            "bytes_model": "12*nnz + 4*(n+1) + 16*n (int32 idx, fp64 val, x read once, y written once)"}
+
+
+def run_gpu(args, cfg):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2405_01599_b200 import _lib
+    from paper_2405_01599_b200 import ktune as K
+
+    dims = cfg["dims"]
+    a = K.stencil27_upper(*dims, device=local) if cfg["sym"] else K.stencil7(*dims, device=local)
+    n, nnz = a.n, a.nnz()
+    B = min_bytes(n, nnz)
+    F = flops(n, nnz, cfg["sym"])
+    stream = torch.cuda.Stream()
+    if cfg["sym"]:
+        choice, rep = K.select_spmv_sym(a)
+    else:
+        choice, rep = K.select_spmv_unsym(a)
+    plan = choice.plan
+    plan.set_stream(stream.cuda_stream)
+    sel = rep.selected_candidate()
+    kname = f"{sel.name} (param {sel.jl})"
+
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    assert _lib.load().ktb_seeded_vector(n, cfg["seed"], 0, x.data_ptr(),
+                                         stream.cuda_stream) == 0
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(2 * max(l2, 64 << 20), dtype=torch.uint8, device="cuda")
+
+    sampler = ClockSampler(gpu_uuid(local))
+    sampler.start()
+    with torch.cuda.stream(stream):
+        # warm-up: >= W steps and ~1 s of load so the clocks settle
+        t_warm = time.perf_counter() + 1.0
+        w = 0
+        while w < args.warmup or time.perf_counter() < t_warm:
+            plan.apply(x, y)
+            w += 1
+            if w % 50 == 0:
+                stream.synchronize()
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            ev[k][0].record(stream)
+            plan.apply(x, y)
+            ev[k][1].record(stream)
+        r1.record(stream)
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    ms = float(np.mean(step_ms))
+    region_ms = r0.elapsed_time(r1)
+
+    # e2e: public API with host buffers (pinned), H2D x + SpMV + D2H y per step
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x.cpu())
+    yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xn, yn = xh.numpy(), yh.numpy()
+    plan.apply(xn, yn)
+    e2e_ms = []
+    for k in range(max(3, args.steps)):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xff)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan.apply(xn, yn)  # copies in, runs, copies out, synchronises
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    clocks = sampler.stop()
+    e2e = float(np.mean(e2e_ms))
+
+    if dist:
+        t = torch.tensor([ms, e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e = float(t[0]), float(t[1])
+
+    if rank == 0:
+        peak, peak_src = peak_hbm()
+        achieved = B / (ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC,
+            "value": ws * B / (ms / 1e3) / 1e9,
+            "unit": "GB/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8d recipe, seeded; replicas per rank)",
+            "config": config_block(cfg, kname),
+            "gflops": ws * F / (ms / 1e3) / 1e9,
+            "pct_hbm_peak": 100.0 * achieved / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_from_profile(cfg),
+                         "peak_source": peak_src,
+                         "kernel": f"{sel.name} apply ({plan.launches} launches: main + fixup)",
+                         "bytes_per_launch": B},
+            "e2e": {"value": ws * B / (e2e / 1e3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "ms_per_step": e2e},
+            "gpu_launches": args.steps * plan.launches,
+            "timed_region_ms": region_ms,
+            "clocks": clocks,
+            "selection": [{"name": c.name, "param": c.jl, "best_ms": c.best_seconds * 1e3,
+                           "correct": c.correct} for c in rep.candidates],
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def traffic_from_profile(cfg):
+    """dram bytes (read+write) per launch of the dominant kernel from the
+    committed ncu --set full summary, if present (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfg["workload"].split(":")[0])
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg):
+    try:
+        eng, n, nnz, x, cores = cpu_reference_engine(cfg)
+        t, reps, _ = time_cpu(eng, x, n)
+        return {"value": min_bytes(n, nnz) / t / 1e9, "unit": "GB/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"{reps} applies ({reps * t:.1f} s) of the full {cfg['workload']} "
+                          f"through the reference's tuned engine ({eng.selected['name']}, "
+                          f"{eng.selected['workers']} OpenMP workers)",
+                "ms_per_apply": t * 1e3}
+    except Exception as e:  # report, never fail the GPU line
+        return {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

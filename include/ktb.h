@@ -1,0 +1,192 @@
+/*
+ * ktb.h -- C ABI of libktb, the B200-native (sm_100a) SpMV engine that drops
+ * in under the reference's OpenATLib-style entry points (ktune).
+ *
+ * Plain C: opaque handles, plain pointers and sizes, int status codes
+ * (0 = OK), thread-local ktb_last_error(). No torch or C++ types cross it.
+ * Every entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/ktune/).
+ *
+ * Index width: the reference's index_t is int64 (common.hpp:13); the host
+ * side of this ABI takes int64 arrays unchanged and narrows to int32 on the
+ * device, failing with KTB_ERR_INVALID if n or nnz >= 2^31.
+ */
+#ifndef KTB_H
+#define KTB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+#define KTB_OK 0
+#define KTB_ERR_INVALID 1  /* contract violation: the ktune::Error cases (common.hpp:18-25) */
+#define KTB_ERR_CUDA 2     /* CUDA runtime failure (no device, launch error, OOM) */
+#define KTB_ERR_SELECT 3   /* every candidate failed the oracle check (autotune.hpp:257) */
+
+/* Message of the last failing call on this thread; reference wording where
+ * the reference has one (e.g. "spmv: dimension mismatch", spmv.hpp:115). */
+const char* ktb_last_error(void);
+int ktb_version(void);
+int ktb_device_count(int* count);
+
+/* ---------------------------------------------------------------- enums */
+/* Kernel tags: ktune::UnsymKernel {u1_row,u2_nnz,u3_bss,u4_ss} and
+ * ktune::SymKernel {s1_row,s2_nnz,s3_nnz_zero_omit} (spmv.hpp:15-16). */
+enum {
+    KTB_U1 = 0, /* row-parallel CRS: warp/vector-per-row          */
+    KTB_U2 = 1, /* nnz-balanced: merge-path tiles                 */
+    KTB_U3 = 2, /* branchless segmented scan (flag-driven)        */
+    KTB_U4 = 3, /* original segmented scan (per-element branch)   */
+    KTB_S1 = 16, /* symmetric, row-based, full-range reduction    */
+    KTB_S2 = 17, /* symmetric, nnz-balanced, full-range reduction */
+    KTB_S3 = 18  /* symmetric, nnz-balanced, zero-omission window */
+};
+enum { KTB_ROW_BASED = 0, KTB_NNZ_BALANCED = 1 }; /* ktune::PartitionScheme (partition.hpp:12) */
+enum { KTB_GENERAL = 0, KTB_SYM_UPPER = 1 };      /* CsrMatrix / SymCsrMatrix (csr.hpp:13,59) */
+enum { KTB_PTR_HOST = 0, KTB_PTR_DEVICE = 1 };
+
+typedef struct ktb_matrix ktb_matrix;
+typedef struct ktb_plan ktb_plan;
+
+/* --------------------------------------------------------------- matrix */
+/* Replaces CsrMatrix / SymCsrMatrix construction + validate()
+ * (csr.hpp:13-65). Validates exactly like csr.hpp:38-54 (same messages),
+ * uploads once to `device` and narrows indices to int32. */
+int ktb_matrix_create(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                      const double* values, int kind, int device, ktb_matrix** out);
+/* Same, from int32 HOST arrays (no narrowing step). */
+int ktb_matrix_create_i32(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                          const double* values, int kind, int device, ktb_matrix** out);
+int ktb_matrix_destroy(ktb_matrix* m);
+/* n, nnz, kind, max_row_nnz (csr.hpp:23-28), bandwidth = max(col - row). */
+int ktb_matrix_info(const ktb_matrix* m, int64_t* n, int64_t* nnz, int* kind,
+                    int64_t* max_row_nnz, int64_t* bandwidth);
+/* Device copies of the stored arrays (int32 row_ptr/col, fp64 values) for
+ * parity tests; any output may be NULL. Host destination pointers. */
+int ktb_matrix_download(const ktb_matrix* m, int32_t* row_ptr, int32_t* col_idx, double* values);
+
+/* Generators (SURVEY.md §8d recipes), built directly on the device.
+ * 3-D 7-point stencil on nx*ny*nz, x fastest, columns sorted
+ * (-z,-y,-x,diag,+x,+y,+z); c_xm/c_xp are the -x/+x coefficients
+ * (configs 1, 4, 5). */
+int ktb_gen_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, double off, double c_xm,
+                     double c_xp, int device, ktb_matrix** out);
+/* 3-D 27-point stencil, diagonal + strict upper triangle (config 2). */
+int ktb_gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
+                            int device, ktb_matrix** out);
+/* Row-block slab of the 7-point stencil for z-planes [z0, z1) with a one-plane
+ * halo: local columns index [halo_lo plane | owned planes | halo_hi plane]
+ * (config 4 sharding). has_lo/has_hi are 0 on end ranks. */
+int ktb_gen_stencil7_slab(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t z1,
+                          double diag, double off, int device, ktb_matrix** out);
+/* lanczos.hpp:17-29 detail::seeded_vector (splitmix64 -> U[-1,1)), written
+ * to a device buffer, element i = value of stream position offset+i. */
+int ktb_seeded_vector(int64_t n, uint64_t seed, int64_t offset, double* d_out, void* stream);
+
+/* ------------------------------------------------ plan artefacts (bit-exact) */
+/* partition.hpp:28-55 build_row_partition, computed on the device.
+ * boundaries: host, num_workers+1 entries. */
+int ktb_row_partition(const ktb_matrix* m, int num_workers, int scheme, int64_t* boundaries);
+/* partition.hpp:73-96 build_reduction_regions for a SYM_UPPER matrix on the
+ * given partition (host arrays, P = num_workers). */
+int ktb_reduction_regions(const ktb_matrix* m, int num_workers, const int64_t* boundaries,
+                          int64_t* lo, int64_t* hi);
+/* bss.hpp:34-69 build_bss_plan on the device. Two calls: sizes first
+ * (jl_eff = min(jl, nnz), total_slices), then the arrays (host, caller-sized;
+ * any may be NULL). */
+int ktb_bss_plan_size(const ktb_matrix* m, int64_t jl, int64_t* jl_eff, int64_t* total_slices);
+int ktb_bss_plan_copy(const ktb_matrix* m, int64_t jl, int64_t* slice_start, int64_t* slice_len,
+                      int64_t* slice_row, int64_t* lane_slice_ptr, int64_t* row_slice_ptr,
+                      uint8_t* row_start_flag);
+/* csr.hpp:88-123 expand_symmetric on the device; out is a new GENERAL matrix
+ * with the reference's exact entry order. */
+int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
+
+/* -------------------------------------------------------------- plans */
+/* An execution plan: kernel + its device-side decomposition + stream.
+ * Replaces the (UnsymChoice|SymChoice) value (autotune.hpp:168-183).
+ *   param:   U1: lanes per row V in {0=auto,1,2,4,...,32};
+ *            U2: merge items per thread (0 = auto);
+ *            U3/U4: nonzeros per segment lane (0 = auto);
+ *            S1/S2: lanes per row (0 = auto); S3: rows per sub-tile (0 = auto).
+ *   workers: the reference worker count P whose partition/regions the plan
+ *            also materialises as artefacts (0 = engine default).
+ *   stream:  cudaStream_t to run on (NULL = the plan creates its own). */
+int ktb_plan_create(ktb_matrix* m, int kernel, int64_t param, int workers, void* stream,
+                    ktb_plan** out);
+int ktb_plan_destroy(ktb_plan* p);
+/* kernel, param actually used, #CTAs of the main kernel, launches per apply,
+ * extra device bytes read/written per apply beyond the minimum-traffic model. */
+int ktb_plan_info(const ktb_plan* p, int* kernel, int64_t* param, int64_t* ctas,
+                  int* launches_per_apply, int64_t* extra_bytes);
+int ktb_plan_set_stream(ktb_plan* p, void* stream);
+
+/* y = A*x. Replaces spmv_unsym (spmv.hpp:111-170) and spmv_sym
+ * (spmv.hpp:180-234). ptr_kind KTB_PTR_DEVICE: x,y are device pointers, the
+ * call is asynchronous on the plan's stream. KTB_PTR_HOST: x,y are host
+ * pointers (pinned for full speed); the call copies x in, runs, copies y out
+ * and synchronises (the LinOp::apply contract, solver_types.hpp:17-20). */
+int ktb_spmv(ktb_plan* p, const double* x, double* y, int ptr_kind);
+/* Same on a row sub-range [row_begin, row_end) of the plan's matrix (the
+ * halo-overlap split of config 4). Only y[row_begin, row_end) is written. */
+int ktb_spmv_rows(ktb_plan* p, int64_t row_begin, int64_t row_end, const double* x, double* y);
+
+/* ------------------------------------------------------------ selector */
+typedef double (*ktb_now_fn)(void* ctx);
+
+typedef struct {
+    const int64_t* params; /* per-kernel parameter sweep for U3 (NULL = default) */
+    int n_params;
+    int timed_trials;      /* default 3 (autotune.hpp:162) */
+    int workers;           /* reference worker count for artefacts (0 = default) */
+    ktb_now_fn now;        /* injected host timer (autotune.hpp:164); NULL = CUDA events */
+    void* now_ctx;
+} ktb_select_opts;
+
+typedef struct {
+    char name[8];          /* "u1".."u3", "s1".."s3" */
+    int ordinal;           /* first tie-break key (autotune.hpp:248-259) */
+    int64_t param;         /* second key (jl analogue) */
+    int workers;
+    int correct;           /* warm-up output matched the check (autotune.hpp:226-229) */
+    int executions;        /* warm-up + timed runs, <= 4 */
+    int n_trials;
+    double best_seconds;
+    double trial_seconds[8];
+} ktb_candidate;
+
+/* select_spmv_unsym / select_spmv_sym (autotune.hpp:267-377) on device
+ * time: probe_vector x (autotune.hpp:188-196), a serial-order device check
+ * (spmv_ref order, bitwise equal to csr.hpp:69-78; for symmetric storage on
+ * the device expand_symmetric), one warm-up = correctness check with
+ * outputs_match tolerance, timed trials, min, lexicographic tie-break
+ * (best, ordinal, param, workers). Returns the winning plan (caller
+ * destroys) and the report. */
+int ktb_select(ktb_matrix* m, const ktb_select_opts* opts, void* stream, ktb_plan** winner,
+               ktb_candidate* cands, int max_cands, int* n_cands, int* selected);
+
+/* ---------------------------------------------------------- host memory */
+int ktb_host_alloc(size_t bytes, void** out);  /* pinned */
+int ktb_host_free(void* p);
+int ktb_device_alloc(int device, size_t bytes, void** out);
+int ktb_device_free(void* p);
+int ktb_memcpy(void* dst, const void* src, size_t bytes, int kind /*cudaMemcpyKind*/, void* stream);
+int ktb_stream_sync(void* stream);
+
+/* ---------------------------------------------------------- timing */
+/* Average device time in ms of `reps` back-to-back applies on the plan's
+ * stream, measured with CUDA events on that stream; when flush_bytes > 0 an
+ * L2-flushing write of that size runs before each apply and is excluded by
+ * per-apply event pairs. x,y device pointers. */
+int ktb_time_spmv(ktb_plan* p, const double* x, double* y, int reps, size_t flush_bytes,
+                  double* avg_ms, double* min_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KTB_H */

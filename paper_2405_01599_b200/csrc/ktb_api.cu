@@ -1,0 +1,581 @@
+// ktb_api.cu -- the extern "C" boundary of libktb (include/ktb.h), plan
+// dispatch and the device-time kernel selector.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "ktb_internal.cuh"
+
+namespace ktb {
+// defined in the kernel translation units
+void u1_setup(ktb_plan* p);
+void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1);
+void u2_setup(ktb_plan* p);
+void u2_run(ktb_plan* p, const double* x, double* y);
+void u3_setup(ktb_plan* p);
+void u3_run(ktb_plan* p, const double* x, double* y);
+void s12_setup(ktb_plan* p);
+void s12_run(ktb_plan* p, const double* x, double* y);
+void s3_setup(ktb_plan* p);
+void s3_run(ktb_plan* p, const double* x, double* y);
+void reduction_regions_dev(const ktb_matrix* m, int P, const int32_t* d_bnd, int64_t* d_lo,
+                           int64_t* d_hi, cudaStream_t s);
+void bss_plan_size(const ktb_matrix* m, int64_t jl, int64_t* jl_eff, int64_t* total,
+                   cudaStream_t s);
+void bss_plan_copy(const ktb_matrix* m, int64_t jl, int64_t* h_start, int64_t* h_len,
+                   int64_t* h_row, int64_t* h_lane, int64_t* h_rowptr, uint8_t* h_flag,
+                   cudaStream_t s);
+ktb_matrix* gen_stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t z1, bool slab,
+                         double diag, double off, double cxm, double cxp, int device);
+ktb_matrix* gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
+                                int device);
+void seeded_vector_dev(int64_t n, uint64_t seed, int64_t offset, double* d_out, cudaStream_t s);
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return KTB_OK;
+    } catch (const Invalid& e) {
+        g_err = e.what();
+        return KTB_ERR_INVALID;
+    } catch (const SelectError& e) {
+        g_err = e.what();
+        return KTB_ERR_SELECT;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return KTB_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return KTB_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return KTB_ERR_CUDA;
+    }
+}
+
+bool is_sym_kernel(int k) { return k == KTB_S1 || k == KTB_S2 || k == KTB_S3; }
+bool is_unsym_kernel(int k) { return k >= KTB_U1 && k <= KTB_U4; }
+
+// csr.hpp:38-54, same checks and messages, on the caller's host arrays.
+template <typename I>
+void validate_host(int64_t n, const I* rp, const I* ci, bool upper, int64_t* max_row,
+                   int64_t* bw) {
+    require(n >= 0, "csr: negative dimension");
+    require(rp != nullptr, "csr: row_ptr length != n+1");
+    require(rp[0] == 0, "csr: row_ptr[0] != 0");
+    const int64_t nnz = rp[n];
+    require(nnz >= 0, "csr: row_ptr[n] != nnz");
+    int64_t ml = 0, b = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        require(rp[i] <= rp[i + 1], "csr: row_ptr not nondecreasing");
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            require(ci[k] >= 0 && ci[k] < n, "csr: column index out of range");
+            if (k > rp[i]) require(ci[k - 1] < ci[k], "csr: columns not strictly increasing");
+            if (upper) require(ci[k] >= i, "sym csr: entry below the diagonal");
+        }
+        ml = std::max<int64_t>(ml, rp[i + 1] - rp[i]);
+        if (rp[i + 1] > rp[i]) b = std::max<int64_t>(b, static_cast<int64_t>(ci[rp[i + 1] - 1]) - i);
+    }
+    *max_row = ml;
+    *bw = b;
+}
+
+template <typename I>
+ktb_matrix* create_matrix(int64_t n, const I* rp, const I* ci, const double* v, int kind,
+                          int device) {
+    require(kind == KTB_GENERAL || kind == KTB_SYM_UPPER, "csr: bad matrix kind");
+    int64_t ml = 0, bw = 0;
+    validate_host(n, rp, ci, kind == KTB_SYM_UPPER, &ml, &bw);
+    const int64_t nnz = rp[n];
+    require(n < (int64_t(1) << 31) - 1 && nnz < (int64_t(1) << 31) - 1,
+            "csr: n or nnz >= 2^31 does not fit the int32 device layout");
+    DeviceGuard g(device);
+    auto* m = new ktb_matrix();
+    try {
+        m->device = device;
+        KTB_CUDA(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+        m->n = n;
+        m->ncols = n;
+        m->nnz = nnz;
+        m->kind = kind;
+        m->max_row_nnz = ml;
+        m->bandwidth = bw;
+        std::vector<int32_t> rp32(n + 1), ci32(nnz);
+        for (int64_t i = 0; i <= n; ++i) rp32[i] = static_cast<int32_t>(rp[i]);
+        for (int64_t k = 0; k < nnz; ++k) ci32[k] = static_cast<int32_t>(ci[k]);
+        m->row_ptr.alloc(n + 1);
+        m->col.alloc(nnz);
+        m->val.alloc(nnz);
+        KTB_CUDA(cudaMemcpy(m->row_ptr.p, rp32.data(), 4 * (n + 1), cudaMemcpyHostToDevice));
+        if (nnz) {
+            KTB_CUDA(cudaMemcpy(m->col.p, ci32.data(), 4 * nnz, cudaMemcpyHostToDevice));
+            KTB_CUDA(cudaMemcpy(m->val.p, v, 8 * nnz, cudaMemcpyHostToDevice));
+        }
+    } catch (...) {
+        delete m;
+        throw;
+    }
+    return m;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- dispatch
+void plan_setup(ktb_plan* p) {
+    switch (p->kernel) {
+        case KTB_U1: u1_setup(p); break;
+        case KTB_U2: u2_setup(p); break;
+        case KTB_U3:
+        case KTB_U4: u3_setup(p); break;
+        case KTB_S1:
+        case KTB_S2: s12_setup(p); break;
+        case KTB_S3: s3_setup(p); break;
+        default: throw Invalid("spmv: unknown kernel");
+    }
+}
+
+void plan_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
+    if (p->m->n == 0) return;
+    switch (p->kernel) {
+        case KTB_U1: u1_run(p, x, y, r0, r1); break;
+        case KTB_U2: u2_run(p, x, y); break;
+        case KTB_U3:
+        case KTB_U4: u3_run(p, x, y); break;
+        case KTB_S1:
+        case KTB_S2: s12_run(p, x, y); break;
+        case KTB_S3: s3_run(p, x, y); break;
+        default: throw Invalid("spmv: unknown kernel");
+    }
+}
+
+}  // namespace ktb
+
+ktb_matrix::~ktb_matrix() { delete expanded; }
+
+ktb_plan::~ktb_plan() {
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+using namespace ktb;
+
+extern "C" {
+
+const char* ktb_last_error(void) { return g_err.c_str(); }
+int ktb_version(void) { return 1; }
+
+int ktb_device_count(int* count) {
+    return guarded([&] { KTB_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int ktb_matrix_create(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                      const double* values, int kind, int device, ktb_matrix** out) {
+    return guarded([&] { *out = create_matrix(n, row_ptr, col_idx, values, kind, device); });
+}
+
+int ktb_matrix_create_i32(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                          const double* values, int kind, int device, ktb_matrix** out) {
+    return guarded([&] { *out = create_matrix(n, row_ptr, col_idx, values, kind, device); });
+}
+
+int ktb_matrix_destroy(ktb_matrix* m) {
+    return guarded([&] {
+        if (m) {
+            DeviceGuard g(m->device);
+            delete m;
+        }
+    });
+}
+
+int ktb_matrix_info(const ktb_matrix* m, int64_t* n, int64_t* nnz, int* kind,
+                    int64_t* max_row_nnz, int64_t* bandwidth) {
+    return guarded([&] {
+        require(m != nullptr, "matrix: null handle");
+        if (n) *n = m->n;
+        if (nnz) *nnz = m->nnz;
+        if (kind) *kind = m->kind;
+        if (max_row_nnz) *max_row_nnz = m->max_row_nnz;
+        if (bandwidth) *bandwidth = m->bandwidth;
+    });
+}
+
+int ktb_matrix_download(const ktb_matrix* m, int32_t* row_ptr, int32_t* col_idx,
+                        double* values) {
+    return guarded([&] {
+        DeviceGuard g(m->device);
+        if (row_ptr)
+            KTB_CUDA(cudaMemcpy(row_ptr, m->row_ptr.p, 4 * (m->n + 1), cudaMemcpyDeviceToHost));
+        if (col_idx && m->nnz)
+            KTB_CUDA(cudaMemcpy(col_idx, m->col.p, 4 * m->nnz, cudaMemcpyDeviceToHost));
+        if (values && m->nnz)
+            KTB_CUDA(cudaMemcpy(values, m->val.p, 8 * m->nnz, cudaMemcpyDeviceToHost));
+    });
+}
+
+int ktb_gen_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, double off, double c_xm,
+                     double c_xp, int device, ktb_matrix** out) {
+    return guarded(
+        [&] { *out = gen_stencil7(nx, ny, nz, 0, nz, false, diag, off, c_xm, c_xp, device); });
+}
+
+int ktb_gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
+                            int device, ktb_matrix** out) {
+    return guarded([&] { *out = gen_stencil27_upper(nx, ny, nz, diag, off, device); });
+}
+
+int ktb_gen_stencil7_slab(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t z1,
+                          double diag, double off, int device, ktb_matrix** out) {
+    return guarded(
+        [&] { *out = gen_stencil7(nx, ny, nz, z0, z1, true, diag, off, off, off, device); });
+}
+
+int ktb_seeded_vector(int64_t n, uint64_t seed, int64_t offset, double* d_out, void* stream) {
+    return guarded([&] {
+        seeded_vector_dev(n, seed, offset, d_out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ktb_row_partition(const ktb_matrix* m, int num_workers, int scheme, int64_t* boundaries) {
+    return guarded([&] {
+        require(num_workers >= 1, "row partition: num_workers must be >= 1");
+        require(scheme == KTB_ROW_BASED || scheme == KTB_NNZ_BALANCED,
+                "row partition: bad scheme");
+        DeviceGuard g(m->device);
+        DBuf<int32_t> d(num_workers + 1);
+        build_row_partition_dev(m, num_workers, scheme, d.p, 0);
+        std::vector<int32_t> h(num_workers + 1);
+        KTB_CUDA(cudaMemcpy(h.data(), d.p, 4 * (num_workers + 1), cudaMemcpyDeviceToHost));
+        for (int p = 0; p <= num_workers; ++p) boundaries[p] = h[p];
+    });
+}
+
+int ktb_reduction_regions(const ktb_matrix* m, int num_workers, const int64_t* boundaries,
+                          int64_t* lo, int64_t* hi) {
+    return guarded([&] {
+        require(m->kind == KTB_SYM_UPPER, "reduction regions: matrix is not symmetric storage");
+        require(num_workers >= 1 && boundaries[num_workers] == m->n,
+                "reduction regions: partition/matrix dimension mismatch");
+        DeviceGuard g(m->device);
+        std::vector<int32_t> b32(num_workers + 1);
+        for (int p = 0; p <= num_workers; ++p) b32[p] = static_cast<int32_t>(boundaries[p]);
+        DBuf<int32_t> db(num_workers + 1);
+        DBuf<int64_t> dlo(num_workers), dhi(num_workers);
+        KTB_CUDA(cudaMemcpy(db.p, b32.data(), 4 * (num_workers + 1), cudaMemcpyHostToDevice));
+        reduction_regions_dev(m, num_workers, db.p, dlo.p, dhi.p, 0);
+        KTB_CUDA(cudaMemcpy(lo, dlo.p, 8 * num_workers, cudaMemcpyDeviceToHost));
+        KTB_CUDA(cudaMemcpy(hi, dhi.p, 8 * num_workers, cudaMemcpyDeviceToHost));
+    });
+}
+
+int ktb_bss_plan_size(const ktb_matrix* m, int64_t jl, int64_t* jl_eff, int64_t* total_slices) {
+    return guarded([&] {
+        DeviceGuard g(m->device);
+        bss_plan_size(m, jl, jl_eff, total_slices, 0);
+    });
+}
+
+int ktb_bss_plan_copy(const ktb_matrix* m, int64_t jl, int64_t* slice_start, int64_t* slice_len,
+                      int64_t* slice_row, int64_t* lane_slice_ptr, int64_t* row_slice_ptr,
+                      uint8_t* row_start_flag) {
+    return guarded([&] {
+        DeviceGuard g(m->device);
+        bss_plan_copy(m, jl, slice_start, slice_len, slice_row, lane_slice_ptr, row_slice_ptr,
+                      row_start_flag, 0);
+    });
+}
+
+int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out) {
+    return guarded([&] { *out = expand_symmetric_dev(m, 0); });
+}
+
+int ktb_plan_create(ktb_matrix* m, int kernel, int64_t param, int workers, void* stream,
+                    ktb_plan** out) {
+    return guarded([&] {
+        require(m != nullptr, "plan: null matrix");
+        if (is_sym_kernel(kernel))
+            require(m->kind == KTB_SYM_UPPER, "spmv: symmetric kernel on a general matrix");
+        else
+            require(is_unsym_kernel(kernel), "spmv: unknown kernel");
+        if (is_unsym_kernel(kernel))
+            require(m->kind == KTB_GENERAL, "spmv: unsymmetric kernel on symmetric storage");
+        DeviceGuard g(m->device);
+        auto* p = new ktb_plan();
+        try {
+            p->m = m;
+            p->kernel = kernel;
+            p->param = param;
+            p->workers = workers > 0 ? workers : m->sm_count;
+            if (stream) {
+                p->stream = static_cast<cudaStream_t>(stream);
+            } else {
+                KTB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+                p->own_stream = true;
+            }
+            if (m->n > 0) plan_setup(p);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int ktb_plan_destroy(ktb_plan* p) {
+    return guarded([&] {
+        if (p) {
+            DeviceGuard g(p->m->device);
+            delete p;
+        }
+    });
+}
+
+int ktb_plan_info(const ktb_plan* p, int* kernel, int64_t* param, int64_t* ctas,
+                  int* launches_per_apply, int64_t* extra_bytes) {
+    return guarded([&] {
+        if (kernel) *kernel = p->kernel;
+        if (param) *param = p->kernel == KTB_U3 || p->kernel == KTB_U4 ? p->jl : p->param;
+        if (ctas) *ctas = p->ctas;
+        if (launches_per_apply) *launches_per_apply = p->launches;
+        if (extra_bytes) *extra_bytes = p->extra_bytes;
+    });
+}
+
+int ktb_plan_set_stream(ktb_plan* p, void* stream) {
+    return guarded([&] {
+        if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+        p->own_stream = false;
+        p->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int ktb_spmv(ktb_plan* p, const double* x, double* y, int ptr_kind) {
+    return guarded([&] {
+        require(p != nullptr, "spmv: null plan");
+        require(x != nullptr && y != nullptr, "spmv: dimension mismatch");
+        const ktb_matrix* m = p->m;
+        DeviceGuard g(m->device);
+        if (ptr_kind == KTB_PTR_DEVICE) {
+            plan_run(p, x, y, 0, m->n);
+            return;
+        }
+        require(ptr_kind == KTB_PTR_HOST, "spmv: bad pointer kind");
+        if (p->dx.n < static_cast<size_t>(m->ncols)) p->dx.alloc(std::max<int64_t>(m->ncols, 1));
+        if (p->dy.n < static_cast<size_t>(m->n)) p->dy.alloc(std::max<int64_t>(m->n, 1));
+        KTB_CUDA(cudaMemcpyAsync(p->dx.p, x, 8 * m->ncols, cudaMemcpyHostToDevice, p->stream));
+        plan_run(p, p->dx.p, p->dy.p, 0, m->n);
+        KTB_CUDA(cudaMemcpyAsync(y, p->dy.p, 8 * m->n, cudaMemcpyDeviceToHost, p->stream));
+        KTB_CUDA(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int ktb_spmv_rows(ktb_plan* p, int64_t row_begin, int64_t row_end, const double* x, double* y) {
+    return guarded([&] {
+        require(p->kernel == KTB_U1, "spmv_rows: row sub-ranges need the U1 plan");
+        require(row_begin >= 0 && row_begin <= row_end && row_end <= p->m->n,
+                "spmv_rows: bad row range");
+        DeviceGuard g(p->m->device);
+        u1_run(p, x, y, row_begin, row_end);
+    });
+}
+
+int ktb_stream_sync(void* stream) {
+    return guarded([&] { KTB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
+}
+
+int ktb_host_alloc(size_t bytes, void** out) {
+    return guarded([&] { KTB_CUDA(cudaMallocHost(out, bytes)); });
+}
+int ktb_host_free(void* p) {
+    return guarded([&] { KTB_CUDA(cudaFreeHost(p)); });
+}
+int ktb_device_alloc(int device, size_t bytes, void** out) {
+    return guarded([&] {
+        DeviceGuard g(device);
+        KTB_CUDA(cudaMalloc(out, bytes));
+    });
+}
+int ktb_device_free(void* p) {
+    return guarded([&] { KTB_CUDA(cudaFree(p)); });
+}
+int ktb_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
+    return guarded([&] {
+        KTB_CUDA(cudaMemcpyAsync(dst, src, bytes, static_cast<cudaMemcpyKind>(kind),
+                                 static_cast<cudaStream_t>(stream)));
+    });
+}
+
+int ktb_time_spmv(ktb_plan* p, const double* x, double* y, int reps, size_t flush_bytes,
+                  double* avg_ms, double* min_ms) {
+    return guarded([&] {
+        require(reps >= 1, "time: reps must be >= 1");
+        DeviceGuard g(p->m->device);
+        DBuf<uint8_t> flush;
+        if (flush_bytes) flush.alloc(flush_bytes);
+        std::vector<cudaEvent_t> ev(2 * reps);
+        for (auto& e : ev) KTB_CUDA(cudaEventCreate(&e));
+        for (int r = 0; r < reps; ++r) {
+            if (flush_bytes)
+                KTB_CUDA(cudaMemsetAsync(flush.p, r & 0xff, flush_bytes, p->stream));
+            KTB_CUDA(cudaEventRecord(ev[2 * r], p->stream));
+            plan_run(p, x, y, 0, p->m->n);
+            KTB_CUDA(cudaEventRecord(ev[2 * r + 1], p->stream));
+        }
+        KTB_CUDA(cudaStreamSynchronize(p->stream));
+        double tot = 0.0, mn = std::numeric_limits<double>::infinity();
+        for (int r = 0; r < reps; ++r) {
+            float ms = 0.f;
+            KTB_CUDA(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+            tot += ms;
+            mn = std::min(mn, static_cast<double>(ms));
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        *avg_ms = tot / reps;
+        if (min_ms) *min_ms = mn;
+    });
+}
+
+// ---------------------------------------------------------------- selector
+// autotune.hpp:216-259 (time_candidate / pick_winner) and :267-377.
+int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_plan** winner,
+               ktb_candidate* cands, int max_cands, int* n_cands, int* selected) {
+    return guarded([&] {
+        require(m != nullptr && m->n > 0 && m->nnz > 0, "kernel selection: empty matrix");
+        DeviceGuard g(m->device);
+        ktb_select_opts opts{};
+        if (opts_in) opts = *opts_in;
+        const int trials = opts.timed_trials > 0 ? std::min(opts.timed_trials, 8) : 3;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        cudaStream_t own = nullptr;
+        if (!st) {
+            KTB_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+            st = own;
+        }
+        const int64_t n = m->n;
+        DBuf<double> x(n), ref(n), y(n);
+        probe_vector_dev(n, x.p, st);
+        // the check: serial-order spmv_ref on the stored (GENERAL) or
+        // expanded (SYM_UPPER, csr.hpp:88-123) matrix
+        if (m->kind == KTB_SYM_UPPER) {
+            if (!m->expanded) m->expanded = expand_symmetric_dev(m, st);
+            check_spmv_ref_order(m->expanded, x.p, ref.p, st);
+        } else {
+            check_spmv_ref_order(m, x.p, ref.p, st);
+        }
+        struct Cand {
+            int kernel;
+            int64_t param;
+            ktb_candidate rep;
+        };
+        std::vector<Cand> list;
+        auto add = [&](int k, int64_t prm, const char* name, int ordinal) {
+            Cand c{k, prm, {}};
+            std::strncpy(c.rep.name, name, 7);
+            c.rep.ordinal = ordinal;
+            c.rep.workers = opts.workers > 0 ? opts.workers : m->sm_count;
+            c.rep.best_seconds = std::numeric_limits<double>::infinity();
+            list.push_back(c);
+        };
+        if (m->kind == KTB_SYM_UPPER) {
+            add(KTB_S1, 0, "s1", 0);
+            add(KTB_S2, 0, "s2", 1);
+            add(KTB_S3, 0, "s3", 2);
+        } else {
+            add(KTB_U1, 0, "u1", 0);
+            add(KTB_U2, 0, "u2", 1);
+            std::vector<int64_t> ept = {4, 8, 16};
+            if (opts.params && opts.n_params > 0) ept.assign(opts.params, opts.params + opts.n_params);
+            for (int64_t e : ept)
+                if (m->nnz >= 4 * e) add(KTB_U3, e, "u3", 2);
+        }
+        std::vector<ktb_plan*> plans(list.size(), nullptr);
+        cudaEvent_t e0, e1;
+        KTB_CUDA(cudaEventCreate(&e0));
+        KTB_CUDA(cudaEventCreate(&e1));
+        for (size_t ci = 0; ci < list.size(); ++ci) {
+            auto& c = list[ci];
+            ktb_plan* p = nullptr;
+            try {
+                p = new ktb_plan();
+                p->m = m;
+                p->kernel = c.kernel;
+                p->param = c.param;
+                p->workers = c.rep.workers;
+                p->stream = st;
+                plan_setup(p);
+            } catch (const Invalid&) {
+                delete p;  // layout not applicable: report as failing the check
+                c.rep.correct = 0;
+                continue;
+            }
+            c.rep.param = (c.kernel == KTB_U3) ? p->jl : p->param;
+            plans[ci] = p;
+            // warm-up doubles as the correctness cross-check (autotune.hpp:226-229)
+            plan_run(p, x.p, y.p, 0, n);
+            c.rep.executions = 1;
+            c.rep.correct = outputs_match_dev(n, y.p, ref.p, st);
+            if (!c.rep.correct) continue;
+            for (int t = 0; t < trials; ++t) {
+                double sec;
+                if (opts.now) {
+                    const double tic = opts.now(opts.now_ctx);
+                    plan_run(p, x.p, y.p, 0, n);
+                    KTB_CUDA(cudaStreamSynchronize(st));
+                    sec = opts.now(opts.now_ctx) - tic;
+                } else {
+                    KTB_CUDA(cudaEventRecord(e0, st));
+                    plan_run(p, x.p, y.p, 0, n);
+                    KTB_CUDA(cudaEventRecord(e1, st));
+                    KTB_CUDA(cudaEventSynchronize(e1));
+                    float ms = 0.f;
+                    KTB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                    sec = ms * 1e-3;
+                }
+                ++c.rep.executions;
+                c.rep.trial_seconds[c.rep.n_trials++] = sec;
+                c.rep.best_seconds = std::min(c.rep.best_seconds, sec);
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        // pick_winner: lexicographic (best, ordinal, param, workers)
+        int best = -1;
+        for (int i = 0; i < static_cast<int>(list.size()); ++i) {
+            const auto& c = list[i].rep;
+            if (!c.correct) continue;
+            if (best < 0) {
+                best = i;
+                continue;
+            }
+            const auto& b = list[best].rep;
+            if (std::make_tuple(c.best_seconds, c.ordinal, c.param, c.workers) <
+                std::make_tuple(b.best_seconds, b.ordinal, b.param, b.workers))
+                best = i;
+        }
+        if (n_cands) *n_cands = static_cast<int>(list.size());
+        if (cands)
+            for (int i = 0; i < static_cast<int>(list.size()) && i < max_cands; ++i)
+                cands[i] = list[i].rep;
+        for (size_t i = 0; i < plans.size(); ++i)
+            if (static_cast<int>(i) != best) delete plans[i];
+        if (best < 0) {
+            if (own) cudaStreamDestroy(own);
+            throw SelectError("kernel selection: every candidate failed the oracle check");
+        }
+        if (selected) *selected = best;
+        ktb_plan* w = plans[best];
+        if (own) {
+            w->stream = own;  // hand the private stream to the winner
+            w->own_stream = true;
+        }
+        *winner = w;
+    });
+}
+
+}  // extern "C"

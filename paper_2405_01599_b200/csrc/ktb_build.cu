@@ -1,0 +1,645 @@
+// ktb_build.cu -- device-side plan artefacts (bit-exact with the reference
+// builders), generators, probe/check kernels used by the selector.
+//
+// Reference builders restated here as parallel integer kernels:
+//   build_row_partition      partition.hpp:28-55
+//   build_reduction_regions  partition.hpp:73-96
+//   build_bss_plan           bss.hpp:34-69
+//   expand_symmetric         csr.hpp:88-123
+//   spmv_ref (check order)   csr.hpp:69-78
+//   probe_vector             autotune.hpp:188-196
+//   outputs_match            autotune.hpp:198-204
+//   seeded_vector            lanczos.hpp:17-29
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "ktb_internal.cuh"
+
+namespace ktb {
+
+// ---------------------------------------------------------------- partition
+// partition.hpp:38-52. ROW_BASED: n*p/P. NNZ_BALANCED: smallest r in [0,n)
+// with row_ptr[r]*P >= p*nnz (std::lower_bound on [begin, end-1)), else n.
+// 64-bit products: p*nnz reaches 7*937,951,232 > 2^31 at config 4.
+__global__ void k_row_partition(const int32_t* __restrict__ rp, int64_t n, int P, int scheme,
+                                int32_t* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > P) return;
+    if (p == 0) { out[0] = 0; return; }
+    if (p == P) { out[P] = static_cast<int32_t>(n); return; }
+    if (scheme == KTB_ROW_BASED) {
+        out[p] = static_cast<int32_t>(n * p / P);
+        return;
+    }
+    const int64_t nnz = rp[n];
+    const int64_t target = static_cast<int64_t>(p) * nnz;
+    int64_t lo = 0, len = n;
+    while (len > 0) {
+        const int64_t half = len >> 1;
+        const int64_t mid = lo + half;
+        if (static_cast<int64_t>(rp[mid]) * P < target) {
+            lo = mid + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    out[p] = static_cast<int32_t>(lo);
+}
+
+void build_row_partition_dev(const ktb_matrix* m, int P, int scheme, int32_t* d_out,
+                             cudaStream_t s) {
+    k_row_partition<<<ceil_div(P + 1, 256), 256, 0, s>>>(m->row_ptr.p, m->n, P, scheme, d_out);
+    KTB_LAUNCH();
+}
+
+// ------------------------------------------------------------------ regions
+// partition.hpp:73-96 for sorted upper rows: the smallest strictly-upper
+// column of row i is its first entry (or the second when the first is the
+// diagonal), the largest is its last entry.
+__global__ void k_regions(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                          const int32_t* __restrict__ bnd, int64_t n, int64_t* lo_out,
+                          int64_t* hi_out) {
+    const int p = blockIdx.x;
+    const int32_t r0 = bnd[p], r1 = bnd[p + 1];
+    int64_t lo = n, hi = 0;
+    for (int32_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        int32_t b = rp[i], e = rp[i + 1];
+        if (b == e) continue;
+        if (col[b] == i) ++b;
+        if (b == e) continue;
+        lo = min(lo, static_cast<int64_t>(col[b]));
+        hi = max(hi, static_cast<int64_t>(col[e - 1]) + 1);
+    }
+    using BR = cub::BlockReduce<int64_t, 256>;
+    __shared__ typename BR::TempStorage t1, t2;
+    const int64_t blo = BR(t1).Reduce(lo, cub::Min());
+    const int64_t bhi = BR(t2).Reduce(hi, cub::Max());
+    if (threadIdx.x == 0) {
+        lo_out[p] = bhi > blo ? blo : 0;
+        hi_out[p] = bhi > blo ? bhi : 0;
+    }
+}
+
+void reduction_regions_dev(const ktb_matrix* m, int P, const int32_t* d_bnd, int64_t* d_lo,
+                           int64_t* d_hi, cudaStream_t s) {
+    k_regions<<<P, 256, 0, s>>>(m->row_ptr.p, m->col.p, d_bnd, m->n, d_lo, d_hi);
+    KTB_LAUNCH();
+}
+
+// ----------------------------------------------------------------- BSS plan
+// bss.hpp:38-69. A slice starts at every lane chunk start nnz*p/jl and at
+// every row start of a nonempty row (row_start_flag); slices partition
+// [0, nnz) in order, so slice t spans [start[t], start[t+1]).
+__global__ void k_bss_flags(const int32_t* __restrict__ rp, int64_t n, uint8_t* flag) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n && rp[i] < rp[i + 1]) flag[rp[i]] = 1;
+}
+
+__global__ void k_bss_chunk_marks(int64_t nnz, int64_t jl, const uint8_t* flag, int32_t* mark) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k < nnz) mark[k] = flag[k];
+}
+
+__global__ void k_bss_chunk_starts(int64_t nnz, int64_t jl, int32_t* mark) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p < jl) mark[nnz * p / jl] = 1;
+}
+
+// row containing nonzero position k: first row r with rp[r+1] > k (skips empty rows)
+__device__ __forceinline__ int64_t row_of_nz(const int32_t* rp, int64_t n, int64_t k) {
+    int64_t lo = 0, len = n;  // search rp[1..n] for first > k
+    while (len > 0) {
+        const int64_t half = len >> 1;
+        const int64_t mid = lo + half;
+        if (rp[mid + 1] <= k) {
+            lo = mid + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    return lo;
+}
+
+__global__ void k_bss_slices(const int32_t* __restrict__ rp, int64_t n, int64_t nnz,
+                             const int32_t* mark, const int32_t* sidx, int64_t* sstart,
+                             int64_t* srow, int32_t* srow32) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= nnz || !mark[k]) return;
+    const int32_t t = sidx[k];
+    const int64_t r = row_of_nz(rp, n, k);
+    if (sstart) sstart[t] = k;
+    if (srow) srow[t] = r;
+    if (srow32) srow32[t] = static_cast<int32_t>(r);
+}
+
+__global__ void k_bss_lens(const int64_t* sstart, int64_t total, int64_t nnz, int64_t* slen) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < total) slen[t] = (t + 1 < total ? sstart[t + 1] : nnz) - sstart[t];
+}
+
+__global__ void k_bss_lane_ptr(int64_t nnz, int64_t jl, int64_t total, const int32_t* sidx,
+                               int64_t* lane_ptr) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p < jl) lane_ptr[p] = sidx[nnz * p / jl];
+    if (p == jl) lane_ptr[jl] = total;
+}
+
+__global__ void k_count_rows(const int32_t* srow, int64_t total, int32_t* cnt) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < total) atomicAdd(&cnt[srow[t]], 1);
+}
+
+__global__ void k_i32_to_i64(const int32_t* in, int64_t count, int64_t* out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < count) out[i] = in[i];
+}
+
+template <typename T>
+static void exclusive_scan(const T* in, T* out, int64_t count, cudaStream_t s) {
+    size_t tmp = 0;
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, count, s));
+    DBuf<uint8_t> t(tmp ? tmp : 1);
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, count, s));
+    KTB_CUDA(cudaStreamSynchronize(s));
+}
+
+struct BssDev {
+    int64_t jl = 0, total = 0;
+    DBuf<uint8_t> flag;
+    DBuf<int32_t> mark, sidx;
+};
+
+static void bss_prepare(const ktb_matrix* m, int64_t jl_in, BssDev& b, cudaStream_t s) {
+    require(jl_in >= 1, "bss plan: jl must be >= 1");
+    require(m->nnz > 0, "bss plan: empty matrix");
+    const int64_t nnz = m->nnz, n = m->n;
+    b.jl = std::min<int64_t>(jl_in, nnz);
+    b.flag.alloc(nnz);
+    KTB_CUDA(cudaMemsetAsync(b.flag.p, 0, nnz, s));
+    k_bss_flags<<<ceil_div(n, 256), 256, 0, s>>>(m->row_ptr.p, n, b.flag.p);
+    KTB_LAUNCH();
+    b.mark.alloc(nnz);
+    b.sidx.alloc(nnz);
+    k_bss_chunk_marks<<<ceil_div(nnz, 256), 256, 0, s>>>(nnz, b.jl, b.flag.p, b.mark.p);
+    k_bss_chunk_starts<<<ceil_div(b.jl, 256), 256, 0, s>>>(nnz, b.jl, b.mark.p);
+    KTB_LAUNCH();
+    exclusive_scan(b.mark.p, b.sidx.p, nnz, s);
+    int32_t last_idx = 0, last_mark = 0;
+    KTB_CUDA(cudaMemcpy(&last_idx, b.sidx.p + nnz - 1, 4, cudaMemcpyDeviceToHost));
+    KTB_CUDA(cudaMemcpy(&last_mark, b.mark.p + nnz - 1, 4, cudaMemcpyDeviceToHost));
+    b.total = static_cast<int64_t>(last_idx) + last_mark;
+}
+
+void bss_plan_size(const ktb_matrix* m, int64_t jl, int64_t* jl_eff, int64_t* total,
+                   cudaStream_t s) {
+    BssDev b;
+    bss_prepare(m, jl, b, s);
+    *jl_eff = b.jl;
+    *total = b.total;
+}
+
+void bss_plan_copy(const ktb_matrix* m, int64_t jl, int64_t* h_start, int64_t* h_len,
+                   int64_t* h_row, int64_t* h_lane, int64_t* h_rowptr, uint8_t* h_flag,
+                   cudaStream_t s) {
+    BssDev b;
+    bss_prepare(m, jl, b, s);
+    const int64_t nnz = m->nnz, n = m->n, T = b.total;
+    DBuf<int64_t> sstart(T), slen(T), srow(T), lane(b.jl + 1), rowptr(n + 1);
+    DBuf<int32_t> srow32(T), cnt(n + 1), cnt_scan(n + 1);
+    k_bss_slices<<<ceil_div(nnz, 256), 256, 0, s>>>(m->row_ptr.p, n, nnz, b.mark.p, b.sidx.p,
+                                                    sstart.p, srow.p, srow32.p);
+    KTB_LAUNCH();
+    k_bss_lens<<<ceil_div(T, 256), 256, 0, s>>>(sstart.p, T, nnz, slen.p);
+    k_bss_lane_ptr<<<ceil_div(b.jl + 1, 256), 256, 0, s>>>(nnz, b.jl, T, b.sidx.p, lane.p);
+    KTB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (n + 1), s));
+    k_count_rows<<<ceil_div(T, 256), 256, 0, s>>>(srow32.p, T, cnt.p);
+    KTB_LAUNCH();
+    exclusive_scan(cnt.p, cnt_scan.p, n + 1, s);  // cnt[n] = 0 -> scan[n] = total
+    k_i32_to_i64<<<ceil_div(n + 1, 256), 256, 0, s>>>(cnt_scan.p, n + 1, rowptr.p);
+    KTB_LAUNCH();
+    if (h_start) KTB_CUDA(cudaMemcpy(h_start, sstart.p, 8 * T, cudaMemcpyDeviceToHost));
+    if (h_len) KTB_CUDA(cudaMemcpy(h_len, slen.p, 8 * T, cudaMemcpyDeviceToHost));
+    if (h_row) KTB_CUDA(cudaMemcpy(h_row, srow.p, 8 * T, cudaMemcpyDeviceToHost));
+    if (h_lane) KTB_CUDA(cudaMemcpy(h_lane, lane.p, 8 * (b.jl + 1), cudaMemcpyDeviceToHost));
+    if (h_rowptr) KTB_CUDA(cudaMemcpy(h_rowptr, rowptr.p, 8 * (n + 1), cudaMemcpyDeviceToHost));
+    if (h_flag) KTB_CUDA(cudaMemcpy(h_flag, b.flag.p, nnz, cudaMemcpyDeviceToHost));
+}
+
+// ------------------------------------------------------------ matrix stats
+__global__ void k_stats(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                        int64_t n, unsigned long long* maxlen, long long* bw) {
+    unsigned long long ml = 0;
+    long long b = LLONG_MIN;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t s = rp[i], e = rp[i + 1];
+        ml = max(ml, static_cast<unsigned long long>(e - s));
+        if (e > s) b = max(b, static_cast<long long>(col[e - 1]) - i);
+    }
+    atomicMax(maxlen, ml);
+    atomicMax(bw, b);
+}
+
+void compute_matrix_stats(ktb_matrix* m, cudaStream_t s) {
+    DBuf<unsigned long long> ml(1);
+    DBuf<long long> bw(1);
+    const long long init = LLONG_MIN;
+    KTB_CUDA(cudaMemsetAsync(ml.p, 0, 8, s));
+    KTB_CUDA(cudaMemcpyAsync(bw.p, &init, 8, cudaMemcpyHostToDevice, s));
+    k_stats<<<4 * m->sm_count, 256, 0, s>>>(m->row_ptr.p, m->col.p, m->n, ml.p, bw.p);
+    KTB_LAUNCH();
+    unsigned long long h_ml = 0;
+    long long h_bw = 0;
+    KTB_CUDA(cudaMemcpyAsync(&h_ml, ml.p, 8, cudaMemcpyDeviceToHost, s));
+    KTB_CUDA(cudaMemcpyAsync(&h_bw, bw.p, 8, cudaMemcpyDeviceToHost, s));
+    KTB_CUDA(cudaStreamSynchronize(s));
+    m->max_row_nnz = static_cast<int64_t>(h_ml);
+    m->bandwidth = h_bw == LLONG_MIN ? 0 : h_bw;
+}
+
+// ------------------------------------------------------- expand_symmetric
+// csr.hpp:88-123. Row j of the full matrix = mirrored entries (i, j), i < j,
+// in ascending source row i, followed by the native upper entries of row j.
+// A stable radix sort of the off-diagonal entries by column j reproduces the
+// ascending-i order within each destination row.
+__global__ void k_expand_count(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                               int64_t n, int32_t* cnt_mirror) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k)
+        if (col[k] != i) atomicAdd(&cnt_mirror[col[k]], 1);
+}
+
+__global__ void k_expand_rowlen(const int32_t* __restrict__ rp, const int32_t* cnt_mirror,
+                                int64_t n, int32_t* len) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) len[i] = cnt_mirror[i] + (rp[i + 1] - rp[i]);
+    if (i == n) len[n] = 0;
+}
+
+__global__ void k_expand_offdiag(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 int64_t n, int32_t* keys, int32_t* src) {
+    // one entry per stored nonzero; diagonal entries get key n (sorted last, ignored)
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
+        keys[k] = col[k] == i ? static_cast<int32_t>(n) : col[k];
+        src[k] = k;
+    }
+}
+
+__global__ void k_row_of_entry(const int32_t* __restrict__ rp, int64_t n, int32_t* row) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) row[k] = static_cast<int32_t>(i);
+}
+
+__global__ void k_expand_fill_mirror(const int32_t* skeys, const int32_t* ssrc,
+                                     const int32_t* erow_start, const int32_t* entry_row,
+                                     const double* val, int64_t n, int64_t nnz, int32_t* ocol,
+                                     double* oval) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= nnz) return;
+    const int32_t j = skeys[t];
+    if (j >= n) return;
+    // rank within segment j: position t minus first position of key j (binary search)
+    int64_t lo = 0, len = t;  // first index with skeys[idx] >= j
+    while (len > 0) {
+        const int64_t half = len >> 1;
+        const int64_t mid = lo + half;
+        if (skeys[mid] < j) {
+            lo = mid + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    const int64_t pos = erow_start[j] + (t - lo);
+    const int32_t k = ssrc[t];
+    ocol[pos] = entry_row[k];
+    oval[pos] = val[k];
+}
+
+__global__ void k_expand_fill_native(const int32_t* __restrict__ rp,
+                                     const int32_t* __restrict__ col, const double* val,
+                                     const int32_t* erow_start, const int32_t* cnt_mirror,
+                                     int64_t n, int32_t* ocol, double* oval) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    int64_t pos = erow_start[i] + cnt_mirror[i];
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k, ++pos) {
+        ocol[pos] = col[k];
+        oval[pos] = val[k];
+    }
+}
+
+ktb_matrix* expand_symmetric_dev(const ktb_matrix* m, cudaStream_t s) {
+    require(m->kind == KTB_SYM_UPPER, "expand_symmetric: matrix is not symmetric storage");
+    DeviceGuard g(m->device);
+    const int64_t n = m->n, nnz = m->nnz;
+    DBuf<int32_t> cnt(n + 1), len(n + 1);
+    KTB_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (n + 1), s));
+    k_expand_count<<<ceil_div(n, 256), 256, 0, s>>>(m->row_ptr.p, m->col.p, n, cnt.p);
+    k_expand_rowlen<<<ceil_div(n + 1, 256), 256, 0, s>>>(m->row_ptr.p, cnt.p, n, len.p);
+    KTB_LAUNCH();
+    auto* out = new ktb_matrix();
+    out->device = m->device;
+    out->n = n;
+    out->ncols = n;
+    out->kind = KTB_GENERAL;
+    out->sm_count = m->sm_count;
+    out->row_ptr.alloc(n + 1);
+    exclusive_scan(len.p, out->row_ptr.p, n + 1, s);
+    int32_t total = 0;
+    KTB_CUDA(cudaMemcpy(&total, out->row_ptr.p + n, 4, cudaMemcpyDeviceToHost));
+    out->nnz = total;
+    out->col.alloc(total);
+    out->val.alloc(total);
+    if (nnz > 0) {
+        DBuf<int32_t> keys(nnz), src(nnz), skeys(nnz), ssrc(nnz), erow(nnz);
+        k_expand_offdiag<<<ceil_div(n, 256), 256, 0, s>>>(m->row_ptr.p, m->col.p, n, keys.p,
+                                                          src.p);
+        k_row_of_entry<<<ceil_div(n, 256), 256, 0, s>>>(m->row_ptr.p, n, erow.p);
+        KTB_LAUNCH();
+        size_t tmp = 0;
+        KTB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.p, skeys.p, src.p, ssrc.p,
+                                                 nnz, 0, 32, s));
+        DBuf<uint8_t> t(tmp ? tmp : 1);
+        KTB_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, keys.p, skeys.p, src.p, ssrc.p, nnz, 0,
+                                                 32, s));
+        k_expand_fill_mirror<<<ceil_div(nnz, 256), 256, 0, s>>>(
+            skeys.p, ssrc.p, out->row_ptr.p, erow.p, m->val.p, n, nnz, out->col.p, out->val.p);
+        k_expand_fill_native<<<ceil_div(n, 256), 256, 0, s>>>(
+            m->row_ptr.p, m->col.p, m->val.p, out->row_ptr.p, cnt.p, n, out->col.p, out->val.p);
+        KTB_LAUNCH();
+    }
+    KTB_CUDA(cudaStreamSynchronize(s));
+    compute_matrix_stats(out, s);
+    return out;
+}
+
+// ----------------------------------------------- selector check machinery
+// csr.hpp:69-78 order: one thread per row, strictly left to right, with
+// explicit round-to-nearest multiply and add (no FMA contraction), which is
+// bitwise what the reference computes when built with default x86-64 flags.
+__global__ void k_check_spmv(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const double* __restrict__ val, int64_t n,
+                             const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(val[k], x[col[k]]));
+    y[i] = s;
+}
+
+void check_spmv_ref_order(const ktb_matrix* m, const double* dx, double* dy, cudaStream_t s) {
+    k_check_spmv<<<ceil_div(m->n, 128), 128, 0, s>>>(m->row_ptr.p, m->col.p, m->val.p, m->n, dx,
+                                                      dy);
+    KTB_LAUNCH();
+}
+
+// autotune.hpp:188-196: x_i from an LCG; the state after i+1 steps is
+// a^(i+1)*s0 + c*(a^(i+1)-1)/(a-1), evaluated with a jump-ahead per thread.
+__global__ void k_probe_vector(int64_t n, double* out) {
+    const int64_t i0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 64;
+    if (i0 >= n) return;
+    const uint64_t A = 6364136223846793005ull, Cc = 1442695040888963407ull;
+    // jump the state to position i0: apply (A, Cc) i0 times via squaring
+    uint64_t acc_mult = 1, acc_plus = 0, cur_mult = A, cur_plus = Cc;
+    uint64_t delta = static_cast<uint64_t>(i0);
+    while (delta > 0) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    uint64_t state = acc_mult * 0x9e3779b97f4a7c15ull + acc_plus;
+    const int64_t end = min(n, i0 + 64);
+    for (int64_t i = i0; i < end; ++i) {
+        state = state * A + Cc;
+        out[i] = 0.5 + static_cast<double>(state >> 11) / 9007199254740992.0;
+    }
+}
+
+void probe_vector_dev(int64_t n, double* d_out, cudaStream_t s) {
+    k_probe_vector<<<ceil_div(ceil_div64(n, 64), 128), 128, 0, s>>>(n, d_out);
+    KTB_LAUNCH();
+}
+
+// lanczos.hpp:17-29 splitmix64: state_i = seed + (i+1)*golden -> closed form.
+__global__ void k_seeded_vector(int64_t n, uint64_t seed, int64_t offset, double* out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    uint64_t z = seed + static_cast<uint64_t>(offset + i + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    out[i] = static_cast<double>(z >> 11) / 4503599627370496.0 - 1.0;
+}
+
+void seeded_vector_dev(int64_t n, uint64_t seed, int64_t offset, double* d_out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_seeded_vector<<<ceil_div(n, 256), 256, 0, s>>>(n, seed, offset, d_out);
+    KTB_LAUNCH();
+}
+
+// autotune.hpp:198-204: scale = max(1, max|ref|) ignoring NaN the way
+// std::max does; mismatch iff |y - ref| > 1e-10 * scale.
+__global__ void k_absmax(const double* __restrict__ r, int64_t n, unsigned long long* out) {
+    unsigned long long m = __double_as_longlong(1.0);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double a = fabs(r[i]);
+        if (a == a) m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+    }
+    atomicMax(out, m);
+}
+
+__global__ void k_mismatch(const double* __restrict__ y, const double* __restrict__ r, int64_t n,
+                           const unsigned long long* scale_bits, unsigned long long* bad) {
+    const double tol = 1e-10 * __longlong_as_double(static_cast<long long>(*scale_bits));
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (fabs(y[i] - r[i]) > tol) ++c;
+    if (c) atomicAdd(bad, c);
+}
+
+int outputs_match_dev(int64_t n, const double* dy, const double* dref, cudaStream_t s) {
+    DBuf<unsigned long long> buf(2);
+    KTB_CUDA(cudaMemsetAsync(buf.p, 0, 16, s));
+    k_absmax<<<592, 256, 0, s>>>(dref, n, buf.p);
+    k_mismatch<<<592, 256, 0, s>>>(dy, dref, n, buf.p, buf.p + 1);
+    KTB_LAUNCH();
+    unsigned long long bad = 0;
+    KTB_CUDA(cudaMemcpyAsync(&bad, buf.p + 1, 8, cudaMemcpyDeviceToHost, s));
+    KTB_CUDA(cudaStreamSynchronize(s));
+    return bad == 0 ? 1 : 0;
+}
+
+// --------------------------------------------------------------- generators
+// 3-D stencils, grid index i = (z*ny + y)*nx + x. Row lengths
+// first, exclusive scan, then columns in ascending order.
+struct Grid {
+    int64_t nx, ny, nz;
+};
+
+__device__ __forceinline__ void grid_xyz(const Grid& g, int64_t i, int64_t& x, int64_t& y,
+                                         int64_t& z) {
+    z = i / (g.nx * g.ny);
+    const int64_t r = i - z * g.nx * g.ny;
+    y = r / g.nx;
+    x = r - y * g.nx;
+}
+
+// 7-point: offsets in ascending order -z,-y,-x,0,+x,+y,+z.
+__global__ void k_s7_len(Grid g, int64_t z0, int64_t nrows, int32_t* len) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r > nrows) return;
+    if (r == nrows) { len[r] = 0; return; }
+    int64_t x, y, z;
+    grid_xyz(g, r + z0 * g.nx * g.ny, x, y, z);
+    len[r] = 1 + (z > 0) + (y > 0) + (x > 0) + (x < g.nx - 1) + (y < g.ny - 1) + (z < g.nz - 1);
+}
+
+__global__ void k_s7_fill(Grid g, int64_t z0, int64_t nrows, int64_t col_base, double diag,
+                          double off, double cxm, double cxp, const int32_t* rp, int32_t* col,
+                          double* val) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r >= nrows) return;
+    const int64_t gi = r + z0 * g.nx * g.ny;
+    int64_t x, y, z;
+    grid_xyz(g, gi, x, y, z);
+    const int64_t plane = g.nx * g.ny;
+    int64_t k = rp[r];
+    auto put = [&](int64_t c, double v) {
+        col[k] = static_cast<int32_t>(c - col_base);
+        val[k] = v;
+        ++k;
+    };
+    if (z > 0) put(gi - plane, off);
+    if (y > 0) put(gi - g.nx, off);
+    if (x > 0) put(gi - 1, cxm);
+    put(gi, diag);
+    if (x < g.nx - 1) put(gi + 1, cxp);
+    if (y < g.ny - 1) put(gi + g.nx, off);
+    if (z < g.nz - 1) put(gi + plane, off);
+}
+
+// 27-point upper: offsets d = (dz*ny + dy)*nx + dx >= 0, ascending.
+__global__ void k_s27u_len(Grid g, int64_t nrows, int32_t* len) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r > nrows) return;
+    if (r == nrows) { len[r] = 0; return; }
+    int64_t x, y, z;
+    grid_xyz(g, r, x, y, z);
+    int c = 0;
+    for (int dz = 0; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (dz == 0 && (dy < 0 || (dy == 0 && dx < 0))) continue;
+                if (x + dx < 0 || x + dx >= g.nx || y + dy < 0 || y + dy >= g.ny ||
+                    z + dz >= g.nz)
+                    continue;
+                ++c;
+            }
+    len[r] = c;
+}
+
+__global__ void k_s27u_fill(Grid g, int64_t nrows, double diag, double off, const int32_t* rp,
+                            int32_t* col, double* val) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r >= nrows) return;
+    int64_t x, y, z;
+    grid_xyz(g, r, x, y, z);
+    int64_t k = rp[r];
+    for (int dz = 0; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (dz == 0 && (dy < 0 || (dy == 0 && dx < 0))) continue;
+                if (x + dx < 0 || x + dx >= g.nx || y + dy < 0 || y + dy >= g.ny ||
+                    z + dz >= g.nz)
+                    continue;
+                const int64_t d = (dz * g.ny + dy) * g.nx + dx;
+                col[k] = static_cast<int32_t>(r + d);
+                val[k] = d == 0 ? diag : off;
+                ++k;
+            }
+}
+
+static ktb_matrix* finish_gen(ktb_matrix* m, DBuf<int32_t>& len, cudaStream_t s) {
+    exclusive_scan(len.p, m->row_ptr.p, m->n + 1, s);
+    int32_t total = 0;
+    KTB_CUDA(cudaMemcpy(&total, m->row_ptr.p + m->n, 4, cudaMemcpyDeviceToHost));
+    m->nnz = total;
+    m->col.alloc(total);
+    m->val.alloc(total);
+    return m;
+}
+
+ktb_matrix* gen_stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t z1,
+                         bool slab, double diag, double off, double cxm, double cxp, int device) {
+    DeviceGuard guard(device);
+    const int64_t plane = nx * ny;
+    const int64_t nrows = (z1 - z0) * plane;
+    require(nx >= 1 && ny >= 1 && nz >= 1 && z0 >= 0 && z1 <= nz && z1 > z0,
+            "stencil7: bad grid");
+    require(nrows < (int64_t(1) << 31) && nrows * 7 < (int64_t(1) << 31),
+            "stencil7: n or nnz >= 2^31 (int32 device indices)");
+    auto* m = new ktb_matrix();
+    m->device = device;
+    KTB_CUDA(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+    m->n = nrows;
+    m->kind = KTB_GENERAL;
+    const bool has_lo = slab && z0 > 0, has_hi = slab && z1 < nz;
+    m->ncols = slab ? nrows + (has_lo ? plane : 0) + (has_hi ? plane : 0) : nrows;
+    const int64_t col_base = slab ? z0 * plane - (has_lo ? plane : 0) : 0;
+    cudaStream_t s = 0;
+    DBuf<int32_t> len(nrows + 1);
+    m->row_ptr.alloc(nrows + 1);
+    const Grid g{nx, ny, nz};
+    k_s7_len<<<ceil_div(nrows + 1, 256), 256, 0, s>>>(g, z0, nrows, len.p);
+    KTB_LAUNCH();
+    finish_gen(m, len, s);
+    k_s7_fill<<<ceil_div(nrows, 256), 256, 0, s>>>(g, z0, nrows, col_base, diag, off, cxm, cxp,
+                                                   m->row_ptr.p, m->col.p, m->val.p);
+    KTB_LAUNCH();
+    KTB_CUDA(cudaStreamSynchronize(s));
+    compute_matrix_stats(m, s);
+    return m;
+}
+
+ktb_matrix* gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
+                                int device) {
+    DeviceGuard guard(device);
+    const int64_t n = nx * ny * nz;
+    require(nx >= 1 && ny >= 1 && nz >= 1, "stencil27: bad grid");
+    require(n * 14 < (int64_t(1) << 31), "stencil27: nnz >= 2^31 (int32 device indices)");
+    auto* m = new ktb_matrix();
+    m->device = device;
+    KTB_CUDA(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+    m->n = n;
+    m->ncols = n;
+    m->kind = KTB_SYM_UPPER;
+    cudaStream_t s = 0;
+    DBuf<int32_t> len(n + 1);
+    m->row_ptr.alloc(n + 1);
+    const Grid g{nx, ny, nz};
+    k_s27u_len<<<ceil_div(n + 1, 256), 256, 0, s>>>(g, n, len.p);
+    KTB_LAUNCH();
+    finish_gen(m, len, s);
+    k_s27u_fill<<<ceil_div(n, 256), 256, 0, s>>>(g, n, diag, off, m->row_ptr.p, m->col.p,
+                                                 m->val.p);
+    KTB_LAUNCH();
+    KTB_CUDA(cudaStreamSynchronize(s));
+    compute_matrix_stats(m, s);
+    return m;
+}
+
+}  // namespace ktb

@@ -1,0 +1,182 @@
+// ktb_internal.cuh -- shared internals of libktb (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ktb.h"
+
+namespace ktb {
+
+// Contract violation (maps to KTB_ERR_INVALID; message = reference wording).
+struct Invalid : std::runtime_error {
+    explicit Invalid(const std::string& m) : std::runtime_error(m) {}
+};
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct SelectError : std::runtime_error {
+    explicit SelectError(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void require(bool cond, const char* msg) {
+    if (!cond) throw Invalid(msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                        std::to_string(line) + ")");
+}
+#define KTB_CUDA(x) ::ktb::cuda_check((x), #x, __FILE__, __LINE__)
+#define KTB_LAUNCH() ::ktb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+constexpr int kNumSMs = 148;  // B200; queried at runtime, this is the default
+
+// RAII device buffer.
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) KTB_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { release(); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        release();
+        p = o.p;
+        n = o.n;
+        o.p = nullptr;
+        o.n = 0;
+        return *this;
+    }
+    size_t bytes() const { return sizeof(T) * n; }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) KTB_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace ktb
+
+// Device-resident CRS. int32 indices (nnz < 2^31), fp64 values.
+struct ktb_matrix {
+    int device = 0;
+    int64_t n = 0, nnz = 0;
+    int64_t ncols = 0;  // == n except for halo slabs (config 4 sharding)
+    int kind = KTB_GENERAL;
+    int64_t max_row_nnz = 0;
+    int64_t bandwidth = 0;  // max(col - row) over stored entries (>= 0 for sym upper)
+    int sm_count = ktb::kNumSMs;
+    ktb::DBuf<int32_t> row_ptr;  // n+1
+    ktb::DBuf<int32_t> col;      // nnz
+    ktb::DBuf<double> val;       // nnz
+    // Lazily built: expanded full matrix (sym) for the selector's check.
+    ktb_matrix* expanded = nullptr;
+    ~ktb_matrix();
+};
+
+namespace ktb {
+
+// ---- plans ---------------------------------------------------------------
+struct MergeCoord {
+    int32_t row;
+    int32_t nz;
+};
+
+// S3 (zero-omission window) execution layout: see ktb_sym.cu.
+struct SymWindowLayout {
+    int ctas = 0;          // persistent CTAs = P of the NNZ_BALANCED partition
+    int rows_per_sub = 0;  // rows per sub-tile (= threads per CTA)
+    int window = 0;        // smem ring length in doubles
+    int64_t padded = 0;    // total SELL slots (entries + padding)
+    int64_t far = 0;       // entries scattered outside the window (atomic path)
+    int64_t spill_total = 0;
+    DBuf<int32_t> cta_row;     // ctas+1 (bit-exact NNZ_BALANCED boundaries)
+    DBuf<int32_t> cta_sub;     // ctas+1 sub-tile ranges
+    DBuf<int64_t> sub_base;    // per sub-tile offset into the SELL arrays
+    DBuf<int32_t> sub_rounds;  // per sub-tile round count
+    DBuf<int32_t> sell_col;    // round-major SELL columns (-1 pad, top bit = far)
+    DBuf<double> sell_val;
+    DBuf<int32_t> spill_hi;    // per CTA: end of its spill range (start = cta_row[c+1])
+    DBuf<int64_t> spill_off;   // per CTA: offset into spill
+    DBuf<double> spill;
+    DBuf<int32_t> head_end;    // per CTA: its head rows [cta_row[c], head_end[c]) get spills
+    DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it
+    DBuf<int32_t> far_i, far_j;
+    DBuf<double> far_v;
+};
+
+}  // namespace ktb
+
+struct ktb_plan {
+    ktb_matrix* m = nullptr;
+    int kernel = KTB_U1;
+    int64_t param = 0;
+    int workers = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t ctas = 0;
+    int launches = 1;
+    int64_t extra_bytes = 0;
+    // U2 merge-path tiles / U3 BSS lanes
+    ktb::DBuf<ktb::MergeCoord> coords;  // U2: tiles+1 merge coordinates
+    int64_t jl = 0;                     // U3: lane count (reference BssPlan jl)
+    int64_t nq = 0;                     // U3: nonempty rows
+    ktb::DBuf<uint32_t> flag_bits;      // U3: row_start_flag, 1 bit per nonzero
+    ktb::DBuf<int32_t> seg_row;         // U3: q-th nonempty row (+ sentinel n)
+    ktb::DBuf<int32_t> tile_q;          // U3: flags before each tile
+    ktb::DBuf<double> carry_val;        // per tile carry-out
+    ktb::DBuf<int32_t> carry_row;
+    int64_t tiles = 0;
+    // S1/S2 row blocks
+    ktb::DBuf<int32_t> blocks;          // P+1 row boundaries
+    // S3
+    ktb::SymWindowLayout sw;
+    // host staging for KTB_PTR_HOST
+    ktb::DBuf<double> dx, dy;
+    ~ktb_plan();
+};
+
+namespace ktb {
+
+// ---- internal entry points (implemented across the .cu files) -------------
+void build_row_partition_dev(const ktb_matrix* m, int P, int scheme, int32_t* d_out,
+                             cudaStream_t s);
+void plan_setup(ktb_plan* p);
+void plan_run(ktb_plan* p, const double* dx, double* dy, int64_t row_begin, int64_t row_end);
+void check_spmv_ref_order(const ktb_matrix* m, const double* dx, double* dy, cudaStream_t s);
+ktb_matrix* expand_symmetric_dev(const ktb_matrix* m, cudaStream_t s);
+void probe_vector_dev(int64_t n, double* d_out, cudaStream_t s);
+int outputs_match_dev(int64_t n, const double* dy, const double* dref, cudaStream_t s);
+void compute_matrix_stats(ktb_matrix* m, cudaStream_t s);
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace ktb

@@ -1,0 +1,438 @@
+// ktb_sym.cu -- symmetric (diagonal + strict upper) CRS SpMV for sm_100a.
+//
+// Reference: spmv_sym (spmv.hpp:180-234). Each worker writes row-direction
+// sums y_i = sum_j U_ij x_j for its rows and scatters transposed products
+// U_ij x_i (j != i) into a private n-vector; a cross-worker reduction then
+// adds the scratch vectors into y over [0,n) (S1/S2) or only over the
+// worker's nonzero region [lo,hi) (S3, partition.hpp:73-96).
+//
+// GPU mapping:
+//   S1/S2  "full-range reduction": the transposed products go straight to y
+//          with fp64 red.global (L2 atomics) after a memset; rows are split
+//          row-based (S1) or into NNZ_BALANCED CTA blocks (S2). Not
+//          deterministic (atomic order), tolerance-checked.
+//   S3     "zero-omission window": one persistent CTA per SM owns an
+//          NNZ_BALANCED row block (bit-exact boundaries, P = #SMs). Its
+//          transposed products accumulate in a shared-memory ring that covers
+//          exactly the CTA's reduction region [lo, hi); rows are finalised
+//          from the ring as soon as no later row of the block can reach them,
+//          and only the part of the region beyond the block (the spill) is
+//          reduced across CTAs, in fixed ascending-CTA order. Shared-memory
+//          fp64 atomics are a CAS loop on sm_100a (ATOMS.CAST.SPIN.64), so
+//          the ring is updated with plain ld/st in ROUNDS: the plan assigns
+//          every entry of a sub-tile of S rows to a round such that no two
+//          entries of one round target the same window slot (greedy bipartite
+//          edge colouring, done once on the host), stores the sub-tile in
+//          round-major SELL order (coalesced), and the kernel separates rounds
+//          with a CTA barrier. The result is deterministic.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ktb_internal.cuh"
+
+namespace ktb {
+
+__device__ __forceinline__ double ld_stream_f64s(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int32_t ld_stream_i32s(const int32_t* p) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// ================================================================ S1 / S2
+template <int V>
+__global__ void __launch_bounds__(256) k_sym_atomic(const int32_t* __restrict__ rp,
+                                                    const int32_t* __restrict__ col,
+                                                    const double* __restrict__ val,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y, int64_t n,
+                                                    const int32_t* __restrict__ blocks) {
+    const int sub = threadIdx.x & (V - 1);
+    int64_t first, stride, last;
+    if (blocks) {  // S2: CTA b owns rows [blocks[b], blocks[b+1])
+        first = blocks[blockIdx.x] + threadIdx.x / V;
+        last = blocks[blockIdx.x + 1];
+        stride = blockDim.x / V;
+    } else {  // S1: contiguous rows in launch order
+        first = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / V;
+        last = n;
+        stride = static_cast<int64_t>(gridDim.x) * blockDim.x / V;
+    }
+    const int64_t trips = first < last ? (last - first + stride - 1) / stride : 0;
+    // all lanes of a group run the same number of trips (shuffle safety)
+    for (int64_t t = 0; t < trips; ++t) {
+        const int64_t i = first + t * stride;
+        const bool active = i < last;
+        int32_t b = 0, e = 0;
+        double xi = 0.0;
+        if (active) {
+            b = __ldg(rp + i);
+            e = __ldg(rp + i + 1);
+            xi = __ldg(x + i);
+        }
+        double s = 0.0;
+        for (int32_t k = b + sub; k < e; k += V) {
+            const int32_t j = ld_stream_i32s(col + k);
+            const double v = ld_stream_f64s(val + k);
+            s += v * __ldg(x + j);
+            if (j != i) atomicAdd(y + j, v * xi);
+        }
+        if (V > 1) {
+#pragma unroll
+            for (int o = V / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, V);
+        }
+        if (active && sub == 0) atomicAdd(y + i, s);
+    }
+}
+
+void s12_setup(ktb_plan* p) {
+    const ktb_matrix* m = p->m;
+    require(m->kind == KTB_SYM_UPPER, "spmv: symmetric kernel on a general matrix");
+    if (p->param <= 0) {
+        const double mean = m->n ? double(m->nnz) / double(m->n) : 1.0;
+        int v = 1;
+        while (v < 32 && v < mean) v <<= 1;
+        p->param = v;
+    }
+    int v = 1;
+    while (v < p->param && v < 32) v <<= 1;
+    p->param = v;
+    if (p->kernel == KTB_S2) {
+        const int P = m->sm_count * 8;
+        p->blocks.alloc(P + 1);
+        build_row_partition_dev(m, P, KTB_NNZ_BALANCED, p->blocks.p, p->stream);
+        p->ctas = P;
+    } else {
+        p->ctas = std::max<int64_t>(1, std::min<int64_t>(ceil_div64(m->n * v, 256),
+                                                         int64_t(m->sm_count) * 64));
+    }
+    p->launches = 2;
+    p->extra_bytes = 8 * m->n;  // y memset
+}
+
+void s12_run(ktb_plan* p, const double* x, double* y) {
+    const ktb_matrix* m = p->m;
+    KTB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->n, p->stream));
+    const int grid = static_cast<int>(p->ctas);
+    const int32_t* blocks = p->kernel == KTB_S2 ? p->blocks.p : nullptr;
+#define KTB_S_CASE(VV)                                                                       \
+    case VV:                                                                                  \
+        k_sym_atomic<VV><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y, \
+                                                      m->n, blocks);                          \
+        break;
+    switch (p->param) {
+        KTB_S_CASE(1)
+        KTB_S_CASE(2)
+        KTB_S_CASE(4)
+        KTB_S_CASE(8)
+        KTB_S_CASE(16)
+        KTB_S_CASE(32)
+        default: throw Invalid("s1/s2: bad lane count");
+    }
+#undef KTB_S_CASE
+    KTB_LAUNCH();
+}
+
+// ================================================================ S3
+constexpr int kS3Threads = 256;  // rows per sub-tile
+constexpr int kS3MaxR = 16;      // rounds held in registers per pass
+constexpr int kS3RoundCap = 256; // max rounds per sub-tile (colour classes)
+
+__device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
+
+__global__ void __launch_bounds__(kS3Threads, 1)
+    k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_sub,
+         const int64_t* __restrict__ sub_base, const int32_t* __restrict__ sub_rounds,
+         const int32_t* __restrict__ scol, const double* __restrict__ sval,
+         const double* __restrict__ x, double* __restrict__ y, int W,
+         const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
+         double* __restrict__ spill) {
+    extern __shared__ double win[];
+    const int tid = threadIdx.x;
+    const int c = blockIdx.x;
+    const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
+    for (int i = tid; i < W; i += kS3Threads) win[i] = 0.0;
+    __syncthreads();
+    const int s_begin = cta_sub[c], s_end = cta_sub[c + 1];
+    int off = 0;  // ring slot of row a (a - R0 mod W)
+    for (int s = s_begin; s < s_end; ++s) {
+        const int32_t a = R0 + (s - s_begin) * kS3Threads;
+        const int32_t i = a + tid;
+        const bool valid = i < R1;
+        const int R = sub_rounds[s];
+        const int64_t base = sub_base[s] + tid;
+        const double xi = valid ? __ldg(x + i) : 0.0;
+        double rowsum = 0.0;
+        for (int r0 = 0; r0 < R; r0 += kS3MaxR) {
+            int32_t cc[kS3MaxR];
+            double vv[kS3MaxR];
+            double xx[kS3MaxR];
+#pragma unroll
+            for (int u = 0; u < kS3MaxR; ++u) {
+                cc[u] = -1;
+                vv[u] = 0.0;
+                if (r0 + u < R) {
+                    const int64_t e = base + static_cast<int64_t>(r0 + u) * kS3Threads;
+                    cc[u] = ld_stream_i32s(scol + e);
+                    vv[u] = ld_stream_f64s(sval + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kS3MaxR; ++u) {
+                xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kS3MaxR; ++u) rowsum += vv[u] * xx[u];
+#pragma unroll
+            for (int u = 0; u < kS3MaxR; ++u) {
+                if (r0 + u < R) {  // uniform over the CTA
+                    const int32_t j = cc[u];
+                    if (j >= 0 && j != i) {
+                        const int slot = wrap(j - a + off, W);
+                        win[slot] += vv[u] * xi;
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+        if (valid) {
+            const int slot = wrap(tid + off, W);
+            y[i] = rowsum + win[slot];
+            win[slot] = 0.0;
+        }
+        __syncthreads();
+        off = wrap(off + kS3Threads, W);
+    }
+    // spill: the region beyond the block, [R1, spill_hi), in ring order
+    const int32_t hi = spill_hi[c];
+    if (hi > R1) {
+        const int64_t so = spill_off[c];
+        for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
+            spill[so + (j - R1)] = win[(j - R0) % W];
+    }
+}
+
+// Head rows of CTA d receive the spills of earlier CTAs, added in ascending
+// source order (deterministic).
+__global__ void k_s3_spill_fixup(const int32_t* __restrict__ cta_row,
+                                 const int32_t* __restrict__ head_end,
+                                 const int32_t* __restrict__ first_src,
+                                 const int32_t* __restrict__ spill_hi,
+                                 const int64_t* __restrict__ spill_off,
+                                 const double* __restrict__ spill, double* __restrict__ y) {
+    const int d = blockIdx.x;
+    const int32_t r0 = cta_row[d], he = head_end[d], c0 = first_src[d];
+    for (int32_t j = r0 + threadIdx.x; j < he; j += blockDim.x) {
+        double s = 0.0;
+        bool any = false;
+        for (int c = c0; c < d; ++c) {
+            if (j < spill_hi[c] && j >= cta_row[c + 1]) {
+                s += spill[spill_off[c] + (j - cta_row[c + 1])];
+                any = true;
+            }
+        }
+        if (any) y[j] += s;
+    }
+}
+
+__global__ void k_s3_far(const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
+                         const double* __restrict__ fv, int64_t count,
+                         const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t < count) atomicAdd(y + fj[t], fv[t] * x[fi[t]]);
+}
+
+void s3_setup(ktb_plan* p) {
+    ktb_matrix* m = p->m;
+    require(m->kind == KTB_SYM_UPPER, "spmv: symmetric kernel on a general matrix");
+    auto& L = p->sw;
+    cudaStream_t st = p->stream;
+    const int S = kS3Threads;
+    const int64_t n = m->n, nnz = m->nnz;
+    const int P = std::max(1, m->sm_count);
+    L.ctas = P;
+    L.rows_per_sub = S;
+    // bit-exact NNZ_BALANCED boundaries with P = #SMs (partition.hpp:42-52)
+    L.cta_row.alloc(P + 1);
+    build_row_partition_dev(m, P, KTB_NNZ_BALANCED, L.cta_row.p, st);
+    std::vector<int32_t> bnd(P + 1), rp(n + 1), col(nnz);
+    std::vector<double> val(nnz);
+    KTB_CUDA(cudaMemcpyAsync(bnd.data(), L.cta_row.p, 4 * (P + 1), cudaMemcpyDeviceToHost, st));
+    KTB_CUDA(cudaMemcpyAsync(rp.data(), m->row_ptr.p, 4 * (n + 1), cudaMemcpyDeviceToHost, st));
+    if (nnz) {
+        KTB_CUDA(cudaMemcpyAsync(col.data(), m->col.p, 4 * nnz, cudaMemcpyDeviceToHost, st));
+        KTB_CUDA(cudaMemcpyAsync(val.data(), m->val.p, 8 * nnz, cudaMemcpyDeviceToHost, st));
+    }
+    KTB_CUDA(cudaStreamSynchronize(st));
+
+    // window: S rows + the largest reach of any row, capped by shared memory
+    int max_smem = 0;
+    KTB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                    m->device));
+    const int64_t cap = std::max<int64_t>(S + 32, (max_smem - 1024) / 8);
+    int64_t reach = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (rp[i + 1] > rp[i]) reach = std::max<int64_t>(reach, col[rp[i + 1] - 1] - i);
+    int64_t W = std::min<int64_t>(cap, ((S + reach + 1 + 31) / 32) * 32);
+    W = std::max<int64_t>(W, S + 32);
+    L.window = static_cast<int>(W);
+
+    std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
+    std::vector<int64_t> sub_base;
+    std::vector<int32_t> scol;
+    std::vector<double> sval;
+    std::vector<int32_t> spill_hi(P), far_i, far_j;
+    std::vector<double> far_v;
+    std::vector<uint64_t> colmask(static_cast<size_t>(W) * (kS3RoundCap / 64), 0);
+    std::vector<int32_t> touched;
+    int64_t total_slots = 0;
+    for (int c = 0; c < P; ++c) {
+        const int32_t R0 = bnd[c], R1 = bnd[c + 1];
+        cta_sub[c] = static_cast<int32_t>(sub_rounds.size());
+        int32_t hi = R1;
+        for (int32_t a = R0; a < R1; a += S) {
+            const int32_t rows = std::min<int32_t>(S, R1 - a);
+            // greedy colouring: entry -> lowest round free in its row and in
+            // its target slot
+            std::vector<std::vector<std::pair<int, int64_t>>> assign(rows);  // (round, k)
+            int R = 0;
+            touched.clear();
+            for (int32_t t = 0; t < rows; ++t) {
+                const int32_t i = a + t;
+                uint64_t rowmask[kS3RoundCap / 64] = {0, 0, 0, 0};
+                for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
+                    const int32_t j = col[k];
+                    const bool scatter = j != i;
+                    const bool far = scatter && (static_cast<int64_t>(j) - a >= W);
+                    uint64_t* cm = nullptr;
+                    if (scatter && !far) {
+                        const size_t slot = static_cast<size_t>(j - a);
+                        cm = &colmask[slot * (kS3RoundCap / 64)];
+                    }
+                    int r = -1;
+                    for (int w = 0; w < kS3RoundCap / 64 && r < 0; ++w) {
+                        const uint64_t busy = rowmask[w] | (cm ? cm[w] : 0);
+                        if (~busy) r = w * 64 + __builtin_ctzll(~busy);
+                    }
+                    require(r >= 0, "s3: row too long for the window layout");
+                    rowmask[r >> 6] |= 1ull << (r & 63);
+                    if (cm) {
+                        if (!(cm[0] | cm[1] | cm[2] | cm[3])) touched.push_back(j - a);
+                        cm[r >> 6] |= 1ull << (r & 63);
+                        hi = std::max<int32_t>(hi, j + 1);
+                    }
+                    if (far) {
+                        far_i.push_back(i);
+                        far_j.push_back(j);
+                        far_v.push_back(val[k]);
+                    }
+                    assign[t].push_back({r, k});
+                    R = std::max(R, r + 1);
+                }
+            }
+            for (int32_t sl : touched)
+                std::memset(&colmask[static_cast<size_t>(sl) * (kS3RoundCap / 64)], 0,
+                            sizeof(uint64_t) * (kS3RoundCap / 64));
+            R = std::max(R, 0);
+            const int64_t basei = static_cast<int64_t>(scol.size());
+            sub_base.push_back(basei);
+            sub_rounds.push_back(R);
+            scol.resize(basei + static_cast<int64_t>(R) * S, -1);
+            sval.resize(basei + static_cast<int64_t>(R) * S, 0.0);
+            for (int32_t t = 0; t < rows; ++t)
+                for (auto [r, k] : assign[t]) {
+                    const int64_t e = basei + static_cast<int64_t>(r) * S + t;
+                    const int32_t j = col[k];
+                    const bool far = j != a + t && (static_cast<int64_t>(j) - a >= W);
+                    scol[e] = far ? static_cast<int32_t>(static_cast<uint32_t>(j) | 0x80000000u)
+                                  : j;
+                    sval[e] = val[k];
+                }
+            total_slots += static_cast<int64_t>(R) * S;
+        }
+        spill_hi[c] = hi;
+    }
+    cta_sub[P] = static_cast<int32_t>(sub_rounds.size());
+    L.padded = total_slots;
+    L.far = static_cast<int64_t>(far_i.size());
+
+    // spill layout and head ranges
+    std::vector<int64_t> spill_off(P);
+    int64_t so = 0;
+    for (int c = 0; c < P; ++c) {
+        spill_off[c] = so;
+        so += std::max<int32_t>(0, spill_hi[c] - bnd[c + 1]);
+    }
+    L.spill_total = so;
+    std::vector<int32_t> head_end(P), first_src(P);
+    for (int d = 0; d < P; ++d) {
+        int32_t he = bnd[d];
+        int32_t fs = d;
+        for (int c = 0; c < d; ++c)
+            if (spill_hi[c] > bnd[d]) {
+                he = std::max<int32_t>(he, std::min<int32_t>(spill_hi[c], bnd[d + 1]));
+                fs = std::min(fs, c);
+            }
+        head_end[d] = he;
+        first_src[d] = fs;
+    }
+
+    auto up32 = [&](DBuf<int32_t>& d, const std::vector<int32_t>& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        if (!h.empty())
+            KTB_CUDA(cudaMemcpyAsync(d.p, h.data(), 4 * h.size(), cudaMemcpyHostToDevice, st));
+    };
+    auto up64 = [&](DBuf<int64_t>& d, const std::vector<int64_t>& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        if (!h.empty())
+            KTB_CUDA(cudaMemcpyAsync(d.p, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st));
+    };
+    auto upd = [&](DBuf<double>& d, const std::vector<double>& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        if (!h.empty())
+            KTB_CUDA(cudaMemcpyAsync(d.p, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st));
+    };
+    up32(L.cta_sub, cta_sub);
+    up64(L.sub_base, sub_base);
+    up32(L.sub_rounds, sub_rounds);
+    up32(L.sell_col, scol);
+    upd(L.sell_val, sval);
+    up32(L.spill_hi, spill_hi);
+    up64(L.spill_off, spill_off);
+    L.spill.alloc(std::max<int64_t>(so, 1));
+    up32(L.head_end, head_end);
+    up32(L.first_src, first_src);
+    up32(L.far_i, far_i);
+    up32(L.far_j, far_j);
+    upd(L.far_v, far_v);
+    KTB_CUDA(cudaStreamSynchronize(st));
+    KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(W * 8)));
+    p->ctas = P;
+    p->launches = 2 + (L.far ? 1 : 0);
+    // padding slots (12 B each) + spill write/read + head-row read-modify-write
+    p->extra_bytes = (total_slots - nnz) * 12 + so * 8 * 2 + so * 8 * 2;
+}
+
+void s3_run(ktb_plan* p, const double* x, double* y) {
+    auto& L = p->sw;
+    k_s3<<<L.ctas, kS3Threads, static_cast<size_t>(L.window) * 8, p->stream>>>(
+        L.cta_row.p, L.cta_sub.p, L.sub_base.p, L.sub_rounds.p, L.sell_col.p, L.sell_val.p, x, y,
+        L.window, L.spill_hi.p, L.spill_off.p, L.spill.p);
+    KTB_LAUNCH();
+    k_s3_spill_fixup<<<L.ctas, 256, 0, p->stream>>>(L.cta_row.p, L.head_end.p, L.first_src.p,
+                                                     L.spill_hi.p, L.spill_off.p, L.spill.p, y);
+    KTB_LAUNCH();
+    if (L.far) {
+        k_s3_far<<<ceil_div(L.far, 256), 256, 0, p->stream>>>(L.far_i.p, L.far_j.p, L.far_v.p,
+                                                               L.far, x, y);
+        KTB_LAUNCH();
+    }
+}
+
+}  // namespace ktb

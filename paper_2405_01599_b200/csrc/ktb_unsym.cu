@@ -1,0 +1,500 @@
+// ktb_unsym.cu -- unsymmetric CRS SpMV kernels for sm_100a.
+//
+//   U1  row-parallel CRS  (spmv.hpp:74-86 with ROW_BASED partition.hpp:38-41)
+//       -> V lanes per row (V = 1..32, from the mean row length), shuffle
+//          reduction; rows are assigned to lane groups in order.
+//   U2  nnz-balanced CRS  (spmv.hpp:74-86 with NNZ_BALANCED partition.hpp:42-52)
+//       -> merge-path tiles: every CTA consumes the same number of
+//          (row-end + nonzero) items; products staged in smem with coalesced
+//          loads; block-wide segmented scan; per-tile carry fixed up after.
+//   U3  branchless segmented scan (spmv.hpp:127-146, bss.hpp:34-69)
+//       -> one GPU thread = one BSS lane; lane chunks follow the reference rule
+//          [nnz*p/jl, nnz*(p+1)/jl) with jl = ceil(nnz / E); row starts come
+//          from the bit-packed row_start_flag array; lane carries are combined
+//          by a block segmented scan, tile carries by the fixup kernel.
+//   U4  original segmented scan (spmv.hpp:148-165): U3 with the per-element
+//       flag branch left in (correctness reference, never a tuning candidate).
+#include <cub/cub.cuh>
+
+#include "ktb_internal.cuh"
+#include "ktb_segscan.cuh"
+
+namespace ktb {
+
+__device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
+__device__ __forceinline__ int32_t ldg_i32(const int32_t* p) { return __ldg(p); }
+
+// Streaming loads for the matrix arrays: read once, do not keep in L1.
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// =============================================================== U1
+template <int V>
+__global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
+                                            const int32_t* __restrict__ col,
+                                            const double* __restrict__ val,
+                                            const double* __restrict__ x, double* __restrict__ y,
+                                            int32_t row_begin, int32_t row_end) {
+    const int sub = threadIdx.x & (V - 1);
+    const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / V;
+    const int64_t row = row_begin + group;
+    const bool active = row < row_end;
+    int32_t b = 0, e = 0;
+    if (active) {
+        b = ldg_i32(rp + row);
+        e = ldg_i32(rp + row + 1);
+    }
+    double s = 0.0;
+    int32_t k = b + sub;
+    // two independent chains for memory-level parallelism
+    double s2 = 0.0;
+    for (; k + V < e; k += 2 * V) {
+        const int32_t c0 = ld_stream_i32(col + k), c1 = ld_stream_i32(col + k + V);
+        const double v0 = ld_stream_f64(val + k), v1 = ld_stream_f64(val + k + V);
+        s += v0 * ldg_f64(x + c0);
+        s2 += v1 * ldg_f64(x + c1);
+    }
+    if (k < e) s += ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
+    s += s2;
+    if (V > 1) {
+#pragma unroll
+        for (int o = V / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, V);
+    }
+    if (active && sub == 0) y[row] = s;
+}
+
+static int pick_lanes(const ktb_matrix* m) {
+    const double mean = m->n ? static_cast<double>(m->nnz) / static_cast<double>(m->n) : 1.0;
+    int v = 1;
+    while (v < 32 && v < mean) v <<= 1;
+    return v;
+}
+
+void u1_setup(ktb_plan* p) {
+    if (p->param <= 0) p->param = pick_lanes(p->m);
+    int v = 1;
+    while (v < p->param && v < 32) v <<= 1;
+    p->param = v;
+    p->launches = 1;
+}
+
+void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return;
+    const int V = static_cast<int>(p->param);
+    const int64_t threads = rows * V;
+    const int grid = ceil_div(threads, 256);
+    p->ctas = grid;
+    const ktb_matrix* m = p->m;
+#define KTB_U1_CASE(VV)                                                                        \
+    case VV:                                                                                    \
+        k_u1<VV><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,          \
+                                              static_cast<int32_t>(r0), static_cast<int32_t>(r1)); \
+        break;
+    switch (V) {
+        KTB_U1_CASE(1)
+        KTB_U1_CASE(2)
+        KTB_U1_CASE(4)
+        KTB_U1_CASE(8)
+        KTB_U1_CASE(16)
+        KTB_U1_CASE(32)
+        default: throw Invalid("u1: bad lane count");
+    }
+#undef KTB_U1_CASE
+    KTB_LAUNCH();
+}
+
+// =============================================================== carries
+// Tile carries (row, value) in tile order; a run of equal rows is summed in
+// order by the first tile of the run and added once: deterministic.
+__global__ void k_fixup_carries(const int32_t* __restrict__ crow,
+                                const double* __restrict__ cval, int64_t tiles, int64_t n,
+                                double* __restrict__ y) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= tiles) return;
+    const int32_t r = crow[t];
+    if (r < 0 || r >= n) return;
+    if (t > 0 && crow[t - 1] == r) return;
+    double s = cval[t];
+    for (int64_t u = t + 1; u < tiles && crow[u] == r; ++u) s += cval[u];
+    y[r] += s;
+}
+
+static void fixup_run(ktb_plan* p, double* y) {
+    k_fixup_carries<<<ceil_div(p->tiles, 256), 256, 0, p->stream>>>(
+        p->carry_row.p, p->carry_val.p, p->tiles, p->m->n, y);
+    KTB_LAUNCH();
+}
+
+// =============================================================== U2
+constexpr int kU2Threads = 256;
+
+// Merge-path search along the diagonal `diag` of the (row ends, nz indices)
+// merge: returns the number of row ends consumed.
+__device__ __forceinline__ int64_t merge_search(const int32_t* __restrict__ row_end, int64_t n,
+                                                int64_t nnz, int64_t diag) {
+    int64_t lo = diag > nnz ? diag - nnz : 0;
+    int64_t hi = diag < n ? diag : n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (static_cast<int64_t>(row_end[mid]) <= diag - mid - 1)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_u2_coords(const int32_t* __restrict__ rp, int64_t n, int64_t nnz,
+                            int64_t tile_items, int64_t tiles, MergeCoord* coords) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t > tiles) return;
+    const int64_t diag = min(t * tile_items, n + nnz);
+    const int64_t r = merge_search(rp + 1, n, nnz, diag);
+    coords[t].row = static_cast<int32_t>(r);
+    coords[t].nz = static_cast<int32_t>(diag - r);
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ rp,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y,
+                                                   const MergeCoord* __restrict__ coords,
+                                                   int32_t* __restrict__ carry_row,
+                                                   double* __restrict__ carry_val) {
+    constexpr int TILE = kU2Threads * IPT;
+    __shared__ double s_prod[TILE];
+    __shared__ int32_t s_end[TILE + 1];
+    const int tid = threadIdx.x;
+    const MergeCoord c0 = coords[blockIdx.x], c1 = coords[blockIdx.x + 1];
+    const int nrows = c1.row - c0.row;
+    const int nnzs = c1.nz - c0.nz;
+    // stage products (coalesced) and row ends
+    for (int i = tid; i < nnzs; i += kU2Threads) {
+        const int32_t k = c0.nz + i;
+        s_prod[i] = ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
+    }
+    for (int i = tid; i < nrows; i += kU2Threads) s_end[i] = ldg_i32(rp + c0.row + 1 + i);
+    if (tid == 0) s_end[nrows] = 0x7fffffff;  // the open row at tile end never closes here
+    __syncthreads();
+
+    // this thread's merge-path start inside the tile
+    const int diag = min(tid * IPT, nrows + nnzs);
+    int lo = max(diag - nnzs, 0), hi = min(diag, nrows);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_end[mid] - c0.nz <= diag - mid - 1)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    int xr = lo, yz = diag - lo;
+    const int end_items = nrows + nnzs;
+    double run = 0.0;
+    double emit_v[IPT];
+    int emit_r[IPT];
+    int nemit = 0;
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+        emit_r[it] = -1;
+        emit_v[it] = 0.0;
+        if (xr + yz < end_items) {
+            if (c0.nz + yz < s_end[xr]) {
+                run += s_prod[yz];
+                ++yz;
+            } else {
+                emit_r[it] = xr;
+                emit_v[it] = run;
+                ++nemit;
+                run = 0.0;
+                ++xr;
+            }
+        }
+    }
+    SegPair agg;
+    const SegPair pre = block_seg_scan_excl<kU2Threads>(SegPair{nemit > 0, run}, &agg);
+    __syncthreads();  // s_prod is reused for row outputs below
+    bool first = true;
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+        if (emit_r[it] >= 0) {
+            s_prod[emit_r[it]] = emit_v[it] + (first ? pre.v : 0.0);
+            first = false;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < nrows; i += kU2Threads) y[c0.row + i] = s_prod[i];
+    if (tid == 0) {
+        carry_row[blockIdx.x] = c1.row;
+        carry_val[blockIdx.x] = agg.v;
+    }
+}
+
+void u2_setup(ktb_plan* p) {
+    if (p->param <= 0) p->param = 8;
+    int ipt = static_cast<int>(p->param);
+    if (ipt != 4 && ipt != 8 && ipt != 12) ipt = 8;
+    p->param = ipt;
+    const ktb_matrix* m = p->m;
+    const int64_t tile_items = static_cast<int64_t>(kU2Threads) * ipt;
+    p->tiles = std::max<int64_t>(1, ceil_div64(m->n + m->nnz, tile_items));
+    p->coords.alloc(p->tiles + 1);
+    p->carry_row.alloc(p->tiles);
+    p->carry_val.alloc(p->tiles);
+    k_u2_coords<<<ceil_div(p->tiles + 1, 256), 256, 0, p->stream>>>(
+        m->row_ptr.p, m->n, m->nnz, tile_items, p->tiles, p->coords.p);
+    KTB_LAUNCH();
+    KTB_CUDA(cudaStreamSynchronize(p->stream));
+    p->ctas = p->tiles;
+    p->launches = 2;
+    p->extra_bytes = p->tiles * (8 + 4 + 8) * 2;
+}
+
+void u2_run(ktb_plan* p, const double* x, double* y) {
+    const ktb_matrix* m = p->m;
+    const int grid = static_cast<int>(p->tiles);
+#define KTB_U2_CASE(I)                                                                       \
+    case I:                                                                                   \
+        k_u2<I><<<grid, kU2Threads, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,   \
+                                                    p->coords.p, p->carry_row.p,              \
+                                                    p->carry_val.p);                          \
+        break;
+    switch (p->param) {
+        KTB_U2_CASE(4)
+        KTB_U2_CASE(8)
+        KTB_U2_CASE(12)
+        default: throw Invalid("u2: bad items per thread");
+    }
+#undef KTB_U2_CASE
+    KTB_LAUNCH();
+    fixup_run(p, y);
+}
+
+// =============================================================== U3 / U4
+constexpr int kU3Threads = 256;
+
+__global__ void k_flag_bits(const int32_t* __restrict__ rp, int64_t n, uint32_t* bits) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) {
+        const int32_t s = rp[i];
+        if (s < rp[i + 1]) atomicOr(&bits[s >> 5], 1u << (s & 31));
+    }
+}
+
+__global__ void k_nonempty_mark(const int32_t* __restrict__ rp, int64_t n, int32_t* mark) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) mark[i] = rp[i] < rp[i + 1];
+}
+
+__global__ void k_nonempty_scatter(const int32_t* __restrict__ rp, int64_t n,
+                                   const int32_t* ord, int32_t* seg_row) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n && rp[i] < rp[i + 1]) seg_row[ord[i]] = static_cast<int32_t>(i);
+}
+
+// tile_q[t] = number of row starts before the tile's first nonzero
+__global__ void k_tile_q(const uint32_t* __restrict__ bits, int64_t nnz, int64_t jl,
+                         int64_t tiles, int32_t* tile_q) {
+    // one block per tile; count set bits in [0, K0) with a strided popc reduction
+    const int64_t t = blockIdx.x;
+    if (t >= tiles) return;
+    const int64_t K0 = nnz * (t * kU3Threads) / jl;
+    const int64_t words = K0 >> 5;
+    long long c = 0;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) c += __popc(bits[w]);
+    if (threadIdx.x == 0 && (K0 & 31)) c += __popc(bits[words] & ((1u << (K0 & 31)) - 1u));
+    using BR = cub::BlockReduce<long long, 256>;
+    __shared__ typename BR::TempStorage tmp;
+    const long long tot = BR(tmp).Sum(c);
+    if (threadIdx.x == 0) tile_q[t] = static_cast<int32_t>(tot);
+}
+
+// E = nominal nonzeros per lane; actual chunk lengths are floor/ceil of
+// nnz/jl, at most E (jl = ceil(nnz/E)), so the per-lane loop is unrolled to E.
+template <int E, bool BRANCHY>
+__global__ void __launch_bounds__(kU3Threads) k_u3(const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y, int64_t n,
+                                                   int64_t nnz, int64_t jl,
+                                                   const uint32_t* __restrict__ bits,
+                                                   const int32_t* __restrict__ seg_row,
+                                                   int64_t nq,
+                                                   const int32_t* __restrict__ tile_q,
+                                                   int32_t* __restrict__ carry_row,
+                                                   double* __restrict__ carry_val) {
+    constexpr int TILE = kU3Threads * E;
+    constexpr int PAD = TILE + TILE / E + 1;
+    __shared__ double s_prod[PAD];
+    const int tid = threadIdx.x;
+    const int64_t t = blockIdx.x;
+    const int64_t p0 = t * kU3Threads;
+    const int64_t p1 = min(p0 + kU3Threads, jl);
+    const int64_t K0 = nnz * p0 / jl, K1 = nnz * p1 / jl;
+    const int span = static_cast<int>(K1 - K0);
+    for (int i = tid; i < span; i += kU3Threads) {
+        const int64_t k = K0 + i;
+        s_prod[i + i / E] = ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
+    }
+    // this lane's chunk (reference rule, bss.hpp:49-50)
+    const int64_t p = p0 + tid;
+    const bool lane_ok = p < jl;
+    const int64_t a = lane_ok ? nnz * p / jl : K1;
+    const int64_t b = lane_ok ? nnz * (p + 1) / jl : K1;
+    const int len = static_cast<int>(b - a);
+    // flag bits of [a, b): at most E+1 <= 33 bits, from two words
+    uint32_t m = 0;
+    if (len > 0) {
+        const int64_t w = a >> 5;
+        const int sh = static_cast<int>(a & 31);
+        uint64_t pair = bits[w];
+        if (((b - 1) >> 5) != w) pair |= static_cast<uint64_t>(bits[w + 1]) << 32;
+        m = static_cast<uint32_t>(pair >> sh);
+        if (len < 32) m &= (1u << len) - 1u;
+    }
+    const int nf = __popc(m);
+    // q of the lane's first element = flags before a = tile_q + block prefix of nf
+    using BS = cub::BlockScan<int, kU3Threads>;
+    __shared__ typename BS::TempStorage scan_tmp;
+    int qpre = 0, qtot = 0;
+    BS(scan_tmp).ExclusiveSum(nf, qpre, qtot);
+    __syncthreads();
+    int64_t q = static_cast<int64_t>(tile_q[t]) + qpre;  // flags strictly before a
+
+    // walk: close the open segment at each row start (flag), emit complete rows
+    double run = 0.0;
+    int first_row = -1;
+    double first_val = 0.0;
+    const int base = static_cast<int>(a - K0);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e < len) {
+            const int li = base + e;
+            const double prod = s_prod[li + li / E];
+            bool f;
+            if (BRANCHY) {
+                // original scan (spmv.hpp:157): fetch and test the element's flag
+                const int64_t k = a + e;
+                f = (__ldg(bits + (k >> 5)) >> (k & 31)) & 1u;
+            } else {
+                f = (m >> e) & 1u;  // BSS: flags of the whole chunk in one register
+            }
+            if (f) {
+                if (q > 0) {
+                    const int32_t r = seg_row[q - 1];
+                    const int32_t rn = seg_row[q];
+                    if (first_row < 0) {
+                        first_row = r;
+                        first_val = run;
+                    } else {
+                        y[r] = run;
+                    }
+                    for (int32_t z = r + 1; z < rn; ++z) y[z] = 0.0;  // empty rows between
+                } else {
+                    for (int32_t z = 0; z < seg_row[0]; ++z) y[z] = 0.0;  // leading empties
+                }
+                run = 0.0;
+                ++q;
+            }
+            run += prod;
+        }
+    }
+    SegPair agg;
+    const SegPair pre = block_seg_scan_excl<kU3Threads>(SegPair{nf > 0, run}, &agg);
+    if (first_row >= 0) y[first_row] = first_val + pre.v;
+    if (lane_ok && p == jl - 1) {
+        // the last nonempty row is never closed by a flag: seed it with 0 and
+        // let the carry fixup add the open segment; trailing empty rows are 0
+        const int32_t last = seg_row[nq - 1];
+        y[last] = 0.0;
+        for (int64_t z = last + 1; z < n; ++z) y[z] = 0.0;
+    }
+    if (tid == 0) {
+        const int64_t qe = static_cast<int64_t>(tile_q[t]) + qtot;  // flags before K1
+        carry_row[t] = qe > 0 ? seg_row[qe - 1] : -1;
+        carry_val[t] = agg.v;
+    }
+}
+
+void u3_setup(ktb_plan* p) {
+    const ktb_matrix* m = p->m;
+    require(m->nnz > 0, "bss plan: empty matrix");
+    int E = p->param > 0 ? static_cast<int>(p->param) : 8;
+    if (E != 4 && E != 8 && E != 16) E = 8;
+    p->param = E;
+    p->jl = ceil_div64(m->nnz, E);
+    p->tiles = ceil_div64(p->jl, kU3Threads);
+    cudaStream_t s = p->stream;
+    const int64_t words = ceil_div64(m->nnz, 32) + 1;
+    p->flag_bits.alloc(words);
+    KTB_CUDA(cudaMemsetAsync(p->flag_bits.p, 0, 4 * words, s));
+    k_flag_bits<<<ceil_div(m->n, 256), 256, 0, s>>>(m->row_ptr.p, m->n, p->flag_bits.p);
+    KTB_LAUNCH();
+    DBuf<int32_t> mark(m->n), ord(m->n);
+    k_nonempty_mark<<<ceil_div(m->n, 256), 256, 0, s>>>(m->row_ptr.p, m->n, mark.p);
+    KTB_LAUNCH();
+    size_t tmp = 0;
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, mark.p, ord.p, m->n, s));
+    DBuf<uint8_t> tb(tmp ? tmp : 1);
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, tmp, mark.p, ord.p, m->n, s));
+    int32_t lo = 0, lm = 0;
+    KTB_CUDA(cudaMemcpyAsync(&lo, ord.p + m->n - 1, 4, cudaMemcpyDeviceToHost, s));
+    KTB_CUDA(cudaMemcpyAsync(&lm, mark.p + m->n - 1, 4, cudaMemcpyDeviceToHost, s));
+    KTB_CUDA(cudaStreamSynchronize(s));
+    p->nq = static_cast<int64_t>(lo) + lm;
+    p->seg_row.alloc(p->nq + 1);
+    k_nonempty_scatter<<<ceil_div(m->n, 256), 256, 0, s>>>(m->row_ptr.p, m->n, ord.p,
+                                                           p->seg_row.p);
+    KTB_LAUNCH();
+    const int32_t nrow = static_cast<int32_t>(m->n);
+    KTB_CUDA(cudaMemcpyAsync(p->seg_row.p + p->nq, &nrow, 4, cudaMemcpyHostToDevice, s));
+    p->tile_q.alloc(p->tiles);
+    k_tile_q<<<static_cast<int>(p->tiles), 256, 0, s>>>(p->flag_bits.p, m->nnz, p->jl, p->tiles,
+                                                        p->tile_q.p);
+    KTB_LAUNCH();
+    p->carry_row.alloc(p->tiles);
+    p->carry_val.alloc(p->tiles);
+    KTB_CUDA(cudaStreamSynchronize(s));
+    p->ctas = p->tiles;
+    p->launches = 2;
+    // flag bits + nonempty-row map replace row_ptr; tile carries
+    p->extra_bytes = 4 * words + 4 * (p->nq - (m->n + 1)) + p->tiles * (4 + 8) * 2;
+}
+
+void u3_run(ktb_plan* p, const double* x, double* y) {
+    const ktb_matrix* m = p->m;
+    const int grid = static_cast<int>(p->tiles);
+    const bool br = p->kernel == KTB_U4;
+#define KTB_U3_CASE(EE)                                                                        \
+    case EE:                                                                                    \
+        if (br)                                                                                 \
+            k_u3<EE, true><<<grid, kU3Threads, 0, p->stream>>>(                                 \
+                m->col.p, m->val.p, x, y, m->n, m->nnz, p->jl, p->flag_bits.p, p->seg_row.p,    \
+                p->nq, p->tile_q.p, p->carry_row.p, p->carry_val.p);                            \
+        else                                                                                    \
+            k_u3<EE, false><<<grid, kU3Threads, 0, p->stream>>>(                                \
+                m->col.p, m->val.p, x, y, m->n, m->nnz, p->jl, p->flag_bits.p, p->seg_row.p,    \
+                p->nq, p->tile_q.p, p->carry_row.p, p->carry_val.p);                            \
+        break;
+    switch (p->param) {
+        KTB_U3_CASE(4)
+        KTB_U3_CASE(8)
+        KTB_U3_CASE(16)
+        default: throw Invalid("u3: bad lane length");
+    }
+#undef KTB_U3_CASE
+    KTB_LAUNCH();
+    fixup_run(p, y);
+}
+
+}  // namespace ktb

@@ -1,0 +1,595 @@
+"""Host-side mirror of the reference's SpMV operator interface (namespace
+``ktune``, /root/reference/proj/include/ktune/*.hpp) running on the B200
+engine behind the C ABI (include/ktb.h).
+
+Same names, argument meaning and error wording as the reference:
+
+===========================  ==============================================
+reference                    here
+===========================  ==============================================
+CsrMatrix / SymCsrMatrix     CsrMatrix / SymCsrMatrix (csr.hpp:13-65)
+build_row_partition          build_row_partition (partition.hpp:28-55)
+build_reduction_regions      build_reduction_regions (partition.hpp:73-96)
+build_bss_plan               build_bss_plan (bss.hpp:34-69)
+expand_symmetric             expand_symmetric (csr.hpp:88-123)
+spmv_unsym / spmv_sym        spmv_unsym / spmv_sym (spmv.hpp:111-234)
+select_spmv_unsym / _sym     select_spmv_unsym / _sym (autotune.hpp:267-377)
+UnsymEngine / SymEngine      UnsymEngine / SymEngine (meta.hpp:20-82)
+LinOp, make_ref_op           LinOp (solver_types.hpp:17-31)
+ktune::Error                 Error
+===========================  ==============================================
+
+Every plan artefact (partition boundaries, regions, BSS flags/slices) is
+computed by device kernels and is bit-exact with the reference builders;
+every SpMV runs on the GPU. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+
+I64 = C.c_int64
+
+
+class Error(RuntimeError):
+    """ktune::Error (common.hpp:18-21): contract violations."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = _lib.load().ktb_last_error().decode()
+    if rc == 1:
+        raise Error(msg)
+    if rc == 3:
+        raise Error(msg)
+    raise CudaError(msg)
+
+
+def require(cond: bool, msg: str) -> None:  # common.hpp:23-25
+    if not cond:
+        raise Error(msg)
+
+
+class UnsymKernel(enum.IntEnum):  # spmv.hpp:15
+    u1_row = 0
+    u2_nnz = 1
+    u3_bss = 2
+    u4_ss = 3
+
+
+class SymKernel(enum.IntEnum):  # spmv.hpp:16 (ABI tags 16..18)
+    s1_row = 16
+    s2_nnz = 17
+    s3_nnz_zero_omit = 18
+
+
+class PartitionScheme(enum.IntEnum):  # partition.hpp:12
+    row_based = 0
+    nnz_balanced = 1
+
+
+def kernel_name(k) -> str:  # spmv.hpp:18-35
+    return {0: "u1", 1: "u2", 2: "u3", 3: "u4", 16: "s1", 17: "s2", 18: "s3"}[int(k)]
+
+
+# ------------------------------------------------------------------ storage
+class _DeviceMatrix:
+    """Owner of a ktb_matrix handle."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.h = handle
+        n, nnz, mx, bw = I64(), I64(), I64(), I64()
+        kind = C.c_int()
+        _check(_lib.load().ktb_matrix_info(handle, C.byref(n), C.byref(nnz), C.byref(kind),
+                                           C.byref(mx), C.byref(bw)))
+        self.n, self.nnz, self.kind = n.value, nnz.value, kind.value
+        self.max_row_nnz, self.bandwidth = mx.value, bw.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().ktb_matrix_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def download(self):
+        rp = np.empty(self.n + 1, np.int32)
+        ci = np.empty(max(self.nnz, 1), np.int32)
+        v = np.empty(max(self.nnz, 1), np.float64)
+        _check(_lib.load().ktb_matrix_download(self.h, rp.ctypes.data, ci.ctypes.data,
+                                               v.ctypes.data))
+        return rp, ci[: self.nnz], v[: self.nnz]
+
+
+@dataclass
+class CsrMatrix:
+    """csr.hpp:13-55: square CRS, int64 indices, fp64 values. Construction
+    validates (csr.hpp:38-54) and uploads to the device once."""
+
+    n: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    device: int = 0
+    _kind: int = field(default=0, repr=False)
+    _dev: Optional[_DeviceMatrix] = field(default=None, repr=False)
+
+    def __post_init__(self):
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, np.int64)
+        self.values = np.ascontiguousarray(self.values, np.float64)
+
+    def nnz(self) -> int:
+        return len(self.values)
+
+    def row_nnz(self, i: int) -> int:
+        return int(self.row_ptr[i + 1] - self.row_ptr[i])
+
+    def max_row_nnz(self) -> int:
+        return int(np.max(np.diff(self.row_ptr))) if self.n > 0 else 0
+
+    def storage_bytes(self) -> int:  # csr.hpp:30-33
+        return 8 * (len(self.row_ptr) + len(self.col_idx) + len(self.values))
+
+    @property
+    def dev(self) -> _DeviceMatrix:
+        if self._dev is None:
+            # csr.hpp:39-43 length checks the C ABI cannot see
+            require(self.n >= 0, "csr: negative dimension")
+            require(len(self.row_ptr) == self.n + 1, "csr: row_ptr length != n+1")
+            require(len(self.col_idx) == len(self.values), "csr: col_idx/values length mismatch")
+            require(self.row_ptr[0] == 0, "csr: row_ptr[0] != 0")
+            require(self.row_ptr[-1] == len(self.values), "csr: row_ptr[n] != nnz")
+            h = C.c_void_p()
+            _check(_lib.load().ktb_matrix_create(self.n, self.row_ptr.ctypes.data,
+                                                 self.col_idx.ctypes.data,
+                                                 self.values.ctypes.data, self._kind,
+                                                 self.device, C.byref(h)))
+            self._dev = _DeviceMatrix(h)
+        return self._dev
+
+    def validate(self) -> None:
+        _ = self.dev
+
+
+@dataclass
+class SymCsrMatrix(CsrMatrix):
+    """csr.hpp:57-65: diagonal + strict upper; A = U + U^T - diag(U)."""
+
+    _kind: int = field(default=1, repr=False)
+
+    def spmv_flops(self) -> int:  # csr.hpp:64
+        return 4 * self.nnz() - 2 * self.n
+
+
+class DeviceCsr:
+    """A matrix generated directly on the device (SURVEY.md §8d recipes);
+    behaves like CsrMatrix/SymCsrMatrix for every call here."""
+
+    def __init__(self, handle: C.c_void_p, sym: bool):
+        self._dev = _DeviceMatrix(handle)
+        self._kind = 1 if sym else 0
+        self.n = self._dev.n
+
+    @property
+    def dev(self):
+        return self._dev
+
+    def nnz(self) -> int:
+        return self._dev.nnz
+
+    def spmv_flops(self) -> int:
+        return 4 * self.nnz() - 2 * self.n if self._kind else 2 * self.nnz()
+
+    def to_host(self):
+        rp, ci, v = self._dev.download()
+        return rp.astype(np.int64), ci.astype(np.int64), v
+
+
+def stencil7(nx, ny, nz, diag=6.0, off=-1.0, c_xm=None, c_xp=None, device=0) -> DeviceCsr:
+    h = C.c_void_p()
+    _check(_lib.load().ktb_gen_stencil7(nx, ny, nz, diag, off, off if c_xm is None else c_xm,
+                                        off if c_xp is None else c_xp, device, C.byref(h)))
+    return DeviceCsr(h, False)
+
+
+def stencil27_upper(nx, ny, nz, diag=26.0, off=-1.0, device=0) -> DeviceCsr:
+    h = C.c_void_p()
+    _check(_lib.load().ktb_gen_stencil27_upper(nx, ny, nz, diag, off, device, C.byref(h)))
+    return DeviceCsr(h, True)
+
+
+def stencil7_slab(nx, ny, nz, z0, z1, diag=6.0, off=-1.0, device=0) -> DeviceCsr:
+    h = C.c_void_p()
+    _check(_lib.load().ktb_gen_stencil7_slab(nx, ny, nz, z0, z1, diag, off, device,
+                                             C.byref(h)))
+    return DeviceCsr(h, False)
+
+
+# -------------------------------------------------------------- artefacts
+@dataclass
+class RowPartition:  # partition.hpp:15-23
+    num_workers: int
+    boundaries: np.ndarray
+    scheme: PartitionScheme
+    n: int = -1
+
+    def lo(self, p):
+        return int(self.boundaries[p])
+
+    def hi(self, p):
+        return int(self.boundaries[p + 1])
+
+    def rows(self):
+        return int(self.boundaries[-1])
+
+
+@dataclass
+class ReductionRegions:  # partition.hpp:60-71
+    num_workers: int
+    lo: np.ndarray
+    hi: np.ndarray
+
+    def total_width(self) -> int:
+        return int(np.sum(self.hi - self.lo))
+
+
+@dataclass
+class BssPlan:  # bss.hpp:19-32
+    jl: int
+    n: int
+    nnz: int
+    slice_start: np.ndarray
+    slice_len: np.ndarray
+    slice_row: np.ndarray
+    lane_slice_ptr: np.ndarray
+    row_slice_ptr: np.ndarray
+    row_start_flag: np.ndarray
+
+    def total_slices(self) -> int:
+        return len(self.slice_start)
+
+
+def build_row_partition(a, num_workers: int, scheme) -> RowPartition:
+    """partition.hpp:28-55 on the device. `a` is a matrix (the reference takes
+    its row_ptr span)."""
+    require(num_workers >= 1, "row partition: num_workers must be >= 1")
+    out = np.empty(num_workers + 1, np.int64)
+    _check(_lib.load().ktb_row_partition(a.dev.h, num_workers, int(scheme), out.ctypes.data))
+    return RowPartition(num_workers, out, PartitionScheme(int(scheme)), a.n)
+
+
+def build_reduction_regions(a, part: RowPartition) -> ReductionRegions:
+    require(part.rows() == a.n, "reduction regions: partition/matrix dimension mismatch")
+    P = part.num_workers
+    lo, hi = np.empty(P, np.int64), np.empty(P, np.int64)
+    b = np.ascontiguousarray(part.boundaries, np.int64)
+    _check(_lib.load().ktb_reduction_regions(a.dev.h, P, b.ctypes.data, lo.ctypes.data,
+                                             hi.ctypes.data))
+    return ReductionRegions(P, lo, hi)
+
+
+def build_bss_plan(a, jl: int) -> BssPlan:
+    require(jl >= 1, "bss plan: jl must be >= 1")
+    require(a.nnz() > 0, "bss plan: empty matrix")
+    L = _lib.load()
+    je, tot = I64(), I64()
+    _check(L.ktb_bss_plan_size(a.dev.h, jl, C.byref(je), C.byref(tot)))
+    T, J, n, nnz = tot.value, je.value, a.n, a.nnz()
+    arr = [np.empty(T, np.int64) for _ in range(3)]
+    lane = np.empty(J + 1, np.int64)
+    rsp = np.empty(n + 1, np.int64)
+    flag = np.empty(nnz, np.uint8)
+    _check(L.ktb_bss_plan_copy(a.dev.h, jl, arr[0].ctypes.data, arr[1].ctypes.data,
+                               arr[2].ctypes.data, lane.ctypes.data, rsp.ctypes.data,
+                               flag.ctypes.data))
+    return BssPlan(J, n, nnz, arr[0], arr[1], arr[2], lane, rsp, flag)
+
+
+def expand_symmetric(a) -> DeviceCsr:
+    require(a._kind == 1, "expand_symmetric: matrix is not symmetric storage")
+    h = C.c_void_p()
+    _check(_lib.load().ktb_expand_symmetric(a.dev.h, C.byref(h)))
+    return DeviceCsr(h, False)
+
+
+# ------------------------------------------------------------------ plans
+class DevicePlan:
+    """ktb_plan: a kernel bound to its device decomposition and stream."""
+
+    def __init__(self, a, kernel: int, param: int = 0, workers: int = 0, stream=None,
+                 handle=None):
+        self.a = a  # keep the matrix alive (engines hold a reference, meta.hpp:44)
+        self.n = a.n
+        if handle is None:
+            h = C.c_void_p()
+            _check(_lib.load().ktb_plan_create(a.dev.h, int(kernel), int(param), int(workers),
+                                               stream, C.byref(h)))
+            handle = h
+        self.h = handle
+        k, prm, ctas, launches, extra = C.c_int(), I64(), I64(), C.c_int(), I64()
+        _check(_lib.load().ktb_plan_info(self.h, C.byref(k), C.byref(prm), C.byref(ctas),
+                                         C.byref(launches), C.byref(extra)))
+        self.kernel, self.param, self.ctas = k.value, prm.value, ctas.value
+        self.launches, self.extra_bytes = launches.value, extra.value
+
+    def set_stream(self, stream) -> None:
+        _check(_lib.load().ktb_plan_set_stream(self.h, stream))
+
+    def apply(self, x, y) -> None:
+        """y = A x. numpy arrays -> host-span mode (copies, synchronous);
+        torch CUDA tensors or raw device pointers (int) -> device mode."""
+        if isinstance(x, np.ndarray):
+            require(x.dtype == np.float64 and y.dtype == np.float64 and x.flags.c_contiguous
+                    and y.flags.c_contiguous, "spmv: dimension mismatch")
+            _check(_lib.load().ktb_spmv(self.h, x.ctypes.data, y.ctypes.data, 0))
+        else:
+            _check(_lib.load().ktb_spmv(self.h, _dptr(x), _dptr(y), 1))
+
+    def apply_rows(self, r0, r1, x, y) -> None:
+        _check(_lib.load().ktb_spmv_rows(self.h, r0, r1, _dptr(x), _dptr(y)))
+
+    def time(self, x, y, reps=20, flush_bytes=0):
+        avg, mn = C.c_double(), C.c_double()
+        _check(_lib.load().ktb_time_spmv(self.h, _dptr(x), _dptr(y), reps, flush_bytes,
+                                         C.byref(avg), C.byref(mn)))
+        return avg.value, mn.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().ktb_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _dptr(t) -> int:
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        require(bool(getattr(t, "is_cuda", False)), "spmv: device mode needs CUDA tensors")
+        return int(t.data_ptr())
+    raise Error("spmv: unsupported vector type")
+
+
+_plan_cache: dict = {}
+
+
+def _plan_for(a, kernel, param=0, workers=0) -> DevicePlan:
+    key = (id(a.dev), int(kernel), int(param), int(workers))
+    p = _plan_cache.get(key)
+    if p is None or p.a is not a:
+        p = DevicePlan(a, kernel, param, workers)
+        _plan_cache[key] = p
+    return p
+
+
+def _len(v) -> int:
+    return int(v.shape[0]) if hasattr(v, "shape") else len(v)
+
+
+def spmv_unsym(kernel, a, part: Optional[RowPartition], plan: Optional[BssPlan], x, y=None):
+    """spmv.hpp:111-170: same contract checks and messages, then the GPU
+    kernel for the variant (U1 vector-per-row, U2 merge-path, U3 BSS, U4 flag
+    scan). Allocating form when y is None (spmv.hpp:238-244)."""
+    kernel = UnsymKernel(int(kernel))
+    if y is None:
+        y = np.empty(a.n, np.float64) if isinstance(x, np.ndarray) else _like(x, a.n)
+    require(_len(x) == a.n and _len(y) == a.n, "spmv: dimension mismatch")
+    if kernel in (UnsymKernel.u1_row, UnsymKernel.u2_nnz):
+        require(part is not None, "spmv: U1/U2 need a row partition")
+        require(part.rows() == a.n, "spmv: partition built for a different matrix")
+        want = (PartitionScheme.row_based if kernel == UnsymKernel.u1_row
+                else PartitionScheme.nnz_balanced)
+        require(part.scheme == want, "spmv: partition scheme does not match kernel")
+        _plan_for(a, kernel).apply(x, y)
+    else:
+        require(plan is not None, "spmv: U3/U4 need a bss plan")
+        require(plan.n == a.n and plan.nnz == a.nnz(), "spmv: plan built for a different matrix")
+        _plan_for(a, kernel).apply(x, y)
+    return y
+
+
+def spmv_sym(kernel, a, part: RowPartition, regions: Optional[ReductionRegions], x, y=None):
+    """spmv.hpp:180-234 contract, GPU kernels S1/S2 (atomic full-range) and
+    S3 (zero-omission smem window)."""
+    kernel = SymKernel(int(kernel))
+    if y is None:
+        y = np.empty(a.n, np.float64) if isinstance(x, np.ndarray) else _like(x, a.n)
+    require(_len(x) == a.n and _len(y) == a.n, "spmv: dimension mismatch")
+    require(part.rows() == a.n, "spmv: partition built for a different matrix")
+    want = PartitionScheme.row_based if kernel == SymKernel.s1_row else PartitionScheme.nnz_balanced
+    require(part.scheme == want, "spmv: partition scheme does not match kernel")
+    omit = kernel == SymKernel.s3_nnz_zero_omit
+    require(not omit or regions is not None, "spmv: S3 needs reduction regions")
+    if omit:
+        require(regions.num_workers == part.num_workers,
+                "spmv: regions built for a different partition")
+    _plan_for(a, kernel).apply(x, y)
+    return y
+
+
+def _like(x, n):
+    import torch
+
+    return torch.empty(n, dtype=torch.float64, device=x.device)
+
+
+# --------------------------------------------------------------- selector
+@dataclass
+class TuningCandidate:  # autotune.hpp:130-139
+    name: str
+    ordinal: int
+    jl: int
+    workers: int
+    trial_seconds: list
+    best_seconds: float
+    correct: bool
+    executions: int
+
+
+@dataclass
+class TuningReport:  # autotune.hpp:141-158
+    candidates: list
+    selected: int = -1
+    trials_per_candidate: int = 3
+    forced: bool = False
+
+    def max_executions(self) -> int:
+        return max((c.executions for c in self.candidates), default=0)
+
+    def selected_candidate(self) -> TuningCandidate:
+        require(0 <= self.selected < len(self.candidates), "tuning report: nothing selected")
+        return self.candidates[self.selected]
+
+
+@dataclass
+class SelectOptions:  # autotune.hpp:160-165
+    jl_candidates: Optional[list] = None  # GPU: nonzeros per BSS lane (jl = nnz / E)
+    timed_trials: int = 3
+    sweep_workers: bool = False
+    now: Optional[Callable[[], float]] = None
+
+
+class _Cand(C.Structure):
+    _fields_ = [("name", C.c_char * 8), ("ordinal", C.c_int), ("param", I64),
+                ("workers", C.c_int), ("correct", C.c_int), ("executions", C.c_int),
+                ("n_trials", C.c_int), ("best_seconds", C.c_double),
+                ("trial_seconds", C.c_double * 8)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("params", C.c_void_p), ("n_params", C.c_int), ("timed_trials", C.c_int),
+                ("workers", C.c_int), ("now", C.c_void_p), ("now_ctx", C.c_void_p)]
+
+
+_NOW = C.CFUNCTYPE(C.c_double, C.c_void_p)
+
+
+@dataclass
+class UnsymChoice:  # autotune.hpp:168-175
+    kernel: UnsymKernel
+    jl: int
+    workers: int
+    plan: DevicePlan
+
+
+@dataclass
+class SymChoice:  # autotune.hpp:177-183
+    kernel: SymKernel
+    workers: int
+    plan: DevicePlan
+
+
+def _select(a, opts: Optional[SelectOptions]):
+    require(a.n > 0 and a.nnz() > 0, "kernel selection: empty matrix")
+    opts = opts or SelectOptions()
+    o = _Opts()
+    params = None
+    if opts.jl_candidates:
+        params = np.ascontiguousarray(opts.jl_candidates, np.int64)
+        o.params, o.n_params = params.ctypes.data, len(params)
+    o.timed_trials = opts.timed_trials
+    cb = None
+    if opts.now is not None:
+        cb = _NOW(lambda _ctx: float(opts.now()))
+        o.now = C.cast(cb, C.c_void_p)
+    cands = (_Cand * 64)()
+    nc, sel = C.c_int(), C.c_int()
+    h = C.c_void_p()
+    _check(_lib.load().ktb_select(a.dev.h, C.byref(o), None, C.byref(h), cands, 64,
+                                  C.byref(nc), C.byref(sel)))
+    rep = TuningReport([], sel.value, opts.timed_trials)
+    for i in range(nc.value):
+        c = cands[i]
+        rep.candidates.append(TuningCandidate(c.name.decode(), c.ordinal, c.param, c.workers,
+                                              list(c.trial_seconds[: c.n_trials]),
+                                              c.best_seconds, bool(c.correct), c.executions))
+    return DevicePlan(a, 0, handle=h), rep
+
+
+def select_spmv_unsym(a, pool=None, opts: Optional[SelectOptions] = None):
+    """autotune.hpp:267-330 on device time; returns (UnsymChoice, TuningReport)."""
+    plan, rep = _select(a, opts)
+    w = rep.selected_candidate()
+    return UnsymChoice(UnsymKernel(plan.kernel), w.jl, w.workers, plan), rep
+
+
+def select_spmv_sym(a, pool=None, opts: Optional[SelectOptions] = None):
+    """autotune.hpp:333-377 on device time; returns (SymChoice, TuningReport)."""
+    plan, rep = _select(a, opts)
+    w = rep.selected_candidate()
+    return SymChoice(SymKernel(plan.kernel), w.workers, plan), rep
+
+
+# ----------------------------------------------------------------- engines
+@dataclass
+class LinOp:  # solver_types.hpp:17-20
+    n: int
+    apply: Callable
+
+
+class _Engine:
+    def __init__(self, a, choice):
+        self.a = a
+        self.choice = choice
+        self._calls = 0
+        self._seconds = 0.0
+
+    def op(self) -> LinOp:
+        """meta.hpp:25-35: a LinOp that runs the tuned kernel, counting calls
+        and in-kernel seconds (host spans -> H2D/D2H inside)."""
+
+        def apply(x, y):
+            t0 = time.perf_counter()
+            self.choice.plan.apply(x, y)
+            self._seconds += time.perf_counter() - t0
+            self._calls += 1
+
+        return LinOp(self.a.n, apply)
+
+    def calls(self) -> int:
+        return self._calls
+
+    def kernel_seconds(self) -> float:
+        return self._seconds
+
+    def workers(self) -> int:
+        return self.choice.workers
+
+
+class UnsymEngine(_Engine):  # meta.hpp:20-49
+    def flops_per_call(self) -> float:
+        return 2.0 * self.a.nnz()
+
+
+class SymEngine(_Engine):  # meta.hpp:51-82
+    def flops_per_call(self) -> float:
+        return float(self.a.spmv_flops())
+
+
+def make_ref_op(a) -> LinOp:
+    """solver_types.hpp:29-31 -- here backed by the device U1 kernel; the
+    CPU oracle lives in oracle/ (tests only)."""
+    plan = _plan_for(a, SymKernel.s3_nnz_zero_omit if a._kind else UnsymKernel.u1_row)
+    return LinOp(a.n, plan.apply)

@@ -1,0 +1,210 @@
+"""Generate tests/golden/*.npz from the REFERENCE ITSELF.
+
+Every output array here is produced by the unmodified reference headers
+(/root/reference/proj/include/ktune) compiled into oracle/_ref/libktune_ref.so
+by oracle/Makefile (see oracle/ref_shim.cpp). Run where the reference tree
+exists:
+
+    make -C oracle && python tests/golden/make_golden.py
+
+The fixtures pin (a) the C restatement in oracle/ktune_oracle.c (tests compare
+it bitwise against these vectors) and (b) the CUDA path (integer artefacts
+bit-exact, fp64 within 1e-12*(|A||x|)_i). Inputs are seeded synthetic
+matrices (the reference ships no matrices or golden files).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))  # tests/
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))  # repo root
+
+import matgen  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+R = O.Ref
+WORKERS = (1, 2, 3, 4, 8)
+JLS = (1, 8, 16, 32, 64, 128, 256)
+
+
+def random_family(seed=20240501, count=48):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for c in range(count):
+        n = int(rng.integers(1, 220))
+        kind = c % 4
+        dens = float(rng.choice([0.005, 0.02, 0.05, 0.2]))
+        if kind == 0:
+            m = matgen.random_csr(n, dens, rng)
+        elif kind == 1:
+            m = matgen.random_csr(n, dens, rng, skew=True)
+        elif kind == 2:
+            m = matgen.random_csr(n, dens, rng, empty_frac=0.3)
+        else:
+            m = matgen.random_csr(n, dens, rng, skew=True, empty_frac=0.1)
+        cases.append(m)
+    return cases
+
+
+def sym_family(seed=77, count=32):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for c in range(count):
+        n = int(rng.integers(1, 200))
+        dens = float(rng.choice([0.01, 0.03, 0.1]))
+        cases.append(matgen.random_csr(n, dens, rng, upper=True, skew=(c % 3 == 1),
+                                       empty_frac=0.2 if c % 3 == 2 else 0.0))
+    cases.append(matgen.stencil27_upper(6, 5, 4))
+    cases.append(matgen.dense_to_csr(np.diag(np.arange(1.0, 9.0)), upper=True))
+    return cases
+
+
+def unsym_golden(cases):
+    out = {"count": np.array(len(cases))}
+    for c, (n, rp, ci, v) in enumerate(cases):
+        p = f"c{c}_"
+        x = R.seeded_vector(n, 1000 + c)
+        out[p + "n"] = np.array(n)
+        out[p + "rp"], out[p + "ci"], out[p + "v"], out[p + "x"] = rp, ci, v, x
+        out[p + "y_ref"] = R.spmv_ref(n, rp, ci, v, x)
+        for P in WORKERS:
+            out[p + f"part_row_{P}"] = R.build_row_partition(rp, P, 0)
+            out[p + f"part_nnz_{P}"] = R.build_row_partition(rp, P, 1)
+            out[p + f"y_u1_{P}"] = R.spmv_unsym(0, n, rp, ci, v, P, 0, x)
+            out[p + f"y_u2_{P}"] = R.spmv_unsym(1, n, rp, ci, v, P, 0, x)
+        if rp[-1] > 0:
+            for jl in JLS:
+                plan = R.build_bss_plan(n, rp, ci, v, jl)
+                for f in ("slice_start", "slice_len", "slice_row", "lane_slice_ptr",
+                          "row_slice_ptr", "row_start_flag"):
+                    out[p + f"bss{jl}_{f}"] = getattr(plan, f)
+                out[p + f"bss{jl}_jl"] = np.array(plan.jl)
+                out[p + f"y_u3_{jl}"] = R.spmv_unsym(2, n, rp, ci, v, 4, jl, x)
+                out[p + f"y_u4_{jl}"] = R.spmv_unsym(3, n, rp, ci, v, 4, jl, x)
+    return out
+
+
+def sym_golden(cases):
+    out = {"count": np.array(len(cases))}
+    for c, (n, rp, ci, v) in enumerate(cases):
+        p = f"c{c}_"
+        x = R.seeded_vector(n, 2000 + c)
+        out[p + "n"] = np.array(n)
+        out[p + "rp"], out[p + "ci"], out[p + "v"], out[p + "x"] = rp, ci, v, x
+        erp, eci, ev = R.expand_symmetric(n, rp, ci, v)
+        out[p + "full_rp"], out[p + "full_ci"], out[p + "full_v"] = erp, eci, ev
+        out[p + "y_ref"] = R.spmv_ref(n, erp, eci, ev, x)
+        for P in WORKERS:
+            lo, hi = R.build_reduction_regions(n, rp, ci, v, P, 1)
+            out[p + f"reg_lo_{P}"], out[p + f"reg_hi_{P}"] = lo, hi
+            lo0, hi0 = R.build_reduction_regions(n, rp, ci, v, P, 0)
+            out[p + f"regrow_lo_{P}"], out[p + f"regrow_hi_{P}"] = lo0, hi0
+            for k in range(3):
+                out[p + f"y_s{k + 1}_{P}"] = R.spmv_sym(k, n, rp, ci, v, P, x)
+    return out
+
+
+def stencil_golden():
+    out = {}
+    # config-1 recipe at 8^3 and config-2 recipe at 8^3 (structure + one product)
+    n, rp, ci, v = matgen.stencil7(8, 8, 8)
+    x = R.seeded_vector(n, 1)
+    out["s7_rp"], out["s7_ci"], out["s7_v"], out["s7_x"] = rp, ci, v, x
+    out["s7_y"] = R.spmv_ref(n, rp, ci, v, x)
+    n, rp, ci, v = matgen.stencil27_upper(8, 8, 8)
+    x = R.seeded_vector(n, 2)
+    out["s27_rp"], out["s27_ci"], out["s27_v"], out["s27_x"] = rp, ci, v, x
+    erp, eci, ev = R.expand_symmetric(n, rp, ci, v)
+    out["s27_y"] = R.spmv_ref(n, erp, eci, ev, x)
+    # config-5 recipe at 16^3: GMRES(30) + MGS known answer from the reference
+    n, rp, ci, v = matgen.stencil7(16, 16, 16, xp=-0.7, xm=-1.3)
+    b = R.spmv_ref(n, rp, ci, v, np.ones(n))
+    xs, res = R.gmres(n, rp, ci, v, b, m=30, tol=1e-8, max_iters=3000)
+    out["cd_rp"], out["cd_ci"], out["cd_v"], out["cd_b"] = rp, ci, v, b
+    out["cd_x"], out["cd_hist"] = xs, res["history"]
+    out["cd_iterations"] = np.array(res["iterations"])
+    out["cd_restarts"] = np.array(res["restarts"])
+    out["cd_spmv_calls"] = np.array(res["spmv_calls"])
+    out["cd_rec"] = np.array(res["recurrence_residual"])
+    out["cd_true"] = np.array(res["true_residual"])
+    # generators: seeded_vector / probe_vector prefixes and long-stream checksums
+    out["seeded_1_64"] = R.seeded_vector(64, 1)
+    out["seeded_3_64"] = R.seeded_vector(64, 3)
+    big = R.seeded_vector(1 << 20, 2)
+    out["seeded_2_sum"] = np.array(np.sum(big))
+    out["seeded_2_last"] = big[-8:].copy()
+    out["probe_64"] = R.probe_vector(64)
+    out["probe_sum_1m"] = np.array(np.sum(R.probe_vector(1 << 20)))
+    return out
+
+
+def select_golden():
+    """select_spmv_* with the injected timer (autotune.hpp:164): a scripted
+    clock makes the choice deterministic."""
+    out = {}
+    rng = np.random.default_rng(5)
+    n, rp, ci, v = matgen.random_csr(300, 0.05, rng)
+    out["u_rp"], out["u_ci"], out["u_v"] = rp, ci, v
+    for tag, durations in (("u2fast", {1: 0.5}), ("tie", {0: 1.0, 1: 1.0}),
+                           ("u3fast", {2: 0.25})):
+        clock = _ScriptedClock(durations)
+        cands, sel = R.select(False, n, rp, ci, v, 4, now=clock)
+        out[f"u_{tag}_sel"] = np.array(sel)
+        out[f"u_{tag}_names"] = np.array([c["name"] for c in cands])
+        out[f"u_{tag}_jl"] = np.array([c["jl"] for c in cands])
+        out[f"u_{tag}_exec"] = np.array([c["executions"] for c in cands])
+        out[f"u_{tag}_best"] = np.array([c["best_seconds"] for c in cands])
+    n, rp, ci, v = matgen.random_csr(200, 0.03, rng, upper=True)
+    out["s_rp"], out["s_ci"], out["s_v"] = rp, ci, v
+    for tag, durations in (("s3fast", {2: 0.5}), ("tie23", {})):
+        clock = _ScriptedClock(durations, sym=True)
+        cands, sel = R.select(True, n, rp, ci, v, 4, now=clock)
+        out[f"s_{tag}_sel"] = np.array(sel)
+        out[f"s_{tag}_names"] = np.array([c["name"] for c in cands])
+        out[f"s_{tag}_best"] = np.array([c["best_seconds"] for c in cands])
+    return out
+
+
+class _ScriptedClock:
+    """Injected timer: each candidate's 3 timed trials read a scripted
+    duration per candidate ordinal, in the order the reference times them
+    (u1, u2, u3@jl... / s1, s2, s3). Unlisted candidates take 1.0 s; for the
+    unsym u3 family jl scales the duration so the smallest jl wins ties."""
+
+    def __init__(self, durations, sym=False):
+        self.t = 0.0
+        self.calls = 0
+        self.durations = durations
+        self.sym = sym
+        self.seq = []
+
+    def __call__(self):
+        # tic/toc pairs; each pair is one timed trial. 3 trials per candidate.
+        pair = self.calls // 2
+        cand = pair // 3
+        if self.calls % 2 == 1:
+            self.t += self._dur(cand)
+        self.calls += 1
+        return self.t
+
+    def _dur(self, cand):
+        ordinal = min(cand, 2)
+        return float(self.durations.get(ordinal, 1.0))
+
+
+def main():
+    np.savez_compressed(os.path.join(HERE, "unsym.npz"), **unsym_golden(random_family()))
+    np.savez_compressed(os.path.join(HERE, "sym.npz"), **sym_golden(sym_family()))
+    np.savez_compressed(os.path.join(HERE, "stencil.npz"), **stencil_golden())
+    np.savez_compressed(os.path.join(HERE, "select.npz"), **select_golden())
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()

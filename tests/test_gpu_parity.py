@@ -1,0 +1,340 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle
+and the reference's golden fixtures.
+
+Bars (BASELINE.json north_star):
+  * integer artefacts (partition boundaries, reduction regions, BSS flags /
+    slices / row assignment, expand_symmetric structure) bit-exact;
+  * fp64 outputs |y_i - y_ref_i| <= 1e-12 * (|A||x|)_i on every row.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import matgen
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 1e-12
+WORKERS = (1, 2, 3, 4, 8)
+JLS = (1, 8, 16, 32, 64, 128, 256)
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2405_01599_b200 import ktune
+
+    return ktune
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def cases(g):
+    for c in range(int(g["count"])):
+        p = f"c{c}_"
+        yield c, p, int(g[p + "n"]), g[p + "rp"], g[p + "ci"], g[p + "v"], g[p + "x"]
+
+
+def assert_close(y, y_ref, absax, what=""):
+    err = np.abs(np.asarray(y) - y_ref)
+    bound = TOL * absax
+    bad = np.nonzero(err > bound)[0]
+    assert bad.size == 0, (what, bad[:5], err[bad[:5]], bound[bad[:5]])
+
+
+def absax_of(n, rp, ci, v, x):
+    return O.spmv_ref(n, rp, ci, np.abs(v), np.abs(x))
+
+
+UNSYM = ("u1_row", "u2_nnz", "u3_bss", "u4_ss")
+SYM = ("s1_row", "s2_nnz", "s3_nnz_zero_omit")
+
+
+# ------------------------------------------------------------ artefacts
+def test_partitions_and_bss_plans_bit_exact(K):
+    g = load("unsym.npz")
+    for c, p, n, rp, ci, v, x in cases(g):
+        a = K.CsrMatrix(n, rp, ci, v)
+        for P in WORKERS:
+            part = K.build_row_partition(a, P, K.PartitionScheme.row_based)
+            assert np.array_equal(part.boundaries, g[p + f"part_row_{P}"]), (c, P)
+            part = K.build_row_partition(a, P, K.PartitionScheme.nnz_balanced)
+            assert np.array_equal(part.boundaries, g[p + f"part_nnz_{P}"]), (c, P)
+        if rp[-1] == 0:
+            continue
+        for jl in JLS:
+            plan = K.build_bss_plan(a, jl)
+            assert plan.jl == int(g[p + f"bss{jl}_jl"])
+            for f in ("slice_start", "slice_len", "slice_row", "lane_slice_ptr",
+                      "row_slice_ptr", "row_start_flag"):
+                assert np.array_equal(getattr(plan, f), g[p + f"bss{jl}_{f}"]), (c, jl, f)
+
+
+def test_regions_and_expand_symmetric_bit_exact(K):
+    g = load("sym.npz")
+    for c, p, n, rp, ci, v, x in cases(g):
+        a = K.SymCsrMatrix(n, rp, ci, v)
+        for P in WORKERS:
+            part = K.build_row_partition(a, P, K.PartitionScheme.nnz_balanced)
+            r = K.build_reduction_regions(a, part)
+            assert np.array_equal(r.lo, g[p + f"reg_lo_{P}"]), (c, P)
+            assert np.array_equal(r.hi, g[p + f"reg_hi_{P}"]), (c, P)
+            part = K.build_row_partition(a, P, K.PartitionScheme.row_based)
+            r = K.build_reduction_regions(a, part)
+            assert np.array_equal(r.lo, g[p + f"regrow_lo_{P}"])
+            assert np.array_equal(r.hi, g[p + f"regrow_hi_{P}"])
+        if n and rp[-1]:
+            full = K.expand_symmetric(a)
+            frp, fci, fv = full.to_host()
+            assert np.array_equal(frp, g[p + "full_rp"]) and np.array_equal(fci, g[p + "full_ci"])
+            assert np.array_equal(fv, g[p + "full_v"])
+
+
+# ------------------------------------------------------------ SpMV parity
+def _run_unsym(K, a, kernel, x):
+    k = K.UnsymKernel[kernel]
+    part = K.build_row_partition(a, 4, K.PartitionScheme.row_based if k == 0
+                                 else K.PartitionScheme.nnz_balanced)
+    plan = K.build_bss_plan(a, 8) if k >= 2 else None
+    return K.spmv_unsym(k, a, part if k < 2 else None, plan, x)
+
+
+def test_unsym_variants_golden(K):
+    g = load("unsym.npz")
+    for c, p, n, rp, ci, v, x in cases(g):
+        a = K.CsrMatrix(n, rp, ci, v)
+        absax = absax_of(n, rp, ci, v, x)
+        for kern in UNSYM:
+            if kern in ("u3_bss", "u4_ss") and rp[-1] == 0:
+                continue
+            y = _run_unsym(K, a, kern, x)
+            assert_close(y, g[p + "y_ref"], absax, (c, kern))
+
+
+def test_u3_equals_u4_bitwise(K):
+    g = load("unsym.npz")
+    for c, p, n, rp, ci, v, x in cases(g):
+        if rp[-1] == 0:
+            continue
+        a = K.CsrMatrix(n, rp, ci, v)
+        assert np.array_equal(_run_unsym(K, a, "u3_bss", x), _run_unsym(K, a, "u4_ss", x)), c
+
+
+def _run_sym(K, a, kernel, x):
+    k = K.SymKernel[kernel]
+    part = K.build_row_partition(a, 4, K.PartitionScheme.row_based if kernel == "s1_row"
+                                 else K.PartitionScheme.nnz_balanced)
+    regions = K.build_reduction_regions(a, part) if kernel == "s3_nnz_zero_omit" else None
+    return K.spmv_sym(k, a, part, regions, x)
+
+
+def test_sym_variants_golden(K):
+    g = load("sym.npz")
+    for c, p, n, rp, ci, v, x in cases(g):
+        a = K.SymCsrMatrix(n, rp, ci, v)
+        absax = absax_of(n, g[p + "full_rp"], g[p + "full_ci"], g[p + "full_v"], x)
+        for kern in SYM:
+            y = _run_sym(K, a, kern, x)
+            assert_close(y, g[p + "y_ref"], absax, (c, kern))
+
+
+def test_s3_is_deterministic(K):
+    n, rp, ci, v = matgen.stencil27_upper(24, 20, 18)
+    a = K.SymCsrMatrix(n, rp, ci, v)
+    x = O.seeded_vector(n, 2)
+    y0 = _run_sym(K, a, "s3_nnz_zero_omit", x)
+    for _ in range(3):
+        assert np.array_equal(_run_sym(K, a, "s3_nnz_zero_omit", x), y0)
+
+
+def test_random_families_all_variants(K):
+    """SPEC.md:559-570 style sweep: random matrices incl. skewed rows, empty
+    rows, single rows, against the oracle."""
+    rng = np.random.default_rng(99)
+    for t in range(30):
+        n = int(rng.integers(1, 700))
+        n, rp, ci, v = matgen.random_csr(n, float(rng.choice([0.002, 0.02, 0.1])), rng,
+                                         skew=bool(t % 2), empty_frac=0.2 * (t % 3 == 2))
+        x = rng.uniform(-1, 1, n)
+        a = K.CsrMatrix(n, rp, ci, v)
+        yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
+        for kern in UNSYM:
+            if kern in ("u3_bss", "u4_ss") and rp[-1] == 0:
+                continue
+            assert_close(_run_unsym(K, a, kern, x), yref, absax, (t, kern))
+        n, rp, ci, v = matgen.random_csr(n, float(rng.choice([0.005, 0.05])), rng, upper=True,
+                                         skew=bool(t % 2))
+        s = K.SymCsrMatrix(n, rp, ci, v)
+        erp, eci, ev = O.expand_symmetric(n, rp, ci, v)
+        yref, absax = O.spmv_ref(n, erp, eci, ev, x), absax_of(n, erp, eci, ev, x)
+        for kern in SYM:
+            assert_close(_run_sym(K, s, kern, x), yref, absax, (t, kern))
+
+
+def test_long_rows_and_empty_rows(K):
+    """Row-length extremes: one row holding most nonzeros (generate.hpp:73-96
+    skewed_rows regime), runs of empty rows, trailing empties."""
+    n = 5000
+    rows = [np.arange(0, n, dtype=np.int64)]
+    rows += [np.array([i], np.int64) for i in range(1, n // 2)]
+    rows += [np.array([], np.int64)] * 700
+    rows += [np.array([3, 17, n - 1], np.int64)]
+    rows += [np.array([], np.int64)] * (n - len(rows))
+    assert len(rows) == n
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.concatenate(rows).astype(np.int64)
+    v = np.random.default_rng(3).uniform(-1, 1, len(ci))
+    x = O.seeded_vector(n, 5)
+    a = K.CsrMatrix(n, rp, ci, v)
+    yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
+    for kern in UNSYM:
+        assert_close(_run_unsym(K, a, kern, x), yref, absax, kern)
+
+
+# ------------------------------------------------------------ configs
+def test_generators_match_recipes(K):
+    for dims in ((8, 8, 8), (5, 7, 3)):
+        d = K.stencil7(*dims)
+        rp, ci, v = d.to_host()
+        n, rp2, ci2, v2 = matgen.stencil7(*dims)
+        assert np.array_equal(rp, rp2) and np.array_equal(ci, ci2) and np.array_equal(v, v2)
+        d = K.stencil27_upper(*dims)
+        rp, ci, v = d.to_host()
+        n, rp2, ci2, v2 = matgen.stencil27_upper(*dims)
+        assert np.array_equal(rp, rp2) and np.array_equal(ci, ci2) and np.array_equal(v, v2)
+    d = K.stencil7(6, 5, 4, diag=6.0, c_xm=-1.3, c_xp=-0.7)
+    rp, ci, v = d.to_host()
+    n, rp2, ci2, v2 = matgen.stencil7(6, 5, 4, xp=-0.7, xm=-1.3)
+    assert np.array_equal(v, v2)
+
+
+def test_config1_full_size_all_unsym(K):
+    """config 1 (64^3 7-pt, n=262,144, nnz=1,810,432) on every row."""
+    import torch
+
+    a = K.stencil7(64, 64, 64)
+    assert a.n == 262144 and a.nnz() == 1810432
+    rp, ci, v = a.to_host()
+    x = O.seeded_vector(a.n, 1)
+    yref, absax = O.spmv_ref(a.n, rp, ci, v, x), absax_of(a.n, rp, ci, v, x)
+    xd = torch.from_numpy(x).cuda()
+    for kern in UNSYM:
+        y = _run_unsym(K, a, kern, xd)
+        assert_close(y.cpu().numpy(), yref, absax, kern)
+
+
+def test_config2_full_size_sym(K):
+    """config 2 (128^3 27-pt upper, n=2,097,152, nnz_s=28,920,060) on every
+    row, all three symmetric kernels, against spmv_ref(expand_symmetric(A))."""
+    import torch
+
+    a = K.stencil27_upper(128, 128, 128)
+    assert a.n == 2097152 and a.nnz() == 28920060
+    rp, ci, v = a.to_host()
+    erp, eci, ev = O.expand_symmetric(a.n, rp, ci, v)
+    assert len(ev) == 55742968
+    x = O.seeded_vector(a.n, 2)
+    yref, absax = O.spmv_ref(a.n, erp, eci, ev, x), absax_of(a.n, erp, eci, ev, x)
+    xd = torch.from_numpy(x).cuda()
+    for kern in SYM:
+        y = _run_sym(K, a, kern, xd)
+        assert_close(y.cpu().numpy(), yref, absax, kern)
+
+
+def test_seeded_vector_device_bitwise(K):
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_01599_b200 import _lib
+
+    n = 100003
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    assert _lib.load().ktb_seeded_vector(n, 7, 0, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), O.seeded_vector(n, 7))
+    part = torch.empty(100, dtype=torch.float64, device="cuda")
+    assert _lib.load().ktb_seeded_vector(100, 7, 500, part.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(part.cpu().numpy(), O.seeded_vector(600, 7)[500:])
+
+
+# ------------------------------------------------------------ selector
+def test_selector_unsym_and_sym(K):
+    n, rp, ci, v = matgen.random_csr(3000, 0.004, np.random.default_rng(1), skew=True)
+    a = K.CsrMatrix(n, rp, ci, v)
+    choice, rep = K.select_spmv_unsym(a)
+    assert rep.selected >= 0 and rep.selected_candidate().correct
+    assert rep.max_executions() <= 4
+    names = [c.name for c in rep.candidates]
+    assert names[:2] == ["u1", "u2"] and set(names[2:]) == {"u3"}
+    x = O.seeded_vector(n, 1)
+    y = np.empty(n)
+    choice.plan.apply(x, y)
+    assert_close(y, O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x))
+    n, rp, ci, v = matgen.stencil27_upper(16, 16, 16)
+    s = K.SymCsrMatrix(n, rp, ci, v)
+    choice, rep = K.select_spmv_sym(s)
+    assert [c.name for c in rep.candidates] == ["s1", "s2", "s3"]
+    assert all(c.correct for c in rep.candidates)
+
+
+def test_selector_injected_timer_and_tie_break(K):
+    """autotune.hpp:164 injected timer; tie -> lowest ordinal."""
+    n, rp, ci, v = matgen.random_csr(400, 0.03, np.random.default_rng(2))
+    a = K.CsrMatrix(n, rp, ci, v)
+    clock = {"t": 0.0}
+
+    def now():
+        clock["t"] += 1.0  # every trial measures exactly 1 s -> all tie
+        return clock["t"]
+
+    choice, rep = K.select_spmv_unsym(a, opts=K.SelectOptions(now=now))
+    assert rep.selected == 0 and choice.kernel == K.UnsymKernel.u1_row
+    assert all(c.best_seconds == 1.0 for c in rep.candidates if c.correct)
+
+
+# ------------------------------------------------------------ contract
+def test_contract_messages(K):
+    n, rp, ci, v = matgen.random_csr(50, 0.1, np.random.default_rng(4))
+    a = K.CsrMatrix(n, rp, ci, v)
+    part = K.build_row_partition(a, 2, K.PartitionScheme.row_based)
+    with pytest.raises(K.Error, match="dimension mismatch"):
+        K.spmv_unsym(K.UnsymKernel.u1_row, a, part, None, np.ones(n + 1))
+    with pytest.raises(K.Error, match="U1/U2 need a row partition"):
+        K.spmv_unsym(K.UnsymKernel.u1_row, a, None, None, np.ones(n))
+    with pytest.raises(K.Error, match="partition scheme does not match kernel"):
+        K.spmv_unsym(K.UnsymKernel.u2_nnz, a, part, None, np.ones(n))
+    with pytest.raises(K.Error, match="U3/U4 need a bss plan"):
+        K.spmv_unsym(K.UnsymKernel.u3_bss, a, None, None, np.ones(n))
+    n2, rp2, ci2, v2 = matgen.random_csr(51, 0.1, np.random.default_rng(5))
+    b = K.CsrMatrix(n2, rp2, ci2, v2)
+    with pytest.raises(K.Error, match="partition built for a different matrix"):
+        K.spmv_unsym(K.UnsymKernel.u1_row, b, part, None, np.ones(n2))
+    with pytest.raises(K.Error, match="plan built for a different matrix"):
+        K.spmv_unsym(K.UnsymKernel.u3_bss, b, None, K.build_bss_plan(a, 8), np.ones(n2))
+    s = K.SymCsrMatrix(*matgen.random_csr(40, 0.1, np.random.default_rng(6), upper=True))
+    sp = K.build_row_partition(s, 2, K.PartitionScheme.nnz_balanced)
+    with pytest.raises(K.Error, match="S3 needs reduction regions"):
+        K.spmv_sym(K.SymKernel.s3_nnz_zero_omit, s, sp, None, np.ones(40))
+    with pytest.raises(K.Error, match="bss plan: jl must be >= 1"):
+        K.build_bss_plan(a, 0)
+
+
+def test_engine_linop_counts(K):
+    n, rp, ci, v = matgen.stencil7(10, 10, 10)
+    a = K.CsrMatrix(n, rp, ci, v)
+    choice, rep = K.select_spmv_unsym(a)
+    eng = K.UnsymEngine(a, choice)
+    op = eng.op()
+    x = O.seeded_vector(n, 9)
+    y = np.empty(n)
+    for _ in range(3):
+        op.apply(x, y)
+    assert eng.calls() == 3 and eng.kernel_seconds() > 0
+    assert_close(y, O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x))
