@@ -128,6 +128,8 @@ struct SymWindowLayout {
     DBuf<double> spill;
     DBuf<int32_t> head_end;    // per CTA: its head rows [cta_row[c], head_end[c]) get spills
     DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it
+    DBuf<int32_t> long_rows;   // rows handled by the long-row path
+    int64_t nlong = 0;
     DBuf<int32_t> far_i, far_j;
     DBuf<double> far_v;
 };

@@ -141,7 +141,7 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // ================================================================ S3
 constexpr int kS3Threads = 256;  // rows per sub-tile
 constexpr int kS3MaxR = 16;      // rounds held in registers per pass
-constexpr int kS3RoundCap = 256; // max rounds per sub-tile (colour classes)
+constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
 
@@ -240,6 +240,35 @@ __global__ void k_s3_spill_fixup(const int32_t* __restrict__ cta_row,
     }
 }
 
+// Rows too long for the round layout: a block per row, row-direction sum plus
+// transposed products with fp64 L2 atomics (after the main kernel wrote y).
+__global__ void __launch_bounds__(256) k_s3_long(const int32_t* __restrict__ rows,
+                                                 const int32_t* __restrict__ rp,
+                                                 const int32_t* __restrict__ col,
+                                                 const double* __restrict__ val,
+                                                 const double* __restrict__ x,
+                                                 double* __restrict__ y) {
+    const int32_t i = rows[blockIdx.x];
+    const double xi = x[i];
+    double s = 0.0;
+    for (int32_t k = rp[i] + threadIdx.x; k < rp[i + 1]; k += blockDim.x) {
+        const int32_t j = col[k];
+        const double v = val[k];
+        s += v * x[j];
+        if (j != i) atomicAdd(y + j, v * xi);
+    }
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        atomicAdd(y + i, t);
+    }
+}
+
 __global__ void k_s3_far(const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
                          const double* __restrict__ fv, int64_t count,
                          const double* __restrict__ x, double* __restrict__ y) {
@@ -288,8 +317,11 @@ void s3_setup(ktb_plan* p) {
     std::vector<double> sval;
     std::vector<int32_t> spill_hi(P), far_i, far_j;
     std::vector<double> far_v;
-    std::vector<uint64_t> colmask(static_cast<size_t>(W) * (kS3RoundCap / 64), 0);
-    std::vector<int32_t> touched;
+    std::vector<uint64_t> colmask(static_cast<size_t>(W), 0);
+    std::vector<int32_t> touched, long_rows;
+    // rows longer than this go to the long-row path (their own block, atomics)
+    const double mean = n ? double(nnz) / double(n) : 1.0;
+    const int64_t long_len = std::max<int64_t>(32, std::min<int64_t>(kS3RoundCap, 4 * mean + 8));
     int64_t total_slots = 0;
     for (int c = 0; c < P; ++c) {
         const int32_t R0 = bnd[c], R1 = bnd[c + 1];
@@ -298,32 +330,34 @@ void s3_setup(ktb_plan* p) {
         for (int32_t a = R0; a < R1; a += S) {
             const int32_t rows = std::min<int32_t>(S, R1 - a);
             // greedy colouring: entry -> lowest round free in its row and in
-            // its target slot
+            // its target slot; a congested slot turns the entry "far"
             std::vector<std::vector<std::pair<int, int64_t>>> assign(rows);  // (round, k)
             int R = 0;
             touched.clear();
             for (int32_t t = 0; t < rows; ++t) {
                 const int32_t i = a + t;
-                uint64_t rowmask[kS3RoundCap / 64] = {0, 0, 0, 0};
+                if (rp[i + 1] - rp[i] > long_len) {
+                    long_rows.push_back(i);
+                    continue;
+                }
+                uint64_t rowmask = 0;
                 for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
                     const int32_t j = col[k];
                     const bool scatter = j != i;
-                    const bool far = scatter && (static_cast<int64_t>(j) - a >= W);
-                    uint64_t* cm = nullptr;
-                    if (scatter && !far) {
-                        const size_t slot = static_cast<size_t>(j - a);
-                        cm = &colmask[slot * (kS3RoundCap / 64)];
+                    bool far = scatter && (static_cast<int64_t>(j) - a >= W);
+                    uint64_t* cm = (scatter && !far) ? &colmask[static_cast<size_t>(j - a)]
+                                                     : nullptr;
+                    uint64_t busy = rowmask | (cm ? *cm : 0);
+                    if (!~busy) {  // slot congested: scatter through the far path
+                        far = true;
+                        cm = nullptr;
+                        busy = rowmask;
                     }
-                    int r = -1;
-                    for (int w = 0; w < kS3RoundCap / 64 && r < 0; ++w) {
-                        const uint64_t busy = rowmask[w] | (cm ? cm[w] : 0);
-                        if (~busy) r = w * 64 + __builtin_ctzll(~busy);
-                    }
-                    require(r >= 0, "s3: row too long for the window layout");
-                    rowmask[r >> 6] |= 1ull << (r & 63);
+                    const int r = __builtin_ctzll(~busy);
+                    rowmask |= 1ull << r;
                     if (cm) {
-                        if (!(cm[0] | cm[1] | cm[2] | cm[3])) touched.push_back(j - a);
-                        cm[r >> 6] |= 1ull << (r & 63);
+                        if (!*cm) touched.push_back(j - a);
+                        *cm |= 1ull << r;
                         hi = std::max<int32_t>(hi, j + 1);
                     }
                     if (far) {
@@ -331,24 +365,22 @@ void s3_setup(ktb_plan* p) {
                         far_j.push_back(j);
                         far_v.push_back(val[k]);
                     }
-                    assign[t].push_back({r, k});
+                    assign[t].push_back({r | (far ? 0x10000 : 0), k});
                     R = std::max(R, r + 1);
                 }
             }
-            for (int32_t sl : touched)
-                std::memset(&colmask[static_cast<size_t>(sl) * (kS3RoundCap / 64)], 0,
-                            sizeof(uint64_t) * (kS3RoundCap / 64));
-            R = std::max(R, 0);
+            for (int32_t sl : touched) colmask[static_cast<size_t>(sl)] = 0;
             const int64_t basei = static_cast<int64_t>(scol.size());
             sub_base.push_back(basei);
             sub_rounds.push_back(R);
             scol.resize(basei + static_cast<int64_t>(R) * S, -1);
             sval.resize(basei + static_cast<int64_t>(R) * S, 0.0);
             for (int32_t t = 0; t < rows; ++t)
-                for (auto [r, k] : assign[t]) {
+                for (auto [rr, k] : assign[t]) {
+                    const int r = rr & 0xffff;
+                    const bool far = rr & 0x10000;
                     const int64_t e = basei + static_cast<int64_t>(r) * S + t;
                     const int32_t j = col[k];
-                    const bool far = j != a + t && (static_cast<int64_t>(j) - a >= W);
                     scol[e] = far ? static_cast<int32_t>(static_cast<uint32_t>(j) | 0x80000000u)
                                   : j;
                     sval[e] = val[k];
@@ -407,6 +439,8 @@ void s3_setup(ktb_plan* p) {
     L.spill.alloc(std::max<int64_t>(so, 1));
     up32(L.head_end, head_end);
     up32(L.first_src, first_src);
+    up32(L.long_rows, long_rows);
+    L.nlong = static_cast<int64_t>(long_rows.size());
     up32(L.far_i, far_i);
     up32(L.far_j, far_j);
     upd(L.far_v, far_v);
@@ -414,7 +448,7 @@ void s3_setup(ktb_plan* p) {
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(W * 8)));
     p->ctas = P;
-    p->launches = 2 + (L.far ? 1 : 0);
+    p->launches = 2 + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
     p->extra_bytes = (total_slots - nnz) * 12 + so * 8 * 2 + so * 8 * 2;
 }
@@ -428,6 +462,12 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
     k_s3_spill_fixup<<<L.ctas, 256, 0, p->stream>>>(L.cta_row.p, L.head_end.p, L.first_src.p,
                                                      L.spill_hi.p, L.spill_off.p, L.spill.p, y);
     KTB_LAUNCH();
+    if (L.nlong) {
+        const ktb_matrix* m = p->m;
+        k_s3_long<<<static_cast<int>(L.nlong), 256, 0, p->stream>>>(
+            L.long_rows.p, m->row_ptr.p, m->col.p, m->val.p, x, y);
+        KTB_LAUNCH();
+    }
     if (L.far) {
         k_s3_far<<<ceil_div(L.far, 256), 256, 0, p->stream>>>(L.far_i.p, L.far_j.p, L.far_v.p,
                                                                L.far, x, y);
