@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "ktb_internal.cuh"
+#include "ktb_ptx.cuh"
 
 namespace ktb {
 
@@ -139,76 +140,174 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 }
 
 // ================================================================ S3
-constexpr int kS3Threads = 256;  // rows per sub-tile
-constexpr int kS3MaxR = 16;      // rounds held in registers per pass
+// Warp-specialised, TMA-pipelined round kernel. One CTA per SM:
+//   warp 8       producer: one elected lane streams the CTA's SELL chunks
+//                (<= kChunkR rounds x 256 rows of cols + vals, contiguous) into
+//                a kStages-deep shared-memory ring with cp.async.bulk, L2
+//                evict_first, completion on mbarriers;
+//   warps 0..7   consumers, one row each: gather x for the NEXT chunk while
+//                running the rounds of the current one; each round is a
+//                plain ld/add/st on the window ring followed by a named
+//                barrier (the plan guarantees distinct targets per round).
+constexpr int kS3Threads = 256;  // consumer threads = rows per sub-tile
+constexpr int kChunkR = 8;       // rounds per pipeline chunk
+constexpr int kStages = 3;
+constexpr int kStageCols = kChunkR * kS3Threads;                 // ints
+constexpr int kStageBytes = kChunkR * kS3Threads * (4 + 8);      // 24576
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
+constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 128;
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
 
-__global__ void __launch_bounds__(kS3Threads, 1)
+__global__ void __launch_bounds__(kS3Threads + 32, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_sub,
          const int64_t* __restrict__ sub_base, const int32_t* __restrict__ sub_rounds,
          const int32_t* __restrict__ scol, const double* __restrict__ sval,
          const double* __restrict__ x, double* __restrict__ y, int W,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
-    extern __shared__ double win[];
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto s_col = [&](int st) { return reinterpret_cast<int32_t*>(smem + st * kStageBytes); };
+    auto s_val = [&](int st) {
+        return reinterpret_cast<double*>(smem + st * kStageBytes + kStageCols * 4);
+    };
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
+
     const int tid = threadIdx.x;
     const int c = blockIdx.x;
     const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
-    for (int i = tid; i < W; i += kS3Threads) win[i] = 0.0;
-    __syncthreads();
     const int s_begin = cta_sub[c], s_end = cta_sub[c + 1];
-    int off = 0;  // ring slot of row a (a - R0 mod W)
-    for (int s = s_begin; s < s_end; ++s) {
-        const int32_t a = R0 + (s - s_begin) * kS3Threads;
-        const int32_t i = a + tid;
-        const bool valid = i < R1;
-        const int R = sub_rounds[s];
-        const int64_t base = sub_base[s] + tid;
-        const double xi = valid ? __ldg(x + i) : 0.0;
-        double rowsum = 0.0;
-        for (int r0 = 0; r0 < R; r0 += kS3MaxR) {
-            int32_t cc[kS3MaxR];
-            double vv[kS3MaxR];
-            double xx[kS3MaxR];
-#pragma unroll
-            for (int u = 0; u < kS3MaxR; ++u) {
-                cc[u] = -1;
-                vv[u] = 0.0;
-                if (r0 + u < R) {
-                    const int64_t e = base + static_cast<int64_t>(r0 + u) * kS3Threads;
-                    cc[u] = ld_stream_i32s(scol + e);
-                    vv[u] = ld_stream_f64s(sval + e);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kS3MaxR; ++u) {
-                xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < kS3MaxR; ++u) rowsum += vv[u] * xx[u];
-#pragma unroll
-            for (int u = 0; u < kS3MaxR; ++u) {
-                if (r0 + u < R) {  // uniform over the CTA
-                    const int32_t j = cc[u];
-                    if (j >= 0 && j != i) {
-                        const int slot = wrap(j - a + off, W);
-                        win[slot] += vv[u] * xi;
-                    }
-                    __syncthreads();
-                }
-            }
+    if (tid == 0) {
+        for (int st = 0; st < kStages; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
         }
-        if (valid) {
-            const int slot = wrap(tid + off, W);
-            y[i] = rowsum + win[slot];
-            win[slot] = 0.0;
-        }
-        __syncthreads();
-        off = wrap(off + kS3Threads, W);
+        fence_mbar_init();
     }
-    // spill: the region beyond the block, [R1, spill_hi), in ring order
+    for (int k = tid; k < W; k += blockDim.x) win[k] = 0.0;
+    __syncthreads();
+
+    if (tid >= kS3Threads) {  // ---------------- producer warp
+        if (tid == kS3Threads) {
+            const uint64_t pol = policy_evict_first();
+            int q = 0;
+            for (int s = s_begin; s < s_end; ++s) {
+                const int R = sub_rounds[s];
+                const int64_t base = sub_base[s];
+                for (int r0 = 0; r0 < R; r0 += kChunkR, ++q) {
+                    const int nr = min(kChunkR, R - r0);
+                    const int st = q % kStages;
+                    if (q >= kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
+                    const uint32_t bc = nr * kS3Threads * 4, bv = nr * kS3Threads * 8;
+                    mbar_arrive_expect_tx(&full[st], bc + bv);
+                    tma_load_1d(s_col(st), scol + base + int64_t(r0) * kS3Threads, bc, &full[st],
+                                pol);
+                    tma_load_1d(s_val(st), sval + base + int64_t(r0) * kS3Threads, bv, &full[st],
+                                pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------- consumers
+    if (s_begin == s_end) return;
+    int s = s_begin, r0 = 0, R = sub_rounds[s], q = 0;
+    int32_t a = R0;
+    int32_t i = a + tid;
+    bool valid = i < R1;
+    double xi = valid ? __ldg(x + i) : 0.0;
+    int off = 0;
+    double rowsum = 0.0;
+    int32_t cc[kChunkR];
+    double xx[kChunkR];
+    {
+        mbar_wait(&full[0], 0);
+        const int nr = min(kChunkR, R);
+#pragma unroll
+        for (int u = 0; u < kChunkR; ++u) cc[u] = u < nr ? s_col(0)[u * kS3Threads + tid] : -1;
+#pragma unroll
+        for (int u = 0; u < kChunkR; ++u)
+            xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
+    }
+    double xi_next = 0.0;
+    while (true) {
+        // next chunk coordinates and its gathers (overlap the rounds below)
+        int s2 = s, r02 = r0 + kChunkR;
+        if (r02 >= R) {
+            s2 = s + 1;
+            r02 = 0;
+        }
+        const bool has_next = s2 < s_end;
+        int R2 = R;
+        int32_t cn[kChunkR];
+        double xn[kChunkR];
+#pragma unroll
+        for (int u = 0; u < kChunkR; ++u) {
+            cn[u] = -1;
+            xn[u] = 0.0;
+        }
+        if (has_next) {
+            if (s2 != s) {
+                R2 = sub_rounds[s2];
+                const int32_t i2 = R0 + (s2 - s_begin) * kS3Threads + tid;
+                xi_next = i2 < R1 ? __ldg(x + i2) : 0.0;
+            }
+            const int st2 = (q + 1) % kStages;
+            mbar_wait(&full[st2], ((q + 1) / kStages) & 1);
+            const int nr2 = min(kChunkR, R2 - r02);
+#pragma unroll
+            for (int u = 0; u < kChunkR; ++u)
+                cn[u] = u < nr2 ? s_col(st2)[u * kS3Threads + tid] : -1;
+#pragma unroll
+            for (int u = 0; u < kChunkR; ++u)
+                xn[u] = cn[u] != -1 ? __ldg(x + (cn[u] & 0x7fffffff)) : 0.0;
+        }
+        // rounds of the current chunk
+        const int st = q % kStages;
+        const int nr = min(kChunkR, R - r0);
+#pragma unroll
+        for (int u = 0; u < kChunkR; ++u) {
+            if (u < nr) {  // uniform over the consumers
+                const double v = s_val(st)[u * kS3Threads + tid];
+                rowsum += v * xx[u];
+                const int32_t j = cc[u];
+                if (j >= 0 && j != i) {
+                    const int slot = wrap(j - a + off, W);
+                    win[slot] += v * xi;
+                }
+                named_bar_sync(1, kS3Threads);
+            }
+        }
+        if (tid == 0) mbar_arrive(&empty[st]);  // every consumer is past its reads
+        if (r0 + kChunkR >= R) {  // sub-tile complete: finalise its rows
+            if (valid) {
+                const int slot = wrap(tid + off, W);
+                y[i] = rowsum + win[slot];
+                win[slot] = 0.0;
+            }
+            named_bar_sync(1, kS3Threads);
+            off = wrap(off + kS3Threads, W);
+            rowsum = 0.0;
+            a += kS3Threads;
+            i = a + tid;
+            valid = i < R1;
+            xi = xi_next;
+        }
+        if (!has_next) break;
+        ++q;
+        s = s2;
+        r0 = r02;
+        R = R2;
+#pragma unroll
+        for (int u = 0; u < kChunkR; ++u) {
+            cc[u] = cn[u];
+            xx[u] = xn[u];
+        }
+    }
+    // spill: the region beyond the block, [R1, spill_hi)
     const int32_t hi = spill_hi[c];
     if (hi > R1) {
         const int64_t so = spill_off[c];
@@ -217,27 +316,47 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     }
 }
 
-// Head rows of CTA d receive the spills of earlier CTAs, added in ascending
-// source order (deterministic).
-__global__ void k_s3_spill_fixup(const int32_t* __restrict__ cta_row,
-                                 const int32_t* __restrict__ head_end,
-                                 const int32_t* __restrict__ first_src,
-                                 const int32_t* __restrict__ spill_hi,
-                                 const int64_t* __restrict__ spill_off,
-                                 const double* __restrict__ spill, double* __restrict__ y) {
-    const int d = blockIdx.x;
-    const int32_t r0 = cta_row[d], he = head_end[d], c0 = first_src[d];
-    for (int32_t j = r0 + threadIdx.x; j < he; j += blockDim.x) {
-        double s = 0.0;
-        bool any = false;
-        for (int c = c0; c < d; ++c) {
-            if (j < spill_hi[c] && j >= cta_row[c + 1]) {
-                s += spill[spill_off[c] + (j - cta_row[c + 1])];
-                any = true;
-            }
+// Head rows of CTA d receive the spills of earlier CTAs, summed in ascending
+// source order and added once (deterministic). One thread per head row.
+__global__ void __launch_bounds__(256) k_s3_spill_fixup(
+    int P, const int64_t* __restrict__ head_prefix, const int32_t* __restrict__ cta_row,
+    const int32_t* __restrict__ first_src, const int32_t* __restrict__ spill_hi,
+    const int64_t* __restrict__ spill_off, const double* __restrict__ spill,
+    double* __restrict__ y) {
+    extern __shared__ int64_t fx[];
+    int64_t* s_pref = fx;                 // P+1
+    int64_t* s_off = fx + (P + 1);        // P
+    int32_t* s_row = reinterpret_cast<int32_t*>(fx + 2 * P + 1);  // P+1
+    int32_t* s_first = s_row + (P + 1);   // P
+    int32_t* s_hi = s_first + P;          // P
+    for (int k = threadIdx.x; k <= P; k += blockDim.x) {
+        s_pref[k] = head_prefix[k];
+        s_row[k] = cta_row[k];
+        if (k < P) {
+            s_off[k] = spill_off[k];
+            s_first[k] = first_src[k];
+            s_hi[k] = spill_hi[k];
         }
-        if (any) y[j] += s;
     }
+    __syncthreads();
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= s_pref[P]) return;
+    int lo = 0, hi = P;  // last d with pref[d] <= t
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pref[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int d = lo;
+    const int32_t j = s_row[d] + static_cast<int32_t>(t - s_pref[d]);
+    double acc = 0.0;
+    bool any = false;
+    for (int c = s_first[d]; c < d; ++c) {
+        if (j < s_hi[c] && j >= s_row[c + 1]) {
+            acc += spill[s_off[c] + (j - s_row[c + 1])];
+            any = true;
+        }
+    }
+    if (any) y[j] += acc;
 }
 
 // Rows too long for the round layout: a block per row, row-direction sum plus
@@ -303,7 +422,7 @@ void s3_setup(ktb_plan* p) {
     int max_smem = 0;
     KTB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                     m->device));
-    const int64_t cap = std::max<int64_t>(S + 32, (max_smem - 1024) / 8);
+    const int64_t cap = std::max<int64_t>(S + 32, (max_smem - kS3SmemFixed) / 8);
     int64_t reach = 0;
     for (int64_t i = 0; i < n; ++i)
         if (rp[i + 1] > rp[i]) reach = std::max<int64_t>(reach, col[rp[i + 1] - 1] - i);
@@ -370,6 +489,7 @@ void s3_setup(ktb_plan* p) {
                 }
             }
             for (int32_t sl : touched) colmask[static_cast<size_t>(sl)] = 0;
+            R = std::max(R, 1);  // every sub-tile is one pipeline item at least
             const int64_t basei = static_cast<int64_t>(scol.size());
             sub_base.push_back(basei);
             sub_rounds.push_back(R);
@@ -413,6 +533,9 @@ void s3_setup(ktb_plan* p) {
         head_end[d] = he;
         first_src[d] = fs;
     }
+    std::vector<int64_t> head_prefix(P + 1, 0);
+    for (int d = 0; d < P; ++d) head_prefix[d + 1] = head_prefix[d] + (head_end[d] - bnd[d]);
+    L.head_total = head_prefix[P];
 
     auto up32 = [&](DBuf<int32_t>& d, const std::vector<int32_t>& h) {
         d.alloc(std::max<size_t>(h.size(), 1));
@@ -438,6 +561,7 @@ void s3_setup(ktb_plan* p) {
     up64(L.spill_off, spill_off);
     L.spill.alloc(std::max<int64_t>(so, 1));
     up32(L.head_end, head_end);
+    up64(L.head_prefix, head_prefix);
     up32(L.first_src, first_src);
     up32(L.long_rows, long_rows);
     L.nlong = static_cast<int64_t>(long_rows.size());
@@ -446,7 +570,7 @@ void s3_setup(ktb_plan* p) {
     upd(L.far_v, far_v);
     KTB_CUDA(cudaStreamSynchronize(st));
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(W * 8)));
+                                  static_cast<int>(kS3SmemFixed + W * 8)));
     p->ctas = P;
     p->launches = 2 + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
@@ -455,13 +579,19 @@ void s3_setup(ktb_plan* p) {
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
-    k_s3<<<L.ctas, kS3Threads, static_cast<size_t>(L.window) * 8, p->stream>>>(
+    k_s3<<<L.ctas, kS3Threads + 32, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
+           p->stream>>>(
         L.cta_row.p, L.cta_sub.p, L.sub_base.p, L.sub_rounds.p, L.sell_col.p, L.sell_val.p, x, y,
         L.window, L.spill_hi.p, L.spill_off.p, L.spill.p);
     KTB_LAUNCH();
-    k_s3_spill_fixup<<<L.ctas, 256, 0, p->stream>>>(L.cta_row.p, L.head_end.p, L.first_src.p,
-                                                     L.spill_hi.p, L.spill_off.p, L.spill.p, y);
-    KTB_LAUNCH();
+    if (L.head_total > 0) {
+        const int P = L.ctas;
+        const size_t sm = (2 * P + 1) * 8 + (3 * P + 1) * 4;
+        k_s3_spill_fixup<<<ceil_div(L.head_total, 256), 256, sm, p->stream>>>(
+            P, L.head_prefix.p, L.cta_row.p, L.first_src.p, L.spill_hi.p, L.spill_off.p,
+            L.spill.p, y);
+        KTB_LAUNCH();
+    }
     if (L.nlong) {
         const ktb_matrix* m = p->m;
         k_s3_long<<<static_cast<int>(L.nlong), 256, 0, p->stream>>>(

@@ -331,6 +331,7 @@ class DevicePlan:
 
     def set_stream(self, stream) -> None:
         _check(_lib.load().ktb_plan_set_stream(self.h, stream))
+        self._stream = stream
 
     def apply(self, x, y) -> None:
         """y = A x. numpy arrays -> host-span mode (copies, synchronous);
@@ -340,12 +341,26 @@ class DevicePlan:
                     and y.flags.c_contiguous, "spmv: dimension mismatch")
             _check(_lib.load().ktb_spmv(self.h, x.ctypes.data, y.ctypes.data, 0))
         else:
+            self._follow_torch_stream(x)
             _check(_lib.load().ktb_spmv(self.h, _dptr(x), _dptr(y), 1))
 
+    def _follow_torch_stream(self, t) -> None:
+        """Device mode runs on the caller's current torch stream so it is
+        ordered with the producer of x and the consumer of y."""
+        if hasattr(t, "data_ptr"):
+            import torch
+
+            s = torch.cuda.current_stream(t.device).cuda_stream
+            if s != getattr(self, "_stream", None):
+                self.set_stream(s)
+                self._stream = s
+
     def apply_rows(self, r0, r1, x, y) -> None:
+        self._follow_torch_stream(x)
         _check(_lib.load().ktb_spmv_rows(self.h, r0, r1, _dptr(x), _dptr(y)))
 
     def time(self, x, y, reps=20, flush_bytes=0):
+        self._follow_torch_stream(x)
         avg, mn = C.c_double(), C.c_double()
         _check(_lib.load().ktb_time_spmv(self.h, _dptr(x), _dptr(y), reps, flush_bytes,
                                          C.byref(avg), C.byref(mn)))
