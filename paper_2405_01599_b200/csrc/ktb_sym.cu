@@ -163,9 +163,10 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_sub,
          const int64_t* __restrict__ sub_base, const int32_t* __restrict__ sub_rounds,
          const int32_t* __restrict__ scol, const double* __restrict__ sval,
-         const double* __restrict__ x, double* __restrict__ y, int W,
+         const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
-         double* __restrict__ spill) {
+         double* __restrict__ spill, const int32_t* __restrict__ head_end,
+         const int32_t* __restrict__ first_src, int* __restrict__ flags, int epoch) {
     extern __shared__ __align__(128) unsigned char smem[];
     auto s_col = [&](int st) { return reinterpret_cast<int32_t*>(smem + st * kStageBytes); };
     auto s_val = [&](int st) {
@@ -192,10 +193,28 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     if (tid >= kS3Threads) {  // ---------------- producer warp
         if (tid == kS3Threads) {
             const uint64_t pol = policy_evict_first();
+            // x is touched first by the far reach of the window: pull the
+            // initial window and then each sub-tile's new front into L2 ahead
+            // of the consumers' gathers (L2 was cold: the bench flushes it).
+            constexpr int kAhead = 4;  // sub-tiles of look-ahead
+            auto pf = [&](int64_t lo, int64_t hi) {
+                lo = max(lo & ~int64_t(1), int64_t(0));
+                hi = min(hi, int64_t(n));
+                if (hi > lo) {
+                    const int64_t cnt = ((hi - lo) + 1) & ~int64_t(1);
+                    prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
+                }
+            };
+            pf(R0, int64_t(R0) + kS3Threads * (kAhead + 1) + reach);
             int q = 0;
             for (int s = s_begin; s < s_end; ++s) {
                 const int R = sub_rounds[s];
                 const int64_t base = sub_base[s];
+                {
+                    const int64_t front = int64_t(R0) + int64_t(s - s_begin + kAhead + 1) *
+                                                            kS3Threads + reach;
+                    pf(front, front + kS3Threads);
+                }
                 for (int r0 = 0; r0 < R; r0 += kChunkR, ++q) {
                     const int nr = min(kChunkR, R - r0);
                     const int st = q % kStages;
@@ -213,7 +232,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     }
 
     // ---------------------------------------------------- consumers
-    if (s_begin == s_end) return;
+    if (s_begin < s_end) {
     int s = s_begin, r0 = 0, R = sub_rounds[s], q = 0;
     int32_t a = R0;
     int32_t i = a + tid;
@@ -307,56 +326,45 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
             xx[u] = xn[u];
         }
     }
-    // spill: the region beyond the block, [R1, spill_hi)
+    }  // s_begin < s_end
+    // spill: the region beyond the block, [R1, spill_hi), published with a
+    // release flag tagged by the launch epoch
     const int32_t hi = spill_hi[c];
     if (hi > R1) {
         const int64_t so = spill_off[c];
         for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
             spill[so + (j - R1)] = win[(j - R0) % W];
     }
-}
-
-// Head rows of CTA d receive the spills of earlier CTAs, summed in ascending
-// source order and added once (deterministic). One thread per head row.
-__global__ void __launch_bounds__(256) k_s3_spill_fixup(
-    int P, const int64_t* __restrict__ head_prefix, const int32_t* __restrict__ cta_row,
-    const int32_t* __restrict__ first_src, const int32_t* __restrict__ spill_hi,
-    const int64_t* __restrict__ spill_off, const double* __restrict__ spill,
-    double* __restrict__ y) {
-    extern __shared__ int64_t fx[];
-    int64_t* s_pref = fx;                 // P+1
-    int64_t* s_off = fx + (P + 1);        // P
-    int32_t* s_row = reinterpret_cast<int32_t*>(fx + 2 * P + 1);  // P+1
-    int32_t* s_first = s_row + (P + 1);   // P
-    int32_t* s_hi = s_first + P;          // P
-    for (int k = threadIdx.x; k <= P; k += blockDim.x) {
-        s_pref[k] = head_prefix[k];
-        s_row[k] = cta_row[k];
-        if (k < P) {
-            s_off[k] = spill_off[k];
-            s_first[k] = first_src[k];
-            s_hi[k] = spill_hi[k];
+    named_bar_sync(1, kS3Threads);
+    if (tid == 0) {
+        __threadfence();
+        st_release_gpu(flags + c, epoch);
+    }
+    // ordered merge of the earlier blocks' spills into this block's head rows
+    // (ascending source block: deterministic). All blocks are co-resident
+    // (cooperative launch) and only wait on lower-numbered blocks.
+    const int32_t he = head_end[c];
+    if (he > R0) {
+        const int c0 = first_src[c];
+        if (tid == 0) {
+            for (int src = c0; src < c; ++src)
+                while (ld_acquire_gpu(flags + src) != epoch) __nanosleep(64);
+            __threadfence();
+        }
+        named_bar_sync(1, kS3Threads);
+        for (int32_t j = R0 + tid; j < he; j += kS3Threads) {
+            double acc = 0.0;
+            bool any = false;
+            for (int src = c0; src < c; ++src) {
+                const int32_t s0 = cta_row[src + 1];
+                if (j >= s0 && j < spill_hi[src]) {
+                    acc += __ldcg(spill + spill_off[src] + (j - s0));
+                    any = true;
+                }
+            }
+            if (any) y[j] += acc;
         }
     }
-    __syncthreads();
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t >= s_pref[P]) return;
-    int lo = 0, hi = P;  // last d with pref[d] <= t
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_pref[mid] <= t) lo = mid; else hi = mid;
-    }
-    const int d = lo;
-    const int32_t j = s_row[d] + static_cast<int32_t>(t - s_pref[d]);
-    double acc = 0.0;
-    bool any = false;
-    for (int c = s_first[d]; c < d; ++c) {
-        if (j < s_hi[c] && j >= s_row[c + 1]) {
-            acc += spill[s_off[c] + (j - s_row[c + 1])];
-            any = true;
-        }
-    }
-    if (any) y[j] += acc;
 }
 
 // Rows too long for the round layout: a block per row, row-direction sum plus
@@ -429,6 +437,7 @@ void s3_setup(ktb_plan* p) {
     int64_t W = std::min<int64_t>(cap, ((S + reach + 1 + 31) / 32) * 32);
     W = std::max<int64_t>(W, S + 32);
     L.window = static_cast<int>(W);
+    L.reach = static_cast<int>(std::min<int64_t>(reach, W));
 
     std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
     std::vector<int64_t> sub_base;
@@ -562,6 +571,9 @@ void s3_setup(ktb_plan* p) {
     L.spill.alloc(std::max<int64_t>(so, 1));
     up32(L.head_end, head_end);
     up64(L.head_prefix, head_prefix);
+    L.flags.alloc(P);
+    KTB_CUDA(cudaMemsetAsync(L.flags.p, 0, sizeof(int) * P, st));
+    L.epoch = 0;
     up32(L.first_src, first_src);
     up32(L.long_rows, long_rows);
     L.nlong = static_cast<int64_t>(long_rows.size());
@@ -572,26 +584,30 @@ void s3_setup(ktb_plan* p) {
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kS3SmemFixed + W * 8)));
     p->ctas = P;
-    p->launches = 2 + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
+    p->launches = 1 + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
     p->extra_bytes = (total_slots - nnz) * 12 + so * 8 * 2 + so * 8 * 2;
 }
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
-    k_s3<<<L.ctas, kS3Threads + 32, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
-           p->stream>>>(
-        L.cta_row.p, L.cta_sub.p, L.sub_base.p, L.sub_rounds.p, L.sell_col.p, L.sell_val.p, x, y,
-        L.window, L.spill_hi.p, L.spill_off.p, L.spill.p);
-    KTB_LAUNCH();
-    if (L.head_total > 0) {
-        const int P = L.ctas;
-        const size_t sm = (2 * P + 1) * 8 + (3 * P + 1) * 4;
-        k_s3_spill_fixup<<<ceil_div(L.head_total, 256), 256, sm, p->stream>>>(
-            P, L.head_prefix.p, L.cta_row.p, L.first_src.p, L.spill_hi.p, L.spill_off.p,
-            L.spill.p, y);
-        KTB_LAUNCH();
-    }
+    const int epoch = ++L.epoch;
+    int W = L.window, reach = L.reach, n = static_cast<int>(p->m->n);
+    const int32_t *cr = L.cta_row.p, *cs = L.cta_sub.p, *sr = L.sub_rounds.p, *sc = L.sell_col.p;
+    const int64_t* sb = L.sub_base.p;
+    const double* sv = L.sell_val.p;
+    const int32_t *sh = L.spill_hi.p, *he = L.head_end.p, *fs = L.first_src.p;
+    const int64_t* so = L.spill_off.p;
+    double* sp = L.spill.p;
+    int* fl = L.flags.p;
+    int ep = epoch;
+    void* args[] = {&cr, &cs, &sb, &sr, &sc, &sv, &x, &y, &W, &reach, &n,
+                    &sh, &so, &sp, &he, &fs, &fl, &ep};
+    KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_s3), dim3(L.ctas),
+                                         dim3(kS3Threads + 32), args,
+                                         kS3SmemFixed + static_cast<size_t>(L.window) * 8,
+                                         p->stream));
+
     if (L.nlong) {
         const ktb_matrix* m = p->m;
         k_s3_long<<<static_cast<int>(L.nlong), 256, 0, p->stream>>>(
