@@ -127,10 +127,8 @@ struct SymWindowLayout {
     DBuf<int64_t> spill_off;   // per CTA: offset into spill
     DBuf<double> spill;
     DBuf<int32_t> head_end;    // per CTA: its head rows [cta_row[c], head_end[c]) get spills
-    DBuf<int64_t> head_prefix; // exclusive prefix of head lengths (P+1)
-    int64_t head_total = 0;
-    DBuf<int> flags;           // per CTA spill-ready flag (= launch epoch)
-    int epoch = 0;
+    DBuf<int32_t> segs;        // fixup segments (d, j0, j1, 0)
+    int64_t nsegs = 0;
     int reach = 0;             // max(col - row), clipped to the window
     DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it
     DBuf<int32_t> long_rows;   // rows handled by the long-row path

@@ -143,21 +143,40 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // Warp-specialised, TMA-pipelined round kernel. One CTA per SM:
 //   warp 8       producer: one elected lane streams the CTA's SELL chunks
 //                (<= kChunkR rounds x 256 rows of cols + vals, contiguous) into
-//                a kStages-deep shared-memory ring with cp.async.bulk, L2
-//                evict_first, completion on mbarriers;
-//   warps 0..7   consumers, one row each: gather x for the NEXT chunk while
-//                running the rounds of the current one; each round is a
-//                plain ld/add/st on the window ring followed by a named
-//                barrier (the plan guarantees distinct targets per round).
+//                a kStages-deep shared-memory ring with cp.async.bulk (L2
+//                evict_first, completion on mbarriers) and bulk-prefetches the
+//                advancing front of x into L2;
+//   warps 0..7   consumers, one row each: gather x for chunk q+2 while running
+//                the rounds of chunk q; each round is a plain ld/add/st on the
+//                window ring followed by a named barrier (the plan guarantees
+//                distinct targets per round).
+// The part of each block's region beyond the block (the spill) goes to a
+// global buffer; k_s3_fixup adds it into the next blocks' head rows in
+// ascending source order, so the result is deterministic.
 constexpr int kS3Threads = 256;  // consumer threads = rows per sub-tile
-constexpr int kChunkR = 8;       // rounds per pipeline chunk
-constexpr int kStages = 3;
+constexpr int kChunkR = 4;       // rounds per pipeline chunk
+constexpr int kStages = 6;
 constexpr int kStageCols = kChunkR * kS3Threads;                 // ints
-constexpr int kStageBytes = kChunkR * kS3Threads * (4 + 8);      // 24576
+constexpr int kStageBytes = kChunkR * kS3Threads * (4 + 8);      // 12288
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 128;
+constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
+
+struct ChunkIt {
+    int s, r0, R;
+};
+
+__device__ __forceinline__ void chunk_advance(ChunkIt& m, int s_end,
+                                              const int32_t* __restrict__ sub_rounds) {
+    m.r0 += kChunkR;
+    if (m.r0 >= m.R) {
+        ++m.s;
+        m.r0 = 0;
+        m.R = m.s < s_end ? sub_rounds[m.s] : 0;
+    }
+}
 
 __global__ void __launch_bounds__(kS3Threads + 32, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_sub,
@@ -165,8 +184,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
          const int32_t* __restrict__ scol, const double* __restrict__ sval,
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
-         double* __restrict__ spill, const int32_t* __restrict__ head_end,
-         const int32_t* __restrict__ first_src, int* __restrict__ flags, int epoch) {
+         double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
     auto s_col = [&](int st) { return reinterpret_cast<int32_t*>(smem + st * kStageBytes); };
     auto s_val = [&](int st) {
@@ -195,7 +213,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
             const uint64_t pol = policy_evict_first();
             // x is touched first by the far reach of the window: pull the
             // initial window and then each sub-tile's new front into L2 ahead
-            // of the consumers' gathers (L2 was cold: the bench flushes it).
+            // of the consumers' gathers (the bench flushes L2 between steps).
             constexpr int kAhead = 4;  // sub-tiles of look-ahead
             auto pf = [&](int64_t lo, int64_t hi) {
                 lo = max(lo & ~int64_t(1), int64_t(0));
@@ -205,16 +223,14 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                     prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
                 }
             };
-            pf(R0, int64_t(R0) + kS3Threads * (kAhead + 1) + reach);
+            if (s_begin < s_end) pf(R0, int64_t(R0) + kS3Threads * (kAhead + 1) + reach);
             int q = 0;
             for (int s = s_begin; s < s_end; ++s) {
                 const int R = sub_rounds[s];
                 const int64_t base = sub_base[s];
-                {
-                    const int64_t front = int64_t(R0) + int64_t(s - s_begin + kAhead + 1) *
-                                                            kS3Threads + reach;
-                    pf(front, front + kS3Threads);
-                }
+                const int64_t front =
+                    int64_t(R0) + int64_t(s - s_begin + kAhead + 1) * kS3Threads + reach;
+                pf(front, front + kS3Threads);
                 for (int r0 = 0; r0 < R; r0 += kChunkR, ++q) {
                     const int nr = min(kChunkR, R - r0);
                     const int st = q % kStages;
@@ -233,137 +249,132 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 
     // ---------------------------------------------------- consumers
     if (s_begin < s_end) {
-    int s = s_begin, r0 = 0, R = sub_rounds[s], q = 0;
-    int32_t a = R0;
-    int32_t i = a + tid;
-    bool valid = i < R1;
-    double xi = valid ? __ldg(x + i) : 0.0;
-    int off = 0;
-    double rowsum = 0.0;
-    int32_t cc[kChunkR];
-    double xx[kChunkR];
-    {
-        mbar_wait(&full[0], 0);
-        const int nr = min(kChunkR, R);
+        // register ring: chunk q (slot 0), q+1 (slot 1), q+2 (slot 2)
+        int32_t c0[kChunkR], c1[kChunkR], c2[kChunkR];
+        double x0[kChunkR], x1[kChunkR], x2[kChunkR];
+        double xi0 = 0.0, xi1 = 0.0, xi2 = 0.0;
+        ChunkIt m0{s_begin, 0, sub_rounds[s_begin]};
+        ChunkIt m1 = m0;
+        chunk_advance(m1, s_end, sub_rounds);
+        ChunkIt m2 = m1;
+        chunk_advance(m2, s_end, sub_rounds);
+        auto gather = [&](const ChunkIt& m, int qq, int32_t (&cc)[kChunkR],
+                          double (&xx)[kChunkR], double& xi) {
+            const int st = qq % kStages;
+            mbar_wait(&full[st], (qq / kStages) & 1);
+            const int nr = min(kChunkR, m.R - m.r0);
 #pragma unroll
-        for (int u = 0; u < kChunkR; ++u) cc[u] = u < nr ? s_col(0)[u * kS3Threads + tid] : -1;
+            for (int u = 0; u < kChunkR; ++u)
+                cc[u] = u < nr ? s_col(st)[u * kS3Threads + tid] : -1;
 #pragma unroll
-        for (int u = 0; u < kChunkR; ++u)
-            xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
-    }
-    double xi_next = 0.0;
-    while (true) {
-        // next chunk coordinates and its gathers (overlap the rounds below)
-        int s2 = s, r02 = r0 + kChunkR;
-        if (r02 >= R) {
-            s2 = s + 1;
-            r02 = 0;
-        }
-        const bool has_next = s2 < s_end;
-        int R2 = R;
-        int32_t cn[kChunkR];
-        double xn[kChunkR];
+            for (int u = 0; u < kChunkR; ++u)
+                xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
+            const int32_t i = R0 + (m.s - s_begin) * kS3Threads + tid;
+            xi = i < R1 ? __ldg(x + i) : 0.0;
+        };
+        gather(m0, 0, c0, x0, xi0);
+        if (m1.s < s_end) gather(m1, 1, c1, x1, xi1);
+        int off = 0;  // ring slot of the current sub-tile's first row
+        double rowsum = 0.0;
+        for (int q = 0; m0.s < s_end; ++q) {
+            if (m2.s < s_end) gather(m2, q + 2, c2, x2, xi2);
+            const int st = q % kStages;
+            const int nr = min(kChunkR, m0.R - m0.r0);
+            const int32_t a = R0 + (m0.s - s_begin) * kS3Threads;
+            const int32_t i = a + tid;
 #pragma unroll
-        for (int u = 0; u < kChunkR; ++u) {
-            cn[u] = -1;
-            xn[u] = 0.0;
-        }
-        if (has_next) {
-            if (s2 != s) {
-                R2 = sub_rounds[s2];
-                const int32_t i2 = R0 + (s2 - s_begin) * kS3Threads + tid;
-                xi_next = i2 < R1 ? __ldg(x + i2) : 0.0;
+            for (int u = 0; u < kChunkR; ++u) {
+                if (u < nr) {  // uniform over the consumers
+                    const double v = s_val(st)[u * kS3Threads + tid];
+                    rowsum += v * x0[u];
+                    const int32_t j = c0[u];
+                    if (j >= 0 && j != i) {
+                        const int slot = wrap(j - a + off, W);
+                        win[slot] += v * xi0;
+                    }
+                    named_bar_sync(1, kS3Threads);
+                }
             }
-            const int st2 = (q + 1) % kStages;
-            mbar_wait(&full[st2], ((q + 1) / kStages) & 1);
-            const int nr2 = min(kChunkR, R2 - r02);
-#pragma unroll
-            for (int u = 0; u < kChunkR; ++u)
-                cn[u] = u < nr2 ? s_col(st2)[u * kS3Threads + tid] : -1;
-#pragma unroll
-            for (int u = 0; u < kChunkR; ++u)
-                xn[u] = cn[u] != -1 ? __ldg(x + (cn[u] & 0x7fffffff)) : 0.0;
-        }
-        // rounds of the current chunk
-        const int st = q % kStages;
-        const int nr = min(kChunkR, R - r0);
-#pragma unroll
-        for (int u = 0; u < kChunkR; ++u) {
-            if (u < nr) {  // uniform over the consumers
-                const double v = s_val(st)[u * kS3Threads + tid];
-                rowsum += v * xx[u];
-                const int32_t j = cc[u];
-                if (j >= 0 && j != i) {
-                    const int slot = wrap(j - a + off, W);
-                    win[slot] += v * xi;
+            if (tid == 0) mbar_arrive(&empty[st]);  // every consumer is past its reads
+            if (m0.r0 + kChunkR >= m0.R) {  // sub-tile complete: finalise its rows
+                if (i < R1) {
+                    const int slot = wrap(tid + off, W);
+                    y[i] = rowsum + win[slot];
+                    win[slot] = 0.0;
                 }
                 named_bar_sync(1, kS3Threads);
+                off = wrap(off + kS3Threads, W);
+                rowsum = 0.0;
             }
-        }
-        if (tid == 0) mbar_arrive(&empty[st]);  // every consumer is past its reads
-        if (r0 + kChunkR >= R) {  // sub-tile complete: finalise its rows
-            if (valid) {
-                const int slot = wrap(tid + off, W);
-                y[i] = rowsum + win[slot];
-                win[slot] = 0.0;
-            }
-            named_bar_sync(1, kS3Threads);
-            off = wrap(off + kS3Threads, W);
-            rowsum = 0.0;
-            a += kS3Threads;
-            i = a + tid;
-            valid = i < R1;
-            xi = xi_next;
-        }
-        if (!has_next) break;
-        ++q;
-        s = s2;
-        r0 = r02;
-        R = R2;
 #pragma unroll
-        for (int u = 0; u < kChunkR; ++u) {
-            cc[u] = cn[u];
-            xx[u] = xn[u];
+            for (int u = 0; u < kChunkR; ++u) {
+                c0[u] = c1[u];
+                x0[u] = x1[u];
+                c1[u] = c2[u];
+                x1[u] = x2[u];
+            }
+            xi0 = xi1;
+            xi1 = xi2;
+            m0 = m1;
+            m1 = m2;
+            chunk_advance(m2, s_end, sub_rounds);
         }
     }
-    }  // s_begin < s_end
-    // spill: the region beyond the block, [R1, spill_hi), published with a
-    // release flag tagged by the launch epoch
+    // spill: the region beyond the block, [R1, spill_hi)
     const int32_t hi = spill_hi[c];
     if (hi > R1) {
         const int64_t so = spill_off[c];
         for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
             spill[so + (j - R1)] = win[(j - R0) % W];
     }
-    named_bar_sync(1, kS3Threads);
-    if (tid == 0) {
-        __threadfence();
-        st_release_gpu(flags + c, epoch);
+}
+
+// Head rows of block d receive the spills of earlier blocks, summed in
+// ascending source order and added once (deterministic). One block per
+// segment of <= kFixRows head rows of one destination, 8 rows per thread with
+// every load issued before use.
+__global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ segs,
+                                                  const int32_t* __restrict__ cta_row,
+                                                  const int32_t* __restrict__ first_src,
+                                                  const int32_t* __restrict__ spill_hi,
+                                                  const int64_t* __restrict__ spill_off,
+                                                  const double* __restrict__ spill,
+                                                  double* __restrict__ y) {
+    constexpr int U = kFixRows / 256;
+    const int4 sg = segs[blockIdx.x];
+    const int d = sg.x;
+    const int32_t j0 = sg.y, j1 = sg.z;
+    double acc[U];
+    bool any[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        acc[u] = 0.0;
+        any[u] = false;
     }
-    // ordered merge of the earlier blocks' spills into this block's head rows
-    // (ascending source block: deterministic). All blocks are co-resident
-    // (cooperative launch) and only wait on lower-numbered blocks.
-    const int32_t he = head_end[c];
-    if (he > R0) {
-        const int c0 = first_src[c];
-        if (tid == 0) {
-            for (int src = c0; src < c; ++src)
-                while (ld_acquire_gpu(flags + src) != epoch) __nanosleep(64);
-            __threadfence();
+    for (int src = first_src[d]; src < d; ++src) {
+        const int32_t s0 = cta_row[src + 1], hi = spill_hi[src];
+        const double* sp = spill + spill_off[src] - s0;
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t j = j0 + u * 256 + threadIdx.x;
+            const bool in = j < j1 && j >= s0 && j < hi;
+            v[u] = in ? __ldcg(sp + j) : 0.0;
+            any[u] |= in;
         }
-        named_bar_sync(1, kS3Threads);
-        for (int32_t j = R0 + tid; j < he; j += kS3Threads) {
-            double acc = 0.0;
-            bool any = false;
-            for (int src = c0; src < c; ++src) {
-                const int32_t s0 = cta_row[src + 1];
-                if (j >= s0 && j < spill_hi[src]) {
-                    acc += __ldcg(spill + spill_off[src] + (j - s0));
-                    any = true;
-                }
-            }
-            if (any) y[j] += acc;
-        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] += v[u];
+    }
+    double yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int32_t j = j0 + u * 256 + threadIdx.x;
+        yv[u] = any[u] ? __ldcg(y + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int32_t j = j0 + u * 256 + threadIdx.x;
+        if (any[u]) y[j] = yv[u] + acc[u];
     }
 }
 
@@ -542,9 +553,15 @@ void s3_setup(ktb_plan* p) {
         head_end[d] = he;
         first_src[d] = fs;
     }
-    std::vector<int64_t> head_prefix(P + 1, 0);
-    for (int d = 0; d < P; ++d) head_prefix[d + 1] = head_prefix[d] + (head_end[d] - bnd[d]);
-    L.head_total = head_prefix[P];
+    std::vector<int32_t> segs;  // (d, j0, j1, 0) per fixup block
+    for (int d = 0; d < P; ++d)
+        for (int32_t j = bnd[d]; j < head_end[d]; j += kFixRows) {
+            segs.push_back(d);
+            segs.push_back(j);
+            segs.push_back(std::min<int32_t>(head_end[d], j + kFixRows));
+            segs.push_back(0);
+        }
+    L.nsegs = static_cast<int64_t>(segs.size() / 4);
 
     auto up32 = [&](DBuf<int32_t>& d, const std::vector<int32_t>& h) {
         d.alloc(std::max<size_t>(h.size(), 1));
@@ -570,10 +587,7 @@ void s3_setup(ktb_plan* p) {
     up64(L.spill_off, spill_off);
     L.spill.alloc(std::max<int64_t>(so, 1));
     up32(L.head_end, head_end);
-    up64(L.head_prefix, head_prefix);
-    L.flags.alloc(P);
-    KTB_CUDA(cudaMemsetAsync(L.flags.p, 0, sizeof(int) * P, st));
-    L.epoch = 0;
+    up32(L.segs, segs);
     up32(L.first_src, first_src);
     up32(L.long_rows, long_rows);
     L.nlong = static_cast<int64_t>(long_rows.size());
@@ -584,29 +598,24 @@ void s3_setup(ktb_plan* p) {
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kS3SmemFixed + W * 8)));
     p->ctas = P;
-    p->launches = 1 + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
+    p->launches = 1 + (L.nsegs ? 1 : 0) + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
     p->extra_bytes = (total_slots - nnz) * 12 + so * 8 * 2 + so * 8 * 2;
 }
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
-    const int epoch = ++L.epoch;
-    int W = L.window, reach = L.reach, n = static_cast<int>(p->m->n);
-    const int32_t *cr = L.cta_row.p, *cs = L.cta_sub.p, *sr = L.sub_rounds.p, *sc = L.sell_col.p;
-    const int64_t* sb = L.sub_base.p;
-    const double* sv = L.sell_val.p;
-    const int32_t *sh = L.spill_hi.p, *he = L.head_end.p, *fs = L.first_src.p;
-    const int64_t* so = L.spill_off.p;
-    double* sp = L.spill.p;
-    int* fl = L.flags.p;
-    int ep = epoch;
-    void* args[] = {&cr, &cs, &sb, &sr, &sc, &sv, &x, &y, &W, &reach, &n,
-                    &sh, &so, &sp, &he, &fs, &fl, &ep};
-    KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_s3), dim3(L.ctas),
-                                         dim3(kS3Threads + 32), args,
-                                         kS3SmemFixed + static_cast<size_t>(L.window) * 8,
-                                         p->stream));
+    k_s3<<<L.ctas, kS3Threads + 32, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
+           p->stream>>>(L.cta_row.p, L.cta_sub.p, L.sub_base.p, L.sub_rounds.p, L.sell_col.p,
+                        L.sell_val.p, x, y, L.window, L.reach, static_cast<int>(p->m->n),
+                        L.spill_hi.p, L.spill_off.p, L.spill.p);
+    KTB_LAUNCH();
+    if (L.nsegs) {
+        k_s3_fixup<<<static_cast<int>(L.nsegs), 256, 0, p->stream>>>(
+            reinterpret_cast<const int4*>(L.segs.p), L.cta_row.p, L.first_src.p, L.spill_hi.p,
+            L.spill_off.p, L.spill.p, y);
+        KTB_LAUNCH();
+    }
 
     if (L.nlong) {
         const ktb_matrix* m = p->m;
