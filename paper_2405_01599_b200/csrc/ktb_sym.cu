@@ -153,11 +153,13 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // The part of each block's region beyond the block (the spill) goes to a
 // global buffer; k_s3_fixup adds it into the next blocks' head rows in
 // ascending source order, so the result is deterministic.
-constexpr int kS3Threads = 256;  // consumer threads = rows per sub-tile
-constexpr int kChunkR = 4;       // rounds per pipeline chunk
-constexpr int kStages = 6;
-constexpr int kStageCols = kChunkR * kS3Threads;                 // ints
-constexpr int kStageBytes = kChunkR * kS3Threads * (4 + 8);      // 12288
+constexpr int kS3Threads = 256;  // consumer threads
+constexpr int kRPT = 4;          // rows per consumer thread
+constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
+constexpr int kStages = 6;       // one round of one sub-tile per stage
+constexpr int kGD = 3;           // gather distance (stages ahead)
+constexpr int kRing = 4;         // register ring slots (>= kGD + 1)
+constexpr int kStageBytes = kRows * (4 + 8);  // 12288
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
@@ -165,15 +167,14 @@ constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
 
 struct ChunkIt {
-    int s, r0, R;
+    int s, r, R;  // sub-tile, round, rounds of that sub-tile
 };
 
 __device__ __forceinline__ void chunk_advance(ChunkIt& m, int s_end,
                                               const int32_t* __restrict__ sub_rounds) {
-    m.r0 += kChunkR;
-    if (m.r0 >= m.R) {
+    if (++m.r >= m.R) {
         ++m.s;
-        m.r0 = 0;
+        m.r = 0;
         m.R = m.s < s_end ? sub_rounds[m.s] : 0;
     }
 }
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     auto s_col = [&](int st) { return reinterpret_cast<int32_t*>(smem + st * kStageBytes); };
     auto s_val = [&](int st) {
-        return reinterpret_cast<double*>(smem + st * kStageBytes + kStageCols * 4);
+        return reinterpret_cast<double*>(smem + st * kStageBytes + kRows * 4);
     };
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     uint64_t* empty = full + kStages;
@@ -211,10 +212,10 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     if (tid >= kS3Threads) {  // ---------------- producer warp
         if (tid == kS3Threads) {
             const uint64_t pol = policy_evict_first();
-            // x is touched first by the far reach of the window: pull the
+            // x is first touched by the far reach of the window: pull the
             // initial window and then each sub-tile's new front into L2 ahead
             // of the consumers' gathers (the bench flushes L2 between steps).
-            constexpr int kAhead = 4;  // sub-tiles of look-ahead
+            constexpr int kAhead = 2;  // sub-tiles of look-ahead
             auto pf = [&](int64_t lo, int64_t hi) {
                 lo = max(lo & ~int64_t(1), int64_t(0));
                 hi = min(hi, int64_t(n));
@@ -223,23 +224,21 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                     prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
                 }
             };
-            if (s_begin < s_end) pf(R0, int64_t(R0) + kS3Threads * (kAhead + 1) + reach);
+            if (s_begin < s_end) pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
             int q = 0;
             for (int s = s_begin; s < s_end; ++s) {
                 const int R = sub_rounds[s];
                 const int64_t base = sub_base[s];
                 const int64_t front =
-                    int64_t(R0) + int64_t(s - s_begin + kAhead + 1) * kS3Threads + reach;
-                pf(front, front + kS3Threads);
-                for (int r0 = 0; r0 < R; r0 += kChunkR, ++q) {
-                    const int nr = min(kChunkR, R - r0);
+                    int64_t(R0) + int64_t(s - s_begin + kAhead + 1) * kRows + reach;
+                pf(front, front + kRows);
+                for (int r = 0; r < R; ++r, ++q) {
                     const int st = q % kStages;
                     if (q >= kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
-                    const uint32_t bc = nr * kS3Threads * 4, bv = nr * kS3Threads * 8;
-                    mbar_arrive_expect_tx(&full[st], bc + bv);
-                    tma_load_1d(s_col(st), scol + base + int64_t(r0) * kS3Threads, bc, &full[st],
+                    mbar_arrive_expect_tx(&full[st], kStageBytes);
+                    tma_load_1d(s_col(st), scol + base + int64_t(r) * kRows, kRows * 4, &full[st],
                                 pol);
-                    tma_load_1d(s_val(st), sval + base + int64_t(r0) * kS3Threads, bv, &full[st],
+                    tma_load_1d(s_val(st), sval + base + int64_t(r) * kRows, kRows * 8, &full[st],
                                 pol);
                 }
             }
@@ -249,75 +248,96 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 
     // ---------------------------------------------------- consumers
     if (s_begin < s_end) {
-        // register ring: chunk q (slot 0), q+1 (slot 1), q+2 (slot 2)
-        int32_t c0[kChunkR], c1[kChunkR], c2[kChunkR];
-        double x0[kChunkR], x1[kChunkR], x2[kChunkR];
-        double xi0 = 0.0, xi1 = 0.0, xi2 = 0.0;
-        ChunkIt m0{s_begin, 0, sub_rounds[s_begin]};
-        ChunkIt m1 = m0;
-        chunk_advance(m1, s_end, sub_rounds);
-        ChunkIt m2 = m1;
-        chunk_advance(m2, s_end, sub_rounds);
-        auto gather = [&](const ChunkIt& m, int qq, int32_t (&cc)[kChunkR],
-                          double (&xx)[kChunkR], double& xi) {
+        // register ring: slot k holds the cols / gathered x / x_i of one round
+        int32_t cr[kRing][kRPT];
+        double xr[kRing][kRPT], xir[kRing][kRPT];
+        auto gather = [&](const ChunkIt& m, int qq, int32_t (&cc)[kRPT], double (&xx)[kRPT],
+                          double (&xi)[kRPT]) {
             const int st = qq % kStages;
             mbar_wait(&full[st], (qq / kStages) & 1);
-            const int nr = min(kChunkR, m.R - m.r0);
+            const int32_t a = R0 + (m.s - s_begin) * kRows;
 #pragma unroll
-            for (int u = 0; u < kChunkR; ++u)
-                cc[u] = u < nr ? s_col(st)[u * kS3Threads + tid] : -1;
+            for (int u = 0; u < kRPT; ++u) cc[u] = s_col(st)[u * kS3Threads + tid];
 #pragma unroll
-            for (int u = 0; u < kChunkR; ++u)
+            for (int u = 0; u < kRPT; ++u)
                 xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
-            const int32_t i = R0 + (m.s - s_begin) * kS3Threads + tid;
-            xi = i < R1 ? __ldg(x + i) : 0.0;
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u) {
+                const int32_t i = a + u * kS3Threads + tid;
+                xi[u] = (m.r == 0 && i < R1) ? __ldg(x + i) : 0.0;
+            }
         };
-        gather(m0, 0, c0, x0, xi0);
-        if (m1.s < s_end) gather(m1, 1, c1, x1, xi1);
+        ChunkIt mg{s_begin, 0, sub_rounds[s_begin]};  // next chunk to gather
+        int qg = 0;
+#pragma unroll
+        for (int k = 0; k < kGD; ++k) {
+            if (mg.s < s_end) {
+                gather(mg, qg, cr[k], xr[k], xir[k]);
+                chunk_advance(mg, s_end, sub_rounds);
+                ++qg;
+            }
+        }
+        ChunkIt mc{s_begin, 0, sub_rounds[s_begin]};  // current chunk
         int off = 0;  // ring slot of the current sub-tile's first row
-        double rowsum = 0.0;
-        for (int q = 0; m0.s < s_end; ++q) {
-            if (m2.s < s_end) gather(m2, q + 2, c2, x2, xi2);
-            const int st = q % kStages;
-            const int nr = min(kChunkR, m0.R - m0.r0);
-            const int32_t a = R0 + (m0.s - s_begin) * kS3Threads;
-            const int32_t i = a + tid;
+        double rowsum[kRPT], xi[kRPT];
 #pragma unroll
-            for (int u = 0; u < kChunkR; ++u) {
-                if (u < nr) {  // uniform over the consumers
-                    const double v = s_val(st)[u * kS3Threads + tid];
-                    rowsum += v * x0[u];
-                    const int32_t j = c0[u];
-                    if (j >= 0 && j != i) {
-                        const int slot = wrap(j - a + off, W);
-                        win[slot] += v * xi0;
+        for (int u = 0; u < kRPT; ++u) rowsum[u] = 0.0;
+        int q = 0;
+        bool alive = true;
+        while (alive) {
+#pragma unroll
+            for (int k = 0; k < kRing; ++k) {
+                if (alive) {
+                    const int kg = (k + kGD) % kRing;
+                    if (mg.s < s_end) {
+                        gather(mg, qg, cr[kg], xr[kg], xir[kg]);
+                        chunk_advance(mg, s_end, sub_rounds);
+                        ++qg;
                     }
-                    named_bar_sync(1, kS3Threads);
-                }
-            }
-            if (tid == 0) mbar_arrive(&empty[st]);  // every consumer is past its reads
-            if (m0.r0 + kChunkR >= m0.R) {  // sub-tile complete: finalise its rows
-                if (i < R1) {
-                    const int slot = wrap(tid + off, W);
-                    y[i] = rowsum + win[slot];
-                    win[slot] = 0.0;
-                }
-                named_bar_sync(1, kS3Threads);
-                off = wrap(off + kS3Threads, W);
-                rowsum = 0.0;
-            }
+                    const int st = q % kStages;
+                    const int32_t a = R0 + (mc.s - s_begin) * kRows;
+                    if (mc.r == 0) {
 #pragma unroll
-            for (int u = 0; u < kChunkR; ++u) {
-                c0[u] = c1[u];
-                x0[u] = x1[u];
-                c1[u] = c2[u];
-                x1[u] = x2[u];
+                        for (int u = 0; u < kRPT; ++u) xi[u] = xir[k][u];
+                    }
+                    double v[kRPT];
+#pragma unroll
+                    for (int u = 0; u < kRPT; ++u) v[u] = s_val(st)[u * kS3Threads + tid];
+                    double wv[kRPT];
+                    int sl[kRPT];
+                    bool sc[kRPT];
+#pragma unroll
+                    for (int u = 0; u < kRPT; ++u) {
+                        rowsum[u] += v[u] * xr[k][u];
+                        const int32_t j = cr[k][u];
+                        sc[u] = j >= 0 && j != a + u * kS3Threads + tid;
+                        sl[u] = wrap(j - a + off, W);
+                        wv[u] = sc[u] ? win[sl[u]] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kRPT; ++u)
+                        if (sc[u]) win[sl[u]] = wv[u] + v[u] * xi[u];
+                    named_bar_sync(1, kS3Threads);
+                    if (tid == 0) mbar_arrive(&empty[st]);  // all consumers are past their reads
+                    if (mc.r + 1 >= mc.R) {  // sub-tile complete: finalise its rows
+#pragma unroll
+                        for (int u = 0; u < kRPT; ++u) {
+                            const int32_t i = a + u * kS3Threads + tid;
+                            if (i < R1) {
+                                const int slot = wrap(u * kS3Threads + tid + off, W);
+                                y[i] = rowsum[u] + win[slot];
+                                win[slot] = 0.0;
+                            }
+                            rowsum[u] = 0.0;
+                        }
+                        named_bar_sync(1, kS3Threads);
+                        off = wrap(off + kRows, W);
+                    }
+                    chunk_advance(mc, s_end, sub_rounds);
+                    ++q;
+                    alive = mc.s < s_end;
+                }
             }
-            xi0 = xi1;
-            xi1 = xi2;
-            m0 = m1;
-            m1 = m2;
-            chunk_advance(m2, s_end, sub_rounds);
         }
     }
     // spill: the region beyond the block, [R1, spill_hi)
@@ -419,7 +439,7 @@ void s3_setup(ktb_plan* p) {
     require(m->kind == KTB_SYM_UPPER, "spmv: symmetric kernel on a general matrix");
     auto& L = p->sw;
     cudaStream_t st = p->stream;
-    const int S = kS3Threads;
+    const int S = kRows;
     const int64_t n = m->n, nnz = m->nnz;
     const int P = std::max(1, m->sm_count);
     L.ctas = P;
