@@ -85,6 +85,11 @@ __device__ __forceinline__ double ldg_hint_f64(const double* p, uint64_t policy)
     return r;
 }
 
+__device__ __forceinline__ void st_hint_f64(double* p, double v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy)
+                 : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

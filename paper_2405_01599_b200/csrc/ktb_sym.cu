@@ -161,7 +161,8 @@ constexpr int kGD = 3;           // gather distance (stages ahead)
 constexpr int kRing = 4;         // register ring slots (>= kGD + 1)
 constexpr int kStageBytes = kRows * (4 + 8);  // 12288
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
-constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 128;
+constexpr int kMaxSubCache = 1024;  // sub-tile round counts cached in smem
+constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 4 * kMaxSubCache + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
@@ -247,95 +248,124 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     }
 
     // ---------------------------------------------------- consumers
+    // Only consumer thread 0 waits on the stage mbarriers, one chunk ahead;
+    // the per-round named barrier then publishes the landed stage to all
+    // consumers (no spinning warps stealing issue slots).
     if (s_begin < s_end) {
-        // register ring: slot k holds the cols / gathered x / x_i of one round
+        const int nsub = s_end - s_begin;
+        const uint64_t keep = policy_evict_last();  // y head rows are re-read by the fixup
+        int* s_R = reinterpret_cast<int*>(full + 2 * kStages);  // <= kMaxSubCache entries
+        const bool cached = nsub <= kMaxSubCache;
+        if (cached)
+            for (int k = tid; k < nsub; k += kS3Threads) s_R[k] = sub_rounds[s_begin + k];
+        named_bar_sync(1, kS3Threads);
+        auto rounds_of = [&](int sl) { return cached ? s_R[sl] : sub_rounds[s_begin + sl]; };
+        // gather iterator (chunk qg): local sub-tile index gs, round gr, rounds gR
+        int gs = 0, gr = 0, gR = rounds_of(0), gst = 0;
+        // wait iterator (chunk qw = qg + 1, waited by tid 0)
+        int ws = 0, wr = 0, wR = gR, wst = 0, wph = 0;
+        auto adv = [&](int& sl, int& r, int& R) {
+            if (++r >= R) {
+                ++sl;
+                r = 0;
+                R = sl < nsub ? rounds_of(sl) : 0;
+            }
+        };
+        auto adv_stage = [](int& st) { st = (st + 1 == kStages) ? 0 : st + 1; };
+        auto wait_next = [&]() {  // tid 0: wait for the chunk after the last gathered one
+            if (tid == 0 && ws < nsub) mbar_wait(&full[wst], wph);
+            adv(ws, wr, wR);
+            if (++wst == kStages) {
+                wst = 0;
+                wph ^= 1;
+            }
+        };
         int32_t cr[kRing][kRPT];
         double xr[kRing][kRPT], xir[kRing][kRPT];
-        auto gather = [&](const ChunkIt& m, int qq, int32_t (&cc)[kRPT], double (&xx)[kRPT],
-                          double (&xi)[kRPT]) {
-            const int st = qq % kStages;
-            mbar_wait(&full[st], (qq / kStages) & 1);
-            const int32_t a = R0 + (m.s - s_begin) * kRows;
+        auto gather = [&](int32_t (&cc)[kRPT], double (&xx)[kRPT], double (&xi)[kRPT]) {
+            const int32_t* sc = s_col(gst) + tid;
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u) cc[u] = s_col(st)[u * kS3Threads + tid];
+            for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
 #pragma unroll
             for (int u = 0; u < kRPT; ++u)
                 xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
+            if (gr == 0) {
+                const int32_t i0 = R0 + gs * kRows + tid;
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u) {
-                const int32_t i = a + u * kS3Threads + tid;
-                xi[u] = (m.r == 0 && i < R1) ? __ldg(x + i) : 0.0;
+                for (int u = 0; u < kRPT; ++u) {
+                    const int32_t i = i0 + u * kS3Threads;
+                    xi[u] = i < R1 ? __ldg(x + i) : 0.0;
+                }
             }
+            adv(gs, gr, gR);
+            adv_stage(gst);
         };
-        ChunkIt mg{s_begin, 0, sub_rounds[s_begin]};  // next chunk to gather
-        int qg = 0;
+        // prologue: chunks 0..kGD landed and visible, gather 0..kGD-1
 #pragma unroll
-        for (int k = 0; k < kGD; ++k) {
-            if (mg.s < s_end) {
-                gather(mg, qg, cr[k], xr[k], xir[k]);
-                chunk_advance(mg, s_end, sub_rounds);
-                ++qg;
-            }
-        }
-        ChunkIt mc{s_begin, 0, sub_rounds[s_begin]};  // current chunk
-        int off = 0;  // ring slot of the current sub-tile's first row
+        for (int k = 0; k <= kGD; ++k) wait_next();
+        named_bar_sync(1, kS3Threads);
+#pragma unroll
+        for (int k = 0; k < kGD; ++k)
+            if (gs < nsub) gather(cr[k], xr[k], xir[k]);
+        int cs = 0, crd = 0, cR = rounds_of(0), cst = 0;  // current chunk
+        int off = 0;                                       // ring slot of the sub-tile's row 0
+        int32_t a = R0;
         double rowsum[kRPT], xi[kRPT];
 #pragma unroll
         for (int u = 0; u < kRPT; ++u) rowsum[u] = 0.0;
-        int q = 0;
         bool alive = true;
         while (alive) {
 #pragma unroll
             for (int k = 0; k < kRing; ++k) {
                 if (alive) {
+                    constexpr int dummy = 0;
+                    (void)dummy;
                     const int kg = (k + kGD) % kRing;
-                    if (mg.s < s_end) {
-                        gather(mg, qg, cr[kg], xr[kg], xir[kg]);
-                        chunk_advance(mg, s_end, sub_rounds);
-                        ++qg;
-                    }
-                    const int st = q % kStages;
-                    const int32_t a = R0 + (mc.s - s_begin) * kRows;
-                    if (mc.r == 0) {
+                    if (gs < nsub) gather(cr[kg], xr[kg], xir[kg]);
+                    if (crd == 0) {
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) xi[u] = xir[k][u];
                     }
-                    double v[kRPT];
-#pragma unroll
-                    for (int u = 0; u < kRPT; ++u) v[u] = s_val(st)[u * kS3Threads + tid];
-                    double wv[kRPT];
+                    const double* sv = s_val(cst) + tid;
+                    double v[kRPT], wv[kRPT];
                     int sl[kRPT];
                     bool sc[kRPT];
 #pragma unroll
+                    for (int u = 0; u < kRPT; ++u) v[u] = sv[u * kS3Threads];
+#pragma unroll
                     for (int u = 0; u < kRPT; ++u) {
                         rowsum[u] += v[u] * xr[k][u];
-                        const int32_t j = cr[k][u];
-                        sc[u] = j >= 0 && j != a + u * kS3Threads + tid;
-                        sl[u] = wrap(j - a + off, W);
+                        const int32_t rel = cr[k][u] - a;  // -1 - a for padding: sc false
+                        sc[u] = cr[k][u] >= 0 && rel != u * kS3Threads + tid;
+                        sl[u] = wrap(rel + off, W);
                         wv[u] = sc[u] ? win[sl[u]] : 0.0;
                     }
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u)
                         if (sc[u]) win[sl[u]] = wv[u] + v[u] * xi[u];
+                    wait_next();
                     named_bar_sync(1, kS3Threads);
-                    if (tid == 0) mbar_arrive(&empty[st]);  // all consumers are past their reads
-                    if (mc.r + 1 >= mc.R) {  // sub-tile complete: finalise its rows
+                    if (tid == 0) mbar_arrive(&empty[cst]);  // all consumers are past its reads
+                    adv_stage(cst);
+                    if (++crd >= cR) {  // sub-tile complete: finalise its rows
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
                             const int32_t i = a + u * kS3Threads + tid;
                             if (i < R1) {
                                 const int slot = wrap(u * kS3Threads + tid + off, W);
-                                y[i] = rowsum[u] + win[slot];
+                                st_hint_f64(y + i, rowsum[u] + win[slot], keep);
                                 win[slot] = 0.0;
                             }
                             rowsum[u] = 0.0;
                         }
                         named_bar_sync(1, kS3Threads);
                         off = wrap(off + kRows, W);
+                        a += kRows;
+                        crd = 0;
+                        ++cs;
+                        cR = cs < nsub ? rounds_of(cs) : 0;
+                        alive = cs < nsub;
                     }
-                    chunk_advance(mc, s_end, sub_rounds);
-                    ++q;
-                    alive = mc.s < s_end;
                 }
             }
         }
@@ -344,8 +374,9 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     const int32_t hi = spill_hi[c];
     if (hi > R1) {
         const int64_t so = spill_off[c];
+        const uint64_t keep = policy_evict_last();
         for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
-            spill[so + (j - R1)] = win[(j - R0) % W];
+            st_hint_f64(spill + so + (j - R1), win[(j - R0) % W], keep);
     }
 }
 
