@@ -161,7 +161,8 @@ constexpr int kGD = 3;           // gather distance (stages ahead)
 constexpr int kRing = 4;         // register ring slots (>= kGD + 1)
 constexpr int kStageBytes = kRows * (4 + 8);  // 12288
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
-constexpr int kMaxSubCache = 1024;  // sub-tile round counts cached in smem
+constexpr int kMaxSubCache = 1024;
+constexpr int kL2Ahead = 12;     // SELL chunks prefetched into L2 ahead of the TMA ring  // sub-tile round counts cached in smem
 constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 4 * kMaxSubCache + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
@@ -226,6 +227,22 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                 }
             };
             if (s_begin < s_end) pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
+            // The SELL stream is also pulled into L2 kL2Ahead chunks ahead of
+            // the smem ring: the window leaves room for only ~74 KB of smem
+            // stages, too little to cover HBM latency on its own.
+            int ps = s_begin, pr = 0, pR = sub_rounds[s_begin];
+            auto l2_ahead = [&]() {
+                if (ps >= s_end) return;
+                const int64_t e = sub_base[ps] + int64_t(pr) * kRows;
+                prefetch_l2_bulk(scol + e, kRows * 4);
+                prefetch_l2_bulk(sval + e, kRows * 8);
+                if (++pr >= pR) {
+                    ++ps;
+                    pr = 0;
+                    pR = ps < s_end ? sub_rounds[ps] : 0;
+                }
+            };
+            for (int k = 0; k < kL2Ahead; ++k) l2_ahead();
             int q = 0;
             for (int s = s_begin; s < s_end; ++s) {
                 const int R = sub_rounds[s];
@@ -234,6 +251,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                     int64_t(R0) + int64_t(s - s_begin + kAhead + 1) * kRows + reach;
                 pf(front, front + kRows);
                 for (int r = 0; r < R; ++r, ++q) {
+                    l2_ahead();
                     const int st = q % kStages;
                     if (q >= kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
                     mbar_arrive_expect_tx(&full[st], kStageBytes);
