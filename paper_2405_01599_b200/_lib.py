@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libktb.so")
+LIB_PATH = os.path.join(HERE, "_lib", os.environ.get("KTB_LIB_NAME", "libktb.so"))
 
 I64 = C.c_int64
 VP = C.c_void_p

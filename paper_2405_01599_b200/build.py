@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
-LIB = os.path.join(LIBDIR, "libktb.so")
+LIB = os.path.join(LIBDIR, os.environ.get("KTB_LIB_NAME", "libktb.so"))
 SOURCES = ["ktb_api.cu", "ktb_build.cu", "ktb_unsym.cu", "ktb_sym.cu", "ktb_gmres.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -43,7 +43,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if not os.path.exists(path):
             continue
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        extra = os.environ.get("KTB_EXTRA_FLAGS", "").split()
+        cmd = [nvcc(), *ARCH, "-O3", *extra, "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                "-c", path, "-o", obj]
         subprocess.run(cmd, check=True)

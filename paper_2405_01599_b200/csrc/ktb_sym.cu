@@ -161,8 +161,7 @@ constexpr int kGD = 3;           // gather distance (stages ahead)
 constexpr int kRing = 4;         // register ring slots (>= kGD + 1)
 constexpr int kStageBytes = kRows * (4 + 8);  // 12288
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
-constexpr int kMaxSubCache = 1024;
-constexpr int kL2Ahead = 12;     // SELL chunks prefetched into L2 ahead of the TMA ring  // sub-tile round counts cached in smem
+constexpr int kMaxSubCache = 1024;  // sub-tile round counts cached in smem
 constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 4 * kMaxSubCache + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
@@ -227,22 +226,6 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                 }
             };
             if (s_begin < s_end) pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
-            // The SELL stream is also pulled into L2 kL2Ahead chunks ahead of
-            // the smem ring: the window leaves room for only ~74 KB of smem
-            // stages, too little to cover HBM latency on its own.
-            int ps = s_begin, pr = 0, pR = sub_rounds[s_begin];
-            auto l2_ahead = [&]() {
-                if (ps >= s_end) return;
-                const int64_t e = sub_base[ps] + int64_t(pr) * kRows;
-                prefetch_l2_bulk(scol + e, kRows * 4);
-                prefetch_l2_bulk(sval + e, kRows * 8);
-                if (++pr >= pR) {
-                    ++ps;
-                    pr = 0;
-                    pR = ps < s_end ? sub_rounds[ps] : 0;
-                }
-            };
-            for (int k = 0; k < kL2Ahead; ++k) l2_ahead();
             int q = 0;
             for (int s = s_begin; s < s_end; ++s) {
                 const int R = sub_rounds[s];
@@ -251,7 +234,6 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                     int64_t(R0) + int64_t(s - s_begin + kAhead + 1) * kRows + reach;
                 pf(front, front + kRows);
                 for (int r = 0; r < R; ++r, ++q) {
-                    l2_ahead();
                     const int st = q % kStages;
                     if (q >= kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
                     mbar_arrive_expect_tx(&full[st], kStageBytes);
@@ -278,6 +260,8 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
             for (int k = tid; k < nsub; k += kS3Threads) s_R[k] = sub_rounds[s_begin + k];
         named_bar_sync(1, kS3Threads);
         auto rounds_of = [&](int sl) { return cached ? s_R[sl] : sub_rounds[s_begin + sl]; };
+        int qtot = 0;  // chunks of this block (only needed when tiny)
+        for (int k = 0; k < nsub && qtot < kGD; ++k) qtot += rounds_of(k);
         // gather iterator (chunk qg): local sub-tile index gs, round gr, rounds gR
         int gs = 0, gr = 0, gR = rounds_of(0), gst = 0;
         // wait iterator (chunk qw = qg + 1, waited by tid 0)
@@ -298,15 +282,27 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                 wph ^= 1;
             }
         };
+        // register ring slot k: cols, vals, gathered x, x_i of one chunk.
+        // A stage is copied to registers when gathered and released right
+        // after the next round barrier, so the smem ring stays in flight.
         int32_t cr[kRing][kRPT];
-        double xr[kRing][kRPT], xir[kRing][kRPT];
-        auto gather = [&](int32_t (&cc)[kRPT], double (&xx)[kRPT], double (&xi)[kRPT]) {
+        double vr[kRing][kRPT], xr[kRing][kRPT], xir[kRing][kRPT];
+        auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT],
+                          double (&xi)[kRPT]) {
             const int32_t* sc = s_col(gst) + tid;
+            const double* sv = s_val(gst) + tid;
 #pragma unroll
             for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u)
+            for (int u = 0; u < kRPT; ++u) vv[u] = sv[u * kS3Threads];
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u) {
+#ifdef KTB_DIAG_NOGATHER
+                xx[u] = cc[u] != -1 ? 1.0 : 0.0;
+#else
                 xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
+#endif
+            }
             if (gr == 0) {
                 const int32_t i0 = R0 + gs * kRows + tid;
 #pragma unroll
@@ -316,17 +312,29 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                 }
             }
             adv(gs, gr, gR);
-            adv_stage(gst);
         };
-        // prologue: chunks 0..kGD landed and visible, gather 0..kGD-1
+        // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1 and
+        // release their stages
 #pragma unroll
         for (int k = 0; k <= kGD; ++k) wait_next();
         named_bar_sync(1, kS3Threads);
 #pragma unroll
-        for (int k = 0; k < kGD; ++k)
-            if (gs < nsub) gather(cr[k], xr[k], xir[k]);
-        int cs = 0, crd = 0, cR = rounds_of(0), cst = 0;  // current chunk
-        int off = 0;                                       // ring slot of the sub-tile's row 0
+        for (int k = 0; k < kGD; ++k) {
+            if (gs < nsub) {
+                gather(cr[k], vr[k], xr[k], xir[k]);
+                adv_stage(gst);
+            }
+        }
+        named_bar_sync(1, kS3Threads);
+        if (tid == 0) {
+            int st = 0;
+            for (int k = 0; k < kGD && k < qtot; ++k) {
+                mbar_arrive(&empty[st]);
+                adv_stage(st);
+            }
+        }
+        int cs = 0, crd = 0, cR = rounds_of(0);  // current chunk
+        int off = 0;                              // ring slot of the sub-tile's row 0
         int32_t a = R0;
         double rowsum[kRPT], xi[kRPT];
 #pragma unroll
@@ -336,35 +344,36 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 #pragma unroll
             for (int k = 0; k < kRing; ++k) {
                 if (alive) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
                     const int kg = (k + kGD) % kRing;
-                    if (gs < nsub) gather(cr[kg], xr[kg], xir[kg]);
+                    const bool gathered = gs < nsub;
+                    const int gst_now = gst;
+                    if (gathered) {
+                        gather(cr[kg], vr[kg], xr[kg], xir[kg]);
+                        adv_stage(gst);
+                    }
                     if (crd == 0) {
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) xi[u] = xir[k][u];
                     }
-                    const double* sv = s_val(cst) + tid;
-                    double v[kRPT], wv[kRPT];
+                    double wv[kRPT];
                     int sl[kRPT];
                     bool sc[kRPT];
 #pragma unroll
-                    for (int u = 0; u < kRPT; ++u) v[u] = sv[u * kS3Threads];
-#pragma unroll
                     for (int u = 0; u < kRPT; ++u) {
-                        rowsum[u] += v[u] * xr[k][u];
-                        const int32_t rel = cr[k][u] - a;  // -1 - a for padding: sc false
+                        rowsum[u] += vr[k][u] * xr[k][u];
+                        const int32_t rel = cr[k][u] - a;
                         sc[u] = cr[k][u] >= 0 && rel != u * kS3Threads + tid;
                         sl[u] = wrap(rel + off, W);
                         wv[u] = sc[u] ? win[sl[u]] : 0.0;
                     }
+#ifndef KTB_DIAG_NORMW
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u)
-                        if (sc[u]) win[sl[u]] = wv[u] + v[u] * xi[u];
+                        if (sc[u]) win[sl[u]] = wv[u] + vr[k][u] * xi[u];
+#endif
                     wait_next();
                     named_bar_sync(1, kS3Threads);
-                    if (tid == 0) mbar_arrive(&empty[cst]);  // all consumers are past its reads
-                    adv_stage(cst);
+                    if (tid == 0 && gathered) mbar_arrive(&empty[gst_now]);  // copied out
                     if (++crd >= cR) {  // sub-tile complete: finalise its rows
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
