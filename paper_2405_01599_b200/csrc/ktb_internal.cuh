@@ -118,9 +118,9 @@ struct SymWindowLayout {
     int64_t far = 0;       // entries scattered outside the window (atomic path)
     int64_t spill_total = 0;
     DBuf<int32_t> cta_row;     // ctas+1 (bit-exact NNZ_BALANCED boundaries)
-    DBuf<int32_t> cta_sub;     // ctas+1 sub-tile ranges
-    DBuf<int64_t> sub_base;    // per sub-tile offset into the SELL arrays
-    DBuf<int32_t> sub_rounds;  // per sub-tile round count
+    DBuf<int32_t> cta_chunk;   // ctas+1: round-chunk ranges per block
+    DBuf<int32_t> chunk_meta;  // per chunk: sub-tile | last | round
+    DBuf<int64_t> cta_base;    // per block: SELL offset of its first chunk
     DBuf<int32_t> sell_col;    // round-major SELL columns (-1 pad, top bit = far)
     DBuf<double> sell_val;
     DBuf<int32_t> spill_hi;    // per CTA: end of its spill range (start = cta_row[c+1])

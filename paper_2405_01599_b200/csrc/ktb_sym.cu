@@ -167,23 +167,16 @@ constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
 
-struct ChunkIt {
-    int s, r, R;  // sub-tile, round, rounds of that sub-tile
-};
-
-__device__ __forceinline__ void chunk_advance(ChunkIt& m, int s_end,
-                                              const int32_t* __restrict__ sub_rounds) {
-    if (++m.r >= m.R) {
-        ++m.s;
-        m.r = 0;
-        m.R = m.s < s_end ? sub_rounds[m.s] : 0;
-    }
-}
+// chunk metadata (one int per round-chunk): bits 0-6 round, bit 7 last round
+// of its sub-tile, bits 8.. sub-tile index local to the block
+__device__ __forceinline__ int meta_round(int m) { return m & 127; }
+__device__ __forceinline__ bool meta_last(int m) { return (m >> 7) & 1; }
+__device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
 
 __global__ void __launch_bounds__(kS3Threads + 32, 1)
-    k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_sub,
-         const int64_t* __restrict__ sub_base, const int32_t* __restrict__ sub_rounds,
-         const int32_t* __restrict__ scol, const double* __restrict__ sval,
+    k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
+         const int32_t* __restrict__ chunk_meta, const int32_t* __restrict__ scol,
+         const double* __restrict__ sval, const int64_t* __restrict__ cta_base,
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
@@ -199,7 +192,12 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     const int tid = threadIdx.x;
     const int c = blockIdx.x;
     const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
-    const int s_begin = cta_sub[c], s_end = cta_sub[c + 1];
+    const int q0 = cta_chunk[c];
+    const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
+    const int32_t* meta = chunk_meta + q0;
+    // chunk q of this block = kRows contiguous SELL slots at cta_base[c] + q*kRows
+    const int32_t* gcol = scol + cta_base[c];
+    const double* gval = sval + cta_base[c];
     if (tid == 0) {
         for (int st = 0; st < kStages; ++st) {
             mbar_init(&full[st], 1);
@@ -211,7 +209,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     __syncthreads();
 
     if (tid >= kS3Threads) {  // ---------------- producer warp
-        if (tid == kS3Threads) {
+        if (tid == kS3Threads && Q > 0) {
             const uint64_t pol = policy_evict_first();
             // x is first touched by the far reach of the window: pull the
             // initial window and then each sub-tile's new front into L2 ahead
@@ -225,22 +223,22 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                     prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
                 }
             };
-            if (s_begin < s_end) pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
-            int q = 0;
-            for (int s = s_begin; s < s_end; ++s) {
-                const int R = sub_rounds[s];
-                const int64_t base = sub_base[s];
-                const int64_t front =
-                    int64_t(R0) + int64_t(s - s_begin + kAhead + 1) * kRows + reach;
-                pf(front, front + kRows);
-                for (int r = 0; r < R; ++r, ++q) {
-                    const int st = q % kStages;
-                    if (q >= kStages) mbar_wait(&empty[st], ((q / kStages) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[st], kStageBytes);
-                    tma_load_1d(s_col(st), scol + base + int64_t(r) * kRows, kRows * 4, &full[st],
-                                pol);
-                    tma_load_1d(s_val(st), sval + base + int64_t(r) * kRows, kRows * 8, &full[st],
-                                pol);
+            pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
+            int st = 0, ph = 0;
+            for (int q = 0; q < Q; ++q) {
+                const int m = __ldg(meta + q);
+                if (meta_round(m) == 0) {
+                    const int64_t front =
+                        int64_t(R0) + int64_t(meta_sub(m) + kAhead + 1) * kRows + reach;
+                    pf(front, front + kRows);
+                }
+                if (q >= kStages) mbar_wait(&empty[st], ph ^ 1);
+                mbar_arrive_expect_tx(&full[st], kStageBytes);
+                tma_load_1d(s_col(st), gcol + int64_t(q) * kRows, kRows * 4, &full[st], pol);
+                tma_load_1d(s_val(st), gval + int64_t(q) * kRows, kRows * 8, &full[st], pol);
+                if (++st == kStages) {
+                    st = 0;
+                    ph ^= 1;
                 }
             }
         }
@@ -249,48 +247,28 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 
     // ---------------------------------------------------- consumers
     // Only consumer thread 0 waits on the stage mbarriers, one chunk ahead;
-    // the per-round named barrier then publishes the landed stage to all
-    // consumers (no spinning warps stealing issue slots).
-    if (s_begin < s_end) {
-        const int nsub = s_end - s_begin;
+    // the per-round named barrier publishes the landed stage to all
+    // consumers. A stage is copied to registers when gathered and released
+    // right after the next barrier, so the smem ring stays in flight.
+    if (Q > 0) {
         const uint64_t keep = policy_evict_last();  // y head rows are re-read by the fixup
-        int* s_R = reinterpret_cast<int*>(full + 2 * kStages);  // <= kMaxSubCache entries
-        const bool cached = nsub <= kMaxSubCache;
-        if (cached)
-            for (int k = tid; k < nsub; k += kS3Threads) s_R[k] = sub_rounds[s_begin + k];
-        named_bar_sync(1, kS3Threads);
-        auto rounds_of = [&](int sl) { return cached ? s_R[sl] : sub_rounds[s_begin + sl]; };
-        int qtot = 0;  // chunks of this block (only needed when tiny)
-        for (int k = 0; k < nsub && qtot < kGD; ++k) qtot += rounds_of(k);
-        // gather iterator (chunk qg): local sub-tile index gs, round gr, rounds gR
-        int gs = 0, gr = 0, gR = rounds_of(0), gst = 0;
-        // wait iterator (chunk qw = qg + 1, waited by tid 0)
-        int ws = 0, wr = 0, wR = gR, wst = 0, wph = 0;
-        auto adv = [&](int& sl, int& r, int& R) {
-            if (++r >= R) {
-                ++sl;
-                r = 0;
-                R = sl < nsub ? rounds_of(sl) : 0;
-            }
-        };
-        auto adv_stage = [](int& st) { st = (st + 1 == kStages) ? 0 : st + 1; };
-        auto wait_next = [&]() {  // tid 0: wait for the chunk after the last gathered one
-            if (tid == 0 && ws < nsub) mbar_wait(&full[wst], wph);
-            adv(ws, wr, wR);
+        int wq = 0, wst = 0, wph = 0;  // next chunk to wait for (tid 0)
+        auto wait_next = [&]() {
+            if (tid == 0 && wq < Q) mbar_wait(&full[wst], wph);
+            ++wq;
             if (++wst == kStages) {
                 wst = 0;
                 wph ^= 1;
             }
         };
-        // register ring slot k: cols, vals, gathered x, x_i of one chunk.
-        // A stage is copied to registers when gathered and released right
-        // after the next round barrier, so the smem ring stays in flight.
+        int gq = 0, gst = 0;  // next chunk to gather
         int32_t cr[kRing][kRPT];
-        double vr[kRing][kRPT], xr[kRing][kRPT], xir[kRing][kRPT];
-        auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT],
-                          double (&xi)[kRPT]) {
+        double vr[kRing][kRPT], xr[kRing][kRPT];
+        int mr[kRing];
+        auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
             const int32_t* sc = s_col(gst) + tid;
             const double* sv = s_val(gst) + tid;
+            mm = __ldg(meta + gq);
 #pragma unroll
             for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
 #pragma unroll
@@ -303,15 +281,8 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                 xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
 #endif
             }
-            if (gr == 0) {
-                const int32_t i0 = R0 + gs * kRows + tid;
-#pragma unroll
-                for (int u = 0; u < kRPT; ++u) {
-                    const int32_t i = i0 + u * kS3Threads;
-                    xi[u] = i < R1 ? __ldg(x + i) : 0.0;
-                }
-            }
-            adv(gs, gr, gR);
+            ++gq;
+            gst = (gst + 1 == kStages) ? 0 : gst + 1;
         };
         // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1 and
         // release their stages
@@ -319,41 +290,35 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
         for (int k = 0; k <= kGD; ++k) wait_next();
         named_bar_sync(1, kS3Threads);
 #pragma unroll
-        for (int k = 0; k < kGD; ++k) {
-            if (gs < nsub) {
-                gather(cr[k], vr[k], xr[k], xir[k]);
-                adv_stage(gst);
-            }
-        }
+        for (int k = 0; k < kGD; ++k)
+            if (gq < Q) gather(cr[k], vr[k], xr[k], mr[k]);
         named_bar_sync(1, kS3Threads);
-        if (tid == 0) {
-            int st = 0;
-            for (int k = 0; k < kGD && k < qtot; ++k) {
-                mbar_arrive(&empty[st]);
-                adv_stage(st);
-            }
-        }
-        int cs = 0, crd = 0, cR = rounds_of(0);  // current chunk
-        int off = 0;                              // ring slot of the sub-tile's row 0
+        if (tid == 0)
+            for (int k = 0; k < kGD && k < Q; ++k) mbar_arrive(&empty[k]);
+        int off = 0;  // ring slot of the current sub-tile's row 0
         int32_t a = R0;
-        double rowsum[kRPT], xi[kRPT];
+        double rowsum[kRPT], xi[kRPT], xin[kRPT];
 #pragma unroll
-        for (int u = 0; u < kRPT; ++u) rowsum[u] = 0.0;
-        bool alive = true;
-        while (alive) {
+        for (int u = 0; u < kRPT; ++u) {
+            rowsum[u] = 0.0;
+            const int32_t i = a + u * kS3Threads + tid;
+            xi[u] = i < R1 ? __ldg(x + i) : 0.0;
+            xin[u] = 0.0;
+        }
+        for (int q = 0; q < Q; q += kRing) {
 #pragma unroll
             for (int k = 0; k < kRing; ++k) {
-                if (alive) {
+                if (q + k < Q) {
                     const int kg = (k + kGD) % kRing;
-                    const bool gathered = gs < nsub;
+                    const bool gathered = gq < Q;
                     const int gst_now = gst;
-                    if (gathered) {
-                        gather(cr[kg], vr[kg], xr[kg], xir[kg]);
-                        adv_stage(gst);
-                    }
-                    if (crd == 0) {
+                    if (gathered) gather(cr[kg], vr[kg], xr[kg], mr[kg]);
+                    if (meta_round(mr[k]) == 0) {  // x_i of the next sub-tile, one sub-tile ahead
 #pragma unroll
-                        for (int u = 0; u < kRPT; ++u) xi[u] = xir[k][u];
+                        for (int u = 0; u < kRPT; ++u) {
+                            const int32_t inext = a + kRows + u * kS3Threads + tid;
+                            xin[u] = inext < R1 ? __ldg(x + inext) : 0.0;
+                        }
                     }
                     double wv[kRPT];
                     int sl[kRPT];
@@ -374,7 +339,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                     wait_next();
                     named_bar_sync(1, kS3Threads);
                     if (tid == 0 && gathered) mbar_arrive(&empty[gst_now]);  // copied out
-                    if (++crd >= cR) {  // sub-tile complete: finalise its rows
+                    if (meta_last(mr[k])) {  // sub-tile complete: finalise its rows
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
                             const int32_t i = a + u * kS3Threads + tid;
@@ -384,14 +349,11 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                                 win[slot] = 0.0;
                             }
                             rowsum[u] = 0.0;
+                            xi[u] = xin[u];
                         }
                         named_bar_sync(1, kS3Threads);
                         off = wrap(off + kRows, W);
                         a += kRows;
-                        crd = 0;
-                        ++cs;
-                        cR = cs < nsub ? rounds_of(cs) : 0;
-                        alive = cs < nsub;
                     }
                 }
             }
@@ -608,6 +570,19 @@ void s3_setup(ktb_plan* p) {
         spill_hi[c] = hi;
     }
     cta_sub[P] = static_cast<int32_t>(sub_rounds.size());
+    // per-block chunk table: one entry per (sub-tile, round), in SELL order
+    std::vector<int32_t> cta_chunk(P + 1, 0), chunk_meta;
+    std::vector<int64_t> cta_base(P, 0);
+    for (int c = 0; c < P; ++c) {
+        cta_chunk[c] = static_cast<int32_t>(chunk_meta.size());
+        cta_base[c] = cta_sub[c] < cta_sub[c + 1] ? sub_base[cta_sub[c]] : 0;
+        for (int sidx = cta_sub[c]; sidx < cta_sub[c + 1]; ++sidx) {
+            const int R = sub_rounds[sidx];
+            for (int r = 0; r < R; ++r)
+                chunk_meta.push_back(((sidx - cta_sub[c]) << 8) | r | (r == R - 1 ? 128 : 0));
+        }
+    }
+    cta_chunk[P] = static_cast<int32_t>(chunk_meta.size());
     L.padded = total_slots;
     L.far = static_cast<int64_t>(far_i.size());
 
@@ -656,9 +631,9 @@ void s3_setup(ktb_plan* p) {
         if (!h.empty())
             KTB_CUDA(cudaMemcpyAsync(d.p, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, st));
     };
-    up32(L.cta_sub, cta_sub);
-    up64(L.sub_base, sub_base);
-    up32(L.sub_rounds, sub_rounds);
+    up32(L.cta_chunk, cta_chunk);
+    up32(L.chunk_meta, chunk_meta);
+    up64(L.cta_base, cta_base);
     up32(L.sell_col, scol);
     upd(L.sell_val, sval);
     up32(L.spill_hi, spill_hi);
@@ -684,8 +659,8 @@ void s3_setup(ktb_plan* p) {
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     k_s3<<<L.ctas, kS3Threads + 32, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
-           p->stream>>>(L.cta_row.p, L.cta_sub.p, L.sub_base.p, L.sub_rounds.p, L.sell_col.p,
-                        L.sell_val.p, x, y, L.window, L.reach, static_cast<int>(p->m->n),
+           p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.sell_col.p, L.sell_val.p,
+                        L.cta_base.p, x, y, L.window, L.reach, static_cast<int>(p->m->n),
                         L.spill_hi.p, L.spill_off.p, L.spill.p);
     KTB_LAUNCH();
     if (L.nsegs) {
