@@ -156,13 +156,12 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 constexpr int kS3Threads = 256;  // consumer threads
 constexpr int kRPT = 4;          // rows per consumer thread
 constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
-constexpr int kStages = 6;       // one round of one sub-tile per stage
-constexpr int kGD = 3;           // gather distance (stages ahead)
-constexpr int kRing = 4;         // register ring slots (>= kGD + 1)
-constexpr int kStageBytes = kRows * (4 + 8);  // 12288
+constexpr int kStages = 8;       // one round of one sub-tile per stage
+constexpr int kGD = 4;           // gather distance (stages ahead)
+constexpr int kRing = 5;         // register ring slots (>= kGD + 1)
+constexpr int kStageBytes = kRows * (2 + 8);  // 10240: int16 rel col + fp64 val
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
-constexpr int kMaxSubCache = 1024;  // sub-tile round counts cached in smem
-constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 4 * kMaxSubCache + 128;
+constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
@@ -175,15 +174,15 @@ __device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
 
 __global__ void __launch_bounds__(kS3Threads + 32, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
-         const int32_t* __restrict__ chunk_meta, const int32_t* __restrict__ scol,
+         const int32_t* __restrict__ chunk_meta, const int16_t* __restrict__ scol,
          const double* __restrict__ sval, const int64_t* __restrict__ cta_base,
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
-    auto s_col = [&](int st) { return reinterpret_cast<int32_t*>(smem + st * kStageBytes); };
-    auto s_val = [&](int st) {
-        return reinterpret_cast<double*>(smem + st * kStageBytes + kRows * 4);
+    auto s_val = [&](int st) { return reinterpret_cast<double*>(smem + st * kStageBytes); };
+    auto s_col = [&](int st) {
+        return reinterpret_cast<int16_t*>(smem + st * kStageBytes + kRows * 8);
     };
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     uint64_t* empty = full + kStages;
@@ -196,7 +195,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
     const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
     const int32_t* meta = chunk_meta + q0;
     // chunk q of this block = kRows contiguous SELL slots at cta_base[c] + q*kRows
-    const int32_t* gcol = scol + cta_base[c];
+    const int16_t* gcol = scol + cta_base[c];
     const double* gval = sval + cta_base[c];
     if (tid == 0) {
         for (int st = 0; st < kStages; ++st) {
@@ -234,7 +233,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                 }
                 if (q >= kStages) mbar_wait(&empty[st], ph ^ 1);
                 mbar_arrive_expect_tx(&full[st], kStageBytes);
-                tma_load_1d(s_col(st), gcol + int64_t(q) * kRows, kRows * 4, &full[st], pol);
+                tma_load_1d(s_col(st), gcol + int64_t(q) * kRows, kRows * 2, &full[st], pol);
                 tma_load_1d(s_val(st), gval + int64_t(q) * kRows, kRows * 8, &full[st], pol);
                 if (++st == kStages) {
                     st = 0;
@@ -262,13 +261,14 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
             }
         };
         int gq = 0, gst = 0;  // next chunk to gather
-        int32_t cr[kRing][kRPT];
+        int32_t cr[kRing][kRPT];  // sub-tile-relative column (-1: padding)
         double vr[kRing][kRPT], xr[kRing][kRPT];
         int mr[kRing];
         auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
-            const int32_t* sc = s_col(gst) + tid;
+            const int16_t* sc = s_col(gst) + tid;
             const double* sv = s_val(gst) + tid;
             mm = __ldg(meta + gq);
+            const double* xa = x + R0 + meta_sub(mm) * kRows;  // x at the chunk's row 0
 #pragma unroll
             for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
 #pragma unroll
@@ -276,9 +276,9 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 #pragma unroll
             for (int u = 0; u < kRPT; ++u) {
 #ifdef KTB_DIAG_NOGATHER
-                xx[u] = cc[u] != -1 ? 1.0 : 0.0;
+                xx[u] = cc[u] >= 0 ? 1.0 : 0.0;
 #else
-                xx[u] = cc[u] != -1 ? __ldg(x + (cc[u] & 0x7fffffff)) : 0.0;
+                xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
 #endif
             }
             ++gq;
@@ -326,8 +326,8 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u) {
                         rowsum[u] += vr[k][u] * xr[k][u];
-                        const int32_t rel = cr[k][u] - a;
-                        sc[u] = cr[k][u] >= 0 && rel != u * kS3Threads + tid;
+                        const int32_t rel = cr[k][u];
+                        sc[u] = rel >= 0 && rel != u * kS3Threads + tid;
                         sl[u] = wrap(rel + off, W);
                         wv[u] = sc[u] ? win[sl[u]] : 0.0;
                     }
@@ -451,7 +451,10 @@ __global__ void k_s3_far(const int32_t* __restrict__ fi, const int32_t* __restri
                          const double* __restrict__ fv, int64_t count,
                          const double* __restrict__ x, double* __restrict__ y) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t < count) atomicAdd(y + fj[t], fv[t] * x[fi[t]]);
+    if (t < count) {  // an out-of-window entry: both of its products
+        atomicAdd(y + fi[t], fv[t] * x[fj[t]]);
+        atomicAdd(y + fj[t], fv[t] * x[fi[t]]);
+    }
 }
 
 void s3_setup(ktb_plan* p) {
@@ -481,7 +484,8 @@ void s3_setup(ktb_plan* p) {
     int max_smem = 0;
     KTB_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                     m->device));
-    const int64_t cap = std::max<int64_t>(S + 32, (max_smem - kS3SmemFixed) / 8);
+    const int64_t cap = std::min<int64_t>(32767,  // int16 relative columns
+                                          std::max<int64_t>(S + 32, (max_smem - kS3SmemFixed) / 8));
     int64_t reach = 0;
     for (int64_t i = 0; i < n; ++i)
         if (rp[i + 1] > rp[i]) reach = std::max<int64_t>(reach, col[rp[i + 1] - 1] - i);
@@ -492,7 +496,7 @@ void s3_setup(ktb_plan* p) {
 
     std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
     std::vector<int64_t> sub_base;
-    std::vector<int32_t> scol;
+    std::vector<int16_t> scol;
     std::vector<double> sval;
     std::vector<int32_t> spill_hi(P), far_i, far_j;
     std::vector<double> far_v;
@@ -544,7 +548,11 @@ void s3_setup(ktb_plan* p) {
                         far_j.push_back(j);
                         far_v.push_back(val[k]);
                     }
-                    assign[t].push_back({r | (far ? 0x10000 : 0), k});
+                    if (far) {  // handled entirely by the far path (row and transposed)
+                        rowmask &= ~(1ull << r);
+                        continue;
+                    }
+                    assign[t].push_back({r, k});
                     R = std::max(R, r + 1);
                 }
             }
@@ -553,16 +561,12 @@ void s3_setup(ktb_plan* p) {
             const int64_t basei = static_cast<int64_t>(scol.size());
             sub_base.push_back(basei);
             sub_rounds.push_back(R);
-            scol.resize(basei + static_cast<int64_t>(R) * S, -1);
+            scol.resize(basei + static_cast<int64_t>(R) * S, int16_t(-1));
             sval.resize(basei + static_cast<int64_t>(R) * S, 0.0);
             for (int32_t t = 0; t < rows; ++t)
-                for (auto [rr, k] : assign[t]) {
-                    const int r = rr & 0xffff;
-                    const bool far = rr & 0x10000;
+                for (auto [r, k] : assign[t]) {
                     const int64_t e = basei + static_cast<int64_t>(r) * S + t;
-                    const int32_t j = col[k];
-                    scol[e] = far ? static_cast<int32_t>(static_cast<uint32_t>(j) | 0x80000000u)
-                                  : j;
+                    scol[e] = static_cast<int16_t>(col[k] - a);  // < W <= 32767
                     sval[e] = val[k];
                 }
             total_slots += static_cast<int64_t>(R) * S;
@@ -634,7 +638,10 @@ void s3_setup(ktb_plan* p) {
     up32(L.cta_chunk, cta_chunk);
     up32(L.chunk_meta, chunk_meta);
     up64(L.cta_base, cta_base);
-    up32(L.sell_col, scol);
+    L.sell_col.alloc(std::max<size_t>(scol.size(), 1));
+    if (!scol.empty())
+        KTB_CUDA(cudaMemcpyAsync(L.sell_col.p, scol.data(), 2 * scol.size(),
+                                 cudaMemcpyHostToDevice, st));
     upd(L.sell_val, sval);
     up32(L.spill_hi, spill_hi);
     up64(L.spill_off, spill_off);
@@ -653,7 +660,9 @@ void s3_setup(ktb_plan* p) {
     p->ctas = P;
     p->launches = 1 + (L.nsegs ? 1 : 0) + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
-    p->extra_bytes = (total_slots - nnz) * 12 + so * 8 * 2 + so * 8 * 2;
+    // SELL stream (10 B/slot incl. padding) vs the 12 B/nnz model, + spill
+    // write/read + head-row read-modify-write in the fixup; row_ptr unused
+    p->extra_bytes = total_slots * 10 - nnz * 12 - 4 * (n + 1) + so * 8 * 2 + so * 8 * 2;
 }
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
