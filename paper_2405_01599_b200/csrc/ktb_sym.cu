@@ -153,15 +153,14 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // The part of each block's region beyond the block (the spill) goes to a
 // global buffer; k_s3_fixup adds it into the next blocks' head rows in
 // ascending source order, so the result is deterministic.
-constexpr int kS3Threads = 256;  // consumer threads
-constexpr int kRPT = 4;          // rows per consumer thread
+constexpr int kS3Threads = 256;  // threads per block (one block per SM)
+constexpr int kRPT = 4;          // rows per thread
 constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
-constexpr int kStages = 8;       // one round of one sub-tile per stage
-constexpr int kGD = 4;           // gather distance (stages ahead)
-constexpr int kRing = 5;         // register ring slots (>= kGD + 1)
-constexpr int kStageBytes = kRows * (2 + 8);  // 10240: int16 rel col + fp64 val
+constexpr int kRS = 6;           // register ring slots (one round-chunk each)
+constexpr int kLD = kRS - 1;     // SELL loads issued kLD rounds ahead
+constexpr int kGX = 3;           // x gathers issued kGX rounds ahead (< kLD)
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
-constexpr int kS3SmemFixed = kStages * kStageBytes + 2 * kStages * 8 + 128;
+constexpr int kS3SmemFixed = 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
@@ -172,7 +171,27 @@ __device__ __forceinline__ int meta_round(int m) { return m & 127; }
 __device__ __forceinline__ bool meta_last(int m) { return (m >> 7) & 1; }
 __device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
 
-__global__ void __launch_bounds__(kS3Threads + 32, 1)
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int ld_stream_s16(const int16_t* p, uint64_t pol) {
+    short r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s16 %0, [%1], %2;"
+                 : "=h"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+// One block per SM owns an NNZ_BALANCED row block. The SELL stream of the
+// block is a sequence of round-chunks (kRows slots each: int16 column
+// relative to the sub-tile's first row, fp64 value). Every thread keeps a
+// kRS-deep register ring: loads for chunk q+kLD and x gathers for chunk
+// q+kGX are issued while chunk q's round runs, so ~kLD rounds of the stream
+// are in flight per SM without any shared-memory staging; shared memory
+// holds only the window ring.
+__global__ void __launch_bounds__(kS3Threads, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
          const int32_t* __restrict__ chunk_meta, const int16_t* __restrict__ scol,
          const double* __restrict__ sval, const int64_t* __restrict__ cta_base,
@@ -180,121 +199,57 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
-    auto s_val = [&](int st) { return reinterpret_cast<double*>(smem + st * kStageBytes); };
-    auto s_col = [&](int st) {
-        return reinterpret_cast<int16_t*>(smem + st * kStageBytes + kRows * 8);
-    };
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty = full + kStages;
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
-
     const int tid = threadIdx.x;
     const int c = blockIdx.x;
     const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
     const int q0 = cta_chunk[c];
     const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
     const int32_t* meta = chunk_meta + q0;
-    // chunk q of this block = kRows contiguous SELL slots at cta_base[c] + q*kRows
-    const int16_t* gcol = scol + cta_base[c];
-    const double* gval = sval + cta_base[c];
-    if (tid == 0) {
-        for (int st = 0; st < kStages; ++st) {
-            mbar_init(&full[st], 1);
-            mbar_init(&empty[st], 1);
+    const int16_t* gcol = scol + cta_base[c] + tid;
+    const double* gval = sval + cta_base[c] + tid;
+    for (int k = tid; k < W; k += kS3Threads) win[k] = 0.0;
+    // x is first touched by the far reach of the window: thread 0 pulls the
+    // initial window and then each sub-tile's new front into L2 ahead of the
+    // gathers (the bench flushes L2 between steps).
+    constexpr int kAhead = 2;  // sub-tiles of look-ahead
+    auto pf = [&](int64_t lo, int64_t hi) {
+        lo = max(lo & ~int64_t(1), int64_t(0));
+        hi = min(hi, int64_t(n));
+        if (hi > lo) {
+            const int64_t cnt = ((hi - lo) + 1) & ~int64_t(1);
+            prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
         }
-        fence_mbar_init();
-    }
-    for (int k = tid; k < W; k += blockDim.x) win[k] = 0.0;
+    };
+    if (tid == 0 && Q > 0) pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
     __syncthreads();
 
-    if (tid >= kS3Threads) {  // ---------------- producer warp
-        if (tid == kS3Threads && Q > 0) {
-            const uint64_t pol = policy_evict_first();
-            // x is first touched by the far reach of the window: pull the
-            // initial window and then each sub-tile's new front into L2 ahead
-            // of the consumers' gathers (the bench flushes L2 between steps).
-            constexpr int kAhead = 2;  // sub-tiles of look-ahead
-            auto pf = [&](int64_t lo, int64_t hi) {
-                lo = max(lo & ~int64_t(1), int64_t(0));
-                hi = min(hi, int64_t(n));
-                if (hi > lo) {
-                    const int64_t cnt = ((hi - lo) + 1) & ~int64_t(1);
-                    prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
-                }
-            };
-            pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
-            int st = 0, ph = 0;
-            for (int q = 0; q < Q; ++q) {
-                const int m = __ldg(meta + q);
-                if (meta_round(m) == 0) {
-                    const int64_t front =
-                        int64_t(R0) + int64_t(meta_sub(m) + kAhead + 1) * kRows + reach;
-                    pf(front, front + kRows);
-                }
-                if (q >= kStages) mbar_wait(&empty[st], ph ^ 1);
-                mbar_arrive_expect_tx(&full[st], kStageBytes);
-                tma_load_1d(s_col(st), gcol + int64_t(q) * kRows, kRows * 2, &full[st], pol);
-                tma_load_1d(s_val(st), gval + int64_t(q) * kRows, kRows * 8, &full[st], pol);
-                if (++st == kStages) {
-                    st = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-        return;
-    }
-
-    // ---------------------------------------------------- consumers
-    // Only consumer thread 0 waits on the stage mbarriers, one chunk ahead;
-    // the per-round named barrier publishes the landed stage to all
-    // consumers. A stage is copied to registers when gathered and released
-    // right after the next barrier, so the smem ring stays in flight.
     if (Q > 0) {
+        const uint64_t pol = policy_evict_first();
         const uint64_t keep = policy_evict_last();  // y head rows are re-read by the fixup
-        int wq = 0, wst = 0, wph = 0;  // next chunk to wait for (tid 0)
-        auto wait_next = [&]() {
-            if (tid == 0 && wq < Q) mbar_wait(&full[wst], wph);
-            ++wq;
-            if (++wst == kStages) {
-                wst = 0;
-                wph ^= 1;
-            }
+        int cr[kRS][kRPT];  // sub-tile-relative column (-1: padding)
+        double vr[kRS][kRPT], xr[kRS][kRPT];
+        int mr[kRS];
+        auto load = [&](int qq, int (&cc)[kRPT], double (&vv)[kRPT], int& mm) {
+            mm = __ldg(meta + qq);
+            const int64_t e = int64_t(qq) * kRows;
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u) cc[u] = ld_stream_s16(gcol + e + u * kS3Threads, pol);
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u) vv[u] = ld_stream_f64(gval + e + u * kS3Threads, pol);
         };
-        int gq = 0, gst = 0;  // next chunk to gather
-        int32_t cr[kRing][kRPT];  // sub-tile-relative column (-1: padding)
-        double vr[kRing][kRPT], xr[kRing][kRPT];
-        int mr[kRing];
-        auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
-            const int16_t* sc = s_col(gst) + tid;
-            const double* sv = s_val(gst) + tid;
-            mm = __ldg(meta + gq);
+        auto gather = [&](const int (&cc)[kRPT], int mm, double (&xx)[kRPT]) {
             const double* xa = x + R0 + meta_sub(mm) * kRows;  // x at the chunk's row 0
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
-#pragma unroll
-            for (int u = 0; u < kRPT; ++u) vv[u] = sv[u * kS3Threads];
-#pragma unroll
-            for (int u = 0; u < kRPT; ++u) {
-#ifdef KTB_DIAG_NOGATHER
-                xx[u] = cc[u] >= 0 ? 1.0 : 0.0;
-#else
-                xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
-#endif
-            }
-            ++gq;
-            gst = (gst + 1 == kStages) ? 0 : gst + 1;
+            for (int u = 0; u < kRPT; ++u) xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
         };
-        // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1 and
-        // release their stages
+        // prologue: loads for chunks 0..kLD-1, gathers for chunks 0..kGX-1
 #pragma unroll
-        for (int k = 0; k <= kGD; ++k) wait_next();
-        named_bar_sync(1, kS3Threads);
+        for (int k = 0; k < kLD; ++k)
+            if (k < Q) load(k, cr[k], vr[k], mr[k]);
 #pragma unroll
-        for (int k = 0; k < kGD; ++k)
-            if (gq < Q) gather(cr[k], vr[k], xr[k], mr[k]);
-        named_bar_sync(1, kS3Threads);
-        if (tid == 0)
-            for (int k = 0; k < kGD && k < Q; ++k) mbar_arrive(&empty[k]);
+        for (int k = 0; k < kGX; ++k)
+            if (k < Q) gather(cr[k], mr[k], xr[k]);
         int off = 0;  // ring slot of the current sub-tile's row 0
         int32_t a = R0;
         double rowsum[kRPT], xi[kRPT], xin[kRPT];
@@ -305,19 +260,30 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
             xi[u] = i < R1 ? __ldg(x + i) : 0.0;
             xin[u] = 0.0;
         }
-        for (int q = 0; q < Q; q += kRing) {
+        for (int q = 0; q < Q; q += kRS) {
 #pragma unroll
-            for (int k = 0; k < kRing; ++k) {
+            for (int k = 0; k < kRS; ++k) {
                 if (q + k < Q) {
-                    const int kg = (k + kGD) % kRing;
-                    const bool gathered = gq < Q;
-                    const int gst_now = gst;
-                    if (gathered) gather(cr[kg], vr[kg], xr[kg], mr[kg]);
-                    if (meta_round(mr[k]) == 0) {  // x_i of the next sub-tile, one sub-tile ahead
+                    const int qq = q + k;
+                    if (qq + kLD < Q) {
+                        const int kl = (k + kLD) % kRS;
+                        load(qq + kLD, cr[kl], vr[kl], mr[kl]);
+                    }
+                    if (qq + kGX < Q) {
+                        const int kx = (k + kGX) % kRS;
+                        gather(cr[kx], mr[kx], xr[kx]);
+                    }
+                    const int m = mr[k];
+                    if (meta_round(m) == 0) {  // new sub-tile: x_i of the next one, and x front
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
                             const int32_t inext = a + kRows + u * kS3Threads + tid;
                             xin[u] = inext < R1 ? __ldg(x + inext) : 0.0;
+                        }
+                        if (tid == 0) {
+                            const int64_t front =
+                                int64_t(a) + int64_t(kAhead + 1) * kRows + reach;
+                            pf(front, front + kRows);
                         }
                     }
                     double wv[kRPT];
@@ -326,20 +292,16 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u) {
                         rowsum[u] += vr[k][u] * xr[k][u];
-                        const int32_t rel = cr[k][u];
+                        const int rel = cr[k][u];
                         sc[u] = rel >= 0 && rel != u * kS3Threads + tid;
                         sl[u] = wrap(rel + off, W);
                         wv[u] = sc[u] ? win[sl[u]] : 0.0;
                     }
-#ifndef KTB_DIAG_NORMW
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u)
                         if (sc[u]) win[sl[u]] = wv[u] + vr[k][u] * xi[u];
-#endif
-                    wait_next();
-                    named_bar_sync(1, kS3Threads);
-                    if (tid == 0 && gathered) mbar_arrive(&empty[gst_now]);  // copied out
-                    if (meta_last(mr[k])) {  // sub-tile complete: finalise its rows
+                    __syncthreads();
+                    if (meta_last(m)) {  // sub-tile complete: finalise its rows
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
                             const int32_t i = a + u * kS3Threads + tid;
@@ -351,7 +313,7 @@ __global__ void __launch_bounds__(kS3Threads + 32, 1)
                             rowsum[u] = 0.0;
                             xi[u] = xin[u];
                         }
-                        named_bar_sync(1, kS3Threads);
+                        __syncthreads();
                         off = wrap(off + kRows, W);
                         a += kRows;
                     }
@@ -667,7 +629,7 @@ void s3_setup(ktb_plan* p) {
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
-    k_s3<<<L.ctas, kS3Threads + 32, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
+    k_s3<<<L.ctas, kS3Threads, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
            p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.sell_col.p, L.sell_val.p,
                         L.cta_base.p, x, y, L.window, L.reach, static_cast<int>(p->m->n),
                         L.spill_hi.p, L.spill_off.p, L.spill.p);
