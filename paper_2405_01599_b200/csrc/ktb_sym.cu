@@ -159,6 +159,7 @@ constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
 constexpr int kRS = 6;           // register ring slots (one round-chunk each)
 constexpr int kLD = kRS - 1;     // SELL loads issued kLD rounds ahead
 constexpr int kGX = 3;           // x gathers issued kGX rounds ahead (< kLD)
+constexpr int kPF = 16;          // SELL chunks bulk-prefetched into L2 ahead
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 constexpr int kS3SmemFixed = 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
@@ -221,7 +222,20 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
         }
     };
-    if (tid == 0 && Q > 0) pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
+    // the SELL stream itself is pulled into L2 kPF chunks ahead so that the
+    // register-ring loads (kLD rounds ahead) hit L2
+    const int16_t* pcol = scol + cta_base[c];
+    const double* pval = sval + cta_base[c];
+    auto pf_chunk = [&](int qq) {
+        if (qq < Q) {
+            prefetch_l2_bulk(pcol + int64_t(qq) * kRows, kRows * 2);
+            prefetch_l2_bulk(pval + int64_t(qq) * kRows, kRows * 8);
+        }
+    };
+    if (tid == 0 && Q > 0) {
+        pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
+        for (int k = 0; k < kPF; ++k) pf_chunk(k);
+    }
     __syncthreads();
 
     if (Q > 0) {
@@ -273,6 +287,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                         const int kx = (k + kGX) % kRS;
                         gather(cr[kx], mr[kx], xr[kx]);
                     }
+                    if (tid == 32) pf_chunk(qq + kPF);
                     const int m = mr[k];
                     if (meta_round(m) == 0) {  // new sub-tile: x_i of the next one, and x front
 #pragma unroll
