@@ -153,15 +153,24 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // The part of each block's region beyond the block (the spill) goes to a
 // global buffer; k_s3_fixup adds it into the next blocks' head rows in
 // ascending source order, so the result is deterministic.
-constexpr int kS3Threads = 256;  // threads per block (one block per SM)
-constexpr int kRPT = 4;          // rows per thread
+constexpr int kS3Threads = 256;  // consumer threads
+#ifndef KTB_S3_RPT
+#define KTB_S3_RPT 8
+#endif
+constexpr int kRPT = KTB_S3_RPT;  // rows per consumer thread
 constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
-constexpr int kRS = 6;           // register ring slots (one round-chunk each)
-constexpr int kLD = kRS - 1;     // SELL loads issued kLD rounds ahead
-constexpr int kGX = 3;           // x gathers issued kGX rounds ahead (< kLD)
-constexpr int kPF = 16;          // SELL chunks bulk-prefetched into L2 ahead
+#ifndef KTB_S3_STAGES
+#define KTB_S3_STAGES 4
+#endif
+#ifndef KTB_S3_GD
+#define KTB_S3_GD 2
+#endif
+constexpr int kStages = KTB_S3_STAGES;  // one round of one sub-tile per stage
+constexpr int kGD = KTB_S3_GD;   // gather distance (stages ahead)
+constexpr int kRing = KTB_S3_GD + 1;  // register ring slots
+constexpr int kStageBytes = kRows * (2 + 8);  // 10240: int16 rel col + fp64 val
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
-constexpr int kS3SmemFixed = 128;
+constexpr int kS3SmemFixed = kStages * kStageBytes + kStages * 8 + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
 __device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
@@ -172,26 +181,12 @@ __device__ __forceinline__ int meta_round(int m) { return m & 127; }
 __device__ __forceinline__ bool meta_last(int m) { return (m >> 7) & 1; }
 __device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
 
-__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
-    double r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-                 : "=d"(r) : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ int ld_stream_s16(const int16_t* p, uint64_t pol) {
-    short r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s16 %0, [%1], %2;"
-                 : "=h"(r) : "l"(p), "l"(pol));
-    return r;
-}
-
-// One block per SM owns an NNZ_BALANCED row block. The SELL stream of the
-// block is a sequence of round-chunks (kRows slots each: int16 column
-// relative to the sub-tile's first row, fp64 value). Every thread keeps a
-// kRS-deep register ring: loads for chunk q+kLD and x gathers for chunk
-// q+kGX are issued while chunk q's round runs, so ~kLD rounds of the stream
-// are in flight per SM without any shared-memory staging; shared memory
-// holds only the window ring.
+// One block of kS3Threads consumer threads per SM (no producer warp, so
+// the full 255-register budget is available). Consumer thread 0 drives the
+// TMA ring: it issues the first kStages chunks, waits for chunk q+kGD+1
+// before each round barrier (the barrier then publishes the landed stage to
+// everyone), and re-issues a stage's next chunk as soon as the stage has been
+// copied into registers.
 __global__ void __launch_bounds__(kS3Threads, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
          const int32_t* __restrict__ chunk_meta, const int16_t* __restrict__ scol,
@@ -200,19 +195,31 @@ __global__ void __launch_bounds__(kS3Threads, 1)
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
+    auto s_val = [&](int st) { return reinterpret_cast<double*>(smem + st * kStageBytes); };
+    auto s_col = [&](int st) {
+        return reinterpret_cast<int16_t*>(smem + st * kStageBytes + kRows * 8);
+    };
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
+
     const int tid = threadIdx.x;
     const int c = blockIdx.x;
     const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
     const int q0 = cta_chunk[c];
     const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
     const int32_t* meta = chunk_meta + q0;
-    const int16_t* gcol = scol + cta_base[c] + tid;
-    const double* gval = sval + cta_base[c] + tid;
-    for (int k = tid; k < W; k += kS3Threads) win[k] = 0.0;
-    // x is first touched by the far reach of the window: thread 0 pulls the
-    // initial window and then each sub-tile's new front into L2 ahead of the
-    // gathers (the bench flushes L2 between steps).
+    // chunk q of this block = kRows contiguous SELL slots at cta_base[c] + q*kRows
+    const int16_t* gcol = scol + cta_base[c];
+    const double* gval = sval + cta_base[c];
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int qq, int st) {  // thread 0 only
+        mbar_arrive_expect_tx(&full[st], kStageBytes);
+        tma_load_1d(s_col(st), gcol + int64_t(qq) * kRows, kRows * 2, &full[st], pol);
+        tma_load_1d(s_val(st), gval + int64_t(qq) * kRows, kRows * 8, &full[st], pol);
+    };
+    // x is first touched by the far reach of the window: pull the initial
+    // window and then each sub-tile's new front into L2 ahead of the gathers
+    // (the bench flushes L2 between steps).
     constexpr int kAhead = 2;  // sub-tiles of look-ahead
     auto pf = [&](int64_t lo, int64_t hi) {
         lo = max(lo & ~int64_t(1), int64_t(0));
@@ -222,48 +229,71 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
         }
     };
-    // the SELL stream itself is pulled into L2 kPF chunks ahead so that the
-    // register-ring loads (kLD rounds ahead) hit L2
-    const int16_t* pcol = scol + cta_base[c];
-    const double* pval = sval + cta_base[c];
-    auto pf_chunk = [&](int qq) {
-        if (qq < Q) {
-            prefetch_l2_bulk(pcol + int64_t(qq) * kRows, kRows * 2);
-            prefetch_l2_bulk(pval + int64_t(qq) * kRows, kRows * 8);
+    if (tid == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
+        fence_mbar_init();
+        if (Q > 0) {
+            for (int k = 0; k < kStages && k < Q; ++k) issue(k, k);
+            pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
         }
-    };
-    if (tid == 0 && Q > 0) {
-        pf(R0, int64_t(R0) + kRows * (kAhead + 1) + reach);
-        for (int k = 0; k < kPF; ++k) pf_chunk(k);
     }
+    for (int k = tid; k < W; k += kS3Threads) win[k] = 0.0;
     __syncthreads();
 
     if (Q > 0) {
-        const uint64_t pol = policy_evict_first();
         const uint64_t keep = policy_evict_last();  // y head rows are re-read by the fixup
-        int cr[kRS][kRPT];  // sub-tile-relative column (-1: padding)
-        double vr[kRS][kRPT], xr[kRS][kRPT];
-        int mr[kRS];
-        auto load = [&](int qq, int (&cc)[kRPT], double (&vv)[kRPT], int& mm) {
-            mm = __ldg(meta + qq);
-            const int64_t e = int64_t(qq) * kRows;
-#pragma unroll
-            for (int u = 0; u < kRPT; ++u) cc[u] = ld_stream_s16(gcol + e + u * kS3Threads, pol);
-#pragma unroll
-            for (int u = 0; u < kRPT; ++u) vv[u] = ld_stream_f64(gval + e + u * kS3Threads, pol);
+        int wq = 0, wst = 0, wph = 0;  // next chunk to wait for (tid 0)
+        auto wait_next = [&]() {
+            if (tid == 0 && wq < Q) mbar_wait(&full[wst], wph);
+            ++wq;
+            if (++wst == kStages) {
+                wst = 0;
+                wph ^= 1;
+            }
         };
-        auto gather = [&](const int (&cc)[kRPT], int mm, double (&xx)[kRPT]) {
+        int gq = 0, gst = 0;  // next chunk to gather
+        int32_t cr[kRing][kRPT];  // sub-tile-relative column (-1: padding)
+        double vr[kRing][kRPT], xr[kRing][kRPT];
+        int mr[kRing];
+        auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
+            const int16_t* sc = s_col(gst) + tid;
+            const double* sv = s_val(gst) + tid;
+            mm = __ldg(meta + gq);
             const double* xa = x + R0 + meta_sub(mm) * kRows;  // x at the chunk's row 0
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u) xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
+            for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u) vv[u] = sv[u * kS3Threads];
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u) {
+#ifdef KTB_DIAG_NOGATHER
+                xx[u] = cc[u] >= 0 ? 1.0 : 0.0;
+#else
+                xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
+#endif
+            }
+            ++gq;
+            gst = (gst + 1 == kStages) ? 0 : gst + 1;
         };
-        // prologue: loads for chunks 0..kLD-1, gathers for chunks 0..kGX-1
+        // refill a stage that has just been copied out with the chunk
+        // kStages further on
+        auto refill = [&](int chunk_done, int st) {
+            if (tid == 0 && chunk_done + kStages < Q) {
+                fence_proxy_async_smem();
+                issue(chunk_done + kStages, st);
+            }
+        };
+        // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1
 #pragma unroll
-        for (int k = 0; k < kLD; ++k)
-            if (k < Q) load(k, cr[k], vr[k], mr[k]);
+        for (int k = 0; k <= kGD; ++k) wait_next();
+        __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kGX; ++k)
-            if (k < Q) gather(cr[k], mr[k], xr[k]);
+        for (int k = 0; k < kGD; ++k)
+            if (gq < Q) gather(cr[k], vr[k], xr[k], mr[k]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kGD; ++k)
+            if (k < Q) refill(k, k % kStages);
         int off = 0;  // ring slot of the current sub-tile's row 0
         int32_t a = R0;
         double rowsum[kRPT], xi[kRPT], xin[kRPT];
@@ -274,30 +304,23 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             xi[u] = i < R1 ? __ldg(x + i) : 0.0;
             xin[u] = 0.0;
         }
-        for (int q = 0; q < Q; q += kRS) {
+        for (int q = 0; q < Q; q += kRing) {
 #pragma unroll
-            for (int k = 0; k < kRS; ++k) {
+            for (int k = 0; k < kRing; ++k) {
                 if (q + k < Q) {
-                    const int qq = q + k;
-                    if (qq + kLD < Q) {
-                        const int kl = (k + kLD) % kRS;
-                        load(qq + kLD, cr[kl], vr[kl], mr[kl]);
-                    }
-                    if (qq + kGX < Q) {
-                        const int kx = (k + kGX) % kRS;
-                        gather(cr[kx], mr[kx], xr[kx]);
-                    }
-                    if (tid == 32) pf_chunk(qq + kPF);
+                    const int kg = (k + kGD) % kRing;
+                    const bool gathered = gq < Q;
+                    const int gq_now = gq, gst_now = gst;
+                    if (gathered) gather(cr[kg], vr[kg], xr[kg], mr[kg]);
                     const int m = mr[k];
-                    if (meta_round(m) == 0) {  // new sub-tile: x_i of the next one, and x front
+                    if (meta_round(m) == 0) {  // x_i of the next sub-tile, and the x front
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
                             const int32_t inext = a + kRows + u * kS3Threads + tid;
                             xin[u] = inext < R1 ? __ldg(x + inext) : 0.0;
                         }
                         if (tid == 0) {
-                            const int64_t front =
-                                int64_t(a) + int64_t(kAhead + 1) * kRows + reach;
+                            const int64_t front = int64_t(a) + int64_t(kAhead + 1) * kRows + reach;
                             pf(front, front + kRows);
                         }
                     }
@@ -307,7 +330,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u) {
                         rowsum[u] += vr[k][u] * xr[k][u];
-                        const int rel = cr[k][u];
+                        const int32_t rel = cr[k][u];
                         sc[u] = rel >= 0 && rel != u * kS3Threads + tid;
                         sl[u] = wrap(rel + off, W);
                         wv[u] = sc[u] ? win[sl[u]] : 0.0;
@@ -315,7 +338,9 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u)
                         if (sc[u]) win[sl[u]] = wv[u] + vr[k][u] * xi[u];
+                    wait_next();
                     __syncthreads();
+                    if (gathered) refill(gq_now, gst_now);
                     if (meta_last(m)) {  // sub-tile complete: finalise its rows
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
