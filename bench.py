@@ -37,11 +37,23 @@ METRIC = "SpMV GB/s (% of HBM peak) & GFLOP/s at 1/2/4/8 B200 vs host-CPU refere
 
 CONFIGS = {
     1: dict(workload="cfg1: 64^3 7-pt Laplacian, full CRS (n=262,144, nnz=1,810,432)",
-            dims=(64, 64, 64), sym=False, seed=1),
+            sym=False, seed=1,
+            gpu=lambda K, dev: K.stencil7(64, 64, 64, device=dev),
+            host=lambda M: M.stencil7(64, 64, 64), sample="the full matrix"),
     2: dict(workload="cfg2: 128^3 27-pt stencil, symmetric upper CRS "
-                     "(n=2,097,152, nnz_s=28,920,060)", dims=(128, 128, 128), sym=True, seed=2),
+                     "(n=2,097,152, nnz_s=28,920,060)", sym=True, seed=2,
+            gpu=lambda K, dev: K.stencil27_upper(128, 128, 128, device=dev),
+            host=lambda M: M.stencil27_upper(128, 128, 128), sample="the full matrix"),
+    3: dict(workload="cfg3: power-law, n=4,000,000, 10% empty rows, Pareto(1.5) lengths <= 65,536, "
+                     "nnz=39,552,727 (DESIGN.md recipe, seed 3)", sym=False, seed=3,
+            gpu=lambda K, dev: K.powerlaw(device=dev),
+            host=lambda M: M.powerlaw(), sample="the full matrix"),
     4: dict(workload="cfg4: 512^3 7-pt Laplacian, full CRS (n=134,217,728, nnz=937,951,232), "
-                     "single GPU", dims=(512, 512, 512), sym=False, seed=4),
+                     "single GPU", sym=False, seed=4,
+            gpu=lambda K, dev: K.stencil7(512, 512, 512, device=dev),
+            host=lambda M: M.stencil7(512, 512, 64),
+            sample="a 512x512x64 slab of the 512^3 7-pt matrix (1/8 of the rows; GB/s is "
+                   "size-intensive)"),
 }
 
 
@@ -140,11 +152,7 @@ def cpu_reference_engine(cfg: dict):
     import matgen
     from oracle import oracle as O
 
-    dims = cfg["dims"]
-    if cfg["sym"]:
-        n, rp, ci, v = matgen.stencil27_upper(*dims)
-    else:
-        n, rp, ci, v = matgen.stencil7(*dims)
+    n, rp, ci, v = cfg["host"](matgen)
     cores = os.cpu_count() or 1
     eng = O.RefEngine(cfg["sym"], n, rp, ci, v, cores)
     x = O.Ref.seeded_vector(n, cfg["seed"])
@@ -195,7 +203,7 @@ def run_reference(args, cfg):
         "impl": "reference",
         "gflops": flops(n, nnz, cfg["sym"]) / t / 1e9,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} applies of the full {cfg['workload']} through "
+                         "sample": f"{args.steps} applies of {cfg['sample']} ({cfg['workload']}) through "
                                    f"the reference's tuned engine ({eng.selected['name']}, "
                                    f"{eng.selected['workers']} OpenMP workers)"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -225,8 +233,7 @@ def run_gpu(args, cfg):
     from paper_2405_01599_b200 import _lib
     from paper_2405_01599_b200 import ktune as K
 
-    dims = cfg["dims"]
-    a = K.stencil27_upper(*dims, device=local) if cfg["sym"] else K.stencil7(*dims, device=local)
+    a = cfg["gpu"](K, local)
     n, nnz = a.n, a.nnz()
     B = min_bytes(n, nnz)
     F = flops(n, nnz, cfg["sym"])
@@ -362,7 +369,7 @@ def cpu_baseline(cfg):
         t, reps, _ = time_cpu(eng, x, n)
         return {"value": min_bytes(n, nnz) / t / 1e9, "unit": "GB/s", "cores": cores,
                 "kind": "reference",
-                "sample": f"{reps} applies ({reps * t:.1f} s) of the full {cfg['workload']} "
+                "sample": f"{reps} applies ({reps * t:.1f} s) of {cfg['sample']} ({cfg['workload']}) "
                           f"through the reference's tuned engine ({eng.selected['name']}, "
                           f"{eng.selected['workers']} OpenMP workers)",
                 "ms_per_apply": t * 1e3}

@@ -83,6 +83,17 @@ int ktb_gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, dou
  * (config 4 sharding). has_lo/has_hi are 0 on end ranks. */
 int ktb_gen_stencil7_slab(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t z1,
                           double diag, double off, int device, ktb_matrix** out);
+/* Irregular power-law matrix of config 3 (recipe in DESIGN.md, counter-based
+ * splitmix64 streams: bit-identical for any thread count and in
+ * tests/matgen.py): n rows, empty_frac empty rows, Pareto(1.5) row lengths
+ * scaled to ~target_nnz, capped at max_len, distinct sorted uniform columns,
+ * values U[-1,1). Built on the host with all cores, uploaded to `device`. */
+int ktb_gen_powerlaw(int64_t n, uint64_t seed, int64_t target_nnz, double empty_frac,
+                     int64_t max_len, int device, ktb_matrix** out);
+/* Host-only form (no GPU needed). row_ptr has n+1 entries; when col/val are
+ * NULL only row_ptr is produced (size query: nnz = row_ptr[n]). */
+int ktb_gen_powerlaw_host(int64_t n, uint64_t seed, int64_t target_nnz, double empty_frac,
+                          int64_t max_len, int64_t* row_ptr, int32_t* col, double* val);
 /* lanczos.hpp:17-29 detail::seeded_vector (splitmix64 -> U[-1,1)), written
  * to a device buffer, element i = value of stream position offset+i. */
 int ktb_seeded_vector(int64_t n, uint64_t seed, int64_t offset, double* d_out, void* stream);

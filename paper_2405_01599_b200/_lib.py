@@ -44,6 +44,9 @@ def load() -> C.CDLL:
         "ktb_gen_stencil7_slab": ([I64, I64, I64, I64, I64, C.c_double, C.c_double, C.c_int,
                                    C.POINTER(VP)], C.c_int),
         "ktb_seeded_vector": ([I64, C.c_uint64, I64, VP, VP], C.c_int),
+        "ktb_gen_powerlaw": ([I64, C.c_uint64, I64, C.c_double, I64, C.c_int, C.POINTER(VP)],
+                             C.c_int),
+        "ktb_gen_powerlaw_host": ([I64, C.c_uint64, I64, C.c_double, I64, VP, VP, VP], C.c_int),
         "ktb_row_partition": ([VP, C.c_int, C.c_int, VP], C.c_int),
         "ktb_reduction_regions": ([VP, C.c_int, VP, VP, VP], C.c_int),
         "ktb_bss_plan_size": ([VP, I64, C.POINTER(I64), C.POINTER(I64)], C.c_int),

@@ -34,6 +34,11 @@ ktb_matrix* gen_stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t
 ktb_matrix* gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
                                 int device);
 void seeded_vector_dev(int64_t n, uint64_t seed, int64_t offset, double* d_out, cudaStream_t s);
+ktb_matrix* gen_powerlaw(int64_t n, uint64_t seed, int64_t target, double empty_frac,
+                         int64_t max_len, int device);
+void powerlaw_host(int64_t n, uint64_t seed, int64_t target, double empty_frac,
+                   int64_t max_len, std::vector<int64_t>& rp, std::vector<int32_t>* col,
+                   std::vector<double>* val);
 
 namespace {
 thread_local std::string g_err;
@@ -234,6 +239,27 @@ int ktb_gen_stencil7_slab(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_
                           double diag, double off, int device, ktb_matrix** out) {
     return guarded(
         [&] { *out = gen_stencil7(nx, ny, nz, z0, z1, true, diag, off, off, off, device); });
+}
+
+int ktb_gen_powerlaw(int64_t n, uint64_t seed, int64_t target_nnz, double empty_frac,
+                     int64_t max_len, int device, ktb_matrix** out) {
+    return guarded([&] { *out = gen_powerlaw(n, seed, target_nnz, empty_frac, max_len, device); });
+}
+
+int ktb_gen_powerlaw_host(int64_t n, uint64_t seed, int64_t target_nnz, double empty_frac,
+                          int64_t max_len, int64_t* row_ptr, int32_t* col, double* val) {
+    return guarded([&] {
+        std::vector<int64_t> rp;
+        std::vector<int32_t> c;
+        std::vector<double> v;
+        powerlaw_host(n, seed, target_nnz, empty_frac, max_len, rp, col ? &c : nullptr,
+                      col ? &v : nullptr);
+        std::copy(rp.begin(), rp.end(), row_ptr);
+        if (col) {
+            std::copy(c.begin(), c.end(), col);
+            std::copy(v.begin(), v.end(), val);
+        }
+    });
 }
 
 int ktb_seeded_vector(int64_t n, uint64_t seed, int64_t offset, double* d_out, void* stream) {

@@ -215,6 +215,29 @@ def stencil27_upper(nx, ny, nz, diag=26.0, off=-1.0, device=0) -> DeviceCsr:
     return DeviceCsr(h, True)
 
 
+def powerlaw(n=4_000_000, seed=3, target_nnz=40_000_000, empty_frac=0.1, max_len=65536,
+             device=0) -> DeviceCsr:
+    """Config 3 (BASELINE.json configs[2]): irregular power-law matrix."""
+    h = C.c_void_p()
+    _check(_lib.load().ktb_gen_powerlaw(n, seed, target_nnz, empty_frac, max_len, device,
+                                        C.byref(h)))
+    return DeviceCsr(h, False)
+
+
+def powerlaw_host(n=4_000_000, seed=3, target_nnz=40_000_000, empty_frac=0.1, max_len=65536):
+    """Host arrays of the same matrix (int64 row_ptr, int64 cols, fp64 values)."""
+    L = _lib.load()
+    rp = np.empty(n + 1, np.int64)
+    _check(L.ktb_gen_powerlaw_host(n, seed, target_nnz, empty_frac, max_len, rp.ctypes.data,
+                                   None, None))
+    nnz = int(rp[-1])
+    ci = np.empty(max(nnz, 1), np.int32)
+    v = np.empty(max(nnz, 1), np.float64)
+    _check(L.ktb_gen_powerlaw_host(n, seed, target_nnz, empty_frac, max_len, rp.ctypes.data,
+                                   ci.ctypes.data, v.ctypes.data))
+    return n, rp, ci[:nnz].astype(np.int64), v[:nnz]
+
+
 def stencil7_slab(nx, ny, nz, z0, z1, diag=6.0, off=-1.0, device=0) -> DeviceCsr:
     h = C.c_void_p()
     _check(_lib.load().ktb_gen_stencil7_slab(nx, ny, nz, z0, z1, diag, off, device,

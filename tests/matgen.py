@@ -104,3 +104,81 @@ def csr_to_dense(n, rp, ci, v):
     for i in range(n):
         a[i, ci[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
     return a
+
+
+# ------------------------------------------------------------------ config 3
+_G = np.uint64(0x9E3779B97F4A7C15)
+_H = np.uint64(0xD1B54A32D192ED03)
+_V = np.uint64(0xA5A5A5A5A5A5A5A5)
+
+
+def _mix(z):
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def _unif(s, k):
+    k = np.asarray(k, np.uint64)
+    return (_mix(s + (k + np.uint64(1)) * _G) >> np.uint64(11)).astype(np.float64) * (
+        1.0 / 9007199254740992.0)
+
+
+def powerlaw(n=4_000_000, seed=3, target=40_000_000, empty_frac=0.1, max_len=65536):
+    """Config 3 recipe, independent numpy restatement of
+    paper_2405_01599_b200/csrc/ktb_gen.cu; bit-identical output."""
+    with np.errstate(over="ignore"):
+        i = np.arange(n, dtype=np.uint64)
+        s = _mix(np.uint64(seed) + (i + np.uint64(1)) * _H)
+        empty = _unif(s, 0) < empty_frac
+        w1 = 1.0 - _unif(s, 1)
+        w = w1 * w1
+        L = np.floor(np.power(w1, -2.0 / 3.0)).astype(np.int64)
+        L = np.clip(L, 1, max_len + 1)
+
+        def le1(l):
+            lf = l.astype(np.float64)
+            return (lf * lf * lf) * w <= 1.0
+
+        while True:
+            up = (L <= max_len) & le1(L + 1)
+            if not up.any():
+                break
+            L += up
+        while True:
+            dn = (L > 1) & ~le1(L)
+            if not dn.any():
+                break
+            L -= dn
+        L = np.minimum(L, max_len)
+        L[empty] = 0
+        total = int(L.sum())
+        q = (L.astype(np.float64) * float(target)) / float(total)
+        lens = np.clip(np.floor(q + 0.5).astype(np.int64), 1, min(max_len, n))
+        lens[L == 0] = 0
+        rp = np.zeros(n + 1, np.int64)
+        np.cumsum(lens, out=rp[1:])
+        nnz = int(rp[-1])
+        row = np.repeat(np.arange(n, dtype=np.int64), lens)
+        k = (np.arange(nnz, dtype=np.int64) - rp[row]).astype(np.uint64)
+        zz = _mix(s[row] + (k + np.uint64(3)) * _G)
+        cand = ((zz >> np.uint64(32)) * np.uint64(n)) >> np.uint64(32)
+        cand = cand.astype(np.int64)
+        order = np.lexsort((cand, row))
+        col = cand[order]
+        dup = np.nonzero((col[1:] == col[:-1]) & (row[1:] == row[:-1]))[0]
+        for r in np.unique(row[dup + 1]):  # rows whose first l candidates collide
+            lo, l = rp[r], rp[r + 1] - rp[r]
+            taken = sorted(set(col[lo:lo + l].tolist()))
+            kk = l
+            while len(taken) < l:
+                z = _mix(np.uint64(s[r]) + (np.uint64(kk) + np.uint64(3)) * _G)
+                c = int((int(z) >> 32) * n >> 32)
+                if c not in taken:
+                    taken.append(c)
+                    taken.sort()
+                kk += 1
+            col[lo:lo + l] = taken
+        pos = k  # position within the sorted row
+        val = 2.0 * _unif(s[row] ^ _V, pos) - 1.0
+    return n, rp, col, val
