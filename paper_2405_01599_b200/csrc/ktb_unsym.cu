@@ -37,7 +37,11 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
 }
 
 // =============================================================== U1
-template <int V>
+// V lanes per row, R consecutive rows per lane group: the row bounds, then
+// the first V entries of all R rows, then their x gathers are issued before
+// any use (R-fold memory-level parallelism); rows longer than V finish in a
+// lane-strided tail loop.
+template <int V, int R>
 __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
                                             const int32_t* __restrict__ col,
                                             const double* __restrict__ val,
@@ -45,30 +49,40 @@ __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
                                             int32_t row_begin, int32_t row_end) {
     const int sub = threadIdx.x & (V - 1);
     const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / V;
-    const int64_t row = row_begin + group;
-    const bool active = row < row_end;
-    int32_t b = 0, e = 0;
-    if (active) {
-        b = ldg_i32(rp + row);
-        e = ldg_i32(rp + row + 1);
+    const int64_t row0 = row_begin + group * R;
+    int32_t b[R], e[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t row = row0 + r;
+        b[r] = row < row_end ? ldg_i32(rp + row) : 0;
+        e[r] = row < row_end ? ldg_i32(rp + row + 1) : 0;
     }
-    double s = 0.0;
-    int32_t k = b + sub;
-    // two independent chains for memory-level parallelism
-    double s2 = 0.0;
-    for (; k + V < e; k += 2 * V) {
-        const int32_t c0 = ld_stream_i32(col + k), c1 = ld_stream_i32(col + k + V);
-        const double v0 = ld_stream_f64(val + k), v1 = ld_stream_f64(val + k + V);
-        s += v0 * ldg_f64(x + c0);
-        s2 += v1 * ldg_f64(x + c1);
+    int32_t c[R];
+    double v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int32_t k = b[r] + sub;
+        c[r] = k < e[r] ? ld_stream_i32(col + k) : -1;
+        v[r] = k < e[r] ? ld_stream_f64(val + k) : 0.0;
     }
-    if (k < e) s += ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
-    s += s2;
+    double s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = c[r] >= 0 ? v[r] * ldg_f64(x + c[r]) : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        for (int32_t k = b[r] + sub + V; k < e[r]; k += V)
+            s[r] += ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
     if (V > 1) {
 #pragma unroll
-        for (int o = V / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, V);
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int o = V / 2; o > 0; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o, V);
     }
-    if (active && sub == 0) y[row] = s;
+    if (sub == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (row0 + r < row_end) y[row0 + r] = s[r];
+    }
 }
 
 static int pick_lanes(const ktb_matrix* m) {
@@ -90,14 +104,16 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
     const int64_t rows = r1 - r0;
     if (rows <= 0) return;
     const int V = static_cast<int>(p->param);
-    const int64_t threads = rows * V;
+    constexpr int R = 4;
+    const int64_t threads = ceil_div64(rows, R) * V;
     const int grid = ceil_div(threads, 256);
     p->ctas = grid;
     const ktb_matrix* m = p->m;
 #define KTB_U1_CASE(VV)                                                                        \
     case VV:                                                                                    \
-        k_u1<VV><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,          \
-                                              static_cast<int32_t>(r0), static_cast<int32_t>(r1)); \
+        k_u1<VV, R><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,       \
+                                                 static_cast<int32_t>(r0),                      \
+                                                 static_cast<int32_t>(r1));                     \
         break;
     switch (V) {
         KTB_U1_CASE(1)
@@ -179,12 +195,31 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
     const MergeCoord c0 = coords[blockIdx.x], c1 = coords[blockIdx.x + 1];
     const int nrows = c1.row - c0.row;
     const int nnzs = c1.nz - c0.nz;
-    // stage products (coalesced) and row ends
-    for (int i = tid; i < nnzs; i += kU2Threads) {
-        const int32_t k = c0.nz + i;
-        s_prod[i] = ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
+    // stage products (coalesced): all column/value loads of the thread first,
+    // then all x gathers, then the products -> IPT independent chains per thread
+    {
+        int32_t cc[IPT];
+        double vv[IPT];
+#pragma unroll
+        for (int u = 0; u < IPT; ++u) {
+            const int i = u * kU2Threads + tid;
+            cc[u] = i < nnzs ? ld_stream_i32(col + c0.nz + i) : -1;
+            vv[u] = i < nnzs ? ld_stream_f64(val + c0.nz + i) : 0.0;
+        }
+        double xv[IPT];
+#pragma unroll
+        for (int u = 0; u < IPT; ++u) xv[u] = cc[u] >= 0 ? ldg_f64(x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < IPT; ++u) {
+            const int i = u * kU2Threads + tid;
+            if (i < nnzs) s_prod[i] = vv[u] * xv[u];
+        }
     }
-    for (int i = tid; i < nrows; i += kU2Threads) s_end[i] = ldg_i32(rp + c0.row + 1 + i);
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const int i = u * kU2Threads + tid;
+        if (i < nrows) s_end[i] = ldg_i32(rp + c0.row + 1 + i);
+    }
     if (tid == 0) s_end[nrows] = 0x7fffffff;  // the open row at tile end never closes here
     __syncthreads();
 
@@ -342,9 +377,22 @@ __global__ void __launch_bounds__(kU3Threads) k_u3(const int32_t* __restrict__ c
     const int64_t p1 = min(p0 + kU3Threads, jl);
     const int64_t K0 = nnz * p0 / jl, K1 = nnz * p1 / jl;
     const int span = static_cast<int>(K1 - K0);
-    for (int i = tid; i < span; i += kU3Threads) {
-        const int64_t k = K0 + i;
-        s_prod[i + i / E] = ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
+    {
+        int32_t cc[E];
+        double vv[E], xv[E];
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            const int i = u * kU3Threads + tid;
+            cc[u] = i < span ? ld_stream_i32(col + K0 + i) : -1;
+            vv[u] = i < span ? ld_stream_f64(val + K0 + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < E; ++u) xv[u] = cc[u] >= 0 ? ldg_f64(x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            const int i = u * kU3Threads + tid;
+            if (i < span) s_prod[i + i / E] = vv[u] * xv[u];
+        }
     }
     // this lane's chunk (reference rule, bss.hpp:49-50)
     const int64_t p = p0 + tid;
