@@ -104,7 +104,10 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
     const int64_t rows = r1 - r0;
     if (rows <= 0) return;
     const int V = static_cast<int>(p->param);
-    constexpr int R = 4;
+#ifndef KTB_U1_R
+#define KTB_U1_R 4
+#endif
+    constexpr int R = KTB_U1_R;
     const int64_t threads = ceil_div64(rows, R) * V;
     const int grid = ceil_div(threads, 256);
     p->ctas = grid;

@@ -30,6 +30,8 @@ def main():
         a = K.stencil27_upper(128, 128, 128)
     elif args.config == 1:
         a = K.stencil7(64, 64, 64)
+    elif args.config == 3:
+        a = K.powerlaw()
     elif args.config == 4:
         a = K.stencil7(512, 512, 512)
     elif args.config == 5:
