@@ -11,7 +11,7 @@ GB/s uses the minimum-traffic model:
     B = 12*nnz + 4*(n+1) + 16*n      (nnz = stored nonzeros)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config 1|2|4]
+                    [--config 1|2|3|4]
 
 N>1 (torchrun): every rank runs its own replica of the workload on its GPU
 (config 2 does not shard: "replicas only", weak scaling, no collective on the
@@ -258,7 +258,7 @@ def run_gpu(args, cfg):
     sampler.start()
     with torch.cuda.stream(stream):
         # warm-up: >= W steps and ~1 s of load so the clocks settle
-        t_warm = time.perf_counter() + 1.0
+        t_warm = time.perf_counter() + args.warm_seconds
         w = 0
         while w < args.warmup or time.perf_counter() < t_warm:
             plan.apply(x, y)
@@ -352,6 +352,114 @@ def run_gpu(args, cfg):
     return 0
 
 
+def run_gpu_dist(args, cfg):
+    """Config 4: z-slab row-block sharding over the ranks (paper_2405_01599_b200
+    .dist), NCCL P2P halo exchange overlapped with the interior rows. Fixed
+    total problem: strong scaling; value = whole-matrix bytes / max-rank time."""
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2405_01599_b200 import dist as D
+
+    nx = ny = nz = 512
+    shard = D.DistSpMV(nx, ny, nz, rank, ws, local, seed=cfg["seed"])
+    n_glob = nx * ny * nz
+    nnz_glob = 7 * n_glob - 6 * nx * nx  # 7-pt stencil with Dirichlet boundary
+    B = min_bytes(n_glob, nnz_glob)
+    B_local = min_bytes(shard.L.n_local, shard.nnz)
+    F = flops(n_glob, nnz_glob, False)
+    stream = torch.cuda.Stream()
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(2 * max(l2, 64 << 20), dtype=torch.uint8, device="cuda")
+    sampler = ClockSampler(gpu_uuid(local))
+    sampler.start()
+    with torch.cuda.stream(stream):
+        t_warm = time.perf_counter() + args.warm_seconds
+        w = 0
+        while w < args.warmup or time.perf_counter() < t_warm:
+            shard.apply()
+            w += 1
+            if w % 10 == 0:
+                stream.synchronize()
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            if dist:  # all ranks start the step together (halo partners)
+                dist.barrier()
+            ev[k][0].record(stream)
+            shard.apply()
+            ev[k][1].record(stream)
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    # e2e: owned x from pinned host, sharded apply, owned y back to host
+    o0, n_loc = shard.L.owned_offset, shard.L.n_local
+    xh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    xh.copy_(shard.x[o0:o0 + n_loc].cpu())
+    yh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    e2e_ms = []
+    with torch.cuda.stream(stream):
+        for k in range(max(3, min(args.steps, 10))):
+            flush.fill_(k & 0xff)
+            if dist:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            shard.x[o0:o0 + n_loc].copy_(xh, non_blocking=True)
+            shard.apply()
+            yh.copy_(shard.y, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+    clocks = sampler.stop()
+    e2e = float(np.mean(e2e_ms))
+    if dist:
+        t = torch.tensor([ms, e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e = float(t[0]), float(t[1])
+    if rank == 0:
+        peak, peak_src = peak_hbm()
+        achieved = B_local / (ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": B / (ms / 1e3) / 1e9, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8d recipe, seeded)",
+            "config": dict(config_block(cfg, "u1 (z-slab shards, NCCL halo)"),
+                           parallelism=f"row-block z-slabs x{ws}, one-plane halo"),
+            "gflops": F / (ms / 1e3) / 1e9,
+            "pct_hbm_peak_per_gpu": 100.0 * achieved / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "u1 (rank 0 slab: interior + 2 boundary planes)",
+                         "bytes_per_launch": B_local},
+            "e2e": {"value": B / (e2e / 1e3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
+                    "ms_per_step": e2e},
+            "gpu_launches": args.steps * shard.launches_per_apply(),
+            "clocks": clocks,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def traffic_from_profile(cfg):
     """dram bytes (read+write) per launch of the dominant kernel from the
     committed ncu --set full summary, if present (profiles/traffic.json)."""
@@ -386,11 +494,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--warm-seconds", type=float, default=1.0,
+                    help="keep warming up at least this long (clocks settle); 0 under ncu")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.config == 4:
+        return run_gpu_dist(args, cfg)
     return run_gpu(args, cfg)
 
 
