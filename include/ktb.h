@@ -180,6 +180,28 @@ typedef struct {
 int ktb_select(ktb_matrix* m, const ktb_select_opts* opts, void* stream, ktb_plan** winner,
                ktb_candidate* cands, int max_cands, int* n_cands, int* selected);
 
+/* ---------------------------------------------------------- consumer */
+typedef struct {
+    int64_t iterations;  /* Arnoldi steps (gmres.hpp:119) */
+    int64_t restarts;
+    int64_t spmv_calls;
+    int converged;
+    int breakdown;
+    int fault_convergence;  /* recurrence met tol, true residual did not (gmres.hpp:169) */
+    double recurrence_residual;
+    double true_residual;
+    double seconds;         /* wall time of the solve */
+    double spmv_seconds;    /* device time inside the SpMV applies (CUDA events) */
+} ktb_gmres_result;
+
+/* gmres_m (gmres.hpp:16-173): restarted GMRES(m) with modified Gram-Schmidt
+ * (ortho.hpp:88-94), x0 = 0, no preconditioner, stop at relative recurrence
+ * residual < tol or max_iters; true residual recomputed at exit. All vectors
+ * device-resident; A is any GENERAL-matrix plan. b, x, history: HOST arrays
+ * (history: max_iters doubles or NULL). */
+int ktb_gmres(ktb_plan* A, const double* b, double* x, int64_t m, double tol, int64_t max_iters,
+              double* history, ktb_gmres_result* res);
+
 /* ---------------------------------------------------------- host memory */
 int ktb_host_alloc(size_t bytes, void** out);  /* pinned */
 int ktb_host_free(void* p);

@@ -1,0 +1,318 @@
+// ktb_gmres.cu -- device-resident restarted GMRES(m) with modified
+// Gram-Schmidt (config 5 consumer; reference gmres.hpp:16-173 with
+// OrthoKind::mgs, ortho.hpp:69-111, identity preconditioner, x0 = 0).
+//
+// Vectors (basis V of m+1 columns, w, r, x, b) live in HBM; the SpMV is the
+// caller's plan. The scalar recurrence (Givens rotations, residual estimate,
+// back-substitution) runs on the host exactly as the reference writes it,
+// fed by device-computed projections. Orthogonalisation is one cooperative
+// kernel per Arnoldi step: per column q it applies w -= h_q V_q and, in the
+// same pass, accumulates the next projection <V_{q+1}, w> (or |w|^2 after the
+// last column), with a deterministic fixed-order grid reduction between
+// passes. Element-wise updates use explicitly rounded mul/add so each element
+// follows the reference's arithmetic; only the dot-product summation order
+// differs (parallel tree instead of serial), hence the iteration count can
+// move by a step or two.
+#include <cooperative_groups.h>
+
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "ktb_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ktb {
+
+constexpr int kGThreads = 512;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < kGThreads / 32; ++k) s += red[k];
+    return s;  // valid in thread 0
+}
+
+// Fixed-order sum of the per-block partials (every thread gets the same).
+__device__ __forceinline__ double grid_total(const double* partials, int nb) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += partials[b];
+    return s;
+}
+
+__global__ void __launch_bounds__(kGThreads) k_mgs(const double* __restrict__ V, int64_t n,
+                                                   int k, double* __restrict__ w,
+                                                   double* __restrict__ vnext,
+                                                   double* __restrict__ h,
+                                                   double* __restrict__ partials,
+                                                   int* __restrict__ breakdown) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[kGThreads / 32];
+    const int nb = gridDim.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    volatile double* vp = partials;
+    // input norm^2 and the first projection <V_0, w>
+    double a = 0.0, b = 0.0;
+    for (int64_t i = t0; i < n; i += stride) {
+        const double wi = w[i];
+        a += wi * wi;
+        b += V[i] * wi;
+    }
+    a = block_sum(a, red);
+    b = block_sum(b, red);
+    if (threadIdx.x == 0) {
+        vp[blockIdx.x] = a;
+        vp[nb + blockIdx.x] = b;
+    }
+    grid.sync();
+    const double in2 = grid_total(partials, nb);
+    double c = grid_total(partials + nb, nb);
+    int slot = 0;  // alternate partial buffers between passes
+    for (int q = 0; q < k; ++q) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) h[q] = c;
+        const double* Vq = V + static_cast<int64_t>(q) * n;
+        const bool last = q + 1 == k;
+        const double* Vn = last ? nullptr : V + static_cast<int64_t>(q + 1) * n;
+        const double mc = -c;
+        double p = 0.0;
+        for (int64_t i = t0; i < n; i += stride) {
+            const double wi = __dadd_rn(w[i], __dmul_rn(mc, Vq[i]));  // axpy(-c, q, v)
+            w[i] = wi;
+            p += last ? wi * wi : Vn[i] * wi;
+        }
+        p = block_sum(p, red);
+        if (threadIdx.x == 0) vp[(slot ^ 1) * nb * 2 + blockIdx.x] = p;
+        grid.sync();
+        slot ^= 1;
+        c = grid_total(partials + slot * nb * 2, nb);
+    }
+    // c = |w|^2 after the last column
+    const double nrm = sqrt(c);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        h[k] = nrm;
+        *breakdown = nrm <= 1e-14 * sqrt(in2) ? 1 : 0;
+    }
+    if (!(nrm <= 1e-14 * sqrt(in2))) {
+        const double inv = 1.0 / nrm;  // scal(1.0 / r.norm, v)
+        for (int64_t i = t0; i < n; i += stride) vnext[i] = __dmul_rn(w[i], inv);
+    }
+}
+
+__global__ void k_sub_from(const double* __restrict__ b, double* __restrict__ r, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) r[i] = __dsub_rn(b[i], r[i]);
+}
+
+__global__ void k_div(const double* __restrict__ r, double beta, double* __restrict__ v,
+                      int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) v[i] = __ddiv_rn(r[i], beta);
+}
+
+__global__ void __launch_bounds__(kGThreads) k_sumsq(const double* __restrict__ r, int64_t n,
+                                                     double* __restrict__ partials) {
+    __shared__ double red[kGThreads / 32];
+    double a = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = r[i];
+        a += v * v;
+    }
+    a = block_sum(a, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = a;
+}
+
+// x += sum_l y_l V_l with the reference's per-element order (w = 0; w += y_l
+// V_l for l ascending; x += 1.0 * w), gmres.hpp:138-143.
+__global__ void k_update_x(const double* __restrict__ V, const double* __restrict__ y, int j,
+                           int64_t n, double* __restrict__ x) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    for (int l = 0; l < j; ++l) acc = __dadd_rn(acc, __dmul_rn(y[l], V[static_cast<int64_t>(l) * n + i]));
+    x[i] = __dadd_rn(x[i], __dmul_rn(1.0, acc));
+}
+
+}  // namespace ktb
+
+namespace ktb {
+
+// Restarted GMRES(m), MGS, x0 = 0 (gmres.hpp:16-173); host b/x spans.
+void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, double tol,
+               int64_t max_iters, double* history, ktb_gmres_result* res) {
+        require(A != nullptr && res != nullptr, "gmres: null argument");
+        require(m >= 1, "gmres: need 1 <= m <= m_max");  // gmres.hpp:20
+        require(tol > 0.0, "gmres: tol must be positive");  // gmres.hpp:21
+        const ktb_matrix* M = A->m;
+        require(M->n == M->ncols, "gmres: dimension mismatch");
+        DeviceGuard g(M->device);
+        const auto t_start = std::chrono::steady_clock::now();
+        const int64_t n = M->n;
+        cudaStream_t st = A->stream;
+        *res = ktb_gmres_result{};
+        int dev = 0, sms = 0, per_sm = 0;
+        KTB_CUDA(cudaGetDevice(&dev));
+        KTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs, kGThreads, 0));
+        require(per_sm >= 1, "gmres: cooperative MGS kernel does not fit");
+        const int nb = sms * std::min(per_sm, 2);
+        DBuf<double> b(n), x(n), r(n), w(n), V(static_cast<size_t>(n) * (m + 1));
+        DBuf<double> partials(4 * nb), dh(m + 2), dy(m + 1);
+        DBuf<int> dbreak(1);
+        KTB_CUDA(cudaMemcpyAsync(b.p, b_host, 8 * n, cudaMemcpyHostToDevice, st));
+        KTB_CUDA(cudaMemsetAsync(x.p, 0, 8 * n, st));
+        const int eb = ceil_div(n, 256);
+        cudaEvent_t ev0, ev1;
+        KTB_CUDA(cudaEventCreate(&ev0));
+        KTB_CUDA(cudaEventCreate(&ev1));
+        bool pending = false;
+        auto settle = [&]() {  // after a stream sync: account the last SpMV
+            if (pending) {
+                float ms = 0.f;
+                KTB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+                res->spmv_seconds += ms * 1e-3;
+                pending = false;
+            }
+        };
+        auto spmv_timed = [&](const double* in, double* out) {
+            KTB_CUDA(cudaEventRecord(ev0, st));
+            plan_run(A, in, out, 0, n);
+            KTB_CUDA(cudaEventRecord(ev1, st));
+            pending = true;
+            res->spmv_calls++;
+        };
+        auto norm2 = [&](const double* v) {
+            k_sumsq<<<nb, kGThreads, 0, st>>>(v, n, partials.p);
+            KTB_LAUNCH();
+            std::vector<double> hp(nb);
+            KTB_CUDA(cudaMemcpyAsync(hp.data(), partials.p, 8 * nb, cudaMemcpyDeviceToHost, st));
+            KTB_CUDA(cudaStreamSynchronize(st));
+            settle();
+            double s = 0.0;
+            for (double v : hp) s += v;
+            return std::sqrt(s);
+        };
+        const double nb2 = norm2(b.p);
+        if (nb2 == 0.0) {
+            res->converged = 1;
+            KTB_CUDA(cudaMemcpyAsync(x_host, x.p, 8 * n, cudaMemcpyDeviceToHost, st));
+            KTB_CUDA(cudaStreamSynchronize(st));
+            return;
+        }
+        const int64_t r_stride = m + 1;
+        std::vector<double> h(m + 2), cs(m + 1), sn(m + 1), gv(m + 2), r_cols(r_stride * m),
+            yv(m + 1);
+        double rr = 1.0;
+        bool stop = false;
+        while (!stop) {
+            spmv_timed(x.p, r.p);
+            k_sub_from<<<eb, 256, 0, st>>>(b.p, r.p, n);
+            KTB_LAUNCH();
+            const double beta = norm2(r.p);
+            rr = beta / nb2;
+            if (rr < tol) {
+                res->converged = 1;
+                break;
+            }
+            k_div<<<eb, 256, 0, st>>>(r.p, beta, V.p, n);
+            KTB_LAUNCH();
+            std::fill(gv.begin(), gv.end(), 0.0);
+            gv[0] = beta;
+            int64_t j = 0;
+            bool lucky = false;
+            while (j < m) {
+                if (res->iterations >= max_iters) {
+                    stop = true;
+                    break;
+                }
+                spmv_timed(V.p + j * n, w.p);
+                // orthogonalise against columns 0..j; V_{j+1} = w / |w|
+                int kk = static_cast<int>(j + 1);
+                const double* Vp = V.p;
+                double* wp = w.p;
+                double* vn = V.p + (j + 1) * n;
+                double* hp = dh.p;
+                double* pp = partials.p;
+                int* bp = dbreak.p;
+                int64_t nn = n;
+                void* args[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &pp, &bp};
+                KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_mgs),
+                                                     dim3(nb), dim3(kGThreads), args, 0, st));
+                int brk = 0;
+                KTB_CUDA(cudaMemcpyAsync(h.data(), dh.p, 8 * (j + 2), cudaMemcpyDeviceToHost, st));
+                KTB_CUDA(cudaMemcpyAsync(&brk, dbreak.p, 4, cudaMemcpyDeviceToHost, st));
+                KTB_CUDA(cudaStreamSynchronize(st));
+                settle();
+                if (brk) {
+                    h[j + 1] = 0.0;
+                    lucky = true;
+                }
+                // gmres.hpp:100-116, verbatim scalar recurrence
+                for (int64_t i = 0; i < j; ++i) {
+                    const double t1 = h[i], t2 = h[i + 1];
+                    h[i] = cs[i] * t1 + sn[i] * t2;
+                    h[i + 1] = -sn[i] * t1 + cs[i] * t2;
+                }
+                const double denom = std::hypot(h[j], h[j + 1]);
+                if (denom == 0.0) {
+                    cs[j] = 1.0;
+                    sn[j] = 0.0;
+                } else {
+                    cs[j] = h[j] / denom;
+                    sn[j] = h[j + 1] / denom;
+                }
+                h[j] = denom;
+                gv[j + 1] = -sn[j] * gv[j];
+                gv[j] *= cs[j];
+                for (int64_t q = 0; q <= j; ++q) r_cols[j * r_stride + q] = h[q];
+                res->iterations++;
+                rr = std::abs(gv[j + 1]) / nb2;
+                if (history) history[res->iterations - 1] = rr;
+                ++j;
+                if (lucky || rr < tol) break;
+            }
+            if (j > 0) {  // gmres.hpp:125-143
+                for (int64_t i = j - 1; i >= 0; --i) {
+                    double s = gv[i];
+                    for (int64_t l = i + 1; l < j; ++l) s -= r_cols[l * r_stride + i] * yv[l];
+                    const double rii = r_cols[i * r_stride + i];
+                    yv[i] = rii != 0.0 ? s / rii : 0.0;
+                }
+                KTB_CUDA(cudaMemcpyAsync(dy.p, yv.data(), 8 * j, cudaMemcpyHostToDevice, st));
+                k_update_x<<<eb, 256, 0, st>>>(V.p, dy.p, static_cast<int>(j), n, x.p);
+                KTB_LAUNCH();
+            }
+            if (rr < tol) {
+                res->converged = 1;
+                break;
+            }
+            if (lucky) {
+                res->breakdown = 1;
+                break;
+            }
+            if (stop) break;
+            res->restarts++;
+        }
+        res->recurrence_residual = rr;
+        spmv_timed(x.p, r.p);
+        k_sub_from<<<eb, 256, 0, st>>>(b.p, r.p, n);
+        KTB_LAUNCH();
+        res->true_residual = norm2(r.p) / nb2;
+        res->fault_convergence = res->converged && res->true_residual > tol;
+        KTB_CUDA(cudaMemcpyAsync(x_host, x.p, 8 * n, cudaMemcpyDeviceToHost, st));
+        KTB_CUDA(cudaStreamSynchronize(st));
+        settle();
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        res->seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+}  // namespace ktb

@@ -631,3 +631,54 @@ def make_ref_op(a) -> LinOp:
     CPU oracle lives in oracle/ (tests only)."""
     plan = _plan_for(a, SymKernel.s3_nnz_zero_omit if a._kind else UnsymKernel.u1_row)
     return LinOp(a.n, plan.apply)
+
+
+# ------------------------------------------------------------------ GMRES
+@dataclass
+class KrylovConfig:  # solver_types.hpp:44-57 (MGS, no restart adaptation)
+    restart_m: int = 30
+    m_max: int = 30
+    tol: float = 1e-8
+    max_iters: int = 10000
+
+
+@dataclass
+class SolverResult:  # solver_types.hpp:64-77
+    x: np.ndarray
+    converged: bool
+    breakdown: bool
+    fault_convergence: bool
+    iterations: int
+    restarts: int
+    recurrence_residual: float
+    true_residual: float
+    residual_history: np.ndarray
+    elapsed_seconds: float
+    spmv_calls: int
+    spmv_seconds: float
+
+
+class _GmresRes(C.Structure):
+    _fields_ = [("iterations", I64), ("restarts", I64), ("spmv_calls", I64),
+                ("converged", C.c_int), ("breakdown", C.c_int), ("fault_convergence", C.c_int),
+                ("recurrence_residual", C.c_double), ("true_residual", C.c_double),
+                ("seconds", C.c_double), ("spmv_seconds", C.c_double)]
+
+
+def gmres_m(a, b, cfg: KrylovConfig = KrylovConfig(), plan: Optional[DevicePlan] = None):
+    """gmres.hpp:16-173 (GMRES(m), MGS, x0 = 0) with every vector in HBM and
+    the SpMV on `plan` (default: the device-time selected kernel)."""
+    require(len(b) == a.n, "gmres: dimension mismatch")
+    require(1 <= cfg.restart_m <= cfg.m_max, "gmres: need 1 <= m <= m_max")
+    require(cfg.tol > 0.0, "gmres: tol must be positive")
+    if plan is None:
+        plan = select_spmv_unsym(a)[0].plan
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.empty(a.n, np.float64)
+    hist = np.zeros(max(cfg.max_iters, 1), np.float64)
+    r = _GmresRes()
+    _check(_lib.load().ktb_gmres(plan.h, b.ctypes.data, x.ctypes.data, cfg.restart_m, cfg.tol,
+                                 cfg.max_iters, hist.ctypes.data, C.byref(r)))
+    return SolverResult(x, bool(r.converged), bool(r.breakdown), bool(r.fault_convergence),
+                        r.iterations, r.restarts, r.recurrence_residual, r.true_residual,
+                        hist[: r.iterations].copy(), r.seconds, r.spmv_calls, r.spmv_seconds)

@@ -1,0 +1,55 @@
+"""Config-5 consumer: device-resident GMRES(30)+MGS against the reference's own
+solver (golden fixture from oracle/_ref, and the C restatement at 32^3).
+Dot products are reduced in parallel (not the reference's serial order), so
+the iteration count may move by +-2 (SURVEY.md §7 hard part 7); the true
+residual must meet tol."""
+import os
+
+import numpy as np
+import pytest
+
+import matgen
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _solve(n, rp, ci, v, b, max_iters=3000):
+    from paper_2405_01599_b200 import ktune as K
+
+    a = K.CsrMatrix(n, rp, ci, v)
+    plan = K.DevicePlan(a, K.UnsymKernel.u1_row)
+    return K.gmres_m(a, b, K.KrylovConfig(30, 30, 1e-8, max_iters), plan=plan)
+
+
+def test_gmres_golden_16cubed():
+    g = np.load(os.path.join(GOLD, "stencil.npz"))
+    rp, ci, v, b = g["cd_rp"], g["cd_ci"], g["cd_v"], g["cd_b"]
+    r = _solve(len(rp) - 1, rp, ci, v, b)
+    assert r.converged and not r.fault_convergence
+    assert abs(r.iterations - int(g["cd_iterations"])) <= 2
+    assert r.true_residual < 1e-8
+    assert np.max(np.abs(r.x - g["cd_x"])) < 1e-6  # both within tol of x = ones
+    k = min(len(r.residual_history), len(g["cd_hist"])) - 3
+    assert np.allclose(r.residual_history[:k], g["cd_hist"][:k], rtol=1e-6, atol=0)
+
+
+def test_gmres_32cubed_vs_restatement():
+    n, rp, ci, v = matgen.stencil7(32, 32, 32, xp=-0.7, xm=-1.3)
+    b = O.spmv_ref(n, rp, ci, v, np.ones(n))
+    xo, ro = O.gmres_mgs(n, rp, ci, v, b)
+    r = _solve(n, rp, ci, v, b)
+    assert r.converged and abs(r.iterations - ro["iterations"]) <= 2
+    assert r.true_residual < 1e-8
+    assert r.spmv_calls == r.iterations + r.restarts + 2
+    assert np.max(np.abs(r.x - 1.0)) < 1e-5
+
+
+def test_gmres_max_iters_and_zero_rhs():
+    n, rp, ci, v = matgen.stencil7(8, 8, 8, xp=-0.7, xm=-1.3)
+    b = O.spmv_ref(n, rp, ci, v, np.ones(n))
+    r = _solve(n, rp, ci, v, b, max_iters=5)
+    assert not r.converged and r.iterations == 5
+    r = _solve(n, rp, ci, v, np.zeros(n))
+    assert r.converged and r.iterations == 0 and not r.x.any()
