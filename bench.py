@@ -460,6 +460,60 @@ def run_gpu_dist(args, cfg):
     return 0
 
 
+def run_gmres(args, cfg):
+    """Config 5: GMRES(30)+MGS on the 128^3 convection-diffusion matrix,
+    b = A*ones, tol 1e-8, <= 3000 iterations (BASELINE.json configs[4]).
+    One step = one full solve; value = SpMV GB/s inside the solve; the solve's
+    iterations / residual / SpMV share are reported beside it."""
+    import torch
+
+    from oracle import oracle as O  # b = A*ones via the oracle (input setup only)
+    from paper_2405_01599_b200 import ktune as K
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    a = K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7, device=local)
+    rp, ci, v = a.to_host()
+    A = K.CsrMatrix(a.n, rp, ci, v, device=local)
+    b = O.spmv_ref(a.n, rp, ci, v, np.ones(a.n))
+    choice, rep = K.select_spmv_unsym(A)
+    kcfg = K.KrylovConfig(30, 30, 1e-8, 3000)
+    for _ in range(max(1, args.warmup // 3)):
+        K.gmres_m(A, b, kcfg, plan=choice.plan)
+    runs = [K.gmres_m(A, b, kcfg, plan=choice.plan) for _ in range(max(1, args.steps // 10))]
+    r = runs[-1]
+    sec = float(np.mean([x.elapsed_seconds for x in runs]))
+    spmv = float(np.mean([x.spmv_seconds for x in runs]))
+    B = min_bytes(a.n, a.nnz())
+    line = {"metric": METRIC, "value": B * r.spmv_calls / spmv / 1e9, "unit": "GB/s",
+            "n_gpus": 1, "steps": len(runs), "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8d recipe)",
+            "config": {"workload": "cfg5: GMRES(30)+MGS, 128^3 7-pt convection-diffusion, "
+                                   "b = A*ones, tol 1e-8, max 3000 its",
+                       "kernel": f"{rep.selected_candidate().name} SpMV + cooperative MGS"},
+            "gmres": {"iterations": r.iterations, "restarts": r.restarts,
+                      "true_residual": r.true_residual, "converged": r.converged,
+                      "spmv_calls": r.spmv_calls, "solve_seconds": sec,
+                      "spmv_seconds": spmv, "spmv_share": spmv / sec,
+                      "reference_iterations_survey": 653}}
+    if not args.no_cpu_baseline:
+        try:
+            n, rp64, ci64, v64 = a.n, rp.astype(np.int64), ci.astype(np.int64), v
+            its = 60  # bounded sample: two restarts of the reference solver
+            _, rr = O.Ref.gmres(n, rp64, ci64, v64, b, 30, 1e-8, its, 1, os.cpu_count() or 1)
+            line["cpu_baseline"] = {
+                "value": B * rr["spmv_calls"] / max(rr["spmv_seconds"], 1e-12) / 1e9,
+                "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"{its} iterations of ktune::gmres_m (MGS) with a U1 UnsymEngine on "
+                          f"all cores: {rr['seconds']:.2f} s ({rr['seconds'] / its * 1e3:.1f} ms/it; "
+                          f"653 its extrapolate to {rr['seconds'] / its * 653:.1f} s)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
+    print(json.dumps(line))
+    return 0
+
+
 def traffic_from_profile(cfg):
     """dram bytes (read+write) per launch of the dominant kernel from the
     committed ncu --set full summary, if present (profiles/traffic.json)."""
@@ -492,17 +546,19 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS) + [5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--warm-seconds", type=float, default=1.0,
                     help="keep warming up at least this long (clocks settle); 0 under ncu")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS.get(args.config, {"workload": "cfg5", "sym": False, "seed": 5})
     if args.impl == "reference":
         return run_reference(args, cfg)
     if args.config == 4:
         return run_gpu_dist(args, cfg)
+    if args.config == 5:
+        return run_gmres(args, cfg)
     return run_gpu(args, cfg)
 
 
