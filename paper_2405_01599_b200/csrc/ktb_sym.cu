@@ -140,25 +140,17 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 }
 
 // ================================================================ S3
-// Warp-specialised, TMA-pipelined round kernel. One CTA per SM:
-//   warp 8       producer: one elected lane streams the CTA's SELL chunks
-//                (<= kChunkR rounds x 256 rows of cols + vals, contiguous) into
-//                a kStages-deep shared-memory ring with cp.async.bulk (L2
-//                evict_first, completion on mbarriers) and bulk-prefetches the
-//                advancing front of x into L2;
-//   warps 0..7   consumers, one row each: gather x for chunk q+2 while running
-//                the rounds of chunk q; each round is a plain ld/add/st on the
-//                window ring followed by a named barrier (the plan guarantees
-//                distinct targets per round).
-// The part of each block's region beyond the block (the spill) goes to a
-// global buffer; k_s3_fixup adds it into the next blocks' head rows in
-// ascending source order, so the result is deterministic.
-constexpr int kS3Threads = 256;  // consumer threads
-#ifndef KTB_S3_RPT
-#define KTB_S3_RPT 8
-#endif
-constexpr int kRPT = KTB_S3_RPT;  // rows per consumer thread
-constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
+// Zero-omission window kernel (see the file header). One block per SM owns
+// its NNZ_BALANCED row block; sub-tiles of kRows rows are processed in
+// rounds from a TMA-fed shared-memory ring (one round of one sub-tile per
+// stage, copied to registers on arrival), x is gathered kGD rounds ahead,
+// and each round's scatter is a plain ld/add/st on the window ring followed
+// by one block barrier. The part of each block's region beyond the block
+// (the spill) goes to a global buffer; k_s3_fixup adds it into the next
+// blocks' head rows in ascending source order (deterministic).
+constexpr int kS3Threads = 512;  // threads per block (one block per SM)
+constexpr int kRPT = 4;          // rows per thread: rows t, t+512, t+1024, t+1536
+constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (2048)
 #ifndef KTB_S3_STAGES
 #define KTB_S3_STAGES 4
 #endif
@@ -166,14 +158,31 @@ constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (1024)
 #define KTB_S3_GD 2
 #endif
 constexpr int kStages = KTB_S3_STAGES;  // one round of one sub-tile per stage
-constexpr int kGD = KTB_S3_GD;   // gather distance (stages ahead)
-constexpr int kRing = KTB_S3_GD + 1;  // register ring slots
-constexpr int kStageBytes = kRows * (2 + 8);  // 10240: int16 rel col + fp64 val
+constexpr int kGD = KTB_S3_GD;           // gather distance (stages ahead)
+constexpr int kRing = KTB_S3_GD + 1;     // register ring slots
+// stage = one round of a sub-tile: fp64 values then int16 sub-tile-relative
+// columns, in a thread-swizzled order so each thread reads its 4 values with
+// two conflict-free LDS.128 (chunk k*512+t holds rows t+1024k, t+1024k+512)
+// and its 4 columns with one LDS.64 (chunk t holds rows t+512u, u = 0..3)
+constexpr int kStageBytes = kRows * (8 + 2);  // 20480
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 constexpr int kS3SmemFixed = kStages * kStageBytes + kStages * 8 + 128;
 constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
 
-__device__ __forceinline__ int wrap(int s, int W) { return s >= W ? s - W : s; }
+// host-side positions of sub-tile row t in a round's value / column arrays
+inline int64_t s3_val_pos(int t) {
+    const int th = t % kS3Threads, u = t / kS3Threads;
+    return (static_cast<int64_t>(u / 2) * kS3Threads + th) * 2 + (u % 2);
+}
+inline int64_t s3_col_pos(int t) {
+    const int th = t % kS3Threads, u = t / kS3Threads;
+    return static_cast<int64_t>(th) * kRPT + u;
+}
+
+// unsigned wrap into [0, W) for s in [0, 2W)
+__device__ __forceinline__ int wrap(int s, int W) {
+    return static_cast<int>(min(static_cast<unsigned>(s), static_cast<unsigned>(s - W)));
+}
 
 // chunk metadata (one int per round-chunk): bits 0-6 round, bit 7 last round
 // of its sub-tile, bits 8.. sub-tile index local to the block
@@ -181,17 +190,18 @@ __device__ __forceinline__ int meta_round(int m) { return m & 127; }
 __device__ __forceinline__ bool meta_last(int m) { return (m >> 7) & 1; }
 __device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
 
-// One block of kS3Threads consumer threads per SM (no producer warp, so
-// the full 255-register budget is available). Consumer thread 0 drives the
-// TMA ring: it issues the first kStages chunks, waits for chunk q+kGD+1
+// One block of kS3Threads threads per SM (no producer warp). Thread 0 drives
+// the TMA ring: it issues the first kStages chunks, waits for chunk q+kGD+1
 // before each round barrier (the barrier then publishes the landed stage to
 // everyone), and re-issues a stage's next chunk as soon as the stage has been
-// copied into registers.
+// copied into registers. The diagonal is a separate dense stream (d), so
+// every SELL entry scatters.
 __global__ void __launch_bounds__(kS3Threads, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
          const int32_t* __restrict__ chunk_meta, const int16_t* __restrict__ scol,
          const double* __restrict__ sval, const int64_t* __restrict__ cta_base,
-         const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
+         const double* __restrict__ diag, const double* __restrict__ x,
+         double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -208,14 +218,13 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     const int q0 = cta_chunk[c];
     const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
     const int32_t* meta = chunk_meta + q0;
-    // chunk q of this block = kRows contiguous SELL slots at cta_base[c] + q*kRows
     const int16_t* gcol = scol + cta_base[c];
     const double* gval = sval + cta_base[c];
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int qq, int st) {  // thread 0 only
         mbar_arrive_expect_tx(&full[st], kStageBytes);
-        tma_load_1d(s_col(st), gcol + int64_t(qq) * kRows, kRows * 2, &full[st], pol);
         tma_load_1d(s_val(st), gval + int64_t(qq) * kRows, kRows * 8, &full[st], pol);
+        tma_load_1d(s_col(st), gcol + int64_t(qq) * kRows, kRows * 2, &full[st], pol);
     };
     // x is first touched by the far reach of the window: pull the initial
     // window and then each sub-tile's new front into L2 ahead of the gathers
@@ -252,31 +261,29 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             }
         };
         int gq = 0, gst = 0;  // next chunk to gather
-        int32_t cr[kRing][kRPT];  // sub-tile-relative column (-1: padding)
+        int cr[kRing][kRPT];  // sub-tile-relative column (-1: padding)
         double vr[kRing][kRPT], xr[kRing][kRPT];
         int mr[kRing];
-        auto gather = [&](int32_t (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
-            const int16_t* sc = s_col(gst) + tid;
-            const double* sv = s_val(gst) + tid;
+        auto gather = [&](int (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
             mm = __ldg(meta + gq);
+            const uint2 cp = *reinterpret_cast<const uint2*>(s_col(gst) + tid * kRPT);
+            cc[0] = static_cast<int16_t>(cp.x & 0xffff);
+            cc[1] = static_cast<int16_t>(cp.x >> 16);
+            cc[2] = static_cast<int16_t>(cp.y & 0xffff);
+            cc[3] = static_cast<int16_t>(cp.y >> 16);
+            const double2* sv = reinterpret_cast<const double2*>(s_val(gst));
+            const double2 v01 = sv[tid];
+            const double2 v23 = sv[kS3Threads + tid];
+            vv[0] = v01.x;
+            vv[1] = v01.y;
+            vv[2] = v23.x;
+            vv[3] = v23.y;
             const double* xa = x + R0 + meta_sub(mm) * kRows;  // x at the chunk's row 0
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u) cc[u] = sc[u * kS3Threads];
-#pragma unroll
-            for (int u = 0; u < kRPT; ++u) vv[u] = sv[u * kS3Threads];
-#pragma unroll
-            for (int u = 0; u < kRPT; ++u) {
-#ifdef KTB_DIAG_NOGATHER
-                xx[u] = cc[u] >= 0 ? 1.0 : 0.0;
-#else
-                xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
-#endif
-            }
+            for (int u = 0; u < kRPT; ++u) xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
             ++gq;
             gst = (gst + 1 == kStages) ? 0 : gst + 1;
         };
-        // refill a stage that has just been copied out with the chunk
-        // kStages further on
         auto refill = [&](int chunk_done, int st) {
             if (tid == 0 && chunk_done + kStages < Q) {
                 fence_proxy_async_smem();
@@ -296,13 +303,14 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             if (k < Q) refill(k, k % kStages);
         int off = 0;  // ring slot of the current sub-tile's row 0
         int32_t a = R0;
-        double rowsum[kRPT], xi[kRPT], xin[kRPT];
+        double rowsum[kRPT], xi[kRPT], di[kRPT], xin[kRPT], din[kRPT];
 #pragma unroll
         for (int u = 0; u < kRPT; ++u) {
             rowsum[u] = 0.0;
             const int32_t i = a + u * kS3Threads + tid;
             xi[u] = i < R1 ? __ldg(x + i) : 0.0;
-            xin[u] = 0.0;
+            di[u] = i < R1 ? __ldg(diag + i) : 0.0;
+            xin[u] = din[u] = 0.0;
         }
         for (int q = 0; q < Q; q += kRing) {
 #pragma unroll
@@ -313,11 +321,12 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                     const int gq_now = gq, gst_now = gst;
                     if (gathered) gather(cr[kg], vr[kg], xr[kg], mr[kg]);
                     const int m = mr[k];
-                    if (meta_round(m) == 0) {  // x_i of the next sub-tile, and the x front
+                    if (meta_round(m) == 0) {  // next sub-tile's x_i and diagonal, the x front
 #pragma unroll
                         for (int u = 0; u < kRPT; ++u) {
                             const int32_t inext = a + kRows + u * kS3Threads + tid;
                             xin[u] = inext < R1 ? __ldg(x + inext) : 0.0;
+                            din[u] = inext < R1 ? __ldg(diag + inext) : 0.0;
                         }
                         if (tid == 0) {
                             const int64_t front = int64_t(a) + int64_t(kAhead + 1) * kRows + reach;
@@ -326,18 +335,15 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                     }
                     double wv[kRPT];
                     int sl[kRPT];
-                    bool sc[kRPT];
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u) {
                         rowsum[u] += vr[k][u] * xr[k][u];
-                        const int32_t rel = cr[k][u];
-                        sc[u] = rel >= 0 && rel != u * kS3Threads + tid;
-                        sl[u] = wrap(rel + off, W);
-                        wv[u] = sc[u] ? win[sl[u]] : 0.0;
+                        sl[u] = wrap(cr[k][u] + off, W);
+                        wv[u] = cr[k][u] >= 0 ? win[sl[u]] : 0.0;
                     }
 #pragma unroll
                     for (int u = 0; u < kRPT; ++u)
-                        if (sc[u]) win[sl[u]] = wv[u] + vr[k][u] * xi[u];
+                        if (cr[k][u] >= 0) win[sl[u]] = wv[u] + vr[k][u] * xi[u];
                     wait_next();
                     __syncthreads();
                     if (gathered) refill(gq_now, gst_now);
@@ -347,11 +353,12 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                             const int32_t i = a + u * kS3Threads + tid;
                             if (i < R1) {
                                 const int slot = wrap(u * kS3Threads + tid + off, W);
-                                st_hint_f64(y + i, rowsum[u] + win[slot], keep);
+                                st_hint_f64(y + i, di[u] * xi[u] + rowsum[u] + win[slot], keep);
                                 win[slot] = 0.0;
                             }
                             rowsum[u] = 0.0;
                             xi[u] = xin[u];
+                            di[u] = din[u];
                         }
                         __syncthreads();
                         off = wrap(off + kRows, W);
@@ -500,6 +507,7 @@ void s3_setup(ktb_plan* p) {
     std::vector<int64_t> sub_base;
     std::vector<int16_t> scol;
     std::vector<double> sval;
+    std::vector<double> sdiag(n, 0.0);  // dense diagonal stream
     std::vector<int32_t> spill_hi(P), far_i, far_j;
     std::vector<double> far_v;
     std::vector<uint64_t> colmask(static_cast<size_t>(W), 0);
@@ -528,7 +536,11 @@ void s3_setup(ktb_plan* p) {
                 uint64_t rowmask = 0;
                 for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
                     const int32_t j = col[k];
-                    const bool scatter = j != i;
+                    if (j == i) {  // the diagonal goes to the dense d stream
+                        sdiag[i] = val[k];
+                        continue;
+                    }
+                    const bool scatter = true;
                     bool far = scatter && (static_cast<int64_t>(j) - a >= W);
                     uint64_t* cm = (scatter && !far) ? &colmask[static_cast<size_t>(j - a)]
                                                      : nullptr;
@@ -567,9 +579,9 @@ void s3_setup(ktb_plan* p) {
             sval.resize(basei + static_cast<int64_t>(R) * S, 0.0);
             for (int32_t t = 0; t < rows; ++t)
                 for (auto [r, k] : assign[t]) {
-                    const int64_t e = basei + static_cast<int64_t>(r) * S + t;
-                    scol[e] = static_cast<int16_t>(col[k] - a);  // < W <= 32767
-                    sval[e] = val[k];
+                    const int64_t e = basei + static_cast<int64_t>(r) * S;
+                    scol[e + s3_col_pos(t)] = static_cast<int16_t>(col[k] - a);  // < W <= 32767
+                    sval[e + s3_val_pos(t)] = val[k];
                 }
             total_slots += static_cast<int64_t>(R) * S;
         }
@@ -656,6 +668,7 @@ void s3_setup(ktb_plan* p) {
     up32(L.far_i, far_i);
     up32(L.far_j, far_j);
     upd(L.far_v, far_v);
+    upd(L.diag, sdiag);
     KTB_CUDA(cudaStreamSynchronize(st));
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kS3SmemFixed + W * 8)));
@@ -664,14 +677,15 @@ void s3_setup(ktb_plan* p) {
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
     // SELL stream (10 B/slot incl. padding) vs the 12 B/nnz model, + spill
     // write/read + head-row read-modify-write in the fixup; row_ptr unused
-    p->extra_bytes = total_slots * 10 - nnz * 12 - 4 * (n + 1) + so * 8 * 2 + so * 8 * 2;
+    p->extra_bytes = total_slots * 10 + 8 * n - nnz * 12 - 4 * (n + 1) + so * 8 * 2 + so * 8 * 2;
 }
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     k_s3<<<L.ctas, kS3Threads, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
            p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.sell_col.p, L.sell_val.p,
-                        L.cta_base.p, x, y, L.window, L.reach, static_cast<int>(p->m->n),
+                        L.cta_base.p, L.diag.p, x, y, L.window, L.reach,
+                        static_cast<int>(p->m->n),
                         L.spill_hi.p, L.spill_off.p, L.spill.p);
     KTB_LAUNCH();
     if (L.nsegs) {
