@@ -121,8 +121,7 @@ struct SymWindowLayout {
     DBuf<int32_t> cta_chunk;   // ctas+1: round-chunk ranges per block
     DBuf<int32_t> chunk_meta;  // per chunk: sub-tile | last | round
     DBuf<int64_t> cta_base;    // per block: SELL offset of its first chunk
-    DBuf<int16_t> sell_col;    // round-major SELL columns relative to the sub-tile (-1 pad)
-    DBuf<double> sell_val;
+    DBuf<unsigned char> sell;  // per round-chunk: fp64 values then int16 relative columns
     DBuf<double> diag;         // dense diagonal (0 for long rows: the long path adds it)
     DBuf<int32_t> spill_hi;    // per CTA: end of its spill range (start = cta_row[c+1])
     DBuf<int64_t> spill_off;   // per CTA: offset into spill

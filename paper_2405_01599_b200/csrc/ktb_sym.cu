@@ -198,9 +198,9 @@ __device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
 // every SELL entry scatters.
 __global__ void __launch_bounds__(kS3Threads, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
-         const int32_t* __restrict__ chunk_meta, const int16_t* __restrict__ scol,
-         const double* __restrict__ sval, const int64_t* __restrict__ cta_base,
-         const double* __restrict__ diag, const double* __restrict__ x,
+         const int32_t* __restrict__ chunk_meta, const unsigned char* __restrict__ sell,
+         const int64_t* __restrict__ cta_base, const double* __restrict__ diag,
+         const double* __restrict__ x,
          double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
@@ -218,13 +218,14 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     const int q0 = cta_chunk[c];
     const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
     const int32_t* meta = chunk_meta + q0;
-    const int16_t* gcol = scol + cta_base[c];
-    const double* gval = sval + cta_base[c];
+    // chunk q of this block = kStageBytes contiguous bytes (values, then
+    // columns) at sell + (cta_base[c] + q) * kStageBytes: one bulk copy each
+    const unsigned char* gchunk = sell + cta_base[c] * kStageBytes;
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int qq, int st) {  // thread 0 only
         mbar_arrive_expect_tx(&full[st], kStageBytes);
-        tma_load_1d(s_val(st), gval + int64_t(qq) * kRows, kRows * 8, &full[st], pol);
-        tma_load_1d(s_col(st), gcol + int64_t(qq) * kRows, kRows * 2, &full[st], pol);
+        tma_load_1d(smem + st * kStageBytes, gchunk + int64_t(qq) * kStageBytes, kStageBytes,
+                    &full[st], pol);
     };
     // x is first touched by the far reach of the window: pull the initial
     // window and then each sub-tile's new front into L2 ahead of the gathers
@@ -505,8 +506,8 @@ void s3_setup(ktb_plan* p) {
 
     std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
     std::vector<int64_t> sub_base;
-    std::vector<int16_t> scol;
-    std::vector<double> sval;
+    std::vector<unsigned char> sell;  // chunk-interleaved SELL stream
+    int64_t nchunks = 0;
     std::vector<double> sdiag(n, 0.0);  // dense diagonal stream
     std::vector<int32_t> spill_hi(P), far_i, far_j;
     std::vector<double> far_v;
@@ -572,16 +573,25 @@ void s3_setup(ktb_plan* p) {
             }
             for (int32_t sl : touched) colmask[static_cast<size_t>(sl)] = 0;
             R = std::max(R, 1);  // every sub-tile is one pipeline item at least
-            const int64_t basei = static_cast<int64_t>(scol.size());
+            const int64_t basei = static_cast<int64_t>(nchunks);  // in chunks
             sub_base.push_back(basei);
             sub_rounds.push_back(R);
-            scol.resize(basei + static_cast<int64_t>(R) * S, int16_t(-1));
-            sval.resize(basei + static_cast<int64_t>(R) * S, 0.0);
+            nchunks += R;
+            if (sell.size() < static_cast<size_t>(nchunks) * kStageBytes) {
+                const size_t old_sz = sell.size();
+                sell.resize(std::max(static_cast<size_t>(nchunks) * kStageBytes, 2 * old_sz));
+                // fresh chunks: values 0.0, columns -1 (padding)
+                for (size_t ch = old_sz / kStageBytes; ch < sell.size() / kStageBytes; ++ch) {
+                    std::memset(&sell[ch * kStageBytes], 0, kRows * 8);
+                    std::memset(&sell[ch * kStageBytes + kRows * 8], 0xff, kRows * 2);
+                }
+            }
             for (int32_t t = 0; t < rows; ++t)
                 for (auto [r, k] : assign[t]) {
-                    const int64_t e = basei + static_cast<int64_t>(r) * S;
-                    scol[e + s3_col_pos(t)] = static_cast<int16_t>(col[k] - a);  // < W <= 32767
-                    sval[e + s3_val_pos(t)] = val[k];
+                    unsigned char* ch = &sell[static_cast<size_t>(basei + r) * kStageBytes];
+                    reinterpret_cast<double*>(ch)[s3_val_pos(t)] = val[k];
+                    reinterpret_cast<int16_t*>(ch + kRows * 8)[s3_col_pos(t)] =
+                        static_cast<int16_t>(col[k] - a);  // < W <= 32767
                 }
             total_slots += static_cast<int64_t>(R) * S;
         }
@@ -652,11 +662,10 @@ void s3_setup(ktb_plan* p) {
     up32(L.cta_chunk, cta_chunk);
     up32(L.chunk_meta, chunk_meta);
     up64(L.cta_base, cta_base);
-    L.sell_col.alloc(std::max<size_t>(scol.size(), 1));
-    if (!scol.empty())
-        KTB_CUDA(cudaMemcpyAsync(L.sell_col.p, scol.data(), 2 * scol.size(),
+    L.sell.alloc(std::max<int64_t>(nchunks, 1) * kStageBytes);
+    if (nchunks)
+        KTB_CUDA(cudaMemcpyAsync(L.sell.p, sell.data(), nchunks * kStageBytes,
                                  cudaMemcpyHostToDevice, st));
-    upd(L.sell_val, sval);
     up32(L.spill_hi, spill_hi);
     up64(L.spill_off, spill_off);
     L.spill.alloc(std::max<int64_t>(so, 1));
@@ -683,7 +692,7 @@ void s3_setup(ktb_plan* p) {
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     k_s3<<<L.ctas, kS3Threads, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
-           p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.sell_col.p, L.sell_val.p,
+           p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.sell.p,
                         L.cta_base.p, L.diag.p, x, y, L.window, L.reach,
                         static_cast<int>(p->m->n),
                         L.spill_hi.p, L.spill_off.p, L.spill.p);
