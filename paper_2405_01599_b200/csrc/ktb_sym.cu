@@ -391,9 +391,11 @@ __global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ segs,
                                                   const double* __restrict__ spill,
                                                   double* __restrict__ y) {
     constexpr int U = kFixRows / 256;
+    constexpr int MS = 4;  // sources handled with all loads in flight at once
     const int4 sg = segs[blockIdx.x];
     const int d = sg.x;
     const int32_t j0 = sg.y, j1 = sg.z;
+    const int c0 = first_src[d];
     double acc[U];
     bool any[U];
 #pragma unroll
@@ -401,19 +403,31 @@ __global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ segs,
         acc[u] = 0.0;
         any[u] = false;
     }
-    for (int src = first_src[d]; src < d; ++src) {
-        const int32_t s0 = cta_row[src + 1], hi = spill_hi[src];
-        const double* sp = spill + spill_off[src] - s0;
-        double v[U];
+    for (int base = c0; base < d; base += MS) {
+        int32_t s0[MS], hi[MS];
+        const double* sp[MS];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t j = j0 + u * 256 + threadIdx.x;
-            const bool in = j < j1 && j >= s0 && j < hi;
-            v[u] = in ? __ldcg(sp + j) : 0.0;
-            any[u] |= in;
+        for (int k = 0; k < MS; ++k) {
+            const int src = base + k;
+            const bool ok = src < d;
+            s0[k] = ok ? cta_row[src + 1] : 0;
+            hi[k] = ok ? spill_hi[src] : 0;
+            sp[k] = ok ? spill + spill_off[src] - s0[k] : spill;
         }
+        double v[MS][U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc[u] += v[u];
+        for (int k = 0; k < MS; ++k)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t j = j0 + u * 256 + threadIdx.x;
+                const bool in = j < j1 && j >= s0[k] && j < hi[k];
+                v[k][u] = in ? __ldcg(sp[k] + j) : 0.0;
+                any[u] |= in;
+            }
+#pragma unroll
+        for (int k = 0; k < MS; ++k)  // ascending source order
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] += v[k][u];
     }
     double yv[U];
 #pragma unroll
