@@ -119,7 +119,8 @@ struct SymWindowLayout {
     int64_t spill_total = 0;
     DBuf<int32_t> cta_row;     // ctas+1 (bit-exact NNZ_BALANCED boundaries)
     DBuf<int32_t> cta_chunk;   // ctas+1: round-chunk ranges per block
-    DBuf<int32_t> chunk_meta;  // per chunk: sub-tile | last | round
+    DBuf<int32_t> chunk_meta;  // per chunk: sub-tile | last | round (padded, see k_s3)
+    DBuf<int32_t> cta_qreal;   // per block: real chunk count
     DBuf<int64_t> cta_base;    // per block: SELL offset of its first chunk
     DBuf<unsigned char> sell;  // per round-chunk: fp64 values then int16 relative columns
     DBuf<double> diag;         // dense diagonal (0 for long rows: the long path adds it)

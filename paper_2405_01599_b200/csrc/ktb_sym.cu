@@ -26,6 +26,7 @@
 //          round-major SELL order (coalesced), and the kernel separates rounds
 //          with a CTA barrier. The result is deterministic.
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 #include <vector>
 
@@ -148,18 +149,17 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // by one block barrier. The part of each block's region beyond the block
 // (the spill) goes to a global buffer; k_s3_fixup adds it into the next
 // blocks' head rows in ascending source order (deterministic).
-constexpr int kS3Threads = 512;  // threads per block (one block per SM)
-constexpr int kRPT = 4;          // rows per thread: rows t, t+512, t+1024, t+1536
+#ifndef KTB_S3_THREADS
+#define KTB_S3_THREADS 512
+#endif
+constexpr int kS3Threads = KTB_S3_THREADS;  // threads per block (one block per SM)
+constexpr int kRPT = 2048 / kS3Threads;     // rows per thread: t + kS3Threads*u
 constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (2048)
-#ifndef KTB_S3_STAGES
-#define KTB_S3_STAGES 4
-#endif
 #ifndef KTB_S3_GD
-#define KTB_S3_GD 2
+#define KTB_S3_GD 1
 #endif
-constexpr int kStages = KTB_S3_STAGES;  // one round of one sub-tile per stage
-constexpr int kGD = KTB_S3_GD;           // gather distance (stages ahead)
-constexpr int kRing = KTB_S3_GD + 1;     // register ring slots
+constexpr int kStages = 4;  // TMA ring depth = register ring depth (one round-chunk each)
+constexpr int kGD = KTB_S3_GD;  // chunks gathered ahead (copied to registers, x gathers issued)
 // stage = one round of a sub-tile: fp64 values then int16 sub-tile-relative
 // columns, in a thread-swizzled order so each thread reads its 4 values with
 // two conflict-free LDS.128 (chunk k*512+t holds rows t+1024k, t+1024k+512)
@@ -179,6 +179,11 @@ inline int64_t s3_col_pos(int t) {
     return static_cast<int64_t>(th) * kRPT + u;
 }
 
+// column u (sign-extended int16) from its packed word
+__device__ __forceinline__ int col_of(uint32_t w, int u) {
+    return (u & 1) ? static_cast<int>(w) >> 16 : static_cast<int>(w << 16) >> 16;
+}
+
 // unsigned wrap into [0, W) for s in [0, 2W)
 __device__ __forceinline__ int wrap(int s, int W) {
     return static_cast<int>(min(static_cast<unsigned>(s), static_cast<unsigned>(s - W)));
@@ -188,27 +193,27 @@ __device__ __forceinline__ int wrap(int s, int W) {
 // of its sub-tile, bits 8.. sub-tile index local to the block
 __device__ __forceinline__ int meta_round(int m) { return m & 127; }
 __device__ __forceinline__ bool meta_last(int m) { return (m >> 7) & 1; }
-__device__ __forceinline__ int meta_sub(int m) { return m >> 8; }
+__device__ __forceinline__ int meta_sub(int m) { return (m >> 8) & 0x3fffff; }
+// padding chunk (the loop runs a multiple of kStages chunks): no data, no work
+constexpr int kMetaEmpty = 1 << 30;
+__device__ __forceinline__ bool meta_empty(int m) { return m & kMetaEmpty; }
 
-// One block of kS3Threads threads per SM (no producer warp). Thread 0 drives
-// the TMA ring: it issues the first kStages chunks, waits for chunk q+kGD+1
-// before each round barrier (the barrier then publishes the landed stage to
-// everyone), and re-issues a stage's next chunk as soon as the stage has been
-// copied into registers. The diagonal is a separate dense stream (d), so
-// every SELL entry scatters.
+// One block of kS3Threads threads per SM. Thread 0 drives the TMA ring: it
+// issues the first kStages chunks, waits for chunk q+kGD+1 before the round
+// barrier of chunk q (the barrier then publishes the landed stage to every
+// thread), and refills a stage with chunk +kStages right after the barrier
+// that follows the stage's copy into registers. Register ring slot and smem
+// stage of chunk q are both q % kStages, so every shared-memory offset below
+// is a compile-time constant of the unrolled loop.
 __global__ void __launch_bounds__(kS3Threads, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
-         const int32_t* __restrict__ chunk_meta, const unsigned char* __restrict__ sell,
+         const int32_t* __restrict__ chunk_meta, const int32_t* __restrict__ cta_qreal,
+         const unsigned char* __restrict__ sell,
          const int64_t* __restrict__ cta_base, const double* __restrict__ diag,
-         const double* __restrict__ x,
-         double* __restrict__ y, int W, int reach, int n,
+         const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
-    auto s_val = [&](int st) { return reinterpret_cast<double*>(smem + st * kStageBytes); };
-    auto s_col = [&](int st) {
-        return reinterpret_cast<int16_t*>(smem + st * kStageBytes + kRows * 8);
-    };
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
 
@@ -216,10 +221,9 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     const int c = blockIdx.x;
     const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
     const int q0 = cta_chunk[c];
-    const int Q = cta_chunk[c + 1] - q0;  // round-chunks of this block
-    const int32_t* meta = chunk_meta + q0;
-    // chunk q of this block = kStageBytes contiguous bytes (values, then
-    // columns) at sell + (cta_base[c] + q) * kStageBytes: one bulk copy each
+    const int QP = cta_chunk[c + 1] - q0 - kGD;  // chunks incl. padding (multiple of kStages)
+    const int Q = cta_qreal[c];                   // real round-chunks of this block
+    const int32_t* meta = chunk_meta + q0;        // QP + kGD entries
     const unsigned char* gchunk = sell + cta_base[c] * kStageBytes;
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int qq, int st) {  // thread 0 only
@@ -252,121 +256,131 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 
     if (Q > 0) {
         const uint64_t keep = policy_evict_last();  // y head rows are re-read by the fixup
-        int wq = 0, wst = 0, wph = 0;  // next chunk to wait for (tid 0)
-        auto wait_next = [&]() {
-            if (tid == 0 && wq < Q) mbar_wait(&full[wst], wph);
-            ++wq;
-            if (++wst == kStages) {
-                wst = 0;
-                wph ^= 1;
+        uint32_t cr[kStages][kRPT / 2];  // packed int16 sub-tile-relative columns (-1: pad)
+        double vr[kStages][kRPT], xr[kStages][kRPT];
+        int mr[kStages];
+        // copy chunk qq (stage ST) to registers and issue its x gathers
+        auto gather = [&](int qq, auto stc) {
+            constexpr int ST = decltype(stc)::value;
+            const int mm = __ldg(meta + qq);
+            mr[ST] = mm;
+            const bool live = !meta_empty(mm);  // padding chunk: its stage holds no data
+            const unsigned char* sb = smem + ST * kStageBytes;
+            if constexpr (kRPT == 8) {
+                const uint4 cp = reinterpret_cast<const uint4*>(sb + kRows * 8)[tid];
+                cr[ST][0] = cp.x;
+                cr[ST][1] = cp.y;
+                cr[ST][2] = cp.z;
+                cr[ST][3] = cp.w;
+            } else {
+                const uint2 cp = reinterpret_cast<const uint2*>(sb + kRows * 8)[tid];
+                cr[ST][0] = cp.x;
+                cr[ST][1] = cp.y;
             }
-        };
-        int gq = 0, gst = 0;  // next chunk to gather
-        int cr[kRing][kRPT];  // sub-tile-relative column (-1: padding)
-        double vr[kRing][kRPT], xr[kRing][kRPT];
-        int mr[kRing];
-        auto gather = [&](int (&cc)[kRPT], double (&vv)[kRPT], double (&xx)[kRPT], int& mm) {
-            mm = __ldg(meta + gq);
-            const uint2 cp = *reinterpret_cast<const uint2*>(s_col(gst) + tid * kRPT);
-            cc[0] = static_cast<int16_t>(cp.x & 0xffff);
-            cc[1] = static_cast<int16_t>(cp.x >> 16);
-            cc[2] = static_cast<int16_t>(cp.y & 0xffff);
-            cc[3] = static_cast<int16_t>(cp.y >> 16);
-            const double2* sv = reinterpret_cast<const double2*>(s_val(gst));
-            const double2 v01 = sv[tid];
-            const double2 v23 = sv[kS3Threads + tid];
-            vv[0] = v01.x;
-            vv[1] = v01.y;
-            vv[2] = v23.x;
-            vv[3] = v23.y;
+#pragma unroll
+            for (int k2 = 0; k2 < kRPT / 2; ++k2) {
+                const double2 vp = reinterpret_cast<const double2*>(sb)[k2 * kS3Threads + tid];
+                vr[ST][2 * k2] = vp.x;
+                vr[ST][2 * k2 + 1] = vp.y;
+            }
             const double* xa = x + R0 + meta_sub(mm) * kRows;  // x at the chunk's row 0
 #pragma unroll
-            for (int u = 0; u < kRPT; ++u) xx[u] = cc[u] >= 0 ? __ldg(xa + cc[u]) : 0.0;
-            ++gq;
-            gst = (gst + 1 == kStages) ? 0 : gst + 1;
-        };
-        auto refill = [&](int chunk_done, int st) {
-            if (tid == 0 && chunk_done + kStages < Q) {
-                fence_proxy_async_smem();
-                issue(chunk_done + kStages, st);
+            for (int u = 0; u < kRPT; ++u) {
+                const int cu = col_of(cr[ST][u >> 1], u);
+                const double g = __ldg(xa + (live ? max(cu, 0) : 0));  // always a valid address
+                xr[ST][u] = cu >= 0 ? g : 0.0;
             }
         };
         // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1
-#pragma unroll
-        for (int k = 0; k <= kGD; ++k) wait_next();
+        if (tid == 0)
+            for (int k = 0; k <= kGD && k < Q; ++k) mbar_wait(&full[k], 0);
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kGD; ++k)
-            if (gq < Q) gather(cr[k], vr[k], xr[k], mr[k]);
+        static_assert(kGD >= 1 && kGD <= 2, "prologue gathers kGD chunks");
+        gather(0, std::integral_constant<int, 0>{});
+        if (kGD > 1) gather(1, std::integral_constant<int, 1>{});
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kGD; ++k)
-            if (k < Q) refill(k, k % kStages);
+        if (tid == 0)
+            for (int k = 0; k < kGD && k + kStages < Q; ++k) {
+                fence_proxy_async_smem();
+                issue(k + kStages, k);
+            }
         int off = 0;  // ring slot of the current sub-tile's row 0
         int32_t a = R0;
-        double rowsum[kRPT], xi[kRPT], di[kRPT], xin[kRPT], din[kRPT];
+        double rowsum[kRPT], xi[kRPT], di[kRPT], xin[kRPT];
 #pragma unroll
         for (int u = 0; u < kRPT; ++u) {
             rowsum[u] = 0.0;
             const int32_t i = a + u * kS3Threads + tid;
             xi[u] = i < R1 ? __ldg(x + i) : 0.0;
-            di[u] = i < R1 ? __ldg(diag + i) : 0.0;
-            xin[u] = din[u] = 0.0;
+            xin[u] = di[u] = 0.0;
         }
-        for (int q = 0; q < Q; q += kRing) {
+        int wph = 0;  // parity of the stage waited for (flips every kStages chunks)
+        auto body = [&](int q, auto kc) {
+            constexpr int K = decltype(kc)::value;          // stage / slot of chunk q
+            constexpr int KG = (K + kGD) % kStages;         // stage / slot of chunk q+kGD
+            constexpr int KW = (K + kGD + 1) % kStages;     // stage of chunk q+kGD+1
+            gather(q + kGD, std::integral_constant<int, KG>{});  // padded meta: always valid
+            const int m = mr[K];
+            if (meta_empty(m)) {  // padding chunk: keep the barrier cadence only
+                __syncthreads();
+                return;
+            }
+            if (meta_round(m) == 0) {  // this sub-tile's diagonal, next one's x_i, the x front
 #pragma unroll
-            for (int k = 0; k < kRing; ++k) {
-                if (q + k < Q) {
-                    const int kg = (k + kGD) % kRing;
-                    const bool gathered = gq < Q;
-                    const int gq_now = gq, gst_now = gst;
-                    if (gathered) gather(cr[kg], vr[kg], xr[kg], mr[kg]);
-                    const int m = mr[k];
-                    if (meta_round(m) == 0) {  // next sub-tile's x_i and diagonal, the x front
-#pragma unroll
-                        for (int u = 0; u < kRPT; ++u) {
-                            const int32_t inext = a + kRows + u * kS3Threads + tid;
-                            xin[u] = inext < R1 ? __ldg(x + inext) : 0.0;
-                            din[u] = inext < R1 ? __ldg(diag + inext) : 0.0;
-                        }
-                        if (tid == 0) {
-                            const int64_t front = int64_t(a) + int64_t(kAhead + 1) * kRows + reach;
-                            pf(front, front + kRows);
-                        }
-                    }
-                    double wv[kRPT];
-                    int sl[kRPT];
-#pragma unroll
-                    for (int u = 0; u < kRPT; ++u) {
-                        rowsum[u] += vr[k][u] * xr[k][u];
-                        sl[u] = wrap(cr[k][u] + off, W);
-                        wv[u] = cr[k][u] >= 0 ? win[sl[u]] : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < kRPT; ++u)
-                        if (cr[k][u] >= 0) win[sl[u]] = wv[u] + vr[k][u] * xi[u];
-                    wait_next();
-                    __syncthreads();
-                    if (gathered) refill(gq_now, gst_now);
-                    if (meta_last(m)) {  // sub-tile complete: finalise its rows
-#pragma unroll
-                        for (int u = 0; u < kRPT; ++u) {
-                            const int32_t i = a + u * kS3Threads + tid;
-                            if (i < R1) {
-                                const int slot = wrap(u * kS3Threads + tid + off, W);
-                                st_hint_f64(y + i, di[u] * xi[u] + rowsum[u] + win[slot], keep);
-                                win[slot] = 0.0;
-                            }
-                            rowsum[u] = 0.0;
-                            xi[u] = xin[u];
-                            di[u] = din[u];
-                        }
-                        __syncthreads();
-                        off = wrap(off + kRows, W);
-                        a += kRows;
-                    }
+                for (int u = 0; u < kRPT; ++u) {
+                    const int32_t i = a + u * kS3Threads + tid;
+                    di[u] = i < R1 ? __ldg(diag + i) : 0.0;
+                    xin[u] = i + kRows < R1 ? __ldg(x + i + kRows) : 0.0;
+                }
+                if (tid == 0) {
+                    const int64_t front = int64_t(a) + int64_t(kAhead + 1) * kRows + reach;
+                    pf(front, front + kRows);
                 }
             }
+            double wv[kRPT];
+            int sl[kRPT];
+#pragma unroll
+            bool sc[kRPT];
+            for (int u = 0; u < kRPT; ++u) {
+                rowsum[u] += vr[K][u] * xr[K][u];
+                const int cu = col_of(cr[K][u >> 1], u);
+                sc[u] = cu >= 0;
+                sl[u] = wrap(cu + off, W);
+                if (sc[u]) wv[u] = win[sl[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < kRPT; ++u)
+                if (sc[u]) win[sl[u]] = wv[u] + vr[K][u] * xi[u];
+            if (tid == 0 && q + kGD + 1 < Q) mbar_wait(&full[KW], wph ^ (KW <= K ? 1 : 0));
+            __syncthreads();
+            if (tid == 0 && q + kGD < Q && q + kGD + kStages < Q) {
+                fence_proxy_async_smem();  // stage KG was copied out before the barrier
+                issue(q + kGD + kStages, KG);
+            }
+            if (meta_last(m)) {  // sub-tile complete: finalise its rows
+#pragma unroll
+                for (int u = 0; u < kRPT; ++u) {
+                    const int32_t i = a + u * kS3Threads + tid;
+                    if (i < R1) {
+                        const int slot = wrap(u * kS3Threads + tid + off, W);
+                        st_hint_f64(y + i, di[u] * xi[u] + rowsum[u] + win[slot], keep);
+                        win[slot] = 0.0;
+                    }
+                    rowsum[u] = 0.0;
+                    xi[u] = xin[u];
+                }
+                __syncthreads();
+                off = wrap(off + kRows, W);
+                a += kRows;
+            }
+        };
+        static_assert(kStages == 4, "the unrolled body covers four stages");
+        for (int q = 0; q < QP; q += kStages) {
+            body(q, std::integral_constant<int, 0>{});
+            body(q + 1, std::integral_constant<int, 1>{});
+            body(q + 2, std::integral_constant<int, 2>{});
+            body(q + 3, std::integral_constant<int, 3>{});
+            wph ^= 1;
         }
     }
     // spill: the region beyond the block, [R1, spill_hi)
@@ -613,16 +627,21 @@ void s3_setup(ktb_plan* p) {
     }
     cta_sub[P] = static_cast<int32_t>(sub_rounds.size());
     // per-block chunk table: one entry per (sub-tile, round), in SELL order
-    std::vector<int32_t> cta_chunk(P + 1, 0), chunk_meta;
+    // per block: real chunks, padded to a multiple of kStages, + kGD look-ahead
+    std::vector<int32_t> cta_chunk(P + 1, 0), chunk_meta, cta_qreal(P, 0);
     std::vector<int64_t> cta_base(P, 0);
     for (int c = 0; c < P; ++c) {
         cta_chunk[c] = static_cast<int32_t>(chunk_meta.size());
         cta_base[c] = cta_sub[c] < cta_sub[c + 1] ? sub_base[cta_sub[c]] : 0;
+        int q = 0;
         for (int sidx = cta_sub[c]; sidx < cta_sub[c + 1]; ++sidx) {
             const int R = sub_rounds[sidx];
-            for (int r = 0; r < R; ++r)
+            for (int r = 0; r < R; ++r, ++q)
                 chunk_meta.push_back(((sidx - cta_sub[c]) << 8) | r | (r == R - 1 ? 128 : 0));
         }
+        cta_qreal[c] = q;
+        const int qp = (q + kStages - 1) / kStages * kStages;
+        for (; q < qp + kGD; ++q) chunk_meta.push_back(kMetaEmpty);
     }
     cta_chunk[P] = static_cast<int32_t>(chunk_meta.size());
     L.padded = total_slots;
@@ -675,6 +694,7 @@ void s3_setup(ktb_plan* p) {
     };
     up32(L.cta_chunk, cta_chunk);
     up32(L.chunk_meta, chunk_meta);
+    up32(L.cta_qreal, cta_qreal);
     up64(L.cta_base, cta_base);
     L.sell.alloc(std::max<int64_t>(nchunks, 1) * kStageBytes);
     if (nchunks)
@@ -706,7 +726,7 @@ void s3_setup(ktb_plan* p) {
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     k_s3<<<L.ctas, kS3Threads, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
-           p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.sell.p,
+           p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p,
                         L.cta_base.p, L.diag.p, x, y, L.window, L.reach,
                         static_cast<int>(p->m->n),
                         L.spill_hi.p, L.spill_off.p, L.spill.p);
