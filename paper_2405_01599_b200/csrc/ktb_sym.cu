@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     const int c = blockIdx.x;
     const int32_t R0 = cta_row[c], R1 = cta_row[c + 1];
     const int q0 = cta_chunk[c];
-    const int QP = cta_chunk[c + 1] - q0 - kGD;  // chunks incl. padding (multiple of kStages)
+    const int QP = cta_chunk[c + 1] - q0 - kGD - 1;  // chunks incl. padding (multiple of kStages)
     const int Q = cta_qreal[c];                   // real round-chunks of this block
-    const int32_t* meta = chunk_meta + q0;        // QP + kGD entries
+    const int32_t* meta = chunk_meta + q0;        // QP + kGD + 1 entries
     const unsigned char* gchunk = sell + cta_base[c] * kStageBytes;
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int qq, int st) {  // thread 0 only
@@ -260,9 +260,11 @@ __global__ void __launch_bounds__(kS3Threads, 1)
         double vr[kStages][kRPT], xr[kStages][kRPT];
         int mr[kStages];
         // copy chunk qq (stage ST) to registers and issue its x gathers
+        int mnext = __ldg(meta + 0);  // metadata of the next chunk to gather
         auto gather = [&](int qq, auto stc) {
             constexpr int ST = decltype(stc)::value;
-            const int mm = __ldg(meta + qq);
+            const int mm = mnext;
+            mnext = __ldg(meta + qq + 1);  // one chunk ahead: never on the gather's critical path
             mr[ST] = mm;
             const bool live = !meta_empty(mm);  // padding chunk: its stage holds no data
             const unsigned char* sb = smem + ST * kStageBytes;
@@ -287,8 +289,8 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #pragma unroll
             for (int u = 0; u < kRPT; ++u) {
                 const int cu = col_of(cr[ST][u >> 1], u);
-                const double g = __ldg(xa + (live ? max(cu, 0) : 0));  // always a valid address
-                xr[ST][u] = cu >= 0 ? g : 0.0;
+                // always a valid address; the padding select happens at use
+                xr[ST][u] = __ldg(xa + (live ? max(cu, 0) : 0));
             }
         };
         // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1
@@ -342,9 +344,9 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #pragma unroll
             bool sc[kRPT];
             for (int u = 0; u < kRPT; ++u) {
-                rowsum[u] += vr[K][u] * xr[K][u];
                 const int cu = col_of(cr[K][u >> 1], u);
                 sc[u] = cu >= 0;
+                rowsum[u] += sc[u] ? vr[K][u] * xr[K][u] : 0.0;
                 sl[u] = wrap(cu + off, W);
                 if (sc[u]) wv[u] = win[sl[u]];
             }
@@ -627,7 +629,7 @@ void s3_setup(ktb_plan* p) {
     }
     cta_sub[P] = static_cast<int32_t>(sub_rounds.size());
     // per-block chunk table: one entry per (sub-tile, round), in SELL order
-    // per block: real chunks, padded to a multiple of kStages, + kGD look-ahead
+    // per block: real chunks, padded to a multiple of kStages, + kGD + 1 look-ahead
     std::vector<int32_t> cta_chunk(P + 1, 0), chunk_meta, cta_qreal(P, 0);
     std::vector<int64_t> cta_base(P, 0);
     for (int c = 0; c < P; ++c) {
@@ -641,7 +643,7 @@ void s3_setup(ktb_plan* p) {
         }
         cta_qreal[c] = q;
         const int qp = (q + kStages - 1) / kStages * kStages;
-        for (; q < qp + kGD; ++q) chunk_meta.push_back(kMetaEmpty);
+        for (; q < qp + kGD + 1; ++q) chunk_meta.push_back(kMetaEmpty);
     }
     cta_chunk[P] = static_cast<int32_t>(chunk_meta.size());
     L.padded = total_slots;
