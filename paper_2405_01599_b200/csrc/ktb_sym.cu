@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     }
     for (int k = tid; k < W; k += kS3Threads) win[k] = 0.0;
     __syncthreads();
+    // let the fixup grid launch early (programmatic dependent launch): its
+    // blocks take SMs as these retire and wait for this grid's completion
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (Q > 0) {
         const uint64_t keep = policy_evict_last();  // y head rows are re-read by the fixup
@@ -408,7 +411,8 @@ __global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ segs,
                                                   double* __restrict__ y) {
     constexpr int U = kFixRows / 256;
     constexpr int MS = 4;  // sources handled with all loads in flight at once
-    const int4 sg = segs[blockIdx.x];
+    const int4 sg = segs[blockIdx.x];  // plan data: readable before the dependency resolves
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_s3 complete and visible
     const int d = sg.x;
     const int32_t j0 = sg.y, j1 = sg.z;
     const int c0 = first_src[d];
@@ -734,10 +738,21 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
                         L.spill_hi.p, L.spill_off.p, L.spill.p);
     KTB_LAUNCH();
     if (L.nsegs) {
-        k_s3_fixup<<<static_cast<int>(L.nsegs), 256, 0, p->stream>>>(
-            reinterpret_cast<const int4*>(L.segs.p), L.cta_row.p, L.first_src.p, L.spill_hi.p,
-            L.spill_off.p, L.spill.p, y);
-        KTB_LAUNCH();
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(L.nsegs));
+        cfg.blockDim = dim3(256);
+        cfg.stream = p->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        KTB_CUDA(cudaLaunchKernelEx(&cfg, k_s3_fixup, reinterpret_cast<const int4*>(L.segs.p),
+                                    static_cast<const int32_t*>(L.cta_row.p),
+                                    static_cast<const int32_t*>(L.first_src.p),
+                                    static_cast<const int32_t*>(L.spill_hi.p),
+                                    static_cast<const int64_t*>(L.spill_off.p),
+                                    static_cast<const double*>(L.spill.p), y));
     }
 
     if (L.nlong) {
