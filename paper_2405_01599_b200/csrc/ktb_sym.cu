@@ -167,7 +167,7 @@ constexpr int kGD = KTB_S3_GD;  // chunks gathered ahead (copied to registers, x
 constexpr int kStageBytes = kRows * (8 + 2);  // 20480
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 constexpr int kS3SmemFixed = kStages * kStageBytes + kStages * 8 + 128;
-constexpr int kFixRows = 2048;   // rows per fixup block (8 per thread)
+constexpr int kFixRows = 1024;   // rows per fixup block (4 per thread)
 
 // host-side positions of sub-tile row t in a round's value / column arrays
 inline int64_t s3_val_pos(int t) {
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ segs,
                                                   const double* __restrict__ spill,
                                                   double* __restrict__ y) {
     constexpr int U = kFixRows / 256;
-    constexpr int MS = 4;  // sources handled with all loads in flight at once
+    constexpr int MS = 2;  // sources handled with all loads in flight at once
     const int4 sg = segs[blockIdx.x];  // plan data: readable before the dependency resolves
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_s3 complete and visible
     const int d = sg.x;
