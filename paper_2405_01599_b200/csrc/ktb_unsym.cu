@@ -24,15 +24,34 @@ namespace ktb {
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int32_t ldg_i32(const int32_t* p) { return __ldg(p); }
 
-// Streaming loads for the matrix arrays: read once, do not keep in L1.
+// Streaming loads for the matrix arrays: read once, do not keep in L1, evict
+// first from L2 (so x, gathered repeatedly, stays resident).
+__device__ __forceinline__ uint64_t pol_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ double ld_stream_f64(const double* p) {
     double r;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(r) : "l"(p), "l"(pol_first()));
     return r;
 }
 __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
     int32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+                 : "=r"(r) : "l"(p), "l"(pol_first()));
+    return r;
+}
+// x gathers: keep in L2
+__device__ __forceinline__ double ld_x(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol_last()));
     return r;
 }
 
@@ -67,11 +86,11 @@ __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
     }
     double s[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[r] = c[r] >= 0 ? v[r] * ldg_f64(x + c[r]) : 0.0;
+    for (int r = 0; r < R; ++r) s[r] = c[r] >= 0 ? v[r] * ld_x(x + c[r]) : 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
         for (int32_t k = b[r] + sub + V; k < e[r]; k += V)
-            s[r] += ld_stream_f64(val + k) * ldg_f64(x + ld_stream_i32(col + k));
+            s[r] += ld_stream_f64(val + k) * ld_x(x + ld_stream_i32(col + k));
     if (V > 1) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
         }
         double xv[IPT];
 #pragma unroll
-        for (int u = 0; u < IPT; ++u) xv[u] = cc[u] >= 0 ? ldg_f64(x + cc[u]) : 0.0;
+        for (int u = 0; u < IPT; ++u) xv[u] = cc[u] >= 0 ? ld_x(x + cc[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < IPT; ++u) {
             const int i = u * kU2Threads + tid;
@@ -390,7 +409,7 @@ __global__ void __launch_bounds__(kU3Threads) k_u3(const int32_t* __restrict__ c
             vv[u] = i < span ? ld_stream_f64(val + K0 + i) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < E; ++u) xv[u] = cc[u] >= 0 ? ldg_f64(x + cc[u]) : 0.0;
+        for (int u = 0; u < E; ++u) xv[u] = cc[u] >= 0 ? ld_x(x + cc[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < E; ++u) {
             const int i = u * kU3Threads + tid;
