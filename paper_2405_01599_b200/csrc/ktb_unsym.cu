@@ -48,6 +48,16 @@ __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
                  : "=r"(r) : "l"(p), "l"(pol_first()));
     return r;
 }
+__device__ __forceinline__ double ld_plain_f64(const double* p) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int32_t ld_plain_i32(const int32_t* p) {
+    int32_t r;
+    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
 // x gathers: keep in L2
 __device__ __forceinline__ double ld_x(const double* p) {
     double r;
@@ -405,11 +415,11 @@ __global__ void __launch_bounds__(kU3Threads) k_u3(const int32_t* __restrict__ c
 #pragma unroll
         for (int u = 0; u < E; ++u) {
             const int i = u * kU3Threads + tid;
-            cc[u] = i < span ? ld_stream_i32(col + K0 + i) : -1;
-            vv[u] = i < span ? ld_stream_f64(val + K0 + i) : 0.0;
+            cc[u] = i < span ? ld_plain_i32(col + K0 + i) : -1;
+            vv[u] = i < span ? ld_plain_f64(val + K0 + i) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < E; ++u) xv[u] = cc[u] >= 0 ? ld_x(x + cc[u]) : 0.0;
+        for (int u = 0; u < E; ++u) xv[u] = cc[u] >= 0 ? ldg_f64(x + cc[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < E; ++u) {
             const int i = u * kU3Threads + tid;
