@@ -338,3 +338,62 @@ def test_engine_linop_counts(K):
         op.apply(x, y)
     assert eng.calls() == 3 and eng.kernel_seconds() > 0
     assert_close(y, O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x))
+
+
+def test_config3_full_size_all_unsym(K):
+    """config 3 (power-law, n=4,000,000, nnz=39,552,727, 10% empty rows, rows
+    up to 65,536) on every row, U1/U2/U3/U4, against the oracle."""
+    import torch
+
+    a = K.powerlaw()
+    assert a.n == 4_000_000 and a.nnz() == 39_552_727
+    rp, ci, v = a.to_host()
+    x = O.seeded_vector(a.n, 3)
+    yref, absax = O.spmv_ref(a.n, rp, ci, v, x), absax_of(a.n, rp, ci, v, x)
+    xd = torch.from_numpy(x).cuda()
+    for kern in UNSYM:
+        y = _run_unsym(K, a, kern, xd)
+        assert_close(y.cpu().numpy(), yref, absax, kern)
+
+
+def test_config4_properties_full_size(K):
+    """config 4 (512^3, 937,951,232 nnz) is too large for the oracle at full
+    size: size-independent properties instead. A*ones = row sums (exact:
+    6 - #neighbours), linearity A(2x + z) = 2Ax + Az, and a z-slab of the
+    full product equals the oracle on the same slab."""
+    import torch
+
+    from paper_2405_01599_b200 import dist as D
+
+    a = K.stencil7(512, 512, 512)
+    assert a.nnz() == 937_951_232
+    plan = K.DevicePlan(a, K.UnsymKernel.u1_row)
+    n = a.n
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(ones)
+    plan.apply(ones, y)
+    torch.cuda.synchronize()
+    # interior rows: 6 - 6 = 0; boundary rows count missing neighbours
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    z, r = idx // (512 * 512), idx % (512 * 512)
+    yy, xx = r // 512, r % 512
+    missing = sum(((c == 0) | (c == 511)).to(torch.float64) for c in (xx, yy, z))
+    assert torch.equal(y, missing)
+    del missing, idx, z, r, yy, xx
+    x = torch.from_numpy(O.seeded_vector(n, 4)).cuda()
+    zz = torch.from_numpy(O.seeded_vector(n, 5)).cuda()
+    ax, az, ac = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    plan.apply(x, ax)
+    plan.apply(zz, az)
+    plan.apply(2.0 * x + zz, ac)
+    torch.cuda.synchronize()
+    scale = (2.0 * ax.abs() + az.abs() + 16.0)
+    assert ((ac - (2.0 * ax + az)).abs() <= 1e-12 * scale * 8).all()
+    # slab 200..203 of the full product vs the oracle on that slab
+    L = D.slab_layout(512, 512, 512, 100, 128)  # planes 400..403
+    nl, rp, ci, v = D.slab_csr_numpy(L)
+    xl = O.seeded_vector(n, 4)[L.col_base:L.col_base + L.x_local_len]
+    yl = O.spmv_ref(nl, rp, ci, v, xl)
+    absl = O.spmv_ref(nl, rp, ci, np.abs(v), np.abs(xl))
+    got = ax[L.row0:L.row0 + nl].cpu().numpy()
+    assert_close(got, yl, absl, "cfg4 slab")
