@@ -66,11 +66,9 @@ __device__ __forceinline__ double ld_x(const double* p) {
 }
 
 // =============================================================== U1
-// V lanes per row, R consecutive rows per lane group, persistent grid-stride
-// loop software-pipelined over three groups: row bounds of group t+2,
-// columns/values of group t+1 and x gathers + reduction of group t are in
-// flight together, so the row_ptr -> col -> x latency chain is paid once per
-// sweep instead of once per group. Rows longer than V finish in a
+// V lanes per row, R consecutive rows per lane group: the row bounds, then
+// the first V entries of all R rows, then their x gathers are issued before
+// any use (R-fold memory-level parallelism); rows longer than V finish in a
 // lane-strided tail loop.
 template <int V, int R>
 __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
@@ -79,65 +77,40 @@ __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
                                             const double* __restrict__ x, double* __restrict__ y,
                                             int32_t row_begin, int32_t row_end) {
     const int sub = threadIdx.x & (V - 1);
-    const int64_t g0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / V;
-    const int64_t gstride = static_cast<int64_t>(gridDim.x) * blockDim.x / V;
-    const int64_t ngroups = (static_cast<int64_t>(row_end - row_begin) + R - 1) / R;
-    auto bounds = [&](int64_t g, int32_t (&b)[R], int32_t (&e)[R]) {
+    const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / V;
+    const int64_t row0 = row_begin + group * R;
+    int32_t b[R], e[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int64_t row = row_begin + g * R + r;
-            const bool ok = g < ngroups && row < row_end;
-            b[r] = ok ? ldg_i32(rp + row) : 0;
-            e[r] = ok ? ldg_i32(rp + row + 1) : 0;
-        }
-    };
-    auto entries = [&](const int32_t (&b)[R], const int32_t (&e)[R], int32_t (&c)[R],
-                       double (&v)[R]) {
+    for (int r = 0; r < R; ++r) {
+        const int64_t row = row0 + r;
+        b[r] = row < row_end ? ldg_i32(rp + row) : 0;
+        e[r] = row < row_end ? ldg_i32(rp + row + 1) : 0;
+    }
+    int32_t c[R];
+    double v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int32_t k = b[r] + sub;
-            c[r] = k < e[r] ? ld_stream_i32(col + k) : -1;
-            v[r] = k < e[r] ? ld_stream_f64(val + k) : 0.0;
-        }
-    };
-    int32_t b0[R], e0[R], b1[R], e1[R], b2[R], e2[R], c0[R], c1[R];
-    double v0[R], v1[R];
-    int64_t g = g0;
-    bounds(g, b0, e0);
-    bounds(g + gstride, b1, e1);
-    entries(b0, e0, c0, v0);
-    for (; g < ngroups; g += gstride) {
-        bounds(g + 2 * gstride, b2, e2);   // stage A: group t+2
-        entries(b1, e1, c1, v1);           // stage B: group t+1
-        double s[R];                       // stage C: group t
+    for (int r = 0; r < R; ++r) {
+        const int32_t k = b[r] + sub;
+        c[r] = k < e[r] ? ld_stream_i32(col + k) : -1;
+        v[r] = k < e[r] ? ld_stream_f64(val + k) : 0.0;
+    }
+    double s[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) s[r] = c0[r] >= 0 ? v0[r] * ld_x(x + c0[r]) : 0.0;
+    for (int r = 0; r < R; ++r) s[r] = c[r] >= 0 ? v[r] * ld_x(x + c[r]) : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        for (int32_t k = b[r] + sub + V; k < e[r]; k += V)
+            s[r] += ld_stream_f64(val + k) * ld_x(x + ld_stream_i32(col + k));
+    if (V > 1) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            for (int32_t k = b0[r] + sub + V; k < e0[r]; k += V)
-                s[r] += ld_stream_f64(val + k) * ld_x(x + ld_stream_i32(col + k));
-        if (V > 1) {
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+            for (int o = V / 2; o > 0; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o, V);
+    }
+    if (sub == 0) {
 #pragma unroll
-                for (int o = V / 2; o > 0; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o, V);
-        }
-        if (sub == 0) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int64_t row = row_begin + g * R + r;
-                if (row < row_end) y[row] = s[r];
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            b0[r] = b1[r];
-            e0[r] = e1[r];
-            c0[r] = c1[r];
-            v0[r] = v1[r];
-            b1[r] = b2[r];
-            e1[r] = e2[r];
-        }
+        for (int r = 0; r < R; ++r)
+            if (row0 + r < row_end) y[row0 + r] = s[r];
     }
 }
 
@@ -165,9 +138,7 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
 #endif
     constexpr int R = KTB_U1_R;
     const int64_t threads = ceil_div64(rows, R) * V;
-    // persistent: enough blocks to fill every SM (8 x 256 threads), grid-stride beyond
-    const int grid = static_cast<int>(std::min<int64_t>(ceil_div64(threads, 256),
-                                                        int64_t(p->m->sm_count) * 8));
+    const int grid = ceil_div(threads, 256);
     p->ctas = grid;
     const ktb_matrix* m = p->m;
 #define KTB_U1_CASE(VV)                                                                        \
