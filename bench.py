@@ -199,7 +199,8 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-        "config": config_block(cfg, f"reference {eng.selected['name']}"),
+        "config": dict(config_block(cfg, f"reference {eng.selected['name']}"),
+                       l2="n/a (host CPU; inputs resident in host memory)"),
         "impl": "reference",
         "gflops": flops(n, nnz, cfg["sym"]) / t / 1e9,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
