@@ -69,6 +69,28 @@ int ktb_matrix_info(const ktb_matrix* m, int64_t* n, int64_t* nnz, int* kind,
  * parity tests; any output may be NULL. Host destination pointers. */
 int ktb_matrix_download(const ktb_matrix* m, int32_t* row_ptr, int32_t* col_idx, double* values);
 
+/* ------------------------------------------------------- Matrix Market */
+/* Coordinate real general/symmetric files (matrix_market.hpp). Same
+ * accept/reject rules and messages as the reference; parsed in parallel. */
+typedef struct ktb_csr_host ktb_csr_host; /* host CRS, int64 indices */
+/* probe_matrix_market (matrix_market.hpp:154-158): header only. */
+int ktb_mm_probe(const char* path, int64_t* n, int64_t* entries, int* symmetric);
+/* load_matrix_market(path, want_symmetric) (matrix_market.hpp:165-194):
+ * *kind = KTB_SYM_UPPER for the SymCsrMatrix alternative, else KTB_GENERAL. */
+int ktb_mm_read(const char* path, int want_symmetric, ktb_csr_host** out);
+int ktb_csr_host_info(const ktb_csr_host* h, int64_t* n, int64_t* nnz, int* kind);
+/* Copies row_ptr (n+1), col_idx (nnz), values (nnz); NULL skips an array. */
+int ktb_csr_host_copy(const ktb_csr_host* h, int64_t* row_ptr, int64_t* col_idx,
+                      double* values);
+/* Uploads as a device matrix (same as ktb_matrix_create on the arrays). */
+int ktb_csr_host_upload(const ktb_csr_host* h, int device, ktb_matrix** out);
+int ktb_csr_host_destroy(ktb_csr_host* h);
+/* write_matrix_market (matrix_market.hpp:223-239): KTB_GENERAL writes
+ * "i j v"; KTB_SYM_UPPER writes the stored upper triangle transposed
+ * (lower form, "symmetric" banner); values "%.17g". */
+int ktb_mm_write(const char* path, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                 const double* values, int kind);
+
 /* Generators (SURVEY.md §8d recipes), built directly on the device.
  * 3-D 7-point stencil on nx*ny*nz, x fastest, columns sorted
  * (-z,-y,-x,diag,+x,+y,+z); c_xm/c_xp are the -x/+x coefficients

@@ -116,6 +116,14 @@ def ref():
         L.kr_gmres.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _I64, C.c_double, _I64,
                                C.c_int, C.c_int, _f64p, _f64p] + [C.c_void_p] * 8
         L.kr_max_threads.restype = C.c_int
+        L.kr_mm_probe.argtypes = [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64),
+                                  C.POINTER(C.c_int)]
+        L.kr_mm_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.kr_mm_info.argtypes = [C.c_void_p, C.POINTER(_I64), C.POINTER(_I64),
+                                 C.POINTER(C.c_int)]
+        L.kr_mm_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.kr_mm_destroy.argtypes = [C.c_void_p]
+        L.kr_mm_write.argtypes = [C.c_char_p, _I64, _i64p, _i64p, _f64p, C.c_int]
         _ref = L
     return _ref
 
@@ -406,6 +414,34 @@ class Ref:
                        converged=bool(conv.value), recurrence_residual=rec.value,
                        true_residual=tru.value, seconds=sec.value, spmv_seconds=ssec.value,
                        history=hist[: its.value].copy())
+
+    @staticmethod
+    def mm_probe(path):
+        n, e, sym = _I64(), _I64(), C.c_int()
+        _chk_ref(ref().kr_mm_probe(os.fsencode(path), C.byref(n), C.byref(e), C.byref(sym)))
+        return n.value, e.value, bool(sym.value)
+
+    @staticmethod
+    def mm_load(path, want_symmetric):
+        """load_matrix_market -> (kind, n, row_ptr, col_idx, values); kind 1 =
+        SymCsrMatrix. Raises OracleError with the reference's message."""
+        h = C.c_void_p()
+        _chk_ref(ref().kr_mm_load(os.fsencode(path), 1 if want_symmetric else 0, C.byref(h)))
+        try:
+            n, nnz, kind = _I64(), _I64(), C.c_int()
+            ref().kr_mm_info(h, C.byref(n), C.byref(nnz), C.byref(kind))
+            rp = np.empty(n.value + 1, np.int64)
+            ci = np.empty(max(nnz.value, 1), np.int64)
+            v = np.empty(max(nnz.value, 1), np.float64)
+            ref().kr_mm_copy(h, rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+            return kind.value, n.value, rp, ci[: nnz.value], v[: nnz.value]
+        finally:
+            ref().kr_mm_destroy(h)
+
+    @staticmethod
+    def mm_write(path, n, rp, ci, v, sym):
+        rp, ci, v = _csr(rp, ci, v)
+        _chk_ref(ref().kr_mm_write(os.fsencode(path), n, rp, ci, v, 1 if sym else 0))
 
 
 class RefEngine:

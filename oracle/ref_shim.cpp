@@ -13,6 +13,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <variant>
 #include <vector>
 
 #include "ktune/ktune.hpp"
@@ -362,6 +363,62 @@ int kr_gmres(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, c
         *true_res = r.true_residual;
         *seconds = r.elapsed_seconds;
         *spmv_seconds = spmv_s;
+    });
+}
+
+// matrix_market.hpp:154-158
+int kr_mm_probe(const char* path, int64_t* n, int64_t* entries, int* symmetric) {
+    return guarded([&] {
+        const MmInfo h = probe_matrix_market(path);
+        *n = h.n;
+        *entries = h.entries;
+        *symmetric = h.symmetric ? 1 : 0;
+    });
+}
+
+// matrix_market.hpp:165-194; the result is held in a CsrMatrix (kind 1 =
+// the SymCsrMatrix alternative) until kr_mm_copy/kr_mm_destroy.
+struct kr_mm {
+    CsrMatrix a;
+    int kind = 0;
+};
+
+int kr_mm_load(const char* path, int want_symmetric, kr_mm** out) {
+    return guarded([&] {
+        auto r = load_matrix_market(path, want_symmetric != 0);
+        auto* h = new kr_mm();
+        if (std::holds_alternative<SymCsrMatrix>(r)) {
+            h->a = static_cast<CsrMatrix&&>(std::get<SymCsrMatrix>(std::move(r)));
+            h->kind = 1;
+        } else {
+            h->a = std::get<CsrMatrix>(std::move(r));
+        }
+        *out = h;
+    });
+}
+
+void kr_mm_info(const kr_mm* h, int64_t* n, int64_t* nnz, int* kind) {
+    *n = h->a.n;
+    *nnz = h->a.nnz();
+    *kind = h->kind;
+}
+
+void kr_mm_copy(const kr_mm* h, int64_t* rp, int64_t* ci, double* v) {
+    std::memcpy(rp, h->a.row_ptr.data(), sizeof(int64_t) * h->a.row_ptr.size());
+    std::memcpy(ci, h->a.col_idx.data(), sizeof(int64_t) * h->a.col_idx.size());
+    std::memcpy(v, h->a.values.data(), sizeof(double) * h->a.values.size());
+}
+
+void kr_mm_destroy(kr_mm* h) { delete h; }
+
+// matrix_market.hpp:223-239
+int kr_mm_write(const char* path, int64_t n, const int64_t* rp, const int64_t* ci,
+                const double* v, int kind) {
+    return guarded([&] {
+        if (kind == 1)
+            write_matrix_market(path, make_sym(n, rp, ci, v));
+        else
+            write_matrix_market(path, make_csr(n, rp, ci, v));
     });
 }
 

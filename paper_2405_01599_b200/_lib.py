@@ -37,6 +37,14 @@ def load() -> C.CDLL:
         "ktb_matrix_info": ([VP, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_int),
                              C.POINTER(I64), C.POINTER(I64)], C.c_int),
         "ktb_matrix_download": ([VP, VP, VP, VP], C.c_int),
+        "ktb_mm_probe": ([C.c_char_p, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_int)],
+                         C.c_int),
+        "ktb_mm_read": ([C.c_char_p, C.c_int, C.POINTER(VP)], C.c_int),
+        "ktb_csr_host_info": ([VP, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_int)], C.c_int),
+        "ktb_csr_host_copy": ([VP, VP, VP, VP], C.c_int),
+        "ktb_csr_host_upload": ([VP, C.c_int, C.POINTER(VP)], C.c_int),
+        "ktb_csr_host_destroy": ([VP], C.c_int),
+        "ktb_mm_write": ([C.c_char_p, I64, VP, VP, VP, C.c_int], C.c_int),
         "ktb_gen_stencil7": ([I64, I64, I64, C.c_double, C.c_double, C.c_double, C.c_double,
                               C.c_int, C.POINTER(VP)], C.c_int),
         "ktb_gen_stencil27_upper": ([I64, I64, I64, C.c_double, C.c_double, C.c_int,

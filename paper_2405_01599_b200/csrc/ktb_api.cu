@@ -226,6 +226,65 @@ int ktb_matrix_download(const ktb_matrix* m, int32_t* row_ptr, int32_t* col_idx,
     });
 }
 
+int ktb_mm_probe(const char* path, int64_t* n, int64_t* entries, int* symmetric) {
+    return guarded([&] {
+        require(path != nullptr, "matrix market: null path");
+        const MmHeader h = mm_probe(path);
+        if (n) *n = h.n;
+        if (entries) *entries = h.entries;
+        if (symmetric) *symmetric = h.symmetric ? 1 : 0;
+    });
+}
+
+int ktb_mm_read(const char* path, int want_symmetric, ktb_csr_host** out) {
+    return guarded([&] {
+        require(path != nullptr && out != nullptr, "matrix market: null path");
+        *out = mm_read(path, want_symmetric != 0);
+    });
+}
+
+int ktb_csr_host_info(const ktb_csr_host* h, int64_t* n, int64_t* nnz, int* kind) {
+    return guarded([&] {
+        require(h != nullptr, "matrix: null handle");
+        if (n) *n = h->n;
+        if (nnz) *nnz = static_cast<int64_t>(h->col.size());
+        if (kind) *kind = h->kind;
+    });
+}
+
+int ktb_csr_host_copy(const ktb_csr_host* h, int64_t* row_ptr, int64_t* col_idx,
+                      double* values) {
+    return guarded([&] {
+        require(h != nullptr, "matrix: null handle");
+        if (row_ptr) std::memcpy(row_ptr, h->row_ptr.data(), 8 * h->row_ptr.size());
+        if (col_idx && !h->col.empty()) std::memcpy(col_idx, h->col.data(), 8 * h->col.size());
+        if (values && !h->val.empty()) std::memcpy(values, h->val.data(), 8 * h->val.size());
+    });
+}
+
+int ktb_csr_host_upload(const ktb_csr_host* h, int device, ktb_matrix** out) {
+    return guarded([&] {
+        require(h != nullptr, "matrix: null handle");
+        *out = create_matrix(h->n, h->row_ptr.data(), h->col.data(), h->val.data(), h->kind,
+                             device);
+    });
+}
+
+int ktb_csr_host_destroy(ktb_csr_host* h) {
+    return guarded([&] { delete h; });
+}
+
+int ktb_mm_write(const char* path, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                 const double* values, int kind) {
+    return guarded([&] {
+        require(path != nullptr, "matrix market: null path");
+        require(kind == KTB_GENERAL || kind == KTB_SYM_UPPER, "matrix: unknown kind");
+        int64_t mr = 0, bw = 0;
+        validate_host(n, row_ptr, col_idx, kind == KTB_SYM_UPPER, &mr, &bw);
+        mm_write(path, n, row_ptr, col_idx, values, kind);
+    });
+}
+
 int ktb_gen_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, double off, double c_xm,
                      double c_xp, int device, ktb_matrix** out) {
     return guarded(

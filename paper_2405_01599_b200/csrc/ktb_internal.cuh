@@ -101,7 +101,25 @@ struct ktb_matrix {
     ~ktb_matrix();
 };
 
+// Host CRS as loaded from a Matrix Market file (reference index width).
+struct ktb_csr_host {
+    int64_t n = 0;
+    int kind = KTB_GENERAL;
+    std::vector<int64_t> row_ptr, col;
+    std::vector<double> val;
+};
+
 namespace ktb {
+
+// ---- Matrix Market ingest (ktb_mm.cu) --------------------------------------
+struct MmHeader {  // ktune::MmInfo (matrix_market.hpp:18-22)
+    int64_t n = 0, entries = 0;
+    bool symmetric = false;
+};
+MmHeader mm_probe(const std::string& path);
+ktb_csr_host* mm_read(const std::string& path, bool want_symmetric);
+void mm_write(const std::string& path, int64_t n, const int64_t* rp, const int64_t* ci,
+              const double* v, int kind);
 
 // ---- plans ---------------------------------------------------------------
 struct MergeCoord {

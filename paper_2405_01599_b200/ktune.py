@@ -245,6 +245,94 @@ def stencil7_slab(nx, ny, nz, z0, z1, diag=6.0, off=-1.0, device=0) -> DeviceCsr
     return DeviceCsr(h, False)
 
 
+# ---------------------------------------------------------- Matrix Market
+@dataclass
+class MmInfo:  # matrix_market.hpp:18-22
+    n: int = 0
+    entries: int = 0
+    symmetric: bool = False
+
+
+def _path(path) -> bytes:
+    import os
+
+    return os.fsencode(path)
+
+
+def probe_matrix_market(path) -> MmInfo:  # matrix_market.hpp:154-158
+    n, e, s = I64(), I64(), C.c_int()
+    _check(_lib.load().ktb_mm_probe(_path(path), C.byref(n), C.byref(e), C.byref(s)))
+    return MmInfo(n.value, e.value, bool(s.value))
+
+
+class _HostCsr:
+    """Owner of a ktb_csr_host handle (the parsed file, int64 host CRS)."""
+
+    def __init__(self, path, want_symmetric: bool):
+        self.h = C.c_void_p()
+        _check(_lib.load().ktb_mm_read(_path(path), int(bool(want_symmetric)), C.byref(self.h)))
+        n, nnz, kind = I64(), I64(), C.c_int()
+        _check(_lib.load().ktb_csr_host_info(self.h, C.byref(n), C.byref(nnz), C.byref(kind)))
+        self.n, self.nnz, self.kind = n.value, nnz.value, kind.value
+
+    def arrays(self):
+        rp = np.empty(self.n + 1, np.int64)
+        ci = np.empty(max(self.nnz, 1), np.int64)
+        v = np.empty(max(self.nnz, 1), np.float64)
+        _check(_lib.load().ktb_csr_host_copy(self.h, rp.ctypes.data, ci.ctypes.data,
+                                             v.ctypes.data))
+        return rp, ci[: self.nnz], v[: self.nnz]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.load().ktb_csr_host_destroy(self.h)
+            self.h = None
+
+
+def load_matrix_market(path, want_symmetric: bool, device: int = 0):
+    """matrix_market.hpp:165-194: SymCsrMatrix when want_symmetric (a general
+    file must then be exactly symmetric), else CsrMatrix (a symmetric file is
+    expanded). Same messages as the reference."""
+    h = _HostCsr(path, want_symmetric)
+    rp, ci, v = h.arrays()
+    cls = SymCsrMatrix if h.kind == 1 else CsrMatrix
+    return cls(h.n, rp, ci, v, device=device)
+
+
+def load_matrix_market_general(path, device: int = 0) -> CsrMatrix:  # :196-198
+    return load_matrix_market(path, False, device)
+
+
+def load_matrix_market_symmetric(path, device: int = 0) -> SymCsrMatrix:  # :200-202
+    return load_matrix_market(path, True, device)
+
+
+def load_matrix_market_device(path, want_symmetric: bool, device: int = 0) -> DeviceCsr:
+    """Parse and upload straight to the device (no numpy copy of the CRS)."""
+    h = _HostCsr(path, want_symmetric)
+    d = C.c_void_p()
+    _check(_lib.load().ktb_csr_host_upload(h.h, device, C.byref(d)))
+    return DeviceCsr(d, h.kind == 1)
+
+
+def write_matrix_market(path, a) -> None:
+    """matrix_market.hpp:223-239: a CsrMatrix writes "general", a
+    SymCsrMatrix its upper storage transposed ("symmetric", lower form)."""
+    if isinstance(a, DeviceCsr):
+        rp, ci, v = a.to_host()
+        n, kind = a.n, a._kind
+    else:
+        rp, ci, v, n, kind = a.row_ptr, a.col_idx, a.values, a.n, a._kind
+    rp = np.ascontiguousarray(rp, np.int64)
+    require(len(rp) == n + 1, "csr: row_ptr length != n+1")
+    ci = np.ascontiguousarray(ci, np.int64)
+    v = np.ascontiguousarray(v, np.float64)
+    require(len(ci) == len(v), "csr: col_idx/values length mismatch")
+    require(rp[-1] == len(v), "csr: row_ptr[n] != nnz")
+    _check(_lib.load().ktb_mm_write(_path(path), n, rp.ctypes.data, ci.ctypes.data,
+                                    v.ctypes.data, kind))
+
+
 # -------------------------------------------------------------- artefacts
 @dataclass
 class RowPartition:  # partition.hpp:15-23
