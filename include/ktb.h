@@ -82,7 +82,8 @@ int ktb_csr_host_info(const ktb_csr_host* h, int64_t* n, int64_t* nnz, int* kind
 /* Copies row_ptr (n+1), col_idx (nnz), values (nnz); NULL skips an array. */
 int ktb_csr_host_copy(const ktb_csr_host* h, int64_t* row_ptr, int64_t* col_idx,
                       double* values);
-/* Uploads as a device matrix (same as ktb_matrix_create on the arrays). */
+/* Uploads as a device matrix (int32 indices): parallel narrowing through a
+ * pinned staging ring; the CRS was already validated by ktb_mm_read. */
 int ktb_csr_host_upload(const ktb_csr_host* h, int device, ktb_matrix** out);
 int ktb_csr_host_destroy(ktb_csr_host* h);
 /* write_matrix_market (matrix_market.hpp:223-239): KTB_GENERAL writes

@@ -265,8 +265,7 @@ int ktb_csr_host_copy(const ktb_csr_host* h, int64_t* row_ptr, int64_t* col_idx,
 int ktb_csr_host_upload(const ktb_csr_host* h, int device, ktb_matrix** out) {
     return guarded([&] {
         require(h != nullptr, "matrix: null handle");
-        *out = create_matrix(h->n, h->row_ptr.data(), h->col.data(), h->val.data(), h->kind,
-                             device);
+        *out = mm_upload(*h, device);
     });
 }
 

@@ -118,6 +118,7 @@ struct MmHeader {  // ktune::MmInfo (matrix_market.hpp:18-22)
 };
 MmHeader mm_probe(const std::string& path);
 ktb_csr_host* mm_read(const std::string& path, bool want_symmetric);
+ktb_matrix* mm_upload(const ktb_csr_host& h, int device);
 void mm_write(const std::string& path, int64_t n, const int64_t* rp, const int64_t* ci,
               const double* v, int kind);
 

@@ -495,6 +495,94 @@ ktb_csr_host* mm_read(const std::string& path, bool want_symmetric) {  // :165-1
     return out.release();
 }
 
+// Loaded CRS -> device matrix. The arrays were validated by mm_read, so
+// this pass only narrows the indices to the device's int32 layout and
+// gathers the row statistics, in parallel, through a pinned staging ring
+// (two 32 MB halves) so the DMA of one chunk overlaps the narrowing of the
+// next.
+ktb_matrix* mm_upload(const ktb_csr_host& h, int device) {
+    const int64_t n = h.n;
+    const int64_t nnz = static_cast<int64_t>(h.col.size());
+    require(n < (int64_t(1) << 31) - 1 && nnz < (int64_t(1) << 31) - 1,
+            "csr: n or nnz >= 2^31 does not fit the int32 device layout");
+    DeviceGuard g(device);
+    auto m = std::make_unique<ktb_matrix>();
+    m->device = device;
+    KTB_CUDA(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
+    m->n = n;
+    m->ncols = n;
+    m->nnz = nnz;
+    m->kind = h.kind;
+    m->row_ptr.alloc(n + 1);
+    m->col.alloc(nnz);
+    m->val.alloc(nnz);
+    const int T = static_cast<int>(std::max<size_t>(1, std::min<size_t>(host_threads(), 64)));
+    std::vector<int64_t> mx(T, 0), bw(T, 0);
+    parallel_for(T, [&](int t) {  // row statistics (csr.hpp max_row_nnz, bandwidth)
+        for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i) {
+            const int64_t b = h.row_ptr[i], e = h.row_ptr[i + 1];
+            mx[t] = std::max(mx[t], e - b);
+            if (e > b) bw[t] = std::max(bw[t], h.col[e - 1] - i);
+        }
+    });
+    m->max_row_nnz = *std::max_element(mx.begin(), mx.end());
+    m->bandwidth = *std::max_element(bw.begin(), bw.end());
+
+    constexpr size_t kHalf = size_t(32) << 20;
+    char* stage = nullptr;
+    KTB_CUDA(cudaHostAlloc(&stage, 2 * kHalf, cudaHostAllocDefault));
+    cudaStream_t st = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    auto cleanup = [&] {
+        if (st) cudaStreamSynchronize(st);
+        for (auto& e : done)
+            if (e) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+        cudaFreeHost(stage);
+    };
+    try {
+        KTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& e : done) KTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        int half = 0;
+        bool used[2] = {false, false};
+        // fill(dst, k0, k1): writes elements [k0, k1) of one array into dst
+        auto pump = [&](void* dev, size_t elem, int64_t count, auto&& fill) {
+            const int64_t per = static_cast<int64_t>(kHalf / elem);
+            for (int64_t k0 = 0; k0 < count; k0 += per) {
+                const int64_t k1 = std::min(count, k0 + per);
+                char* buf = stage + half * kHalf;
+                if (used[half]) KTB_CUDA(cudaEventSynchronize(done[half]));
+                parallel_for(T, [&](int t) {
+                    const int64_t a = k0 + (k1 - k0) * t / T, b = k0 + (k1 - k0) * (t + 1) / T;
+                    fill(buf, k0, a, b);
+                });
+                KTB_CUDA(cudaMemcpyAsync(static_cast<char*>(dev) + k0 * elem, buf,
+                                         (k1 - k0) * elem, cudaMemcpyHostToDevice, st));
+                KTB_CUDA(cudaEventRecord(done[half], st));
+                used[half] = true;
+                half ^= 1;
+            }
+        };
+        pump(m->row_ptr.p, 4, n + 1, [&](char* buf, int64_t k0, int64_t a, int64_t b) {
+            auto* d = reinterpret_cast<int32_t*>(buf) - k0;
+            for (int64_t k = a; k < b; ++k) d[k] = static_cast<int32_t>(h.row_ptr[k]);
+        });
+        pump(m->col.p, 4, nnz, [&](char* buf, int64_t k0, int64_t a, int64_t b) {
+            auto* d = reinterpret_cast<int32_t*>(buf) - k0;
+            for (int64_t k = a; k < b; ++k) d[k] = static_cast<int32_t>(h.col[k]);
+        });
+        pump(m->val.p, 8, nnz, [&](char* buf, int64_t k0, int64_t a, int64_t b) {
+            std::memcpy(buf + (a - k0) * 8, h.val.data() + a, (b - a) * 8);
+        });
+        KTB_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    return m.release();
+}
+
 // matrix_market.hpp:206-239: general as "i j v", symmetric storage (upper)
 // transposed to the conventional lower form; values "%.17g".
 void mm_write(const std::string& path, int64_t n, const int64_t* rp, const int64_t* ci,

@@ -63,3 +63,20 @@ def test_general_file_engine(K, tmp_path):
     y = np.empty(n)
     K.UnsymEngine(a, choice).op().apply(x, y)
     _check(y, n, rp, ci, v, x)
+
+
+def test_upload_ring_bytes_and_stats(K, tmp_path):
+    """ktb_csr_host_upload (pinned staging ring, parallel narrowing) gives the
+    same device bytes and row statistics as ktb_matrix_create, on a file big
+    enough to cross several 32 MB staging chunks."""
+    n, rp, ci, v = matgen.stencil27_upper(100, 100, 100)  # 13.7M stored entries
+    v = v + np.random.default_rng(2).standard_normal(len(v))
+    path = str(tmp_path / "big.mtx")
+    K.write_matrix_market(path, K.SymCsrMatrix(n, rp, ci, v))
+    d = K.load_matrix_market_device(path, True)
+    ref = K.SymCsrMatrix(n, rp, ci, v).dev
+    got = d.dev.download()
+    want = ref.download()
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+    assert (d.dev.max_row_nnz, d.dev.bandwidth) == (ref.max_row_nnz, ref.bandwidth)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--sym", action="store_true")
     ap.add_argument("--ref", action="store_true", help="also time the reference loader")
     ap.add_argument("--keep", default=None)
+    ap.add_argument("--device", action="store_true", help="also time file -> device matrix")
     a = ap.parse_args()
     import matgen  # tests/matgen.py
 
@@ -49,6 +50,20 @@ def main():
     print(f"ktb_mm_read: {best:.3f}s  {size / best / 1e9:.2f} GB/s  "
           f"{m.nnz() / best / 1e6:.1f} M entries/s  ({os.cpu_count()} host cores)")
     assert np.array_equal(b.col_idx, m.col_idx) and np.array_equal(b.values, m.values)
+    if a.device:
+        import torch
+
+        K.load_matrix_market_device(path, a.sym)  # warm the CUDA context
+        torch.cuda.synchronize()
+        best_d = 1e9
+        for _ in range(3):
+            t0 = time.perf_counter()
+            d = K.load_matrix_market_device(path, a.sym)
+            torch.cuda.synchronize()
+            best_d = min(best_d, time.perf_counter() - t0)
+            del d
+        print(f"file -> device (ktb_mm_read + ktb_csr_host_upload): {best_d:.3f}s  "
+              f"{size / best_d / 1e9:.2f} GB/s of text")
     if a.ref:
         t0 = time.perf_counter()
         r = O.Ref.mm_load(path, a.sym)
