@@ -225,6 +225,42 @@ typedef struct {
 int ktb_gmres(ktb_plan* A, const double* b, double* x, int64_t m, double tol, int64_t max_iters,
               double* history, ktb_gmres_result* res);
 
+/* ------------------------------------------- general row-block sharding */
+/* SURVEY.md §8f row 3 (no reference counterpart: the reference is single
+ * process). Rank `rank` of `world` owns rows and x entries
+ * [boundaries[rank], boundaries[rank+1]) of an n_global-row CRS; row_ptr /
+ * col_idx / values are ITS rows (local row_ptr, GLOBAL column ids). The
+ * rows split into A_d (owned columns, square, a regular ktb_matrix: any
+ * kernel, any plan, the selector) and A_o (rows touching other ranks'
+ * columns, over the ghost index space). Ghost columns are sorted ascending,
+ * so they arrive grouped by owner rank: one receive buffer = the ghost
+ * vector. create/info/ghosts/set_sends are host-only (no device calls). */
+typedef struct ktb_dist ktb_dist;
+int ktb_dist_create(int64_t n_global, int world, const int64_t* boundaries, int rank,
+                    const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                    ktb_dist** out);
+int ktb_dist_destroy(ktb_dist* d);
+/* n_local rows; n_ghost columns; stored entries of A_d / A_o; rows of A_o. */
+int ktb_dist_info(const ktb_dist* d, int64_t* n_local, int64_t* n_ghost, int64_t* nnz_local,
+                  int64_t* nnz_ghost, int64_t* ghost_rows);
+/* Ghost column ids (global, ascending; n_ghost) and per-owner counts (world). */
+int ktb_dist_ghosts(const ktb_dist* d, int64_t* ghost_cols, int64_t* recv_counts);
+/* What this rank sends: per-peer counts (world) and the owned global column
+ * ids concatenated in peer order (each peer's ghost list for this rank). */
+int ktb_dist_set_sends(ktb_dist* d, const int64_t* send_counts, const int64_t* send_cols);
+/* Host copies of the split (CPU tests): A_d as CRS (n_local+1, nnz_local);
+ * A_o as (row ids, row_ptr ghost_rows+1, ghost-space columns, values). */
+int ktb_dist_local_csr(const ktb_dist* d, int32_t* row_ptr, int32_t* col_idx, double* values);
+int ktb_dist_ghost_csr(const ktb_dist* d, int32_t* rows, int32_t* row_ptr, int32_t* col_idx,
+                       double* values);
+/* Upload both blocks to `device`; the A_d handle stays owned by d. */
+int ktb_dist_upload(ktb_dist* d, int device);
+int ktb_dist_local_matrix(ktb_dist* d, ktb_matrix** local);
+/* send_buf[k] = x_owned[send_idx[k]] (device pointers). */
+int ktb_dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, void* stream);
+/* y += A_o x_ghost (device pointers); run after A_d x_owned -> y. */
+int ktb_dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, void* stream);
+
 /* ---------------------------------------------------------- host memory */
 int ktb_host_alloc(size_t bytes, void** out);  /* pinned */
 int ktb_host_free(void* p);

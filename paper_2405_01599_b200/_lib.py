@@ -45,6 +45,17 @@ def load() -> C.CDLL:
         "ktb_csr_host_upload": ([VP, C.c_int, C.POINTER(VP)], C.c_int),
         "ktb_csr_host_destroy": ([VP], C.c_int),
         "ktb_mm_write": ([C.c_char_p, I64, VP, VP, VP, C.c_int], C.c_int),
+        "ktb_dist_create": ([I64, C.c_int, VP, C.c_int, VP, VP, VP, C.POINTER(VP)], C.c_int),
+        "ktb_dist_destroy": ([VP], C.c_int),
+        "ktb_dist_info": ([VP] + [C.POINTER(I64)] * 5, C.c_int),
+        "ktb_dist_ghosts": ([VP, VP, VP], C.c_int),
+        "ktb_dist_set_sends": ([VP, VP, VP], C.c_int),
+        "ktb_dist_local_csr": ([VP, VP, VP, VP], C.c_int),
+        "ktb_dist_ghost_csr": ([VP, VP, VP, VP, VP], C.c_int),
+        "ktb_dist_upload": ([VP, C.c_int], C.c_int),
+        "ktb_dist_local_matrix": ([VP, C.POINTER(VP)], C.c_int),
+        "ktb_dist_pack": ([VP, VP, VP, VP], C.c_int),
+        "ktb_dist_ghost_spmv": ([VP, VP, VP, VP], C.c_int),
         "ktb_gen_stencil7": ([I64, I64, I64, C.c_double, C.c_double, C.c_double, C.c_double,
                               C.c_int, C.POINTER(VP)], C.c_int),
         "ktb_gen_stencil27_upper": ([I64, I64, I64, C.c_double, C.c_double, C.c_int,

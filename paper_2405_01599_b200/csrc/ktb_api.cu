@@ -284,6 +284,101 @@ int ktb_mm_write(const char* path, int64_t n, const int64_t* row_ptr, const int6
     });
 }
 
+int ktb_dist_create(int64_t n_global, int world, const int64_t* boundaries, int rank,
+                    const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                    ktb_dist** out) {
+    return guarded(
+        [&] { *out = dist_create(n_global, world, boundaries, rank, row_ptr, col_idx, values); });
+}
+
+int ktb_dist_destroy(ktb_dist* d) {
+    return guarded([&] {
+        if (d) {
+            if (d->device >= 0) {
+                DeviceGuard g(d->device);
+                delete d;
+            } else {
+                delete d;
+            }
+        }
+    });
+}
+
+int ktb_dist_info(const ktb_dist* d, int64_t* n_local, int64_t* n_ghost, int64_t* nnz_local,
+                  int64_t* nnz_ghost, int64_t* ghost_rows) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        if (n_local) *n_local = d->n_loc;
+        if (n_ghost) *n_ghost = static_cast<int64_t>(d->ghosts.size());
+        if (nnz_local) *nnz_local = static_cast<int64_t>(d->d_v.size());
+        if (nnz_ghost) *nnz_ghost = static_cast<int64_t>(d->o_v.size());
+        if (ghost_rows) *ghost_rows = static_cast<int64_t>(d->o_rows.size());
+    });
+}
+
+int ktb_dist_ghosts(const ktb_dist* d, int64_t* ghost_cols, int64_t* recv_counts) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        if (ghost_cols) std::copy(d->ghosts.begin(), d->ghosts.end(), ghost_cols);
+        if (recv_counts) std::copy(d->recv_counts.begin(), d->recv_counts.end(), recv_counts);
+    });
+}
+
+int ktb_dist_set_sends(ktb_dist* d, const int64_t* send_counts, const int64_t* send_cols) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        dist_set_sends(d, send_counts, send_cols);
+    });
+}
+
+int ktb_dist_local_csr(const ktb_dist* d, int32_t* row_ptr, int32_t* col_idx, double* values) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        if (row_ptr) std::copy(d->d_rp.begin(), d->d_rp.end(), row_ptr);
+        if (col_idx) std::copy(d->d_ci.begin(), d->d_ci.end(), col_idx);
+        if (values) std::copy(d->d_v.begin(), d->d_v.end(), values);
+    });
+}
+
+int ktb_dist_ghost_csr(const ktb_dist* d, int32_t* rows, int32_t* row_ptr, int32_t* col_idx,
+                       double* values) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        if (rows) std::copy(d->o_rows.begin(), d->o_rows.end(), rows);
+        if (row_ptr) std::copy(d->o_rp.begin(), d->o_rp.end(), row_ptr);
+        if (col_idx) std::copy(d->o_ci.begin(), d->o_ci.end(), col_idx);
+        if (values) std::copy(d->o_v.begin(), d->o_v.end(), values);
+    });
+}
+
+int ktb_dist_upload(ktb_dist* d, int device) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        dist_upload(d, device);
+    });
+}
+
+int ktb_dist_local_matrix(ktb_dist* d, ktb_matrix** local) {
+    return guarded([&] {
+        require(d != nullptr && d->local != nullptr, "dist: not uploaded");
+        *local = d->local;
+    });
+}
+
+int ktb_dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, void* stream) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        dist_pack(d, x_owned, send_buf, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ktb_dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, void* stream) {
+    return guarded([&] {
+        require(d != nullptr, "dist: null handle");
+        dist_ghost_spmv(d, x_ghost, y, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int ktb_gen_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, double off, double c_xm,
                      double c_xp, int device, ktb_matrix** out) {
     return guarded(

@@ -109,6 +109,27 @@ struct ktb_csr_host {
     std::vector<double> val;
 };
 
+// One rank's share of a row-block sharded CRS (ktb_dist.cu).
+struct ktb_dist {
+    int64_t n_global = 0, row0 = 0, n_loc = 0;
+    int world = 1, rank = 0;
+    std::vector<int64_t> bnd;
+    // host split
+    std::vector<int32_t> d_rp, d_ci, o_rows, o_rp, o_ci;
+    std::vector<double> d_v, o_v;
+    std::vector<int64_t> ghosts, recv_counts;
+    std::vector<int32_t> send_idx;
+    std::vector<int64_t> send_counts;
+    bool sends_set = false;
+    // device
+    int device = -1;
+    ktb_matrix* local = nullptr;  // A_d
+    ktb::DBuf<int32_t> dev_orows, dev_orp, dev_oci, dev_send;
+    ktb::DBuf<double> dev_ov;
+    int lanes = 1;
+    ~ktb_dist() { delete local; }
+};
+
 namespace ktb {
 
 // ---- Matrix Market ingest (ktb_mm.cu) --------------------------------------
@@ -121,6 +142,14 @@ ktb_csr_host* mm_read(const std::string& path, bool want_symmetric);
 ktb_matrix* mm_upload(const ktb_csr_host& h, int device);
 void mm_write(const std::string& path, int64_t n, const int64_t* rp, const int64_t* ci,
               const double* v, int kind);
+
+// ---- general row-block sharding (ktb_dist.cu) -----------------------------
+ktb_dist* dist_create(int64_t n_global, int world, const int64_t* bnd, int rank,
+                      const int64_t* rp, const int64_t* ci, const double* v);
+void dist_set_sends(ktb_dist* d, const int64_t* counts, const int64_t* cols);
+void dist_upload(ktb_dist* d, int device);
+void dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, cudaStream_t s);
+void dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, cudaStream_t s);
 
 // ---- plans ---------------------------------------------------------------
 struct MergeCoord {

@@ -208,3 +208,253 @@ def local_exchange(layouts, xs) -> None:
             for pp, ss, _ in halo_plan(src_L):
                 if pp == L.rank:
                     x[r] = src_x[ss]
+
+
+# ======================================================================
+# General row-block sharding of an arbitrary CRS.
+# The split and ghost bookkeeping are native (libktb ktb_dist_*, host-only
+# until upload); this layer exchanges the ghost lists once and drives the
+# per-apply pack -> NCCL send/recv -> A_d x (overlapped) -> y += A_o x_g.
+# ======================================================================
+def nnz_balanced_boundaries(row_ptr, world: int) -> np.ndarray:
+    """partition.hpp:28-55 NNZ_BALANCED on host: boundary p is the smallest
+    row r with row_ptr[r] * P >= p * nnz (exact int64), r < n."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    n, nnz = len(rp) - 1, int(rp[-1])
+    out = np.empty(world + 1, np.int64)
+    out[0], out[world] = 0, n
+    scaled = rp[:-1] * world
+    for p in range(1, world):
+        out[p] = np.searchsorted(scaled, p * nnz, side="left")
+    return out
+
+
+class DistCsr:
+    """One rank's share of a row-block sharded CRS (ktb_dist handle).
+    row_ptr/col_idx/values: this rank's rows (local row_ptr, GLOBAL columns)."""
+
+    def __init__(self, n_global, boundaries, rank, world, row_ptr, col_idx, values):
+        import ctypes as C
+
+        from . import _lib
+        from .ktune import _check
+
+        self._C, self._L, self._check = C, _lib.load(), _check
+        self.boundaries = np.ascontiguousarray(boundaries, np.int64)
+        self.rank, self.world, self.n_global = rank, world, n_global
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        ci = np.ascontiguousarray(col_idx, np.int64)
+        v = np.ascontiguousarray(values, np.float64)
+        self.h = C.c_void_p()
+        _check(self._L.ktb_dist_create(n_global, world, self.boundaries.ctypes.data, rank,
+                                       rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                       C.byref(self.h)))
+        vals = [C.c_int64() for _ in range(5)]
+        _check(self._L.ktb_dist_info(self.h, *[C.byref(x) for x in vals]))
+        (self.n_local, self.n_ghost, self.nnz_local, self.nnz_ghost,
+         self.ghost_rows) = [x.value for x in vals]
+        self.ghosts = np.empty(max(self.n_ghost, 1), np.int64)
+        self.recv_counts = np.empty(world, np.int64)
+        _check(self._L.ktb_dist_ghosts(self.h, self.ghosts.ctypes.data,
+                                       self.recv_counts.ctypes.data))
+        self.ghosts = self.ghosts[: self.n_ghost]
+        self.send_counts = None
+        self.send_cols = None
+
+    @property
+    def row0(self) -> int:
+        return int(self.boundaries[self.rank])
+
+    def recv_offsets(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.recv_counts)])
+
+    def send_offsets(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.send_counts)])
+
+    def set_sends(self, counts, cols) -> None:
+        self.send_counts = np.ascontiguousarray(counts, np.int64)
+        self.send_cols = np.ascontiguousarray(cols, np.int64)
+        self._check(self._L.ktb_dist_set_sends(self.h, self.send_counts.ctypes.data,
+                                               self.send_cols.ctypes.data))
+
+    def local_csr(self):
+        rp = np.empty(self.n_local + 1, np.int32)
+        ci = np.empty(max(self.nnz_local, 1), np.int32)
+        v = np.empty(max(self.nnz_local, 1), np.float64)
+        self._check(self._L.ktb_dist_local_csr(self.h, rp.ctypes.data, ci.ctypes.data,
+                                               v.ctypes.data))
+        return rp, ci[: self.nnz_local], v[: self.nnz_local]
+
+    def ghost_csr(self):
+        rows = np.empty(max(self.ghost_rows, 1), np.int32)
+        rp = np.empty(self.ghost_rows + 1, np.int32)
+        ci = np.empty(max(self.nnz_ghost, 1), np.int32)
+        v = np.empty(max(self.nnz_ghost, 1), np.float64)
+        self._check(self._L.ktb_dist_ghost_csr(self.h, rows.ctypes.data, rp.ctypes.data,
+                                               ci.ctypes.data, v.ctypes.data))
+        return rows[: self.ghost_rows], rp, ci[: self.nnz_ghost], v[: self.nnz_ghost]
+
+    def upload(self, device: int):
+        """Both blocks to `device`; returns A_d as a (borrowed) DeviceCsr."""
+        from .ktune import DeviceCsr
+
+        self._check(self._L.ktb_dist_upload(self.h, device))
+        m = self._C.c_void_p()
+        self._check(self._L.ktb_dist_local_matrix(self.h, self._C.byref(m)))
+        return DeviceCsr(m, False, owner=self)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.ktb_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def exchange_ghost_lists(dc: DistCsr, group=None, device=None):
+    """Once per matrix: every rank learns which of its owned columns each peer
+    needs. Counts by all_gather (world x world), lists by one batch of
+    point-to-point transfers. Returns (send_counts, send_cols)."""
+    import torch
+    import torch.distributed as dist
+
+    W, r = dc.world, dc.rank
+    dev = "cpu" if device is None else f"cuda:{device}"
+    mine = torch.as_tensor(dc.recv_counts, dtype=torch.int64, device=dev)
+    allc = [torch.empty(W, dtype=torch.int64, device=dev) for _ in range(W)]
+    dist.all_gather(allc, mine, group=group)
+    send_counts = np.array([int(allc[p][r]) for p in range(W)], np.int64)
+    ro = dc.recv_offsets()
+    so = np.concatenate([[0], np.cumsum(send_counts)])
+    ghosts = torch.as_tensor(dc.ghosts, dtype=torch.int64, device=dev)
+    out = torch.empty(int(so[-1]), dtype=torch.int64, device=dev)
+    ops = []
+    for p in range(W):
+        if p == r:
+            continue
+        if dc.recv_counts[p]:
+            ops.append(dist.P2POp(dist.isend, ghosts[ro[p]:ro[p + 1]], p, group))
+        if send_counts[p]:
+            ops.append(dist.P2POp(dist.irecv, out[so[p]:so[p + 1]], p, group))
+    if ops:
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+    return send_counts, out.cpu().numpy()
+
+
+class DistCsrSpMV:
+    """y = A x for an arbitrary CRS sharded by rows over the process group
+    (one rank per GPU, NCCL). x and y are row-sharded like A; the local
+    diagonal block runs the selected/tuned kernel, overlapped with the ghost
+    exchange; the off-diagonal block accumulates after it."""
+
+    def __init__(self, n_global, boundaries, rank, world, row_ptr, col_idx, values, device,
+                 kernel=None, group=None, sends=None, dc=None):
+        import torch
+
+        from . import ktune as K
+
+        self.dc = dc or DistCsr(n_global, boundaries, rank, world, row_ptr, col_idx, values)
+        if sends is None:
+            counts, cols = exchange_ghost_lists(self.dc, group, device)
+        else:  # precomputed (single-process emulation: local_send_lists)
+            counts, cols = sends
+        self.dc.set_sends(counts, cols)
+        self.device, self.group = device, group
+        self.A_d = self.dc.upload(device)
+        if kernel is None and self.A_d.nnz() > 0:
+            choice, self.report = K.select_spmv_unsym(self.A_d)
+            self.plan = choice.plan
+        else:
+            self.plan = K.DevicePlan(self.A_d, int(kernel if kernel is not None else 0))
+            self.report = None
+        dev = f"cuda:{device}"
+        self.xg = torch.zeros(max(self.dc.n_ghost, 1), dtype=torch.float64, device=dev)
+        self.send = torch.empty(max(int(counts.sum()), 1), dtype=torch.float64, device=dev)
+        self._ro, self._so = self.dc.recv_offsets(), self.dc.send_offsets()
+
+    @property
+    def n_local(self) -> int:
+        return self.dc.n_local
+
+    def _stream(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def pack(self, x_owned) -> None:
+        self.dc._check(self.dc._L.ktb_dist_pack(self.dc.h, x_owned.data_ptr(),
+                                                self.send.data_ptr(), self._stream()))
+
+    def exchange(self):
+        import torch.distributed as dist
+
+        ops = []
+        for p in range(self.dc.world):
+            if p == self.dc.rank:
+                continue
+            if self.dc.send_counts[p]:
+                ops.append(dist.P2POp(dist.isend, self.send[self._so[p]:self._so[p + 1]], p,
+                                      self.group))
+            if self.dc.recv_counts[p]:
+                ops.append(dist.P2POp(dist.irecv, self.xg[self._ro[p]:self._ro[p + 1]], p,
+                                      self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def ghost_spmv(self, y) -> None:
+        self.dc._check(self.dc._L.ktb_dist_ghost_spmv(self.dc.h, self.xg.data_ptr(),
+                                                      y.data_ptr(), self._stream()))
+
+    def apply(self, x_owned, y):
+        """One sharded y = A x (torch CUDA tensors of length n_local)."""
+        self.pack(x_owned)
+        reqs = self.exchange()
+        if self.A_d.nnz() > 0:
+            self.plan.apply(x_owned, y)
+        else:
+            y.zero_()
+        for q in reqs:
+            q.wait()
+        self.ghost_spmv(y)
+        return y
+
+    def launches_per_apply(self) -> int:
+        return int(self.dc.send_counts.sum() > 0) + self.plan.launches + int(self.dc.ghost_rows > 0)
+
+
+def local_send_lists(dcs):
+    """What exchange_ghost_lists returns on each rank, computed in one
+    process from all ranks' DistCsr objects."""
+    W = len(dcs)
+    out = []
+    for r in range(W):
+        counts = np.zeros(W, np.int64)
+        cols = []
+        for p in range(W):
+            if p == r:
+                continue
+            ro = dcs[p].recv_offsets()
+            seg = dcs[p].ghosts[ro[r]:ro[r + 1]]
+            counts[p] = len(seg)
+            cols.append(seg)
+        out.append((counts, np.concatenate(cols) if cols else np.zeros(0, np.int64)))
+    return out
+
+
+def local_ghost_exchange(spmvs, xs) -> None:
+    """Single-process stand-in for the per-apply exchange over all ranks'
+    DistCsrSpMV objects on one device (plain copies of the same slices)."""
+    for s, x in zip(spmvs, xs):
+        s.pack(x)
+    for s in spmvs:
+        r = s.dc.rank
+        for p in range(s.dc.world):
+            if p == r or not s.dc.recv_counts[p]:
+                continue
+            src = spmvs[p]
+            so = src._so
+            s.xg[s._ro[p]:s._ro[p + 1]] = src.send[so[r]:so[r + 1]]

@@ -88,8 +88,9 @@ def kernel_name(k) -> str:  # spmv.hpp:18-35
 class _DeviceMatrix:
     """Owner of a ktb_matrix handle."""
 
-    def __init__(self, handle: C.c_void_p):
+    def __init__(self, handle: C.c_void_p, owned: bool = True):
         self.h = handle
+        self.owned = owned  # borrowed handles (e.g. a ktb_dist's A_d) are not destroyed here
         n, nnz, mx, bw = I64(), I64(), I64(), I64()
         kind = C.c_int()
         _check(_lib.load().ktb_matrix_info(handle, C.byref(n), C.byref(nnz), C.byref(kind),
@@ -99,7 +100,8 @@ class _DeviceMatrix:
 
     def close(self):
         if getattr(self, "h", None):
-            _lib.load().ktb_matrix_destroy(self.h)
+            if self.owned:
+                _lib.load().ktb_matrix_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -182,8 +184,9 @@ class DeviceCsr:
     """A matrix generated directly on the device (SURVEY.md §8d recipes);
     behaves like CsrMatrix/SymCsrMatrix for every call here."""
 
-    def __init__(self, handle: C.c_void_p, sym: bool):
-        self._dev = _DeviceMatrix(handle)
+    def __init__(self, handle: C.c_void_p, sym: bool, owner=None):
+        self._owner = owner  # keeps the owner of a borrowed handle alive
+        self._dev = _DeviceMatrix(handle, owned=owner is None)
         self._kind = 1 if sym else 0
         self.n = self._dev.n
 
