@@ -353,10 +353,56 @@ def run_gpu(args, cfg):
     return 0
 
 
+class _GeneralShard:
+    """--shard: an arbitrary config matrix split by NNZ_BALANCED row blocks
+    over the ranks (dist.DistCsrSpMV: native split + ghost map, NCCL ghost
+    exchange overlapped with the diagonal block). Same fields as DistSpMV."""
+
+    def __init__(self, cfg, rank, ws, local):
+        import types
+
+        import torch
+
+        from paper_2405_01599_b200 import _lib
+        from paper_2405_01599_b200 import dist as D
+
+        if cfg["seed"] == 3:  # config 3: the native multi-threaded host generator
+            from paper_2405_01599_b200 import ktune as K
+
+            n, rp, ci, v = K.powerlaw_host()
+        else:
+            import matgen
+
+            n, rp, ci, v = cfg["host"](matgen)
+        self.n_glob, self.nnz_glob = n, int(rp[-1])
+        b = D.nnz_balanced_boundaries(rp, ws)
+        r0, r1 = int(b[rank]), int(b[rank + 1])
+        self.sp = D.DistCsrSpMV(n, b, rank, ws, rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]],
+                                v[rp[r0]:rp[r1]], local)
+        del rp, ci, v
+        self.nnz = self.sp.A_d.nnz() + self.sp.dc.nnz_ghost
+        self.kname = ("u%d" % (self.sp.plan.kernel + 1)) if self.sp.A_d.nnz() else "none"
+        self.L = types.SimpleNamespace(owned_offset=0, n_local=self.sp.n_local)
+        dev = f"cuda:{local}"
+        self.x = torch.empty(max(self.sp.n_local, 1), dtype=torch.float64, device=dev)
+        assert _lib.load().ktb_seeded_vector(self.sp.n_local, cfg["seed"], r0, self.x.data_ptr(),
+                                             torch.cuda.current_stream(local).cuda_stream) == 0
+        self.y = torch.empty_like(self.x)
+
+    def apply(self):
+        n = self.sp.n_local
+        return self.sp.apply(self.x[:n], self.y[:n])
+
+    def launches_per_apply(self):
+        return self.sp.launches_per_apply()
+
+
 def run_gpu_dist(args, cfg):
     """Config 4: z-slab row-block sharding over the ranks (paper_2405_01599_b200
-    .dist), NCCL P2P halo exchange overlapped with the interior rows. Fixed
-    total problem: strong scaling; value = whole-matrix bytes / max-rank time."""
+    .dist), NCCL P2P halo exchange overlapped with the interior rows; with
+    --shard (configs 1/3): general NNZ_BALANCED row blocks with a ghost-column
+    exchange. Fixed total problem: strong scaling; value = whole-matrix bytes
+    / max-rank time."""
     import torch
 
     ws, rank, local = dist_env()
@@ -368,10 +414,20 @@ def run_gpu_dist(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2405_01599_b200 import dist as D
 
-    nx = ny = nz = 512
-    shard = D.DistSpMV(nx, ny, nz, rank, ws, local, seed=cfg["seed"])
-    n_glob = nx * ny * nz
-    nnz_glob = 7 * n_glob - 6 * nx * nx  # 7-pt stencil with Dirichlet boundary
+    if args.config == 4:
+        nx = ny = nz = 512
+        shard = D.DistSpMV(nx, ny, nz, rank, ws, local, seed=cfg["seed"])
+        n_glob = nx * ny * nz
+        nnz_glob = 7 * n_glob - 6 * nx * nx  # 7-pt stencil with Dirichlet boundary
+        klabel = "u1 (z-slab shards, NCCL halo)"
+        par = f"row-block z-slabs x{ws}, one-plane halo"
+        rlabel = "u1 (rank 0 slab: interior + 2 boundary planes)"
+    else:
+        shard = _GeneralShard(cfg, rank, ws, local)
+        n_glob, nnz_glob = shard.n_glob, shard.nnz_glob
+        klabel = f"{shard.kname} on A_d + ghost accumulate (general row blocks, NCCL ghosts)"
+        par = f"NNZ_BALANCED row blocks x{ws}, ghost-column exchange"
+        rlabel = f"{shard.kname} (rank 0 diagonal block) + k_ghost_acc"
     B = min_bytes(n_glob, nnz_glob)
     B_local = min_bytes(shard.L.n_local, shard.nnz)
     F = flops(n_glob, nnz_glob, False)
@@ -439,13 +495,12 @@ def run_gpu_dist(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-            "config": dict(config_block(cfg, "u1 (z-slab shards, NCCL halo)"),
-                           parallelism=f"row-block z-slabs x{ws}, one-plane halo"),
+            "config": dict(config_block(cfg, klabel), parallelism=par),
             "gflops": F / (ms / 1e3) / 1e9,
             "pct_hbm_peak_per_gpu": 100.0 * achieved / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "u1 (rank 0 slab: interior + 2 boundary planes)",
+                         "kernel": rlabel,
                          "bytes_per_launch": B_local},
             "e2e": {"value": B / (e2e / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
@@ -549,6 +604,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS) + [5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="configs 1/3: general row-block sharding over the ranks "
+                         "(default: replicas)")
     ap.add_argument("--warm-seconds", type=float, default=1.0,
                     help="keep warming up at least this long (clocks settle); 0 under ncu")
     args = ap.parse_args()
@@ -556,7 +614,7 @@ def main():
     cfg = CONFIGS.get(args.config, {"workload": "cfg5", "sym": False, "seed": 5})
     if args.impl == "reference":
         return run_reference(args, cfg)
-    if args.config == 4:
+    if args.config == 4 or (args.shard and args.config in (1, 3)):
         return run_gpu_dist(args, cfg)
     if args.config == 5:
         return run_gmres(args, cfg)

@@ -323,6 +323,8 @@ def exchange_ghost_lists(dc: DistCsr, group=None, device=None):
     import torch.distributed as dist
 
     W, r = dc.world, dc.rank
+    if W == 1:  # nothing to exchange (and no process group is required)
+        return np.zeros(1, np.int64), np.zeros(0, np.int64)
     dev = "cpu" if device is None else f"cuda:{device}"
     mine = torch.as_tensor(dc.recv_counts, dtype=torch.int64, device=dev)
     allc = [torch.empty(W, dtype=torch.int64, device=dev) for _ in range(W)]
