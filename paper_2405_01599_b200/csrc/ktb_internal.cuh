@@ -199,7 +199,8 @@ struct ktb_plan {
     int launches = 1;
     int64_t extra_bytes = 0;
     // U2 merge-path tiles / U3 BSS lanes
-    ktb::DBuf<ktb::MergeCoord> coords;  // U2: tiles+1 merge coordinates
+    ktb::DBuf<ktb::MergeCoord> coords;  // U2 merge path: tiles+1 merge coordinates
+    ktb::DBuf<int32_t> wrow;            // U2 warp tiles: first row of each tile (+ n)
     int64_t jl = 0;                     // U3: lane count (reference BssPlan jl)
     int64_t nq = 0;                     // U3: nonempty rows
     ktb::DBuf<uint32_t> flag_bits;      // U3: row_start_flag, 1 bit per nonzero

@@ -307,12 +307,195 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
     }
 }
 
+// ---- U2, warp tiles --------------------------------------------------------
+// Each warp owns T = 32*IPT consecutive nonzeros [z0, z0+T) (nnz-balanced)
+// and the rows whose end falls in (z0, z0+T] (wrow[w] .. wrow[w+1]). No
+// block-level synchronisation: the 8 warps of a CTA are independent.
+//   1. striped, coalesced col/val loads; x gathers (all IPT in flight);
+//   2. meanwhile the row ends of the tile become a T-bit mask (smem, one
+//      atomicOr per row) plus the ordinal -> row list; empty rows get y = 0;
+//   3. products go to a padded per-warp smem buffer (stride IPT+2 doubles,
+//      so the blocked 16-byte reads below are bank-conflict free) and each
+//      thread sums its IPT consecutive products, emitting every row that
+//      ends inside them;
+//   4. the head segment of each thread takes the carry of the lanes before
+//      it: one flag-aware warp scan (the flags are the ballot of "has an
+//      end", so only the value is shuffled);
+//   5. the open row at the tile end is the tile carry (k_fixup_carries).
+#ifndef KTB_U2W_MINB
+#define KTB_U2W_MINB 5
+#endif
+template <int IPT>
+__global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y,
+                                                          const int32_t* __restrict__ wrow,
+                                                          int64_t nnz, int64_t tiles,
+                                                          int32_t* __restrict__ carry_row,
+                                                          double* __restrict__ carry_val) {
+    constexpr int T = 32 * IPT;
+    static_assert(IPT == 4 || IPT == 8, "u2w: IPT");
+    // thread b's IPT products are b's row of the buffer; its 16-byte chunks
+    // are XOR-swizzled by the row's position among the rows sharing a 128-byte
+    // line (b >> SH), so the striped 8-byte stores and the blocked 16-byte
+    // loads are both bank-conflict free
+    constexpr int SH = IPT == 8 ? 1 : 2;
+    __shared__ __align__(16) double s_prod[8][T];
+    // s_end[i] = 1 + row ending at item i of the tile, 0 = no row ends there
+    __shared__ __align__(16) int32_t s_end[8][T];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (w >= tiles) return;
+    const int64_t z0 = w * T;
+    const int cnt = static_cast<int>(nnz - z0 < T ? nnz - z0 : T);
+    const int32_t ra = __ldg(wrow + w), rb = __ldg(wrow + w + 1);
+#pragma unroll
+    for (int q = 0; q < IPT; q += 4)
+        *reinterpret_cast<int4*>(&s_end[warp][lane * IPT + q]) = make_int4(0, 0, 0, 0);
+
+    int32_t c[IPT];
+    double v[IPT];
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const int i = u * 32 + lane;
+        c[u] = i < cnt ? ld_stream_i32(col + z0 + i) : -1;
+        v[u] = i < cnt ? ld_stream_f64(val + z0 + i) : 0.0;
+    }
+    // first 32 row bounds in flight together with the gathers
+    bool in = ra + lane < rb;
+    int32_t rb_ = in ? __ldg(rp + ra + lane) : 0;
+    int32_t re_ = in ? __ldg(rp + ra + lane + 1) : 0;
+    double xv[IPT];
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) xv[u] = c[u] >= 0 ? ld_x(x + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+        const int i = u * 32 + lane;
+        const int b = i / IPT, j = i % IPT;
+        s_prod[warp][b * IPT + ((((j >> 1) ^ ((b >> SH) & (IPT / 2 - 1))) << 1) | (j & 1))] =
+            v[u] * xv[u];
+    }
+    __syncwarp();  // s_end zeroed before the scatter below
+    for (int32_t r0 = ra;;) {
+        const int32_t r = r0 + lane;
+        if (in) {
+            if (re_ > rb_)
+                s_end[warp][re_ - 1 - z0] = r + 1;
+            else
+                y[r] = 0.0;  // empty row
+        }
+        r0 += 32;
+        if (r0 >= rb) break;
+        in = r0 + lane < rb;
+        rb_ = in ? __ldg(rp + r0 + lane) : 0;
+        re_ = in ? __ldg(rp + r0 + lane + 1) : 0;
+    }
+    __syncwarp();
+
+    double p[IPT];
+#pragma unroll
+    for (int cc = 0; cc < IPT / 2; ++cc) {
+        const int phys = (cc ^ ((lane >> SH) & (IPT / 2 - 1))) << 1;
+        const double2 q = *reinterpret_cast<const double2*>(&s_prod[warp][lane * IPT + phys]);
+        p[2 * cc] = q.x;
+        p[2 * cc + 1] = q.y;
+    }
+    int32_t er[IPT];
+#pragma unroll
+    for (int q = 0; q < IPT; q += 4) {
+        const int4 e4 = *reinterpret_cast<const int4*>(&s_end[warp][lane * IPT + q]);
+        er[q] = e4.x;
+        er[q + 1] = e4.y;
+        er[q + 2] = e4.z;
+        er[q + 3] = e4.w;
+    }
+    double run = 0.0, head = 0.0;
+    int32_t head_row = 0;
+    bool has = false;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        run += p[j];
+        if (er[j]) {
+            if (has) {
+                y[er[j] - 1] = run;
+            } else {
+                head = run;
+                head_row = er[j] - 1;
+            }
+            has = true;
+            run = 0.0;
+        }
+    }
+    // S(t) = tail_t + (has_t ? 0 : S(t-1)) over the lanes
+    const uint32_t F = __ballot_sync(0xffffffffu, has);
+    double S = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double up = __shfl_up_sync(0xffffffffu, S, d);
+        if (lane >= d && ((F >> (lane - d + 1)) & ((1u << d) - 1u)) == 0u) S += up;
+    }
+    double cin = __shfl_up_sync(0xffffffffu, S, 1);
+    if (lane == 0) cin = 0.0;
+    if (has) y[head_row] = head + cin;
+    if (lane == 31) {
+        carry_row[w] = rb;
+        carry_val[w] = S;
+    }
+}
+
+// first row whose end lies beyond z = w*T (w = 0: row 0)
+__global__ void k_u2w_rows(const int32_t* __restrict__ rp, int64_t n, int64_t nnz, int64_t T,
+                           int64_t tiles, int32_t* __restrict__ wrow) {
+    const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (w > tiles) return;
+    if (w == 0) {
+        wrow[0] = 0;
+        return;
+    }
+    const int64_t z = min(w * T, nnz);
+    int64_t lo = 0, hi = n;  // first r in [0, n) with rp[r+1] > z, else n
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (static_cast<int64_t>(rp[mid + 1]) > z)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    wrow[w] = static_cast<int32_t>(lo);
+}
+
+// param: 4 / 8 = warp tiles with that many items per thread (default 8);
+// 104 / 108 / 112 = the merge-path kernel with IPT = param - 100.
 void u2_setup(ktb_plan* p) {
     if (p->param <= 0) p->param = 8;
-    int ipt = static_cast<int>(p->param);
-    if (ipt != 4 && ipt != 8 && ipt != 12) ipt = 8;
-    p->param = ipt;
+    const int prm = static_cast<int>(p->param);
     const ktb_matrix* m = p->m;
+    if (prm == 4 || prm == 8) {
+        const int64_t T = 32 * prm;
+        p->tiles = std::max<int64_t>(1, ceil_div64(m->nnz, T));
+        p->wrow.alloc(p->tiles + 1);
+        p->carry_row.alloc(p->tiles);
+        p->carry_val.alloc(p->tiles);
+#ifdef KTB_U2W_CARVEOUT
+        KTB_CUDA(cudaFuncSetAttribute(k_u2w<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      KTB_U2W_CARVEOUT));
+        KTB_CUDA(cudaFuncSetAttribute(k_u2w<8>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      KTB_U2W_CARVEOUT));
+#endif
+        k_u2w_rows<<<ceil_div(p->tiles + 1, 256), 256, 0, p->stream>>>(
+            m->row_ptr.p, m->n, m->nnz, T, p->tiles, p->wrow.p);
+        KTB_LAUNCH();
+        KTB_CUDA(cudaStreamSynchronize(p->stream));
+        p->ctas = ceil_div64(p->tiles, 8);
+        p->launches = 2;
+        p->extra_bytes = p->tiles * (4 + 4 + 8) * 2;
+        return;
+    }
+    int ipt = prm - 100;
+    if (ipt != 4 && ipt != 8 && ipt != 12) ipt = 8;
+    p->param = 100 + ipt;
     const int64_t tile_items = static_cast<int64_t>(kU2Threads) * ipt;
     p->tiles = std::max<int64_t>(1, ceil_div64(m->n + m->nnz, tile_items));
     p->coords.alloc(p->tiles + 1);
@@ -329,6 +512,25 @@ void u2_setup(ktb_plan* p) {
 
 void u2_run(ktb_plan* p, const double* x, double* y) {
     const ktb_matrix* m = p->m;
+    const int prm = static_cast<int>(p->param);
+    if (prm < 100) {
+        const int grid = static_cast<int>(ceil_div64(p->tiles, 8));
+#define KTB_U2W_CASE(I)                                                                      \
+    case I:                                                                                   \
+        k_u2w<I><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,         \
+                                              p->wrow.p, m->nnz, p->tiles, p->carry_row.p,    \
+                                              p->carry_val.p);                                \
+        break;
+        switch (prm) {
+            KTB_U2W_CASE(4)
+            KTB_U2W_CASE(8)
+            default: throw Invalid("u2: bad items per thread");
+        }
+#undef KTB_U2W_CASE
+        KTB_LAUNCH();
+        fixup_run(p, y);
+        return;
+    }
     const int grid = static_cast<int>(p->tiles);
 #define KTB_U2_CASE(I)                                                                       \
     case I:                                                                                   \
@@ -336,7 +538,7 @@ void u2_run(ktb_plan* p, const double* x, double* y) {
                                                     p->coords.p, p->carry_row.p,              \
                                                     p->carry_val.p);                          \
         break;
-    switch (p->param) {
+    switch (prm - 100) {
         KTB_U2_CASE(4)
         KTB_U2_CASE(8)
         KTB_U2_CASE(12)

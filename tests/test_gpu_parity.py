@@ -397,3 +397,30 @@ def test_config4_properties_full_size(K):
     absl = O.spmv_ref(nl, rp, ci, np.abs(v), np.abs(xl))
     got = ax[L.row0:L.row0 + nl].cpu().numpy()
     assert_close(got, yl, absl, "cfg4 slab")
+
+
+def test_u2_all_tile_variants(K):
+    """Every U2 implementation (warp tiles IPT 4/8, merge path 104/108/112)
+    on random, skewed, empty-row and long-row matrices."""
+    rng = np.random.default_rng(7)
+    mats = []
+    for t in range(8):
+        n = int(rng.integers(1, 3000))
+        mats.append(matgen.random_csr(n, float(rng.choice([0.001, 0.01, 0.05])), rng,
+                                      skew=bool(t % 2), empty_frac=0.3 * (t % 3 == 2)))
+    n = 6000  # one huge row, singletons, a run of empties, trailing empties
+    rows = [np.arange(0, n, dtype=np.int64)] + [np.array([i], np.int64) for i in range(1, 3000)]
+    rows += [np.array([], np.int64)] * 1500 + [np.array([5, 9], np.int64)] * 1000
+    rows += [np.array([], np.int64)] * (n - len(rows))
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    mats.append((n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1]))))
+    mats.append((4, np.zeros(5, np.int64), np.zeros(0, np.int64), np.zeros(0)))  # all empty
+    for n, rp, ci, v in mats:
+        x = rng.uniform(-1, 1, n)
+        a = K.CsrMatrix(n, rp, ci, v)
+        yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
+        for prm in (4, 8, 104, 108, 112):
+            plan = K.DevicePlan(a, K.UnsymKernel.u2_nnz, prm)
+            y = np.full(n, np.nan)
+            plan.apply(x, y)
+            assert_close(y, yref, absax, (n, prm))
