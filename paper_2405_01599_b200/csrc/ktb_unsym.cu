@@ -342,6 +342,10 @@ __global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __rest
     // line (b >> SH), so the striped 8-byte stores and the blocked 16-byte
     // loads are both bank-conflict free
     constexpr int SH = IPT == 8 ? 1 : 2;
+    // s_end: 16-byte chunks of 4 ints, IPT/4 per thread row, 32/IPT rows per
+    // 128-byte line -> chunk swizzle by (b >> ESH)
+    constexpr int ESH = IPT == 8 ? 2 : 3;
+    constexpr int EMASK = IPT / 4 - 1;
     __shared__ __align__(16) double s_prod[8][T];
     // s_end[i] = 1 + row ending at item i of the tile, 0 = no row ends there
     __shared__ __align__(16) int32_t s_end[8][T];
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __rest
     const int32_t ra = __ldg(wrow + w), rb = __ldg(wrow + w + 1);
 #pragma unroll
     for (int q = 0; q < IPT; q += 4)
-        *reinterpret_cast<int4*>(&s_end[warp][lane * IPT + q]) = make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(&s_end[warp][lane * IPT + q]) = make_int4(0, 0, 0, 0);  // own row
 
     int32_t c[IPT];
     double v[IPT];
@@ -381,8 +385,11 @@ __global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __rest
     for (int32_t r0 = ra;;) {
         const int32_t r = r0 + lane;
         if (in) {
-            if (re_ > rb_)
-                s_end[warp][re_ - 1 - z0] = r + 1;
+            if (re_ > rb_) {
+                const int i = static_cast<int>(re_ - 1 - z0);
+                const int b = i / IPT, j = i % IPT;
+                s_end[warp][b * IPT + ((((j >> 2) ^ ((b >> ESH) & EMASK)) << 2) | (j & 3))] = r + 1;
+            }
             else
                 y[r] = 0.0;  // empty row
         }
@@ -405,7 +412,8 @@ __global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __rest
     int32_t er[IPT];
 #pragma unroll
     for (int q = 0; q < IPT; q += 4) {
-        const int4 e4 = *reinterpret_cast<const int4*>(&s_end[warp][lane * IPT + q]);
+        const int phys = ((q >> 2) ^ ((lane >> ESH) & EMASK)) << 2;
+        const int4 e4 = *reinterpret_cast<const int4*>(&s_end[warp][lane * IPT + phys]);
         er[q] = e4.x;
         er[q + 1] = e4.y;
         er[q + 2] = e4.z;
