@@ -68,6 +68,10 @@ int ktb_matrix_info(const ktb_matrix* m, int64_t* n, int64_t* nnz, int* kind,
 /* Device copies of the stored arrays (int32 row_ptr/col, fp64 values) for
  * parity tests; any output may be NULL. Host destination pointers. */
 int ktb_matrix_download(const ktb_matrix* m, int32_t* row_ptr, int32_t* col_idx, double* values);
+/* Rows [row_begin, row_end) of a GENERAL device matrix as a new device matrix
+ * over the same column space (row_ptr rebased; used to give the interior and
+ * boundary rows of a halo slab their own plans). */
+int ktb_matrix_slice(const ktb_matrix* m, int64_t row_begin, int64_t row_end, ktb_matrix** out);
 
 /* ------------------------------------------------------- Matrix Market */
 /* Coordinate real general/symmetric files (matrix_market.hpp). Same

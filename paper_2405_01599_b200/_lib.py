@@ -37,6 +37,7 @@ def load() -> C.CDLL:
         "ktb_matrix_info": ([VP, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_int),
                              C.POINTER(I64), C.POINTER(I64)], C.c_int),
         "ktb_matrix_download": ([VP, VP, VP, VP], C.c_int),
+        "ktb_matrix_slice": ([VP, I64, I64, C.POINTER(VP)], C.c_int),
         "ktb_mm_probe": ([C.c_char_p, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_int)],
                          C.c_int),
         "ktb_mm_read": ([C.c_char_p, C.c_int, C.POINTER(VP)], C.c_int),

@@ -38,6 +38,7 @@ void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, dou
                int64_t max_iters, double* history, ktb_gmres_result* res);
 ktb_matrix* gen_powerlaw(int64_t n, uint64_t seed, int64_t target, double empty_frac,
                          int64_t max_len, int device);
+ktb_matrix* matrix_slice(const ktb_matrix* m, int64_t r0, int64_t r1);
 void powerlaw_host(int64_t n, uint64_t seed, int64_t target, double empty_frac,
                    int64_t max_len, std::vector<int64_t>& rp, std::vector<int32_t>* col,
                    std::vector<double>* val);
@@ -224,6 +225,11 @@ int ktb_matrix_download(const ktb_matrix* m, int32_t* row_ptr, int32_t* col_idx,
         if (values && m->nnz)
             KTB_CUDA(cudaMemcpy(values, m->val.p, 8 * m->nnz, cudaMemcpyDeviceToHost));
     });
+}
+
+int ktb_matrix_slice(const ktb_matrix* m, int64_t row_begin, int64_t row_end,
+                     ktb_matrix** out) {
+    return guarded([&] { *out = matrix_slice(m, row_begin, row_end); });
 }
 
 int ktb_mm_probe(const char* path, int64_t* n, int64_t* entries, int* symmetric) {

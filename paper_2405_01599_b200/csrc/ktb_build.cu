@@ -228,6 +228,53 @@ void bss_plan_copy(const ktb_matrix* m, int64_t jl, int64_t* h_start, int64_t* h
     if (h_flag) KTB_CUDA(cudaMemcpy(h_flag, b.flag.p, nnz, cudaMemcpyDeviceToHost));
 }
 
+// ------------------------------------------------------------ row slices
+__global__ void k_rebase(const int32_t* __restrict__ rp, int64_t r0, int64_t rows,
+                         int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i <= rows) out[i] = rp[r0 + i] - rp[r0];
+}
+
+// Rows [r0, r1) of a GENERAL matrix as a new device matrix over the same
+// column space (ncols kept): the halo-overlap split of a slab into interior
+// and boundary parts, each with its own plan.
+ktb_matrix* matrix_slice(const ktb_matrix* m, int64_t r0, int64_t r1) {
+    require(m != nullptr, "matrix: null handle");
+    require(m->kind == KTB_GENERAL, "matrix slice: general matrices only");
+    require(r0 >= 0 && r0 <= r1 && r1 <= m->n, "matrix slice: bad row range");
+    DeviceGuard g(m->device);
+    cudaStream_t s = 0;
+    int32_t z[2] = {0, 0};
+    KTB_CUDA(cudaMemcpy(&z[0], m->row_ptr.p + r0, 4, cudaMemcpyDeviceToHost));
+    KTB_CUDA(cudaMemcpy(&z[1], m->row_ptr.p + r1, 4, cudaMemcpyDeviceToHost));
+    auto* out = new ktb_matrix();
+    try {
+        out->device = m->device;
+        out->sm_count = m->sm_count;
+        out->n = r1 - r0;
+        out->ncols = m->ncols;
+        out->nnz = z[1] - z[0];
+        out->kind = KTB_GENERAL;
+        out->row_ptr.alloc(out->n + 1);
+        out->col.alloc(out->nnz);
+        out->val.alloc(out->nnz);
+        k_rebase<<<ceil_div(out->n + 1, 256), 256, 0, s>>>(m->row_ptr.p, r0, out->n,
+                                                          out->row_ptr.p);
+        KTB_LAUNCH();
+        if (out->nnz) {
+            KTB_CUDA(cudaMemcpyAsync(out->col.p, m->col.p + z[0], 4 * out->nnz,
+                                     cudaMemcpyDeviceToDevice, s));
+            KTB_CUDA(cudaMemcpyAsync(out->val.p, m->val.p + z[0], 8 * out->nnz,
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+        compute_matrix_stats(out, s);
+    } catch (...) {
+        delete out;
+        throw;
+    }
+    return out;
+}
+
 // ------------------------------------------------------------ matrix stats
 __global__ void k_stats(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                         int64_t n, unsigned long long* maxlen, long long* bw) {

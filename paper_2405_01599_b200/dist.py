@@ -147,9 +147,13 @@ def slab_csr_numpy(L: SlabLayout, diag=6.0, off=-1.0):
 
 
 class DistSpMV:
-    """Config-4 sharded SpMV on this rank's GPU (torch.distributed, NCCL)."""
+    """Config-4 sharded SpMV on this rank's GPU (torch.distributed, NCCL).
+    The slab is split once into its interior rows (no halo columns; U2 warp
+    tiles by default) and the boundary planes (U1), each a device matrix with
+    its own plan over the same local x."""
 
-    def __init__(self, nx, ny, nz, rank, world, device, seed=4, diag=6.0, off=-1.0):
+    def __init__(self, nx, ny, nz, rank, world, device, seed=4, diag=6.0, off=-1.0,
+                 interior_kernel=1):
         import torch
 
         from . import _lib
@@ -157,8 +161,18 @@ class DistSpMV:
 
         self.L = slab_layout(nx, ny, nz, rank, world)
         self.device = device
-        self.A = K.stencil7_slab(nx, ny, nz, self.L.z0, self.L.z1, diag, off, device=device)
-        self.plan = K.DevicePlan(self.A, K.UnsymKernel.u1_row)
+        slab = K.stencil7_slab(nx, ny, nz, self.L.z0, self.L.z1, diag, off, device=device)
+        self._nnz = slab.nnz()
+        lo, hi = self.L.interior_rows()
+        self.parts = []  # (r0, r1, plan)
+        if hi > lo:
+            a = slab.slice_rows(lo, hi)
+            self.parts.append((lo, hi, K.DevicePlan(a, int(interior_kernel))))
+        self.boundary = []
+        for b0, b1 in self.L.boundary_ranges():
+            a = slab.slice_rows(b0, b1)
+            self.boundary.append((b0, b1, K.DevicePlan(a, K.UnsymKernel.u1_row)))
+        del slab
         self.x = torch.empty(self.L.x_local_len, dtype=torch.float64, device=f"cuda:{device}")
         self.y = torch.empty(self.L.n_local, dtype=torch.float64, device=f"cuda:{device}")
         owned = self.x[self.L.owned_offset:self.L.owned_offset + self.L.n_local]
@@ -169,32 +183,29 @@ class DistSpMV:
 
     @property
     def nnz(self) -> int:
-        return self.A.nnz()
+        return self._nnz
+
+    def _run(self, parts):
+        for r0, r1, plan in parts:
+            plan.apply(self.x, self.y[r0:r1])
 
     def apply(self):
         """One sharded y = A x with halo/interior overlap (see module doc)."""
         reqs = halo_exchange(self.L, self.x)
-        lo, hi = self.L.interior_rows()
-        if hi > lo:
-            self.plan.apply_rows(lo, hi, self.x, self.y)
+        self._run(self.parts)
         for r in reqs:
             r.wait()  # the current stream waits for the NCCL transfers
-        for b0, b1 in self.L.boundary_ranges():
-            self.plan.apply_rows(b0, b1, self.x, self.y)
+        self._run(self.boundary)
         return self.y
 
     def compute_local(self):
         """The local rows only (halos assumed in place): interior + boundary."""
-        lo, hi = self.L.interior_rows()
-        if hi > lo:
-            self.plan.apply_rows(lo, hi, self.x, self.y)
-        for b0, b1 in self.L.boundary_ranges():
-            self.plan.apply_rows(b0, b1, self.x, self.y)
+        self._run(self.parts)
+        self._run(self.boundary)
         return self.y
 
     def launches_per_apply(self) -> int:
-        lo, hi = self.L.interior_rows()
-        return int(hi > lo) + len(self.L.boundary_ranges())
+        return sum(p.launches for _, _, p in self.parts + self.boundary)
 
 
 def local_exchange(layouts, xs) -> None:

@@ -204,6 +204,12 @@ class DeviceCsr:
         rp, ci, v = self._dev.download()
         return rp.astype(np.int64), ci.astype(np.int64), v
 
+    def slice_rows(self, r0: int, r1: int) -> "DeviceCsr":
+        """Rows [r0, r1) as a new device matrix (same column space)."""
+        h = C.c_void_p()
+        _check(_lib.load().ktb_matrix_slice(self._dev.h, r0, r1, C.byref(h)))
+        return DeviceCsr(h, False)
+
 
 def stencil7(nx, ny, nz, diag=6.0, off=-1.0, c_xm=None, c_xp=None, device=0) -> DeviceCsr:
     h = C.c_void_p()
