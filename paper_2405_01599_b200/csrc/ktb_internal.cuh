@@ -176,7 +176,8 @@ struct SymWindowLayout {
     DBuf<int64_t> spill_off;   // per CTA: offset into spill
     DBuf<double> spill;
     DBuf<int32_t> head_end;    // per CTA: its head rows [cta_row[c], head_end[c]) get spills
-    DBuf<int32_t> segs;        // fixup segments (d, j0, j1, 0)
+    DBuf<int32_t> segs;        // fixup block descriptors (3 int4 each, see s3_setup)
+    DBuf<int32_t> seg_src;     // per fixup block: its spilling sources, ascending
     int64_t nsegs = 0;
     int reach = 0;             // max(col - row), clipped to the window
     DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it

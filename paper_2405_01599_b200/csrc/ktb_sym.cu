@@ -400,65 +400,60 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 
 // Head rows of block d receive the spills of earlier blocks, summed in
 // ascending source order and added once (deterministic). One block per
-// segment of <= kFixRows head rows of one destination, 8 rows per thread with
-// every load issued before use.
-__global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ segs,
+// segment of <= kFixRows head rows of one destination, 4 rows per thread; the
+// segment's source metadata is plan data loaded before griddepcontrol.wait,
+// so after it every y and spill load of the thread goes out at once.
+__global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ desc,
+                                                  const int32_t* __restrict__ seg_src,
                                                   const int32_t* __restrict__ cta_row,
-                                                  const int32_t* __restrict__ first_src,
                                                   const int32_t* __restrict__ spill_hi,
                                                   const int64_t* __restrict__ spill_off,
                                                   const double* __restrict__ spill,
                                                   double* __restrict__ y) {
     constexpr int U = kFixRows / 256;
-    constexpr int MS = 2;  // sources handled with all loads in flight at once
-    const int4 sg = segs[blockIdx.x];  // plan data: readable before the dependency resolves
+    // plan data, readable before the dependency resolves: rows [j0, j1), the
+    // number of sources spilling into them (ascending), the first two
+    // sources' ranges and spill bases inline
+    const int4 a = desc[3 * blockIdx.x], b = desc[3 * blockIdx.x + 1], c = desc[3 * blockIdx.x + 2];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // k_s3 complete and visible
-    const int d = sg.x;
-    const int32_t j0 = sg.y, j1 = sg.z;
-    const int c0 = first_src[d];
+    const int32_t j0 = a.x, j1 = a.y, ns = a.z;
+    const int64_t base0 = static_cast<int64_t>(
+        static_cast<uint64_t>(static_cast<uint32_t>(c.x)) | (static_cast<uint64_t>(c.y) << 32));
+    const int64_t base1 = static_cast<int64_t>(
+        static_cast<uint64_t>(static_cast<uint32_t>(c.z)) | (static_cast<uint64_t>(c.w) << 32));
+    double yv[U], v0[U], v1[U];
+    bool touched[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // every load of the block in one round trip
+        const int32_t j = j0 + u * 256 + threadIdx.x;
+        const bool in = j < j1;
+        const bool i0 = in && ns > 0 && j >= b.x && j < b.y;
+        const bool i1 = in && ns > 1 && j >= b.z && j < b.w;
+        yv[u] = in ? __ldcg(y + j) : 0.0;
+        v0[u] = i0 ? __ldcg(spill + base0 + j) : 0.0;
+        v1[u] = i1 ? __ldcg(spill + base1 + j) : 0.0;
+        touched[u] = i0 || i1;
+    }
     double acc[U];
-    bool any[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        acc[u] = 0.0;
-        any[u] = false;
-    }
-    for (int base = c0; base < d; base += MS) {
-        int32_t s0[MS], hi[MS];
-        const double* sp[MS];
+    for (int u = 0; u < U; ++u) acc[u] = v0[u] + v1[u];  // ascending source order
+    for (int k = 2; k < ns; ++k) {  // more than two sources: rare (tiny blocks)
+        const int src = seg_src[a.w + k];
+        const int32_t s0 = cta_row[src + 1], hi = spill_hi[src];
+        const double* sp = spill + spill_off[src] - s0;
 #pragma unroll
-        for (int k = 0; k < MS; ++k) {
-            const int src = base + k;
-            const bool ok = src < d;
-            s0[k] = ok ? cta_row[src + 1] : 0;
-            hi[k] = ok ? spill_hi[src] : 0;
-            sp[k] = ok ? spill + spill_off[src] - s0[k] : spill;
-        }
-        double v[MS][U];
-#pragma unroll
-        for (int k = 0; k < MS; ++k)
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int32_t j = j0 + u * 256 + threadIdx.x;
-                const bool in = j < j1 && j >= s0[k] && j < hi[k];
-                v[k][u] = in ? __ldcg(sp[k] + j) : 0.0;
-                any[u] |= in;
+        for (int u = 0; u < U; ++u) {
+            const int32_t j = j0 + u * 256 + threadIdx.x;
+            if (j < j1 && j >= s0 && j < hi) {
+                acc[u] += __ldcg(sp + j);
+                touched[u] = true;
             }
-#pragma unroll
-        for (int k = 0; k < MS; ++k)  // ascending source order
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] += v[k][u];
-    }
-    double yv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int32_t j = j0 + u * 256 + threadIdx.x;
-        yv[u] = any[u] ? __ldcg(y + j) : 0.0;
+        }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int32_t j = j0 + u * 256 + threadIdx.x;
-        if (any[u]) y[j] = yv[u] + acc[u];
+        if (touched[u]) y[j] = yv[u] + acc[u];
     }
 }
 
@@ -673,15 +668,33 @@ void s3_setup(ktb_plan* p) {
         head_end[d] = he;
         first_src[d] = fs;
     }
-    std::vector<int32_t> segs;  // (d, j0, j1, 0) per fixup block
+    // fixup blocks: <= kFixRows head rows of one destination each, with the
+    // sources whose spill range meets them (ascending) -- 3 int4 per block:
+    // (j0, j1, nsrc, list offset), (s0, hi) x 2, spill base (off - s0) x 2
+    std::vector<int32_t> segs, seg_src;
     for (int d = 0; d < P; ++d)
         for (int32_t j = bnd[d]; j < head_end[d]; j += kFixRows) {
-            segs.push_back(d);
-            segs.push_back(j);
-            segs.push_back(std::min<int32_t>(head_end[d], j + kFixRows));
-            segs.push_back(0);
+            const int32_t j1 = std::min<int32_t>(head_end[d], j + kFixRows);
+            const int32_t list = static_cast<int32_t>(seg_src.size());
+            for (int c = first_src[d]; c < d; ++c)
+                if (spill_hi[c] > j && bnd[c + 1] < j1) seg_src.push_back(c);
+            const int32_t ns = static_cast<int32_t>(seg_src.size()) - list;
+            int32_t rng[4] = {0, 0, 0, 0};
+            int64_t base[2] = {0, 0};
+            for (int k = 0; k < std::min(ns, 2); ++k) {
+                const int c = seg_src[list + k];
+                rng[2 * k] = bnd[c + 1];
+                rng[2 * k + 1] = spill_hi[c];
+                base[k] = spill_off[c] - bnd[c + 1];
+            }
+            const int32_t v[12] = {j, j1, ns, list, rng[0], rng[1], rng[2], rng[3],
+                                   static_cast<int32_t>(base[0] & 0xffffffff),
+                                   static_cast<int32_t>(base[0] >> 32),
+                                   static_cast<int32_t>(base[1] & 0xffffffff),
+                                   static_cast<int32_t>(base[1] >> 32)};
+            segs.insert(segs.end(), v, v + 12);
         }
-    L.nsegs = static_cast<int64_t>(segs.size() / 4);
+    L.nsegs = static_cast<int64_t>(segs.size() / 12);
 
     auto up32 = [&](DBuf<int32_t>& d, const std::vector<int32_t>& h) {
         d.alloc(std::max<size_t>(h.size(), 1));
@@ -711,6 +724,7 @@ void s3_setup(ktb_plan* p) {
     L.spill.alloc(std::max<int64_t>(so, 1));
     up32(L.head_end, head_end);
     up32(L.segs, segs);
+    up32(L.seg_src, seg_src);
     up32(L.first_src, first_src);
     up32(L.long_rows, long_rows);
     L.nlong = static_cast<int64_t>(long_rows.size());
@@ -748,8 +762,8 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         KTB_CUDA(cudaLaunchKernelEx(&cfg, k_s3_fixup, reinterpret_cast<const int4*>(L.segs.p),
+                                    static_cast<const int32_t*>(L.seg_src.p),
                                     static_cast<const int32_t*>(L.cta_row.p),
-                                    static_cast<const int32_t*>(L.first_src.p),
                                     static_cast<const int32_t*>(L.spill_hi.p),
                                     static_cast<const int64_t*>(L.spill_off.p),
                                     static_cast<const double*>(L.spill.p), y));
