@@ -265,6 +265,24 @@ int ktb_dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, vo
 /* y += A_o x_ghost (device pointers); run after A_d x_owned -> y. */
 int ktb_dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, void* stream);
 
+/* ------------------------------- distributed Krylov building blocks */
+/* Device BLAS-1 for GMRES over row-sharded vectors (dot / axpy / scal of
+ * common.hpp:33-56 and the passes of ortho.hpp:55-111); the caller
+ * all-reduces the local partial dots (NCCL). Deterministic reductions.
+ * V: column-major basis, column j at V + j*ldv. All pointers device. */
+/* scratch doubles needed by ktb_vec_mdot for k columns */
+int64_t ktb_vec_mdot_scratch(int k);
+/* out[j] = <V_j, w>, j < k (local partial dot products) */
+int ktb_vec_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* out,
+                 double* scratch, void* stream);
+/* w += alpha * coef[j] * V_j for j = 0..k-1 in order (k axpy calls fused) */
+int ktb_vec_maxpy(int64_t n, int k, const double* V, int64_t ldv, const double* coef,
+                  double alpha, double* w, void* stream);
+/* y = a*x + b*y */
+int ktb_vec_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);
+/* x[i] *= s (divide = 0, scal) or x[i] /= s (divide = 1) */
+int ktb_vec_scale(int64_t n, double s, int divide, double* x, void* stream);
+
 /* ---------------------------------------------------------- host memory */
 int ktb_host_alloc(size_t bytes, void** out);  /* pinned */
 int ktb_host_free(void* p);

@@ -46,6 +46,11 @@ def load() -> C.CDLL:
         "ktb_csr_host_upload": ([VP, C.c_int, C.POINTER(VP)], C.c_int),
         "ktb_csr_host_destroy": ([VP], C.c_int),
         "ktb_mm_write": ([C.c_char_p, I64, VP, VP, VP, C.c_int], C.c_int),
+        "ktb_vec_mdot_scratch": ([C.c_int], I64),
+        "ktb_vec_mdot": ([I64, C.c_int, VP, I64, VP, VP, VP, VP], C.c_int),
+        "ktb_vec_maxpy": ([I64, C.c_int, VP, I64, VP, C.c_double, VP, VP], C.c_int),
+        "ktb_vec_axpby": ([I64, C.c_double, VP, C.c_double, VP, VP], C.c_int),
+        "ktb_vec_scale": ([I64, C.c_double, C.c_int, VP, VP], C.c_int),
         "ktb_dist_create": ([I64, C.c_int, VP, C.c_int, VP, VP, VP, C.POINTER(VP)], C.c_int),
         "ktb_dist_destroy": ([VP], C.c_int),
         "ktb_dist_info": ([VP] + [C.POINTER(I64)] * 5, C.c_int),
@@ -106,4 +111,5 @@ def declared_symbols() -> list[str]:
 
     hdr = os.path.join(os.path.dirname(HERE), "include", "ktb.h")
     txt = open(hdr).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void)\s+(ktb_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*|void)\s+(ktb_\w+)\(", txt,
+                                 re.M)))

@@ -232,6 +232,28 @@ int ktb_matrix_slice(const ktb_matrix* m, int64_t row_begin, int64_t row_end,
     return guarded([&] { *out = matrix_slice(m, row_begin, row_end); });
 }
 
+int64_t ktb_vec_mdot_scratch(int k) { return vec_mdot_scratch(k); }
+
+int ktb_vec_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* out,
+                 double* scratch, void* stream) {
+    return guarded(
+        [&] { vec_mdot(n, k, V, ldv, w, out, scratch, static_cast<cudaStream_t>(stream)); });
+}
+
+int ktb_vec_maxpy(int64_t n, int k, const double* V, int64_t ldv, const double* coef,
+                  double alpha, double* w, void* stream) {
+    return guarded(
+        [&] { vec_maxpy(n, k, V, ldv, coef, alpha, w, static_cast<cudaStream_t>(stream)); });
+}
+
+int ktb_vec_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream) {
+    return guarded([&] { vec_axpby(n, a, x, b, y, static_cast<cudaStream_t>(stream)); });
+}
+
+int ktb_vec_scale(int64_t n, double s, int divide, double* x, void* stream) {
+    return guarded([&] { vec_scale(n, s, divide, x, static_cast<cudaStream_t>(stream)); });
+}
+
 int ktb_mm_probe(const char* path, int64_t* n, int64_t* entries, int* symmetric) {
     return guarded([&] {
         require(path != nullptr, "matrix market: null path");

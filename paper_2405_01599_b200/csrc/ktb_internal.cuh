@@ -151,6 +151,15 @@ void dist_upload(ktb_dist* d, int device);
 void dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, cudaStream_t s);
 void dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, cudaStream_t s);
 
+// ---- device BLAS-1 of the distributed Krylov loop (ktb_vec.cu) -----------
+int64_t vec_mdot_scratch(int k);
+void vec_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* out,
+              double* scratch, cudaStream_t s);
+void vec_maxpy(int64_t n, int k, const double* V, int64_t ldv, const double* coef, double alpha,
+               double* w, cudaStream_t s);
+void vec_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s);
+void vec_scale(int64_t n, double sc, int divide, double* x, cudaStream_t s);
+
 // ---- plans ---------------------------------------------------------------
 struct MergeCoord {
     int32_t row;

@@ -1,0 +1,284 @@
+"""Restarted GMRES(m) over row-sharded vectors: the
+reference's gmres_m (gmres.hpp:16-173) and orthogonalize (ortho.hpp:69-111)
+with every global reduction a sum of local partials across the process group
+(NCCL all-reduce on GPUs).
+
+The loop is the reference's, statement for statement: the Givens rotations,
+back-substitution and stopping rule run on host scalars; vectors stay on the
+device and go through libktb's deterministic BLAS-1 kernels (ktb_vec_*).
+Each orthogonaliser keeps its reduction structure, so its all-reduce count
+per Arnoldi step is explicit:
+
+    mgs   k+2  (one per projection, the input norm, the output norm)
+    cgs   3    (all projections at once, two norms)
+    dgks  4    (two classical passes)
+    bcgs  ceil(k / block_len) + 2
+
+`op` is any row-sharded operator with ``n_local`` and ``apply(x, y)``
+(dist.DistCsrSpMV, or a single-rank DevicePlan wrapper); ``ops`` the local
+vector kernels (DeviceVecOps here; tests drive the same loop on CPU ranks
+with a stand-in); ``allreduce`` sums a tensor in place over the ranks.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+ORTHO = ("cgs", "mgs", "dgks", "bcgs")  # ortho.hpp:12 OrthoKind
+
+
+@dataclass
+class DistSolverResult:  # the SolverResult fields gmres_m fills (solver_types.hpp:56-77)
+    x: object = None
+    iterations: int = 0
+    converged: bool = False
+    breakdown: bool = False
+    breakdown_reason: str = ""
+    recurrence_residual: float = 0.0
+    true_residual: float = 0.0
+    fault_convergence: bool = False
+    residual_history: list = field(default_factory=list)
+    restarts: list = field(default_factory=list)
+    allreduces: int = 0
+    elapsed_seconds: float = 0.0
+
+
+class DeviceVecOps:
+    """Local BLAS-1 on torch CUDA tensors through libktb (ktb_vec_*)."""
+
+    def __init__(self, max_cols: int, device: int):
+        import torch
+
+        from . import _lib
+
+        self._L = _lib.load()
+        self.device = device
+        self.scratch = torch.empty(max(int(self._L.ktb_vec_mdot_scratch(max_cols)), 1),
+                                   dtype=torch.float64, device=f"cuda:{device}")
+
+    def _s(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _chk(self, rc):
+        if rc != 0:
+            from .ktune import _check
+
+            _check(rc)
+
+    def empty(self, *shape):
+        import torch
+
+        return torch.empty(*shape, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def zeros(self, *shape):
+        import torch
+
+        return torch.zeros(*shape, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def mdot(self, V, k, w, out):
+        """out[:k] = V[:k] . w (local partials); V is (cols, n) row-major."""
+        n = w.shape[0]
+        self._chk(self._L.ktb_vec_mdot(n, k, V.data_ptr(), V.stride(0), w.data_ptr(),
+                                       out.data_ptr(), self.scratch.data_ptr(), self._s()))
+
+    def maxpy(self, V, k, coef, alpha, w):
+        """w += alpha * coef[j] * V[j], j = 0..k-1 in order."""
+        n = w.shape[0]
+        self._chk(self._L.ktb_vec_maxpy(n, k, V.data_ptr(), V.stride(0), coef.data_ptr(),
+                                        float(alpha), w.data_ptr(), self._s()))
+
+    def axpby(self, a, x, b, y):
+        self._chk(self._L.ktb_vec_axpby(y.shape[0], float(a), x.data_ptr(), float(b),
+                                        y.data_ptr(), self._s()))
+
+    def scale(self, s, x, divide=False):
+        self._chk(self._L.ktb_vec_scale(x.shape[0], float(s), int(divide), x.data_ptr(),
+                                        self._s()))
+
+    def to_host(self, t):
+        return t.detach().cpu().tolist()
+
+    def from_host(self, vals, out):
+        import torch
+
+        out.copy_(torch.tensor(vals, dtype=torch.float64))
+
+
+def process_group_allreduce(group=None):
+    """Sum a tensor in place over the default (or given) process group; a
+    no-op for a single rank."""
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return lambda t: None
+    return lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+class _Counter:
+    def __init__(self, allreduce):
+        self.f, self.n = allreduce, 0
+
+    def __call__(self, t):
+        self.n += 1
+        self.f(t)
+
+
+def _norm(ops, ar, v, buf):
+    ops.mdot(v.unsqueeze(0), 1, v, buf)
+    ar(buf[:1])
+    return math.sqrt(ops.to_host(buf[:1])[0])
+
+
+def orthogonalize(kind, V, k, w, ops, ar, bufs, block_len=4):
+    """ortho.hpp:69-111 on sharded vectors: returns (h[0..k], breakdown);
+    w becomes the new unit vector unless breakdown."""
+    if kind not in ORTHO:
+        raise ValueError(f"orthogonalize: unknown kind {kind!r}")
+    if block_len < 1:
+        raise ValueError("orthogonalize: block length must be >= 1")
+    coef, nbuf = bufs
+    input_norm = _norm(ops, ar, w, nbuf)
+    h = [0.0] * (k + 1)
+
+    def classical(first, count):  # detail::classical_pass (ortho.hpp:55-64)
+        if count == 0:
+            return
+        ops.mdot(V[first:first + count], count, w, coef)
+        ar(coef[:count])
+        ops.maxpy(V[first:first + count], count, coef, -1.0, w)
+        c = ops.to_host(coef[:count])
+        for j in range(count):
+            h[first + j] += c[j]
+
+    if kind == "cgs":
+        classical(0, k)
+    elif kind == "dgks":
+        classical(0, k)
+        classical(0, k)
+    elif kind == "mgs":
+        for j in range(k):  # one projection at a time, coefficient stays on the device
+            ops.mdot(V[j:j + 1], 1, w, coef[j:j + 1])
+            ar(coef[j:j + 1])
+            ops.maxpy(V[j:j + 1], 1, coef[j:j + 1], -1.0, w)
+        c = ops.to_host(coef[:k])
+        for j in range(k):
+            h[j] += c[j]
+    else:  # bcgs
+        for b in range(0, k, block_len):
+            classical(b, min(block_len, k - b))
+    norm = _norm(ops, ar, w, nbuf)
+    h[k] = norm
+    if norm <= 1e-14 * input_norm:
+        return h, True
+    ops.scale(1.0 / norm, w)
+    return h, False
+
+
+def gmres_m_dist(op, b, m=30, tol=1e-8, max_iters=3000, ortho="mgs", block_len=4, ops=None,
+                 allreduce=None, max_time=math.inf) -> DistSolverResult:
+    """gmres.hpp:16-173 (no preconditioner, fixed restart m) with sharded
+    vectors. b: this rank's slice (device tensor for DeviceVecOps)."""
+    if m < 1:
+        raise ValueError("gmres: need 1 <= m <= m_max")
+    if tol <= 0.0:
+        raise ValueError("gmres: tol must be positive")
+    if b.shape[0] != op.n_local:
+        raise ValueError("gmres: dimension mismatch")
+    ar = _Counter(allreduce or process_group_allreduce())
+    ops = ops or DeviceVecOps(m + 1, b.device.index)
+    n = op.n_local
+    t0 = time.perf_counter()
+    res = DistSolverResult()
+    coef = ops.zeros(m + 1)
+    nbuf = ops.zeros(1)
+    x = ops.zeros(n)
+    res.x = x
+    nb = _norm(ops, ar, b, nbuf)
+    if nb == 0.0:
+        res.converged = True
+        res.allreduces = ar.n
+        res.elapsed_seconds = time.perf_counter() - t0
+        return res
+    V = ops.zeros(m + 1, n)
+    r, w = ops.zeros(n), ops.zeros(n)
+    cs, sn = [0.0] * (m + 1), [0.0] * (m + 1)
+    r_cols = [[0.0] * (m + 1) for _ in range(m)]
+    rr = 1.0
+    stop = False
+    while not stop:
+        op.apply(x, r)
+        ops.axpby(1.0, b, -1.0, r)  # r = b - A x
+        beta = _norm(ops, ar, r, nbuf)
+        rr = beta / nb
+        if rr < tol:
+            res.converged = True
+            break
+        ops.axpby(1.0, r, 0.0, V[0])
+        ops.scale(beta, V[0], divide=True)  # basis[i] = r[i] / beta
+        g = [0.0] * (m + 2)
+        g[0] = beta
+        j = 0
+        lucky = False
+        while j < m:
+            if res.iterations >= max_iters or time.perf_counter() - t0 > max_time:
+                stop = True
+                break
+            op.apply(V[j], w)
+            h, breakdown = orthogonalize(ortho, V, j + 1, w, ops, ar, (coef, nbuf), block_len)
+            if breakdown:
+                h[j + 1] = 0.0
+                lucky = True
+            else:
+                ops.axpby(1.0, w, 0.0, V[j + 1])
+            for i in range(j):
+                t1, t2 = h[i], h[i + 1]
+                h[i] = cs[i] * t1 + sn[i] * t2
+                h[i + 1] = -sn[i] * t1 + cs[i] * t2
+            denom = math.hypot(h[j], h[j + 1])
+            if denom == 0.0:
+                cs[j], sn[j] = 1.0, 0.0
+            else:
+                cs[j], sn[j] = h[j] / denom, h[j + 1] / denom
+            h[j] = denom
+            g[j + 1] = -sn[j] * g[j]
+            g[j] *= cs[j]
+            r_cols[j][: j + 1] = h[: j + 1]
+            res.iterations += 1
+            rr = abs(g[j + 1]) / nb
+            res.residual_history.append(rr)
+            j += 1
+            if lucky or rr < tol:
+                break
+        if j > 0:  # back-substitute R y = g, x += Q y
+            y = [0.0] * j
+            for i in range(j - 1, -1, -1):
+                s = g[i]
+                for l in range(i + 1, j):
+                    s -= r_cols[l][i] * y[l]
+                rii = r_cols[i][i]
+                y[i] = s / rii if rii != 0.0 else 0.0
+            ops.from_host(y, coef[:j])
+            ops.scale(0.0, w)
+            ops.maxpy(V[:j], j, coef, 1.0, w)
+            ops.axpby(1.0, w, 1.0, x)
+        if rr < tol:
+            res.converged = True
+            break
+        if lucky:
+            res.breakdown = True
+            res.breakdown_reason = "arnoldi breakdown before reaching tol"
+            break
+        if stop:
+            break
+        res.restarts.append((res.iterations, m))
+    res.recurrence_residual = rr
+    op.apply(x, r)
+    ops.axpby(1.0, b, -1.0, r)
+    res.true_residual = _norm(ops, ar, r, nbuf) / nb
+    res.fault_convergence = res.converged and res.true_residual > tol
+    res.allreduces = ar.n
+    res.elapsed_seconds = time.perf_counter() - t0
+    return res
