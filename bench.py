@@ -540,58 +540,181 @@ def run_gpu_dist(args, cfg):
     return 0
 
 
+class _TimedOp:
+    """Row-sharded operator wrapper that times every apply with CUDA events
+    on the current stream (SpMV device seconds inside the solve)."""
+
+    def __init__(self, op, launches):
+        self.op, self.n_local, self.launches_per = op, op.n_local, launches
+        self.events, self.calls = [], 0
+
+    def apply(self, x, y):
+        import torch
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self.op.apply(x, y)
+        e1.record()
+        self.events.append((e0, e1))
+        self.calls += 1
+
+    def seconds(self):
+        return sum(a.elapsed_time(b) for a, b in self.events) * 1e-3
+
+
 def run_gmres(args, cfg):
     """Config 5: GMRES(30)+MGS on the 128^3 convection-diffusion matrix,
-    b = A*ones, tol 1e-8, <= 3000 iterations (BASELINE.json configs[4]).
-    One step = one full solve; value = SpMV GB/s inside the solve; the solve's
-    iterations / residual / SpMV share are reported beside it."""
+    b = A*ones (computed by our SpMV), tol 1e-8, <= 3000 iterations
+    (BASELINE.json configs[4]). One step = one full solve. value = SpMV GB/s
+    inside the solve (algorithmic bytes x SpMV calls / SpMV device seconds);
+    e2e = the same bytes over the wall time of the public call with host b in
+    and host x out. Default: the fused single-GPU solver (ktb_gmres, one
+    replica per rank). --shard: krylov.gmres_m_dist over general row blocks,
+    all-reduced dots (NCCL), one solve across all ranks."""
     import torch
 
-    from oracle import oracle as O  # b = A*ones via the oracle (input setup only)
+    from paper_2405_01599_b200 import _lib
     from paper_2405_01599_b200 import ktune as K
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     a = K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7, device=local)
-    rp, ci, v = a.to_host()
-    A = K.CsrMatrix(a.n, rp, ci, v, device=local)
-    b = O.spmv_ref(a.n, rp, ci, v, np.ones(a.n))
-    choice, rep = K.select_spmv_unsym(A)
+    n, nnz = a.n, a.nnz()
+    B = min_bytes(n, nnz)
     kcfg = K.KrylovConfig(30, 30, 1e-8, 3000)
-    for _ in range(max(1, args.warmup // 3)):
-        K.gmres_m(A, b, kcfg, plan=choice.plan)
-    runs = [K.gmres_m(A, b, kcfg, plan=choice.plan) for _ in range(max(1, args.steps // 10))]
-    r = runs[-1]
-    sec = float(np.mean([x.elapsed_seconds for x in runs]))
-    spmv = float(np.mean([x.spmv_seconds for x in runs]))
-    B = min_bytes(a.n, a.nnz())
-    line = {"metric": METRIC, "value": B * r.spmv_calls / spmv / 1e9, "unit": "GB/s",
-            "n_gpus": 1, "steps": len(runs), "warmup": args.warmup, "ms_per_step": sec * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (SURVEY.md §8d recipe)",
-            "config": {"workload": "cfg5: GMRES(30)+MGS, 128^3 7-pt convection-diffusion, "
-                                   "b = A*ones, tol 1e-8, max 3000 its",
-                       "kernel": f"{rep.selected_candidate().name} SpMV + cooperative MGS"},
-            "gmres": {"iterations": r.iterations, "restarts": r.restarts,
-                      "true_residual": r.true_residual, "converged": r.converged,
-                      "spmv_calls": r.spmv_calls, "solve_seconds": sec,
-                      "spmv_seconds": spmv, "spmv_share": spmv / sec,
-                      "reference_iterations_survey": 653}}
-    if not args.no_cpu_baseline:
-        try:
-            n, rp64, ci64, v64 = a.n, rp.astype(np.int64), ci.astype(np.int64), v
-            its = 60  # bounded sample: two restarts of the reference solver
-            _, rr = O.Ref.gmres(n, rp64, ci64, v64, b, 30, 1e-8, its, 1, os.cpu_count() or 1)
-            line["cpu_baseline"] = {
-                "value": B * rr["spmv_calls"] / max(rr["spmv_seconds"], 1e-12) / 1e9,
+    sampler = ClockSampler(gpu_uuid(local))
+    if not args.shard:
+        choice, rep = K.select_spmv_unsym(a)
+        plan = choice.plan
+        kname = f"{rep.selected_candidate().name} SpMV + cooperative MGS (ktb_gmres)"
+        ones = torch.ones(n, dtype=torch.float64, device="cuda")
+        bd = torch.empty_like(ones)
+        plan.apply(ones, bd)  # b = A * ones on the device
+        torch.cuda.synchronize()
+        b_host = bd.cpu().numpy()
+        for _ in range(max(1, args.warmup // 3)):
+            K.gmres_m(a, b_host, kcfg, plan=plan)
+        sampler.start()
+        runs = []
+        for _ in range(max(1, args.steps // 10)):
+            t0 = time.perf_counter()
+            r = K.gmres_m(a, b_host, kcfg, plan=plan)  # host b in, host x out
+            runs.append((r, time.perf_counter() - t0))
+        clocks = sampler.stop()
+        r = runs[-1][0]
+        wall = float(np.mean([t for _, t in runs]))
+        spmv = float(np.mean([x.spmv_seconds for x, _ in runs]))
+        calls, its, cyc = r.spmv_calls, r.iterations, r.restarts + 1
+        L = plan.launches
+        launches = 1 + cyc * (L + 4) + its * (L + 1) + L + 2
+        info = {"iterations": its, "restarts": r.restarts, "true_residual": r.true_residual,
+                "converged": r.converged, "spmv_calls": calls, "solve_seconds": wall}
+        par, ranks_note = "replicas (one full solve per GPU)", ws
+        value_scale = ws
+    else:
+        from paper_2405_01599_b200 import dist as D
+        from paper_2405_01599_b200 import krylov as KR
+
+        rp, ci, v = a.to_host()
+        bnd = D.nnz_balanced_boundaries(rp, ws)
+        r0, r1 = int(bnd[rank]), int(bnd[rank + 1])
+        op = D.DistCsrSpMV(n, bnd, rank, ws, rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]],
+                           v[rp[r0]:rp[r1]], local)
+        del rp, ci, v
+        kname = f"u{op.plan.kernel + 1} on A_d + ghost acc, gmres_m_dist (MGS, NCCL all-reduce)"
+        ones = torch.ones(op.n_local, dtype=torch.float64, device="cuda")
+        bd = torch.empty_like(ones)
+        op.apply(ones, bd)
+        b_host = bd.cpu().numpy()
+        ar = KR.process_group_allreduce()
+        ops = KR.DeviceVecOps(31, local)
+        for _ in range(max(1, args.warmup // 3)):
+            KR.gmres_m_dist(op, bd, m=30, tol=1e-8, max_iters=3000, ortho="mgs", ops=ops,
+                            allreduce=ar)
+        if dist:
+            dist.barrier()
+        sampler.start()
+        runs = []
+        for _ in range(max(1, args.steps // 10)):
+            top = _TimedOp(op, op.launches_per_apply())
+            ops.launches = 0
+            t0 = time.perf_counter()
+            bh = torch.from_numpy(b_host).pin_memory().cuda(non_blocking=True)  # host b in
+            rr = KR.gmres_m_dist(top, bh, m=30, tol=1e-8, max_iters=3000, ortho="mgs", ops=ops,
+                                 allreduce=ar)
+            xh = rr.x.cpu()  # host x out
+            torch.cuda.synchronize()
+            runs.append((rr, time.perf_counter() - t0, top.seconds(), top.calls, ops.launches,
+                         top.launches_per * top.calls))
+        clocks = sampler.stop()
+        r = runs[-1][0]
+        wall = float(np.mean([t for _, t, *_ in runs]))
+        spmv = float(np.mean([s for _, _, s, *_ in runs]))
+        if dist:
+            t = torch.tensor([wall, spmv], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall, spmv = float(t[0]), float(t[1])
+        calls, its = runs[-1][3], r.iterations
+        launches = runs[-1][4] + runs[-1][5]
+        info = {"iterations": its, "restarts": len(r.restarts), "true_residual": r.true_residual,
+                "converged": r.converged, "spmv_calls": calls, "solve_seconds": wall,
+                "allreduces": r.allreduces}
+        par, ranks_note = f"one solve over {ws} NNZ_BALANCED row blocks", 1
+        value_scale = 1
+        del xh
+    info.update({"spmv_seconds": spmv, "spmv_share": spmv / wall,
+                 "reference_iterations_survey": 653})
+    peak, peak_src = peak_hbm()
+    achieved = B * calls / spmv / 1e9
+    if rank == 0:
+        line = {"metric": METRIC, "value": value_scale * achieved, "unit": "GB/s", "n_gpus": ws,
+                "steps": len(runs), "warmup": args.warmup, "ms_per_step": wall * 1e3,
+                "higher_is_better": True, "scaling": "weak" if not args.shard else "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8d recipe)",
+                "config": {"workload": "cfg5: GMRES(30)+MGS, 128^3 7-pt convection-diffusion, "
+                                       "b = A*ones, tol 1e-8, max 3000 its",
+                           "kernel": kname, "parallelism": par,
+                           "value_def": "algorithmic SpMV bytes x SpMV calls / SpMV device "
+                                        "seconds inside the solve"},
+                "gmres": info,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                             "kernel": "the SpMV applies inside the solve"},
+                "e2e": {"value": value_scale * B * calls / wall / 1e9, "unit": "GB/s",
+                        "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                        "def": "same SpMV bytes over the wall time of the whole solve call, "
+                               "host b in, host x out"},
+                "gpu_launches": launches * len(runs) * ranks_note,
+                "clocks": clocks}
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = _gmres_cpu_baseline(a, B)
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def _gmres_cpu_baseline(a, B):
+    from oracle import oracle as O  # cpu_baseline leg only
+
+    try:
+        rp, ci, v = a.to_host()
+        n = a.n
+        b = O.spmv_ref(n, rp, ci, v, np.ones(n))
+        its = 60  # bounded sample: two restarts of the reference solver
+        _, rr = O.Ref.gmres(n, rp, ci, v, b, 30, 1e-8, its, 1, os.cpu_count() or 1)
+        return {"value": B * rr["spmv_calls"] / max(rr["spmv_seconds"], 1e-12) / 1e9,
                 "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                 "sample": f"{its} iterations of ktune::gmres_m (MGS) with a U1 UnsymEngine on "
-                          f"all cores: {rr['seconds']:.2f} s ({rr['seconds'] / its * 1e3:.1f} ms/it; "
-                          f"653 its extrapolate to {rr['seconds'] / its * 653:.1f} s)"}
-        except Exception as e:
-            line["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
-    print(json.dumps(line))
-    return 0
+                          f"all cores: {rr['seconds']:.2f} s ({rr['seconds'] / its * 1e3:.1f} "
+                          f"ms/it; 653 its extrapolate to {rr['seconds'] / its * 653:.1f} s)"}
+    except Exception as e:
+        return {"value": None, "sample": f"unavailable: {e}"}
 
 
 def traffic_from_profile(cfg):
@@ -629,8 +752,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS) + [5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
-                    help="configs 1/3: general row-block sharding over the ranks "
-                         "(default: replicas)")
+                    help="configs 1/3: general row-block sharding over the ranks; config 5: "
+                         "one distributed solve (default: replicas)")
     ap.add_argument("--warm-seconds", type=float, default=1.0,
                     help="keep warming up at least this long (clocks settle); 0 under ncu")
     args = ap.parse_args()

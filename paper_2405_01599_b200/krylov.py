@@ -54,6 +54,7 @@ class DeviceVecOps:
 
         self._L = _lib.load()
         self.device = device
+        self.launches = 0  # kernels launched (mdot = 2, the others 1)
         self.scratch = torch.empty(max(int(self._L.ktb_vec_mdot_scratch(max_cols)), 1),
                                    dtype=torch.float64, device=f"cuda:{device}")
 
@@ -83,20 +84,24 @@ class DeviceVecOps:
         n = w.shape[0]
         self._chk(self._L.ktb_vec_mdot(n, k, V.data_ptr(), V.stride(0), w.data_ptr(),
                                        out.data_ptr(), self.scratch.data_ptr(), self._s()))
+        self.launches += 2 if k else 0
 
     def maxpy(self, V, k, coef, alpha, w):
         """w += alpha * coef[j] * V[j], j = 0..k-1 in order."""
         n = w.shape[0]
         self._chk(self._L.ktb_vec_maxpy(n, k, V.data_ptr(), V.stride(0), coef.data_ptr(),
                                         float(alpha), w.data_ptr(), self._s()))
+        self.launches += 1 if k and n else 0
 
     def axpby(self, a, x, b, y):
         self._chk(self._L.ktb_vec_axpby(y.shape[0], float(a), x.data_ptr(), float(b),
                                         y.data_ptr(), self._s()))
+        self.launches += 1 if y.shape[0] else 0
 
     def scale(self, s, x, divide=False):
         self._chk(self._L.ktb_vec_scale(x.shape[0], float(s), int(divide), x.data_ptr(),
                                         self._s()))
+        self.launches += 1 if x.shape[0] else 0
 
     def to_host(self, t):
         return t.detach().cpu().tolist()
