@@ -283,6 +283,26 @@ int ktb_vec_axpby(int64_t n, double a, const double* x, double b, double* y, voi
 /* x[i] *= s (divide = 0, scal) or x[i] /= s (divide = 1) */
 int ktb_vec_scale(int64_t n, double s, int divide, double* x, void* stream);
 
+/* -------------------------------------------------------------- ILU(0) */
+/* ilu0.hpp: incomplete LU on the pattern of a GENERAL matrix (unit L, U on
+ * the stored pattern). Factors and solves are bitwise equal to the
+ * reference's (level-scheduled rows, reference operation order, no FMA). */
+typedef struct ktb_ilu ktb_ilu;
+/* ilu0_factorize (ilu0.hpp:23-69); same messages ("ilu0: structurally
+ * missing diagonal in row i", "ilu0: zero pivot at row i"). stream may be
+ * NULL. */
+int ktb_ilu0_create(const ktb_matrix* m, void* stream, ktb_ilu** out);
+/* n, dependency levels of the lower / upper sweeps, kernel launches per apply */
+int ktb_ilu0_info(const ktb_ilu* f, int64_t* n, int64_t* lower_levels, int64_t* upper_levels,
+                  int64_t* launches_per_apply);
+/* IluFactors::diag_ptr (n) and ::values (nnz) to host; either may be NULL */
+int ktb_ilu0_download(const ktb_ilu* f, int32_t* diag_ptr, double* values);
+/* ilu0_apply (ilu0.hpp:73-87): z = (LU)^{-1} r. ptr_kind KTB_PTR_DEVICE: device
+ * pointers, enqueued on `stream` (NULL = the legacy default stream);
+ * KTB_PTR_HOST: host arrays, synchronous. */
+int ktb_ilu0_apply(ktb_ilu* f, const double* r, double* z, int ptr_kind, void* stream);
+int ktb_ilu0_destroy(ktb_ilu* f);
+
 /* ---------------------------------------------------------- host memory */
 int ktb_host_alloc(size_t bytes, void** out);  /* pinned */
 int ktb_host_free(void* p);

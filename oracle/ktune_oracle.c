@@ -475,3 +475,56 @@ int ko_gmres_mgs(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
     free(r); free(z); free(w);
     return 0;
 }
+
+/* ilu0.hpp:23-69 */
+int64_t ko_ilu0_factorize(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                          double* values, int64_t* diag_ptr) {
+    for (int64_t i = 0; i < n; ++i) {
+        diag_ptr[i] = -1;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+            if (col_idx[k] == i) {
+                diag_ptr[i] = k;
+                break;
+            }
+        if (diag_ptr[i] < 0) return -(1 + i);
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t kp = row_ptr[i]; kp < row_ptr[i + 1]; ++kp) {
+            const int64_t k = col_idx[kp];
+            if (k >= i) break;
+            const double pivot = values[diag_ptr[k]];
+            if (pivot == 0.0) return 1 + k;
+            const double lik = values[kp] / pivot;
+            values[kp] = lik;
+            int64_t pi = kp + 1, pk = diag_ptr[k] + 1;
+            while (pi < row_ptr[i + 1] && pk < row_ptr[k + 1]) {
+                if (col_idx[pi] == col_idx[pk]) {
+                    values[pi] -= lik * values[pk];
+                    ++pi;
+                    ++pk;
+                } else if (col_idx[pi] < col_idx[pk]) {
+                    ++pi;
+                } else {
+                    ++pk;
+                }
+            }
+        }
+        if (values[diag_ptr[i]] == 0.0) return 1 + i;
+    }
+    return 0;
+}
+
+/* ilu0.hpp:73-87 */
+void ko_ilu0_apply(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                   const double* values, const int64_t* diag_ptr, const double* r, double* z) {
+    for (int64_t i = 0; i < n; ++i) {
+        double s = r[i];
+        for (int64_t k = row_ptr[i]; col_idx[k] < i; ++k) s -= values[k] * z[col_idx[k]];
+        z[i] = s;
+    }
+    for (int64_t i = n - 1; i >= 0; --i) {
+        double s = z[i];
+        for (int64_t k = diag_ptr[i] + 1; k < row_ptr[i + 1]; ++k) s -= values[k] * z[col_idx[k]];
+        z[i] = s / values[diag_ptr[i]];
+    }
+}

@@ -107,6 +107,16 @@ int ko_gmres_mgs(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                  const double* values, const double* b, int64_t m, double tol,
                  int64_t max_iters, double* x, double* history, ko_gmres_result* res);
 
+/* ilu0.hpp:23-69 ilu0_factorize on the pattern of A (in place on a copy of
+ * values): diag_ptr[n] and values[nnz] receive the combined L\U factors.
+ * Returns 0, or -(1 + i) for "structurally missing diagonal in row i", or
+ * (1 + i) for "zero pivot at row i" (the reference's first raise). */
+int64_t ko_ilu0_factorize(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                          double* values, int64_t* diag_ptr);
+/* ilu0.hpp:73-87 ilu0_apply: forward (unit L) then backward (U) sweeps. */
+void ko_ilu0_apply(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                   const double* values, const int64_t* diag_ptr, const double* r, double* z);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,9 @@ def lib():
         L.ko_norm2.restype = C.c_double
         L.ko_gmres_mgs.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _I64, C.c_double, _I64,
                                    _f64p, _f64p, C.c_void_p]
+        L.ko_ilu0_factorize.argtypes = [_I64, _i64p, _i64p, _f64p, _i64p]
+        L.ko_ilu0_factorize.restype = _I64
+        L.ko_ilu0_apply.argtypes = [_I64, _i64p, _i64p, _f64p, _i64p, _f64p, _f64p]
         _ora = L
     return _ora
 
@@ -116,6 +119,8 @@ def ref():
         L.kr_gmres.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _I64, C.c_double, _I64,
                                C.c_int, C.c_int, _f64p, _f64p] + [C.c_void_p] * 8
         L.kr_max_threads.restype = C.c_int
+        L.kr_ilu0_factorize.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _i64p]
+        L.kr_ilu0_apply.argtypes = [_I64, _i64p, _i64p, _f64p, _i64p, _f64p, _f64p]
         L.kr_mm_probe.argtypes = [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64),
                                   C.POINTER(C.c_int)]
         L.kr_mm_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
@@ -279,6 +284,28 @@ def gmres_mgs(n, rp, ci, v, b, m=30, tol=1e-8, max_iters=3000):
     return x, res
 
 
+def ilu0_factorize(n, rp, ci, v):
+    """ilu0.hpp:23-69 -> (values, diag_ptr); raises OracleError with the
+    reference's message on a missing diagonal / zero pivot."""
+    rp, ci, v = _csr(rp, ci, v)
+    vals = v.copy()
+    diag = np.empty(max(n, 1), np.int64)
+    rc = lib().ko_ilu0_factorize(n, rp, ci, vals, diag)
+    if rc < 0:
+        raise OracleError(f"ilu0: structurally missing diagonal in row {-rc - 1}")
+    if rc > 0:
+        raise OracleError(f"ilu0: zero pivot at row {rc - 1}")
+    return vals, diag[:n]
+
+
+def ilu0_apply(n, rp, ci, fv, diag, r):
+    rp, ci, fv = _csr(rp, ci, fv)
+    z = np.empty(n, np.float64)
+    lib().ko_ilu0_apply(n, rp, ci, fv, np.ascontiguousarray(diag, np.int64),
+                        np.ascontiguousarray(r, np.float64), z)
+    return z
+
+
 # ------------------------------------------------------------------ reference
 class _Cand(C.Structure):
     _fields_ = [("name", C.c_char * 8), ("ordinal", C.c_int), ("jl", _I64),
@@ -414,6 +441,22 @@ class Ref:
                        converged=bool(conv.value), recurrence_residual=rec.value,
                        true_residual=tru.value, seconds=sec.value, spmv_seconds=ssec.value,
                        history=hist[: its.value].copy())
+
+    @staticmethod
+    def ilu0_factorize(n, rp, ci, v):
+        rp, ci, v = _csr(rp, ci, v)
+        vals = np.empty(max(len(v), 1), np.float64)
+        diag = np.empty(max(n, 1), np.int64)
+        _chk_ref(ref().kr_ilu0_factorize(n, rp, ci, v, vals, diag))
+        return vals[: len(v)], diag[:n]
+
+    @staticmethod
+    def ilu0_apply(n, rp, ci, fv, diag, r):
+        rp, ci, fv = _csr(rp, ci, fv)
+        z = np.empty(n, np.float64)
+        _chk_ref(ref().kr_ilu0_apply(n, rp, ci, fv, np.ascontiguousarray(diag, np.int64),
+                                     np.ascontiguousarray(r, np.float64), z))
+        return z
 
     @staticmethod
     def mm_probe(path):

@@ -422,4 +422,28 @@ int kr_mm_write(const char* path, int64_t n, const int64_t* rp, const int64_t* c
     });
 }
 
+
+// ilu0.hpp:23-69 (+ messages) and :73-87
+int kr_ilu0_factorize(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                      double* values_out, int64_t* diag_out) {
+    return guarded([&] {
+        const auto f = ilu0_factorize(make_csr(n, rp, ci, v));
+        std::memcpy(values_out, f.values.data(), sizeof(double) * f.values.size());
+        std::memcpy(diag_out, f.diag_ptr.data(), sizeof(int64_t) * f.diag_ptr.size());
+    });
+}
+
+int kr_ilu0_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double* fv,
+                  const int64_t* diag, const double* r, double* z) {
+    return guarded([&] {
+        IluFactors f;
+        f.n = n;
+        f.row_ptr.assign(rp, rp + n + 1);
+        f.col_idx.assign(ci, ci + rp[n]);
+        f.values.assign(fv, fv + rp[n]);
+        f.diag_ptr.assign(diag, diag + n);
+        ilu0_apply(f, std::span<const double>(r, n), std::span<double>(z, n));
+    });
+}
+
 }  // extern "C"

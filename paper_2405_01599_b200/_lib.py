@@ -46,6 +46,11 @@ def load() -> C.CDLL:
         "ktb_csr_host_upload": ([VP, C.c_int, C.POINTER(VP)], C.c_int),
         "ktb_csr_host_destroy": ([VP], C.c_int),
         "ktb_mm_write": ([C.c_char_p, I64, VP, VP, VP, C.c_int], C.c_int),
+        "ktb_ilu0_create": ([VP, VP, C.POINTER(VP)], C.c_int),
+        "ktb_ilu0_info": ([VP] + [C.POINTER(I64)] * 4, C.c_int),
+        "ktb_ilu0_download": ([VP, VP, VP], C.c_int),
+        "ktb_ilu0_apply": ([VP, VP, VP, C.c_int, VP], C.c_int),
+        "ktb_ilu0_destroy": ([VP], C.c_int),
         "ktb_vec_mdot_scratch": ([C.c_int], I64),
         "ktb_vec_mdot": ([I64, C.c_int, VP, I64, VP, VP, VP, VP], C.c_int),
         "ktb_vec_maxpy": ([I64, C.c_int, VP, I64, VP, C.c_double, VP, VP], C.c_int),

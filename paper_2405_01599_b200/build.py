@@ -14,7 +14,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, os.environ.get("KTB_LIB_NAME", "libktb.so"))
 SOURCES = ["ktb_api.cu", "ktb_build.cu", "ktb_unsym.cu", "ktb_sym.cu", "ktb_gen.cu", "ktb_gmres.cu",
-           "ktb_mm.cu", "ktb_dist.cu", "ktb_vec.cu"]
+           "ktb_mm.cu", "ktb_dist.cu", "ktb_vec.cu",
+           "ktb_ilu.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

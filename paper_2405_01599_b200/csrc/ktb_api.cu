@@ -232,6 +232,47 @@ int ktb_matrix_slice(const ktb_matrix* m, int64_t row_begin, int64_t row_end,
     return guarded([&] { *out = matrix_slice(m, row_begin, row_end); });
 }
 
+int ktb_ilu0_create(const ktb_matrix* m, void* stream, ktb_ilu** out) {
+    return guarded([&] { *out = ilu0_create(m, static_cast<cudaStream_t>(stream)); });
+}
+
+int ktb_ilu0_info(const ktb_ilu* f, int64_t* n, int64_t* lower_levels, int64_t* upper_levels,
+                  int64_t* launches_per_apply) {
+    return guarded([&] {
+        require(f != nullptr, "ilu0: null handle");
+        ilu0_info(f, n, lower_levels, upper_levels, launches_per_apply);
+    });
+}
+
+int ktb_ilu0_download(const ktb_ilu* f, int32_t* diag_ptr, double* values) {
+    return guarded([&] {
+        require(f != nullptr, "ilu0: null handle");
+        ilu0_download(f, diag_ptr, values);
+    });
+}
+
+int ktb_ilu0_apply(ktb_ilu* f, const double* r, double* z, int ptr_kind, void* stream) {
+    return guarded([&] {
+        require(f != nullptr, "ilu0: null handle");
+        require(ptr_kind == KTB_PTR_HOST || ptr_kind == KTB_PTR_DEVICE, "ilu0: bad pointer kind");
+        int64_t n = 0;
+        ilu0_info(f, &n, nullptr, nullptr, nullptr);
+        if (ptr_kind == KTB_PTR_DEVICE) {
+            ilu0_apply(f, r, z, static_cast<cudaStream_t>(stream));
+            return;
+        }
+        DBuf<double> dr(std::max<int64_t>(n, 1)), dz(std::max<int64_t>(n, 1));
+        if (n) KTB_CUDA(cudaMemcpy(dr.p, r, 8 * n, cudaMemcpyHostToDevice));
+        ilu0_apply(f, dr.p, dz.p, nullptr);  // legacy default stream, then synchronous
+        KTB_CUDA(cudaStreamSynchronize(nullptr));
+        if (n) KTB_CUDA(cudaMemcpy(z, dz.p, 8 * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+int ktb_ilu0_destroy(ktb_ilu* f) {
+    return guarded([&] { ilu0_destroy(f); });
+}
+
 int64_t ktb_vec_mdot_scratch(int k) { return vec_mdot_scratch(k); }
 
 int ktb_vec_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* out,

@@ -151,6 +151,13 @@ void dist_upload(ktb_dist* d, int device);
 void dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, cudaStream_t s);
 void dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, cudaStream_t s);
 
+// ---- ILU(0) (ktb_ilu.cu) ---------------------------------------------------
+ktb_ilu* ilu0_create(const ktb_matrix* m, cudaStream_t user_stream);
+void ilu0_apply(ktb_ilu* f, const double* r, double* z, cudaStream_t s);
+void ilu0_info(const ktb_ilu* f, int64_t* n, int64_t* nl, int64_t* nu, int64_t* launches);
+void ilu0_download(const ktb_ilu* f, int32_t* diag, double* val);
+void ilu0_destroy(ktb_ilu* f);
+
 // ---- device BLAS-1 of the distributed Krylov loop (ktb_vec.cu) -----------
 int64_t vec_mdot_scratch(int k);
 void vec_mdot(int64_t n, int k, const double* V, int64_t ldv, const double* w, double* out,

@@ -342,6 +342,64 @@ def write_matrix_market(path, a) -> None:
                                     v.ctypes.data, kind))
 
 
+# ----------------------------------------------------------------- ILU(0)
+class IluFactors:
+    """ilu0.hpp:14-18 IluFactors, resident on the device (ktb_ilu): the
+    combined unit-L / U factors on A's pattern plus the level schedules of
+    the two triangular sweeps."""
+
+    def __init__(self, handle, a):
+        self.h, self.a = handle, a
+        n, nl, nu, la = I64(), I64(), I64(), I64()
+        _check(_lib.load().ktb_ilu0_info(handle, C.byref(n), C.byref(nl), C.byref(nu),
+                                         C.byref(la)))
+        self.n, self.lower_levels, self.upper_levels = n.value, nl.value, nu.value
+        self.launches_per_apply = la.value
+
+    def download(self):
+        """(diag_ptr int64[n], values fp64[nnz]) -- the reference's fields."""
+        nnz = self.a.nnz()
+        d = np.empty(max(self.n, 1), np.int32)
+        v = np.empty(max(nnz, 1), np.float64)
+        _check(_lib.load().ktb_ilu0_download(self.h, d.ctypes.data, v.ctypes.data))
+        return d[: self.n].astype(np.int64), v[:nnz]
+
+    def apply(self, r, z) -> None:
+        if isinstance(r, np.ndarray):
+            require(len(r) == self.n and len(z) == self.n, "ilu0: dimension mismatch")
+            r = np.ascontiguousarray(r, np.float64)
+            _check(_lib.load().ktb_ilu0_apply(self.h, r.ctypes.data, z.ctypes.data, 0, None))
+        else:
+            import torch
+
+            require(r.shape[0] == self.n and z.shape[0] == self.n, "ilu0: dimension mismatch")
+            s = torch.cuda.current_stream(r.device).cuda_stream
+            _check(_lib.load().ktb_ilu0_apply(self.h, _dptr(r), _dptr(z), 1, s))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                _lib.load().ktb_ilu0_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+
+def ilu0_factorize(a) -> IluFactors:
+    """ilu0.hpp:23-69 on the device; same failure messages."""
+    h = C.c_void_p()
+    _check(_lib.load().ktb_ilu0_create(a.dev.h, None, C.byref(h)))
+    return IluFactors(h, a)
+
+
+def ilu0_apply(f: IluFactors, r, z=None):
+    """ilu0.hpp:73-93: z = (LU)^{-1} r (allocating form when z is None)."""
+    if z is None:
+        z = np.empty(f.n, np.float64) if isinstance(r, np.ndarray) else _like(r, f.n)
+    f.apply(r, z)
+    return z
+
+
 # -------------------------------------------------------------- artefacts
 @dataclass
 class RowPartition:  # partition.hpp:15-23

@@ -196,11 +196,78 @@ class _ScriptedClock:
         return float(self.durations.get(ordinal, 1.0))
 
 
+def with_diagonal(n, rp, ci, v, rng, dominant):
+    """Insert every missing diagonal entry; optionally make rows diagonally
+    dominant (otherwise the pivots are whatever elimination produces)."""
+    rows = []
+    for i in range(n):
+        c = list(ci[rp[i]:rp[i + 1]])
+        x = list(v[rp[i]:rp[i + 1]])
+        if i not in c:
+            c.append(i)
+            x.append(float(rng.uniform(-1, 1)))
+        o = np.argsort(c)
+        c, x = np.array(c, np.int64)[o], np.array(x)[o]
+        if dominant:
+            x[c == i] = np.sum(np.abs(x)) + 1.0
+        rows.append((c, x))
+    rp2 = np.concatenate([[0], np.cumsum([len(c) for c, _ in rows])]).astype(np.int64)
+    return (n, rp2, np.concatenate([c for c, _ in rows]), np.concatenate([x for _, x in rows]))
+
+
+def ilu0_family(seed=4242, count=24):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for c in range(count):
+        n = int(rng.integers(1, 300))
+        dens = float(rng.choice([0.005, 0.02, 0.08]))
+        m = matgen.random_csr(n, dens, rng, skew=bool(c % 3 == 1), empty_frac=0.0)
+        cases.append(with_diagonal(*m, rng, dominant=bool(c % 2 == 0)))
+    cases.append(matgen.stencil7(6, 5, 4, xp=-0.7, xm=-1.3))  # config-5 operator
+    cases.append(matgen.stencil7(9, 7, 5))
+    return cases
+
+
+def ilu0_golden(cases):
+    """ilu0_factorize / ilu0_apply (ilu0.hpp) outputs + the two error cases."""
+    out = {"count": np.int64(len(cases))}
+    for c, (n, rp, ci, v) in enumerate(cases):
+        p = f"c{c}_"
+        fv, diag = R.ilu0_factorize(n, rp, ci, v)
+        r = R.seeded_vector(n, 100 + c)
+        out.update({p + "n": np.int64(n), p + "rp": rp, p + "ci": ci, p + "v": v, p + "fv": fv,
+                    p + "diag": diag, p + "r": r,
+                    p + "z": R.ilu0_apply(n, rp, ci, fv, diag, r)})
+    errs = []
+    for n, rp, ci, v in [  # missing diagonal in row 1; zero pivot at row 1; zero pivot at row 0
+            (3, np.array([0, 2, 3, 5]), np.array([0, 1, 0, 1, 2]), np.ones(5)),
+            (2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.ones(4)),
+            (2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([0.0, 1.0, 1.0, 1.0]))]:
+        try:
+            R.ilu0_factorize(n, rp, ci, v)
+            errs.append("")
+        except O.OracleError as e:
+            errs.append(str(e))
+    out["errors"] = np.array(errs)
+    return out
+
+
 def main():
-    np.savez_compressed(os.path.join(HERE, "unsym.npz"), **unsym_golden(random_family()))
-    np.savez_compressed(os.path.join(HERE, "sym.npz"), **sym_golden(sym_family()))
-    np.savez_compressed(os.path.join(HERE, "stencil.npz"), **stencil_golden())
-    np.savez_compressed(os.path.join(HERE, "select.npz"), **select_golden())
+    only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
+
+    def want(name):
+        return only is None or name in only
+
+    if want("unsym"):
+        np.savez_compressed(os.path.join(HERE, "unsym.npz"), **unsym_golden(random_family()))
+    if want("sym"):
+        np.savez_compressed(os.path.join(HERE, "sym.npz"), **sym_golden(sym_family()))
+    if want("stencil"):
+        np.savez_compressed(os.path.join(HERE, "stencil.npz"), **stencil_golden())
+    if want("select"):
+        np.savez_compressed(os.path.join(HERE, "select.npz"), **select_golden())
+    if want("ilu0"):
+        np.savez_compressed(os.path.join(HERE, "ilu0.npz"), **ilu0_golden(ilu0_family()))
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

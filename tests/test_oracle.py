@@ -201,3 +201,27 @@ def test_selector_golden_with_injected_timer():
     assert int(g["s_s3fast_sel"]) == 2
     assert int(g["s_tie23_sel"]) == 0
     assert (g["u_u2fast_exec"] <= 4).all()
+
+
+def test_ilu0_restatement_pinned_bitwise():
+    """oracle ko_ilu0_factorize / ko_ilu0_apply == the reference's
+    ilu0_factorize / ilu0_apply (tests/golden/ilu0.npz) bit for bit, and the
+    same failure messages."""
+    g = np.load(os.path.join(GOLD, "ilu0.npz"))
+    for c in range(int(g["count"])):
+        p = f"c{c}_"
+        n, rp, ci, v = int(g[p + "n"]), g[p + "rp"], g[p + "ci"], g[p + "v"]
+        fv, diag = O.ilu0_factorize(n, rp, ci, v)
+        assert np.array_equal(diag, g[p + "diag"])
+        assert np.array_equal(fv.view(np.int64), g[p + "fv"].view(np.int64)), c
+        z = O.ilu0_apply(n, rp, ci, fv, diag, g[p + "r"])
+        assert np.array_equal(z.view(np.int64), g[p + "z"].view(np.int64)), c
+    errs = []
+    for n, rp, ci, v in [
+            (3, np.array([0, 2, 3, 5]), np.array([0, 1, 0, 1, 2]), np.ones(5)),
+            (2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.ones(4)),
+            (2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([0.0, 1.0, 1.0, 1.0]))]:
+        with pytest.raises(O.OracleError) as e:
+            O.ilu0_factorize(n, rp, ci, v)
+        errs.append(str(e.value))
+    assert errs == list(g["errors"])
