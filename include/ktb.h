@@ -284,10 +284,16 @@ int ktb_vec_axpby(int64_t n, double a, const double* x, double b, double* y, voi
 int ktb_vec_scale(int64_t n, double s, int divide, double* x, void* stream);
 
 /* -------------------------------------------------------------- ILU(0) */
+typedef struct ktb_ilu ktb_ilu;
+/* gmres_m with ILU(0) right preconditioning (gmres.hpp:16-173 with
+ * Precond{ilu0_apply}, the pairing meta.hpp:195-201 makes): each Arnoldi
+ * step applies z = M^{-1} v_j before the SpMV, the correction is
+ * x += M^{-1}(Q y). Same arguments as ktb_gmres plus the factors. */
+int ktb_gmres_ilu0(ktb_plan* A, ktb_ilu* P, const double* b, double* x, int64_t m, double tol,
+                   int64_t max_iters, double* history, ktb_gmres_result* res);
 /* ilu0.hpp: incomplete LU on the pattern of a GENERAL matrix (unit L, U on
  * the stored pattern). Factors and solves are bitwise equal to the
  * reference's (level-scheduled rows, reference operation order, no FMA). */
-typedef struct ktb_ilu ktb_ilu;
 /* ilu0_factorize (ilu0.hpp:23-69); same messages ("ilu0: structurally
  * missing diagonal in row i", "ilu0: zero pivot at row i"). stream may be
  * NULL. */

@@ -121,6 +121,8 @@ def ref():
         L.kr_max_threads.restype = C.c_int
         L.kr_ilu0_factorize.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _i64p]
         L.kr_ilu0_apply.argtypes = [_I64, _i64p, _i64p, _f64p, _i64p, _f64p, _f64p]
+        L.kr_gmres_ilu0.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _I64, C.c_double, _I64,
+                                    C.c_int, _f64p] + [C.c_void_p] * 4
         L.kr_mm_probe.argtypes = [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64),
                                   C.POINTER(C.c_int)]
         L.kr_mm_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
@@ -457,6 +459,19 @@ class Ref:
         _chk_ref(ref().kr_ilu0_apply(n, rp, ci, fv, np.ascontiguousarray(diag, np.int64),
                                      np.ascontiguousarray(r, np.float64), z))
         return z
+
+    @staticmethod
+    def gmres_ilu0(n, rp, ci, v, b, m=30, tol=1e-8, max_iters=3000, ortho_kind=1):
+        """The reference's gmres_m with Precond = its ilu0_apply."""
+        rp, ci, v = _csr(rp, ci, v)
+        x = np.empty(n, np.float64)
+        its, rs = _I64(), _I64()
+        conv, tru = C.c_int(), C.c_double()
+        _chk_ref(ref().kr_gmres_ilu0(n, rp, ci, v, np.ascontiguousarray(b, np.float64), m, tol,
+                                     max_iters, ortho_kind, x, C.byref(its), C.byref(rs),
+                                     C.byref(conv), C.byref(tru)))
+        return x, dict(iterations=its.value, restarts=rs.value, converged=bool(conv.value),
+                       true_residual=tru.value)
 
     @staticmethod
     def mm_probe(path):

@@ -446,4 +446,32 @@ int kr_ilu0_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     });
 }
 
+
+// gmres_m with the ILU(0) right preconditioner (gmres.hpp:16-173 with
+// Precond{ilu0_apply}, as meta.hpp:195-201 wires it), sequential operator.
+int kr_gmres_ilu0(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                  const double* b, int64_t m, double tol, int64_t max_iters, int ortho_kind,
+                  double* x, int64_t* iterations, int64_t* restarts, int* converged,
+                  double* true_res) {
+    return guarded([&] {
+        const auto a = make_csr(n, rp, ci, v);
+        const IluFactors f = ilu0_factorize(a);
+        Precond pc;
+        pc.apply = [&f](std::span<const double> r, std::span<double> z) { ilu0_apply(f, r, z); };
+        KrylovConfig cfg;
+        cfg.restart_m = m;
+        cfg.m_max = m;
+        cfg.tol = tol;
+        cfg.max_iters = max_iters;
+        cfg.max_time = 1e30;
+        cfg.ortho.kind = static_cast<OrthoKind>(ortho_kind);
+        const SolverResult r = gmres_m(make_ref_op(a), std::span<const double>(b, n), cfg, pc);
+        std::memcpy(x, r.x.data(), sizeof(double) * n);
+        *iterations = r.iterations;
+        *restarts = static_cast<int64_t>(r.restarts.size());
+        *converged = r.converged ? 1 : 0;
+        *true_res = r.true_residual;
+    });
+}
+
 }  // extern "C"

@@ -100,6 +100,7 @@ def load() -> C.CDLL:
         "ktb_time_spmv": ([VP, VP, VP, C.c_int, C.c_size_t, C.POINTER(C.c_double),
                            C.POINTER(C.c_double)], C.c_int),
         "ktb_gmres": ([VP, VP, VP, I64, C.c_double, I64, VP, VP], C.c_int),
+        "ktb_gmres_ilu0": ([VP, VP, VP, VP, I64, C.c_double, I64, VP, VP], C.c_int),
     }
     for name, spec in sig.items():
         if spec is None:

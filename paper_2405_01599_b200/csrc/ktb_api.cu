@@ -34,8 +34,8 @@ ktb_matrix* gen_stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t
 ktb_matrix* gen_stencil27_upper(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
                                 int device);
 void seeded_vector_dev(int64_t n, uint64_t seed, int64_t offset, double* d_out, cudaStream_t s);
-void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, double tol,
-               int64_t max_iters, double* history, ktb_gmres_result* res);
+void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, int64_t m,
+               double tol, int64_t max_iters, double* history, ktb_gmres_result* res);
 ktb_matrix* gen_powerlaw(int64_t n, uint64_t seed, int64_t target, double empty_frac,
                          int64_t max_len, int device);
 ktb_matrix* matrix_slice(const ktb_matrix* m, int64_t r0, int64_t r1);
@@ -637,7 +637,15 @@ int ktb_spmv_rows(ktb_plan* p, int64_t row_begin, int64_t row_end, const double*
 
 int ktb_gmres(ktb_plan* A, const double* b, double* x, int64_t m, double tol, int64_t max_iters,
               double* history, ktb_gmres_result* res) {
-    return guarded([&] { gmres_run(A, b, x, m, tol, max_iters, history, res); });
+    return guarded([&] { gmres_run(A, nullptr, b, x, m, tol, max_iters, history, res); });
+}
+
+int ktb_gmres_ilu0(ktb_plan* A, ktb_ilu* P, const double* b, double* x, int64_t m, double tol,
+                   int64_t max_iters, double* history, ktb_gmres_result* res) {
+    return guarded([&] {
+        require(P != nullptr, "ilu0: null handle");
+        gmres_run(A, P, b, x, m, tol, max_iters, history, res);
+    });
 }
 
 int ktb_stream_sync(void* stream) {

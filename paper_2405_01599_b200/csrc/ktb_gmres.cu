@@ -140,13 +140,20 @@ __global__ void k_update_x(const double* __restrict__ V, const double* __restric
     x[i] = __dadd_rn(x[i], __dmul_rn(1.0, acc));
 }
 
+// x += 1.0 * z (gmres.hpp:142 axpy(1.0, z, res.x))
+__global__ void k_add_z(const double* __restrict__ z, int64_t n, double* __restrict__ x) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(1.0, z[i]));
+}
+
 }  // namespace ktb
 
 namespace ktb {
 
-// Restarted GMRES(m), MGS, x0 = 0 (gmres.hpp:16-173); host b/x spans.
-void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, double tol,
-               int64_t max_iters, double* history, ktb_gmres_result* res) {
+// Restarted GMRES(m), MGS, x0 = 0 (gmres.hpp:16-173); host b/x spans. P:
+// optional ILU(0) right preconditioner (Precond, solver_types.hpp:22-27).
+void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, int64_t m,
+               double tol, int64_t max_iters, double* history, ktb_gmres_result* res) {
         require(A != nullptr && res != nullptr, "gmres: null argument");
         require(m >= 1, "gmres: need 1 <= m <= m_max");  // gmres.hpp:20
         require(tol > 0.0, "gmres: tol must be positive");  // gmres.hpp:21
@@ -163,7 +170,13 @@ void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, dou
         KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs, kGThreads, 0));
         require(per_sm >= 1, "gmres: cooperative MGS kernel does not fit");
         const int nb = sms * std::min(per_sm, 2);
+        if (P) {
+            int64_t pn = 0;
+            ilu0_info(P, &pn, nullptr, nullptr, nullptr);
+            require(pn == n, "gmres: dimension mismatch");
+        }
         DBuf<double> b(n), x(n), r(n), w(n), V(static_cast<size_t>(n) * (m + 1));
+        DBuf<double> zp(P ? n : 1);
         DBuf<double> partials(4 * nb), dh(m + 2), dy(m + 1);
         DBuf<int> dbreak(1);
         KTB_CUDA(cudaMemcpyAsync(b.p, b_host, 8 * n, cudaMemcpyHostToDevice, st));
@@ -232,7 +245,12 @@ void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, dou
                     stop = true;
                     break;
                 }
-                spmv_timed(V.p + j * n, w.p);
+                if (P) {  // gmres.hpp:91-92: z = M^{-1} v_j, w = A z
+                    ilu0_apply(P, V.p + j * n, zp.p, st);
+                    spmv_timed(zp.p, w.p);
+                } else {
+                    spmv_timed(V.p + j * n, w.p);
+                }
                 // orthogonalise against columns 0..j; V_{j+1} = w / |w|
                 int kk = static_cast<int>(j + 1);
                 const double* Vp = V.p;
@@ -286,7 +304,15 @@ void gmres_run(ktb_plan* A, const double* b_host, double* x_host, int64_t m, dou
                     yv[i] = rii != 0.0 ? s / rii : 0.0;
                 }
                 KTB_CUDA(cudaMemcpyAsync(dy.p, yv.data(), 8 * j, cudaMemcpyHostToDevice, st));
-                k_update_x<<<eb, 256, 0, st>>>(V.p, dy.p, static_cast<int>(j), n, x.p);
+                if (P) {  // w = Q y; z = M^{-1} w; x += z (gmres.hpp:138-143)
+                    KTB_CUDA(cudaMemsetAsync(w.p, 0, 8 * n, st));
+                    k_update_x<<<eb, 256, 0, st>>>(V.p, dy.p, static_cast<int>(j), n, w.p);
+                    KTB_LAUNCH();
+                    ilu0_apply(P, w.p, zp.p, st);
+                    k_add_z<<<eb, 256, 0, st>>>(zp.p, n, x.p);
+                } else {
+                    k_update_x<<<eb, 256, 0, st>>>(V.p, dy.p, static_cast<int>(j), n, x.p);
+                }
                 KTB_LAUNCH();
             }
             if (rr < tol) {

@@ -183,9 +183,12 @@ def orthogonalize(kind, V, k, w, ops, ar, bufs, block_len=4):
 
 
 def gmres_m_dist(op, b, m=30, tol=1e-8, max_iters=3000, ortho="mgs", block_len=4, ops=None,
-                 allreduce=None, max_time=math.inf) -> DistSolverResult:
-    """gmres.hpp:16-173 (no preconditioner, fixed restart m) with sharded
-    vectors. b: this rank's slice (device tensor for DeviceVecOps)."""
+                 allreduce=None, max_time=math.inf, precond=None) -> DistSolverResult:
+    """gmres.hpp:16-173 (fixed restart m) with sharded vectors. b: this rank's
+    slice (device tensor for DeviceVecOps). precond(r, z): the right
+    preconditioner on this rank's slice (e.g. ILU(0) factors of the rank's
+    diagonal block -- block Jacobi across ranks; the exact reference
+    pairing on one rank)."""
     if m < 1:
         raise ValueError("gmres: need 1 <= m <= m_max")
     if tol <= 0.0:
@@ -209,6 +212,7 @@ def gmres_m_dist(op, b, m=30, tol=1e-8, max_iters=3000, ortho="mgs", block_len=4
         return res
     V = ops.zeros(m + 1, n)
     r, w = ops.zeros(n), ops.zeros(n)
+    zp = ops.zeros(n) if precond is not None else None
     cs, sn = [0.0] * (m + 1), [0.0] * (m + 1)
     r_cols = [[0.0] * (m + 1) for _ in range(m)]
     rr = 1.0
@@ -231,7 +235,11 @@ def gmres_m_dist(op, b, m=30, tol=1e-8, max_iters=3000, ortho="mgs", block_len=4
             if res.iterations >= max_iters or time.perf_counter() - t0 > max_time:
                 stop = True
                 break
-            op.apply(V[j], w)
+            if precond is not None:  # gmres.hpp:91-92
+                precond(V[j], zp)
+                op.apply(zp, w)
+            else:
+                op.apply(V[j], w)
             h, breakdown = orthogonalize(ortho, V, j + 1, w, ops, ar, (coef, nbuf), block_len)
             if breakdown:
                 h[j + 1] = 0.0
@@ -268,7 +276,11 @@ def gmres_m_dist(op, b, m=30, tol=1e-8, max_iters=3000, ortho="mgs", block_len=4
             ops.from_host(y, coef[:j])
             ops.scale(0.0, w)
             ops.maxpy(V[:j], j, coef, 1.0, w)
-            ops.axpby(1.0, w, 1.0, x)
+            if precond is not None:
+                precond(w, zp)
+                ops.axpby(1.0, zp, 1.0, x)
+            else:
+                ops.axpby(1.0, w, 1.0, x)
         if rr < tol:
             res.converged = True
             break

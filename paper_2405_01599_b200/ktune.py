@@ -820,9 +820,11 @@ class _GmresRes(C.Structure):
                 ("seconds", C.c_double), ("spmv_seconds", C.c_double)]
 
 
-def gmres_m(a, b, cfg: KrylovConfig = KrylovConfig(), plan: Optional[DevicePlan] = None):
+def gmres_m(a, b, cfg: KrylovConfig = KrylovConfig(), plan: Optional[DevicePlan] = None,
+            precond: Optional["IluFactors"] = None):
     """gmres.hpp:16-173 (GMRES(m), MGS, x0 = 0) with every vector in HBM and
-    the SpMV on `plan` (default: the device-time selected kernel)."""
+    the SpMV on `plan` (default: the device-time selected kernel); `precond`
+    = ILU(0) factors (ilu0_factorize) as the right preconditioner."""
     require(len(b) == a.n, "gmres: dimension mismatch")
     require(1 <= cfg.restart_m <= cfg.m_max, "gmres: need 1 <= m <= m_max")
     require(cfg.tol > 0.0, "gmres: tol must be positive")
@@ -832,8 +834,13 @@ def gmres_m(a, b, cfg: KrylovConfig = KrylovConfig(), plan: Optional[DevicePlan]
     x = np.empty(a.n, np.float64)
     hist = np.zeros(max(cfg.max_iters, 1), np.float64)
     r = _GmresRes()
-    _check(_lib.load().ktb_gmres(plan.h, b.ctypes.data, x.ctypes.data, cfg.restart_m, cfg.tol,
-                                 cfg.max_iters, hist.ctypes.data, C.byref(r)))
+    if precond is None:
+        _check(_lib.load().ktb_gmres(plan.h, b.ctypes.data, x.ctypes.data, cfg.restart_m,
+                                     cfg.tol, cfg.max_iters, hist.ctypes.data, C.byref(r)))
+    else:
+        _check(_lib.load().ktb_gmres_ilu0(plan.h, precond.h, b.ctypes.data, x.ctypes.data,
+                                          cfg.restart_m, cfg.tol, cfg.max_iters,
+                                          hist.ctypes.data, C.byref(r)))
     return SolverResult(x, bool(r.converged), bool(r.breakdown), bool(r.fault_convergence),
                         r.iterations, r.restarts, r.recurrence_residual, r.true_residual,
                         hist[: r.iterations].copy(), r.seconds, r.spmv_calls, r.spmv_seconds)

@@ -178,3 +178,31 @@ def test_single_rank_loop_and_allreduce_counts():
     with pytest.raises(ValueError, match="unknown kind"):
         KR.gmres_m_dist(Op(), torch.from_numpy(bg.copy()), ortho="householder", ops=CpuVecOps(),
                         allreduce=lambda t: None)
+
+
+def test_single_rank_ilu0_right_preconditioning_matches_reference():
+    """The host loop with a right preconditioner (here the oracle's ILU(0),
+    test infrastructure) reproduces the reference's gmres_m + ilu0 pairing."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n, rp, ci, v = _matrix()
+    bg = O.spmv_ref(n, rp, ci, v, np.ones(n))
+    fv, diag = O.ilu0_factorize(n, rp, ci, v)
+
+    class Op:
+        n_local = n
+
+        def apply(self, x, y):
+            y.copy_(torch.from_numpy(O.spmv_ref(n, rp, ci, v, x.numpy())))
+
+    def pc(r, z):
+        z.copy_(torch.from_numpy(O.ilu0_apply(n, rp, ci, fv, diag, r.numpy())))
+
+    res = KR.gmres_m_dist(Op(), torch.from_numpy(bg.copy()), m=30, tol=1e-8, max_iters=500,
+                          ops=CpuVecOps(), allreduce=lambda t: None, precond=pc)
+    xr, rr = O.Ref.gmres_ilu0(n, rp, ci, v, bg)
+    assert res.converged and res.true_residual < 1e-8
+    assert abs(res.iterations - rr["iterations"]) <= 2, (res.iterations, rr["iterations"])
+    assert res.iterations < 0.5 * KR.gmres_m_dist(
+        Op(), torch.from_numpy(bg.copy()), m=30, tol=1e-8, max_iters=500, ops=CpuVecOps(),
+        allreduce=lambda t: None).iterations
