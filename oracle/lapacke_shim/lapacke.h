@@ -1,6 +1,8 @@
 /* Minimal LAPACKE prototypes so the reference umbrella headers that include
- * dense_eig.hpp compile in this image (no lapacke.h is installed). Nothing in
- * oracle/_ref calls these; they are declarations only. TEST INFRASTRUCTURE. */
+ * dense_eig.hpp compile in this image (no lapacke.h is installed).
+ * libktune_ref.so calls neither; libktune_ref_eig.so (the reference's Lanczos)
+ * calls LAPACKE_dsteqr, resolved from the OpenBLAS the python env bundles
+ * (oracle/Makefile). TEST INFRASTRUCTURE. */
 #pragma once
 typedef int lapack_int;
 #define LAPACK_ROW_MAJOR 101

@@ -139,6 +139,42 @@ class OracleError(RuntimeError):
     pass
 
 
+REF_EIG_SO = os.path.join(os.path.dirname(REF_SO), "libktune_ref_eig.so")
+_ref_eig = None
+
+
+def ref_eig_available() -> bool:
+    return os.path.exists(REF_EIG_SO)
+
+
+def ref_eig():
+    """The reference's Lanczos (oracle/ref_shim_eig.cpp, LAPACKE from the
+    python env's bundled OpenBLAS)."""
+    global _ref_eig
+    if _ref_eig is None:
+        L = C.CDLL(REF_EIG_SO)
+        L.kre_last_error.restype = C.c_char_p
+        L.kre_lanczos.argtypes = [_I64, _i64p, _i64p, _f64p, _I64, _I64, C.c_double, _I64,
+                                  C.c_int, C.c_uint64, _f64p, _f64p] + [C.c_void_p] * 4
+        _ref_eig = L
+    return _ref_eig
+
+
+def ref_lanczos(n, rp, ci, v, k, m=30, tol=1e-8, max_iters=10000, ortho_kind=1, seed=20080517):
+    """lanczos_restarted(SymCsrMatrix, k, cfg) of the reference (sym upper
+    storage in) -> (eigenvalues, residuals, info dict)."""
+    rp, ci, v = _csr(rp, ci, v)
+    ev, rs = np.zeros(k), np.zeros(k)
+    nf, its, rst = _I64(), _I64(), _I64()
+    conv = C.c_int()
+    rc = ref_eig().kre_lanczos(n, rp, ci, v, k, m, tol, max_iters, ortho_kind, seed, ev, rs,
+                               C.byref(nf), C.byref(its), C.byref(rst), C.byref(conv))
+    if rc:
+        raise OracleError(ref_eig().kre_last_error().decode())
+    return ev[: nf.value], rs[: nf.value], dict(iterations=its.value, restarts=rst.value,
+                                                converged=bool(conv.value))
+
+
 def _chk_ref(rc: int) -> None:
     if rc != 0:
         raise OracleError(ref().kr_last_error().decode())

@@ -111,6 +111,15 @@ class DeviceVecOps:
 
         out.copy_(torch.tensor(vals, dtype=torch.float64))
 
+    def copy(self, src, dst):
+        self.axpby(1.0, src, 0.0, dst)
+
+    def seeded(self, seed, offset, out):
+        """out[i] = detail::seeded_vector(N, seed)[offset + i] (lanczos.hpp:17-29)."""
+        self._chk(self._L.ktb_seeded_vector(out.shape[0], int(seed) & (2 ** 64 - 1), int(offset),
+                                            out.data_ptr(), self._s()))
+        self.launches += 1 if out.shape[0] else 0
+
 
 def process_group_allreduce(group=None):
     """Sum a tensor in place over the default (or given) process group; a
@@ -296,6 +305,162 @@ def gmres_m_dist(op, b, m=30, tol=1e-8, max_iters=3000, ortho="mgs", block_len=4
     ops.axpby(1.0, b, -1.0, r)
     res.true_residual = _norm(ops, ar, r, nbuf) / nb
     res.fault_convergence = res.converged and res.true_residual > tol
+    res.allreduces = ar.n
+    res.elapsed_seconds = time.perf_counter() - t0
+    return res
+
+
+@dataclass
+class DistEigenResult:  # EigenResult (solver_types.hpp:79-100), real eigenpairs
+    eigenvalues: list = field(default_factory=list)
+    eigenvectors: list = field(default_factory=list)  # this rank's slices
+    residuals: list = field(default_factory=list)
+    max_residual: float = 0.0
+    converged: bool = False
+    breakdown: bool = False
+    breakdown_reason: str = ""
+    fault_convergence: bool = False
+    iterations: int = 0
+    restarts: list = field(default_factory=list)
+    residual_history: list = field(default_factory=list)
+    allreduces: int = 0
+    elapsed_seconds: float = 0.0
+
+
+def tridiag_eig(alpha, beta):
+    """dense_eig.hpp:22-35 (LAPACKE_dsteqr, compz 'I'): eigenvalues ascending,
+    eigenvector i = column i. dstev computes the vectors with the same dsteqr
+    QL iteration. Host scalars (m <= m_max)."""
+    import numpy as np
+    from scipy.linalg import eigh_tridiagonal
+
+    d = np.asarray(alpha, np.float64)
+    if len(d) == 1:
+        return np.array([d[0]]), np.ones((1, 1))
+    return eigh_tridiagonal(d, np.asarray(beta, np.float64), lapack_driver="stev")
+
+
+def lanczos_restarted_dist(op, k, m=30, m_max=None, tol=1e-8, max_iters=10000, ortho="mgs",
+                           block_len=4, seed=20080517, row0=0, n_global=None, ops=None,
+                           allreduce=None, max_time=math.inf) -> DistEigenResult:
+    """lanczos.hpp:54-192: explicitly restarted Lanczos for the k largest-
+    magnitude eigenpairs of a symmetric operator, every new basis vector fully
+    re-orthogonalised (the configured variant; DGKS for seating and locking),
+    on row-sharded vectors. `op` is the symmetric operator on this rank's
+    rows (e.g. the S3 plan: SymEngine::op, meta.hpp:53-68); row0/n_global
+    place this rank's slice of the seeded start vector."""
+    n = op.n_local
+    N = n if n_global is None else n_global
+    m_max = m if m_max is None else m_max
+    if k < 1:
+        raise ValueError("lanczos: k must be >= 1")
+    if k > N:
+        raise ValueError("lanczos: k exceeds the matrix dimension")
+    if m < k + 2:
+        raise ValueError("lanczos: restart_m must be >= k+2")
+    if m > m_max:
+        raise ValueError("lanczos: restart_m exceeds m_max")
+    ar = _Counter(allreduce or process_group_allreduce())
+    ops = ops or DeviceVecOps(k + m_max + 2, op.device if hasattr(op, "device") else 0)
+    t0 = time.perf_counter()
+    res = DistEigenResult()
+    cols = k + m_max + 2
+    vecs = ops.zeros(cols, n)
+    coef = ops.zeros(cols)
+    nbuf = ops.zeros(1)
+    bufs = (coef, nbuf)
+    w = ops.zeros(n)
+    start = ops.zeros(n)
+    ops.seeded(seed, row0, start)
+    reseed = seed
+    nlocked = 0
+    locked_vals = []
+    msize = m
+    out_of_budget = False
+    while nlocked < k and not out_of_budget:
+        seated = False
+        for _ in range(16):  # seat the start vector orthogonal to the locked set
+            ops.copy(start, w)
+            _, brk = orthogonalize("dgks", vecs, nlocked, w, ops, ar, bufs, block_len)
+            if not brk:
+                seated = True
+                break
+            reseed += 1
+            ops.seeded(reseed, row0, start)
+        if not seated:
+            res.breakdown = True
+            res.breakdown_reason = "invariant subspace exhausted before k pairs"
+            break
+        ops.copy(w, vecs[nlocked])
+        alpha, beta = [], []
+        ma = 0
+        for j in range(msize):
+            if res.iterations >= max_iters or time.perf_counter() - t0 > max_time:
+                out_of_budget = True
+                break
+            op.apply(vecs[nlocked + j], w)
+            res.iterations += 1
+            h, brk = orthogonalize(ortho, vecs, nlocked + j + 1, w, ops, ar, bufs, block_len)
+            alpha.append(h[nlocked + j])
+            ma = j + 1
+            if brk:
+                beta.append(0.0)  # the subspace closed exactly
+                break
+            beta.append(h[nlocked + j + 1])
+            ops.copy(w, vecs[nlocked + j + 1])
+        if ma == 0:
+            break
+        vals, Y = tridiag_eig(alpha, beta[: ma - 1])
+        beta_last = beta[ma - 1]
+        order = sorted(range(ma), key=lambda i: -abs(vals[i]))  # stable, as magnitude_order
+        want = min(k - nlocked, ma)
+        sample = 0.0
+        ready, restart_dir = [], None
+        for t in range(want):
+            i = order[t]
+            y = [float(Y[l, i]) for l in range(ma)]
+            est = abs(beta_last * y[ma - 1])
+            sample = max(sample, est)
+            ops.scale(0.0, w)
+            ops.from_host(y, coef[:ma])
+            ops.maxpy(vecs[nlocked:nlocked + ma], ma, coef, 1.0, w)
+            if est < tol:
+                v = ops.zeros(n)
+                ops.copy(w, v)
+                ready.append((float(vals[i]), v))
+            elif restart_dir is None:
+                restart_dir = ops.zeros(n)
+                ops.copy(w, restart_dir)
+        for val, vec in ready:
+            _, brk = orthogonalize("dgks", vecs, nlocked, vec, ops, ar, bufs, block_len)
+            if brk:
+                continue
+            ops.copy(vec, vecs[nlocked])
+            nlocked += 1
+            locked_vals.append(val)
+        if nlocked >= k:
+            break
+        if restart_dir is not None:
+            start = restart_dir
+        else:
+            reseed += 1
+            ops.seeded(reseed, row0, start)
+        if not out_of_budget:
+            res.restarts.append((res.iterations, msize))
+            if sample > 0.0:
+                res.residual_history.append(sample)
+    res.converged = nlocked >= k
+    r = ops.zeros(n)
+    for i in sorted(range(nlocked), key=lambda i: -abs(locked_vals[i])):
+        v = vecs[i]
+        op.apply(v, r)  # true_residual_eigen (solver_types.hpp:113-119)
+        ops.axpby(-locked_vals[i], v, 1.0, r)
+        rn = _norm(ops, ar, r, nbuf)
+        res.eigenvalues.append(locked_vals[i])
+        res.eigenvectors.append(v)
+        res.residuals.append(rn)
+        res.max_residual = max(res.max_residual, rn)
+    res.fault_convergence = res.converged and res.max_residual > tol
     res.allreduces = ar.n
     res.elapsed_seconds = time.perf_counter() - t0
     return res

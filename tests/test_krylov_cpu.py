@@ -32,6 +32,16 @@ def _matrix():
 class CpuVecOps:
     """torch-CPU stand-in for DeviceVecOps (same method contract)."""
 
+    def __init__(self, n_global=None):
+        self.n_global = n_global
+
+    def copy(self, src, dst):
+        dst.copy_(src)
+
+    def seeded(self, seed, offset, out):
+        full = O.seeded_vector(self.n_global, seed)
+        out.copy_(torch.from_numpy(full[offset:offset + out.shape[0]].copy()))
+
     def empty(self, *s):
         return torch.empty(*s, dtype=torch.float64)
 
