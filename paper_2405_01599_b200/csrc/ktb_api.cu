@@ -48,6 +48,10 @@ thread_local std::string g_err;
 
 template <typename F>
 int guarded(F&& f) {
+    // a launch check (cudaGetLastError) must only see this call's launches:
+    // drop any non-sticky error an earlier call (or a caller's own runtime
+    // use) left behind -- those were reported where they happened
+    (void)cudaGetLastError();
     try {
         f();
         return KTB_OK;

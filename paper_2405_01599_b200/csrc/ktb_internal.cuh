@@ -28,9 +28,11 @@ inline void require(bool cond, const char* msg) {
 }
 
 inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
-    if (e != cudaSuccess)
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // reported here: do not leak into a later launch check
         throw CudaError(std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
                         std::to_string(line) + ")");
+    }
 }
 #define KTB_CUDA(x) ::ktb::cuda_check((x), #x, __FILE__, __LINE__)
 #define KTB_LAUNCH() ::ktb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
