@@ -16,6 +16,10 @@
 //   build_reduction_regions (partition.hpp:73-96) ktb_cpp::build_reduction_regions
 //   build_bss_plan (bss.hpp:34-69)                ktb_cpp::bss_plan_arrays
 //   ktune::Error (common.hpp:18-21)               ktb_cpp::Error (same messages)
+//   ilu0_factorize / ilu0_apply (ilu0.hpp)        ktb_cpp::Ilu0 (.apply, .factors,
+//     + Precond (solver_types.hpp:22-27)            .precond() -> ktune::Precond)
+//   load_matrix_market / write_matrix_market      ktb_cpp::load_matrix_market<Csr, Sym>,
+//     (matrix_market.hpp:165-239)                   ktb_cpp::write_matrix_market
 //
 // Matrices are taken by duck typing (any type with members n, row_ptr,
 // col_idx, values holding int64 / double contiguous storage), so the
@@ -32,6 +36,8 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <variant>
 #include <vector>
 
 #include "ktb.h"
@@ -295,6 +301,102 @@ inline std::pair<std::vector<index_t>, std::vector<index_t>> build_reduction_reg
     std::vector<index_t> lo(P), hi(P);
     check(ktb_reduction_regions(m.get(), P, boundaries.data(), lo.data(), hi.data()));
     return {lo, hi};
+}
+
+// ---------------------------------------------------------------- ILU(0)
+// ilu0_factorize on the device (bit-exact factors); precond() plugs the
+// device solve into the reference's solvers as their Precond.
+struct PrecondView {
+    std::function<void(std::span<const double>, std::span<double>)> apply;
+    template <typename P>
+    operator P() const {
+        P p;
+        p.apply = apply;
+        return p;
+    }
+};
+
+class Ilu0 {
+public:
+    explicit Ilu0(std::shared_ptr<DeviceMatrix> m) : m_(std::move(m)) {
+        check(ktb_ilu0_create(m_->get(), nullptr, &h_));
+    }
+    template <typename M>
+    explicit Ilu0(const M& a, int device = 0)
+        : Ilu0(std::make_shared<DeviceMatrix>(a, false, device)) {}
+    ~Ilu0() {
+        if (h_) ktb_ilu0_destroy(h_);
+    }
+    Ilu0(const Ilu0&) = delete;
+    Ilu0& operator=(const Ilu0&) = delete;
+    // ilu0.hpp:73-87 on host spans (z = (LU)^{-1} r)
+    void apply(std::span<const double> r, std::span<double> z) const {
+        if (static_cast<index_t>(r.size()) != m_->n() || static_cast<index_t>(z.size()) != m_->n())
+            throw Error("ilu0: dimension mismatch");
+        check(ktb_ilu0_apply(h_, r.data(), z.data(), KTB_PTR_HOST, nullptr));
+    }
+    // device pointers, enqueued on `stream` (nullptr = legacy default stream)
+    void apply_device(const double* r, double* z, void* stream = nullptr) const {
+        check(ktb_ilu0_apply(h_, r, z, KTB_PTR_DEVICE, stream));
+    }
+    // IluFactors::diag_ptr and ::values (ilu0.hpp:14-18)
+    std::pair<std::vector<index_t>, std::vector<double>> factors() const {
+        int64_t nnz = 0;
+        check(ktb_matrix_info(m_->get(), nullptr, &nnz, nullptr, nullptr, nullptr));
+        std::vector<int32_t> d(static_cast<std::size_t>(m_->n()));
+        std::vector<double> v(static_cast<std::size_t>(nnz));
+        check(ktb_ilu0_download(h_, d.data(), v.data()));
+        return {std::vector<index_t>(d.begin(), d.end()), std::move(v)};
+    }
+    PrecondView precond() const {
+        return {[this](std::span<const double> r, std::span<double> z) { apply(r, z); }};
+    }
+    ktb_ilu* get() const { return h_; }
+
+private:
+    std::shared_ptr<DeviceMatrix> m_;
+    ktb_ilu* h_ = nullptr;
+};
+
+// ------------------------------------------------------- Matrix Market
+// load_matrix_market (matrix_market.hpp:165-194): the same variant shape --
+// Sym when want_symmetric, Csr otherwise -- for any duck-typed Csr / Sym.
+template <typename Csr, typename Sym>
+std::variant<Csr, Sym> load_matrix_market(const std::string& path, bool want_symmetric) {
+    ktb_csr_host* h = nullptr;
+    check(ktb_mm_read(path.c_str(), want_symmetric ? 1 : 0, &h));
+    int64_t n = 0, nnz = 0;
+    int kind = 0;
+    const int rc = ktb_csr_host_info(h, &n, &nnz, &kind);
+    if (rc != KTB_OK) {
+        ktb_csr_host_destroy(h);
+        check(rc);
+    }
+    auto fill = [&](auto& a) {
+        a.n = n;
+        a.row_ptr.resize(static_cast<std::size_t>(n + 1));
+        a.col_idx.resize(static_cast<std::size_t>(nnz));
+        a.values.resize(static_cast<std::size_t>(nnz));
+        const int r2 = ktb_csr_host_copy(h, a.row_ptr.data(), a.col_idx.data(), a.values.data());
+        ktb_csr_host_destroy(h);
+        check(r2);
+    };
+    if (kind == KTB_SYM_UPPER) {
+        Sym s;
+        fill(s);
+        return s;
+    }
+    Csr a;
+    fill(a);
+    return a;
+}
+
+// write_matrix_market (matrix_market.hpp:223-239); symmetric_upper selects the
+// SymCsrMatrix form (stored upper triangle written as the lower form)
+template <typename M>
+void write_matrix_market(const std::string& path, const M& a, bool symmetric_upper) {
+    check(ktb_mm_write(path.c_str(), a.n, a.row_ptr.data(), a.col_idx.data(), a.values.data(),
+                       symmetric_upper ? KTB_SYM_UPPER : KTB_GENERAL));
 }
 
 }  // namespace ktb_cpp

@@ -8,9 +8,18 @@
 //    -> same iteration count (+-2) and converged true residual < tol.
 // 2. ktune::gen_poisson2d (SymCsrMatrix): ktb_cpp::select_spmv_sym winner vs
 //    ktune::spmv_ref(ktune::expand_symmetric(A)).
+// 4. ILU(0): ktb_cpp::Ilu0 factors bit-exact vs ktune::ilu0_factorize, and
+//    ktune::gmres_m(engine op, b, cfg, ilu.precond()) vs the reference's own
+//    gmres_m + Precond{ilu0_apply} -> same iterations (+-2).
+// 5. Matrix Market: a file written by ktune::write_matrix_market loads through
+//    ktb_cpp::load_matrix_market into the same CsrMatrix / SymCsrMatrix as
+//    ktune::load_matrix_market; ktb_cpp::write_matrix_market is byte-identical.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
 
 #include "ktune/ktune.hpp"
 #include "ktune_b200.hpp"
@@ -93,6 +102,62 @@ int main(int argc, char** argv) {
         fail = 1;
     } catch (const ktb_cpp::Error& e) {
         if (std::string(e.what()) != "spmv: dimension mismatch") fail = 1;
+    }
+
+    // ---- 4: ILU(0) factors and the preconditioned reference solver
+    {
+        const auto fref = ktune::ilu0_factorize(a);
+        ktb_cpp::Ilu0 ilu(a);
+        const auto [diag, vals] = ilu.factors();
+        bool same = diag == fref.diag_ptr && vals.size() == fref.values.size();
+        for (std::size_t k = 0; same && k < vals.size(); ++k)
+            same = std::memcmp(&vals[k], &fref.values[k], sizeof(double)) == 0;
+        ktune::Precond pref;
+        pref.apply = [&fref](std::span<const double> r, std::span<double> z) {
+            ktune::ilu0_apply(fref, r, z);
+        };
+        const auto rp = ktune::gmres_m(ktune::make_ref_op(a), b, cfg, pref);
+        const ktune::Precond pgpu = ilu.precond();
+        const auto gp = ktune::gmres_m(op, b, cfg, pgpu);
+        const double tr = ktune::true_residual_linear(a, gp.x, b);
+        std::printf("{\"ilu0\": {\"factors_bitwise\": %d, \"ref_iterations\": %lld, "
+                    "\"gpu_iterations\": %lld, \"gpu_true_residual\": %.3g}}\n",
+                    same ? 1 : 0, static_cast<long long>(rp.iterations),
+                    static_cast<long long>(gp.iterations), tr);
+        if (!same || !gp.converged || tr >= cfg.tol ||
+            std::llabs(gp.iterations - rp.iterations) > 2)
+            fail = 1;
+    }
+    // ---- 5: Matrix Market through the B200 loader
+    {
+        const std::string fs = "/tmp/ktb_shim_sym.mtx", fg = "/tmp/ktb_shim_gen.mtx";
+        ktune::write_matrix_market(fs, s);
+        ktune::write_matrix_market(fg, a);
+        const auto rs = std::get<ktune::SymCsrMatrix>(ktune::load_matrix_market(fs, true));
+        const auto ks = std::get<ktune::SymCsrMatrix>(
+            ktb_cpp::load_matrix_market<ktune::CsrMatrix, ktune::SymCsrMatrix>(fs, true));
+        const auto rg = std::get<ktune::CsrMatrix>(ktune::load_matrix_market(fs, false));
+        const auto kg = std::get<ktune::CsrMatrix>(
+            ktb_cpp::load_matrix_market<ktune::CsrMatrix, ktune::SymCsrMatrix>(fs, false));
+        bool ok = rs.row_ptr == ks.row_ptr && rs.col_idx == ks.col_idx && rs.values == ks.values &&
+                  rg.row_ptr == kg.row_ptr && rg.col_idx == kg.col_idx && rg.values == kg.values;
+        ktb_cpp::write_matrix_market("/tmp/ktb_shim_gen2.mtx", a, false);
+        auto slurp = [](const std::string& p) {
+            std::ifstream in(p);
+            std::stringstream ss;
+            ss << in.rdbuf();
+            return ss.str();
+        };
+        ok = ok && slurp(fg) == slurp("/tmp/ktb_shim_gen2.mtx");
+        try {  // same message as the reference for a general file that is not symmetric
+            (void)ktb_cpp::load_matrix_market<ktune::CsrMatrix, ktune::SymCsrMatrix>(fg, true);
+            ok = false;
+        } catch (const ktb_cpp::Error& e) {
+            ok = ok && std::string(e.what()) ==
+                           "matrix market: general file is not numerically symmetric: " + fg;
+        }
+        std::printf("{\"matrix_market\": {\"identical\": %d}}\n", ok ? 1 : 0);
+        if (!ok) fail = 1;
     }
     std::printf("{\"ok\": %s}\n", fail ? "false" : "true");
     return fail;

@@ -34,3 +34,9 @@ def test_reference_gmres_runs_on_b200_engine():
     g = info["gmres"]
     assert abs(g["gpu_iterations"] - g["ref_iterations"]) <= 2
     assert g["gpu_true_residual"] < 1e-8 and g["max_executions"] <= 4
+    # ktb_cpp::Ilu0: factors bit-exact vs ktune::ilu0_factorize; as the Precond of
+    # ktune::gmres_m it matches the reference's own ILU-preconditioned solve
+    i = info["ilu0"]
+    assert i["factors_bitwise"] == 1 and abs(i["gpu_iterations"] - i["ref_iterations"]) <= 2
+    # ktb_cpp::load_matrix_market / write_matrix_market vs the reference's
+    assert info["matrix_market"]["identical"] == 1
