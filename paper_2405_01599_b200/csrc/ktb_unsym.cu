@@ -356,8 +356,10 @@ __global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __rest
     const int cnt = static_cast<int>(nnz - z0 < T ? nnz - z0 : T);
     const int32_t ra = __ldg(wrow + w), rb = __ldg(wrow + w + 1);
 #pragma unroll
-    for (int q = 0; q < IPT; q += 4)
-        *reinterpret_cast<int4*>(&s_end[warp][lane * IPT + q]) = make_int4(0, 0, 0, 0);  // own row
+    for (int q = 0; q < IPT; q += 4) {  // own row, in the swizzled chunk order (conflict-free)
+        const int phys = ((q >> 2) ^ ((lane >> ESH) & EMASK)) << 2;
+        *reinterpret_cast<int4*>(&s_end[warp][lane * IPT + phys]) = make_int4(0, 0, 0, 0);
+    }
 
     int32_t c[IPT];
     double v[IPT];
