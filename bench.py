@@ -443,9 +443,9 @@ def run_gpu_dist(args, cfg):
         shard = D.DistSpMV(nx, ny, nz, rank, ws, local, seed=cfg["seed"])
         n_glob = nx * ny * nz
         nnz_glob = 7 * n_glob - 6 * nx * nx  # 7-pt stencil with Dirichlet boundary
-        klabel = "u2 interior + u1 boundary planes (z-slab shards, NCCL halo)"
+        klabel = "u1 warp-sliced (param 100) interior + boundary planes (z-slab shards, NCCL halo)"
         par = f"row-block z-slabs x{ws}, one-plane halo"
-        rlabel = "u2 warp tiles on the rank-0 slab interior + u1 on its boundary planes"
+        rlabel = "u1 thread-per-row over the warp-sliced copy (rank-0 slab interior + boundary planes)"
     else:
         shard = _GeneralShard(cfg, rank, ws, local)
         n_glob, nnz_glob = shard.n_glob, shard.nnz_glob

@@ -745,6 +745,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
             Cand c{k, prm, {}};
             std::strncpy(c.rep.name, name, 7);
             c.rep.ordinal = ordinal;
+            c.rep.param = prm;  // replaced by the plan's resolved value once set up
             c.rep.workers = opts.workers > 0 ? opts.workers : m->sm_count;
             c.rep.best_seconds = std::numeric_limits<double>::infinity();
             list.push_back(c);
@@ -755,6 +756,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
             add(KTB_S3, 0, "s3", 2);
         } else {
             add(KTB_U1, 0, "u1", 0);
+            add(KTB_U1, 100, "u1", 0);  // thread per row over the warp-sliced copy
             add(KTB_U2, 0, "u2", 1);
             std::vector<int64_t> ept = {4, 8, 16};
             if (opts.params && opts.n_params > 0) ept.assign(opts.params, opts.params + opts.n_params);

@@ -228,6 +228,10 @@ struct ktb_plan {
     ktb::DBuf<double> carry_val;        // per tile carry-out
     ktb::DBuf<int32_t> carry_row;
     int64_t tiles = 0;
+    // U1 param 100: warp-sliced (SELL-32) copy of the matrix, see ktb_unsym.cu
+    ktb::DBuf<int64_t> sell_off;        // slices+1 element offsets (slice width = diff / 32)
+    ktb::DBuf<int32_t> sell_col;        // -1 = padding
+    ktb::DBuf<double> sell_val;
     // S1/S2 row blocks
     ktb::DBuf<int32_t> blocks;          // P+1 row boundaries
     // S3

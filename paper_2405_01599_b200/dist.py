@@ -148,12 +148,12 @@ def slab_csr_numpy(L: SlabLayout, diag=6.0, off=-1.0):
 
 class DistSpMV:
     """Config-4 sharded SpMV on this rank's GPU (torch.distributed, NCCL).
-    The slab is split once into its interior rows (no halo columns; U2 warp
-    tiles by default) and the boundary planes (U1), each a device matrix with
-    its own plan over the same local x."""
+    The slab is split once into its interior rows (no halo columns) and the
+    boundary planes, each a device matrix with its own plan over the same
+    local x; both default to U1 over the warp-sliced copy (param 100)."""
 
     def __init__(self, nx, ny, nz, rank, world, device, seed=4, diag=6.0, off=-1.0,
-                 interior_kernel=1):
+                 interior_kernel=0, interior_param=100, boundary_param=100):
         import torch
 
         from . import _lib
@@ -167,11 +167,12 @@ class DistSpMV:
         self.parts = []  # (r0, r1, plan)
         if hi > lo:
             a = slab.slice_rows(lo, hi)
-            self.parts.append((lo, hi, K.DevicePlan(a, int(interior_kernel))))
+            self.parts.append((lo, hi, K.DevicePlan(a, int(interior_kernel), int(interior_param))))
         self.boundary = []
         for b0, b1 in self.L.boundary_ranges():
             a = slab.slice_rows(b0, b1)
-            self.boundary.append((b0, b1, K.DevicePlan(a, K.UnsymKernel.u1_row)))
+            self.boundary.append((b0, b1, K.DevicePlan(a, K.UnsymKernel.u1_row,
+                                                       int(boundary_param))))
         del slab
         self.x = torch.empty(self.L.x_local_len, dtype=torch.float64, device=f"cuda:{device}")
         self.y = torch.empty(self.L.n_local, dtype=torch.float64, device=f"cuda:{device}")

@@ -272,7 +272,8 @@ def test_selector_unsym_and_sym(K):
     assert rep.selected >= 0 and rep.selected_candidate().correct
     assert rep.max_executions() <= 4
     names = [c.name for c in rep.candidates]
-    assert names[:2] == ["u1", "u2"] and set(names[2:]) == {"u3"}
+    assert names[:3] == ["u1", "u1", "u2"] and set(names[3:]) == {"u3"}
+    assert rep.candidates[1].jl == 100  # param slot (reference name jl): the warp-sliced U1
     x = O.seeded_vector(n, 1)
     y = np.empty(n)
     choice.plan.apply(x, y)
@@ -400,8 +401,9 @@ def test_config4_properties_full_size(K):
 
 
 def test_u2_all_tile_variants(K):
-    """Every U2 implementation (warp tiles IPT 4/8, merge path 104/108/112)
-    on random, skewed, empty-row and long-row matrices."""
+    """Every U2 implementation (warp tiles IPT 4/8, vector warp tiles
+    208/216, merge path 104/108/112) on random, skewed, empty-row and long-row
+    matrices; the vector tiles are bitwise equal to the scalar ones."""
     rng = np.random.default_rng(7)
     mats = []
     for t in range(8):
@@ -419,8 +421,61 @@ def test_u2_all_tile_variants(K):
         x = rng.uniform(-1, 1, n)
         a = K.CsrMatrix(n, rp, ci, v)
         yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
-        for prm in (4, 8, 104, 108, 112):
+        ys = {}
+        for prm in (4, 8, 208, 216, 300, 104, 108, 112):
             plan = K.DevicePlan(a, K.UnsymKernel.u2_nnz, prm)
             y = np.full(n, np.nan)
             plan.apply(x, y)
             assert_close(y, yref, absax, (n, prm))
+            ys[prm] = y
+        assert np.array_equal(ys[8], ys[208]) and np.array_equal(ys[8], ys[300]), n
+
+
+def test_u1_warp_sliced_bitwise_reference(K):
+    """U1 param 100 (thread per row over the SELL-32 copy) sums every row
+    left to right with unfused multiply-add, exactly like the reference's U1
+    worker and spmv_ref: y is bitwise equal to the oracle on random, skewed
+    and empty-row matrices, config 1 and config 5 at full size, and on row
+    sub-ranges. A layout whose padding would more than triple the matrix is
+    refused."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    mats = []
+    for t in range(8):
+        n = int(rng.integers(1, 3000))
+        mats.append(matgen.random_csr(n, float(rng.choice([0.001, 0.01, 0.05])), rng,
+                                      skew=False, empty_frac=0.3 * (t % 3 == 2)))
+    for n, rp, ci, v in mats:
+        x = rng.uniform(-1, 1, n)
+        a = K.CsrMatrix(n, rp, ci, v)
+        plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
+        assert plan.param == 100
+        y = np.full(n, np.nan)
+        plan.apply(x, y)
+        assert np.array_equal(y, O.spmv_ref(n, rp, ci, v, x)), n
+    for a, seed in ((K.stencil7(64, 64, 64), 1),
+                    (K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7), 5)):
+        rp, ci, v = a.to_host()
+        x = O.seeded_vector(a.n, seed)
+        yref = O.spmv_ref(a.n, rp, ci, v, x)
+        plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
+        plan.apply(xd, yd)
+        torch.cuda.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), yref)
+        yd.fill_(float("nan"))
+        r0, r1 = 4133, a.n - 77  # unaligned to the 32-row slices
+        plan.apply_rows(r0, r1, xd, yd)
+        torch.cuda.synchronize()
+        got = yd.cpu().numpy()
+        assert np.array_equal(got[r0:r1], yref[r0:r1])
+        assert np.isnan(got[:r0]).all() and np.isnan(got[r1:]).all()
+    # one 6000-long row among singletons: padding 32x the matrix -> refused
+    n = 6000
+    rows = [np.arange(0, n, dtype=np.int64)] + [np.array([i], np.int64) for i in range(1, n)]
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    a = K.CsrMatrix(n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1])))
+    with pytest.raises(Exception):
+        K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
