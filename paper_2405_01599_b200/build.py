@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        obj = os.path.join(LIBDIR, os.path.basename(LIB) + "." + src.replace(".cu", ".o"))
         extra = os.environ.get("KTB_EXTRA_FLAGS", "").split()
         cmd = [nvcc(), *ARCH, "-O3", *extra, "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",

@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -105,6 +106,173 @@ __global__ void __launch_bounds__(kGThreads) k_mgs(const double* __restrict__ V,
     }
 }
 
+// ---- MGS with w resident on chip --------------------------------------------
+// The same projections, update arithmetic and breakdown test as k_mgs, but
+// w never goes back to HBM inside the step: one CTA of kRThreads per SM owns
+// a contiguous slice of E * kRThreads elements, w's slice lives in registers
+// (E per thread) and the slice of the next column in shared memory. Per
+// column q the pass is: w_i -= h_q * V_q,i (V_q from shared memory, loaded by
+// the previous pass), load V_{q+1} (the only HBM traffic: one basis column
+// per projection) into the same shared slot, accumulate <V_{q+1}, w>. The grid
+// reduction is fixed-order and computed identically by every CTA (one warp
+// reads the per-CTA partials in order + a fixed shuffle tree), so every CTA
+// sees the same h_q bit for bit.
+constexpr int kRThreads = 1024;
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[2 * w] = a;
+        red[2 * w + 1] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // fixed order: warp sums in a shuffle tree
+        a = red[2 * l];
+        b = red[2 * l + 1];
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+    }
+}
+
+// every CTA: identical fixed-order total of nb partials (stride 2: pairs)
+__device__ __forceinline__ void grid_total2(const double* part, int nb, double* bc) {
+    if (threadIdx.x < 32) {
+        // all loads in flight at once (nb <= 32 * kMaxPart), then the fixed-order sum
+        constexpr int kMaxPart = 8;
+        double2 pv[kMaxPart];
+#pragma unroll
+        for (int m = 0; m < kMaxPart; ++m) {
+            const int k = threadIdx.x + 32 * m;
+            pv[m] = k < nb ? __ldcg(reinterpret_cast<const double2*>(part) + k) : make_double2(0.0, 0.0);
+        }
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxPart; ++m) {
+            a += pv[m].x;
+            b += pv[m].y;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (threadIdx.x == 0) {
+            bc[0] = a;
+            bc[1] = b;
+        }
+    }
+    __syncthreads();
+}
+
+template <int E>
+__global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restrict__ V, int64_t n,
+                                                          int k, const double* __restrict__ w,
+                                                          double* __restrict__ vnext,
+                                                          double* __restrict__ h,
+                                                          double* __restrict__ partials,
+                                                          int* __restrict__ breakdown) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double s_v[];  // E * kRThreads: this CTA's slice of the current column
+    __shared__ double red[2 * kRThreads / 32];
+    __shared__ double bc[2];
+    const int nb = gridDim.x, tid = threadIdx.x;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * E * kRThreads + tid;
+    double wr[E];
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
+        wr[e] = i < n ? w[i] : 0.0;
+        const double v = i < n ? V[i] : 0.0;
+        s_v[e * kRThreads + tid] = v;
+        a += wr[e] * wr[e];
+        b += v * wr[e];
+    }
+    block_sum2(a, b, red);
+    if (tid == 0) {
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+    }
+    grid.sync();
+    grid_total2(partials, nb, bc);
+    const double in2 = bc[0];
+    double c = bc[1];
+    int slot = 1;  // partial buffers alternate between passes
+    // V_{q+1} is loaded one pass ahead: its HBM latency overlaps the grid
+    // reduction of the previous projection
+    double vn[E];
+    auto load_col = [&](int col) {
+        const double* Vc = V + static_cast<int64_t>(col) * n;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
+            vn[e] = i < n ? __ldcg(Vc + i) : 0.0;
+        }
+    };
+    // and pulled into L2 two passes ahead (one bulk prefetch of this CTA's slice)
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * E * kRThreads;
+    const int64_t s1 = min(n, s0 + static_cast<int64_t>(E) * kRThreads);
+    auto prefetch_col = [&](int col) {
+        const uint32_t bytes = static_cast<uint32_t>(((s1 - s0) * 8) & ~int64_t(15));
+        if (tid == 0 && bytes > 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             V + static_cast<int64_t>(col) * n + s0),
+                         "r"(bytes)
+                         : "memory");
+    };
+    if (k > 1) load_col(1);
+    if (k > 2) prefetch_col(2);
+    if (k > 3) prefetch_col(3);
+    for (int q = 0; q < k; ++q) {
+        if (blockIdx.x == 0 && tid == 0) h[q] = c;
+        const bool last = q + 1 == k;
+        const double mc = -c;
+        double p = 0.0, dummy = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double wi = __dadd_rn(wr[e], __dmul_rn(mc, s_v[e * kRThreads + tid]));
+            wr[e] = wi;
+            if (last) {
+                p += wi * wi;
+            } else {
+                s_v[e * kRThreads + tid] = vn[e];
+                p += vn[e] * wi;
+            }
+        }
+        if (q + 2 < k) load_col(q + 2);
+        if (q + 4 < k) prefetch_col(q + 4);
+        block_sum2(p, dummy, red);
+        double* part = partials + slot * 2 * nb;
+        if (tid == 0) {
+            part[2 * blockIdx.x] = p;
+            part[2 * blockIdx.x + 1] = 0.0;
+        }
+        grid.sync();
+        grid_total2(part, nb, bc);
+        c = bc[0];
+        slot ^= 1;
+    }
+    const double nrm = sqrt(c);
+    const bool brk = nrm <= 1e-14 * sqrt(in2);
+    if (blockIdx.x == 0 && tid == 0) {
+        h[k] = nrm;
+        *breakdown = brk ? 1 : 0;
+    }
+    if (!brk) {
+        const double inv = 1.0 / nrm;  // scal(1.0 / r.norm, v)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
+            if (i < n) vnext[i] = __dmul_rn(wr[e], inv);
+        }
+    }
+}
+
 __global__ void k_sub_from(const double* __restrict__ b, double* __restrict__ r, int64_t n) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < n) r[i] = __dsub_rn(b[i], r[i]);
@@ -170,6 +338,37 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs, kGThreads, 0));
         require(per_sm >= 1, "gmres: cooperative MGS kernel does not fit");
         const int nb = sms * std::min(per_sm, 2);
+        // resident-w MGS: one CTA per SM holds E * kRThreads elements
+        const int64_t per_cta = ceil_div64(n, static_cast<int64_t>(sms) * kRThreads);
+        int E = 0;
+        for (int e : {1, 2, 4, 8, 12, 14, 16})
+            if (e >= per_cta) {
+                E = e;
+                break;
+            }
+        const void* res_fn = nullptr;
+        switch (E) {
+            case 1: res_fn = reinterpret_cast<const void*>(&k_mgs_res<1>); break;
+            case 2: res_fn = reinterpret_cast<const void*>(&k_mgs_res<2>); break;
+            case 4: res_fn = reinterpret_cast<const void*>(&k_mgs_res<4>); break;
+            case 8: res_fn = reinterpret_cast<const void*>(&k_mgs_res<8>); break;
+            case 12: res_fn = reinterpret_cast<const void*>(&k_mgs_res<12>); break;
+            case 14: res_fn = reinterpret_cast<const void*>(&k_mgs_res<14>); break;
+            case 16: res_fn = reinterpret_cast<const void*>(&k_mgs_res<16>); break;
+            default: break;
+        }
+        const size_t res_smem = static_cast<size_t>(E) * kRThreads * 8;
+        int res_nb = 0;
+        if (res_fn && !std::getenv("KTB_GMRES_STREAM_MGS")) {
+            KTB_CUDA(cudaFuncSetAttribute(res_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(res_smem)));
+            int occ = 0;
+            KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, res_fn, kRThreads,
+                                                                   res_smem));
+            // E * kRThreads * grid must cover n with one CTA per SM
+            if (occ >= 1) res_nb = static_cast<int>(ceil_div64(n, static_cast<int64_t>(E) * kRThreads));
+            if (res_nb > sms) res_nb = 0;
+        }
         if (P) {
             int64_t pn = 0;
             ilu0_info(P, &pn, nullptr, nullptr, nullptr);
@@ -177,7 +376,7 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         }
         DBuf<double> b(n), x(n), r(n), w(n), V(static_cast<size_t>(n) * (m + 1));
         DBuf<double> zp(P ? n : 1);
-        DBuf<double> partials(4 * nb), dh(m + 2), dy(m + 1);
+        DBuf<double> partials(4 * std::max(nb, sms)), dh(m + 2), dy(m + 1);
         DBuf<int> dbreak(1);
         KTB_CUDA(cudaMemcpyAsync(b.p, b_host, 8 * n, cudaMemcpyHostToDevice, st));
         KTB_CUDA(cudaMemsetAsync(x.p, 0, 8 * n, st));
@@ -261,8 +460,12 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
                 int* bp = dbreak.p;
                 int64_t nn = n;
                 void* args[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &pp, &bp};
-                KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_mgs),
-                                                     dim3(nb), dim3(kGThreads), args, 0, st));
+                if (res_nb > 0)
+                    KTB_CUDA(cudaLaunchCooperativeKernel(res_fn, dim3(res_nb), dim3(kRThreads),
+                                                         args, res_smem, st));
+                else
+                    KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_mgs),
+                                                         dim3(nb), dim3(kGThreads), args, 0, st));
                 int brk = 0;
                 KTB_CUDA(cudaMemcpyAsync(h.data(), dh.p, 8 * (j + 2), cudaMemcpyDeviceToHost, st));
                 KTB_CUDA(cudaMemcpyAsync(&brk, dbreak.p, 4, cudaMemcpyDeviceToHost, st));

@@ -277,10 +277,12 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                 cr[ST][1] = cp.y;
                 cr[ST][2] = cp.z;
                 cr[ST][3] = cp.w;
-            } else {
+            } else if constexpr (kRPT == 4) {
                 const uint2 cp = reinterpret_cast<const uint2*>(sb + kRows * 8)[tid];
                 cr[ST][0] = cp.x;
                 cr[ST][1] = cp.y;
+            } else {  // kRPT == 2
+                cr[ST][0] = reinterpret_cast<const uint32_t*>(sb + kRows * 8)[tid];
             }
 #pragma unroll
             for (int k2 = 0; k2 < kRPT / 2; ++k2) {
