@@ -119,7 +119,52 @@ __global__ void __launch_bounds__(kGThreads) k_mgs(const double* __restrict__ V,
 // sees the same h_q bit for bit.
 constexpr int kRThreads = 1024;
 
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+// Cross-CTA exchange without a grid barrier: CTA b publishes its partial of
+// reduction r as one 16-byte (value, tag) store into slot[r * nb + b], the
+// tag being unique to this launch and reduction; warp 0 of every CTA polls
+// the nb slots until each carries the expected tag (16-byte stores and loads
+// of one aligned pair are seen whole, the property CUB's decoupled look-back
+// relies on), then sums them in a fixed order + a fixed shuffle tree, so
+// every CTA obtains the same total bit for bit. One L2 round trip after the
+// last CTA's store replaces barrier + re-read.
+constexpr int kMaxPart = 8;  // nb <= 256
+
+__device__ __forceinline__ void publish(double2* slot, double v, long long tag) {
+    __stcg(slot, make_double2(v, __longlong_as_double(tag)));
+}
+
+// warp 0 only; returns the total in every lane of warp 0
+__device__ __forceinline__ double poll_total(const double2* slot, int nb, long long tag) {
+    const int lane = threadIdx.x & 31;
+    double acc[kMaxPart];
+    unsigned pending = 0;
+#pragma unroll
+    for (int m = 0; m < kMaxPart; ++m) {
+        acc[m] = 0.0;
+        if (lane + 32 * m < nb) pending |= 1u << m;
+    }
+    while (pending) {
+#pragma unroll
+        for (int m = 0; m < kMaxPart; ++m) {
+            if ((pending >> m) & 1u) {
+                const double2 v = __ldcv(slot + lane + 32 * m);
+                if (__double_as_longlong(v.y) == tag) {
+                    acc[m] = v.x;
+                    pending &= ~(1u << m);
+                }
+            }
+        }
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int m = 0; m < kMaxPart; ++m) t += acc[m];
+    __syncwarp();
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
+// block sum of a (and b) into warp 0 (every lane of warp 0 holds the sums)
+__device__ __forceinline__ void block_sum_w0(double& a, double& b, double* red) {
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         b += __shfl_xor_sync(0xffffffffu, b, o);
@@ -130,53 +175,26 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
         red[2 * w + 1] = b;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // fixed order: warp sums in a shuffle tree
-        a = red[2 * l];
-        b = red[2 * l + 1];
-        for (int o = 16; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-    }
-}
-
-// every CTA: identical fixed-order total of nb partials (stride 2: pairs)
-__device__ __forceinline__ void grid_total2(const double* part, int nb, double* bc) {
     if (threadIdx.x < 32) {
-        // all loads in flight at once (nb <= 32 * kMaxPart), then the fixed-order sum
-        constexpr int kMaxPart = 8;
-        double2 pv[kMaxPart];
-#pragma unroll
-        for (int m = 0; m < kMaxPart; ++m) {
-            const int k = threadIdx.x + 32 * m;
-            pv[m] = k < nb ? __ldcg(reinterpret_cast<const double2*>(part) + k) : make_double2(0.0, 0.0);
-        }
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int m = 0; m < kMaxPart; ++m) {
-            a += pv[m].x;
-            b += pv[m].y;
-        }
+        a = l < blockDim.x / 32 ? red[2 * l] : 0.0;
+        b = l < blockDim.x / 32 ? red[2 * l + 1] : 0.0;
         for (int o = 16; o > 0; o >>= 1) {
             a += __shfl_xor_sync(0xffffffffu, a, o);
             b += __shfl_xor_sync(0xffffffffu, b, o);
         }
-        if (threadIdx.x == 0) {
-            bc[0] = a;
-            bc[1] = b;
-        }
     }
-    __syncthreads();
 }
 
+// slots: (k + 2) * nb pairs; tag0: unique per launch (the host advances it
+// by 64 each launch), tags tag0 + r for reductions r = 0..k+1
 template <int E>
 __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restrict__ V, int64_t n,
                                                           int k, const double* __restrict__ w,
                                                           double* __restrict__ vnext,
                                                           double* __restrict__ h,
-                                                          double* __restrict__ partials,
-                                                          int* __restrict__ breakdown) {
-    cg::grid_group grid = cg::this_grid();
+                                                          double2* __restrict__ slots,
+                                                          int* __restrict__ breakdown,
+                                                          long long tag0) {
     extern __shared__ double s_v[];  // E * kRThreads: this CTA's slice of the current column
     __shared__ double red[2 * kRThreads / 32];
     __shared__ double bc[2];
@@ -193,18 +211,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
         a += wr[e] * wr[e];
         b += v * wr[e];
     }
-    block_sum2(a, b, red);
-    if (tid == 0) {
-        partials[2 * blockIdx.x] = a;
-        partials[2 * blockIdx.x + 1] = b;
-    }
-    grid.sync();
-    grid_total2(partials, nb, bc);
-    const double in2 = bc[0];
-    double c = bc[1];
-    int slot = 1;  // partial buffers alternate between passes
-    // V_{q+1} is loaded one pass ahead: its HBM latency overlaps the grid
-    // reduction of the previous projection
+    // V_{q+1} is loaded one pass ahead (its latency overlaps the exchange of
+    // the previous projection) and pulled into L2 two passes ahead
     double vn[E];
     auto load_col = [&](int col) {
         const double* Vc = V + static_cast<int64_t>(col) * n;
@@ -214,7 +222,6 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
             vn[e] = i < n ? __ldcg(Vc + i) : 0.0;
         }
     };
-    // and pulled into L2 two passes ahead (one bulk prefetch of this CTA's slice)
     const int64_t s0 = static_cast<int64_t>(blockIdx.x) * E * kRThreads;
     const int64_t s1 = min(n, s0 + static_cast<int64_t>(E) * kRThreads);
     auto prefetch_col = [&](int col) {
@@ -228,6 +235,22 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
     if (k > 1) load_col(1);
     if (k > 2) prefetch_col(2);
     if (k > 3) prefetch_col(3);
+    block_sum_w0(a, b, red);
+    if (tid == 0) {
+        publish(slots + blockIdx.x, a, tag0);
+        publish(slots + nb + blockIdx.x, b, tag0 + 1);
+    }
+    if (tid < 32) {
+        const double t0 = poll_total(slots, nb, tag0);
+        const double t1 = poll_total(slots + nb, nb, tag0 + 1);
+        if (tid == 0) {
+            bc[0] = t0;
+            bc[1] = t1;
+        }
+    }
+    __syncthreads();
+    const double in2 = bc[0];
+    double c = bc[1];
     for (int q = 0; q < k; ++q) {
         if (blockIdx.x == 0 && tid == 0) h[q] = c;
         const bool last = q + 1 == k;
@@ -246,16 +269,15 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
         }
         if (q + 2 < k) load_col(q + 2);
         if (q + 4 < k) prefetch_col(q + 4);
-        block_sum2(p, dummy, red);
-        double* part = partials + slot * 2 * nb;
-        if (tid == 0) {
-            part[2 * blockIdx.x] = p;
-            part[2 * blockIdx.x + 1] = 0.0;
+        block_sum_w0(p, dummy, red);
+        double2* sl = slots + static_cast<int64_t>(q + 2) * nb;
+        if (tid == 0) publish(sl + blockIdx.x, p, tag0 + q + 2);
+        if (tid < 32) {
+            const double t = poll_total(sl, nb, tag0 + q + 2);
+            if (tid == 0) bc[0] = t;
         }
-        grid.sync();
-        grid_total2(part, nb, bc);
+        __syncthreads();
         c = bc[0];
-        slot ^= 1;
     }
     const double nrm = sqrt(c);
     const bool brk = nrm <= 1e-14 * sqrt(in2);
@@ -376,7 +398,11 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         }
         DBuf<double> b(n), x(n), r(n), w(n), V(static_cast<size_t>(n) * (m + 1));
         DBuf<double> zp(P ? n : 1);
-        DBuf<double> partials(4 * std::max(nb, sms)), dh(m + 2), dy(m + 1);
+        DBuf<double> partials(4 * nb), dh(m + 2), dy(m + 1);
+        // k_mgs_res exchange slots: (m + 2) reductions x CTAs, tags never repeat
+        DBuf<double2> slots(static_cast<size_t>(m + 3) * std::max(res_nb, 1));
+        KTB_CUDA(cudaMemsetAsync(slots.p, 0, slots.bytes(), st));
+        long long tag = 64;
         DBuf<int> dbreak(1);
         KTB_CUDA(cudaMemcpyAsync(b.p, b_host, 8 * n, cudaMemcpyHostToDevice, st));
         KTB_CUDA(cudaMemsetAsync(x.p, 0, 8 * n, st));
@@ -460,10 +486,14 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
                 int* bp = dbreak.p;
                 int64_t nn = n;
                 void* args[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &pp, &bp};
-                if (res_nb > 0)
+                double2* sp = slots.p;
+                void* rargs[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &sp, &bp, &tag};
+                if (res_nb > 0) {
+                    // cooperative launch: all CTAs co-resident (they poll each other)
                     KTB_CUDA(cudaLaunchCooperativeKernel(res_fn, dim3(res_nb), dim3(kRThreads),
-                                                         args, res_smem, st));
-                else
+                                                         rargs, res_smem, st));
+                    tag += 64;
+                } else
                     KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_mgs),
                                                          dim3(nb), dim3(kGThreads), args, 0, st));
                 int brk = 0;
