@@ -187,6 +187,13 @@ __device__ __forceinline__ void block_sum_w0(double& a, double& b, double* red) 
 
 // slots: (k + 2) * nb pairs; tag0: unique per launch (the host advances it
 // by 64 each launch), tags tag0 + r for reductions r = 0..k+1
+// issue point pinned (volatile asm is not moved across the exchange below)
+__device__ __forceinline__ double ld_cg_pinned(const double* p) {
+    double r;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+
 template <int E>
 __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restrict__ V, int64_t n,
                                                           int k, const double* __restrict__ w,
@@ -195,31 +202,35 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
                                                           double2* __restrict__ slots,
                                                           int* __restrict__ breakdown,
                                                           long long tag0) {
-    extern __shared__ double s_v[];  // E * kRThreads: this CTA's slice of the current column
+    // this CTA's slices: w and the current column (E * kRThreads each)
+    extern __shared__ double smem_d[];
+    double* s_w = smem_d;
+    double* s_v = smem_d + E * kRThreads;
     __shared__ double red[2 * kRThreads / 32];
     __shared__ double bc[2];
     const int nb = gridDim.x, tid = threadIdx.x;
     const int64_t base = static_cast<int64_t>(blockIdx.x) * E * kRThreads + tid;
-    double wr[E];
     double a = 0.0, b = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
-        wr[e] = i < n ? w[i] : 0.0;
+        const double wi = i < n ? w[i] : 0.0;
         const double v = i < n ? V[i] : 0.0;
+        s_w[e * kRThreads + tid] = wi;
         s_v[e * kRThreads + tid] = v;
-        a += wr[e] * wr[e];
-        b += v * wr[e];
+        a += wi * wi;
+        b += v * wi;
     }
-    // V_{q+1} is loaded one pass ahead (its latency overlaps the exchange of
-    // the previous projection) and pulled into L2 two passes ahead
+    // V_{q+1} is loaded one pass ahead into registers (its latency overlaps
+    // the exchange of the previous projection) and pulled into L2 two passes
+    // ahead
     double vn[E];
     auto load_col = [&](int col) {
         const double* Vc = V + static_cast<int64_t>(col) * n;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
-            vn[e] = i < n ? __ldcg(Vc + i) : 0.0;
+            vn[e] = i < n ? ld_cg_pinned(Vc + i) : 0.0;
         }
     };
     const int64_t s0 = static_cast<int64_t>(blockIdx.x) * E * kRThreads;
@@ -258,12 +269,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
         double p = 0.0, dummy = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const double wi = __dadd_rn(wr[e], __dmul_rn(mc, s_v[e * kRThreads + tid]));
-            wr[e] = wi;
+            const int o = e * kRThreads + tid;
+            const double wi = __dadd_rn(s_w[o], __dmul_rn(mc, s_v[o]));  // axpy(-c, q, v)
+            s_w[o] = wi;
             if (last) {
                 p += wi * wi;
             } else {
-                s_v[e * kRThreads + tid] = vn[e];
+                s_v[o] = vn[e];
                 p += vn[e] * wi;
             }
         }
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
-            if (i < n) vnext[i] = __dmul_rn(wr[e], inv);
+            if (i < n) vnext[i] = __dmul_rn(s_w[e * kRThreads + tid], inv);
         }
     }
 }
@@ -379,7 +391,7 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
             case 16: res_fn = reinterpret_cast<const void*>(&k_mgs_res<16>); break;
             default: break;
         }
-        const size_t res_smem = static_cast<size_t>(E) * kRThreads * 8;
+        const size_t res_smem = static_cast<size_t>(E) * kRThreads * 16;  // w and V slices
         int res_nb = 0;
         if (res_fn && !std::getenv("KTB_GMRES_STREAM_MGS")) {
             KTB_CUDA(cudaFuncSetAttribute(res_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,12 +410,11 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         }
         DBuf<double> b(n), x(n), r(n), w(n), V(static_cast<size_t>(n) * (m + 1));
         DBuf<double> zp(P ? n : 1);
-        DBuf<double> partials(4 * nb), dh(m + 2), dy(m + 1);
+        DBuf<double> partials(4 * nb), dy(m + 1);
         // k_mgs_res exchange slots: (m + 2) reductions x CTAs, tags never repeat
         DBuf<double2> slots(static_cast<size_t>(m + 3) * std::max(res_nb, 1));
         KTB_CUDA(cudaMemsetAsync(slots.p, 0, slots.bytes(), st));
         long long tag = 64;
-        DBuf<int> dbreak(1);
         KTB_CUDA(cudaMemcpyAsync(b.p, b_host, 8 * n, cudaMemcpyHostToDevice, st));
         KTB_CUDA(cudaMemsetAsync(x.p, 0, 8 * n, st));
         const int eb = ceil_div(n, 256);
@@ -444,6 +455,63 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
             KTB_CUDA(cudaStreamSynchronize(st));
             return;
         }
+        // per-step outputs of the pipelined Arnoldi loop (pinned host memory
+        // the MGS kernel writes directly); per-step SpMV and completion events
+        PinnedBuf<double> h_pin(static_cast<size_t>(m + 1) * (m + 2));
+        PinnedBuf<int> brk_pin(m + 1);
+        std::vector<cudaEvent_t> ev_s(m + 1), ev_e(m + 1), ev_step(m + 1);
+        for (int64_t q = 0; q <= m; ++q) {
+            KTB_CUDA(cudaEventCreate(&ev_s[q]));
+            KTB_CUDA(cudaEventCreate(&ev_e[q]));
+            KTB_CUDA(cudaEventCreateWithFlags(&ev_step[q], cudaEventDisableTiming));
+        }
+        struct EvGuard {
+            std::vector<cudaEvent_t>* v[3];
+            ~EvGuard() {
+                for (auto* e : v)
+                    for (auto x : *e) cudaEventDestroy(x);
+            }
+        } ev_guard{{&ev_s, &ev_e, &ev_step}};
+        auto launch_step = [&](int64_t jj) {
+            const double* src = V.p + jj * n;
+            if (P) {  // gmres.hpp:91-92: z = M^{-1} v_j, w = A z
+                ilu0_apply(P, src, zp.p, st);
+                src = zp.p;
+            }
+            KTB_CUDA(cudaEventRecord(ev_s[jj], st));
+            plan_run(A, src, w.p, 0, n);
+            KTB_CUDA(cudaEventRecord(ev_e[jj], st));
+            // orthogonalise against columns 0..jj; V_{jj+1} = w / |w|
+            int kk = static_cast<int>(jj + 1);
+            const double* Vp = V.p;
+            double* wp = w.p;
+            double* vn = V.p + (jj + 1) * n;
+            // projections and the breakdown flag go straight to pinned host
+            // memory (mapped under UVA): no copy nodes between the steps
+            double* hp = h_pin.p + jj * (m + 2);
+            double* pp = partials.p;
+            int* bp = brk_pin.p + jj;
+            int64_t nn = n;
+            if (res_nb > 0) {
+                // cooperative launch: all CTAs co-resident (they poll each other)
+                double2* sp = slots.p;
+                void* rargs[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &sp, &bp, &tag};
+                KTB_CUDA(cudaLaunchCooperativeKernel(res_fn, dim3(res_nb), dim3(kRThreads),
+                                                     rargs, res_smem, st));
+                tag += 64;
+            } else {
+                void* args[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &pp, &bp};
+                KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_mgs),
+                                                     dim3(nb), dim3(kGThreads), args, 0, st));
+            }
+            KTB_CUDA(cudaEventRecord(ev_step[jj], st));
+        };
+        auto account_step = [&](int64_t jj) {  // a step the recurrence takes
+            float ms = 0.f;
+            KTB_CUDA(cudaEventElapsedTime(&ms, ev_s[jj], ev_e[jj]));
+            res->spmv_seconds += ms * 1e-3;
+            res->spmv_calls++;
+        };
         const int64_t r_stride = m + 1;
         std::vector<double> h(m + 2), cs(m + 1), sn(m + 1), gv(m + 2), r_cols(r_stride * m),
             yv(m + 1);
@@ -465,43 +533,28 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
             gv[0] = beta;
             int64_t j = 0;
             bool lucky = false;
+            int64_t launched = -1;
             while (j < m) {
                 if (res->iterations >= max_iters) {
                     stop = true;
                     break;
                 }
-                if (P) {  // gmres.hpp:91-92: z = M^{-1} v_j, w = A z
-                    ilu0_apply(P, V.p + j * n, zp.p, st);
-                    spmv_timed(zp.p, w.p);
-                } else {
-                    spmv_timed(V.p + j * n, w.p);
+                // the device runs one Arnoldi step ahead of the host recurrence:
+                // step j+1 only needs V_{j+1} (written by step j's MGS), so it is
+                // enqueued before step j's projections are read back; a step the
+                // host then does not take (convergence, breakdown, iteration cap)
+                // is discarded (not counted; it only wrote V_{j+2} and w)
+                if (launched < j) launch_step(j);
+                launched = j;
+                if (j + 1 < m) {
+                    launch_step(j + 1);
+                    launched = j + 1;
                 }
-                // orthogonalise against columns 0..j; V_{j+1} = w / |w|
-                int kk = static_cast<int>(j + 1);
-                const double* Vp = V.p;
-                double* wp = w.p;
-                double* vn = V.p + (j + 1) * n;
-                double* hp = dh.p;
-                double* pp = partials.p;
-                int* bp = dbreak.p;
-                int64_t nn = n;
-                void* args[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &pp, &bp};
-                double2* sp = slots.p;
-                void* rargs[] = {&Vp, &nn, &kk, &wp, &vn, &hp, &sp, &bp, &tag};
-                if (res_nb > 0) {
-                    // cooperative launch: all CTAs co-resident (they poll each other)
-                    KTB_CUDA(cudaLaunchCooperativeKernel(res_fn, dim3(res_nb), dim3(kRThreads),
-                                                         rargs, res_smem, st));
-                    tag += 64;
-                } else
-                    KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_mgs),
-                                                         dim3(nb), dim3(kGThreads), args, 0, st));
-                int brk = 0;
-                KTB_CUDA(cudaMemcpyAsync(h.data(), dh.p, 8 * (j + 2), cudaMemcpyDeviceToHost, st));
-                KTB_CUDA(cudaMemcpyAsync(&brk, dbreak.p, 4, cudaMemcpyDeviceToHost, st));
-                KTB_CUDA(cudaStreamSynchronize(st));
-                settle();
-                if (brk) {
+                KTB_CUDA(cudaEventSynchronize(ev_step[j]));
+                account_step(j);
+                const double* hj = h_pin.p + j * (m + 2);
+                for (int64_t q = 0; q <= j + 1; ++q) h[q] = hj[q];
+                if (brk_pin.p[j]) {
                     h[j + 1] = 0.0;
                     lucky = true;
                 }

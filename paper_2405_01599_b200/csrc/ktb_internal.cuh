@@ -71,6 +71,20 @@ struct DBuf {
     size_t bytes() const { return sizeof(T) * n; }
 };
 
+// RAII pinned host buffer (async device->host copies).
+template <typename T>
+struct PinnedBuf {
+    T* p = nullptr;
+    explicit PinnedBuf(size_t count) {
+        if (count) KTB_CUDA(cudaMallocHost(&p, sizeof(T) * count));
+    }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+};
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

@@ -79,7 +79,7 @@ int main() {
     cudaMemset(w, 0, 8 * n);
     const int nb = static_cast<int>((n + E * kRThreads - 1) / (E * kRThreads));
     const size_t smem = E * kRThreads * 8;
-    cudaFuncSetAttribute(k_mgs_res<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_mgs_res<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * smem));
     cudaFuncSetAttribute(k_stream_only<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -91,7 +91,7 @@ int main() {
             int64_t nn = n;
             void* args[] = {&V, &nn, &kk, &w, &vn, &h, &part, &brk, &tag};
             cudaEventRecord(a);
-            cudaLaunchCooperativeKernel((void*)k_mgs_res<E>, nb, kRThreads, args, smem, 0);
+            cudaLaunchCooperativeKernel((void*)k_mgs_res<E>, nb, kRThreads, args, 2 * smem, 0);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             cudaEventElapsedTime(&t[0], a, b);
