@@ -246,6 +246,7 @@ struct ktb_plan {
     ktb::DBuf<int64_t> sell_off;        // slices+1 element offsets (slice width = diff / 32)
     ktb::DBuf<int32_t> sell_col;        // -1 = padding
     ktb::DBuf<double> sell_val;
+    int ell_width = 0;                  // > 0: every slice has this width (offsets implicit)
     // S1/S2 row blocks
     ktb::DBuf<int32_t> blocks;          // P+1 row boundaries
     // S3

@@ -190,10 +190,16 @@ __device__ __forceinline__ int wrap(int s, int W) {
 }
 
 // chunk metadata (one int per round-chunk): bits 0-6 round, bit 7 last round
-// of its sub-tile, bits 8.. sub-tile index local to the block
+// of its sub-tile, bit 8 "no barrier after" (this round and the next target
+// disjoint window slots), bits 9.. sub-tile index local to the block
+#ifndef KTB_S3_PAIRS
+#define KTB_S3_PAIRS 0
+#endif
+constexpr bool kS3Pairs = KTB_S3_PAIRS;
 __device__ __forceinline__ int meta_round(int m) { return m & 127; }
 __device__ __forceinline__ bool meta_last(int m) { return (m >> 7) & 1; }
-__device__ __forceinline__ int meta_sub(int m) { return (m >> 8) & 0x3fffff; }
+__device__ __forceinline__ bool meta_nobar(int m) { return (m >> 8) & 1; }
+__device__ __forceinline__ int meta_sub(int m) { return (m >> 9) & 0x1fffff; }
 // padding chunk (the loop runs a multiple of kStages chunks): no data, no work
 constexpr int kMetaEmpty = 1 << 30;
 __device__ __forceinline__ bool meta_empty(int m) { return m & kMetaEmpty; }
@@ -322,6 +328,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             xin[u] = di[u] = 0.0;
         }
         int wph = 0;  // parity of the stage waited for (flips every kStages chunks)
+        int pend = -1;  // thread 0: chunk whose refill waits for the next barrier
         auto body = [&](int q, auto kc) {
             constexpr int K = decltype(kc)::value;          // stage / slot of chunk q
             constexpr int KG = (K + kGD) % kStages;         // stage / slot of chunk q+kGD
@@ -358,11 +365,26 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #pragma unroll
             for (int u = 0; u < kRPT; ++u)
                 if (sc[u]) win[sl[u]] = wv[u] + vr[K][u] * xi[u];
+            if (meta_nobar(m)) {
+                // next round targets other slots: no barrier; every thread
+                // checks the stage it gathers next itself, and the refill of
+                // stage KG waits for the next barrier
+                if (q + kGD + 1 < Q) mbar_wait(&full[KW], wph ^ (KW <= K ? 1 : 0));
+                if (tid == 0 && q + kGD < Q && q + kGD + kStages < Q) pend = q + kGD + kStages;
+                return;
+            }
             if (tid == 0 && q + kGD + 1 < Q) mbar_wait(&full[KW], wph ^ (KW <= K ? 1 : 0));
             __syncthreads();
-            if (tid == 0 && q + kGD < Q && q + kGD + kStages < Q) {
-                fence_proxy_async_smem();  // stage KG was copied out before the barrier
-                issue(q + kGD + kStages, KG);
+            if (tid == 0) {
+                if (pend >= 0) {  // the refill deferred by the previous round
+                    fence_proxy_async_smem();
+                    issue(pend, (KG + kStages - 1) % kStages);
+                    pend = -1;
+                }
+                if (q + kGD < Q && q + kGD + kStages < Q) {
+                    fence_proxy_async_smem();  // stage KG was copied out before the barrier
+                    issue(q + kGD + kStages, KG);
+                }
             }
             if (meta_last(m)) {  // sub-tile complete: finalise its rows
 #pragma unroll
@@ -536,6 +558,7 @@ void s3_setup(ktb_plan* p) {
     L.reach = static_cast<int>(std::min<int64_t>(reach, W));
 
     std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
+    std::vector<char> sub_nobar;  // per chunk in SELL order: no barrier after it
     std::vector<int64_t> sub_base;
     std::vector<unsigned char> sell;  // chunk-interleaved SELL stream
     int64_t nchunks = 0;
@@ -602,8 +625,44 @@ void s3_setup(ktb_plan* p) {
                     R = std::max(R, r + 1);
                 }
             }
+            // rounds whose window targets are disjoint may run back to back
+            // without a block barrier between them: conflict[r] = rounds
+            // sharing a target slot with round r; execution order = pairs of
+            // disjoint rounds (greedy) then singles, never two elided
+            // barriers in a row, the sub-tile's last chunk always barriered
+            std::vector<uint64_t> conflict(kS3RoundCap, 0);
+            for (int32_t sl : touched) {
+                uint64_t mm = colmask[static_cast<size_t>(sl)];
+                const uint64_t all = mm;
+                while (mm) {
+                    const int r = __builtin_ctzll(mm);
+                    mm &= mm - 1;
+                    conflict[r] |= all;
+                }
+            }
             for (int32_t sl : touched) colmask[static_cast<size_t>(sl)] = 0;
             R = std::max(R, 1);  // every sub-tile is one pipeline item at least
+            std::vector<int> order, pos_of(R, -1);
+            std::vector<char> paired(R, 0), nobar;
+            for (int r = 0; r < R; ++r) {
+                if (pos_of[r] >= 0) continue;
+                int mate = -1;
+                if (kS3Pairs)
+                    for (int t2 = r + 1; t2 < R; ++t2)
+                        if (pos_of[t2] < 0 && !((conflict[r] >> t2) & 1)) {
+                            mate = t2;
+                            break;
+                        }
+                pos_of[r] = static_cast<int>(order.size());
+                order.push_back(r);
+                nobar.push_back(mate >= 0 ? 1 : 0);
+                if (mate >= 0) {
+                    pos_of[mate] = static_cast<int>(order.size());
+                    order.push_back(mate);
+                    nobar.push_back(0);
+                }
+            }
+            sub_nobar.insert(sub_nobar.end(), nobar.begin(), nobar.end());
             const int64_t basei = static_cast<int64_t>(nchunks);  // in chunks
             sub_base.push_back(basei);
             sub_rounds.push_back(R);
@@ -619,7 +678,7 @@ void s3_setup(ktb_plan* p) {
             }
             for (int32_t t = 0; t < rows; ++t)
                 for (auto [r, k] : assign[t]) {
-                    unsigned char* ch = &sell[static_cast<size_t>(basei + r) * kStageBytes];
+                    unsigned char* ch = &sell[static_cast<size_t>(basei + pos_of[r]) * kStageBytes];
                     reinterpret_cast<double*>(ch)[s3_val_pos(t)] = val[k];
                     reinterpret_cast<int16_t*>(ch + kRows * 8)[s3_col_pos(t)] =
                         static_cast<int16_t>(col[k] - a);  // < W <= 32767
@@ -639,8 +698,10 @@ void s3_setup(ktb_plan* p) {
         int q = 0;
         for (int sidx = cta_sub[c]; sidx < cta_sub[c + 1]; ++sidx) {
             const int R = sub_rounds[sidx];
+            const int64_t q0g = sub_base[sidx];
             for (int r = 0; r < R; ++r, ++q)
-                chunk_meta.push_back(((sidx - cta_sub[c]) << 8) | r | (r == R - 1 ? 128 : 0));
+                chunk_meta.push_back(((sidx - cta_sub[c]) << 9) | r | (r == R - 1 ? 128 : 0) |
+                                     (sub_nobar[q0g + r] ? 256 : 0));
         }
         cta_qreal[c] = q;
         const int qp = (q + kStages - 1) / kStages * kStages;

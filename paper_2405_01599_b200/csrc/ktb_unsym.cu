@@ -132,13 +132,20 @@ __global__ void __launch_bounds__(256) k_u1s(const int64_t* __restrict__ soff,
                                              const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
-                                             int32_t row_begin, int32_t row_end) {
+                                             int32_t row_begin, int32_t row_end, int ell) {
     const int lane = threadIdx.x & 31;
     const int64_t s = (row_begin >> 5) + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
     const int64_t row = s * 32 + lane;
     if (s * 32 >= row_end) return;
-    const int64_t o = __ldg(soff + s);
-    const int W = static_cast<int>((__ldg(soff + s + 1) - o) >> 5);
+    int64_t o;
+    int W;
+    if (ell) {  // uniform width: offsets implicit
+        o = s * 32 * ell;
+        W = ell;
+    } else {
+        o = __ldg(soff + s);
+        W = static_cast<int>((__ldg(soff + s + 1) - o) >> 5);
+    }
     const int32_t* sc = scol + o + lane;
     const double* sv = sval + o + lane;
     double sum = 0.0;
@@ -173,6 +180,11 @@ __global__ void k_sell_width(const int32_t* __restrict__ rp, int64_t n, int64_t 
     w32[s] = static_cast<int64_t>(w) * 32;
 }
 
+__global__ void k_fill_i64(int64_t* __restrict__ a, int64_t count, int64_t v) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < count) a[i] = v;
+}
+
 __global__ void k_sell_fill(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                             const double* __restrict__ val, int64_t n,
                             const int64_t* __restrict__ soff, int32_t* __restrict__ scol,
@@ -198,10 +210,27 @@ static void u1_sell_setup(ktb_plan* p) {
     k_sell_width<<<ceil_div(slices + 1, 256), 256, 0, p->stream>>>(m->row_ptr.p, m->n, slices,
                                                                      p->sell_off.p);
     KTB_LAUNCH();
-    size_t tmp = 0;
+    // uniform width (ELL: slice offsets implicit, one dependent load fewer per
+    // warp) when it costs at most 1/16 more than the per-slice widths
+    DBuf<int64_t> stats(2);
+    size_t tmp = 0, tmp2 = 0;
     KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, p->sell_off.p, p->sell_off.p,
                                            slices + 1, p->stream));
-    DBuf<unsigned char> scratch(tmp);
+    KTB_CUDA(cub::DeviceReduce::Max(nullptr, tmp2, p->sell_off.p, stats.p, slices, p->stream));
+    DBuf<unsigned char> scratch(std::max(tmp, tmp2));
+    KTB_CUDA(cub::DeviceReduce::Max(scratch.p, tmp2, p->sell_off.p, stats.p, slices, p->stream));
+    KTB_CUDA(cub::DeviceReduce::Sum(nullptr, tmp2, p->sell_off.p, stats.p + 1, slices, p->stream));
+    if (tmp2 > scratch.n) scratch.alloc(tmp2);
+    KTB_CUDA(cub::DeviceReduce::Sum(scratch.p, tmp2, p->sell_off.p, stats.p + 1, slices, p->stream));
+    int64_t st[2] = {0, 0};
+    KTB_CUDA(cudaMemcpyAsync(st, stats.p, sizeof(st), cudaMemcpyDeviceToHost, p->stream));
+    KTB_CUDA(cudaStreamSynchronize(p->stream));
+    p->ell_width = 0;
+    if (st[0] > 0 && st[0] * slices <= st[1] + st[1] / 16) {
+        p->ell_width = static_cast<int>(st[0] / 32);
+        k_fill_i64<<<ceil_div(slices, 256), 256, 0, p->stream>>>(p->sell_off.p, slices, st[0]);
+        KTB_LAUNCH();
+    }
     KTB_CUDA(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, p->sell_off.p, p->sell_off.p,
                                            slices + 1, p->stream));
     int64_t padded = 0;
@@ -216,7 +245,7 @@ static void u1_sell_setup(ktb_plan* p) {
         m->row_ptr.p, m->col.p, m->val.p, m->n, p->sell_off.p, p->sell_col.p, p->sell_val.p);
     KTB_LAUNCH();
     KTB_CUDA(cudaStreamSynchronize(p->stream));
-    p->extra_bytes = 8 * (slices + 1) + 12 * (padded - m->nnz) - 4 * (m->n + 1);
+    p->extra_bytes = (p->ell_width ? 0 : 8 * (slices + 1)) + 12 * (padded - m->nnz) - 4 * (m->n + 1);
 }
 
 static int pick_lanes(const ktb_matrix* m) {
@@ -247,7 +276,8 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         const int grid = ceil_div((s1 - s0) * 32, 256);
         p->ctas = grid;
         k_u1s<<<grid, 256, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y,
-                                           static_cast<int32_t>(r0), static_cast<int32_t>(r1));
+                                           static_cast<int32_t>(r0), static_cast<int32_t>(r1),
+                                           p->ell_width);
         KTB_LAUNCH();
         return;
     }
