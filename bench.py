@@ -525,7 +525,11 @@ def run_gpu_dist(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                          "kernel": rlabel,
-                         "bytes_per_launch": B_local},
+                         "bytes_per_launch": B_local,
+                         "note": "peak is the measured copy (read + write) bandwidth; a "
+                                 "read-dominated stream can exceed it (frac > 1); the "
+                                 "warp-sliced kernel does not read row_ptr (4 B/row of the "
+                                 "model)"},
             "e2e": {"value": B / (e2e / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
                     "ms_per_step": e2e},
@@ -683,7 +687,9 @@ def run_gmres(args, cfg):
                                         "seconds inside the solve"},
                 "gmres": info,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                             "frac": achieved / peak,
+                             "traffic": traffic_from_profile({"workload": "cfg5:"}),
+                             "peak_source": peak_src,
                              "kernel": "the SpMV applies inside the solve"},
                 "e2e": {"value": value_scale * B * calls / wall / 1e9, "unit": "GB/s",
                         "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,

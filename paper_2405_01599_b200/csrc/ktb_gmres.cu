@@ -550,7 +550,13 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
                     launch_step(j + 1);
                     launched = j + 1;
                 }
-                KTB_CUDA(cudaEventSynchronize(ev_step[j]));
+                // spin on the step's event (a blocking sync lets the OS park the
+                // host thread: measured 2-3x outliers in the solve time)
+                for (;;) {
+                    const cudaError_t q = cudaEventQuery(ev_step[j]);
+                    if (q == cudaSuccess) break;
+                    if (q != cudaErrorNotReady) KTB_CUDA(q);
+                }
                 account_step(j);
                 const double* hj = h_pin.p + j * (m + 2);
                 for (int64_t q = 0; q <= j + 1; ++q) h[q] = hj[q];
