@@ -213,6 +213,9 @@ struct SymWindowLayout {
     int64_t nsegs = 0;
     int reach = 0;             // max(col - row), clipped to the window
     DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it
+    bool coop = false;         // spills merged inside k_s3 (cooperative launch)
+    DBuf<int> flags;           // per CTA: epoch of its last published spill
+    int epoch = 0;
     DBuf<int32_t> long_rows;   // rows handled by the long-row path
     int64_t nlong = 0;
     DBuf<int32_t> far_i, far_j;

@@ -30,6 +30,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdlib>
+
 #include "ktb_internal.cuh"
 #include "ktb_ptx.cuh"
 
@@ -218,7 +220,8 @@ __global__ void __launch_bounds__(kS3Threads, 1)
          const int64_t* __restrict__ cta_base, const double* __restrict__ diag,
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
-         double* __restrict__ spill) {
+         double* __restrict__ spill, int* __restrict__ flags, int epoch,
+         const int32_t* __restrict__ head_end, const int32_t* __restrict__ first_src) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
@@ -419,6 +422,79 @@ __global__ void __launch_bounds__(kS3Threads, 1)
         const uint64_t keep = policy_evict_last();
         for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
             st_hint_f64(spill + so + (j - R1), win[(j - R0) % W], keep);
+    }
+    if (!flags) return;  // k_s3_fixup merges the spills
+    // In-kernel merge (cooperative launch: every block is resident). Publish
+    // this block's spill, wait for the blocks spilling into this one, then
+    // add their spills into the head rows [R0, head_end) -- the arithmetic of
+    // k_s3_fixup (sources ascending, y + (s_a + s_b + ...)), so y is the same
+    // bit for bit; all loads of a pass are in flight together.
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        st_release_gpu(flags + c, epoch);
+    }
+    const int32_t he = head_end[c];
+    if (he <= R0) return;
+    const int fs = first_src[c];
+    if (tid == 0)
+        for (int src = fs; src < c; ++src)
+            if (spill_hi[src] > R0)
+                while (ld_acquire_gpu(flags + src) != epoch) {
+                }
+    __syncthreads();
+    // the first two sources whose spill meets the head rows, inline
+    int sa = -1, sb = -1;
+    for (int src = fs; src < c; ++src)
+        if (spill_hi[src] > R0) {
+            if (sa < 0)
+                sa = src;
+            else if (sb < 0)
+                sb = src;
+        }
+    const int32_t a0 = sa >= 0 ? cta_row[sa + 1] : 0, a1 = sa >= 0 ? spill_hi[sa] : 0;
+    const int32_t b0 = sb >= 0 ? cta_row[sb + 1] : 0, b1 = sb >= 0 ? spill_hi[sb] : 0;
+    const double* spa = sa >= 0 ? spill + spill_off[sa] - a0 : spill;
+    const double* spb = sb >= 0 ? spill + spill_off[sb] - b0 : spill;
+#ifndef KTB_S3_MU
+#define KTB_S3_MU 14
+#endif
+    constexpr int MU = KTB_S3_MU;  // rows per thread per pass
+    for (int32_t j0 = R0; j0 < he; j0 += MU * kS3Threads) {
+        double yv[MU], va[MU], vb[MU];
+        bool tch[MU];
+#pragma unroll
+        for (int u = 0; u < MU; ++u) {
+            const int32_t j = j0 + u * kS3Threads + tid;
+            const bool in = j < he;
+            const bool ia = in && j >= a0 && j < a1;
+            const bool ib = in && j >= b0 && j < b1;
+            yv[u] = in ? __ldcg(y + j) : 0.0;
+            va[u] = ia ? __ldcg(spa + j) : 0.0;
+            vb[u] = ib ? __ldcg(spb + j) : 0.0;
+            tch[u] = ia || ib;
+        }
+        double acc[MU];
+#pragma unroll
+        for (int u = 0; u < MU; ++u) acc[u] = va[u] + vb[u];
+        for (int src = sb + 1; sb >= 0 && src < c; ++src) {  // more sources: rare
+            const int32_t s0 = cta_row[src + 1], shi = spill_hi[src];
+            if (shi <= R0) continue;
+            const double* sp = spill + spill_off[src] - s0;
+#pragma unroll
+            for (int u = 0; u < MU; ++u) {
+                const int32_t j = j0 + u * kS3Threads + tid;
+                if (j < he && j >= s0 && j < shi) {
+                    acc[u] += __ldcg(sp + j);
+                    tch[u] = true;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < MU; ++u) {
+            const int32_t j = j0 + u * kS3Threads + tid;
+            if (tch[u]) y[j] = yv[u] + acc[u];
+        }
     }
 }
 
@@ -799,7 +875,25 @@ void s3_setup(ktb_plan* p) {
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kS3SmemFixed + W * 8)));
     p->ctas = P;
-    p->launches = 1 + (L.nsegs ? 1 : 0) + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
+    // KTB_S3_MERGE=1: merge the spills inside k_s3 (cooperative launch, every
+    // block resident) instead of the PDL-launched k_s3_fixup. Bitwise the
+    // same y; measured slower on config 2 (85.2 vs 82.9 us per apply: the
+    // tail merge is latency-bound while the fixup's blocks fill the SMs as
+    // k_s3's retire), so off by default.
+    {
+        int occ = 0, sms = 0;
+        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, k_s3, kS3Threads, static_cast<size_t>(kS3SmemFixed + W * 8)));
+        KTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
+        const char* env = std::getenv("KTB_S3_MERGE");
+        L.coop = env && env[0] == '1' && static_cast<int64_t>(occ) * sms >= P;
+        if (L.coop) {
+            L.flags.alloc(P);
+            KTB_CUDA(cudaMemsetAsync(L.flags.p, 0, sizeof(int) * P, st));
+            KTB_CUDA(cudaStreamSynchronize(st));
+        }
+    }
+    p->launches = 1 + (L.nsegs && !L.coop ? 1 : 0) + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
     // SELL stream (10 B/slot incl. padding) vs the 12 B/nnz model, + spill
     // write/read + head-row read-modify-write in the fixup; row_ptr unused
@@ -808,13 +902,35 @@ void s3_setup(ktb_plan* p) {
 
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
-    k_s3<<<L.ctas, kS3Threads, kS3SmemFixed + static_cast<size_t>(L.window) * 8,
-           p->stream>>>(L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p,
-                        L.cta_base.p, L.diag.p, x, y, L.window, L.reach,
-                        static_cast<int>(p->m->n),
-                        L.spill_hi.p, L.spill_off.p, L.spill.p);
-    KTB_LAUNCH();
-    if (L.nsegs) {
+    const size_t smem = kS3SmemFixed + static_cast<size_t>(L.window) * 8;
+    if (L.coop) {  // spills merged inside k_s3 (all blocks resident)
+        const int32_t* cta_row = L.cta_row.p;
+        const int32_t* cta_chunk = L.cta_chunk.p;
+        const int32_t* meta = L.chunk_meta.p;
+        const int32_t* qreal = L.cta_qreal.p;
+        const unsigned char* sell = L.sell.p;
+        const int64_t* base = L.cta_base.p;
+        const double* diag = L.diag.p;
+        int W = L.window, reach = L.reach, n = static_cast<int>(p->m->n);
+        const int32_t* shi = L.spill_hi.p;
+        const int64_t* soff = L.spill_off.p;
+        double* spill = L.spill.p;
+        int* flags = L.flags.p;
+        int epoch = ++L.epoch;
+        const int32_t* he = L.head_end.p;
+        const int32_t* fs = L.first_src.p;
+        void* args[] = {&cta_row, &cta_chunk, &meta, &qreal, &sell, &base, &diag, &x, &y, &W,
+                        &reach, &n, &shi, &soff, &spill, &flags, &epoch, &he, &fs};
+        KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_s3), dim3(L.ctas),
+                                             dim3(kS3Threads), args, smem, p->stream));
+    } else {
+        k_s3<<<L.ctas, kS3Threads, smem, p->stream>>>(
+            L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p, L.cta_base.p,
+            L.diag.p, x, y, L.window, L.reach, static_cast<int>(p->m->n), L.spill_hi.p,
+            L.spill_off.p, L.spill.p, nullptr, 0, L.head_end.p, L.first_src.p);
+        KTB_LAUNCH();
+    }
+    if (L.nsegs && !L.coop) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(L.nsegs));
         cfg.blockDim = dim3(256);

@@ -479,3 +479,32 @@ def test_u1_warp_sliced_bitwise_reference(K):
     a = K.CsrMatrix(n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1])))
     with pytest.raises(Exception):
         K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
+
+
+def test_s3_in_kernel_merge_matches_fixup_kernel(K, monkeypatch):
+    """KTB_S3_MERGE=1 merges the spills into the head rows inside k_s3
+    (cooperative launch) with k_s3_fixup's arithmetic: y is bitwise equal to
+    the default two-kernel path, on config 2 and on a small matrix."""
+    import torch
+
+    cases = [(K.stencil27_upper(128, 128, 128), 2)]
+    n, rp, ci, v = matgen.stencil27_upper(40, 37, 30)
+    cases.append((K.SymCsrMatrix(n, rp, ci, v), 5))
+    for a, seed in cases:
+        x = torch.from_numpy(O.seeded_vector(a.n, seed)).cuda()
+        ys = []
+        for env in ("0", "1"):
+            monkeypatch.setenv("KTB_S3_MERGE", env)
+            plan = K.DevicePlan(a, K.SymKernel.s3_nnz_zero_omit)
+            y = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
+            for _ in range(3):  # repeated applies reuse the published-spill flags
+                plan.apply(x, y)
+            torch.cuda.synchronize()
+            ys.append(y.cpu().numpy())
+            plan.close()
+        assert np.array_equal(ys[0], ys[1])
+        if a.n < 100000:
+            erp, eci, ev = O.expand_symmetric(n, rp, ci, v)
+            xh = O.seeded_vector(a.n, seed)
+            assert_close(ys[0], O.spmv_ref(a.n, erp, eci, ev, xh),
+                         absax_of(a.n, erp, eci, ev, xh), "s3 merge")
