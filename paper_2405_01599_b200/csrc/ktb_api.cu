@@ -174,6 +174,8 @@ ktb_matrix::~ktb_matrix() { delete expanded; }
 
 ktb_plan::~ktb_plan() {
     if (own_stream && stream) cudaStreamDestroy(stream);
+    delete long_plan;
+    delete long_m;
 }
 
 using namespace ktb;
@@ -631,7 +633,8 @@ int ktb_spmv(ktb_plan* p, const double* x, double* y, int ptr_kind) {
 
 int ktb_spmv_rows(ktb_plan* p, int64_t row_begin, int64_t row_end, const double* x, double* y) {
     return guarded([&] {
-        require(p->kernel == KTB_U1, "spmv_rows: row sub-ranges need the U1 plan");
+        require(p->kernel == KTB_U1 && p->param != 101,
+                "spmv_rows: row sub-ranges need the U1 plan");
         require(row_begin >= 0 && row_begin <= row_end && row_end <= p->m->n,
                 "spmv_rows: bad row range");
         DeviceGuard g(p->m->device);
@@ -757,6 +760,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
         } else {
             add(KTB_U1, 0, "u1", 0);
             add(KTB_U1, 100, "u1", 0);  // thread per row over the warp-sliced copy
+            add(KTB_U1, 101, "u1", 0);  // the same over rows sorted by length
             add(KTB_U2, 0, "u2", 1);
             std::vector<int64_t> ept = {4, 8, 16};
             if (opts.params && opts.n_params > 0) ept.assign(opts.params, opts.params + opts.n_params);

@@ -250,6 +250,13 @@ struct ktb_plan {
     ktb::DBuf<int32_t> sell_col;        // -1 = padding
     ktb::DBuf<double> sell_val;
     int ell_width = 0;                  // > 0: every slice has this width (offsets implicit)
+    // U1 param 101: rows sorted by length into the slices (slot -> row), rows
+    // longer than the slice cap in a compact sub-matrix run by U2 warp tiles
+    ktb::DBuf<int32_t> sell_perm;
+    ktb::DBuf<int32_t> long_rows;
+    ktb::DBuf<double> long_y;
+    ktb_matrix* long_m = nullptr;
+    ktb_plan* long_plan = nullptr;
     // S1/S2 row blocks
     ktb::DBuf<int32_t> blocks;          // P+1 row boundaries
     // S3

@@ -132,11 +132,13 @@ __global__ void __launch_bounds__(256) k_u1s(const int64_t* __restrict__ soff,
                                              const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
-                                             int32_t row_begin, int32_t row_end, int ell) {
+                                             int32_t row_begin, int32_t row_end, int ell,
+                                             const int32_t* __restrict__ perm) {
     const int lane = threadIdx.x & 31;
     const int64_t s = (row_begin >> 5) + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
-    const int64_t row = s * 32 + lane;
+    int64_t row = s * 32 + lane;
     if (s * 32 >= row_end) return;
+    if (perm) row = __ldg(perm + row);  // sorted slices: slot -> row (-1: padding)
     int64_t o;
     int W;
     if (ell) {  // uniform width: offsets implicit
@@ -164,7 +166,71 @@ __global__ void __launch_bounds__(256) k_u1s(const int64_t* __restrict__ soff,
         for (int u = 0; u < kSellUnroll; ++u)
             if (c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
     }
-    if (row >= row_begin && row < row_end) y[row] = sum;
+    if (perm ? row >= 0 : (row >= row_begin && row < row_end)) y[row] = sum;
+}
+
+// ---- U1 param 101 setup helpers: rows sorted by length ----------------------
+__global__ void k_sort_keys(const int32_t* __restrict__ rp, int64_t n, int32_t cap,
+                            int32_t* __restrict__ key, int32_t* __restrict__ row) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int32_t len = rp[i + 1] - rp[i];
+    key[i] = len <= cap ? len : -1;  // long rows sort last
+    row[i] = static_cast<int32_t>(i);
+}
+
+// slice widths from the sorted keys (slot 32s holds the slice's longest row)
+__global__ void k_sorted_width(const int32_t* __restrict__ key, int64_t ns, int64_t slices,
+                               int64_t* __restrict__ w32) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s > slices) return;
+    w32[s] = s == slices ? 0 : static_cast<int64_t>(key[s * 32]) * 32;
+}
+
+__global__ void k_sorted_fill(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, const int32_t* __restrict__ srow,
+                              int64_t ns, int64_t slices, const int64_t* __restrict__ soff,
+                              int32_t* __restrict__ perm, int32_t* __restrict__ scol,
+                              double* __restrict__ sval) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t s = t >> 5;
+    if (s >= slices) return;
+    const int lane = static_cast<int>(t & 31);
+    const int32_t r = t < ns ? srow[t] : -1;
+    perm[t] = r;
+    const int64_t o = soff[s];
+    const int W = static_cast<int>((soff[s + 1] - o) >> 5);
+    const int32_t b = r >= 0 ? rp[r] : 0, len = r >= 0 ? rp[r + 1] - b : 0;
+    for (int k = 0; k < W; ++k) {
+        const int64_t d = o + static_cast<int64_t>(k) * 32 + lane;
+        scol[d] = k < len ? col[b + k] : -1;
+        sval[d] = k < len ? val[b + k] : 0.0;
+    }
+}
+
+__global__ void k_long_counts(const int32_t* __restrict__ rp, const int32_t* __restrict__ lrow,
+                              int64_t nl, int32_t* __restrict__ lrp) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i <= nl) lrp[i] = i < nl ? rp[lrow[i] + 1] - rp[lrow[i]] : 0;
+}
+
+// one block per long row: copy its entries into the compact sub-matrix
+__global__ void k_long_copy(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, const int32_t* __restrict__ lrow,
+                            const int32_t* __restrict__ lrp, int32_t* __restrict__ lcol,
+                            double* __restrict__ lval) {
+    const int32_t r = lrow[blockIdx.x];
+    const int32_t b = rp[r], len = rp[r + 1] - b, d = lrp[blockIdx.x];
+    for (int32_t k = threadIdx.x; k < len; k += blockDim.x) {
+        lcol[d + k] = col[b + k];
+        lval[d + k] = val[b + k];
+    }
+}
+
+__global__ void k_scatter_rows(const double* __restrict__ src, const int32_t* __restrict__ rows,
+                               int64_t nl, double* __restrict__ y) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < nl) y[rows[i]] = src[i];
 }
 
 __global__ void k_sell_width(const int32_t* __restrict__ rp, int64_t n, int64_t slices,
@@ -248,6 +314,101 @@ static void u1_sell_setup(ktb_plan* p) {
     p->extra_bytes = (p->ell_width ? 0 : 8 * (slices + 1)) + 12 * (padded - m->nnz) - 4 * (m->n + 1);
 }
 
+// U1 param 101: rows of length <= kSortedCap sorted by length (descending,
+// stable) into warp slices -- near-uniform slice widths for any row-length
+// distribution; longer rows go to a compact sub-matrix reduced by U2 warp
+// tiles into long_y and scattered into y. Row sums of the sliced rows keep
+// the reference's left-to-right order; the long rows' carry the tiles' order.
+constexpr int32_t kSortedCap = 256;
+static void u1_sorted_setup(ktb_plan* p) {
+    const ktb_matrix* m = p->m;
+    const int64_t n = m->n;
+    cudaStream_t st = p->stream;
+    DBuf<int32_t> key(n), row(n), skey(n), srow(n);
+    k_sort_keys<<<ceil_div(n, 256), 256, 0, st>>>(m->row_ptr.p, n, kSortedCap, key.p, row.p);
+    KTB_LAUNCH();
+    size_t tmp = 0;
+    KTB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, key.p, skey.p, row.p,
+                                                       srow.p, n, 0, 32, st));
+    DBuf<unsigned char> scratch(tmp);
+    KTB_CUDA(cub::DeviceRadixSort::SortPairsDescending(scratch.p, tmp, key.p, skey.p, row.p,
+                                                       srow.p, n, 0, 32, st));
+    // short rows: the sorted prefix with key >= 0
+    std::vector<int32_t> hkey(n);
+    KTB_CUDA(cudaMemcpyAsync(hkey.data(), skey.p, 4 * n, cudaMemcpyDeviceToHost, st));
+    KTB_CUDA(cudaStreamSynchronize(st));
+    int64_t ns = n;
+    while (ns > 0 && hkey[ns - 1] < 0) --ns;
+    const int64_t nl = n - ns;
+    const int64_t slices = std::max<int64_t>(1, ceil_div64(ns, 32));
+    p->sell_off.alloc(slices + 1);
+    k_sorted_width<<<ceil_div(slices + 1, 256), 256, 0, st>>>(skey.p, ns, slices, p->sell_off.p);
+    KTB_LAUNCH();
+    if (ns == 0) KTB_CUDA(cudaMemsetAsync(p->sell_off.p, 0, 8 * (slices + 1), st));
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, p->sell_off.p, p->sell_off.p,
+                                           slices + 1, st));
+    if (tmp > scratch.n) scratch.alloc(tmp);
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, p->sell_off.p, p->sell_off.p,
+                                           slices + 1, st));
+    int64_t padded = 0;
+    KTB_CUDA(cudaMemcpyAsync(&padded, p->sell_off.p + slices, 8, cudaMemcpyDeviceToHost, st));
+    KTB_CUDA(cudaStreamSynchronize(st));
+    p->sell_col.alloc(std::max<int64_t>(padded, 1));
+    p->sell_val.alloc(std::max<int64_t>(padded, 1));
+    p->sell_perm.alloc(slices * 32);
+    k_sorted_fill<<<ceil_div(slices * 32, 256), 256, 0, st>>>(
+        m->row_ptr.p, m->col.p, m->val.p, srow.p, ns, slices, p->sell_off.p, p->sell_perm.p,
+        p->sell_col.p, p->sell_val.p);
+    KTB_LAUNCH();
+    p->ell_width = 0;
+    int64_t long_nnz = 0;
+    if (nl > 0) {
+        p->long_rows.alloc(nl);
+        KTB_CUDA(cudaMemcpyAsync(p->long_rows.p, srow.p + ns, 4 * nl, cudaMemcpyDeviceToDevice, st));
+        auto* lm = new ktb_matrix();
+        p->long_m = lm;
+        lm->device = m->device;
+        lm->n = nl;
+        lm->ncols = m->ncols;
+        lm->kind = KTB_GENERAL;
+        lm->sm_count = m->sm_count;
+        lm->row_ptr.alloc(nl + 1);
+        k_long_counts<<<ceil_div(nl + 1, 256), 256, 0, st>>>(m->row_ptr.p, p->long_rows.p, nl,
+                                                             lm->row_ptr.p);
+        KTB_LAUNCH();
+        KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, lm->row_ptr.p, lm->row_ptr.p, nl + 1,
+                                               st));
+        if (tmp > scratch.n) scratch.alloc(tmp);
+        KTB_CUDA(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, lm->row_ptr.p, lm->row_ptr.p,
+                                               nl + 1, st));
+        int32_t lnnz = 0;
+        KTB_CUDA(cudaMemcpyAsync(&lnnz, lm->row_ptr.p + nl, 4, cudaMemcpyDeviceToHost, st));
+        KTB_CUDA(cudaStreamSynchronize(st));
+        lm->nnz = long_nnz = lnnz;
+        lm->col.alloc(lnnz);
+        lm->val.alloc(lnnz);
+        k_long_copy<<<static_cast<int>(nl), 256, 0, st>>>(m->row_ptr.p, m->col.p, m->val.p,
+                                                          p->long_rows.p, lm->row_ptr.p, lm->col.p,
+                                                          lm->val.p);
+        KTB_LAUNCH();
+        KTB_CUDA(cudaStreamSynchronize(st));
+        auto* lp = new ktb_plan();
+        p->long_plan = lp;
+        lp->m = lm;
+        lp->kernel = KTB_U2;
+        lp->param = 8;
+        lp->workers = p->workers;
+        lp->stream = st;
+        plan_setup(lp);
+        p->long_y.alloc(nl);
+    }
+    KTB_CUDA(cudaStreamSynchronize(st));
+    // vs the model: padding slots, perm (4 B/slot) instead of row_ptr, the
+    // long rows' tile bookkeeping and their y round trip
+    p->extra_bytes = 12 * (padded + long_nnz - m->nnz) + 4 * (slices * 32) - 4 * (m->n + 1) +
+                     (p->long_plan ? p->long_plan->extra_bytes + 16 * nl : 0);
+}
+
 static int pick_lanes(const ktb_matrix* m) {
     const double mean = m->n ? static_cast<double>(m->nnz) / static_cast<double>(m->n) : 1.0;
     int v = 1;
@@ -261,6 +422,11 @@ void u1_setup(ktb_plan* p) {
         p->launches = 1;
         return;
     }
+    if (p->param == 101) {
+        u1_sorted_setup(p);
+        p->launches = 1 + (p->long_plan ? p->long_plan->launches + 1 : 0);
+        return;
+    }
     if (p->param <= 0) p->param = pick_lanes(p->m);
     int v = 1;
     while (v < p->param && v < 32) v <<= 1;
@@ -271,13 +437,30 @@ void u1_setup(ktb_plan* p) {
 void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
     const int64_t rows = r1 - r0;
     if (rows <= 0) return;
+    if (p->param == 101) {  // whole matrix (spmv_rows refuses 101)
+        if (p->long_plan) {
+            p->long_plan->stream = p->stream;  // the plan's stream may have been re-bound
+            plan_run(p->long_plan, x, p->long_y.p, 0, p->long_plan->m->n);
+            const int64_t nl = p->long_plan->m->n;
+            k_scatter_rows<<<ceil_div(nl, 256), 256, 0, p->stream>>>(p->long_y.p, p->long_rows.p,
+                                                                      nl, y);
+            KTB_LAUNCH();
+        }
+        const int64_t slices = static_cast<int64_t>(p->sell_off.n) - 1;
+        const int grid = ceil_div(slices * 32, 256);
+        p->ctas = grid;
+        k_u1s<<<grid, 256, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y, 0,
+                                           static_cast<int32_t>(slices * 32), 0, p->sell_perm.p);
+        KTB_LAUNCH();
+        return;
+    }
     if (p->param == 100) {
         const int64_t s0 = r0 >> 5, s1 = ceil_div64(r1, 32);
         const int grid = ceil_div((s1 - s0) * 32, 256);
         p->ctas = grid;
         k_u1s<<<grid, 256, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y,
                                            static_cast<int32_t>(r0), static_cast<int32_t>(r1),
-                                           p->ell_width);
+                                           p->ell_width, nullptr);
         KTB_LAUNCH();
         return;
     }

@@ -272,8 +272,9 @@ def test_selector_unsym_and_sym(K):
     assert rep.selected >= 0 and rep.selected_candidate().correct
     assert rep.max_executions() <= 4
     names = [c.name for c in rep.candidates]
-    assert names[:3] == ["u1", "u1", "u2"] and set(names[3:]) == {"u3"}
-    assert rep.candidates[1].jl == 100  # param slot (reference name jl): the warp-sliced U1
+    assert names[:4] == ["u1", "u1", "u1", "u2"] and set(names[4:]) == {"u3"}
+    # param slot (reference name jl): the warp-sliced U1 and its row-sorted form
+    assert rep.candidates[1].jl == 100 and rep.candidates[2].jl == 101
     x = O.seeded_vector(n, 1)
     y = np.empty(n)
     choice.plan.apply(x, y)
@@ -508,3 +509,49 @@ def test_s3_in_kernel_merge_matches_fixup_kernel(K, monkeypatch):
             xh = O.seeded_vector(a.n, seed)
             assert_close(ys[0], O.spmv_ref(a.n, erp, eci, ev, xh),
                          absax_of(a.n, erp, eci, ev, xh), "s3 merge")
+
+
+def test_u1_sorted_slices(K):
+    """U1 param 101: rows of length <= 256 sorted by length into warp slices
+    (bitwise equal to spmv_ref on those rows: same left-to-right unfused sum),
+    longer rows through U2 warp tiles on a compact sub-matrix (tolerance);
+    random, skewed, empty-row and very long-row matrices, config 3 at full
+    size."""
+    import torch
+
+    rng = np.random.default_rng(13)
+    mats = []
+    for t in range(6):
+        n = int(rng.integers(1, 3000))
+        mats.append(matgen.random_csr(n, float(rng.choice([0.001, 0.01, 0.05])), rng,
+                                      skew=bool(t % 2), empty_frac=0.3 * (t % 3 == 2)))
+    n = 6000  # one huge row, singletons, empties, rows just around the cap
+    rows = [np.arange(0, n, dtype=np.int64)] + [np.array([i], np.int64) for i in range(1, 2000)]
+    rows += [np.array([], np.int64)] * 1500
+    rows += [np.sort(rng.choice(n, 256 + (i % 3) - 1, replace=False)).astype(np.int64)
+             for i in range(60)]
+    rows += [np.array([5, 9], np.int64)] * (n - len(rows))
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    mats.append((n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1]))))
+    for n, rp, ci, v in mats:
+        x = rng.uniform(-1, 1, n)
+        a = K.CsrMatrix(n, rp, ci, v)
+        plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 101)
+        y = np.full(n, np.nan)
+        plan.apply(x, y)
+        yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
+        assert_close(y, yref, absax, (n, 101))
+        short = np.diff(rp) <= 256
+        assert np.array_equal(y[short], yref[short]), n
+    a = K.powerlaw()
+    rp, ci, v = a.to_host()
+    x = O.seeded_vector(a.n, 3)
+    yref, absax = O.spmv_ref(a.n, rp, ci, v, x), absax_of(a.n, rp, ci, v, x)
+    plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 101)
+    y = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
+    plan.apply(torch.from_numpy(x).cuda(), y)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy()
+    assert_close(got, yref, absax, "cfg3 101")
+    short = np.diff(rp) <= 256
+    assert np.array_equal(got[short], yref[short])
