@@ -176,6 +176,9 @@ ktb_plan::~ktb_plan() {
     if (own_stream && stream) cudaStreamDestroy(stream);
     delete long_plan;
     delete long_m;
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
 }
 
 using namespace ktb;

@@ -257,6 +257,8 @@ struct ktb_plan {
     ktb::DBuf<double> long_y;
     ktb_matrix* long_m = nullptr;
     ktb_plan* long_plan = nullptr;
+    cudaStream_t side = nullptr;        // the long rows run beside the slices
+    cudaEvent_t fork = nullptr, join = nullptr;
     // S1/S2 row blocks
     ktb::DBuf<int32_t> blocks;          // P+1 row boundaries
     // S3

@@ -401,6 +401,9 @@ static void u1_sorted_setup(ktb_plan* p) {
         lp->stream = st;
         plan_setup(lp);
         p->long_y.alloc(nl);
+        KTB_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        KTB_CUDA(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+        KTB_CUDA(cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming));
     }
     KTB_CUDA(cudaStreamSynchronize(st));
     // vs the model: padding slots, perm (4 B/slot) instead of row_ptr, the
@@ -438,13 +441,19 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
     const int64_t rows = r1 - r0;
     if (rows <= 0) return;
     if (p->param == 101) {  // whole matrix (spmv_rows refuses 101)
+        // the long rows (U2 tiles on the sub-matrix, then a scatter into y) run
+        // on a side stream forked from and joined back to the plan's stream:
+        // they overlap the slice kernel (disjoint rows of y, x read-only)
         if (p->long_plan) {
-            p->long_plan->stream = p->stream;  // the plan's stream may have been re-bound
+            KTB_CUDA(cudaEventRecord(p->fork, p->stream));
+            KTB_CUDA(cudaStreamWaitEvent(p->side, p->fork, 0));
+            p->long_plan->stream = p->side;
             plan_run(p->long_plan, x, p->long_y.p, 0, p->long_plan->m->n);
             const int64_t nl = p->long_plan->m->n;
-            k_scatter_rows<<<ceil_div(nl, 256), 256, 0, p->stream>>>(p->long_y.p, p->long_rows.p,
-                                                                      nl, y);
+            k_scatter_rows<<<ceil_div(nl, 256), 256, 0, p->side>>>(p->long_y.p, p->long_rows.p,
+                                                                    nl, y);
             KTB_LAUNCH();
+            KTB_CUDA(cudaEventRecord(p->join, p->side));
         }
         const int64_t slices = static_cast<int64_t>(p->sell_off.n) - 1;
         const int grid = ceil_div(slices * 32, 256);
@@ -452,6 +461,7 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         k_u1s<<<grid, 256, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y, 0,
                                            static_cast<int32_t>(slices * 32), 0, p->sell_perm.p);
         KTB_LAUNCH();
+        if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
         return;
     }
     if (p->param == 100) {
@@ -493,23 +503,34 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
 }
 
 // =============================================================== carries
-// Tile carries (row, value) in tile order; a run of equal rows is summed in
-// order by the first tile of the run and added once: deterministic.
+// Tile carries (row, value) in tile order; the rows are non-decreasing, so
+// the tiles carrying one row form a run. One warp per tile: a tile that
+// starts a run sums the run 32 carries at a time (lane-strided partial sums,
+// then a fixed shuffle tree: deterministic) and adds it to y once; other
+// tiles exit. A run of L tiles costs L/32 dependent rounds (a 65,536-long
+// row spans 256 tiles: 8), where a serial walk cost L.
 __global__ void k_fixup_carries(const int32_t* __restrict__ crow,
                                 const double* __restrict__ cval, int64_t tiles, int64_t n,
                                 double* __restrict__ y) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (t >= tiles) return;
-    const int32_t r = crow[t];
+    const int32_t r = __ldg(crow + t);
     if (r < 0 || r >= n) return;
-    if (t > 0 && crow[t - 1] == r) return;
-    double s = cval[t];
-    for (int64_t u = t + 1; u < tiles && crow[u] == r; ++u) s += cval[u];
-    y[r] += s;
+    if (t > 0 && __ldg(crow + t - 1) == r) return;  // not the run's first tile
+    double acc = 0.0;
+    for (int64_t u0 = t;; u0 += 32) {
+        const int64_t u = u0 + lane;
+        const bool same = u < tiles && __ldg(crow + u) == r;
+        if (same) acc += __ldg(cval + u);
+        if (__ballot_sync(0xffffffffu, same) != 0xffffffffu) break;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[r] += acc;
 }
 
 static void fixup_run(ktb_plan* p, double* y) {
-    k_fixup_carries<<<ceil_div(p->tiles, 256), 256, 0, p->stream>>>(
+    k_fixup_carries<<<ceil_div(p->tiles * 32, 256), 256, 0, p->stream>>>(
         p->carry_row.p, p->carry_val.p, p->tiles, p->m->n, y);
     KTB_LAUNCH();
 }
