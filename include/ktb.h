@@ -169,6 +169,15 @@ int ktb_plan_set_stream(ktb_plan* p, void* stream);
  * pointers (pinned for full speed); the call copies x in, runs, copies y out
  * and synchronises (the LinOp::apply contract, solver_types.hpp:17-20). */
 int ktb_spmv(ktb_plan* p, const double* x, double* y, int ptr_kind);
+/* y_k = A*x_k for k < count, host vectors x + k*ldx, y + k*ldy (ldx/ldy in
+ * doubles; 0 = the same vector every time, still copied every time): the
+ * LinOp::apply contract of ktb_spmv(KTB_PTR_HOST) applied count times, with
+ * the host->device copy of vector k+1 and the device->host copy of result
+ * k-1 overlapping the SpMV of k (two device buffer pairs, copy-in / compute
+ * / copy-out streams). Host memory should be pinned for the overlap.
+ * Returns after the last result is in y. */
+int ktb_spmv_host_pipelined(ktb_plan* p, int64_t count, const double* x, int64_t ldx,
+                            double* y, int64_t ldy);
 /* Same on a row sub-range [row_begin, row_end) of the plan's matrix (the
  * halo-overlap split of config 4). Only y[row_begin, row_end) is written. */
 int ktb_spmv_rows(ktb_plan* p, int64_t row_begin, int64_t row_end, const double* x, double* y);

@@ -88,6 +88,7 @@ def load() -> C.CDLL:
                            C.POINTER(C.c_int), C.POINTER(I64)], C.c_int),
         "ktb_plan_set_stream": ([VP, VP], C.c_int),
         "ktb_spmv": ([VP, VP, VP, C.c_int], C.c_int),
+        "ktb_spmv_host_pipelined": ([VP, I64, VP, I64, VP, I64], C.c_int),
         "ktb_spmv_rows": ([VP, I64, I64, VP, VP], C.c_int),
         "ktb_select": ([VP, VP, VP, C.POINTER(VP), VP, C.c_int, C.POINTER(C.c_int),
                         C.POINTER(C.c_int)], C.c_int),

@@ -176,6 +176,13 @@ ktb_plan::~ktb_plan() {
     if (own_stream && stream) cudaStreamDestroy(stream);
     delete long_plan;
     delete long_m;
+    for (int b = 0; b < 2; ++b) {
+        if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+        if (ev_comp[b]) cudaEventDestroy(ev_comp[b]);
+        if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+    }
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
     if (fork) cudaEventDestroy(fork);
     if (join) cudaEventDestroy(join);
     if (side) cudaStreamDestroy(side);
@@ -630,6 +637,54 @@ int ktb_spmv(ktb_plan* p, const double* x, double* y, int ptr_kind) {
         KTB_CUDA(cudaMemcpyAsync(p->dx.p, x, 8 * m->ncols, cudaMemcpyHostToDevice, p->stream));
         plan_run(p, p->dx.p, p->dy.p, 0, m->n);
         KTB_CUDA(cudaMemcpyAsync(y, p->dy.p, 8 * m->n, cudaMemcpyDeviceToHost, p->stream));
+        KTB_CUDA(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int ktb_spmv_host_pipelined(ktb_plan* p, int64_t count, const double* x, int64_t ldx,
+                            double* y, int64_t ldy) {
+    return guarded([&] {
+        require(p != nullptr, "spmv: null plan");
+        require(x != nullptr && y != nullptr && count >= 0 && ldx >= 0 && ldy >= 0,
+                "spmv: dimension mismatch");
+        const ktb_matrix* m = p->m;
+        DeviceGuard g(m->device);
+        const int64_t nx = std::max<int64_t>(m->ncols, 1), ny = std::max<int64_t>(m->n, 1);
+        if (p->dx.n < static_cast<size_t>(nx)) p->dx.alloc(nx);
+        if (p->dy.n < static_cast<size_t>(ny)) p->dy.alloc(ny);
+        if (p->dx2.n < static_cast<size_t>(nx)) p->dx2.alloc(nx);
+        if (p->dy2.n < static_cast<size_t>(ny)) p->dy2.alloc(ny);
+        if (!p->cin) {
+            KTB_CUDA(cudaStreamCreateWithFlags(&p->cin, cudaStreamNonBlocking));
+            KTB_CUDA(cudaStreamCreateWithFlags(&p->cout, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b) {
+                KTB_CUDA(cudaEventCreateWithFlags(&p->ev_in[b], cudaEventDisableTiming));
+                KTB_CUDA(cudaEventCreateWithFlags(&p->ev_comp[b], cudaEventDisableTiming));
+                KTB_CUDA(cudaEventCreateWithFlags(&p->ev_out[b], cudaEventDisableTiming));
+            }
+        }
+        double* bx[2] = {p->dx.p, p->dx2.p};
+        double* by[2] = {p->dy.p, p->dy2.p};
+        // both copy streams start after whatever the plan's stream holds
+        KTB_CUDA(cudaEventRecord(p->ev_comp[0], p->stream));
+        KTB_CUDA(cudaStreamWaitEvent(p->cin, p->ev_comp[0], 0));
+        KTB_CUDA(cudaStreamWaitEvent(p->cout, p->ev_comp[0], 0));
+        for (int64_t k = 0; k < count; ++k) {
+            const int b = static_cast<int>(k & 1);
+            if (k >= 2) KTB_CUDA(cudaStreamWaitEvent(p->cin, p->ev_comp[b], 0));  // bx[b] free
+            KTB_CUDA(cudaMemcpyAsync(bx[b], x + k * ldx, 8 * m->ncols, cudaMemcpyHostToDevice,
+                                     p->cin));
+            KTB_CUDA(cudaEventRecord(p->ev_in[b], p->cin));
+            KTB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[b], 0));
+            if (k >= 2) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[b], 0));  // by[b] free
+            plan_run(p, bx[b], by[b], 0, m->n);
+            KTB_CUDA(cudaEventRecord(p->ev_comp[b], p->stream));
+            KTB_CUDA(cudaStreamWaitEvent(p->cout, p->ev_comp[b], 0));
+            KTB_CUDA(cudaMemcpyAsync(y + k * ldy, by[b], 8 * m->n, cudaMemcpyDeviceToHost,
+                                     p->cout));
+            KTB_CUDA(cudaEventRecord(p->ev_out[b], p->cout));
+        }
+        KTB_CUDA(cudaStreamSynchronize(p->cout));
         KTB_CUDA(cudaStreamSynchronize(p->stream));
     });
 }

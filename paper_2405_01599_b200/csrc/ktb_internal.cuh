@@ -265,6 +265,11 @@ struct ktb_plan {
     ktb::SymWindowLayout sw;
     // host staging for KTB_PTR_HOST
     ktb::DBuf<double> dx, dy;
+    // ktb_spmv_host_pipelined: second buffer pair, copy streams, events
+    ktb::DBuf<double> dx2, dy2;
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
+                ev_out[2] = {nullptr, nullptr};
     ~ktb_plan();
 };
 

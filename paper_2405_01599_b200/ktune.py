@@ -533,6 +533,29 @@ class DevicePlan:
                 self.set_stream(s)
                 self._stream = s
 
+    def apply_host_pipelined(self, x, y, count=None) -> None:
+        """y_k = A x_k for host vectors (rows of 2-D float64 arrays, or one
+        1-D vector reused `count` times -- still copied every time): host->
+        device copy of k+1 and device->host copy of k-1 overlap the SpMV of k
+        (ktb_spmv_host_pipelined). Pinned host memory gives the overlap."""
+        x, y = np.asarray(x), np.asarray(y)
+        require(x.dtype == np.float64 and y.dtype == np.float64 and x.flags.c_contiguous
+                and y.flags.c_contiguous, "spmv: dimension mismatch")
+        if x.ndim == 1:
+            require(count is not None and x.shape[0] == self.a.n, "spmv: dimension mismatch")
+            cnt, ldx = int(count), 0
+        else:
+            cnt, ldx = x.shape[0], x.shape[1]
+            require(ldx == self.a.n, "spmv: dimension mismatch")
+        if y.ndim == 1:
+            require(y.shape[0] == self.a.n, "spmv: dimension mismatch")
+            ldy = 0
+        else:
+            require(y.shape[0] == cnt and y.shape[1] == self.a.n, "spmv: dimension mismatch")
+            ldy = y.shape[1]
+        _check(_lib.load().ktb_spmv_host_pipelined(self.h, cnt, x.ctypes.data, ldx,
+                                                   y.ctypes.data, ldy))
+
     def apply_rows(self, r0, r1, x, y) -> None:
         self._follow_torch_stream(x)
         _check(_lib.load().ktb_spmv_rows(self.h, r0, r1, _dptr(x), _dptr(y)))

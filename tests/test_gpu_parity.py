@@ -555,3 +555,24 @@ def test_u1_sorted_slices(K):
     assert_close(got, yref, absax, "cfg3 101")
     short = np.diff(rp) <= 256
     assert np.array_equal(got[short], yref[short])
+
+
+def test_host_pipelined_batch(K):
+    """ktb_spmv_host_pipelined: every vector's result equals the single-call
+    host path (same plan), for distinct inputs (2-D) and a reused input."""
+    import torch
+
+    for a, kern, prm in ((K.stencil7(40, 30, 20), K.UnsymKernel.u1_row, 100),
+                         (K.stencil27_upper(24, 20, 16), K.SymKernel.s3_nnz_zero_omit, 0)):
+        plan = K.DevicePlan(a, kern, prm)
+        rng = np.random.default_rng(5)
+        X = torch.from_numpy(rng.uniform(-1, 1, (7, a.n))).pin_memory()
+        Y = torch.full((7, a.n), float("nan"), dtype=torch.float64).pin_memory()
+        plan.apply_host_pipelined(X.numpy(), Y.numpy())
+        for k in range(7):
+            yk = np.empty(a.n)
+            plan.apply(X.numpy()[k].copy(), yk)
+            assert np.array_equal(Y.numpy()[k], yk), k
+        y1 = np.full(a.n, np.nan)
+        plan.apply_host_pipelined(X.numpy()[3].copy(), y1, count=5)
+        assert np.array_equal(y1, Y.numpy()[3])
