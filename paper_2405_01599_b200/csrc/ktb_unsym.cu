@@ -179,6 +179,20 @@ __global__ void k_sort_keys(const int32_t* __restrict__ rp, int64_t n, int32_t c
     row[i] = static_cast<int32_t>(i);
 }
 
+// keys sorted descending: the number of keys >= 0
+__global__ void k_count_nonneg_sorted(const int32_t* __restrict__ key, int64_t n,
+                                      int64_t* __restrict__ out) {
+    int64_t lo = 0, hi = n;  // first index with key < 0
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (key[mid] >= 0)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    *out = lo;
+}
+
 // slice widths from the sorted keys (slot 32s holds the slice's longest row)
 __global__ void k_sorted_width(const int32_t* __restrict__ key, int64_t ns, int64_t slices,
                                int64_t* __restrict__ w32) {
@@ -333,12 +347,13 @@ static void u1_sorted_setup(ktb_plan* p) {
     DBuf<unsigned char> scratch(tmp);
     KTB_CUDA(cub::DeviceRadixSort::SortPairsDescending(scratch.p, tmp, key.p, skey.p, row.p,
                                                        srow.p, n, 0, 32, st));
-    // short rows: the sorted prefix with key >= 0
-    std::vector<int32_t> hkey(n);
-    KTB_CUDA(cudaMemcpyAsync(hkey.data(), skey.p, 4 * n, cudaMemcpyDeviceToHost, st));
+    // short rows: the sorted prefix with key >= 0 (binary search on the device)
+    DBuf<int64_t> d_ns(1);
+    k_count_nonneg_sorted<<<1, 1, 0, st>>>(skey.p, n, d_ns.p);
+    KTB_LAUNCH();
+    int64_t ns = 0;
+    KTB_CUDA(cudaMemcpyAsync(&ns, d_ns.p, 8, cudaMemcpyDeviceToHost, st));
     KTB_CUDA(cudaStreamSynchronize(st));
-    int64_t ns = n;
-    while (ns > 0 && hkey[ns - 1] < 0) --ns;
     const int64_t nl = n - ns;
     const int64_t slices = std::max<int64_t>(1, ceil_div64(ns, 32));
     p->sell_off.alloc(slices + 1);
