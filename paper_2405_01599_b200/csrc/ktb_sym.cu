@@ -194,6 +194,9 @@ __device__ __forceinline__ int wrap(int s, int W) {
 // chunk metadata (one int per round-chunk): bits 0-6 round, bit 7 last round
 // of its sub-tile, bit 8 "no barrier after" (this round and the next target
 // disjoint window slots), bits 9.. sub-tile index local to the block
+#ifndef KTB_S3_ABL
+#define KTB_S3_ABL 0  // timing ablations (wrong results): 1 no gathers, 2 no window, 4 no barrier
+#endif
 #ifndef KTB_S3_PAIRS
 #define KTB_S3_PAIRS 0
 #endif
@@ -304,7 +307,11 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             for (int u = 0; u < kRPT; ++u) {
                 const int cu = col_of(cr[ST][u >> 1], u);
                 // always a valid address; the padding select happens at use
+#if KTB_S3_ABL & 1
+                xr[ST][u] = 1.0 + cu;  // ablation: no x gathers
+#else
                 xr[ST][u] = __ldg(xa + (live ? max(cu, 0) : 0));
+#endif
             }
         };
         // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1
@@ -363,11 +370,17 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                 sc[u] = cu >= 0;
                 rowsum[u] += sc[u] ? vr[K][u] * xr[K][u] : 0.0;
                 sl[u] = wrap(cu + off, W);
+#if !(KTB_S3_ABL & 2)
                 if (sc[u]) wv[u] = win[sl[u]];
+#endif
             }
+#if !(KTB_S3_ABL & 2)
 #pragma unroll
             for (int u = 0; u < kRPT; ++u)
                 if (sc[u]) win[sl[u]] = wv[u] + vr[K][u] * xi[u];
+#else
+            rowsum[0] += xi[1] * vr[K][2];  // ablation: no window RMW
+#endif
             if (meta_nobar(m)) {
                 // next round targets other slots: no barrier; every thread
                 // checks the stage it gathers next itself, and the refill of
@@ -377,7 +390,11 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                 return;
             }
             if (tid == 0 && q + kGD + 1 < Q) mbar_wait(&full[KW], wph ^ (KW <= K ? 1 : 0));
+#if KTB_S3_ABL & 4
+            if (q + kGD + 1 < Q) mbar_wait(&full[KW], wph ^ (KW <= K ? 1 : 0));  // ablation: no barrier
+#else
             __syncthreads();
+#endif
             if (tid == 0) {
                 if (pend >= 0) {  // the refill deferred by the previous round
                     fence_proxy_async_smem();
