@@ -169,7 +169,10 @@ constexpr int kGD = KTB_S3_GD;  // chunks gathered ahead (copied to registers, x
 constexpr int kStageBytes = kRows * (8 + 2);  // 20480
 constexpr int kS3RoundCap = 64;  // max rounds per sub-tile (colour classes)
 constexpr int kS3SmemFixed = kStages * kStageBytes + kStages * 8 + 128;
-constexpr int kFixRows = 1024;   // rows per fixup block (4 per thread)
+#ifndef KTB_S3_FIXROWS
+#define KTB_S3_FIXROWS 1024
+#endif
+constexpr int kFixRows = KTB_S3_FIXROWS;  // rows per fixup block (kFixRows / 256 per thread)
 
 // host-side positions of sub-tile row t in a round's value / column arrays
 inline int64_t s3_val_pos(int t) {
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 // segment of <= kFixRows head rows of one destination, 4 rows per thread; the
 // segment's source metadata is plan data loaded before griddepcontrol.wait,
 // so after it every y and spill load of the thread goes out at once.
-__global__ void __launch_bounds__(256) k_s3_fixup(const int4* __restrict__ desc,
+__global__ void __launch_bounds__(256, kFixRows <= 1024 ? 1 : 4) k_s3_fixup(const int4* __restrict__ desc,
                                                   const int32_t* __restrict__ seg_src,
                                                   const int32_t* __restrict__ cta_row,
                                                   const int32_t* __restrict__ spill_hi,
