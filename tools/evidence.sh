@@ -22,8 +22,8 @@ ncu --set full --clock-control none --import-source on -k regex:"k_u1s" -c 1 -o 
   python tools/prof_kernels.py --config 5 --kernels u1 --params 100 --reps 1 --time-reps 1 > $O/ncu_u1s5.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_u1s" -c 1 -o $O/u1s_cfg1 \
   python tools/prof_kernels.py --config 1 --kernels u1 --params 100 --reps 1 --time-reps 1 > $O/ncu_u1s1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_u2w" -c 1 -o $O/u2w_cfg3 \
-  python tools/prof_kernels.py --config 3 --kernels u2 --params 8 --reps 1 --time-reps 1 > $O/ncu_u2w3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_u1s" -c 1 -o $O/u1s_cfg3 \
+  python tools/prof_kernels.py --config 3 --kernels u1 --params 101 --reps 1 --time-reps 1 > $O/ncu_u1s3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_mgs_res" --launch-skip 25 -c 1 -o $O/mgs_cfg5 \
   python bench.py --config 5 --steps 1 --warmup 0 --warm-seconds 0 --no-cpu-baseline > $O/ncu_mgs.log 2>&1
 echo done > $O/DONE
