@@ -53,3 +53,33 @@ def test_gmres_max_iters_and_zero_rhs():
     assert not r.converged and r.iterations == 5
     r = _solve(n, rp, ci, v, np.zeros(n))
     assert r.converged and r.iterations == 0 and not r.x.any()
+
+
+def test_gmres_both_mgs_kernels_and_config5(monkeypatch):
+    """The resident-w MGS (default) and the streaming MGS (KTB_GMRES_STREAM_MGS,
+    used when a slice does not fit on chip) against the C restatement, plus
+    config 5 at full size: the reference's 653 iterations +-2, true residual
+    < tol, one SpMV per iteration + one per restart cycle + the final check."""
+    from paper_2405_01599_b200 import ktune as K
+
+    n, rp, ci, v = matgen.stencil7(24, 20, 16, xp=-0.7, xm=-1.3)
+    b = O.spmv_ref(n, rp, ci, v, np.ones(n))
+    xo, ro = O.gmres_mgs(n, rp, ci, v, b)
+    for env in ("", "1"):
+        if env:
+            monkeypatch.setenv("KTB_GMRES_STREAM_MGS", env)
+        r = _solve(n, rp, ci, v, b)
+        assert r.converged and abs(r.iterations - ro["iterations"]) <= 2, env
+        assert r.true_residual < 1e-8
+    monkeypatch.delenv("KTB_GMRES_STREAM_MGS")
+    a = K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7)
+    plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
+    import torch
+
+    ones = torch.ones(a.n, dtype=torch.float64, device="cuda")
+    bd = torch.empty_like(ones)
+    plan.apply(ones, bd)
+    torch.cuda.synchronize()
+    r = K.gmres_m(a, bd.cpu().numpy(), K.KrylovConfig(30, 30, 1e-8, 3000), plan=plan)
+    assert r.converged and abs(r.iterations - 653) <= 2 and r.true_residual < 1e-8
+    assert r.spmv_calls == r.iterations + r.restarts + 2
