@@ -15,7 +15,10 @@
 // with a barrier between them (chains of one-row levels cost a barrier, not
 // a launch). The apply's launch sequence (forward then backward) is captured
 // once in a CUDA graph over internal buffers.
+#include <cub/cub.cuh>
+
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -102,6 +105,134 @@ __global__ void __launch_bounds__(kRunThreads) k_ilu_run(const int32_t* __restri
     }
 }
 
+// ---- the apply as one cluster launch per sweep ----------------------------
+// The triangular sweeps are latency chains (levels x dependent round trips).
+// A level-ordered packed copy of each triangle lets one thread-block cluster
+// walk all levels of a sweep in one launch: the rows of a level are spread
+// over the cluster's threads and a cluster barrier separates levels. Each
+// row's record -- row id, entry count and its first kPre entries (the
+// reference's order) -- sits at fixed-stride slots, so it is one round of
+// independent loads, issued for the next level before the barrier; z is
+// read through L2 (other SMs of the cluster wrote it); the z stores are
+// fenced at cluster scope before those prefetch loads and the barrier
+// arrival itself is relaxed, so the barrier does not wait for the prefetch.
+// A level then costs one round of z gathers + the store fence + the barrier.
+constexpr int kClThreads = 1024;
+constexpr int kPre = 4;
+
+struct Packed {  // one sweep, rows in level order
+    DBuf<int32_t> row, cnt;   // row id, strict-triangle entries of the row
+    DBuf<int32_t> col;        // kPre x count (slot u of record t at u * count + t)
+    DBuf<double> val;
+    DBuf<double> dval;        // the factor's diagonal of the record's row (backward)
+    DBuf<int32_t> xptr, xcol; // entries beyond kPre: CSR over records
+    DBuf<double> xval;
+    DBuf<int32_t> lev;        // levels+1 boundaries into the records
+    int32_t nlev = 0;
+    int64_t count = 0;
+    int cluster = 0;          // CTAs per cluster (0: not used)
+};
+
+template <bool BACK>
+__global__ void __launch_bounds__(kClThreads, 1)
+    k_ilu_sweep_cluster(const int32_t* __restrict__ prow, const int32_t* __restrict__ pcnt,
+                        const int32_t* __restrict__ pcol, const double* __restrict__ pval,
+                        const double* __restrict__ pdiag,
+                        const int32_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
+                        const double* __restrict__ xval, int64_t count,
+                        const int32_t* __restrict__ lev, int32_t nlev,
+                        const double* __restrict__ r, double* z) {
+    const int nthr = kClThreads * static_cast<int>(gridDim.x);  // one cluster = the grid
+    const int g = blockIdx.x * kClThreads + threadIdx.x;
+    struct Rec {
+        int32_t i, m;
+        int32_t c[kPre];
+        double v[kPre], d;
+    };
+    // a row's record: independent loads of setup data only (one round trip;
+    // the fence before each barrier waits for it, so it must stay one trip)
+    auto load = [&](int64_t t, Rec& R) {
+        R.i = __ldg(prow + t);
+        R.m = __ldg(pcnt + t);
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) {
+            R.c[u] = __ldg(pcol + u * count + t);
+            R.v[u] = __ldg(pval + u * count + t);
+        }
+        R.d = BACK ? __ldg(pdiag + t) : 1.0;
+    };
+    auto finish = [&](int64_t t, const Rec& R) {
+        // the reference's order: s = r_i (z_i backward), s -= l_ik z_k in entry
+        // order; the starting value goes out with the gathers (one round trip)
+        double zk[kPre];
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) zk[u] = u < R.m ? __ldcg(z + R.c[u]) : 0.0;
+        double sacc = BACK ? __ldcg(z + R.i) : __ldg(r + R.i);
+#pragma unroll
+        for (int u = 0; u < kPre; ++u)
+            if (u < R.m) sacc = __dsub_rn(sacc, __dmul_rn(R.v[u], zk[u]));
+        if (R.m > kPre)
+            for (int32_t k = __ldg(xptr + t); k < __ldg(xptr + t + 1); ++k)
+                sacc = __dsub_rn(sacc, __dmul_rn(__ldg(xval + k), __ldcg(z + __ldg(xcol + k))));
+        if (BACK) sacc = __ddiv_rn(sacc, R.d);
+        __stcg(z + R.i, sacc);
+    };
+    Rec cur{}, nxt{};
+    int32_t lb = nlev > 0 ? __ldg(lev) : 0, le = nlev > 0 ? __ldg(lev + 1) : 0;
+    if (nlev > 0 && lb + g < le) load(lb + g, cur);
+    for (int32_t l = 0; l < nlev; ++l) {
+        const int32_t nb = l + 1 < nlev ? __ldg(lev + l + 1) : 0;
+        const int32_t ne = l + 1 < nlev ? __ldg(lev + l + 2) : 0;
+        // the next level's first record goes out with this level's gathers;
+        // the records two levels ahead are pulled into L2 (bulk prefetch: no
+        // completion to wait for, so the fence below does not wait for it)
+        if (l + 2 < nlev && threadIdx.x < 11) {
+            const int64_t b2 = __ldg(lev + l + 2), e2 = __ldg(lev + l + 3);
+            const int a = threadIdx.x;  // one array per thread: row, cnt, col x kPre, val x kPre, d
+            const char* base;
+            int es;
+            if (a == 0) {
+                base = reinterpret_cast<const char*>(prow);
+                es = 4;
+            } else if (a == 1) {
+                base = reinterpret_cast<const char*>(pcnt);
+                es = 4;
+            } else if (a < 2 + kPre) {
+                base = reinterpret_cast<const char*>(pcol + (a - 2) * count);
+                es = 4;
+            } else if (a < 2 + 2 * kPre) {
+                base = reinterpret_cast<const char*>(pval + (a - 2 - kPre) * count);
+                es = 8;
+            } else {
+                base = reinterpret_cast<const char*>(pdiag);
+                es = 8;
+            }
+            if (blockIdx.x == static_cast<unsigned>(a) % gridDim.x && (BACK || a != 2 + 2 * kPre)) {
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(base + b2 * es) & ~uintptr_t(15);
+                const uintptr_t hi = (reinterpret_cast<uintptr_t>(base + e2 * es) + 15) & ~uintptr_t(15);
+                if (hi > lo)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
+                                 "r"(static_cast<uint32_t>(hi - lo))
+                                 : "memory");
+            }
+        }
+        if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
+        if (lb + g < le) finish(lb + g, cur);
+        for (int32_t t = lb + g + nthr; t < le; t += nthr) {
+            Rec R;
+            load(t, R);
+            finish(t, R);
+        }
+        // z stores ordered before the barrier (the record loads are not)
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n"
+                     "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        cur = nxt;
+        lb = nb;
+        le = ne;
+    }
+}
+
 struct Schedule {
     std::vector<int32_t> ptr;  // level boundaries into rows
     DBuf<int32_t> rows, dptr;
@@ -152,6 +283,7 @@ struct ktb_ilu {
     ktb::DBuf<int32_t> rp, col, diag;
     ktb::DBuf<double> val;
     ktb::Schedule lower, upper;
+    ktb::Packed plow, pup;  // cluster apply (when the device supports the cluster)
     ktb::DBuf<double> rbuf, zbuf;
     ktb::DBuf<int> err;
     cudaStream_t stream = nullptr;
@@ -181,6 +313,137 @@ void run_schedule(const Schedule& S, const ktb_ilu* f, const double* r, double* 
         }
         KTB_LAUNCH();
     }
+}
+
+// largest cluster (16 non-portable, else 8) the sweep kernel can run as;
+// 0 = use the per-level launches (KTB_ILU_LEVEL_LAUNCHES=1 forces that)
+int cluster_size_for_sweeps(int device) {
+    const char* env = std::getenv("KTB_ILU_LEVEL_LAUNCHES");
+    if (env && env[0] == '1') return 0;
+    int supported = 0;
+    cudaDeviceGetAttribute(&supported, cudaDevAttrClusterLaunch, device);
+    if (!supported) return 0;
+    for (const void* fn : {reinterpret_cast<const void*>(&k_ilu_sweep_cluster<false>),
+                           reinterpret_cast<const void*>(&k_ilu_sweep_cluster<true>)})
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+    for (int cs : {16, 8}) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kClThreads);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, &k_ilu_sweep_cluster<false>, &cfg) ==
+                cudaSuccess &&
+            nclusters >= 1)
+            return cs;
+        cudaGetLastError();
+    }
+    return 0;
+}
+
+__global__ void k_pack_counts(const int32_t* __restrict__ rows, int64_t n,
+                              const int32_t* __restrict__ rp, const int32_t* __restrict__ diag,
+                              bool upper, int32_t* __restrict__ cnt, int32_t* __restrict__ xcnt) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n) return;
+    const int32_t i = rows[t];
+    const int32_t b = upper ? diag[i] + 1 : rp[i], e = upper ? rp[i + 1] : diag[i];
+    cnt[t] = e - b;
+    xcnt[t] = max(0, e - b - kPre);
+}
+
+__global__ void k_pack_fill(const int32_t* __restrict__ rows, int64_t n,
+                            const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const double* __restrict__ val, const int32_t* __restrict__ diag,
+                            bool upper, int32_t* __restrict__ pc, double* __restrict__ pv,
+                            double* __restrict__ pd, const int32_t* __restrict__ xptr,
+                            int32_t* __restrict__ xc, double* __restrict__ xv) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n) return;
+    const int32_t i = rows[t];
+    const int32_t b = upper ? diag[i] + 1 : rp[i], e = upper ? rp[i + 1] : diag[i];
+    for (int u = 0; u < kPre; ++u) {
+        const bool ok = b + u < e;
+        pc[u * n + t] = ok ? col[b + u] : 0;
+        pv[u * n + t] = ok ? val[b + u] : 0.0;
+    }
+    pd[t] = val[diag[i]];
+    for (int32_t k = b + kPre; k < e; ++k) {
+        xc[xptr[t] + k - b - kPre] = col[k];
+        xv[xptr[t] + k - b - kPre] = val[k];
+    }
+}
+
+// rows in schedule (level) order with their strict-triangle entries, values
+// from the factors (lower: unit L below the diagonal; upper: above it); built
+// on the device from the factors in place
+void build_packed(const Schedule& S, const ktb_ilu* f, bool upper, Packed& P, cudaStream_t s) {
+    const int64_t n = f->n;
+    P.nlev = static_cast<int32_t>(S.ptr.size()) - 1;
+    P.count = n;
+    P.row.alloc(std::max<int64_t>(n, 1));
+    P.cnt.alloc(std::max<int64_t>(n, 1));
+    P.xptr.alloc(n + 1);
+    KTB_CUDA(cudaMemcpyAsync(P.row.p, S.rows.p, 4 * n, cudaMemcpyDeviceToDevice, s));
+    k_pack_counts<<<ceil_div(n, 256), 256, 0, s>>>(S.rows.p, n, f->rp.p, f->diag.p, upper,
+                                                   P.cnt.p, P.xptr.p);
+    KTB_LAUNCH();
+    size_t tmp = 0;
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, P.xptr.p, P.xptr.p, n + 1, s));
+    DBuf<unsigned char> scratch(tmp);
+    KTB_CUDA(cudaMemsetAsync(P.xptr.p + n, 0, 4, s));
+    KTB_CUDA(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, P.xptr.p, P.xptr.p, n + 1, s));
+    int32_t nx = 0;
+    KTB_CUDA(cudaMemcpyAsync(&nx, P.xptr.p + n, 4, cudaMemcpyDeviceToHost, s));
+    KTB_CUDA(cudaStreamSynchronize(s));
+    P.col.alloc(static_cast<size_t>(kPre) * std::max<int64_t>(n, 1));
+    P.val.alloc(static_cast<size_t>(kPre) * std::max<int64_t>(n, 1));
+    P.dval.alloc(std::max<int64_t>(n, 1));
+    P.xcol.alloc(std::max(nx, 1));
+    P.xval.alloc(std::max(nx, 1));
+    k_pack_fill<<<ceil_div(n, 256), 256, 0, s>>>(S.rows.p, n, f->rp.p, f->col.p, f->val.p,
+                                                 f->diag.p, upper, P.col.p, P.val.p, P.dval.p,
+                                                 P.xptr.p, P.xcol.p, P.xval.p);
+    KTB_LAUNCH();
+    P.lev.alloc(S.ptr.size());
+    KTB_CUDA(cudaMemcpyAsync(P.lev.p, S.ptr.data(), 4 * S.ptr.size(), cudaMemcpyHostToDevice, s));
+    KTB_CUDA(cudaStreamSynchronize(s));
+}
+
+template <bool BACK>
+void launch_cluster_sweep(const Packed& P, const ktb_ilu* f, const double* r, double* z,
+                          cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(P.cluster);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P.cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KTB_CUDA(cudaLaunchKernelEx(&cfg, k_ilu_sweep_cluster<BACK>,
+                                static_cast<const int32_t*>(P.row.p),
+                                static_cast<const int32_t*>(P.cnt.p),
+                                static_cast<const int32_t*>(P.col.p),
+                                static_cast<const double*>(P.val.p),
+                                static_cast<const double*>(P.dval.p),
+                                static_cast<const int32_t*>(P.xptr.p),
+                                static_cast<const int32_t*>(P.xcol.p),
+                                static_cast<const double*>(P.xval.p), P.count,
+                                static_cast<const int32_t*>(P.lev.p), P.nlev, r, z));
 }
 
 }  // namespace
@@ -254,16 +517,30 @@ ktb_ilu* ilu0_create(const ktb_matrix* m, cudaStream_t user_stream) {
     KTB_CUDA(cudaStreamSynchronize(s));
     if (first_zero != big)
         throw Invalid("ilu0: zero pivot at row " + std::to_string(first_zero));
+    // packed, level-ordered triangles for the cluster sweeps (factor values)
+    const int cs = cluster_size_for_sweeps(m->device);
+    if (cs > 0 && n > 0) {
+        build_packed(f->lower, f.get(), false, f->plow, s);
+        build_packed(f->upper, f.get(), true, f->pup, s);
+        f->plow.cluster = f->pup.cluster = cs;
+    }
     // the apply: forward then backward sweep over rbuf -> zbuf, as one graph
     cudaGraph_t graph;
     KTB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    run_schedule<kForward>(f->lower, f.get(), f->rbuf.p, f->zbuf.p, f->err.p, s);
-    run_schedule<kBackward>(f->upper, f.get(), f->rbuf.p, f->zbuf.p, f->err.p, s);
+    if (f->plow.cluster) {
+        launch_cluster_sweep<false>(f->plow, f.get(), f->rbuf.p, f->zbuf.p, s);
+        launch_cluster_sweep<true>(f->pup, f.get(), f->rbuf.p, f->zbuf.p, s);
+    } else {
+        run_schedule<kForward>(f->lower, f.get(), f->rbuf.p, f->zbuf.p, f->err.p, s);
+        run_schedule<kBackward>(f->upper, f.get(), f->rbuf.p, f->zbuf.p, f->err.p, s);
+    }
     KTB_CUDA(cudaStreamEndCapture(s, &graph));
     const cudaError_t ie = cudaGraphInstantiate(&f->apply_graph, graph, 0);
     cudaGraphDestroy(graph);
     KTB_CUDA(ie);
-    f->launches = static_cast<int64_t>(f->lower.segs.size() + f->upper.segs.size());
+    f->launches = f->plow.cluster ? 2
+                                  : static_cast<int64_t>(f->lower.segs.size() +
+                                                         f->upper.segs.size());
     return f.release();
 }
 
