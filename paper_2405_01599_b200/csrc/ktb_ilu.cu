@@ -183,7 +183,6 @@ __global__ void __launch_bounds__(kClThreads, 1)
     for (int32_t l = 0; l < nlev; ++l) {
         const int32_t nb = l + 1 < nlev ? __ldg(lev + l + 1) : 0;
         const int32_t ne = l + 1 < nlev ? __ldg(lev + l + 2) : 0;
-        // the next level's first record goes out with this level's gathers;
         // the records two levels ahead are pulled into L2 (bulk prefetch: no
         // completion to wait for, so the fence below does not wait for it)
         if (l + 2 < nlev && threadIdx.x < 11) {
@@ -216,15 +215,18 @@ __global__ void __launch_bounds__(kClThreads, 1)
                                  : "memory");
             }
         }
-        if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
         if (lb + g < le) finish(lb + g, cur);
         for (int32_t t = lb + g + nthr; t < le; t += nthr) {
             Rec R;
             load(t, R);
             finish(t, R);
         }
-        // z stores ordered before the barrier (the record loads are not)
+        // z stores ordered before the barrier; the next level's first record
+        // (L2-resident: bulk-prefetched two levels ago) is loaded after the
+        // fence, so the fence does not wait for it, and lands during the
+        // barrier
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
         asm volatile("barrier.cluster.arrive.relaxed.aligned;\n"
                      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
         cur = nxt;
