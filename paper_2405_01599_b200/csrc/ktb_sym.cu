@@ -306,6 +306,15 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                 vr[ST][2 * k2 + 1] = vp.y;
             }
             const double* xa = x + R0 + meta_sub(mm) * kRows;  // x at the chunk's row 0
+            // opaque to the optimiser: the gathers below then form their
+            // addresses as xa + 8*off (one wide multiply-add) instead of
+            // re-associating into 64-bit index arithmetic per gather
+#ifndef KTB_S3_OPAQUE_XA
+#define KTB_S3_OPAQUE_XA 1
+#endif
+#if KTB_S3_OPAQUE_XA
+            asm("mov.b64 %0, %0;" : "+l"(xa));
+#endif
 #pragma unroll
             for (int u = 0; u < kRPT; ++u) {
                 const int cu = col_of(cr[ST][u >> 1], u);
@@ -313,7 +322,9 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #if KTB_S3_ABL & 1
                 xr[ST][u] = 1.0 + cu;  // ablation: no x gathers
 #else
-                xr[ST][u] = __ldg(xa + (live ? max(cu, 0) : 0));
+                // unsigned 32-bit offset from the chunk's base pointer: one
+                // wide multiply-add per address instead of 64-bit index math
+                xr[ST][u] = __ldg(xa + static_cast<uint32_t>(live ? max(cu, 0) : 0));
 #endif
             }
         };
