@@ -352,6 +352,42 @@ __global__ void k_add_z(const double* __restrict__ z, int64_t n, double* __restr
 
 namespace ktb {
 
+struct GmresWork {
+    int64_t n, m;
+    bool prec;
+    int nb, res_nb;
+    DBuf<double> b, x, r, w, V, zp, partials, dy;
+    DBuf<double2> slots;  // k_mgs_res exchange: (m + 2) reductions x CTAs
+    long long tag = 64;
+    PinnedBuf<double> h_pin;
+    PinnedBuf<int> brk_pin;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> ev_s, ev_e, ev_step;
+    GmresWork(int64_t n_, int64_t m_, bool prec_, int nb_, int res_nb_)
+        : n(n_), m(m_), prec(prec_), nb(nb_), res_nb(res_nb_), b(n_), x(n_), r(n_), w(n_),
+          V(static_cast<size_t>(n_) * (m_ + 1)), zp(prec_ ? n_ : 1), partials(4 * nb_),
+          dy(m_ + 1), slots(static_cast<size_t>(m_ + 3) * std::max(res_nb_, 1)),
+          h_pin(static_cast<size_t>(m_ + 1) * (m_ + 2)), brk_pin(m_ + 1), ev_s(m_ + 1),
+          ev_e(m_ + 1), ev_step(m_ + 1) {
+        KTB_CUDA(cudaEventCreate(&ev0));
+        KTB_CUDA(cudaEventCreate(&ev1));
+        for (int64_t q = 0; q <= m_; ++q) {
+            KTB_CUDA(cudaEventCreate(&ev_s[q]));
+            KTB_CUDA(cudaEventCreate(&ev_e[q]));
+            KTB_CUDA(cudaEventCreateWithFlags(&ev_step[q], cudaEventDisableTiming));
+        }
+    }
+    ~GmresWork() {
+        for (auto e : {ev0, ev1})
+            if (e) cudaEventDestroy(e);
+        for (auto* v : {&ev_s, &ev_e, &ev_step})
+            for (auto e : *v)
+                if (e) cudaEventDestroy(e);
+    }
+    GmresWork(const GmresWork&) = delete;
+    GmresWork& operator=(const GmresWork&) = delete;
+};
+
 // Restarted GMRES(m), MGS, x0 = 0 (gmres.hpp:16-173); host b/x spans. P:
 // optional ILU(0) right preconditioner (Precond, solver_types.hpp:22-27).
 void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, int64_t m,
@@ -408,19 +444,33 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
             ilu0_info(P, &pn, nullptr, nullptr, nullptr);
             require(pn == n, "gmres: dimension mismatch");
         }
-        DBuf<double> b(n), x(n), r(n), w(n), V(static_cast<size_t>(n) * (m + 1));
-        DBuf<double> zp(P ? n : 1);
-        DBuf<double> partials(4 * nb), dy(m + 1);
-        // k_mgs_res exchange slots: (m + 2) reductions x CTAs, tags never repeat
-        DBuf<double2> slots(static_cast<size_t>(m + 3) * std::max(res_nb, 1));
-        KTB_CUDA(cudaMemsetAsync(slots.p, 0, slots.bytes(), st));
-        long long tag = 64;
+        // workspace cached on the plan (device vectors, basis, exchange slots,
+        // pinned step outputs, events): repeated solves allocate nothing --
+        // per-solve cudaMalloc/cudaMallocHost of ~0.5 GB showed up as
+        // occasional 0.3-0.5 s outliers in the solve time
+        auto* Wk = static_cast<GmresWork*>(A->gmres_ws.get());
+        if (!Wk || Wk->n != n || Wk->m != m || Wk->prec != (P != nullptr) || Wk->nb != nb ||
+            Wk->res_nb != res_nb) {
+            A->gmres_ws.reset();
+            A->gmres_ws = std::shared_ptr<void>(new GmresWork(n, m, P != nullptr, nb, res_nb),
+                                                [](void* q) { delete static_cast<GmresWork*>(q); });
+            Wk = static_cast<GmresWork*>(A->gmres_ws.get());
+            KTB_CUDA(cudaMemsetAsync(Wk->slots.p, 0, Wk->slots.bytes(), st));
+        }
+        DBuf<double>& b = Wk->b;
+        DBuf<double>& x = Wk->x;
+        DBuf<double>& r = Wk->r;
+        DBuf<double>& w = Wk->w;
+        DBuf<double>& V = Wk->V;
+        DBuf<double>& zp = Wk->zp;
+        DBuf<double>& partials = Wk->partials;
+        DBuf<double>& dy = Wk->dy;
+        DBuf<double2>& slots = Wk->slots;
+        long long& tag = Wk->tag;  // exchange tags never repeat across solves
         KTB_CUDA(cudaMemcpyAsync(b.p, b_host, 8 * n, cudaMemcpyHostToDevice, st));
         KTB_CUDA(cudaMemsetAsync(x.p, 0, 8 * n, st));
         const int eb = ceil_div(n, 256);
-        cudaEvent_t ev0, ev1;
-        KTB_CUDA(cudaEventCreate(&ev0));
-        KTB_CUDA(cudaEventCreate(&ev1));
+        cudaEvent_t ev0 = Wk->ev0, ev1 = Wk->ev1;
         bool pending = false;
         auto settle = [&]() {  // after a stream sync: account the last SpMV
             if (pending) {
@@ -457,21 +507,9 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         }
         // per-step outputs of the pipelined Arnoldi loop (pinned host memory
         // the MGS kernel writes directly); per-step SpMV and completion events
-        PinnedBuf<double> h_pin(static_cast<size_t>(m + 1) * (m + 2));
-        PinnedBuf<int> brk_pin(m + 1);
-        std::vector<cudaEvent_t> ev_s(m + 1), ev_e(m + 1), ev_step(m + 1);
-        for (int64_t q = 0; q <= m; ++q) {
-            KTB_CUDA(cudaEventCreate(&ev_s[q]));
-            KTB_CUDA(cudaEventCreate(&ev_e[q]));
-            KTB_CUDA(cudaEventCreateWithFlags(&ev_step[q], cudaEventDisableTiming));
-        }
-        struct EvGuard {
-            std::vector<cudaEvent_t>* v[3];
-            ~EvGuard() {
-                for (auto* e : v)
-                    for (auto x : *e) cudaEventDestroy(x);
-            }
-        } ev_guard{{&ev_s, &ev_e, &ev_step}};
+        auto& h_pin = Wk->h_pin;
+        auto& brk_pin = Wk->brk_pin;
+        auto &ev_s = Wk->ev_s, &ev_e = Wk->ev_e, &ev_step = Wk->ev_step;
         auto launch_step = [&](int64_t jj) {
             const double* src = V.p + jj * n;
             if (P) {  // gmres.hpp:91-92: z = M^{-1} v_j, w = A z
@@ -627,8 +665,6 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         KTB_CUDA(cudaMemcpyAsync(x_host, x.p, 8 * n, cudaMemcpyDeviceToHost, st));
         KTB_CUDA(cudaStreamSynchronize(st));
         settle();
-        cudaEventDestroy(ev0);
-        cudaEventDestroy(ev1);
         res->seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }

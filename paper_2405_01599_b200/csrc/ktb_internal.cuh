@@ -1,6 +1,8 @@
 // ktb_internal.cuh -- shared internals of libktb (not part of the ABI).
 #pragma once
 
+#include <memory>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -265,6 +267,8 @@ struct ktb_plan {
     ktb::SymWindowLayout sw;
     // host staging for KTB_PTR_HOST
     ktb::DBuf<double> dx, dy;
+    // GMRES workspace reused across solves with this plan (ktb_gmres.cu)
+    std::shared_ptr<void> gmres_ws;
     // ktb_spmv_host_pipelined: second buffer pair, copy streams, events
     ktb::DBuf<double> dx2, dy2;
     cudaStream_t cin = nullptr, cout = nullptr;
