@@ -447,6 +447,8 @@ def test_u1_warp_sliced_bitwise_reference(K):
         n = int(rng.integers(1, 3000))
         mats.append(matgen.random_csr(n, float(rng.choice([0.001, 0.01, 0.05])), rng,
                                       skew=False, empty_frac=0.3 * (t % 3 == 2)))
+    mats.append((4, np.zeros(5, np.int64), np.zeros(0, np.int64), np.zeros(0)))  # all empty
+    mats.append((1, np.array([0, 1], np.int64), np.array([0], np.int64), np.array([2.5])))
     for n, rp, ci, v in mats:
         x = rng.uniform(-1, 1, n)
         a = K.CsrMatrix(n, rp, ci, v)
@@ -533,6 +535,8 @@ def test_u1_sorted_slices(K):
     rows += [np.array([5, 9], np.int64)] * (n - len(rows))
     rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
     mats.append((n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1]))))
+    mats.append((4, np.zeros(5, np.int64), np.zeros(0, np.int64), np.zeros(0)))  # all empty
+    mats.append((1, np.array([0, 1], np.int64), np.array([0], np.int64), np.array([2.5])))
     for n, rp, ci, v in mats:
         x = rng.uniform(-1, 1, n)
         a = K.CsrMatrix(n, rp, ci, v)
