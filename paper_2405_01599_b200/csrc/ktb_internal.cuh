@@ -216,6 +216,7 @@ struct SymWindowLayout {
     int reach = 0;             // max(col - row), clipped to the window
     DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it
     bool coop = false;         // spills merged inside k_s3 (cooperative launch)
+    int fix_grid = 0;          // > 0: persistent fixup with this many blocks
     DBuf<int> flags;           // per CTA: epoch of its last published spill
     int epoch = 0;
     DBuf<int32_t> long_rows;   // rows handled by the long-row path
