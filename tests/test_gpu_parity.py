@@ -486,8 +486,10 @@ def test_u1_warp_sliced_bitwise_reference(K):
 
 def test_s3_in_kernel_merge_matches_fixup_kernel(K, monkeypatch):
     """KTB_S3_MERGE=1 merges the spills into the head rows inside k_s3
-    (cooperative launch) with k_s3_fixup's arithmetic: y is bitwise equal to
-    the default two-kernel path, on config 2 and on a small matrix."""
+    (cooperative launch) and KTB_S3_FIXUP_GRID=1 runs the fixup as a
+    persistent two-deep kernel, both with k_s3_fixup's arithmetic: y is
+    bitwise equal to the default two-kernel path, on config 2 and on a small
+    matrix."""
     import torch
 
     cases = [(K.stencil27_upper(128, 128, 128), 2)]
@@ -496,8 +498,9 @@ def test_s3_in_kernel_merge_matches_fixup_kernel(K, monkeypatch):
     for a, seed in cases:
         x = torch.from_numpy(O.seeded_vector(a.n, seed)).cuda()
         ys = []
-        for env in ("0", "1"):
-            monkeypatch.setenv("KTB_S3_MERGE", env)
+        for merge, grid in (("0", "0"), ("1", "0"), ("0", "1")):
+            monkeypatch.setenv("KTB_S3_MERGE", merge)
+            monkeypatch.setenv("KTB_S3_FIXUP_GRID", grid)
             plan = K.DevicePlan(a, K.SymKernel.s3_nnz_zero_omit)
             y = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
             for _ in range(3):  # repeated applies reuse the published-spill flags
@@ -505,7 +508,7 @@ def test_s3_in_kernel_merge_matches_fixup_kernel(K, monkeypatch):
             torch.cuda.synchronize()
             ys.append(y.cpu().numpy())
             plan.close()
-        assert np.array_equal(ys[0], ys[1])
+        assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
         if a.n < 100000:
             erp, eci, ev = O.expand_symmetric(n, rp, ci, v)
             xh = O.seeded_vector(a.n, seed)
