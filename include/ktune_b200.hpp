@@ -117,6 +117,18 @@ public:
             throw Error("spmv: dimension mismatch");  // spmv.hpp:114-115
         check(ktb_spmv(h_, x.data(), y.data(), KTB_PTR_HOST));
     }
+    // count host vectors back to back (x_k = x[k*n ...], y_k likewise; one
+    // vector reused when x.size() == n): the copies of neighbouring vectors
+    // overlap the SpMV (ktb_spmv_host_pipelined; pinned memory for overlap)
+    void apply_batch(std::span<const double> x, std::span<double> y, index_t count) const {
+        const index_t n = m_->n();
+        const bool x1 = static_cast<index_t>(x.size()) == n;
+        const bool y1 = static_cast<index_t>(y.size()) == n;
+        if (count < 0 || (!x1 && static_cast<index_t>(x.size()) != n * count) ||
+            (!y1 && static_cast<index_t>(y.size()) != n * count))
+            throw Error("spmv: dimension mismatch");
+        check(ktb_spmv_host_pipelined(h_, count, x.data(), x1 ? 0 : n, y.data(), y1 ? 0 : n));
+    }
     // device pointers, asynchronous on the plan's stream
     void apply_device(const double* x, double* y) const {
         check(ktb_spmv(h_, x, y, KTB_PTR_DEVICE));
