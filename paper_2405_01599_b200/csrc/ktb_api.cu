@@ -824,6 +824,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
             if (opts.params && opts.n_params > 0) ept.assign(opts.params, opts.params + opts.n_params);
             for (int64_t e : ept)
                 if (m->nnz >= 4 * e) add(KTB_U3, e, "u3", 2);
+            add(KTB_U3, 1008, "u3", 2);  // warp-level flag-driven BSS tiles
         }
         std::vector<ktb_plan*> plans(list.size(), nullptr);
         cudaEvent_t e0, e1;

@@ -245,6 +245,8 @@ struct ktb_plan {
     ktb::DBuf<uint32_t> flag_bits;      // U3: row_start_flag, 1 bit per nonzero
     ktb::DBuf<int32_t> seg_row;         // U3: q-th nonempty row (+ sentinel n)
     ktb::DBuf<int32_t> tile_q;          // U3: flags before each tile
+    ktb::DBuf<int32_t> zero_rows;       // U3 warp tiles: empty rows + the last nonempty row
+    int64_t nzero = 0;
     ktb::DBuf<double> carry_val;        // per tile carry-out
     ktb::DBuf<int32_t> carry_row;
     int64_t tiles = 0;

@@ -1383,6 +1383,134 @@ __global__ void k_tile_q(const uint32_t* __restrict__ bits, int64_t nnz, int64_t
     if (threadIdx.x == 0) tile_q[t] = static_cast<int32_t>(tot);
 }
 
+// ---- U3, warp-level BSS (param 1008) ---------------------------------------
+// The branchless segmented scan as a flag-driven warp-level scan: a warp owns
+// 256 consecutive nonzeros, lane b the 8 at [z0 + 8b, z0 + 8b + 8) (16-byte
+// vector loads), whose row-start flags are one byte of the reference's
+// row_start_flag bit array (bss.hpp:34-69). Segment ids come from the tile's
+// flag prefix + a warp prefix of the lanes' popcounts; a flag closes the
+// previous segment, whose row is seg_row[q] (the nonempty-row map). The run
+// before a lane's first flag takes the carry of the lanes before it (one
+// flag-aware warp scan, as k_u2w), the run open at the tile end is the tile
+// carry (k_fixup_carries). Empty rows and the last nonempty row (never closed
+// by a flag) are zeroed first by k_zero_rows.
+__global__ void k_tile_pop(const uint32_t* __restrict__ bits, int64_t tiles,
+                           int32_t* __restrict__ pop) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t > tiles) return;
+    int c = 0;
+    if (t < tiles)
+        for (int k = 0; k < 8; ++k) c += __popc(bits[t * 8 + k]);
+    pop[t] = c;
+}
+
+__global__ void k_zero_rows(const int32_t* __restrict__ rows, int64_t cnt, double* __restrict__ y) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < cnt) y[rows[i]] = 0.0;
+}
+
+__global__ void k_empty_list(const int32_t* __restrict__ rp, int64_t n,
+                             const int32_t* __restrict__ ord, int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n && rp[i] == rp[i + 1]) out[i - ord[i]] = static_cast<int32_t>(i);  // ord = nonempty before i
+}
+
+__global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
+                                                 const double* __restrict__ val,
+                                                 const double* __restrict__ x,
+                                                 double* __restrict__ y, int64_t nnz,
+                                                 int64_t tiles,
+                                                 const uint32_t* __restrict__ bits,
+                                                 const int32_t* __restrict__ seg_row,
+                                                 const int32_t* __restrict__ wq,
+                                                 int32_t* __restrict__ carry_row,
+                                                 double* __restrict__ carry_val) {
+    constexpr int IPT = 8, NS = 4;  // NS: segment rows fetched ahead per lane
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (w >= tiles) return;
+    const int64_t z0 = w * 256, k0 = z0 + lane * IPT;
+    int32_t c[IPT];
+    double v[IPT];
+    if (z0 + 256 <= nnz) {
+#pragma unroll
+        for (int q = 0; q < IPT; q += 4) {
+            const int4 c4 = ld_stream_v4i32(col + k0 + q);
+            c[q] = c4.x;
+            c[q + 1] = c4.y;
+            c[q + 2] = c4.z;
+            c[q + 3] = c4.w;
+        }
+#pragma unroll
+        for (int q = 0; q < IPT; q += 2) {
+            const double2 v2 = ld_stream_v2f64(val + k0 + q);
+            v[q] = v2.x;
+            v[q + 1] = v2.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const bool ok = k0 + j < nnz;
+            c[j] = ok ? ld_stream_i32(col + k0 + j) : -1;
+            v[j] = ok ? ld_stream_f64(val + k0 + j) : 0.0;
+        }
+    }
+    // this lane's 8 flags: one byte of the bit array
+    const uint32_t m = (__ldg(bits + (k0 >> 5)) >> ((lane & 3) * 8)) & 0xffu;
+    const int nf = __popc(m);
+    int qx = nf;  // warp exclusive prefix of the flag counts
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int up = __shfl_up_sync(0xffffffffu, qx, d);
+        if (lane >= d) qx += up;
+    }
+    const int qb = __ldg(wq + w) + qx - nf;  // flags before this lane's first element
+    // rows of the segments this lane closes (qb-1 .. qb+nf-2) and the one it
+    // leaves open (qb+nf-1), fetched with the gathers
+    int32_t sr[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        const int q = qb - 1 + i;
+        sr[i] = (i <= nf && q >= 0) ? __ldg(seg_row + q) : 0;
+    }
+    double xv[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) xv[j] = c[j] >= 0 ? ld_x(x + c[j]) : 0.0;
+    double run = 0.0, head = 0.0;
+    bool has = false;
+    int closed = 0;  // segments closed so far in this lane
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if ((m >> j) & 1u) {  // a row starts here: the open segment closes
+            if (has) {
+                const int32_t r = closed < NS ? sr[closed] : __ldg(seg_row + qb - 1 + closed);
+                y[r] = run;
+            } else {
+                head = run;
+            }
+            has = true;
+            ++closed;
+            run = 0.0;
+        }
+        run += __dmul_rn(v[j], xv[j]);
+    }
+    const uint32_t F = __ballot_sync(0xffffffffu, has);
+    double S = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double up = __shfl_up_sync(0xffffffffu, S, d);
+        if (lane >= d && ((F >> (lane - d + 1)) & ((1u << d) - 1u)) == 0u) S += up;
+    }
+    double cin = __shfl_up_sync(0xffffffffu, S, 1);
+    if (lane == 0) cin = 0.0;
+    if (has && qb >= 1) y[sr[0]] = head + cin;
+    if (lane == 31) {
+        const int q = qb + nf - 1;  // the segment open at the tile end
+        carry_row[w] = q >= 0 ? (nf < NS ? sr[nf] : __ldg(seg_row + q)) : -1;
+        carry_val[w] = S;
+    }
+}
+
 // E = nominal nonzeros per lane; actual chunk lengths are floor/ceil of
 // nnz/jl, at most E (jl = ceil(nnz/E)), so the per-lane loop is unrolled to E.
 template <int E, bool BRANCHY>
@@ -1506,11 +1634,13 @@ __global__ void __launch_bounds__(kU3Threads) k_u3(const int32_t* __restrict__ c
 void u3_setup(ktb_plan* p) {
     const ktb_matrix* m = p->m;
     require(m->nnz > 0, "bss plan: empty matrix");
+    const bool warp_tiles = p->param == 1008 && p->kernel == KTB_U3;
     int E = p->param > 0 ? static_cast<int>(p->param) : 8;
+    if (warp_tiles) E = 8;
     if (E != 4 && E != 8 && E != 16) E = 8;
-    p->param = E;
+    p->param = warp_tiles ? 1008 : E;
     p->jl = ceil_div64(m->nnz, E);
-    p->tiles = ceil_div64(p->jl, kU3Threads);
+    p->tiles = warp_tiles ? ceil_div64(m->nnz, 256) : ceil_div64(p->jl, kU3Threads);
     cudaStream_t s = p->stream;
     const int64_t words = ceil_div64(m->nnz, 32) + 1;
     p->flag_bits.alloc(words);
@@ -1535,21 +1665,62 @@ void u3_setup(ktb_plan* p) {
     KTB_LAUNCH();
     const int32_t nrow = static_cast<int32_t>(m->n);
     KTB_CUDA(cudaMemcpyAsync(p->seg_row.p + p->nq, &nrow, 4, cudaMemcpyHostToDevice, s));
-    p->tile_q.alloc(p->tiles);
-    k_tile_q<<<static_cast<int>(p->tiles), 256, 0, s>>>(p->flag_bits.p, m->nnz, p->jl, p->tiles,
-                                                        p->tile_q.p);
-    KTB_LAUNCH();
+    if (warp_tiles) {
+        // flags before each 256-nonzero tile: per-tile popcounts + a scan
+        p->tile_q.alloc(p->tiles + 1);
+        if (ceil_div64(m->nnz, 32) + 1 < p->tiles * 8) {
+            // the bit array covers whole tiles (zero padded)
+            DBuf<uint32_t> nb(p->tiles * 8);
+            KTB_CUDA(cudaMemsetAsync(nb.p, 0, 4 * p->tiles * 8, s));
+            KTB_CUDA(cudaMemcpyAsync(nb.p, p->flag_bits.p, 4 * words, cudaMemcpyDeviceToDevice, s));
+            p->flag_bits = std::move(nb);
+        }
+        k_tile_pop<<<ceil_div(p->tiles + 1, 256), 256, 0, s>>>(p->flag_bits.p, p->tiles,
+                                                              p->tile_q.p);
+        KTB_LAUNCH();
+        size_t t2 = 0;
+        KTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, p->tile_q.p, p->tile_q.p,
+                                               p->tiles + 1, s));
+        DBuf<uint8_t> tb2(t2 ? t2 : 1);
+        KTB_CUDA(cub::DeviceScan::ExclusiveSum(tb2.p, t2, p->tile_q.p, p->tile_q.p, p->tiles + 1,
+                                               s));
+        // rows no flag closes: the empty ones and the last nonempty row
+        p->nzero = m->n - p->nq + 1;
+        p->zero_rows.alloc(p->nzero);
+        k_empty_list<<<ceil_div(m->n, 256), 256, 0, s>>>(m->row_ptr.p, m->n, ord.p,
+                                                         p->zero_rows.p);
+        KTB_LAUNCH();
+        KTB_CUDA(cudaMemcpyAsync(p->zero_rows.p + p->nzero - 1, p->seg_row.p + p->nq - 1, 4,
+                                 cudaMemcpyDeviceToDevice, s));
+        p->ctas = ceil_div64(p->tiles, 8);
+    } else {
+        p->tile_q.alloc(p->tiles);
+        k_tile_q<<<static_cast<int>(p->tiles), 256, 0, s>>>(p->flag_bits.p, m->nnz, p->jl,
+                                                            p->tiles, p->tile_q.p);
+        KTB_LAUNCH();
+    }
     p->carry_row.alloc(p->tiles);
     p->carry_val.alloc(p->tiles);
     KTB_CUDA(cudaStreamSynchronize(s));
-    p->ctas = p->tiles;
-    p->launches = 2;
+    if (!warp_tiles) p->ctas = p->tiles;
+    p->launches = warp_tiles ? 3 : 2;
     // flag bits + nonempty-row map replace row_ptr; tile carries
-    p->extra_bytes = 4 * words + 4 * (p->nq - (m->n + 1)) + p->tiles * (4 + 8) * 2;
+    p->extra_bytes = 4 * words + 4 * (p->nq - (m->n + 1)) + p->tiles * (4 + 8) * 2 +
+                     (warp_tiles ? 12 * p->nzero : 0);
 }
 
 void u3_run(ktb_plan* p, const double* x, double* y) {
     const ktb_matrix* m = p->m;
+    if (p->param == 1008 && p->kernel == KTB_U3) {
+        k_zero_rows<<<ceil_div(p->nzero, 256), 256, 0, p->stream>>>(p->zero_rows.p, p->nzero, y);
+        KTB_LAUNCH();
+        k_u3w<<<static_cast<int>(ceil_div64(p->tiles, 8)), 256, 0, p->stream>>>(
+            m->col.p, m->val.p, x, y, m->nnz, p->tiles, p->flag_bits.p, p->seg_row.p,
+            p->tile_q.p, p->carry_row.p, p->carry_val.p);
+        KTB_LAUNCH();
+        fixup_run(p, y);
+        return;
+    }
     const int grid = static_cast<int>(p->tiles);
     const bool br = p->kernel == KTB_U4;
 #define KTB_U3_CASE(EE)                                                                        \

@@ -273,6 +273,7 @@ def test_selector_unsym_and_sym(K):
     assert rep.max_executions() <= 4
     names = [c.name for c in rep.candidates]
     assert names[:4] == ["u1", "u1", "u1", "u2"] and set(names[4:]) == {"u3"}
+    assert all(c.correct for c in rep.candidates[3:])  # U2 and every U3 form
     # param slot (reference name jl): the warp-sliced U1 and its row-sorted form
     assert rep.candidates[1].jl == 100 and rep.candidates[2].jl == 101
     x = O.seeded_vector(n, 1)
@@ -583,3 +584,49 @@ def test_host_pipelined_batch(K):
         y1 = np.full(a.n, np.nan)
         plan.apply_host_pipelined(X.numpy()[3].copy(), y1, count=5)
         assert np.array_equal(y1, Y.numpy()[3])
+
+
+def test_u3_warp_bss_tiles(K):
+    """U3 param 1008: the branchless segmented scan as a flag-driven warp-level
+    scan over 256-nonzero tiles (row starts from the reference's flag bits,
+    rows from the nonempty-row map), within tolerance of spmv_ref on random,
+    skewed, empty-row, leading-empty and long-row matrices and config 3, and
+    of the U2 warp tiles (same tiles; a row ending exactly at a tile boundary
+    is closed by the next tile, so its partial sums associate differently)."""
+    import torch
+
+    rng = np.random.default_rng(17)
+    mats = []
+    for t in range(8):
+        n = int(rng.integers(1, 3000))
+        mats.append(matgen.random_csr(n, float(rng.choice([0.001, 0.01, 0.05])), rng,
+                                      skew=bool(t % 2), empty_frac=0.3 * (t % 3 == 2)))
+    n = 6000  # one huge row, singletons, a run of empties, trailing empties
+    rows = [np.arange(0, n, dtype=np.int64)] + [np.array([i], np.int64) for i in range(1, 3000)]
+    rows += [np.array([], np.int64)] * 1500 + [np.array([5, 9], np.int64)] * 1000
+    rows += [np.array([], np.int64)] * (n - len(rows))
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    mats.append((n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1]))))
+    rows = [np.array([], np.int64)] * 50 + [np.array([3], np.int64)]  # leading empties
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    mats.append((51, rp, np.concatenate(rows), np.array([1.5])))
+    for n, rp, ci, v in mats:
+        if rp[-1] == 0:
+            continue
+        x = rng.uniform(-1, 1, n)
+        a = K.CsrMatrix(n, rp, ci, v)
+        y3, y2 = np.full(n, np.nan), np.full(n, np.nan)
+        K.DevicePlan(a, K.UnsymKernel.u3_bss, 1008).apply(x, y3)
+        K.DevicePlan(a, K.UnsymKernel.u2_nnz, 8).apply(x, y2)
+        absax = absax_of(n, rp, ci, v, x)
+        assert_close(y3, O.spmv_ref(n, rp, ci, v, x), absax, (n, "u3w"))
+        assert_close(y3, y2, absax, (n, "u3w vs u2"))
+    a = K.powerlaw()
+    rp, ci, v = a.to_host()
+    x = O.seeded_vector(a.n, 3)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
+    K.DevicePlan(a, K.UnsymKernel.u3_bss, 1008).apply(xd, y)
+    torch.cuda.synchronize()
+    assert_close(y.cpu().numpy(), O.spmv_ref(a.n, rp, ci, v, x), absax_of(a.n, rp, ci, v, x),
+                 "cfg3 u3w")
