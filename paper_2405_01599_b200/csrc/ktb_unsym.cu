@@ -1455,8 +1455,15 @@ __global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
             v[j] = ok ? ld_stream_f64(val + k0 + j) : 0.0;
         }
     }
+    // flags and the tile prefix go out with the column/value loads; the x
+    // gathers are issued before the flag scan waits on them
+    const uint32_t fw = __ldg(bits + (k0 >> 5));
+    const int wq0 = __ldg(wq + w);
+    double xv[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) xv[j] = c[j] >= 0 ? ld_x(x + c[j]) : 0.0;
     // this lane's 8 flags: one byte of the bit array
-    const uint32_t m = (__ldg(bits + (k0 >> 5)) >> ((lane & 3) * 8)) & 0xffu;
+    const uint32_t m = (fw >> ((lane & 3) * 8)) & 0xffu;
     const int nf = __popc(m);
     int qx = nf;  // warp exclusive prefix of the flag counts
 #pragma unroll
@@ -1464,7 +1471,7 @@ __global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
         const int up = __shfl_up_sync(0xffffffffu, qx, d);
         if (lane >= d) qx += up;
     }
-    const int qb = __ldg(wq + w) + qx - nf;  // flags before this lane's first element
+    const int qb = wq0 + qx - nf;  // flags before this lane's first element
     // rows of the segments this lane closes (qb-1 .. qb+nf-2) and the one it
     // leaves open (qb+nf-1), fetched with the gathers
     int32_t sr[NS];
@@ -1473,9 +1480,6 @@ __global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
         const int q = qb - 1 + i;
         sr[i] = (i <= nf && q >= 0) ? __ldg(seg_row + q) : 0;
     }
-    double xv[IPT];
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) xv[j] = c[j] >= 0 ? ld_x(x + c[j]) : 0.0;
     double run = 0.0, head = 0.0;
     bool has = false;
     int closed = 0;  // segments closed so far in this lane
