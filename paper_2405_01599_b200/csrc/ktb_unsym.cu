@@ -1455,23 +1455,30 @@ __global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
             v[j] = ok ? ld_stream_f64(val + k0 + j) : 0.0;
         }
     }
-    // flags and the tile prefix go out with the column/value loads; the x
-    // gathers are issued before the flag scan waits on them
-    const uint32_t fw = __ldg(bits + (k0 >> 5));
+    // the tile's 8 flag words (one sector; every lane reads all of them, so
+    // the lane's prefix is local popcounts instead of a shuffle scan) and the
+    // tile prefix go out with the column/value loads; the x gathers are issued
+    // before anything waits on them
+    const uint4 fa = __ldg(reinterpret_cast<const uint4*>(bits + (z0 >> 5)));
+    const uint4 fb = __ldg(reinterpret_cast<const uint4*>(bits + (z0 >> 5)) + 1);
     const int wq0 = __ldg(wq + w);
     double xv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) xv[j] = c[j] >= 0 ? ld_x(x + c[j]) : 0.0;
-    // this lane's 8 flags: one byte of the bit array
-    const uint32_t m = (fw >> ((lane & 3) * 8)) & 0xffu;
-    const int nf = __popc(m);
-    int qx = nf;  // warp exclusive prefix of the flag counts
+    // this lane's 8 flags: byte (lane & 3) of word lane >> 2
+    const uint32_t fw8[8] = {fa.x, fa.y, fa.z, fa.w, fb.x, fb.y, fb.z, fb.w};
+    const int wi = lane >> 2, sh = (lane & 3) * 8;
+    uint32_t fw = 0;
+    int before = 0;  // flags of the tile before this lane's first element
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int up = __shfl_up_sync(0xffffffffu, qx, d);
-        if (lane >= d) qx += up;
+    for (int k = 0; k < 8; ++k) {
+        if (k < wi) before += __popc(fw8[k]);
+        if (k == wi) fw = fw8[k];
     }
-    const int qb = wq0 + qx - nf;  // flags before this lane's first element
+    before += __popc(fw & ((1u << sh) - 1u));
+    const uint32_t m = (fw >> sh) & 0xffu;
+    const int nf = __popc(m);
+    const int qb = wq0 + before;  // flags before this lane's first element
     // rows of the segments this lane closes (qb-1 .. qb+nf-2) and the one it
     // leaves open (qb+nf-1), fetched with the gathers
     int32_t sr[NS];
