@@ -119,6 +119,9 @@ __global__ void __launch_bounds__(kRunThreads) k_ilu_run(const int32_t* __restri
 // A level then costs one round of z gathers + the store fence + the barrier.
 constexpr int kClThreads = 1024;
 constexpr int kPre = 4;
+#ifndef KTB_ILU_SPLIT_BARRIER
+#define KTB_ILU_SPLIT_BARRIER 1
+#endif
 
 struct Packed {  // one sweep, rows in level order
     DBuf<int32_t> row, cnt;   // row id, strict-triangle entries of the row
@@ -151,15 +154,31 @@ __global__ void __launch_bounds__(kClThreads, 1)
     };
     // a row's record: independent loads of setup data only (one round trip;
     // the fence before each barrier waits for it, so it must stay one trip)
+    // records stream through once per apply: evict-first, so they do not
+    // push z (re-read every level) out of L2
+    uint64_t ef;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(ef));
+    auto ldi = [&](const int32_t* p) {
+        int32_t v;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+            : "=r"(v) : "l"(p), "l"(ef));
+        return v;
+    };
+    auto ldd = [&](const double* p) {
+        double v;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+            : "=d"(v) : "l"(p), "l"(ef));
+        return v;
+    };
     auto load = [&](int64_t t, Rec& R) {
-        R.i = __ldg(prow + t);
-        R.m = __ldg(pcnt + t);
+        R.i = ldi(prow + t);
+        R.m = ldi(pcnt + t);
 #pragma unroll
         for (int u = 0; u < kPre; ++u) {
-            R.c[u] = __ldg(pcol + u * count + t);
-            R.v[u] = __ldg(pval + u * count + t);
+            R.c[u] = ldi(pcol + u * count + t);
+            R.v[u] = ldd(pval + u * count + t);
         }
-        R.d = BACK ? __ldg(pdiag + t) : 1.0;
+        R.d = BACK ? ldd(pdiag + t) : 1.0;
     };
     auto finish = [&](int64_t t, const Rec& R) {
         // the reference's order: s = r_i (z_i backward), s -= l_ik z_k in entry
@@ -225,10 +244,18 @@ __global__ void __launch_bounds__(kClThreads, 1)
         // (L2-resident: bulk-prefetched two levels ago) is loaded after the
         // fence, so the fence does not wait for it, and lands during the
         // barrier
+#if KTB_ILU_SPLIT_BARRIER
+        // split-phase: the arrive releases this level's z stores, the next
+        // record's loads go out between arrive and wait
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#else
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
         if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
         asm volatile("barrier.cluster.arrive.relaxed.aligned;\n"
                      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
         cur = nxt;
         lb = nb;
         le = ne;
