@@ -147,10 +147,17 @@ int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
 /* -------------------------------------------------------------- plans */
 /* An execution plan: kernel + its device-side decomposition + stream.
  * Replaces the (UnsymChoice|SymChoice) value (autotune.hpp:168-183).
- *   param:   U1: lanes per row V in {0=auto,1,2,4,...,32};
- *            U2: merge items per thread (0 = auto);
- *            U3/U4: nonzeros per segment lane (0 = auto);
- *            S1/S2: lanes per row (0 = auto); S3: rows per sub-tile (0 = auto).
+ *   param:   U1: lanes per row V in {0=auto,1,2,4,...,32}; 100 = one thread
+ *                per row over a warp-sliced (SELL-32/ELL) copy, bitwise equal
+ *                to spmv_ref; 101 = the same over rows sorted by length (rows
+ *                > 256 through U2 tiles on a side stream);
+ *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8); 208/216 =
+ *                the same with 16-byte vector loads; 300 = TMA-fed tiles;
+ *                104/108/112 = merge-path tiles;
+ *            U3/U4: nonzeros per segment lane E in {4,8,16} (0 = 8); U3 1008
+ *                = flag-driven warp-level BSS over 256-nonzero tiles;
+ *            S1/S2: lanes per row (0 = auto); S3: 0 (2048-row sub-tiles).
+ *            The selector (ktb_select) sweeps these; see INTEGRATION.md.
  *   workers: the reference worker count P whose partition/regions the plan
  *            also materialises as artefacts (0 = engine default).
  *   stream:  cudaStream_t to run on (NULL = the plan creates its own). */
