@@ -128,7 +128,11 @@ __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
 // at once. The plan builds the copy on the device (k_sell_*); it is refused
 // when padding would more than triple the matrix (power-law rows).
 constexpr int kSellUnroll = 8;
-__global__ void __launch_bounds__(256) k_u1s(const int64_t* __restrict__ soff,
+#ifndef KTB_U1S_MINB
+#define KTB_U1S_MINB 1  // 7 (config 1's 8192 slices in one wave) caps registers at 32 and
+                        // spills: slower on configs 1, 4 and 5
+#endif
+__global__ void __launch_bounds__(256, KTB_U1S_MINB) k_u1s(const int64_t* __restrict__ soff,
                                              const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
