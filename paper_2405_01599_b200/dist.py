@@ -199,6 +199,12 @@ class DistSpMV:
         self._run(self.boundary)
         return self.y
 
+    def exchange_only(self):
+        """The halo exchange of one apply alone (for timing it): the two
+        one-plane messages, waited on by the current stream."""
+        for r in halo_exchange(self.L, self.x):
+            r.wait()
+
     def compute_local(self):
         """The local rows only (halos assumed in place): interior + boundary."""
         self._run(self.parts)
@@ -435,6 +441,12 @@ class DistCsrSpMV:
             q.wait()
         self.ghost_spmv(y)
         return y
+
+    def exchange_only(self, x_owned):
+        """Pack + ghost exchange of one apply alone (for timing it)."""
+        self.pack(x_owned)
+        for q in self.exchange():
+            q.wait()
 
     def launches_per_apply(self) -> int:
         return int(self.dc.send_counts.sum() > 0) + self.plan.launches + int(self.dc.ghost_rows > 0)
