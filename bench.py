@@ -562,7 +562,10 @@ def run_gpu_dist(args, cfg):
             "exchange_def": "the step's x-halo / ghost exchange alone (NCCL P2P, max over "
                             "ranks); inside the step it overlaps the interior rows",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak,
+                         "traffic": traffic_from_profile(cfg) if ws == 1 and args.config == 4
+                         else None,
+                         "peak_source": peak_src,
                          "kernel": rlabel,
                          "bytes_per_launch": B_local,
                          "note": "peak is the measured copy (read + write) bandwidth; a "
