@@ -22,6 +22,11 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# the reference's OpenMP pool (CPU baseline / reference arm): one thread per
+# physical core, bound close
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
 import subprocess
 import sys
 import threading
@@ -230,7 +235,7 @@ def run_reference(args, cfg):
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} applies of {cfg['sample']} ({cfg['workload']}) through "
                                    f"the reference's tuned engine ({eng.selected['name']}, "
-                                   f"{eng.selected['workers']} OpenMP workers)"},
+                                   f"{eng.selected['workers']} OpenMP workers)", **REF_BUILD},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -776,6 +781,12 @@ def traffic_from_profile(cfg):
         return None
 
 
+REF_BUILD = {"build": "unmodified reference headers via oracle/Makefile: g++ -O2 -std=c++20 "
+                      "-fopenmp -ffp-contract=off (no -march=native)",
+             "binding": "OMP_PROC_BIND=%s OMP_PLACES=%s" % (os.environ.get("OMP_PROC_BIND"),
+                                                          os.environ.get("OMP_PLACES"))}
+
+
 def cpu_baseline(cfg):
     try:
         eng, n, nnz, x, cores = cpu_reference_engine(cfg)
@@ -785,7 +796,7 @@ def cpu_baseline(cfg):
                 "sample": f"{reps} applies ({reps * t:.1f} s) of {cfg['sample']} ({cfg['workload']}) "
                           f"through the reference's tuned engine ({eng.selected['name']}, "
                           f"{eng.selected['workers']} OpenMP workers)",
-                "ms_per_apply": t * 1e3}
+                "ms_per_apply": t * 1e3, **REF_BUILD}
     except Exception as e:  # report, never fail the GPU line
         return {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                 "sample": f"unavailable: {e}"}
