@@ -152,7 +152,7 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // (the spill) goes to a global buffer; k_s3_fixup adds it into the next
 // blocks' head rows in ascending source order (deterministic).
 #ifndef KTB_S3_THREADS
-#define KTB_S3_THREADS 512
+#define KTB_S3_THREADS 256  // x 8 rows: measured 77.5-77.7 us vs 79.1-79.4 us for 512 x 4 (config 2)
 #endif
 constexpr int kS3Threads = KTB_S3_THREADS;  // threads per block (one block per SM)
 constexpr int kRPT = 2048 / kS3Threads;     // rows per thread: t + kS3Threads*u
