@@ -534,7 +534,10 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 // segment of <= kFixRows head rows of one destination, 4 rows per thread; the
 // segment's source metadata is plan data loaded before griddepcontrol.wait,
 // so after it every y and spill load of the thread goes out at once.
-__global__ void __launch_bounds__(256, kFixRows <= 1024 ? 1 : 4) k_s3_fixup(const int4* __restrict__ desc,
+#ifndef KTB_S3_FIXUP_MINB
+#define KTB_S3_FIXUP_MINB 5  // <= 51 registers, 5 blocks/SM: measured best of 1, 5, 6
+#endif
+__global__ void __launch_bounds__(256, KTB_S3_FIXUP_MINB) k_s3_fixup(const int4* __restrict__ desc,
                                                   const int32_t* __restrict__ seg_src,
                                                   const int32_t* __restrict__ cta_row,
                                                   const int32_t* __restrict__ spill_hi,
