@@ -249,7 +249,10 @@ __global__ void __launch_bounds__(kS3Threads, 1)
     // x is first touched by the far reach of the window: pull the initial
     // window and then each sub-tile's new front into L2 ahead of the gathers
     // (the bench flushes L2 between steps).
-    constexpr int kAhead = 2;  // sub-tiles of look-ahead
+#ifndef KTB_S3_AHEAD
+#define KTB_S3_AHEAD 2
+#endif
+    constexpr int kAhead = KTB_S3_AHEAD;  // sub-tiles of look-ahead
     auto pf = [&](int64_t lo, int64_t hi) {
         lo = max(lo & ~int64_t(1), int64_t(0));
         hi = min(hi, int64_t(n));
