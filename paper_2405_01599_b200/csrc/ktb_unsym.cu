@@ -128,11 +128,15 @@ __global__ void __launch_bounds__(256) k_u1(const int32_t* __restrict__ rp,
 // at once. The plan builds the copy on the device (k_sell_*); it is refused
 // when padding would more than triple the matrix (power-law rows).
 constexpr int kSellUnroll = 8;
+#ifndef KTB_U1S_THREADS
+#define KTB_U1S_THREADS 128  // 4 slices per CTA: vs 256, config 4 2.13-2.15 vs 2.33 ms, config 5 39.5 vs 42 us
+#endif
+constexpr int kU1sThreads = KTB_U1S_THREADS;
 #ifndef KTB_U1S_MINB
 #define KTB_U1S_MINB 1  // 7 (config 1's 8192 slices in one wave) caps registers at 32 and
                         // spills: slower on configs 1, 4 and 5
 #endif
-__global__ void __launch_bounds__(256, KTB_U1S_MINB) k_u1s(const int64_t* __restrict__ soff,
+__global__ void __launch_bounds__(kU1sThreads, KTB_U1S_MINB) k_u1s(const int64_t* __restrict__ soff,
                                              const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
@@ -475,9 +479,9 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
             KTB_CUDA(cudaEventRecord(p->join, p->side));
         }
         const int64_t slices = static_cast<int64_t>(p->sell_off.n) - 1;
-        const int grid = ceil_div(slices * 32, 256);
+        const int grid = ceil_div(slices * 32, kU1sThreads);
         p->ctas = grid;
-        k_u1s<<<grid, 256, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y, 0,
+        k_u1s<<<grid, kU1sThreads, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y, 0,
                                            static_cast<int32_t>(slices * 32), 0, p->sell_perm.p);
         KTB_LAUNCH();
         if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
@@ -485,9 +489,9 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
     }
     if (p->param == 100) {
         const int64_t s0 = r0 >> 5, s1 = ceil_div64(r1, 32);
-        const int grid = ceil_div((s1 - s0) * 32, 256);
+        const int grid = ceil_div((s1 - s0) * 32, kU1sThreads);
         p->ctas = grid;
-        k_u1s<<<grid, 256, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y,
+        k_u1s<<<grid, kU1sThreads, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y,
                                            static_cast<int32_t>(r0), static_cast<int32_t>(r1),
                                            p->ell_width, nullptr);
         KTB_LAUNCH();
