@@ -701,8 +701,12 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
 #ifndef KTB_U2W_MINB
 #define KTB_U2W_MINB 5
 #endif
+#ifndef KTB_TILE_WARPS
+#define KTB_TILE_WARPS 4  // warps per CTA of the U2/U3 warp-tile kernels (8: 4 % slower on config 3)
+#endif
+constexpr int kTileWarps = KTB_TILE_WARPS;
 template <int IPT>
-__global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __restrict__ rp,
+__global__ void __launch_bounds__(32 * kTileWarps, KTB_U2W_MINB * 8 / kTileWarps) k_u2w(const int32_t* __restrict__ rp,
                                                           const int32_t* __restrict__ col,
                                                           const double* __restrict__ val,
                                                           const double* __restrict__ x,
@@ -722,11 +726,11 @@ __global__ void __launch_bounds__(256, KTB_U2W_MINB) k_u2w(const int32_t* __rest
     // 128-byte line -> chunk swizzle by (b >> ESH)
     constexpr int ESH = IPT == 8 ? 2 : 3;
     constexpr int EMASK = IPT / 4 - 1;
-    __shared__ __align__(16) double s_prod[8][T];
+    __shared__ __align__(16) double s_prod[kTileWarps][T];
     // s_end[i] = 1 + row ending at item i of the tile, 0 = no row ends there
-    __shared__ __align__(16) int32_t s_end[8][T];
+    __shared__ __align__(16) int32_t s_end[kTileWarps][T];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * kTileWarps + warp;
     if (w >= tiles) return;
     const int64_t z0 = w * T;
     const int cnt = static_cast<int>(nnz - z0 < T ? nnz - z0 : T);
@@ -1317,10 +1321,10 @@ void u2_run(ktb_plan* p, const double* x, double* y) {
         return;
     }
     if (prm < 100) {
-        const int grid = static_cast<int>(ceil_div64(p->tiles, 8));
+        const int grid = static_cast<int>(ceil_div64(p->tiles, kTileWarps));
 #define KTB_U2W_CASE(I)                                                                      \
     case I:                                                                                   \
-        k_u2w<I><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,         \
+        k_u2w<I><<<grid, 32 * kTileWarps, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,         \
                                               p->wrow.p, m->nnz, p->tiles, p->carry_row.p,    \
                                               p->carry_val.p);                                \
         break;
@@ -1423,7 +1427,7 @@ __global__ void k_empty_list(const int32_t* __restrict__ rp, int64_t n,
     if (i < n && rp[i] == rp[i + 1]) out[i - ord[i]] = static_cast<int32_t>(i);  // ord = nonempty before i
 }
 
-__global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
+__global__ void __launch_bounds__(32 * kTileWarps, 32 / kTileWarps) k_u3w(const int32_t* __restrict__ col,
                                                  const double* __restrict__ val,
                                                  const double* __restrict__ x,
                                                  double* __restrict__ y, int64_t nnz,
@@ -1435,7 +1439,7 @@ __global__ void __launch_bounds__(256, 4) k_u3w(const int32_t* __restrict__ col,
                                                  double* __restrict__ carry_val) {
     constexpr int IPT = 8, NS = 4;  // NS: segment rows fetched ahead per lane
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * kTileWarps + warp;
     if (w >= tiles) return;
     const int64_t z0 = w * 256, k0 = z0 + lane * IPT;
     int32_t c[IPT];
@@ -1733,7 +1737,7 @@ void u3_run(ktb_plan* p, const double* x, double* y) {
     if (p->param == 1008 && p->kernel == KTB_U3) {
         k_zero_rows<<<ceil_div(p->nzero, 256), 256, 0, p->stream>>>(p->zero_rows.p, p->nzero, y);
         KTB_LAUNCH();
-        k_u3w<<<static_cast<int>(ceil_div64(p->tiles, 8)), 256, 0, p->stream>>>(
+        k_u3w<<<static_cast<int>(ceil_div64(p->tiles, kTileWarps)), 32 * kTileWarps, 0, p->stream>>>(
             m->col.p, m->val.p, x, y, m->nnz, p->tiles, p->flag_bits.p, p->seg_row.p,
             p->tile_q.p, p->carry_row.p, p->carry_val.p);
         KTB_LAUNCH();
