@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(kGThreads) k_mgs(const double* __restrict__ V,
 // reduction is fixed-order and computed identically by every CTA (one warp
 // reads the per-CTA partials in order + a fixed shuffle tree), so every CTA
 // sees the same h_q bit for bit.
-constexpr int kRThreads = 1024;
+#ifndef KTB_MGS_THREADS
+#define KTB_MGS_THREADS 1024  // 512 (E up to 32) measured equal
+#endif
+constexpr int kRThreads = KTB_MGS_THREADS;
 
 // Cross-CTA exchange without a grid barrier: CTA b publishes its partial of
 // reduction r as one 16-byte (value, tag) store into slot[r * nb + b], the
@@ -411,7 +414,7 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         // resident-w MGS: one CTA per SM holds E * kRThreads elements
         const int64_t per_cta = ceil_div64(n, static_cast<int64_t>(sms) * kRThreads);
         int E = 0;
-        for (int e : {1, 2, 4, 8, 12, 14, 16})
+        for (int e : {1, 2, 4, 8, 12, 14, 16, 24, 28, 32})
             if (e >= per_cta) {
                 E = e;
                 break;
@@ -425,6 +428,9 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
             case 12: res_fn = reinterpret_cast<const void*>(&k_mgs_res<12>); break;
             case 14: res_fn = reinterpret_cast<const void*>(&k_mgs_res<14>); break;
             case 16: res_fn = reinterpret_cast<const void*>(&k_mgs_res<16>); break;
+            case 24: res_fn = reinterpret_cast<const void*>(&k_mgs_res<24>); break;
+            case 28: res_fn = reinterpret_cast<const void*>(&k_mgs_res<28>); break;
+            case 32: res_fn = reinterpret_cast<const void*>(&k_mgs_res<32>); break;
             default: break;
         }
         const size_t res_smem = static_cast<size_t>(E) * kRThreads * 16;  // w and V slices

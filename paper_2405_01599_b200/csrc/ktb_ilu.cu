@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(kRunThreads) k_ilu_run(const int32_t* __restri
 // fenced at cluster scope before those prefetch loads and the barrier
 // arrival itself is relaxed, so the barrier does not wait for the prefetch.
 // A level then costs one round of z gathers + the store fence + the barrier.
-constexpr int kClThreads = 1024;
+#ifndef KTB_ILU_CL_THREADS
+#define KTB_ILU_CL_THREADS 512  // per CTA of the 16-CTA cluster: 2.46 ms per apply vs 3.0 ms at 1024
+#endif
+constexpr int kClThreads = KTB_ILU_CL_THREADS;
 constexpr int kPre = 4;
 #ifndef KTB_ILU_SPLIT_BARRIER
 #define KTB_ILU_SPLIT_BARRIER 1
