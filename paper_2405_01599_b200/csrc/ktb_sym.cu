@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             }
             double wv[kRPT];
             int sl[kRPT];
-#pragma unroll
             bool sc[kRPT];
+#pragma unroll
             for (int u = 0; u < kRPT; ++u) {
                 const int cu = col_of(cr[K][u >> 1], u);
                 sc[u] = cu >= 0;
