@@ -373,7 +373,7 @@ def run_gpu(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profile(cfg),
                          "peak_source": peak_src,
-                         "kernel": f"{sel.name} apply ({plan.launches} launches: main + fixup)",
+                         "kernel": f"{sel.name} apply ({plan.launches} launch{'es' if plan.launches != 1 else ''})",
                          "bytes_per_launch": B},
             "e2e": {"value": ws * B / (e2e / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
