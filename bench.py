@@ -2,20 +2,27 @@
 """SpMV benchmark (BASELINE.json metric: "SpMV GB/s (% of HBM peak) & GFLOP/s
 at 1/2/4/8 B200 vs host-CPU reference").
 
-Default workload = BASELINE.json configs[1] (config 2): 3-D 27-point stencil
-on 128^3, symmetric upper-triangle storage (n=2,097,152, nnz_s=28,920,060),
-x = seeded_vector(n, 2). One step = one y = A*x through the tuned engine
-(select_spmv_sym on device time -> S3 window kernel on this matrix).
+Default workload = config 4 (BASELINE.json configs[3], the one quoted "at
+1/2/4/8 B200" and the largest that fits one GPU): 3-D 7-point Laplacian on
+512^3 (n=134,217,728, nnz=937,951,232), full CRS, row-block partitioned by
+z-planes over the ranks with a one-plane x halo. One step = one y = A*x
+through libktb's native halo operator (ktb_halo_spmv: NCCL group on a
+high-priority stream overlapped with the interior rows, boundary planes after
+an event wait; U1 thread-per-row over the warp-sliced copy, bitwise equal to
+the reference's spmv_ref). The same code path runs at every N.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config 1|2|3|4|5] [--shard] [--ref-build release|native|parity]
+
+--gpus N with WORLD_SIZE unset re-launches itself under torchrun with N ranks
+(127.0.0.1 rendezvous), failing loudly if fewer than N GPUs exist; under
+torchrun (the driver's launch) each rank drives LOCAL_RANK's GPU. The control
+plane (id hand-off, barriers, max over ranks) is torch.distributed on gloo;
+the data plane is libktb's own NCCL communicator.
 
 GB/s uses the minimum-traffic model:
     B = 12*nnz + 4*(n+1) + 16*n      (nnz = stored nonzeros)
-
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config 1|2|3|4]
-
-N>1 (torchrun): every rank runs its own replica of the workload on its GPU
-(config 2 does not shard: "replicas only", weak scaling, no collective on the
-data path); ms_per_step is the max over ranks, value sums all ranks' bytes.
+Config 4: value = whole-matrix B / max-over-ranks step time (strong scaling).
 """
 from __future__ import annotations
 
@@ -27,12 +34,18 @@ import os
 # physical core, bound close
 os.environ.setdefault("OMP_PROC_BIND", "close")
 os.environ.setdefault("OMP_PLACES", "cores")
-import subprocess
-import sys
-import threading
-import time
+# the NCCL communicator init line (nranks, devices) goes to a per-process log
+# that bench.py re-emits on stderr and in the JSON line
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ktb_bench_nccl.%h.%p.log")
+import socket  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
 
-import numpy as np
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -40,25 +53,46 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "SpMV GB/s (% of HBM peak) & GFLOP/s at 1/2/4/8 B200 vs host-CPU reference"
 
+
+def _ref_stencil(nx, ny, nz):
+    def make(pool, variant):
+        from oracle import oracle as O
+
+        return O.RefEngine.stencil7(nx, ny, nz, 6.0, -1.0, pool, variant)
+    return make
+
+
+def _ref_host(builder, sym):
+    def make(pool, variant):
+        import matgen
+        from oracle import oracle as O
+
+        n, rp, ci, v = builder(matgen)
+        return O.RefEngine(sym, n, rp, ci, v, pool, variant)
+    return make
+
+
 CONFIGS = {
     1: dict(workload="cfg1: 64^3 7-pt Laplacian, full CRS (n=262,144, nnz=1,810,432)",
-            sym=False, seed=1,
+            sym=False, seed=1, n=262_144, nnz=1_810_432,
             gpu=lambda K, dev: K.stencil7(64, 64, 64, device=dev),
-            host=lambda M: M.stencil7(64, 64, 64), sample="the full matrix"),
+            host=lambda M: M.stencil7(64, 64, 64), ref=_ref_stencil(64, 64, 64),
+            sample="the full matrix"),
     2: dict(workload="cfg2: 128^3 27-pt stencil, symmetric upper CRS "
                      "(n=2,097,152, nnz_s=28,920,060)", sym=True, seed=2,
             gpu=lambda K, dev: K.stencil27_upper(128, 128, 128, device=dev),
-            host=lambda M: M.stencil27_upper(128, 128, 128), sample="the full matrix"),
+            host=lambda M: M.stencil27_upper(128, 128, 128),
+            ref=_ref_host(lambda M: M.stencil27_upper(128, 128, 128), True),
+            sample="the full matrix"),
     3: dict(workload="cfg3: power-law, n=4,000,000, 10% empty rows, Pareto(1.5) lengths <= 65,536, "
                      "nnz=39,552,727 (DESIGN.md recipe, seed 3)", sym=False, seed=3,
             gpu=lambda K, dev: K.powerlaw(device=dev),
-            host=lambda M: M.powerlaw(), sample="the full matrix"),
+            host=lambda M: M.powerlaw(), ref=_ref_host(lambda M: M.powerlaw(), False),
+            sample="the full matrix"),
     4: dict(workload="cfg4: 512^3 7-pt Laplacian, full CRS (n=134,217,728, nnz=937,951,232), "
-                     "single GPU", sym=False, seed=4,
-            gpu=lambda K, dev: K.stencil7(512, 512, 512, device=dev),
-            host=lambda M: M.stencil7(512, 512, 64),
-            sample="a 512x512x64 slab of the 512^3 7-pt matrix (1/8 of the rows; GB/s is "
-                   "size-intensive)"),
+                     "z-plane row blocks over the ranks, one-plane x halo",
+            sym=False, seed=4, n=134_217_728, nnz=937_951_232,
+            ref=_ref_stencil(512, 512, 512), sample="the full 512^3 matrix"),
 }
 
 
@@ -103,11 +137,112 @@ def peak_hbm() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def physical_cores() -> int:
+    """Physical cores (distinct (physical id, core id) pairs, i.e. lscpu
+    sockets x cores per socket), bounded by this process's CPU affinity."""
+    try:
+        pairs, cur = set(), {}
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if not line.strip():
+                    if "core id" in cur:
+                        pairs.add((cur.get("physical id", "0"), cur["core id"]))
+                    cur = {}
+                    continue
+                k, _, v = line.partition(":")
+                cur[k.strip()] = v.strip()
+        if "core id" in cur:
+            pairs.add((cur.get("physical id", "0"), cur["core id"]))
+        n = len(pairs) or (os.cpu_count() or 1)
+    except OSError:
+        n = os.cpu_count() or 1
+    return max(1, min(n, len(os.sched_getaffinity(0))))
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: exec N ranks under
+    torch.distributed.run on this node (127.0.0.1 rendezvous)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if not args.launch_probe:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s)"}),
+                  file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+class Control:
+    """The host control plane across ranks (torch.distributed on gloo):
+    barriers, max over ranks, gathering small objects. Not on the data path."""
+
+    def __init__(self, ws: int):
+        self.ws = ws
+        self.dist = None
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, vals):
+        if not self.dist:
+            return list(vals)
+        import torch
+
+        t = torch.tensor(list(vals), dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return [float(v) for v in t]
+
+    def min(self, vals):
+        return [-v for v in self.max([-v for v in vals])]
+
+    def gather(self, obj):
+        if not self.dist:
+            return [obj]
+        out = [None] * self.ws
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+def nccl_init_lines() -> list[str]:
+    """This process's NCCL communicator-init lines (NCCL_DEBUG=INFO, INIT)."""
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    path = path.replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
+    try:
+        with open(path) as f:
+            return [ln.strip() for ln in f if "Init COMPLETE" in ln or "nRanks" in ln]
+    except OSError:
+        return []
 
 
 # ----------------------------------------------------------------- clocks
@@ -175,43 +310,83 @@ def gpu_uuid(dev: int) -> str:
 
 
 # ---------------------------------------------------------- CPU baseline
-def cpu_reference_engine(cfg: dict):
-    """The reference's own tuned CPU path (oracle/_ref = unmodified reference
-    headers): select_spmv_sym/unsym + Sym/UnsymEngine::op, all host threads."""
-    import matgen
+REF_BINDING = "OMP_PROC_BIND=%s OMP_PLACES=%s" % (os.environ.get("OMP_PROC_BIND"),
+                                                 os.environ.get("OMP_PLACES"))
+
+
+def reference_engine(cfg: dict, variant: str):
+    """The reference's own tuned CPU path (oracle/_ref: the unmodified
+    reference headers): select_spmv_sym/unsym + Sym/UnsymEngine::op on a
+    WorkerPool of every physical core."""
+    cores = physical_cores()
+    eng = cfg["ref"](cores, variant)
     from oracle import oracle as O
 
-    n, rp, ci, v = cfg["host"](matgen)
-    cores = os.cpu_count() or 1
-    eng = O.RefEngine(cfg["sym"], n, rp, ci, v, cores)
-    x = O.Ref.seeded_vector(n, cfg["seed"])
-    return eng, n, len(ci), x, cores
+    x = O.Ref.seeded_vector(eng.n, cfg["seed"])
+    return eng, x, cores
 
 
-def time_cpu(eng, x, n, max_seconds=10.0, max_reps=2000, min_reps=3):
-    y = np.empty(n)
-    eng.apply(x, y)  # warm
-    times = []
-    t_end = time.perf_counter() + max_seconds
-    while (len(times) < min_reps) or (time.perf_counter() < t_end and len(times) < max_reps):
-        t0 = time.perf_counter()
-        eng.apply(x, y)
-        times.append(time.perf_counter() - t0)
-    return float(np.mean(times)), len(times), y
+def _engine_desc(eng) -> dict:
+    cands, sel = eng.report()
+    return {"selected": f"{eng.selected['name']} (jl {eng.selected['jl']}, "
+                        f"{eng.selected['workers']} workers)",
+            "selection_seconds": eng.select_seconds,
+            "candidates": [{"name": c["name"], "jl": c["jl"], "best_ms": c["best_seconds"] * 1e3,
+                            "correct": c["correct"]} for c in cands]}
 
 
-# ------------------------------------------------------------- main arms
+def cpu_baseline(cfg, variant="release", seconds=10.0):
+    from oracle import oracle as O
+
+    try:
+        eng, x, cores = reference_engine(cfg, variant)
+        y = np.empty(eng.n)
+        eng.apply(x, y)  # warm
+        ts = []
+        t_end = time.perf_counter() + seconds
+        while len(ts) < 3 or time.perf_counter() < t_end:
+            t0 = time.perf_counter()
+            eng.apply(x, y)
+            ts.append(time.perf_counter() - t0)
+        t = float(np.mean(ts))
+        nnz = cfg.get("nnz") or eng.nnz
+        return {"value": min_bytes(eng.n, nnz) / t / 1e9, "unit": "GB/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"{len(ts)} applies ({sum(ts):.1f} s) of {cfg['sample']} through the "
+                          f"reference's tuned engine ({eng.selected['name']}, "
+                          f"{eng.selected['workers']} OpenMP workers)",
+                "ms_per_apply": t * 1e3, "build": O.REF_FLAGS[variant], "binding": REF_BINDING,
+                **_engine_desc(eng)}
+    except Exception as e:  # report, never fail the GPU line
+        return {"value": None, "unit": "GB/s", "cores": physical_cores(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def config_block(cfg, kernel):
+    return {"workload": cfg["workload"], "kernel": kernel,
+            "x": f"seeded_vector(n, {cfg['seed']})",
+            "l2": L2_NOTE,
+            "bytes_model": "12*nnz + 4*(n+1) + 16*n (int32 idx, fp64 val, x read once, y written once)"}
+
+
+# ------------------------------------------------------------- reference arm
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle as O
 
-    if not O.ref_available():
-        print(json.dumps({"impl": "reference",
-                          "unavailable": "oracle/_ref/libktune_ref.so not built"}))
+    if args.config == 5:
+        print(json.dumps({"impl": "reference", "unavailable": "config 5 reference arm: see "
+                          "cpu_baseline of `bench.py --config 5`"}))
         return 0
-    eng, n, nnz, x, cores = cpu_reference_engine(cfg)
+    if not O.ref_available(args.ref_build):
+        print(json.dumps({"impl": "reference",
+                          "unavailable": f"oracle/_ref ({args.ref_build} build) not built"}))
+        return 0
+    eng, x, cores = reference_engine(cfg, args.ref_build)
+    n = eng.n
+    nnz = cfg.get("nnz") or eng.nnz
     B = min_bytes(n, nnz)
     y = np.empty(n)
     for _ in range(args.warmup):
@@ -224,266 +399,171 @@ def run_reference(args, cfg):
     t = float(np.mean(ts))
     gbs = B / t / 1e9
     line = {
-        "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.config == 4 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8d recipe, seeded)",
         "config": dict(config_block(cfg, f"reference {eng.selected['name']}"),
                        l2="n/a (host CPU; inputs resident in host memory)"),
         "impl": "reference",
         "gflops": flops(n, nnz, cfg["sym"]) / t / 1e9,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} applies of {cfg['sample']} ({cfg['workload']}) through "
-                                   f"the reference's tuned engine ({eng.selected['name']}, "
-                                   f"{eng.selected['workers']} OpenMP workers)", **REF_BUILD},
+                         "sample": f"{args.steps} applies of {cfg['sample']} ({cfg['workload']}) "
+                                   f"through the reference's tuned engine "
+                                   f"({eng.selected['name']}, {eng.selected['workers']} OpenMP "
+                                   f"workers); rank 0 only",
+                         "build": O.REF_FLAGS[args.ref_build], "binding": REF_BINDING,
+                         **_engine_desc(eng)},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
 
 
-def config_block(cfg, kernel):
-    return {"workload": cfg["workload"], "kernel": kernel,
-            "x": f"seeded_vector(n, {cfg['seed']})",
-            "l2": L2_NOTE,
-            "bytes_model": "12*nnz + 4*(n+1) + 16*n (int32 idx, fp64 val, x read once, y written once)"}
-
-
-def run_gpu(args, cfg):
+# -------------------------------------------------- single-GPU plan (1, 2, 3)
+def measure_plan(cfg, local, steps, warmup, warm_seconds, sampler=None):
+    """select_spmv_* on device time, then `steps` cold-L2 applies; returns a
+    dict of the numbers (device ms per apply, e2e host-call ms, selection)."""
     import torch
-
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2405_01599_b200 import _lib
     from paper_2405_01599_b200 import ktune as K
 
+    t0 = time.perf_counter()
     a = cfg["gpu"](K, local)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
     n, nnz = a.n, a.nnz()
-    B = min_bytes(n, nnz)
-    F = flops(n, nnz, cfg["sym"])
     stream = torch.cuda.Stream()
-    if cfg["sym"]:
-        choice, rep = K.select_spmv_sym(a)
-    else:
-        choice, rep = K.select_spmv_unsym(a)
+    t0 = time.perf_counter()
+    choice, rep = (K.select_spmv_sym if cfg["sym"] else K.select_spmv_unsym)(a)
+    t_select = time.perf_counter() - t0
     plan = choice.plan
     plan.set_stream(stream.cuda_stream)
     sel = rep.selected_candidate()
-    kname = f"{sel.name} (param {sel.jl})"
-
     x = torch.empty(n, dtype=torch.float64, device="cuda")
-    assert _lib.load().ktb_seeded_vector(n, cfg["seed"], 0, x.data_ptr(),
-                                         stream.cuda_stream) == 0
+    assert _lib.load().ktb_seeded_vector(n, cfg["seed"], 0, x.data_ptr(), stream.cuda_stream) == 0
     y = torch.empty(n, dtype=torch.float64, device="cuda")
-    l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    flush = L2Flush(l2)
-
-    sampler = ClockSampler(gpu_uuid(local))
-    sampler.start()
+    flush = L2Flush(torch.cuda.get_device_properties(local).L2_cache_size)
+    if sampler:
+        sampler.start()
     with torch.cuda.stream(stream):
-        # warm-up: >= W steps and ~1 s of load so the clocks settle
-        t_warm = time.perf_counter() + args.warm_seconds
+        t_warm = time.perf_counter() + warm_seconds
         w = 0
-        while w < args.warmup or time.perf_counter() < t_warm:
+        while w < warmup or time.perf_counter() < t_warm:
             plan.apply(x, y)
             w += 1
             if w % 50 == 0:
                 stream.synchronize()
         stream.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        r0.record(stream)
-        for k in range(args.steps):
+              for _ in range(steps)]
+        for k in range(steps):
             flush(k)
             ev[k][0].record(stream)
             plan.apply(x, y)
             ev[k][1].record(stream)
-        r1.record(stream)
         stream.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    ms = float(np.mean(step_ms))
-    region_ms = r0.elapsed_time(r1)
-
-    # e2e: public API with host buffers (pinned), H2D x + SpMV + D2H y per step
+    ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev]))
+    # e2e: the public host call, pipelined over steps (ktb_spmv_host_pipelined)
     xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     xh.copy_(x.cpu())
     yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     xn, yn = xh.numpy(), yh.numpy()
-    plan.apply(xn, yn)
-    e2e_ms = []
-    for k in range(max(3, args.steps)):
-        with torch.cuda.stream(stream):
-            flush(k)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        plan.apply(xn, yn)  # copies in, runs, copies out, synchronises
-        e1.record(stream)
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-    e2e_single = float(np.mean(e2e_ms))
-    # pipelined: the same per-step H2D x / SpMV / D2H y through the public
-    # batched host call (ktb_spmv_host_pipelined), copies of neighbouring
-    # steps overlapping the SpMV; wall clock around the call (it returns
-    # after the last y is on the host)
-    kpipe = max(3, args.steps)
+    kpipe = max(3, steps)
     plan.apply_host_pipelined(xn, yn, count=2)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     plan.apply_host_pipelined(xn, yn, count=kpipe)
     e2e = (time.perf_counter() - t0) * 1e3 / kpipe
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler else None
+    return dict(n=n, nnz=nnz, ms=ms, e2e_ms=e2e, plan=plan, sel=sel, rep=rep, clocks=clocks,
+                build_s=t_build, select_s=t_select)
 
-    if dist:
-        t = torch.tensor([ms, e2e, e2e_single], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, e2e, e2e_single = float(t[0]), float(t[1]), float(t[2])
 
+def run_gpu(args, cfg):
+    """Configs 1-3: the tuned plan on each rank's GPU (replicas only: these
+    matrices are not sharded by default; weak scaling, no collective)."""
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    ctl = Control(ws)
+    ctl.barrier()
+    r = measure_plan(cfg, local, args.steps, args.warmup, args.warm_seconds,
+                     ClockSampler(gpu_uuid(local)))
+    ms, e2e = ctl.max([r["ms"], r["e2e_ms"]])
+    n, nnz, plan, sel = r["n"], r["nnz"], r["plan"], r["sel"]
+    B, F = min_bytes(n, nnz), flops(n, nnz, cfg["sym"])
     if rank == 0:
         peak, peak_src = peak_hbm()
         achieved = B / (ms / 1e3) / 1e9
         line = {
-            "metric": METRIC,
-            "value": ws * B / (ms / 1e3) / 1e9,
-            "unit": "GB/s",
-            "n_gpus": ws,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64",
+            "metric": METRIC, "value": ws * achieved, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded; replicas per rank)",
-            "config": config_block(cfg, kname),
+            "config": dict(config_block(cfg, f"{sel.name} (param {sel.jl})"),
+                           parallelism=f"replicas x{ws}"),
             "gflops": ws * F / (ms / 1e3) / 1e9,
             "pct_hbm_peak": 100.0 * achieved / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profile(cfg),
                          "peak_source": peak_src,
-                         "kernel": f"{sel.name} apply ({plan.launches} launch{'es' if plan.launches != 1 else ''})",
+                         "kernel": f"{sel.name} apply ({plan.launches} launch"
+                                   f"{'es' if plan.launches != 1 else ''})",
                          "bytes_per_launch": B},
             "e2e": {"value": ws * B / (e2e / 1e3) / 1e9, "unit": "GB/s",
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "h2d_bytes_per_step": ws * 8 * n, "d2h_bytes_per_step": ws * 8 * n,
                     "ms_per_step": e2e,
                     "def": "public batched host call (ktb_spmv_host_pipelined): every step "
                            "copies its x in from pinned host memory and its y out; copies "
-                           "of neighbouring steps overlap the SpMV; wall clock",
-                    "unpipelined": {"value": ws * B / (e2e_single / 1e3) / 1e9,
-                                    "ms_per_step": e2e_single,
-                                    "def": "one ktb_spmv(KTB_PTR_HOST) call per step, "
-                                           "CUDA events"}},
-            "gpu_launches": args.steps * plan.launches,
-            "timed_region_ms": region_ms,
-            "clocks": clocks,
+                           "of neighbouring steps overlap the SpMV; wall clock"},
+            "gpu_launches": ws * args.steps * plan.launches,
+            "clocks": r["clocks"],
+            "setup_seconds": {"matrix": r["build_s"], "selection": r["select_s"]},
             "selection": [{"name": c.name, "param": c.jl, "best_ms": c.best_seconds * 1e3,
-                           "correct": c.correct} for c in rep.candidates],
+                           "correct": c.correct} for c in r["rep"].candidates],
         }
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg)
+            line["cpu_baseline"] = cpu_baseline(cfg, args.ref_build)
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    ctl.close()
     return 0
 
 
-class _GeneralShard:
-    """--shard: an arbitrary config matrix split by NNZ_BALANCED row blocks
-    over the ranks (dist.DistCsrSpMV: native split + ghost map, NCCL ghost
-    exchange overlapped with the diagonal block). Same fields as DistSpMV."""
-
-    def __init__(self, cfg, rank, ws, local):
-        import types
-
-        import torch
-
-        from paper_2405_01599_b200 import _lib
-        from paper_2405_01599_b200 import dist as D
-
-        if cfg["seed"] == 3:  # config 3: the native multi-threaded host generator
-            from paper_2405_01599_b200 import ktune as K
-
-            n, rp, ci, v = K.powerlaw_host()
-        else:
-            import matgen
-
-            n, rp, ci, v = cfg["host"](matgen)
-        self.n_glob, self.nnz_glob = n, int(rp[-1])
-        b = D.nnz_balanced_boundaries(rp, ws)
-        r0, r1 = int(b[rank]), int(b[rank + 1])
-        self.sp = D.DistCsrSpMV(n, b, rank, ws, rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]],
-                                v[rp[r0]:rp[r1]], local)
-        del rp, ci, v
-        self.nnz = self.sp.A_d.nnz() + self.sp.dc.nnz_ghost
-        self.kname = ("u%d" % (self.sp.plan.kernel + 1)) if self.sp.A_d.nnz() else "none"
-        self.L = types.SimpleNamespace(owned_offset=0, n_local=self.sp.n_local)
-        dev = f"cuda:{local}"
-        self.x = torch.empty(max(self.sp.n_local, 1), dtype=torch.float64, device=dev)
-        assert _lib.load().ktb_seeded_vector(self.sp.n_local, cfg["seed"], r0, self.x.data_ptr(),
-                                             torch.cuda.current_stream(local).cuda_stream) == 0
-        self.y = torch.empty_like(self.x)
-
-    def apply(self):
-        n = self.sp.n_local
-        return self.sp.apply(self.x[:n], self.y[:n])
-
-    def launches_per_apply(self):
-        return self.sp.launches_per_apply()
-
-    def exchange_only(self):
-        n = self.sp.n_local
-        self.sp.exchange_only(self.x[:n])
-
-
-def run_gpu_dist(args, cfg):
-    """Config 4: z-slab row-block sharding over the ranks (paper_2405_01599_b200
-    .dist), NCCL P2P halo exchange overlapped with the interior rows; with
-    --shard (configs 1/3): general NNZ_BALANCED row blocks with a ghost-column
-    exchange. Fixed total problem: strong scaling; value = whole-matrix bytes
-    / max-rank time."""
+# ---------------------------------------------------- config 4: halo shards
+def run_halo(args, cfg):
+    """Config 4 over the ranks: z-slab row blocks, native halo operator over
+    libktb's NCCL communicator, the same code path at every N (at N=1 the
+    interior is every row and there is no message)."""
     import torch
+
+    from paper_2405_01599_b200 import dist as D
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2405_01599_b200 import dist as D
-
-    if args.config == 4:
-        nx = ny = nz = 512
-        shard = D.DistSpMV(nx, ny, nz, rank, ws, local, seed=cfg["seed"])
-        n_glob = nx * ny * nz
-        nnz_glob = 7 * n_glob - 6 * nx * nx  # 7-pt stencil with Dirichlet boundary
-        klabel = "u1 warp-sliced (param 100) interior + boundary planes (z-slab shards, NCCL halo)"
-        par = f"row-block z-slabs x{ws}, one-plane halo"
-        rlabel = "u1 thread-per-row over the warp-sliced copy (rank-0 slab interior + boundary planes)"
-    else:
-        shard = _GeneralShard(cfg, rank, ws, local)
-        n_glob, nnz_glob = shard.n_glob, shard.nnz_glob
-        klabel = f"{shard.kname} on A_d + ghost accumulate (general row blocks, NCCL ghosts)"
-        par = f"NNZ_BALANCED row blocks x{ws}, ghost-column exchange"
-        rlabel = f"{shard.kname} (rank 0 diagonal block) + k_ghost_acc"
-    B = min_bytes(n_glob, nnz_glob)
-    B_local = min_bytes(shard.L.n_local, shard.nnz)
-    F = flops(n_glob, nnz_glob, False)
+    ctl = Control(ws)
+    t0 = time.perf_counter()
+    comm = D.Comm.nccl(device=local)
+    t_comm = time.perf_counter() - t0
+    nccl_lines = ctl.gather(nccl_init_lines())
+    if rank == 0:
+        for r, lines in enumerate(nccl_lines):
+            for ln in lines:
+                print(f"[rank {r}] {ln}", file=sys.stderr)
+    t0 = time.perf_counter()
+    shard = D.DistSpMV(512, 512, 512, comm, seed=cfg["seed"])
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    shard.set_timing(True)
+    n_glob, nnz_glob = cfg["n"], cfg["nnz"]
+    B, F = min_bytes(n_glob, nnz_glob), flops(n_glob, nnz_glob, False)
+    ir, inz, br, bnz = shard.parts()
+    B_int = min_bytes(ir, inz)
     stream = torch.cuda.Stream()
-    l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    flush = L2Flush(l2)
+    flush = L2Flush(torch.cuda.get_device_properties(local).L2_cache_size)
     sampler = ClockSampler(gpu_uuid(local))
     sampler.start()
     with torch.cuda.stream(stream):
@@ -495,30 +575,30 @@ def run_gpu_dist(args, cfg):
             if w % 10 == 0:
                 stream.synchronize()
         stream.synchronize()
-        if dist:
-            dist.barrier()
+        ctl.barrier()
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
+        kern = []
         for k in range(args.steps):
             flush(k)
-            if dist:  # all ranks start the step together (halo partners)
-                dist.barrier()
+            stream.synchronize()
+            ctl.barrier()  # halo partners start the step together
             ev[k][0].record(stream)
             shard.apply()
             ev[k][1].record(stream)
-        stream.synchronize()
-        if dist:
-            dist.barrier()
+            stream.synchronize()
+            kern.append(shard.last_times())
+        ctl.barrier()
         torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-    # the exchange step alone (halo planes / packed ghosts over NCCL P2P), same
-    # stream and events; 0 messages at one rank
+    int_ms = float(np.mean([a for a, _ in kern]))
+    bnd_ms = float(np.mean([b for _, b in kern]))
+    # the exchange step alone (one NCCL group), same stream and events
     hx = []
     with torch.cuda.stream(stream):
         for k in range(max(3, min(args.steps, 20))):
-            if dist:
-                dist.barrier()
+            ctl.barrier()
             h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             h0.record(stream)
             shard.exchange_only()
@@ -526,68 +606,182 @@ def run_gpu_dist(args, cfg):
             h1.synchronize()
             hx.append(h0.elapsed_time(h1))
     halo_ms = float(np.mean(hx))
-    # e2e: owned x from pinned host, sharded apply, owned y back to host
-    o0, n_loc = shard.L.owned_offset, shard.L.n_local
-    xh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-    xh.copy_(shard.x[o0:o0 + n_loc].cpu())
-    yh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-    e2e_ms = []
-    with torch.cuda.stream(stream):
+    # e2e: the public host call (ktb_halo_spmv_host): owned x from pinned host
+    # memory in, owned y out, copies overlapped with the rows inside the call
+    xo = shard.x[shard.owned_offset:shard.owned_offset + shard.n_local].cpu().pin_memory()
+    yh = torch.empty(shard.n_local, dtype=torch.float64).pin_memory()
+    xn, yn = xo.numpy(), yh.numpy()
+    e2e = {}
+    for chunks in (16, 1):
+        shard.apply_host(xn, yn, chunks=chunks)  # warm
+        ts = []
         for k in range(max(3, min(args.steps, 10))):
-            flush(k)
-            if dist:
-                dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            shard.x[o0:o0 + n_loc].copy_(xh, non_blocking=True)
-            shard.apply()
-            yh.copy_(shard.y, non_blocking=True)
-            e1.record(stream)
-            e1.synchronize()
-            e2e_ms.append(e0.elapsed_time(e1))
+            with torch.cuda.stream(stream):
+                flush(k)
+            stream.synchronize()
+            ctl.barrier()
+            t0 = time.perf_counter()
+            shard.apply_host(xn, yn, chunks=chunks)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        e2e[chunks] = float(np.mean(ts))
     clocks = sampler.stop()
-    e2e = float(np.mean(e2e_ms))
-    if dist:
-        t = torch.tensor([ms, e2e, halo_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, e2e, halo_ms = float(t[0]), float(t[1]), float(t[2])
+    ach_rank = B_int / (int_ms / 1e3) / 1e9 if int_ms > 0 else 0.0
+    ms, e2e16, e2e1, halo_max, int_max, bnd_max = ctl.max(
+        [ms, e2e[16], e2e[1], halo_ms, int_ms, bnd_ms])
+    ach_min, = ctl.min([ach_rank])
     if rank == 0:
         peak, peak_src = peak_hbm()
-        achieved = B_local / (ms / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": B / (ms / 1e3) / 1e9, "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-            "config": dict(config_block(cfg, klabel), parallelism=par),
+            "config": dict(config_block(cfg, "u1 thread-per-row over the warp-sliced copy "
+                                             "(param 100), ktb_halo_spmv"),
+                           parallelism=f"row-block z-slabs x{ws}, one-plane halo, NCCL P2P"),
             "gflops": F / (ms / 1e3) / 1e9,
-            "pct_hbm_peak_per_gpu": 100.0 * achieved / peak,
-            "per_gpu_gbs": achieved,
-            "exchange_ms": halo_ms,
-            "exchange_def": "the step's x-halo / ghost exchange alone (NCCL P2P, max over "
-                            "ranks); inside the step it overlaps the interior rows",
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": traffic_from_profile(cfg) if ws == 1 and args.config == 4
-                         else None,
+            "per_gpu_gbs": B / ws / (ms / 1e3) / 1e9,
+            "pct_hbm_peak_per_gpu": 100.0 * B / ws / (ms / 1e3) / 1e9 / peak,
+            "exchange_ms": halo_max,
+            "exchange_def": "the step's halo exchange alone (one NCCL group, max over ranks); "
+                            "inside the step it overlaps the interior rows",
+            "kernel_ms": {"interior": int_max, "boundary": bnd_max,
+                          "def": "CUDA events on the compute stream around the interior / "
+                                 "boundary rows of each timed step, mean, max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": ach_min, "peak": peak, "unit": "GB/s",
+                         "frac": ach_min / peak,
+                         "traffic": traffic_from_profile(cfg) if ws == 1 else None,
                          "peak_source": peak_src,
-                         "kernel": rlabel,
-                         "bytes_per_launch": B_local,
+                         "kernel": "k_u1s over the interior rows (1 launch per step)",
+                         "bytes_per_launch": B_int,
                          "note": "peak is the measured copy (read + write) bandwidth; a "
                                  "read-dominated stream can exceed it (frac > 1); the "
                                  "warp-sliced kernel does not read row_ptr (4 B/row of the "
-                                 "model)"},
-            "e2e": {"value": B / (e2e / 1e3) / 1e9, "unit": "GB/s",
+                                 "model); achieved = min over ranks"},
+            "e2e": {"value": B / (e2e16 / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
-                    "ms_per_step": e2e},
-            "gpu_launches": args.steps * shard.launches_per_apply(),
+                    "ms_per_step": e2e16,
+                    "def": "ktb_halo_spmv_host on every rank: owned x from pinned host memory "
+                           "in, owned y out, copies overlapped with 16 row chunks inside the "
+                           "call; wall clock, max over ranks",
+                    "unchunked": {"value": B / (e2e1 / 1e3) / 1e9, "ms_per_step": e2e1}},
+            "gpu_launches": args.steps * shard.launches_per_apply() * ws,
             "clocks": clocks,
+            "nccl": {"version": comm.nccl_version, "world": comm.world,
+                     "comm_init": [ln for lines in nccl_lines for ln in lines
+                                   if "Init COMPLETE" in ln]},
+            "setup_seconds": {"comm": t_comm, "matrix_and_plans": t_setup},
         }
-        if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg)
+        if ws == 1:
+            if not args.no_secondary:
+                line["secondary"] = secondary_cfg2(local, args)
+            if not args.no_cpu_baseline:
+                line["cpu_baseline"] = cpu_baseline(cfg, args.ref_build)
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    shard.close()
+    comm.close()
+    ctl.close()
+    return 0
+
+
+def secondary_cfg2(local, args):
+    """Config 2 (S3, symmetric upper) at one GPU, GPU side only: kept in the
+    headline line as an extra key (row a11's driver-timed evidence)."""
+    try:
+        r = measure_plan(CONFIGS[2], local, max(10, min(args.steps, 50)), args.warmup, 0.5)
+        B = min_bytes(r["n"], r["nnz"])
+        peak, _ = peak_hbm()
+        a = B / (r["ms"] / 1e3) / 1e9
+        return {"cfg2_s3": {"workload": CONFIGS[2]["workload"],
+                            "kernel": f"{r['sel'].name} (param {r['sel'].jl})",
+                            "ms_per_step": r["ms"], "value": a, "unit": "GB/s",
+                            "frac": a / peak, "launches": r["plan"].launches,
+                            "gflops": flops(r["n"], r["nnz"], True) / (r["ms"] / 1e3) / 1e9,
+                            "e2e_gbs": B / (r["e2e_ms"] / 1e3) / 1e9,
+                            "setup_seconds": {"matrix": r["build_s"], "selection": r["select_s"]},
+                            "l2": L2_NOTE}}
+    except Exception as e:
+        return {"cfg2_s3": {"unavailable": str(e)}}
+
+
+# ------------------------------------- configs 1/3 --shard: general row blocks
+def run_general_shard(args, cfg):
+    """--shard (configs 1/3): NNZ_BALANCED row blocks over the ranks, native
+    ghost exchange (ktb_dist_spmv over libktb's NCCL communicator)."""
+    import torch
+
+    from paper_2405_01599_b200 import _lib
+    from paper_2405_01599_b200 import dist as D
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    ctl = Control(ws)
+    comm = D.Comm.nccl(device=local)
+    if cfg["seed"] == 3:
+        from paper_2405_01599_b200 import ktune as K
+
+        n, rp, ci, v = K.powerlaw_host()
+    else:
+        import matgen
+
+        n, rp, ci, v = cfg["host"](matgen)
+    nnz_glob = int(rp[-1])
+    b = D.nnz_balanced_boundaries(rp, ws)
+    r0, r1 = int(b[rank]), int(b[rank + 1])
+    sp = D.DistCsrSpMV(n, b, comm, rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]], v[rp[r0]:rp[r1]])
+    del rp, ci, v
+    x = torch.empty(max(sp.n_local, 1), dtype=torch.float64, device="cuda")
+    assert _lib.load().ktb_seeded_vector(sp.n_local, cfg["seed"], r0, x.data_ptr(),
+                                         torch.cuda.current_stream().cuda_stream) == 0
+    y = torch.empty_like(x)
+    B, F = min_bytes(n, nnz_glob), flops(n, nnz_glob, False)
+    stream = torch.cuda.Stream()
+    flush = L2Flush(torch.cuda.get_device_properties(local).L2_cache_size)
+    sampler = ClockSampler(gpu_uuid(local))
+    sampler.start()
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            sp.apply(x[:sp.n_local], y[:sp.n_local])
+        stream.synchronize()
+        ctl.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush(k)
+            stream.synchronize()
+            ctl.barrier()
+            ev[k][0].record(stream)
+            sp.apply(x[:sp.n_local], y[:sp.n_local])
+            ev[k][1].record(stream)
+        stream.synchronize()
+        hx = []
+        for k in range(max(3, min(args.steps, 20))):
+            ctl.barrier()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            sp.exchange_only(x[:sp.n_local])
+            h1.record(stream)
+            h1.synchronize()
+            hx.append(h0.elapsed_time(h1))
+    clocks = sampler.stop()
+    ms, halo = ctl.max([float(np.mean([a.elapsed_time(b) for a, b in ev])), float(np.mean(hx))])
+    if rank == 0:
+        peak, peak_src = peak_hbm()
+        line = {"metric": METRIC, "value": B / (ms / 1e3) / 1e9, "unit": "GB/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (SURVEY.md §8d recipe, seeded)",
+                "config": dict(config_block(cfg, f"{sp.kernel_name()} on A_d + k_ghost_acc "
+                                                 "(ktb_dist_spmv)"),
+                               parallelism=f"NNZ_BALANCED row blocks x{ws}, ghost exchange"),
+                "gflops": F / (ms / 1e3) / 1e9, "exchange_ms": halo,
+                "roofline": {"bound": "hbm", "achieved": B / ws / (ms / 1e3) / 1e9,
+                             "peak": peak, "unit": "GB/s",
+                             "frac": B / ws / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                             "peak_source": peak_src, "kernel": "the sharded apply per rank"},
+                "gpu_launches": args.steps * sp.launches_per_apply() * ws, "clocks": clocks}
+        print(json.dumps(line))
+    ctl.close()
     return 0
 
 
@@ -629,11 +823,7 @@ def run_gmres(args, cfg):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctl = Control(ws)
     a = K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7, device=local)
     n, nnz = a.n, a.nnz()
     B = min_bytes(n, nnz)
@@ -674,21 +864,21 @@ def run_gmres(args, cfg):
         rp, ci, v = a.to_host()
         bnd = D.nnz_balanced_boundaries(rp, ws)
         r0, r1 = int(bnd[rank]), int(bnd[rank + 1])
-        op = D.DistCsrSpMV(n, bnd, rank, ws, rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]],
-                           v[rp[r0]:rp[r1]], local)
+        comm = D.Comm.nccl(device=local)
+        op = D.DistCsrSpMV(n, bnd, comm, rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]],
+                           v[rp[r0]:rp[r1]])
         del rp, ci, v
-        kname = f"u{op.plan.kernel + 1} on A_d + ghost acc, gmres_m_dist (MGS, NCCL all-reduce)"
+        kname = f"{op.kernel_name()} on A_d + ghost acc, gmres_m_dist (MGS, NCCL all-reduce)"
         ones = torch.ones(op.n_local, dtype=torch.float64, device="cuda")
         bd = torch.empty_like(ones)
         op.apply(ones, bd)
         b_host = bd.cpu().numpy()
-        ar = KR.process_group_allreduce()
+        ar = KR.comm_allreduce(comm)
         ops = KR.DeviceVecOps(31, local)
         for _ in range(max(1, args.warmup // 3)):
             KR.gmres_m_dist(op, bd, m=30, tol=1e-8, max_iters=3000, ortho="mgs", ops=ops,
                             allreduce=ar)
-        if dist:
-            dist.barrier()
+        ctl.barrier()
         sampler.start()
         runs = []
         for _ in range(max(1, args.steps // 10)):
@@ -706,10 +896,7 @@ def run_gmres(args, cfg):
         r = runs[-1][0]
         wall = float(np.mean([t for _, t, *_ in runs]))
         spmv = float(np.mean([s for _, _, s, *_ in runs]))
-        if dist:
-            t = torch.tensor([wall, spmv], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall, spmv = float(t[0]), float(t[1])
+        wall, spmv = ctl.max([wall, spmv])
         calls, its = runs[-1][3], r.iterations
         launches = runs[-1][4] + runs[-1][5]
         info = {"iterations": its, "restarts": len(r.restarts), "true_residual": r.true_residual,
@@ -745,29 +932,39 @@ def run_gmres(args, cfg):
                 "gpu_launches": launches * len(runs) * ranks_note,
                 "clocks": clocks}
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = _gmres_cpu_baseline(a, B)
+            line["cpu_baseline"] = _gmres_cpu_baseline(a, B, args.gmres_full_reference)
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    ctl.close()
     return 0
 
 
-def _gmres_cpu_baseline(a, B):
+def _gmres_cpu_baseline(a, B, full=False):
+    """The reference's gmres_m (MGS) with a U1 UnsymEngine on every physical
+    core: a 60-iteration sample by default, the whole 653-iteration solve with
+    --gmres-full-reference (about a minute on 16 cores)."""
     from oracle import oracle as O  # cpu_baseline leg only
 
     try:
         rp, ci, v = a.to_host()
         n = a.n
         b = O.spmv_ref(n, rp, ci, v, np.ones(n))
-        its = 60  # bounded sample: two restarts of the reference solver
-        _, rr = O.Ref.gmres(n, rp, ci, v, b, 30, 1e-8, its, 1, os.cpu_count() or 1)
+        its = 3000 if full else 60
+        cores = physical_cores()
+        _, rr = O.Ref.gmres(n, rp, ci, v, b, 30, 1e-8, its, 1, cores)
+        done = rr["iterations"]
+        what = (f"the whole solve: {done} iterations, {rr['seconds']:.2f} s, true residual "
+                f"{rr['true_residual']:.3e}" if full else
+                f"{its} iterations (two restarts): {rr['seconds']:.2f} s "
+                f"({rr['seconds'] / its * 1e3:.1f} ms/it)")
         return {"value": B * rr["spmv_calls"] / max(rr["spmv_seconds"], 1e-12) / 1e9,
-                "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
-                "sample": f"{its} iterations of ktune::gmres_m (MGS) with a U1 UnsymEngine on "
-                          f"all cores: {rr['seconds']:.2f} s ({rr['seconds'] / its * 1e3:.1f} "
-                          f"ms/it; 653 its extrapolate to {rr['seconds'] / its * 653:.1f} s)"}
+                "unit": "GB/s", "cores": cores, "kind": "reference",
+                "solve_seconds": rr["seconds"], "iterations": done,
+                "spmv_share": rr["spmv_seconds"] / max(rr["seconds"], 1e-12),
+                "sample": f"ktune::gmres_m (MGS) with a U1 UnsymEngine on all physical cores, "
+                          + what, "build": O.REF_FLAGS["parity"]}
     except Exception as e:
         return {"value": None, "sample": f"unavailable: {e}"}
+
 
 
 def traffic_from_profile(cfg):
@@ -781,47 +978,47 @@ def traffic_from_profile(cfg):
         return None
 
 
-REF_BUILD = {"build": "unmodified reference headers via oracle/Makefile: g++ -O2 -std=c++20 "
-                      "-fopenmp -ffp-contract=off (no -march=native)",
-             "binding": "OMP_PROC_BIND=%s OMP_PLACES=%s" % (os.environ.get("OMP_PROC_BIND"),
-                                                          os.environ.get("OMP_PLACES"))}
-
-
-def cpu_baseline(cfg):
-    try:
-        eng, n, nnz, x, cores = cpu_reference_engine(cfg)
-        t, reps, _ = time_cpu(eng, x, n)
-        return {"value": min_bytes(n, nnz) / t / 1e9, "unit": "GB/s", "cores": cores,
-                "kind": "reference",
-                "sample": f"{reps} applies ({reps * t:.1f} s) of {cfg['sample']} ({cfg['workload']}) "
-                          f"through the reference's tuned engine ({eng.selected['name']}, "
-                          f"{eng.selected['workers']} OpenMP workers)",
-                "ms_per_apply": t * 1e3, **REF_BUILD}
-    except Exception as e:  # report, never fail the GPU line
-        return {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
-                "sample": f"unavailable: {e}"}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS) + [5])
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS) + [5])
+    ap.add_argument("--ref-build", default="release", choices=["release", "native", "parity"],
+                    help="reference build for the reference arm / cpu_baseline "
+                         "(oracle/Makefile): the reference's CMake Release (default), "
+                         "+ -march=native, or the -ffp-contract=off parity build")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="config 4: skip the config-2 S3 extra key")
     ap.add_argument("--shard", action="store_true",
                     help="configs 1/3: general row-block sharding over the ranks; config 5: "
                          "one distributed solve (default: replicas)")
+    ap.add_argument("--gmres-full-reference", action="store_true",
+                    help="config 5: time the reference's whole 653-iteration solve")
     ap.add_argument("--warm-seconds", type=float, default=1.0,
                     help="keep warming up at least this long (clocks settle); 0 under ncu")
+    ap.add_argument("--launch-probe", action="store_true",
+                    help="print each rank's launch environment and exit (CPU test of the "
+                         "--gpus self-launch)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
+    if args.launch_probe:
+        ws, rank, local = dist_env()
+        print(json.dumps({"launch_probe": True, "rank": rank, "world": ws, "local_rank": local,
+                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
+        return 0
     cfg = CONFIGS.get(args.config, {"workload": "cfg5", "sym": False, "seed": 5})
     if args.impl == "reference":
         return run_reference(args, cfg)
-    if args.config == 4 or (args.shard and args.config in (1, 3)):
-        return run_gpu_dist(args, cfg)
+    if args.config == 4:
+        return run_halo(args, cfg)
+    if args.shard and args.config in (1, 3):
+        return run_general_shard(args, cfg)
     if args.config == 5:
         return run_gmres(args, cfg)
     return run_gpu(args, cfg)

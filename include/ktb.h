@@ -281,6 +281,111 @@ int ktb_dist_pack(const ktb_dist* d, const double* x_owned, double* send_buf, vo
 /* y += A_o x_ghost (device pointers); run after A_d x_owned -> y. */
 int ktb_dist_ghost_spmv(const ktb_dist* d, const double* x_ghost, double* y, void* stream);
 
+/* ------------------------------------------ communicator (native NCCL) */
+/* The multi-GPU data plane: one process per GPU, one
+ * communicator per process. No reference counterpart (the reference is a
+ * single-process OpenMP library). */
+typedef struct ktb_comm ktb_comm;
+typedef struct ktb_loopback_world ktb_loopback_world;
+#define KTB_COMM_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+enum { KTB_SUM = 0, KTB_MAX = 1 };
+/* ncclGetUniqueId: rank 0 calls it and hands the bytes to every rank out of
+ * band (MPI, a TCP store, torch.distributed.broadcast_object_list). */
+int ktb_comm_id(uint8_t* id /* KTB_COMM_ID_BYTES */);
+/* ncclCommInitRank on `device` (collective over the world). */
+int ktb_comm_create(const uint8_t* id, int world, int rank, int device, ktb_comm** out);
+/* Borrow a caller's ncclComm_t (e.g. torch's ProcessGroupNCCL::_comm_ptr());
+ * it is not destroyed by ktb_comm_destroy. device < 0: take the comm's. */
+int ktb_comm_wrap(void* nccl_comm, int device, ktb_comm** out);
+/* Test transport: `world` ranks inside ONE process, each rank driven by its
+ * own host thread; messages are matched on the host and moved by device
+ * copies (no kernel ever waits on another rank). Same semantics as NCCL's
+ * grouped send/recv, all-reduce and all-gather, host-synchronous. */
+int ktb_loopback_world_create(int world, ktb_loopback_world** out);
+int ktb_loopback_world_destroy(ktb_loopback_world* w);
+int ktb_comm_create_loopback(ktb_loopback_world* w, int rank, int device, ktb_comm** out);
+int ktb_comm_info(const ktb_comm* c, int* world, int* rank, int* device, int* nccl_version,
+                  int* is_nccl);
+int ktb_comm_destroy(ktb_comm* c);
+/* In place over device doubles (KTB_SUM / KTB_MAX), enqueued on stream. */
+int ktb_comm_allreduce(ktb_comm* c, double* buf, int64_t count, int op, void* stream);
+/* recv[r*bytes, (r+1)*bytes) = rank r's `send` (device buffers). */
+int ktb_comm_allgather(ktb_comm* c, const void* send, void* recv, size_t bytes, void* stream);
+/* One grouped send + receive (peer < 0 or 0 bytes skips that half). */
+int ktb_comm_sendrecv(ktb_comm* c, const void* send, size_t send_bytes, int send_peer, void* recv,
+                      size_t recv_bytes, int recv_peer, void* stream);
+
+/* ------------------------------------- halo row-block operator (config 4) */
+/* spmv_unsym (spmv.hpp:111-126) over a row block with a banded halo: `local`
+ * holds this rank's n rows with LOCAL columns over [halo_lo | owned n |
+ * halo_hi] (ncols = halo_lo + n + halo_hi); rank r-1 owns the rows just
+ * below, r+1 just above. Collective: the ranks exchange their shapes, so
+ * each learns how many owned entries its neighbours read. The rows split into
+ * the interior (no halo column) and the boundary rows, each a row slice with
+ * its own plan (kernel/param as ktb_plan_create; the matrix may be destroyed
+ * after this call). */
+typedef struct ktb_halo ktb_halo;
+int ktb_halo_create(ktb_matrix* local, int64_t halo_lo, int64_t halo_hi, ktb_comm* comm,
+                    int kernel, int64_t param, ktb_halo** out);
+/* Config 4's shard: z-planes [r*nz/W, (r+1)*nz/W) of the 3-D 7-point stencil
+ * with one-plane halos, generated on the communicator's device. */
+int ktb_halo_create_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
+                             ktb_comm* comm, int kernel, int64_t param, ktb_halo** out);
+/* The same from this rank's rows in the caller's global numbering (rows
+ * [row0, row0+n_local) of an n_global-row matrix, int64 row_ptr local, GLOBAL
+ * columns): the halos are the column ranges below row0 and above the block
+ * (a banded row block; columns in between are read from the owned x). */
+int ktb_halo_create_csr(int64_t n_global, int64_t row0, int64_t n_local, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* values, ktb_comm* comm, int kernel,
+                        int64_t param, ktb_halo** out);
+int ktb_halo_info(const ktb_halo* h, int64_t* n_local, int64_t* x_len, int64_t* owned_offset,
+                  int64_t* interior_begin, int64_t* interior_end, int64_t* nnz, int* launches);
+/* Rows and stored entries of the interior and boundary parts. */
+int ktb_halo_parts(const ktb_halo* h, int64_t* interior_rows, int64_t* interior_nnz,
+                   int64_t* boundary_rows, int64_t* boundary_nnz);
+/* y = A x (device pointers, asynchronous on stream). x has x_len entries with
+ * the owned ones at owned_offset; the halo entries are written by the
+ * exchange: one NCCL group (send owned edges, receive halos in place) on a
+ * high-priority communication stream, overlapped with the interior rows on
+ * `stream`; the boundary rows follow an event wait. */
+int ktb_halo_spmv(ktb_halo* h, double* x, double* y, void* stream);
+/* The exchange alone (stream waits for it). */
+int ktb_halo_exchange(ktb_halo* h, double* x, void* stream);
+/* y = A x from HOST memory (LinOp::apply contract, solver_types.hpp:17-20):
+ * x_owned (n_local, pinned for overlap) in, y (n_local) out, synchronous.
+ * The copies overlap inside the call: x goes host->device in `chunks` row
+ * chunks, each interior row chunk runs once the x chunks its columns reach
+ * have landed, and its y rows go device->host while later chunks compute;
+ * the halo exchange follows the last x chunk, the boundary rows run last. */
+int ktb_halo_spmv_host(ktb_halo* h, const double* x_owned, double* y, int chunks);
+/* Per-apply kernel timing (CUDA events on the apply's stream): after
+ * ktb_halo_set_timing(h, 1), ktb_halo_timing returns the device time of the
+ * last apply's interior rows and boundary rows (waits for them). */
+int ktb_halo_set_timing(ktb_halo* h, int on);
+int ktb_halo_timing(ktb_halo* h, double* interior_ms, double* boundary_ms);
+int ktb_halo_destroy(ktb_halo* h);
+
+/* ------------------------------- general split over a communicator */
+/* Attach a ktb_dist split to a communicator (collective): uploads to the
+ * comm's device, exchanges the ghost lists (all-gather of counts, grouped
+ * send/recv of the lists; replaces ktb_dist_set_sends) and builds the A_d
+ * plan (kernel/param; U1 param 100 falls back to U2 tiles when the
+ * warp-sliced copy is refused). */
+int ktb_dist_connect(ktb_dist* d, ktb_comm* comm, int kernel, int64_t param);
+/* Use a caller-owned plan for A_d (built on ktb_dist_local_matrix, e.g. by
+ * ktb_select); NULL restores zero-fill for an empty A_d. */
+int ktb_dist_set_plan(ktb_dist* d, ktb_plan* plan);
+/* y = A x over the row block (device pointers, asynchronous on stream):
+ * pack -> NCCL ghost exchange on the communication stream, overlapped with
+ * A_d x_owned -> y on `stream` -> y += A_o x_ghost after an event wait. */
+int ktb_dist_spmv(ktb_dist* d, const double* x_owned, double* y, void* stream);
+/* Pack + ghost exchange alone (stream waits for it). */
+int ktb_dist_exchange(ktb_dist* d, const double* x_owned, void* stream);
+int ktb_dist_launches(const ktb_dist* d, int* launches);
+/* The send lists in force (after ktb_dist_connect or ktb_dist_set_sends):
+ * per-peer counts (world) and the owned GLOBAL column ids in peer order. */
+int ktb_dist_sends(const ktb_dist* d, int64_t* send_counts, int64_t* send_cols);
+
 /* ------------------------------- distributed Krylov building blocks */
 /* Device BLAS-1 for GMRES over row-sharded vectors (dot / axpy / scal of
  * common.hpp:33-56 and the passes of ortho.hpp:55-111); the caller

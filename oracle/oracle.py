@@ -80,17 +80,31 @@ def lib():
     return _ora
 
 
-def ref_available() -> bool:
-    return os.path.exists(REF_SO)
+# The reference compiled three ways (oracle/Makefile): "parity" (-O2
+# -ffp-contract=off: bitwise with the restatement, the checker), "release"
+# (the reference's own CMake Release: -O3 -DNDEBUG) and "native" (Release +
+# -march=native); the last two are CPU baselines only.
+REF_VARIANTS = {"parity": REF_SO,
+                "release": os.path.join(HERE, "_ref", "libktune_ref_rel.so"),
+                "native": os.path.join(HERE, "_ref", "libktune_ref_native.so")}
+REF_FLAGS = {"parity": "g++ -O2 -std=c++20 -fopenmp -ffp-contract=off",
+             "release": "g++ -O3 -DNDEBUG -std=c++20 -fopenmp (the reference's CMake Release)",
+             "native": "g++ -O3 -DNDEBUG -march=native -std=c++20 -fopenmp"}
+_refs: dict = {}
 
 
-def ref():
+def ref_available(variant: str = "parity") -> bool:
+    return os.path.exists(REF_VARIANTS[variant])
+
+
+def ref(variant: str = "parity"):
     global _ref
-    if _ref is None:
-        if not os.path.exists(REF_SO):
-            raise FileNotFoundError(f"{REF_SO} missing: run `make -C oracle ref` where the "
+    if variant not in _refs:
+        path = REF_VARIANTS[variant]
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where the "
                                     "reference tree is present")
-        L = C.CDLL(REF_SO)
+        L = C.CDLL(path)
         L.kr_last_error.restype = C.c_char_p
         L.kr_validate.argtypes = [_I64, _i64p, _i64p, _f64p, C.c_int]
         L.kr_spmv_ref.argtypes = [_I64, _i64p, _i64p, _f64p, _f64p, _f64p]
@@ -131,8 +145,14 @@ def ref():
         L.kr_mm_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.kr_mm_destroy.argtypes = [C.c_void_p]
         L.kr_mm_write.argtypes = [C.c_char_p, _I64, _i64p, _i64p, _f64p, C.c_int]
-        _ref = L
-    return _ref
+        L.kr_engine_create_stencil7.argtypes = [_I64, _I64, _I64, C.c_double, C.c_double,
+                                                C.c_int, C.POINTER(C.c_void_p)]
+        L.kr_engine_report.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int)]
+        _refs[variant] = L
+        if variant == "parity":
+            _ref = L
+    return _refs[variant]
 
 
 class OracleError(RuntimeError):
@@ -175,9 +195,9 @@ def ref_lanczos(n, rp, ci, v, k, m=30, tol=1e-8, max_iters=10000, ortho_kind=1, 
                                                 converged=bool(conv.value))
 
 
-def _chk_ref(rc: int) -> None:
+def _chk_ref(rc: int, L=None) -> None:
     if rc != 0:
-        raise OracleError(ref().kr_last_error().decode())
+        raise OracleError((L or ref()).kr_last_error().decode())
 
 
 def _csr(rp, ci, v):
@@ -539,26 +559,62 @@ class Ref:
 
 
 class RefEngine:
-    """The reference's tuned engine (select_spmv_* + Unsym/SymEngine::op)."""
+    """The reference's tuned engine (select_spmv_* + Unsym/SymEngine::op).
+    ``select_seconds`` is the wall time of the reference's selection (plan
+    builds + every candidate's warm-up and timed runs)."""
 
-    def __init__(self, sym, n, rp, ci, v, pool_size):
-        self._keep = _csr(rp, ci, v)
+    def __init__(self, sym, n, rp, ci, v, pool_size, variant="parity", _handle=None):
+        import time
+
+        self.variant = variant
+        self.L = ref(variant)
+        t0 = time.perf_counter()
+        if _handle is None:
+            self._keep = _csr(rp, ci, v)
+            h = C.c_void_p()
+            _chk_ref(self.L.kr_engine_create(1 if sym else 0, n, *self._keep, pool_size,
+                                             C.byref(h)), self.L)
+        else:
+            h = _handle
+        self.select_seconds = time.perf_counter() - t0
         self.n = n
-        h = C.c_void_p()
-        _chk_ref(ref().kr_engine_create(1 if sym else 0, n, *self._keep, pool_size, C.byref(h)))
+        self.nnz = int(rp[-1]) if rp is not None else None
         self.h = h
         name = C.create_string_buffer(8)
         jl, w, best = _I64(), C.c_int(), C.c_double()
-        ref().kr_engine_selected(h, name, C.byref(jl), C.byref(w), C.byref(best))
+        self.L.kr_engine_selected(h, name, C.byref(jl), C.byref(w), C.byref(best))
         self.selected = dict(name=name.value.decode(), jl=jl.value, workers=w.value,
                              best_seconds=best.value)
 
+    @classmethod
+    def stencil7(cls, nx, ny, nz, diag=6.0, off=-1.0, pool_size=1, variant="parity"):
+        """The engine over the 7-point stencil built in place by the shim
+        (kr_engine_create_stencil7): configs 1 and 4 at full size."""
+        import time
+
+        L = ref(variant)
+        h = C.c_void_p()
+        t0 = time.perf_counter()
+        _chk_ref(L.kr_engine_create_stencil7(nx, ny, nz, diag, off, pool_size, C.byref(h)), L)
+        e = cls(False, nx * ny * nz, None, None, None, pool_size, variant, _handle=h)
+        e.select_seconds = time.perf_counter() - t0
+        e.nnz = 7 * nx * ny * nz - 2 * (nx * ny + ny * nz + nx * nz)
+        return e
+
+    def report(self):
+        """The TuningReport candidates (autotune.hpp:216-259)."""
+        out = (_Cand * 64)()
+        n, sel = C.c_int(), C.c_int()
+        self.L.kr_engine_report(self.h, out, 64, C.byref(n), C.byref(sel))
+        return [dict(name=c.name.decode(), jl=c.jl, workers=c.workers, correct=bool(c.correct),
+                     best_seconds=c.best_seconds) for c in out[:n.value]], sel.value
+
     def apply(self, x: np.ndarray, y: np.ndarray) -> None:
-        _chk_ref(ref().kr_engine_apply(self.h, x.ctypes.data, y.ctypes.data))
+        _chk_ref(self.L.kr_engine_apply(self.h, x.ctypes.data, y.ctypes.data), self.L)
 
     def close(self):
         if self.h:
-            ref().kr_engine_destroy(self.h)
+            self.L.kr_engine_destroy(self.h)
             self.h = None
 
     def __del__(self):

@@ -295,6 +295,74 @@ int kr_engine_create(int sym, int64_t n, const int64_t* rp, const int64_t* ci, c
     });
 }
 
+// The same engine over the 3-D 7-point stencil (configs 1 and 4) built in
+// place as a ktune::CsrMatrix by all threads: no host copy of a 16 GB int64
+// CRS through Python (bench.py's full 512^3 reference arm). Input recipe
+// index (z*ny + y)*nx + x, columns sorted -z,-y,-x,diag,+x,+y,+z.
+int kr_engine_create_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, double off,
+                              int pool_size, kr_engine** out) {
+    return guarded([&] {
+        auto e = std::make_unique<kr_engine>();
+        const int64_t n = nx * ny * nz, plane = nx * ny;
+        CsrMatrix& a = e->a;
+        a.n = n;
+        a.row_ptr.assign(n + 1, 0);
+        auto count = [&](int64_t i) {
+            const int64_t z = i / plane, r = i % plane, y = r / nx, x = r % nx;
+            return int64_t(1) + (z > 0) + (y > 0) + (x > 0) + (x < nx - 1) + (y < ny - 1) +
+                   (z < nz - 1);
+        };
+        const int T = std::max(1, pool_size);  // OMP_NUM_THREADS may be 1 (torchrun)
+        std::vector<int64_t> part(T + 1, 0);
+#pragma omp parallel num_threads(T)
+        {
+            const int t = omp_get_thread_num();
+            const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+            int64_t acc = 0;
+            for (int64_t i = lo; i < hi; ++i) acc += count(i);
+            part[t + 1] = acc;
+#pragma omp barrier
+#pragma omp single
+            for (int k = 0; k < T; ++k) part[k + 1] += part[k];
+            acc = part[t];
+            for (int64_t i = lo; i < hi; ++i) {
+                a.row_ptr[i] = acc;
+                acc += count(i);
+            }
+        }
+        a.row_ptr[n] = part[T];
+        a.col_idx.resize(a.row_ptr[n]);
+        a.values.resize(a.row_ptr[n]);
+#pragma omp parallel for schedule(static) num_threads(T)
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t z = i / plane, r = i % plane, y = r / nx, x = r % nx;
+            int64_t k = a.row_ptr[i];
+            auto put = [&](int64_t c, double val) {
+                a.col_idx[k] = c;
+                a.values[k++] = val;
+            };
+            if (z > 0) put(i - plane, off);
+            if (y > 0) put(i - nx, off);
+            if (x > 0) put(i - 1, off);
+            put(i, diag);
+            if (x < nx - 1) put(i + 1, off);
+            if (y < ny - 1) put(i + nx, off);
+            if (z < nz - 1) put(i + plane, off);
+        }
+        a.validate();
+        WorkerPool pool(pool_size);
+        auto [choice, rep] = select_spmv_unsym(e->a, pool);
+        e->rep = rep;
+        e->ue = std::make_unique<UnsymEngine>(e->a, choice);
+        e->op = e->ue->op();
+        *out = e.release();
+    });
+}
+
+void kr_engine_report(const kr_engine* e, kr_cand* out, int max_out, int* n_out, int* selected) {
+    export_report(e->rep, out, max_out, n_out, selected);
+}
+
 void kr_engine_selected(const kr_engine* e, char* name, int64_t* jl, int* workers,
                         double* best_seconds) {
     const auto& c = e->rep.selected_candidate();

@@ -67,6 +67,37 @@ def load() -> C.CDLL:
         "ktb_dist_local_matrix": ([VP, C.POINTER(VP)], C.c_int),
         "ktb_dist_pack": ([VP, VP, VP, VP], C.c_int),
         "ktb_dist_ghost_spmv": ([VP, VP, VP, VP], C.c_int),
+        "ktb_comm_id": ([VP], C.c_int),
+        "ktb_comm_create": ([VP, C.c_int, C.c_int, C.c_int, C.POINTER(VP)], C.c_int),
+        "ktb_comm_wrap": ([VP, C.c_int, C.POINTER(VP)], C.c_int),
+        "ktb_loopback_world_create": ([C.c_int, C.POINTER(VP)], C.c_int),
+        "ktb_loopback_world_destroy": ([VP], C.c_int),
+        "ktb_comm_create_loopback": ([VP, C.c_int, C.c_int, C.POINTER(VP)], C.c_int),
+        "ktb_comm_info": ([VP] + [C.POINTER(C.c_int)] * 5, C.c_int),
+        "ktb_comm_destroy": ([VP], C.c_int),
+        "ktb_comm_allreduce": ([VP, VP, I64, C.c_int, VP], C.c_int),
+        "ktb_comm_allgather": ([VP, VP, VP, C.c_size_t, VP], C.c_int),
+        "ktb_comm_sendrecv": ([VP, VP, C.c_size_t, C.c_int, VP, C.c_size_t, C.c_int, VP],
+                              C.c_int),
+        "ktb_halo_create": ([VP, I64, I64, VP, C.c_int, I64, C.POINTER(VP)], C.c_int),
+        "ktb_halo_create_stencil7": ([I64, I64, I64, C.c_double, C.c_double, VP, C.c_int, I64,
+                                      C.POINTER(VP)], C.c_int),
+        "ktb_halo_create_csr": ([I64, I64, I64, VP, VP, VP, VP, C.c_int, I64, C.POINTER(VP)],
+                                C.c_int),
+        "ktb_halo_info": ([VP] + [C.POINTER(I64)] * 6 + [C.POINTER(C.c_int)], C.c_int),
+        "ktb_halo_parts": ([VP] + [C.POINTER(I64)] * 4, C.c_int),
+        "ktb_halo_spmv": ([VP, VP, VP, VP], C.c_int),
+        "ktb_halo_exchange": ([VP, VP, VP], C.c_int),
+        "ktb_halo_spmv_host": ([VP, VP, VP, C.c_int], C.c_int),
+        "ktb_halo_destroy": ([VP], C.c_int),
+        "ktb_halo_set_timing": ([VP, C.c_int], C.c_int),
+        "ktb_halo_timing": ([VP, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+        "ktb_dist_connect": ([VP, VP, C.c_int, I64], C.c_int),
+        "ktb_dist_set_plan": ([VP, VP], C.c_int),
+        "ktb_dist_spmv": ([VP, VP, VP, VP], C.c_int),
+        "ktb_dist_exchange": ([VP, VP, VP], C.c_int),
+        "ktb_dist_launches": ([VP, C.POINTER(C.c_int)], C.c_int),
+        "ktb_dist_sends": ([VP, VP, VP], C.c_int),
         "ktb_gen_stencil7": ([I64, I64, I64, C.c_double, C.c_double, C.c_double, C.c_double,
                               C.c_int, C.POINTER(VP)], C.c_int),
         "ktb_gen_stencil27_upper": ([I64, I64, I64, C.c_double, C.c_double, C.c_int,

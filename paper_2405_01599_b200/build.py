@@ -8,15 +8,20 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, os.environ.get("KTB_LIB_NAME", "libktb.so"))
 SOURCES = ["ktb_api.cu", "ktb_build.cu", "ktb_unsym.cu", "ktb_sym.cu", "ktb_gen.cu", "ktb_gmres.cu",
-           "ktb_mm.cu", "ktb_dist.cu", "ktb_vec.cu",
+           "ktb_mm.cu", "ktb_dist.cu", "ktb_comm.cu", "ktb_vec.cu",
            "ktb_ilu.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL for the native halo / ghost exchange (ktb_comm.cu): the system headers
+# for the types; libnccl.so.2 itself is dlopen'ed at the first communicator
+# call (the copy torch already loaded, else the system library).
+NCCL_INC = os.environ.get("KTB_NCCL_INC", "/usr/include")
 
 
 def nvcc() -> str:
@@ -39,20 +44,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+    cmds, objs = [], []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
         obj = os.path.join(LIBDIR, os.path.basename(LIB) + "." + src.replace(".cu", ".o"))
         extra = os.environ.get("KTB_EXTRA_FLAGS", "").split()
-        cmd = [nvcc(), *ARCH, "-O3", *extra, "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
-               "-c", path, "-o", obj]
-        subprocess.run(cmd, check=True)
+        cmds.append([nvcc(), *ARCH, "-O3", *extra, "-lineinfo", "-std=c++17", "-Xcompiler",
+                     "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
+                     "-I", NCCL_INC, "-c", path, "-o", obj])
         objs.append(obj)
+    # translation units are independent: compile them concurrently
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.run, c, check=True) for c in cmds]:
+            f.result()
     tmp = LIB + ".tmp"
-    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

@@ -8,6 +8,8 @@
 #include <tuple>
 #include <vector>
 
+#include <functional>
+
 #include "ktb_internal.cuh"
 
 namespace ktb {
@@ -79,7 +81,8 @@ bool is_unsym_kernel(int k) { return k >= KTB_U1 && k <= KTB_U4; }
 // csr.hpp:38-54, same checks and messages, on the caller's host arrays.
 template <typename I>
 void validate_host(int64_t n, const I* rp, const I* ci, bool upper, int64_t* max_row,
-                   int64_t* bw) {
+                   int64_t* bw, int64_t ncols = -1) {
+    if (ncols < 0) ncols = n;
     require(n >= 0, "csr: negative dimension");
     require(rp != nullptr, "csr: row_ptr length != n+1");
     require(rp[0] == 0, "csr: row_ptr[0] != 0");
@@ -89,7 +92,7 @@ void validate_host(int64_t n, const I* rp, const I* ci, bool upper, int64_t* max
     for (int64_t i = 0; i < n; ++i) {
         require(rp[i] <= rp[i + 1], "csr: row_ptr not nondecreasing");
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-            require(ci[k] >= 0 && ci[k] < n, "csr: column index out of range");
+            require(ci[k] >= 0 && ci[k] < ncols, "csr: column index out of range");
             if (k > rp[i]) require(ci[k - 1] < ci[k], "csr: columns not strictly increasing");
             if (upper) require(ci[k] >= i, "sym csr: entry below the diagonal");
         }
@@ -102,10 +105,12 @@ void validate_host(int64_t n, const I* rp, const I* ci, bool upper, int64_t* max
 
 template <typename I>
 ktb_matrix* create_matrix(int64_t n, const I* rp, const I* ci, const double* v, int kind,
-                          int device) {
+                          int device, int64_t ncols = -1) {
     require(kind == KTB_GENERAL || kind == KTB_SYM_UPPER, "csr: bad matrix kind");
+    if (ncols < 0) ncols = n;
+    require(ncols < (int64_t(1) << 31) - 1, "csr: n or nnz >= 2^31 does not fit the int32 device layout");
     int64_t ml = 0, bw = 0;
-    validate_host(n, rp, ci, kind == KTB_SYM_UPPER, &ml, &bw);
+    validate_host(n, rp, ci, kind == KTB_SYM_UPPER, &ml, &bw, ncols);
     const int64_t nnz = rp[n];
     require(n < (int64_t(1) << 31) - 1 && nnz < (int64_t(1) << 31) - 1,
             "csr: n or nnz >= 2^31 does not fit the int32 device layout");
@@ -115,7 +120,7 @@ ktb_matrix* create_matrix(int64_t n, const I* rp, const I* ci, const double* v, 
         m->device = device;
         KTB_CUDA(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, device));
         m->n = n;
-        m->ncols = n;
+        m->ncols = ncols;
         m->nnz = nnz;
         m->kind = kind;
         m->max_row_nnz = ml;
@@ -140,6 +145,14 @@ ktb_matrix* create_matrix(int64_t n, const I* rp, const I* ci, const double* v, 
 
 }  // namespace
 
+int guarded_call(const std::function<void()>& f) { return guarded(f); }
+
+// A GENERAL n x ncols device matrix from int64 host CRS (halo row blocks).
+ktb_matrix* matrix_create_rect(int64_t n, int64_t ncols, const int64_t* rp, const int64_t* ci,
+                               const double* v, int device) {
+    return create_matrix(n, rp, ci, v, KTB_GENERAL, device, ncols);
+}
+
 // ---------------------------------------------------------------- dispatch
 void plan_setup(ktb_plan* p) {
     switch (p->kernel) {
@@ -152,6 +165,24 @@ void plan_setup(ktb_plan* p) {
         case KTB_S3: s3_setup(p); break;
         default: throw Invalid("spmv: unknown kernel");
     }
+}
+
+ktb_plan* plan_create_internal(ktb_matrix* m, int kernel, int64_t param, int workers,
+                               cudaStream_t stream) {
+    DeviceGuard g(m->device);
+    std::unique_ptr<ktb_plan> p(new ktb_plan());
+    p->m = m;
+    p->kernel = kernel;
+    p->param = param;
+    p->workers = workers > 0 ? workers : m->sm_count;
+    if (stream) {
+        p->stream = stream;
+    } else {
+        KTB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        p->own_stream = true;
+    }
+    if (m->n > 0) plan_setup(p.get());
+    return p.release();
 }
 
 void plan_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
@@ -571,25 +602,7 @@ int ktb_plan_create(ktb_matrix* m, int kernel, int64_t param, int workers, void*
             require(is_unsym_kernel(kernel), "spmv: unknown kernel");
         if (is_unsym_kernel(kernel))
             require(m->kind == KTB_GENERAL, "spmv: unsymmetric kernel on symmetric storage");
-        DeviceGuard g(m->device);
-        auto* p = new ktb_plan();
-        try {
-            p->m = m;
-            p->kernel = kernel;
-            p->param = param;
-            p->workers = workers > 0 ? workers : m->sm_count;
-            if (stream) {
-                p->stream = static_cast<cudaStream_t>(stream);
-            } else {
-                KTB_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-                p->own_stream = true;
-            }
-            if (m->n > 0) plan_setup(p);
-        } catch (...) {
-            delete p;
-            throw;
-        }
-        *out = p;
+        *out = plan_create_internal(m, kernel, param, workers, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "ktb_internal.cuh"
+#include "ktb_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -238,13 +239,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
     };
     const int64_t s0 = static_cast<int64_t>(blockIdx.x) * E * kRThreads;
     const int64_t s1 = min(n, s0 + static_cast<int64_t>(E) * kRThreads);
-    auto prefetch_col = [&](int col) {
-        const uint32_t bytes = static_cast<uint32_t>(((s1 - s0) * 8) & ~int64_t(15));
-        if (tid == 0 && bytes > 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                             V + static_cast<int64_t>(col) * n + s0),
-                         "r"(bytes)
-                         : "memory");
+    auto prefetch_col = [&](int col) {  // column starts are only 8-byte aligned for odd n
+        const double* c0 = V + static_cast<int64_t>(col) * n;
+        if (tid == 0 && s1 > s0) prefetch_l2_range(c0 + s0, c0 + s1);
     };
     if (k > 1) load_col(1);
     if (k > 2) prefetch_col(2);

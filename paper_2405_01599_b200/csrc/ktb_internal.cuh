@@ -1,6 +1,7 @@
 // ktb_internal.cuh -- shared internals of libktb (not part of the ABI).
 #pragma once
 
+#include <functional>
 #include <memory>
 
 #include <cuda_runtime.h>
@@ -127,6 +128,10 @@ struct ktb_csr_host {
     std::vector<double> val;
 };
 
+namespace ktb {
+void dist_comm_free(ktb_dist* d);  // ktb_comm.cu: the attached exchange state
+}
+
 // One rank's share of a row-block sharded CRS (ktb_dist.cu).
 struct ktb_dist {
     int64_t n_global = 0, row0 = 0, n_loc = 0;
@@ -145,7 +150,12 @@ struct ktb_dist {
     ktb::DBuf<int32_t> dev_orows, dev_orp, dev_oci, dev_send;
     ktb::DBuf<double> dev_ov;
     int lanes = 1;
-    ~ktb_dist() { delete local; }
+    // ktb_dist_connect: communicator, ghost / send buffers, A_d plan, streams
+    void* comm_state = nullptr;
+    ~ktb_dist() {
+        ktb::dist_comm_free(this);
+        delete local;
+    }
 };
 
 namespace ktb {
@@ -286,12 +296,18 @@ namespace ktb {
 void build_row_partition_dev(const ktb_matrix* m, int P, int scheme, int32_t* d_out,
                              cudaStream_t s);
 void plan_setup(ktb_plan* p);
+ktb_plan* plan_create_internal(ktb_matrix* m, int kernel, int64_t param, int workers,
+                               cudaStream_t stream);
 void plan_run(ktb_plan* p, const double* dx, double* dy, int64_t row_begin, int64_t row_end);
 void check_spmv_ref_order(const ktb_matrix* m, const double* dx, double* dy, cudaStream_t s);
 ktb_matrix* expand_symmetric_dev(const ktb_matrix* m, cudaStream_t s);
 void probe_vector_dev(int64_t n, double* d_out, cudaStream_t s);
 int outputs_match_dev(int64_t n, const double* dy, const double* dref, cudaStream_t s);
 void compute_matrix_stats(ktb_matrix* m, cudaStream_t s);
+
+// Runs f, mapping the exception types above to KTB_ERR_* and the thread's
+// ktb_last_error() message (ktb_api.cu).
+int guarded_call(const std::function<void()>& f);
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -75,6 +75,18 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// Bring the bytes [begin, end) into L2 for ANY addresses: the range is widened
+// to 16-byte boundaries (the bulk-prefetch alignment rule); the widened bytes
+// stay inside the allocation's 256-byte granule, so nothing unmapped is named.
+__device__ __forceinline__ void prefetch_l2_range(const void* begin, const void* end) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(begin) & ~uintptr_t(15);
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(end) + 15) & ~uintptr_t(15);
+    if (hi > lo)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo),
+                     "r"(static_cast<uint32_t>(hi - lo))
+                     : "memory");
+}
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -253,13 +253,10 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #define KTB_S3_AHEAD 2
 #endif
     constexpr int kAhead = KTB_S3_AHEAD;  // sub-tiles of look-ahead
-    auto pf = [&](int64_t lo, int64_t hi) {
-        lo = max(lo & ~int64_t(1), int64_t(0));
+    auto pf = [&](int64_t lo, int64_t hi) {  // x may be only 8-byte aligned (basis columns)
+        lo = max(lo, int64_t(0));
         hi = min(hi, int64_t(n));
-        if (hi > lo) {
-            const int64_t cnt = ((hi - lo) + 1) & ~int64_t(1);
-            prefetch_l2_bulk(x + lo, static_cast<uint32_t>(cnt * 8));
-        }
+        if (hi > lo) prefetch_l2_range(x + lo, x + hi);
     };
     if (tid == 0) {
         for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);

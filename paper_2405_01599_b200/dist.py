@@ -1,25 +1,28 @@
-"""Row-block (z-slab) sharding of the config-4 SpMV across GPUs with a
-one-plane x halo exchanged by NCCL point-to-point.
+"""Row-block sharding of SpMV across GPUs: the
+Python face of libktb's native data plane (csrc/ktb_comm.cu).
 
 The reference has no distributed path; this is the B200
-framework's scale-out of spmv_unsym (spmv.hpp:111): rank r of P owns the
-z-planes [r*nz/P, (r+1)*nz/P) of the 3-D 7-point stencil, i.e. a contiguous
-row block, and y stays row-sharded (no reduction collective).
+framework's scale-out of spmv_unsym (spmv.hpp:111): each rank owns a
+contiguous row block and the same entries of x and y (y stays row-sharded:
+no reduction collective). Two operators, both native C++ behind the C ABI:
 
-Local x layout on each rank:  [halo_lo plane | owned planes | halo_hi plane]
-(end ranks omit the missing neighbour's plane). Local column index =
-global column - col_base, col_base = first owned row - (plane if halo_lo).
+* ``DistSpMV`` (config 4): z-slab of the 3-D 7-point stencil, local x laid
+  out [halo_lo plane | owned planes | halo_hi plane]; per apply one NCCL
+  group (send the owned edge planes, receive the halos in place) on a
+  high-priority stream, overlapped with the interior rows; the boundary
+  planes run after an event wait (ktb_halo_spmv).
+* ``DistCsrSpMV`` (any CRS): NNZ_BALANCED row blocks split into A_d (owned
+  columns, any tuned kernel) and A_o (ghost columns); ghost lists exchanged
+  once; per apply pack -> NCCL ghost exchange overlapped with A_d x ->
+  y += A_o x_ghost (ktb_dist_spmv).
 
-Per apply:
-  1. the two boundary planes of owned x are sent to the neighbours and the
-     halo planes received, as one batch of NCCL send/recv (batch_isend_irecv);
-  2. the interior rows (which touch no halo) run on the compute stream while
-     NCCL moves the halos over NVLink;
-  3. the compute stream waits for the exchange and runs the two boundary
-     planes.
+The communicator is ``Comm``: NCCL (``Comm.nccl``; torch.distributed only
+hands the unique id around) or, for single-GPU checks of the same native
+code, an in-process loopback world (``Comm.loopback`` + ``run_ranks``).
 
-Host-side layout logic (SlabLayout, halo_ops) is plain Python so the
-multi-rank protocol is testable on CPU with the gloo backend.
+``SlabLayout`` / ``halo_plan`` / ``halo_exchange`` / ``exchange_ghost_lists``
+restate the native protocol in Python over torch.distributed so that the
+multi-rank logic is testable on CPU ranks with the gloo backend.
 """
 from __future__ import annotations
 
@@ -146,73 +149,258 @@ def slab_csr_numpy(L: SlabLayout, diag=6.0, off=-1.0):
     return L.n_local, rp, ci, v
 
 
-class DistSpMV:
-    """Config-4 sharded SpMV on this rank's GPU (torch.distributed, NCCL).
-    The slab is split once into its interior rows (no halo columns) and the
-    boundary planes, each a device matrix with its own plan over the same
-    local x; both default to U1 over the warp-sliced copy (param 100)."""
+class Comm:
+    """ktb_comm: the native communicator of the data plane (include/ktb.h).
 
-    def __init__(self, nx, ny, nz, rank, world, device, seed=4, diag=6.0, off=-1.0,
-                 interior_kernel=0, interior_param=100, boundary_param=100):
+    NCCL (the product path): ``Comm.nccl(group, device)`` -- rank 0 draws
+    the NCCL unique id inside libktb, torch.distributed (any backend, here
+    only as the out-of-band channel) hands it to every rank, and every rank
+    calls ncclCommInitRank through ``ktb_comm_create``. ``Comm.loopback``:
+    W ranks inside one process (one host thread per rank) for single-GPU
+    checks of the native exchange code (see ktb_comm.cu)."""
+
+    def __init__(self, handle, keep=None):
+        import ctypes as C
+
+        from . import _lib
+        from .ktune import _check
+
+        self.h, self._keep, self._L, self._check = handle, keep, _lib.load(), _check
+        v = [C.c_int() for _ in range(5)]
+        _check(self._L.ktb_comm_info(self.h, *[C.byref(x) for x in v]))
+        self.world, self.rank, self.device, self.nccl_version, nccl = [x.value for x in v]
+        self.is_nccl = bool(nccl)
+
+    @classmethod
+    def nccl(cls, group=None, device=None) -> "Comm":
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .ktune import _check
+
+        L = _lib.load()
+        dev = torch.cuda.current_device() if device is None else int(device)
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(L.ktb_comm_id(uid))
+        if world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            C.memmove(uid, box[0], 128)
+        h = C.c_void_p()
+        _check(L.ktb_comm_create(uid, world, rank, dev, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def wrap(cls, nccl_comm_ptr: int, device: int = -1) -> "Comm":
+        """Borrow an existing ncclComm_t (e.g. ProcessGroupNCCL._comm_ptr())."""
+        import ctypes as C
+
+        from . import _lib
+        from .ktune import _check
+
+        h = C.c_void_p()
+        _check(_lib.load().ktb_comm_wrap(C.c_void_p(nccl_comm_ptr), device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def loopback(cls, world: int, device: int = 0) -> list:
+        import ctypes as C
+
+        from . import _lib
+        from .ktune import _check
+
+        L = _lib.load()
+        w = C.c_void_p()
+        _check(L.ktb_loopback_world_create(world, C.byref(w)))
+        keep = _LoopWorld(w)
+        out = []
+        for r in range(world):
+            h = C.c_void_p()
+            _check(L.ktb_comm_create_loopback(w, r, device, C.byref(h)))
+            out.append(cls(h, keep))
+        return out
+
+    def _stream(self, stream=None) -> int:
+        import torch
+
+        if stream is not None:
+            return int(stream)
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def allreduce(self, t, op: str = "sum", stream=None) -> None:
+        """In place over a float64 CUDA tensor (deterministic on loopback)."""
+        self._check(self._L.ktb_comm_allreduce(self.h, t.data_ptr(), t.numel(),
+                                               1 if op == "max" else 0, self._stream(stream)))
+
+    def allgather(self, send, recv, stream=None) -> None:
+        self._check(self._L.ktb_comm_allgather(self.h, send.data_ptr(), recv.data_ptr(),
+                                               send.numel() * send.element_size(),
+                                               self._stream(stream)))
+
+    def barrier(self) -> None:
+        """Host barrier: a one-element all-reduce, then wait for it."""
+        import torch
+
+        t = torch.zeros(1, dtype=torch.float64, device=f"cuda:{self.device}")
+        self.allreduce(t)
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.ktb_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _LoopWorld:
+    def __init__(self, h):
+        from . import _lib
+
+        self.h, self._L = h, _lib.load()
+
+    def __del__(self):
+        try:
+            self._L.ktb_loopback_world_destroy(self.h)
+        except Exception:
+            pass
+
+
+def run_ranks(world: int, fn):
+    """fn(rank) on `world` host threads at once (collective native calls on
+    loopback communicators); returns the results in rank order and re-raises
+    the first failure."""
+    import threading
+
+    out, errs = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            import torch
+
+            torch.cuda.set_device(0)
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001 (re-raised below)
+            errs[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
+class DistSpMV:
+    """Config-4 sharded SpMV on this rank's GPU, native end to end (ktb_halo:
+    the slab generated on the device, interior/boundary row plans, the NCCL
+    halo group on a high-priority stream overlapped with the interior rows).
+    Collective: every rank of ``comm`` constructs it together."""
+
+    def __init__(self, nx, ny, nz, comm: Comm, seed=4, diag=6.0, off=-1.0, kernel=0, param=100):
+        import ctypes as C
+
         import torch
 
         from . import _lib
-        from . import ktune as K
+        from .ktune import _check
 
-        self.L = slab_layout(nx, ny, nz, rank, world)
-        self.device = device
-        slab = K.stencil7_slab(nx, ny, nz, self.L.z0, self.L.z1, diag, off, device=device)
-        self._nnz = slab.nnz()
-        lo, hi = self.L.interior_rows()
-        self.parts = []  # (r0, r1, plan)
-        if hi > lo:
-            a = slab.slice_rows(lo, hi)
-            self.parts.append((lo, hi, K.DevicePlan(a, int(interior_kernel), int(interior_param))))
-        self.boundary = []
-        for b0, b1 in self.L.boundary_ranges():
-            a = slab.slice_rows(b0, b1)
-            self.boundary.append((b0, b1, K.DevicePlan(a, K.UnsymKernel.u1_row,
-                                                       int(boundary_param))))
-        del slab
-        self.x = torch.empty(self.L.x_local_len, dtype=torch.float64, device=f"cuda:{device}")
-        self.y = torch.empty(self.L.n_local, dtype=torch.float64, device=f"cuda:{device}")
-        owned = self.x[self.L.owned_offset:self.L.owned_offset + self.L.n_local]
-        rc = _lib.load().ktb_seeded_vector(self.L.n_local, seed, self.L.row0, owned.data_ptr(),
-                                           torch.cuda.current_stream(device).cuda_stream)
-        if rc != 0:
-            raise RuntimeError(_lib.load().ktb_last_error().decode())
+        self.comm, self._L, self._check = comm, _lib.load(), _check
+        self.L = slab_layout(nx, ny, nz, comm.rank, comm.world)
+        self.device = comm.device
+        h = C.c_void_p()
+        _check(self._L.ktb_halo_create_stencil7(nx, ny, nz, diag, off, comm.h, int(kernel),
+                                                int(param), C.byref(h)))
+        self.h = h
+        v = [C.c_int64() for _ in range(6)] + [C.c_int()]
+        _check(self._L.ktb_halo_info(self.h, *[C.byref(x) for x in v]))
+        (self.n_local, self.x_len, self.owned_offset, self.interior_begin, self.interior_end,
+         self._nnz, self._launches) = [x.value for x in v]
+        assert (self.n_local, self.x_len, self.owned_offset) == (
+            self.L.n_local, self.L.x_local_len, self.L.owned_offset)
+        dev = f"cuda:{self.device}"
+        self.x = torch.zeros(self.x_len, dtype=torch.float64, device=dev)
+        self.y = torch.empty(self.n_local, dtype=torch.float64, device=dev)
+        owned = self.x[self.owned_offset:self.owned_offset + self.n_local]
+        _check(self._L.ktb_seeded_vector(self.n_local, seed, self.L.row0, owned.data_ptr(),
+                                         torch.cuda.current_stream(self.device).cuda_stream))
 
     @property
     def nnz(self) -> int:
         return self._nnz
 
-    def _run(self, parts):
-        for r0, r1, plan in parts:
-            plan.apply(self.x, self.y[r0:r1])
+    def parts(self):
+        """(interior_rows, interior_nnz, boundary_rows, boundary_nnz)."""
+        import ctypes as C
 
-    def apply(self):
-        """One sharded y = A x with halo/interior overlap (see module doc)."""
-        reqs = halo_exchange(self.L, self.x)
-        self._run(self.parts)
-        for r in reqs:
-            r.wait()  # the current stream waits for the NCCL transfers
-        self._run(self.boundary)
+        v = [C.c_int64() for _ in range(4)]
+        self._check(self._L.ktb_halo_parts(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def _s(self, stream=None):
+        import torch
+
+        return int(stream) if stream is not None else \
+            torch.cuda.current_stream(self.device).cuda_stream
+
+    def apply(self, stream=None):
+        """One sharded y = A x (ktb_halo_spmv) on the current torch stream."""
+        self._check(self._L.ktb_halo_spmv(self.h, self.x.data_ptr(), self.y.data_ptr(),
+                                          self._s(stream)))
         return self.y
 
-    def exchange_only(self):
-        """The halo exchange of one apply alone (for timing it): the two
-        one-plane messages, waited on by the current stream."""
-        for r in halo_exchange(self.L, self.x):
-            r.wait()
+    def apply_host(self, x_owned, y, chunks: int = 16) -> None:
+        """y = A x with host arrays (owned x in, owned y out; pinned memory
+        for the in-call copy/compute overlap), synchronous
+        (ktb_halo_spmv_host)."""
+        x_owned, y = np.asarray(x_owned), np.asarray(y)
+        assert x_owned.dtype == np.float64 and y.dtype == np.float64
+        assert x_owned.shape == (self.n_local,) and y.shape == (self.n_local,)
+        assert x_owned.flags.c_contiguous and y.flags.c_contiguous
+        self._check(self._L.ktb_halo_spmv_host(self.h, x_owned.ctypes.data, y.ctypes.data,
+                                               int(chunks)))
 
-    def compute_local(self):
-        """The local rows only (halos assumed in place): interior + boundary."""
-        self._run(self.parts)
-        self._run(self.boundary)
-        return self.y
+    def exchange_only(self, stream=None):
+        """The halo exchange of one apply alone (ktb_halo_exchange)."""
+        self._check(self._L.ktb_halo_exchange(self.h, self.x.data_ptr(), self._s(stream)))
 
     def launches_per_apply(self) -> int:
-        return sum(p.launches for _, _, p in self.parts + self.boundary)
+        return self._launches
+
+    def set_timing(self, on: bool = True) -> None:
+        self._check(self._L.ktb_halo_set_timing(self.h, int(on)))
+
+    def last_times(self):
+        """(interior_ms, boundary_ms) of the last apply (set_timing first)."""
+        import ctypes as C
+
+        a, b = C.c_double(), C.c_double()
+        self._check(self._L.ktb_halo_timing(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.ktb_halo_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def local_exchange(layouts, xs) -> None:
@@ -231,8 +419,7 @@ def local_exchange(layouts, xs) -> None:
 # ======================================================================
 # General row-block sharding of an arbitrary CRS.
 # The split and ghost bookkeeping are native (libktb ktb_dist_*, host-only
-# until upload); this layer exchanges the ghost lists once and drives the
-# per-apply pack -> NCCL send/recv -> A_d x (overlapped) -> y += A_o x_g.
+# until upload); the exchange is native too (ktb_dist_connect/spmv).
 # ======================================================================
 def nnz_balanced_boundaries(row_ptr, world: int) -> np.ndarray:
     """partition.hpp:28-55 NNZ_BALANCED on host: boundary p is the smallest
@@ -334,8 +521,9 @@ class DistCsr:
 
 
 def exchange_ghost_lists(dc: DistCsr, group=None, device=None):
-    """Once per matrix: every rank learns which of its owned columns each peer
-    needs. Counts by all_gather (world x world), lists by one batch of
+    """Python restatement of ktb_dist_connect's list exchange over
+    torch.distributed (CPU gloo tests of the protocol): every rank learns
+    which of its owned columns each peer needs. Counts by all_gather (world x world), lists by one batch of
     point-to-point transfers. Returns (send_counts, send_cols)."""
     import torch
     import torch.distributed as dist
@@ -367,89 +555,75 @@ def exchange_ghost_lists(dc: DistCsr, group=None, device=None):
 
 
 class DistCsrSpMV:
-    """y = A x for an arbitrary CRS sharded by rows over the process group
-    (one rank per GPU, NCCL). x and y are row-sharded like A; the local
-    diagonal block runs the selected/tuned kernel, overlapped with the ghost
-    exchange; the off-diagonal block accumulates after it."""
+    """y = A x for an arbitrary CRS sharded by rows over a communicator (one
+    rank per GPU), native end to end: ktb_dist_connect exchanges the ghost
+    lists over the communicator once; every apply is ktb_dist_spmv (pack ->
+    grouped NCCL send/recv of the ghosts on a high-priority stream,
+    overlapped with the A_d plan -> y += A_o x_ghost). Collective: every rank
+    constructs it together. kernel None: A_d's plan comes from the selector
+    (select_spmv_unsym on device time) and is handed to the split."""
 
-    def __init__(self, n_global, boundaries, rank, world, row_ptr, col_idx, values, device,
-                 kernel=None, group=None, sends=None, dc=None):
-        import torch
+    def __init__(self, n_global, boundaries, comm: Comm, row_ptr=None, col_idx=None, values=None,
+                 kernel=None, param=0, dc=None):
+        import ctypes as C
 
         from . import ktune as K
 
-        self.dc = dc or DistCsr(n_global, boundaries, rank, world, row_ptr, col_idx, values)
-        if sends is None:
-            counts, cols = exchange_ghost_lists(self.dc, group, device)
-        else:  # precomputed (single-process emulation: local_send_lists)
-            counts, cols = sends
-        self.dc.set_sends(counts, cols)
-        self.device, self.group = device, group
-        self.A_d = self.dc.upload(device)
+        self.comm = comm
+        self.dc = dc or DistCsr(n_global, boundaries, comm.rank, comm.world, row_ptr, col_idx,
+                                values)
+        L, chk = self.dc._L, self.dc._check
+        k0, p0 = (0, 100) if kernel is None else (int(kernel), int(param))
+        chk(L.ktb_dist_connect(self.dc.h, comm.h, k0, p0))
+        self.device = comm.device
+        m = C.c_void_p()
+        chk(L.ktb_dist_local_matrix(self.dc.h, C.byref(m)))
+        self.A_d = K.DeviceCsr(m, False, owner=self.dc)
+        self.report = None
+        self.plan = None
         if kernel is None and self.A_d.nnz() > 0:
             choice, self.report = K.select_spmv_unsym(self.A_d)
             self.plan = choice.plan
-        else:
-            self.plan = K.DevicePlan(self.A_d, int(kernel if kernel is not None else 0))
-            self.report = None
-        dev = f"cuda:{device}"
-        self.xg = torch.zeros(max(self.dc.n_ghost, 1), dtype=torch.float64, device=dev)
-        self.send = torch.empty(max(int(counts.sum()), 1), dtype=torch.float64, device=dev)
-        self._ro, self._so = self.dc.recv_offsets(), self.dc.send_offsets()
+            chk(L.ktb_dist_set_plan(self.dc.h, self.plan.h))
+        # the lists the native connect derived (for reporting and parity tests)
+        cnt = np.empty(comm.world, np.int64)
+        chk(L.ktb_dist_sends(self.dc.h, cnt.ctypes.data, None))
+        cols = np.empty(max(int(cnt.sum()), 1), np.int64)
+        chk(L.ktb_dist_sends(self.dc.h, None, cols.ctypes.data))
+        self.dc.send_counts, self.dc.send_cols = cnt, cols[:int(cnt.sum())]
 
     @property
     def n_local(self) -> int:
         return self.dc.n_local
 
-    def _stream(self):
+    def _stream(self, stream=None):
         import torch
 
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return int(stream) if stream is not None else \
+            torch.cuda.current_stream(self.device).cuda_stream
 
-    def pack(self, x_owned) -> None:
-        self.dc._check(self.dc._L.ktb_dist_pack(self.dc.h, x_owned.data_ptr(),
-                                                self.send.data_ptr(), self._stream()))
-
-    def exchange(self):
-        import torch.distributed as dist
-
-        ops = []
-        for p in range(self.dc.world):
-            if p == self.dc.rank:
-                continue
-            if self.dc.send_counts[p]:
-                ops.append(dist.P2POp(dist.isend, self.send[self._so[p]:self._so[p + 1]], p,
-                                      self.group))
-            if self.dc.recv_counts[p]:
-                ops.append(dist.P2POp(dist.irecv, self.xg[self._ro[p]:self._ro[p + 1]], p,
-                                      self.group))
-        return dist.batch_isend_irecv(ops) if ops else []
-
-    def ghost_spmv(self, y) -> None:
-        self.dc._check(self.dc._L.ktb_dist_ghost_spmv(self.dc.h, self.xg.data_ptr(),
-                                                      y.data_ptr(), self._stream()))
-
-    def apply(self, x_owned, y):
-        """One sharded y = A x (torch CUDA tensors of length n_local)."""
-        self.pack(x_owned)
-        reqs = self.exchange()
-        if self.A_d.nnz() > 0:
-            self.plan.apply(x_owned, y)
-        else:
-            y.zero_()
-        for q in reqs:
-            q.wait()
-        self.ghost_spmv(y)
+    def apply(self, x_owned, y, stream=None):
+        """One sharded y = A x (CUDA tensors of length n_local)."""
+        self.dc._check(self.dc._L.ktb_dist_spmv(self.dc.h, x_owned.data_ptr(), y.data_ptr(),
+                                                self._stream(stream)))
         return y
 
-    def exchange_only(self, x_owned):
+    def exchange_only(self, x_owned, stream=None):
         """Pack + ghost exchange of one apply alone (for timing it)."""
-        self.pack(x_owned)
-        for q in self.exchange():
-            q.wait()
+        self.dc._check(self.dc._L.ktb_dist_exchange(self.dc.h, x_owned.data_ptr(),
+                                                    self._stream(stream)))
 
     def launches_per_apply(self) -> int:
-        return int(self.dc.send_counts.sum() > 0) + self.plan.launches + int(self.dc.ghost_rows > 0)
+        import ctypes as C
+
+        n = C.c_int()
+        self.dc._check(self.dc._L.ktb_dist_launches(self.dc.h, C.byref(n)))
+        return n.value
+
+    def kernel_name(self) -> str:
+        if self.plan is not None:
+            return "u%d" % (self.plan.kernel + 1)
+        return "u1/u2 default" if self.A_d.nnz() else "none"
 
 
 def local_send_lists(dcs):
@@ -469,18 +643,3 @@ def local_send_lists(dcs):
             cols.append(seg)
         out.append((counts, np.concatenate(cols) if cols else np.zeros(0, np.int64)))
     return out
-
-
-def local_ghost_exchange(spmvs, xs) -> None:
-    """Single-process stand-in for the per-apply exchange over all ranks'
-    DistCsrSpMV objects on one device (plain copies of the same slices)."""
-    for s, x in zip(spmvs, xs):
-        s.pack(x)
-    for s in spmvs:
-        r = s.dc.rank
-        for p in range(s.dc.world):
-            if p == r or not s.dc.recv_counts[p]:
-                continue
-            src = spmvs[p]
-            so = src._so
-            s.xg[s._ro[p]:s._ro[p + 1]] = src.send[so[r]:so[r + 1]]

@@ -36,7 +36,7 @@ def test_device_gmres_all_orthogonalisers(kind):
     n, rp, ci, v = matgen.stencil7(20, 18, 16, xp=-0.7, xm=-1.3)
     b = _b(n, rp, ci, v)
     bnd = D.nnz_balanced_boundaries(rp, 1)
-    op = D.DistCsrSpMV(n, bnd, 0, 1, rp, ci, v, 0)
+    op = D.DistCsrSpMV(n, bnd, D.Comm.nccl(device=0), rp, ci, v, kernel=0, param=100)
     res = KR.gmres_m_dist(op, torch.from_numpy(b).cuda(), m=30, tol=1e-8, max_iters=1000,
                           ortho=kind)
     assert res.converged and res.true_residual < 1e-8
