@@ -38,7 +38,7 @@ os.environ.setdefault("OMP_PLACES", "cores")
 # that bench.py re-emits on stderr and in the JSON line
 os.environ.setdefault("NCCL_DEBUG", "INFO")
 os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ktb_bench_nccl.%h.%p.log")
+os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/ktb_bench_nccl.{os.getpid()}.log")
 import socket  # noqa: E402
 import subprocess  # noqa: E402
 import sys  # noqa: E402
@@ -139,7 +139,12 @@ def peak_hbm() -> tuple[float, str]:
 
 def physical_cores() -> int:
     """Physical cores (distinct (physical id, core id) pairs, i.e. lscpu
-    sockets x cores per socket), bounded by this process's CPU affinity."""
+    sockets x cores per socket), bounded by the CPU affinity this process
+    started with (read at import, before CUDA/NCCL touch any thread mask)."""
+    return _PHYS_CORES
+
+
+def _physical_cores() -> int:
     try:
         pairs, cur = set(), {}
         with open("/proc/cpuinfo") as f:
@@ -157,6 +162,9 @@ def physical_cores() -> int:
     except OSError:
         n = os.cpu_count() or 1
     return max(1, min(n, len(os.sched_getaffinity(0))))
+
+
+_PHYS_CORES = _physical_cores()
 
 
 def dist_env():
@@ -237,7 +245,7 @@ class Control:
 def nccl_init_lines() -> list[str]:
     """This process's NCCL communicator-init lines (NCCL_DEBUG=INFO, INIT)."""
     path = os.environ.get("NCCL_DEBUG_FILE", "")
-    path = path.replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
+    path = path.replace("%h", socket.gethostname().split(".")[0]).replace("%p", str(os.getpid()))
     try:
         with open(path) as f:
             return [ln.strip() for ln in f if "Init COMPLETE" in ln or "nRanks" in ln]
@@ -335,28 +343,25 @@ def _engine_desc(eng) -> dict:
                             "correct": c["correct"]} for c in cands]}
 
 
-def cpu_baseline(cfg, variant="release", seconds=10.0):
-    from oracle import oracle as O
-
+def cpu_baseline(args, seconds=10.0):
+    """The reference arm (`--impl reference`) in a FRESH process: no CUDA or
+    NCCL state (NCCL pins the calling thread's CPU affinity during
+    communicator init, which would squeeze the OpenMP pool onto one core),
+    timing as many applies as fit in `seconds` on every physical core."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK",
+                        "MASTER_ADDR", "MASTER_PORT", "TORCHELASTIC_RUN_ID", "OMP_NUM_THREADS")}
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference",
+           "--config", str(args.config), "--steps", "3", "--warmup", "1",
+           "--ref-build", args.ref_build, "--ref-seconds", str(seconds)]
     try:
-        eng, x, cores = reference_engine(cfg, variant)
-        y = np.empty(eng.n)
-        eng.apply(x, y)  # warm
-        ts = []
-        t_end = time.perf_counter() + seconds
-        while len(ts) < 3 or time.perf_counter() < t_end:
-            t0 = time.perf_counter()
-            eng.apply(x, y)
-            ts.append(time.perf_counter() - t0)
-        t = float(np.mean(ts))
-        nnz = cfg.get("nnz") or eng.nnz
-        return {"value": min_bytes(eng.n, nnz) / t / 1e9, "unit": "GB/s", "cores": cores,
-                "kind": "reference",
-                "sample": f"{len(ts)} applies ({sum(ts):.1f} s) of {cfg['sample']} through the "
-                          f"reference's tuned engine ({eng.selected['name']}, "
-                          f"{eng.selected['workers']} OpenMP workers)",
-                "ms_per_apply": t * 1e3, "build": O.REF_FLAGS[variant], "binding": REF_BINDING,
-                **_engine_desc(eng)}
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+        line = next(json.loads(ln) for ln in reversed(out.stdout.splitlines())
+                    if ln.startswith("{"))
+        cb = dict(line["cpu_baseline"])
+        cb["ms_per_apply"] = line["ms_per_step"]
+        cb["sample"] = cb["sample"].replace("rank 0 only", "a fresh process")
+        return cb
     except Exception as e:  # report, never fail the GPU line
         return {"value": None, "unit": "GB/s", "cores": physical_cores(), "kind": "reference",
                 "sample": f"unavailable: {e}"}
@@ -392,7 +397,8 @@ def run_reference(args, cfg):
     for _ in range(args.warmup):
         eng.apply(x, y)
     ts = []
-    for _ in range(args.steps):
+    t_end = time.perf_counter() + (args.ref_seconds or 0.0)
+    while len(ts) < args.steps or (args.ref_seconds and time.perf_counter() < t_end):
         t0 = time.perf_counter()
         eng.apply(x, y)
         ts.append(time.perf_counter() - t0)
@@ -400,7 +406,7 @@ def run_reference(args, cfg):
     gbs = B / t / 1e9
     line = {
         "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "steps": len(ts), "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong" if args.config == 4 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8d recipe, seeded)",
@@ -409,7 +415,7 @@ def run_reference(args, cfg):
         "impl": "reference",
         "gflops": flops(n, nnz, cfg["sym"]) / t / 1e9,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} applies of {cfg['sample']} ({cfg['workload']}) "
+                         "sample": f"{len(ts)} applies of {cfg['sample']} ({cfg['workload']}) "
                                    f"through the reference's tuned engine "
                                    f"({eng.selected['name']}, {eng.selected['workers']} OpenMP "
                                    f"workers); rank 0 only",
@@ -527,7 +533,7 @@ def run_gpu(args, cfg):
                            "correct": c.correct} for c in r["rep"].candidates],
         }
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, args.ref_build)
+            line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line))
     ctl.close()
     return 0
@@ -676,7 +682,7 @@ def run_halo(args, cfg):
             if not args.no_secondary:
                 line["secondary"] = secondary_cfg2(local, args)
             if not args.no_cpu_baseline:
-                line["cpu_baseline"] = cpu_baseline(cfg, args.ref_build)
+                line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line))
     shard.close()
     comm.close()
@@ -990,6 +996,8 @@ def main():
                          "(oracle/Makefile): the reference's CMake Release (default), "
                          "+ -march=native, or the -ffp-contract=off parity build")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=0.0,
+                    help=argparse.SUPPRESS)  # cpu_baseline: time applies for this long
     ap.add_argument("--no-secondary", action="store_true",
                     help="config 4: skip the config-2 S3 extra key")
     ap.add_argument("--shard", action="store_true",

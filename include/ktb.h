@@ -169,6 +169,12 @@ int ktb_plan_destroy(ktb_plan* p);
 int ktb_plan_info(const ktb_plan* p, int* kernel, int64_t* param, int64_t* ctas,
                   int* launches_per_apply, int64_t* extra_bytes);
 int ktb_plan_set_stream(ktb_plan* p, void* stream);
+/* S3 layout facts: entries outside the shared-memory window (or on a
+ * congested slot), rows too long for the round layout -- both applied by the
+ * deterministic per-target patch pass (patch_rows targets) -- the spill
+ * doubles merged by the fixup, the window length and the SELL slots. */
+int ktb_plan_s3_info(const ktb_plan* p, int64_t* far_entries, int64_t* long_rows,
+                     int64_t* patch_rows, int64_t* spill_doubles, int* window, int64_t* slots);
 
 /* y = A*x. Replaces spmv_unsym (spmv.hpp:111-170) and spmv_sym
  * (spmv.hpp:180-234). ptr_kind KTB_PTR_DEVICE: x,y are device pointers, the

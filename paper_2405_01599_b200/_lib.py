@@ -118,6 +118,8 @@ def load() -> C.CDLL:
         "ktb_plan_info": ([VP, C.POINTER(C.c_int), C.POINTER(I64), C.POINTER(I64),
                            C.POINTER(C.c_int), C.POINTER(I64)], C.c_int),
         "ktb_plan_set_stream": ([VP, VP], C.c_int),
+        "ktb_plan_s3_info": ([VP] + [C.POINTER(I64)] * 4 + [C.POINTER(C.c_int),
+                                                            C.POINTER(I64)], C.c_int),
         "ktb_spmv": ([VP, VP, VP, C.c_int], C.c_int),
         "ktb_spmv_host_pipelined": ([VP, I64, VP, I64, VP, I64], C.c_int),
         "ktb_spmv_rows": ([VP, I64, I64, VP, VP], C.c_int),

@@ -626,6 +626,20 @@ int ktb_plan_info(const ktb_plan* p, int* kernel, int64_t* param, int64_t* ctas,
     });
 }
 
+int ktb_plan_s3_info(const ktb_plan* p, int64_t* far_entries, int64_t* long_rows,
+                     int64_t* patch_rows, int64_t* spill_doubles, int* window, int64_t* slots) {
+    return guarded([&] {
+        require(p != nullptr && p->kernel == KTB_S3, "plan: not an S3 plan");
+        const auto& L = p->sw;
+        if (far_entries) *far_entries = L.far;
+        if (long_rows) *long_rows = L.nlong;
+        if (patch_rows) *patch_rows = L.npatch;
+        if (spill_doubles) *spill_doubles = L.spill_total;
+        if (window) *window = L.window;
+        if (slots) *slots = L.padded;
+    });
+}
+
 int ktb_plan_set_stream(ktb_plan* p, void* stream) {
     return guarded([&] {
         if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);

@@ -229,10 +229,13 @@ struct SymWindowLayout {
     int fix_grid = 0;          // > 0: persistent fixup with this many blocks
     DBuf<int> flags;           // per CTA: epoch of its last published spill
     int epoch = 0;
-    DBuf<int32_t> long_rows;   // rows handled by the long-row path
-    int64_t nlong = 0;
-    DBuf<int32_t> far_i, far_j;
-    DBuf<double> far_v;
+    int64_t nlong = 0;         // rows too long for the round layout
+    // entries outside the window (far) and the long rows, as per-target
+    // contribution lists: y[t] += sum_k v_k x[src_k] in a fixed order, one
+    // warp per target row after the window pass (deterministic)
+    int64_t npatch = 0;        // target rows
+    DBuf<int32_t> patch_row, patch_rp, patch_src;
+    DBuf<double> patch_val;
 };
 
 }  // namespace ktb

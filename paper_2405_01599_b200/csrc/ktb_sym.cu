@@ -30,7 +30,9 @@
 #include <cstring>
 #include <vector>
 
+#include <atomic>
 #include <cstdlib>
+#include <thread>
 
 #include "ktb_internal.cuh"
 #include "ktb_ptx.cuh"
@@ -680,42 +682,28 @@ __global__ void __launch_bounds__(256) k_s3_fixup_persistent(
     }
 }
 
-// Rows too long for the round layout: a block per row, row-direction sum plus
-// transposed products with fp64 L2 atomics (after the main kernel wrote y).
-__global__ void __launch_bounds__(256) k_s3_long(const int32_t* __restrict__ rows,
-                                                 const int32_t* __restrict__ rp,
-                                                 const int32_t* __restrict__ col,
-                                                 const double* __restrict__ val,
-                                                 const double* __restrict__ x,
-                                                 double* __restrict__ y) {
-    const int32_t i = rows[blockIdx.x];
-    const double xi = x[i];
+// Entries the window pass leaves out (far from the window, congested slots)
+// and rows too long for the round layout, as per-target contribution lists:
+// one warp per target row sums its contributions lane-strided, reduces with
+// a fixed butterfly and adds once into y[t] (after the window pass and the
+// fixup): deterministic for any input.
+__global__ void __launch_bounds__(256) k_s3_patch(const int32_t* __restrict__ rows,
+                                                  const int32_t* __restrict__ rp,
+                                                  const int32_t* __restrict__ src,
+                                                  const double* __restrict__ val, int64_t m,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ y) {
+    const int64_t g = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= m) return;  // whole warps exit together
     double s = 0.0;
-    for (int32_t k = rp[i] + threadIdx.x; k < rp[i + 1]; k += blockDim.x) {
-        const int32_t j = col[k];
-        const double v = val[k];
-        s += v * x[j];
-        if (j != i) atomicAdd(y + j, v * xi);
-    }
-    __shared__ double red[8];
+    for (int32_t k = __ldg(rp + g) + lane; k < __ldg(rp + g + 1); k += 32)
+        s += __ldg(val + k) * __ldg(x + __ldg(src + k));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
-        atomicAdd(y + i, t);
-    }
-}
-
-__global__ void k_s3_far(const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
-                         const double* __restrict__ fv, int64_t count,
-                         const double* __restrict__ x, double* __restrict__ y) {
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t < count) {  // an out-of-window entry: both of its products
-        atomicAdd(y + fi[t], fv[t] * x[fj[t]]);
-        atomicAdd(y + fj[t], fv[t] * x[fi[t]]);
+    if (lane == 0) {
+        const int32_t t = __ldg(rows + g);
+        y[t] = y[t] + s;
     }
 }
 
@@ -756,23 +744,27 @@ void s3_setup(ktb_plan* p) {
     L.window = static_cast<int>(W);
     L.reach = static_cast<int>(std::min<int64_t>(reach, W));
 
-    std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
-    std::vector<char> sub_nobar;  // per chunk in SELL order: no barrier after it
-    std::vector<int64_t> sub_base;
-    std::vector<unsigned char> sell;  // chunk-interleaved SELL stream
-    int64_t nchunks = 0;
-    std::vector<double> sdiag(n, 0.0);  // dense diagonal stream
-    std::vector<int32_t> spill_hi(P), far_i, far_j;
-    std::vector<double> far_v;
-    std::vector<uint64_t> colmask(static_cast<size_t>(W), 0);
-    std::vector<int32_t> touched, long_rows;
-    // rows longer than this go to the long-row path (their own block, atomics)
+    // Per block (independent given the bit-exact boundaries): colour each
+    // sub-tile's entries into rounds and lay out its round-chunks. Blocks run
+    // on all host cores; the merge below concatenates them in block order, so
+    // the layout is identical for any thread count.
+    struct BlockOut {
+        std::vector<int32_t> rounds;      // per sub-tile
+        std::vector<char> nobar;          // per chunk: no barrier after it
+        std::vector<unsigned char> sell;  // the block's round-chunks
+        std::vector<int32_t> far_i, far_j, long_rows;
+        std::vector<double> far_v;
+        int32_t spill_hi = 0;
+        int64_t slots = 0;
+    };
+    std::vector<double> sdiag(n, 0.0);  // dense diagonal stream (rows disjoint per block)
+    std::vector<BlockOut> outs(P);
+    // rows longer than this go to the long-row path
     const double mean = n ? double(nnz) / double(n) : 1.0;
     const int64_t long_len = std::max<int64_t>(32, std::min<int64_t>(kS3RoundCap, 4 * mean + 8));
-    int64_t total_slots = 0;
-    for (int c = 0; c < P; ++c) {
+    auto do_block = [&](int c, std::vector<uint64_t>& colmask, std::vector<int32_t>& touched) {
+        BlockOut& o = outs[c];
         const int32_t R0 = bnd[c], R1 = bnd[c + 1];
-        cta_sub[c] = static_cast<int32_t>(sub_rounds.size());
         int32_t hi = R1;
         for (int32_t a = R0; a < R1; a += S) {
             const int32_t rows = std::min<int32_t>(S, R1 - a);
@@ -784,7 +776,7 @@ void s3_setup(ktb_plan* p) {
             for (int32_t t = 0; t < rows; ++t) {
                 const int32_t i = a + t;
                 if (rp[i + 1] - rp[i] > long_len) {
-                    long_rows.push_back(i);
+                    o.long_rows.push_back(i);
                     continue;
                 }
                 uint64_t rowmask = 0;
@@ -794,32 +786,24 @@ void s3_setup(ktb_plan* p) {
                         sdiag[i] = val[k];
                         continue;
                     }
-                    const bool scatter = true;
-                    bool far = scatter && (static_cast<int64_t>(j) - a >= W);
-                    uint64_t* cm = (scatter && !far) ? &colmask[static_cast<size_t>(j - a)]
-                                                     : nullptr;
+                    bool far = static_cast<int64_t>(j) - a >= W;
+                    uint64_t* cm = !far ? &colmask[static_cast<size_t>(j - a)] : nullptr;
                     uint64_t busy = rowmask | (cm ? *cm : 0);
                     if (!~busy) {  // slot congested: scatter through the far path
                         far = true;
                         cm = nullptr;
-                        busy = rowmask;
+                    }
+                    if (far) {  // handled entirely by the patch pass (row and transposed)
+                        o.far_i.push_back(i);
+                        o.far_j.push_back(j);
+                        o.far_v.push_back(val[k]);
+                        continue;
                     }
                     const int r = __builtin_ctzll(~busy);
                     rowmask |= 1ull << r;
-                    if (cm) {
-                        if (!*cm) touched.push_back(j - a);
-                        *cm |= 1ull << r;
-                        hi = std::max<int32_t>(hi, j + 1);
-                    }
-                    if (far) {
-                        far_i.push_back(i);
-                        far_j.push_back(j);
-                        far_v.push_back(val[k]);
-                    }
-                    if (far) {  // handled entirely by the far path (row and transposed)
-                        rowmask &= ~(1ull << r);
-                        continue;
-                    }
+                    if (!*cm) touched.push_back(j - a);
+                    *cm |= 1ull << r;
+                    hi = std::max<int32_t>(hi, j + 1);
                     assign[t].push_back({r, k});
                     R = std::max(R, r + 1);
                 }
@@ -842,7 +826,6 @@ void s3_setup(ktb_plan* p) {
             for (int32_t sl : touched) colmask[static_cast<size_t>(sl)] = 0;
             R = std::max(R, 1);  // every sub-tile is one pipeline item at least
             std::vector<int> order, pos_of(R, -1);
-            std::vector<char> paired(R, 0), nobar;
             for (int r = 0; r < R; ++r) {
                 if (pos_of[r] >= 0) continue;
                 int mate = -1;
@@ -854,37 +837,75 @@ void s3_setup(ktb_plan* p) {
                         }
                 pos_of[r] = static_cast<int>(order.size());
                 order.push_back(r);
-                nobar.push_back(mate >= 0 ? 1 : 0);
+                o.nobar.push_back(mate >= 0 ? 1 : 0);
                 if (mate >= 0) {
                     pos_of[mate] = static_cast<int>(order.size());
                     order.push_back(mate);
-                    nobar.push_back(0);
+                    o.nobar.push_back(0);
                 }
             }
-            sub_nobar.insert(sub_nobar.end(), nobar.begin(), nobar.end());
-            const int64_t basei = static_cast<int64_t>(nchunks);  // in chunks
-            sub_base.push_back(basei);
-            sub_rounds.push_back(R);
-            nchunks += R;
-            if (sell.size() < static_cast<size_t>(nchunks) * kStageBytes) {
-                const size_t old_sz = sell.size();
-                sell.resize(std::max(static_cast<size_t>(nchunks) * kStageBytes, 2 * old_sz));
-                // fresh chunks: values 0.0, columns -1 (padding)
-                for (size_t ch = old_sz / kStageBytes; ch < sell.size() / kStageBytes; ++ch) {
-                    std::memset(&sell[ch * kStageBytes], 0, kRows * 8);
-                    std::memset(&sell[ch * kStageBytes + kRows * 8], 0xff, kRows * 2);
-                }
+            const size_t basei = o.sell.size() / kStageBytes;  // in chunks, block-local
+            o.rounds.push_back(R);
+            o.sell.resize((basei + R) * kStageBytes);
+            for (size_t ch = basei; ch < basei + R; ++ch) {  // values 0.0, columns -1 (padding)
+                std::memset(&o.sell[ch * kStageBytes], 0, kRows * 8);
+                std::memset(&o.sell[ch * kStageBytes + kRows * 8], 0xff, kRows * 2);
             }
             for (int32_t t = 0; t < rows; ++t)
                 for (auto [r, k] : assign[t]) {
-                    unsigned char* ch = &sell[static_cast<size_t>(basei + pos_of[r]) * kStageBytes];
+                    unsigned char* ch = &o.sell[(basei + pos_of[r]) * kStageBytes];
                     reinterpret_cast<double*>(ch)[s3_val_pos(t)] = val[k];
                     reinterpret_cast<int16_t*>(ch + kRows * 8)[s3_col_pos(t)] =
                         static_cast<int16_t>(col[k] - a);  // < W <= 32767
                 }
-            total_slots += static_cast<int64_t>(R) * S;
+            o.slots += static_cast<int64_t>(R) * S;
         }
-        spill_hi[c] = hi;
+        o.spill_hi = hi;
+    };
+    {
+        const int T = std::max(1, std::min<int>(P, static_cast<int>(std::thread::hardware_concurrency())));
+        std::atomic<int> next{0};
+        auto worker = [&] {
+            std::vector<uint64_t> colmask(static_cast<size_t>(W), 0);
+            std::vector<int32_t> touched;
+            for (int c; (c = next.fetch_add(1)) < P;) do_block(c, colmask, touched);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < T; ++t) pool.emplace_back(worker);
+        worker();
+        for (auto& t : pool) t.join();
+    }
+    // merge in block order
+    std::vector<int32_t> cta_sub(P + 1, 0), sub_rounds;
+    std::vector<char> sub_nobar;  // per chunk in SELL order: no barrier after it
+    std::vector<int64_t> sub_base;
+    std::vector<int32_t> spill_hi(P), far_i, far_j, long_rows;
+    std::vector<double> far_v;
+    int64_t nchunks = 0, total_slots = 0;
+    for (int c = 0; c < P; ++c) {
+        const BlockOut& o = outs[c];
+        cta_sub[c] = static_cast<int32_t>(sub_rounds.size());
+        for (int32_t R : o.rounds) {
+            sub_base.push_back(nchunks);
+            sub_rounds.push_back(R);
+            nchunks += R;
+        }
+        sub_nobar.insert(sub_nobar.end(), o.nobar.begin(), o.nobar.end());
+        far_i.insert(far_i.end(), o.far_i.begin(), o.far_i.end());
+        far_j.insert(far_j.end(), o.far_j.begin(), o.far_j.end());
+        far_v.insert(far_v.end(), o.far_v.begin(), o.far_v.end());
+        long_rows.insert(long_rows.end(), o.long_rows.begin(), o.long_rows.end());
+        spill_hi[c] = o.spill_hi;
+        total_slots += o.slots;
+    }
+    std::vector<unsigned char> sell(static_cast<size_t>(nchunks) * kStageBytes);
+    {
+        size_t pos = 0;
+        for (auto& o : outs) {
+            if (!o.sell.empty()) std::memcpy(&sell[pos], o.sell.data(), o.sell.size());
+            pos += o.sell.size();
+            std::vector<unsigned char>().swap(o.sell);
+        }
     }
     cta_sub[P] = static_cast<int32_t>(sub_rounds.size());
     // per-block chunk table: one entry per (sub-tile, round), in SELL order
@@ -988,11 +1009,44 @@ void s3_setup(ktb_plan* p) {
     up32(L.segs, segs);
     up32(L.seg_src, seg_src);
     up32(L.first_src, first_src);
-    up32(L.long_rows, long_rows);
+    // far entries (both products) and long rows (row sum incl. diagonal and
+    // transposed products) as contributions grouped by target row; the
+    // stable sort keeps each target's contributions in a fixed order
     L.nlong = static_cast<int64_t>(long_rows.size());
-    up32(L.far_i, far_i);
-    up32(L.far_j, far_j);
-    upd(L.far_v, far_v);
+    {
+        struct Contrib {
+            int32_t t, s;
+            double v;
+        };
+        std::vector<Contrib> cs;
+        for (size_t e = 0; e < far_i.size(); ++e) {
+            cs.push_back({far_i[e], far_j[e], far_v[e]});
+            cs.push_back({far_j[e], far_i[e], far_v[e]});
+        }
+        for (int32_t i : long_rows)
+            for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
+                cs.push_back({i, col[k], val[k]});
+                if (col[k] != i) cs.push_back({col[k], i, val[k]});
+            }
+        std::stable_sort(cs.begin(), cs.end(),
+                         [](const Contrib& a, const Contrib& b) { return a.t < b.t; });
+        std::vector<int32_t> prow, prp(1, 0), psrc(cs.size());
+        std::vector<double> pval(cs.size());
+        for (size_t e = 0; e < cs.size(); ++e) {
+            if (e == 0 || cs[e].t != cs[e - 1].t) {
+                if (e) prp.push_back(static_cast<int32_t>(e));
+                prow.push_back(cs[e].t);
+            }
+            psrc[e] = cs[e].s;
+            pval[e] = cs[e].v;
+        }
+        if (!cs.empty()) prp.push_back(static_cast<int32_t>(cs.size()));
+        L.npatch = static_cast<int64_t>(prow.size());
+        up32(L.patch_row, prow);
+        up32(L.patch_rp, prp);
+        up32(L.patch_src, psrc);
+        upd(L.patch_val, pval);
+    }
     upd(L.diag, sdiag);
     KTB_CUDA(cudaStreamSynchronize(st));
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1016,7 +1070,7 @@ void s3_setup(ktb_plan* p) {
             KTB_CUDA(cudaStreamSynchronize(st));
         }
     }
-    p->launches = 1 + (L.nsegs && !L.coop ? 1 : 0) + (L.far ? 1 : 0) + (L.nlong ? 1 : 0);
+    p->launches = 1 + (L.nsegs && !L.coop ? 1 : 0) + (L.npatch ? 1 : 0);
     // KTB_S3_FIXUP_GRID=1: persistent, two-deep fixup over the resident blocks
     // instead of one block per segment (measured 82.3 vs 80.3-80.9 us on
     // config 2: the per-segment blocks already fill the SMs as k_s3's CTAs
@@ -1092,15 +1146,9 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
                                     static_cast<const double*>(L.spill.p), y));
     }
 
-    if (L.nlong) {
-        const ktb_matrix* m = p->m;
-        k_s3_long<<<static_cast<int>(L.nlong), 256, 0, p->stream>>>(
-            L.long_rows.p, m->row_ptr.p, m->col.p, m->val.p, x, y);
-        KTB_LAUNCH();
-    }
-    if (L.far) {
-        k_s3_far<<<ceil_div(L.far, 256), 256, 0, p->stream>>>(L.far_i.p, L.far_j.p, L.far_v.p,
-                                                               L.far, x, y);
+    if (L.npatch) {
+        k_s3_patch<<<ceil_div(L.npatch, 8), 256, 0, p->stream>>>(
+            L.patch_row.p, L.patch_rp.p, L.patch_src.p, L.patch_val.p, L.npatch, x, y);
         KTB_LAUNCH();
     }
 }

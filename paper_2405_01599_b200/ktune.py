@@ -507,6 +507,16 @@ class DevicePlan:
         self.kernel, self.param, self.ctas = k.value, prm.value, ctas.value
         self.launches, self.extra_bytes = launches.value, extra.value
 
+    def s3_info(self) -> dict:
+        """S3 layout facts (ktb_plan_s3_info): far entries, long rows, patch
+        target rows, spill doubles, window length, SELL slots."""
+        v = [I64() for _ in range(4)]
+        w, slots = C.c_int(), I64()
+        _check(_lib.load().ktb_plan_s3_info(self.h, *[C.byref(q) for q in v], C.byref(w),
+                                            C.byref(slots)))
+        return dict(far=v[0].value, long_rows=v[1].value, patch_rows=v[2].value,
+                    spill=v[3].value, window=w.value, slots=slots.value)
+
     def set_stream(self, stream) -> None:
         _check(_lib.load().ktb_plan_set_stream(self.h, stream))
         self._stream = stream
