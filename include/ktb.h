@@ -129,6 +129,11 @@ int ktb_seeded_vector(int64_t n, uint64_t seed, int64_t offset, double* d_out, v
 /* partition.hpp:28-55 build_row_partition, computed on the device.
  * boundaries: host, num_workers+1 entries. */
 int ktb_row_partition(const ktb_matrix* m, int num_workers, int scheme, int64_t* boundaries);
+/* The same from a HOST int64 row_ptr (n+1 entries) -- the reference's
+ * build_row_partition(std::span<const index_t> row_ptr, P, scheme) form --
+ * computed on `device`. */
+int ktb_row_partition_rowptr(const int64_t* row_ptr, int64_t n, int num_workers, int scheme,
+                             int device, int64_t* boundaries);
 /* partition.hpp:73-96 build_reduction_regions for a SYM_UPPER matrix on the
  * given partition (host arrays, P = num_workers). */
 int ktb_reduction_regions(const ktb_matrix* m, int num_workers, const int64_t* boundaries,

@@ -109,6 +109,7 @@ def load() -> C.CDLL:
                              C.c_int),
         "ktb_gen_powerlaw_host": ([I64, C.c_uint64, I64, C.c_double, I64, VP, VP, VP], C.c_int),
         "ktb_row_partition": ([VP, C.c_int, C.c_int, VP], C.c_int),
+        "ktb_row_partition_rowptr": ([VP, I64, C.c_int, C.c_int, C.c_int, VP], C.c_int),
         "ktb_reduction_regions": ([VP, C.c_int, VP, VP, VP], C.c_int),
         "ktb_bss_plan_size": ([VP, I64, C.POINTER(I64), C.POINTER(I64)], C.c_int),
         "ktb_bss_plan_copy": ([VP, I64, VP, VP, VP, VP, VP, VP], C.c_int),

@@ -41,6 +41,8 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
 ktb_matrix* gen_powerlaw(int64_t n, uint64_t seed, int64_t target, double empty_frac,
                          int64_t max_len, int device);
 ktb_matrix* matrix_slice(const ktb_matrix* m, int64_t r0, int64_t r1);
+void build_row_partition_rowptr(const int64_t* h_rp, int64_t n, int P, int scheme, int device,
+                                int64_t* h_out);
 void powerlaw_host(int64_t n, uint64_t seed, int64_t target, double empty_frac,
                    int64_t max_len, std::vector<int64_t>& rp, std::vector<int32_t>* col,
                    std::vector<double>* val);
@@ -550,6 +552,17 @@ int ktb_row_partition(const ktb_matrix* m, int num_workers, int scheme, int64_t*
         std::vector<int32_t> h(num_workers + 1);
         KTB_CUDA(cudaMemcpy(h.data(), d.p, 4 * (num_workers + 1), cudaMemcpyDeviceToHost));
         for (int p = 0; p <= num_workers; ++p) boundaries[p] = h[p];
+    });
+}
+
+int ktb_row_partition_rowptr(const int64_t* row_ptr, int64_t n, int num_workers, int scheme,
+                             int device, int64_t* boundaries) {
+    return guarded([&] {
+        require(num_workers >= 1, "row partition: num_workers must be >= 1");
+        require(scheme == KTB_ROW_BASED || scheme == KTB_NNZ_BALANCED,
+                "row partition: bad scheme");
+        require(n >= 0 && row_ptr != nullptr, "csr: row_ptr length != n+1");
+        build_row_partition_rowptr(row_ptr, n, num_workers, scheme, device, boundaries);
     });
 }
 

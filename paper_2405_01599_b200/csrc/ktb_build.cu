@@ -22,14 +22,15 @@ namespace ktb {
 // partition.hpp:38-52. ROW_BASED: n*p/P. NNZ_BALANCED: smallest r in [0,n)
 // with row_ptr[r]*P >= p*nnz (std::lower_bound on [begin, end-1)), else n.
 // 64-bit products: p*nnz reaches 7*937,951,232 > 2^31 at config 4.
-__global__ void k_row_partition(const int32_t* __restrict__ rp, int64_t n, int P, int scheme,
-                                int32_t* __restrict__ out) {
+template <typename I, typename O>
+__global__ void k_row_partition(const I* __restrict__ rp, int64_t n, int P, int scheme,
+                                O* __restrict__ out) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p > P) return;
     if (p == 0) { out[0] = 0; return; }
-    if (p == P) { out[P] = static_cast<int32_t>(n); return; }
+    if (p == P) { out[P] = static_cast<O>(n); return; }
     if (scheme == KTB_ROW_BASED) {
-        out[p] = static_cast<int32_t>(n * p / P);
+        out[p] = static_cast<O>(n * p / P);
         return;
     }
     const int64_t nnz = rp[n];
@@ -45,13 +46,26 @@ __global__ void k_row_partition(const int32_t* __restrict__ rp, int64_t n, int P
             len = half;
         }
     }
-    out[p] = static_cast<int32_t>(lo);
+    out[p] = static_cast<O>(lo);
 }
 
 void build_row_partition_dev(const ktb_matrix* m, int P, int scheme, int32_t* d_out,
                              cudaStream_t s) {
     k_row_partition<<<ceil_div(P + 1, 256), 256, 0, s>>>(m->row_ptr.p, m->n, P, scheme, d_out);
     KTB_LAUNCH();
+}
+
+// The same rule over a caller's int64 row_ptr (the reference's
+// build_row_partition(std::span<const index_t> row_ptr, ...) signature):
+// uploaded once per call, int64 boundaries.
+void build_row_partition_rowptr(const int64_t* h_rp, int64_t n, int P, int scheme, int device,
+                                int64_t* h_out) {
+    DeviceGuard g(device);
+    DBuf<int64_t> rp(n + 1), out(P + 1);
+    KTB_CUDA(cudaMemcpy(rp.p, h_rp, 8 * (n + 1), cudaMemcpyHostToDevice));
+    k_row_partition<<<ceil_div(P + 1, 256), 256>>>(rp.p, n, P, scheme, out.p);
+    KTB_LAUNCH();
+    KTB_CUDA(cudaMemcpy(h_out, out.p, 8 * (P + 1), cudaMemcpyDeviceToHost));
 }
 
 // ------------------------------------------------------------------ regions

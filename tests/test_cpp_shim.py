@@ -40,3 +40,40 @@ def test_reference_gmres_runs_on_b200_engine():
     assert i["factors_bitwise"] == 1 and abs(i["gpu_iterations"] - i["ref_iterations"]) <= 2
     # ktb_cpp::load_matrix_market / write_matrix_market vs the reference's
     assert info["matrix_market"]["identical"] == 1
+
+
+REF_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "ref_api_drop_in")
+
+
+def test_ref_api_header_compiles_standalone(tmp_path):
+    """ktune_b200_ref.hpp (the kernel-level ktune signatures) needs only
+    ktb.h, ktune_b200.hpp and the C++20 standard library."""
+    gxx = shutil.which("g++") or "/usr/bin/g++"
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "ktune_b200_ref.hpp"\n'
+                   'int main() { ktb_ref::CsrMatrix a; ktb_ref::WorkerPool p(2);\n'
+                   '  std::vector<double> x, y; ktb_ref::RowPartition r;\n'
+                   '  if (a.n) ktb_ref::spmv_unsym(ktb_ref::UnsymKernel::u1_row, a, &r, nullptr,'
+                   ' x, y, p); return 0; }\n')
+    subprocess.run([gxx, "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                    str(src)], check=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_BIN),
+                    reason="kernel-level drop-in binary not built (needs reference headers)")
+def test_reference_call_sequences_with_namespace_changed():
+    """tests/cpp/ref_api_drop_in.cpp: meta.hpp:171-190 with ktune:: -> ktb_ref::
+    (both branches) feeding the reference's gmres_m (iterations +-2 vs the
+    unmodified sequence); spmv_unsym/spmv_sym with the reference signatures
+    (U1/U2 bitwise = spmv_ref, the rest within 1e-12 (|A||x|)_i); device
+    artefact builders bit-exact; the reference's error messages; one device
+    copy across 200 calls."""
+    out = subprocess.run([REF_BIN, "20"], capture_output=True, text=True, timeout=900)
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    info = {k: v for d in lines for k, v in d.items()}
+    assert out.returncode == 0 and info.get("ok") is True, out.stdout + out.stderr
+    for k in ("meta_stable", "meta_select"):
+        assert abs(info[k]["gpu_iterations"] - info[k]["ref_iterations"]) <= 2
+    assert info["messages"]["same"] == info["messages"]["cases"]
+    assert info["residency"]["after_200_calls"] == info["residency"]["device_matrices_before"]
