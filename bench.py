@@ -165,6 +165,9 @@ def _physical_cores() -> int:
 
 
 _PHYS_CORES = _physical_cores()
+# the CPU set this process started with: NCCL narrows a communicator-creating
+# thread's affinity, and a child would inherit the narrowed mask
+_AFFINITY0 = set(os.sched_getaffinity(0))
 
 
 def dist_env():
@@ -355,7 +358,8 @@ def cpu_baseline(args, seconds=10.0):
            "--config", str(args.config), "--steps", "3", "--warmup", "1",
            "--ref-build", args.ref_build, "--ref-seconds", str(seconds)]
     try:
-        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900,
+                             preexec_fn=lambda: os.sched_setaffinity(0, _AFFINITY0))
         line = next(json.loads(ln) for ln in reversed(out.stdout.splitlines())
                     if ln.startswith("{"))
         cb = dict(line["cpu_baseline"])

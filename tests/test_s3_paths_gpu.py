@@ -75,14 +75,13 @@ def test_far_entries_beyond_the_window():
 
 
 def test_congested_slot():
-    """Every row of the first tiles also touches column 3000: one window slot
-    targeted by far more than 64 rows of a sub-tile."""
-    n = 9000
+    """Every row of a 2048-row tile also touches one column just past the
+    tile: one window slot targeted by far more than 64 rows of a sub-tile
+    (n large enough that the 148 blocks hold whole sub-tiles)."""
+    n = 148 * 4096
     rows = []
     for i in range(n):
-        c = [i, min(i + 1, n - 1)]
-        if i < 3000:
-            c.append(3000)
+        c = [i, min(i + 1, n - 1), min((i // 2048) * 2048 + 2048 + 100, n - 1)]
         rows.append(np.unique(np.array(c, np.int64)))
     info = _run(n, *_sym_csr(n, rows)[1:])
     assert info["far"] > 0
