@@ -247,11 +247,14 @@ class Control:
 
 def nccl_init_lines() -> list[str]:
     """This process's NCCL communicator-init lines (NCCL_DEBUG=INFO, INIT)."""
+    import ctypes
+
+    ctypes.CDLL(None).fflush(None)  # NCCL's debug FILE is buffered
     path = os.environ.get("NCCL_DEBUG_FILE", "")
     path = path.replace("%h", socket.gethostname().split(".")[0]).replace("%p", str(os.getpid()))
     try:
         with open(path) as f:
-            return [ln.strip() for ln in f if "Init COMPLETE" in ln or "nRanks" in ln]
+            return [ln.strip() for ln in f if "Init COMPLETE" in ln or " nRanks " in ln]
     except OSError:
         return []
 

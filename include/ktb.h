@@ -156,13 +156,15 @@ int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
  *                per row over a warp-sliced (SELL-32/ELL) copy, bitwise equal
  *                to spmv_ref; 101 = the same over rows sorted by length (rows
  *                > 256 through U2 tiles on a side stream);
- *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8); 208/216 =
- *                the same with 16-byte vector loads; 300 = TMA-fed tiles;
+ *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8);
  *                104/108/112 = merge-path tiles;
  *            U3/U4: nonzeros per segment lane E in {4,8,16} (0 = 8); U3 1008
  *                = flag-driven warp-level BSS over 256-nonzero tiles;
  *            S1/S2: lanes per row (0 = auto); S3: 0 (2048-row sub-tiles).
  *            The selector (ktb_select) sweeps these; see INTEGRATION.md.
+ *            Bits 16..31 of param carry a launch shape (CTA threads; 0 =
+ *            default): U1 100/101 take 64/128/256, U2 warp tiles and U3 1008
+ *            take 128/256; the selector times each shape as a candidate.
  *   workers: the reference worker count P whose partition/regions the plan
  *            also materialises as artefacts (0 = engine default).
  *   stream:  cudaStream_t to run on (NULL = the plan creates its own). */
@@ -222,6 +224,8 @@ typedef struct {
     int n_trials;
     double best_seconds;
     double trial_seconds[8];
+    int cta_threads;       /* launch shape (CTA threads; 0 = the kernel's default) */
+    double setup_seconds;  /* plan build (host + device) before the warm-up */
 } ktb_candidate;
 
 /* select_spmv_unsym / select_spmv_sym (autotune.hpp:267-377) on device

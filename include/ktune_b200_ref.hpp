@@ -42,8 +42,8 @@
 // The integer artefacts (RowPartition, ReductionRegions, BssPlan) are built
 // by the device builders and are bit-exact with the reference's. They are
 // validated exactly as the reference validates them; the GPU kernels use
-// their own decomposition (CTAs, warp tiles, nonzeros per lane), so U1 and
-// U2 results are bitwise equal to spmv_ref and U3/U4/S1-S3 agree within
+// their own decomposition (CTAs, warp tiles, nonzeros per lane): U1 over the
+// warp-sliced copy is bitwise equal to spmv_ref, every kernel agrees within
 // 1e-12 (|A||x|)_i.
 #pragma once
 

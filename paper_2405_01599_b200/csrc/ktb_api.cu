@@ -157,6 +157,12 @@ ktb_matrix* matrix_create_rect(int64_t n, int64_t ncols, const int64_t* rp, cons
 
 // ---------------------------------------------------------------- dispatch
 void plan_setup(ktb_plan* p) {
+    // param = variant | (CTA threads << 16): the launch shape rides in the
+    // high bits so that a shape is an ordinary selector candidate
+    if (p->param >= (int64_t(1) << 16)) {
+        p->cta_threads = static_cast<int>((p->param >> 16) & 0xffff);
+        p->param &= 0xffff;
+    }
     switch (p->kernel) {
         case KTB_U1: u1_setup(p); break;
         case KTB_U2: u2_setup(p); break;
@@ -632,7 +638,10 @@ int ktb_plan_info(const ktb_plan* p, int* kernel, int64_t* param, int64_t* ctas,
                   int* launches_per_apply, int64_t* extra_bytes) {
     return guarded([&] {
         if (kernel) *kernel = p->kernel;
-        if (param) *param = p->kernel == KTB_U3 || p->kernel == KTB_U4 ? p->jl : p->param;
+        if (param)
+            *param = p->kernel == KTB_U3 || p->kernel == KTB_U4
+                         ? p->jl
+                         : p->param | (static_cast<int64_t>(p->cta_threads) << 16);
         if (ctas) *ctas = p->ctas;
         if (launches_per_apply) *launches_per_apply = p->launches;
         if (extra_bytes) *extra_bytes = p->extra_bytes;
@@ -819,11 +828,24 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
         ktb_select_opts opts{};
         if (opts_in) opts = *opts_in;
         const int trials = opts.timed_trials > 0 ? std::min(opts.timed_trials, 8) : 3;
+        // RAII for everything this call creates: a throw anywhere below
+        // (CUDA error, bad_alloc) leaks no plan, event or stream
+        struct StreamGuard {
+            cudaStream_t s = nullptr;
+            ~StreamGuard() {
+                if (s) cudaStreamDestroy(s);
+            }
+        } own;
+        struct EventGuard {
+            cudaEvent_t e = nullptr;
+            ~EventGuard() {
+                if (e) cudaEventDestroy(e);
+            }
+        } e0, e1;
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        cudaStream_t own = nullptr;
         if (!st) {
-            KTB_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
-            st = own;
+            KTB_CUDA(cudaStreamCreateWithFlags(&own.s, cudaStreamNonBlocking));
+            st = own.s;
         }
         const int64_t n = m->n;
         DBuf<double> x(n), ref(n), y(n);
@@ -842,54 +864,69 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
             ktb_candidate rep;
         };
         std::vector<Cand> list;
-        auto add = [&](int k, int64_t prm, const char* name, int ordinal) {
-            Cand c{k, prm, {}};
+        auto add = [&](int k, int64_t prm, const char* name, int ordinal, int threads = 0) {
+            Cand c{k, prm | (static_cast<int64_t>(threads) << 16), {}};
             std::strncpy(c.rep.name, name, 7);
             c.rep.ordinal = ordinal;
             c.rep.param = prm;  // replaced by the plan's resolved value once set up
             c.rep.workers = opts.workers > 0 ? opts.workers : m->sm_count;
             c.rep.best_seconds = std::numeric_limits<double>::infinity();
+            c.rep.cta_threads = threads;
             list.push_back(c);
         };
+        // the reference's candidate set (autotune.hpp:283-313: U1, U2, U3 x
+        // lane counts / S1, S2, S3) crossed with the GPU variants of each and
+        // their launch shapes -- the GPU form of the worker-count sweep
+        // (autotune.hpp:163, 206-212): CTA threads instead of OpenMP threads
         if (m->kind == KTB_SYM_UPPER) {
             add(KTB_S1, 0, "s1", 0);
             add(KTB_S2, 0, "s2", 1);
             add(KTB_S3, 0, "s3", 2);
         } else {
             add(KTB_U1, 0, "u1", 0);
-            add(KTB_U1, 100, "u1", 0);  // thread per row over the warp-sliced copy
-            add(KTB_U1, 101, "u1", 0);  // the same over rows sorted by length
-            add(KTB_U2, 0, "u2", 1);
+            for (int t : {128, 64, 256}) add(KTB_U1, 100, "u1", 0, t);  // warp-sliced copy
+            for (int t : {128, 64, 256}) add(KTB_U1, 101, "u1", 0, t);  // rows sorted by length
+            for (int t : {128, 256}) add(KTB_U2, 8, "u2", 1, t);         // warp tiles
+            add(KTB_U2, 108, "u2", 1);                                   // merge-path tiles
             std::vector<int64_t> ept = {4, 8, 16};
             if (opts.params && opts.n_params > 0) ept.assign(opts.params, opts.params + opts.n_params);
             for (int64_t e : ept)
                 if (m->nnz >= 4 * e) add(KTB_U3, e, "u3", 2);
-            add(KTB_U3, 1008, "u3", 2);  // warp-level flag-driven BSS tiles
+            for (int t : {128, 256}) add(KTB_U3, 1008, "u3", 2, t);  // warp-level BSS tiles
         }
-        std::vector<ktb_plan*> plans(list.size(), nullptr);
-        cudaEvent_t e0, e1;
-        KTB_CUDA(cudaEventCreate(&e0));
-        KTB_CUDA(cudaEventCreate(&e1));
+        KTB_CUDA(cudaEventCreate(&e0.e));
+        KTB_CUDA(cudaEventCreate(&e1.e));
+        // only the incumbent winner stays alive: candidates are timed one at
+        // a time and a loser's device copy is released at once, so selection
+        // holds at most two plans (pick_winner, autotune.hpp:242-259, applied
+        // incrementally -- the same lexicographic (best, ordinal, param,
+        // workers) order, earlier candidate kept on a full tie)
+        std::unique_ptr<ktb_plan> best_plan;
+        int best = -1;
+        auto better = [&](const ktb_candidate& c, const ktb_candidate& b) {
+            return std::make_tuple(c.best_seconds, c.ordinal, c.param, c.workers) <
+                   std::make_tuple(b.best_seconds, b.ordinal, b.param, b.workers);
+        };
         for (size_t ci = 0; ci < list.size(); ++ci) {
             auto& c = list[ci];
-            ktb_plan* p = nullptr;
+            std::unique_ptr<ktb_plan> p(new ktb_plan());
+            const auto t_setup = std::chrono::steady_clock::now();
             try {
-                p = new ktb_plan();
                 p->m = m;
                 p->kernel = c.kernel;
                 p->param = c.param;
                 p->workers = c.rep.workers;
                 p->stream = st;
-                plan_setup(p);
+                plan_setup(p.get());
             } catch (const Invalid&) {
-                delete p;  // layout not applicable: report as failing the check
-                c.rep.correct = 0;
+                c.rep.correct = 0;  // layout not applicable: reported as failing the check
                 continue;
             }
+            c.rep.setup_seconds =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_setup).count();
             c.rep.param = (c.kernel == KTB_U3) ? p->jl : p->param;
-            plans[ci] = p;
             // warm-up doubles as the correctness cross-check (autotune.hpp:226-229)
-            plan_run(p, x.p, y.p, 0, n);
+            plan_run(p.get(), x.p, y.p, 0, n);
             c.rep.executions = 1;
             c.rep.correct = outputs_match_dev(n, y.p, ref.p, st);
             if (!c.rep.correct) continue;
@@ -897,56 +934,40 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
                 double sec;
                 if (opts.now) {
                     const double tic = opts.now(opts.now_ctx);
-                    plan_run(p, x.p, y.p, 0, n);
+                    plan_run(p.get(), x.p, y.p, 0, n);
                     KTB_CUDA(cudaStreamSynchronize(st));
                     sec = opts.now(opts.now_ctx) - tic;
                 } else {
-                    KTB_CUDA(cudaEventRecord(e0, st));
-                    plan_run(p, x.p, y.p, 0, n);
-                    KTB_CUDA(cudaEventRecord(e1, st));
-                    KTB_CUDA(cudaEventSynchronize(e1));
+                    KTB_CUDA(cudaEventRecord(e0.e, st));
+                    plan_run(p.get(), x.p, y.p, 0, n);
+                    KTB_CUDA(cudaEventRecord(e1.e, st));
+                    KTB_CUDA(cudaEventSynchronize(e1.e));
                     float ms = 0.f;
-                    KTB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                    KTB_CUDA(cudaEventElapsedTime(&ms, e0.e, e1.e));
                     sec = ms * 1e-3;
                 }
                 ++c.rep.executions;
                 c.rep.trial_seconds[c.rep.n_trials++] = sec;
                 c.rep.best_seconds = std::min(c.rep.best_seconds, sec);
             }
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        // pick_winner: lexicographic (best, ordinal, param, workers)
-        int best = -1;
-        for (int i = 0; i < static_cast<int>(list.size()); ++i) {
-            const auto& c = list[i].rep;
-            if (!c.correct) continue;
-            if (best < 0) {
-                best = i;
-                continue;
+            if (best < 0 || better(c.rep, list[best].rep)) {
+                KTB_CUDA(cudaStreamSynchronize(st));
+                best = static_cast<int>(ci);
+                best_plan = std::move(p);  // the previous incumbent is released here
             }
-            const auto& b = list[best].rep;
-            if (std::make_tuple(c.best_seconds, c.ordinal, c.param, c.workers) <
-                std::make_tuple(b.best_seconds, b.ordinal, b.param, b.workers))
-                best = i;
         }
         if (n_cands) *n_cands = static_cast<int>(list.size());
         if (cands)
             for (int i = 0; i < static_cast<int>(list.size()) && i < max_cands; ++i)
                 cands[i] = list[i].rep;
-        for (size_t i = 0; i < plans.size(); ++i)
-            if (static_cast<int>(i) != best) delete plans[i];
-        if (best < 0) {
-            if (own) cudaStreamDestroy(own);
-            throw SelectError("kernel selection: every candidate failed the oracle check");
-        }
+        if (best < 0) throw SelectError("kernel selection: every candidate failed the oracle check");
         if (selected) *selected = best;
-        ktb_plan* w = plans[best];
-        if (own) {
-            w->stream = own;  // hand the private stream to the winner
-            w->own_stream = true;
+        if (own.s) {  // hand the private stream to the winner
+            best_plan->stream = own.s;
+            best_plan->own_stream = true;
+            own.s = nullptr;
         }
-        *winner = w;
+        *winner = best_plan.release();
     });
 }
 

@@ -219,16 +219,10 @@ struct SymWindowLayout {
     DBuf<int32_t> spill_hi;    // per CTA: end of its spill range (start = cta_row[c+1])
     DBuf<int64_t> spill_off;   // per CTA: offset into spill
     DBuf<double> spill;
-    DBuf<int32_t> head_end;    // per CTA: its head rows [cta_row[c], head_end[c]) get spills
     DBuf<int32_t> segs;        // fixup block descriptors (3 int4 each, see s3_setup)
     DBuf<int32_t> seg_src;     // per fixup block: its spilling sources, ascending
     int64_t nsegs = 0;
     int reach = 0;             // max(col - row), clipped to the window
-    DBuf<int32_t> first_src;   // per CTA: first source CTA spilling into it
-    bool coop = false;         // spills merged inside k_s3 (cooperative launch)
-    int fix_grid = 0;          // > 0: persistent fixup with this many blocks
-    DBuf<int> flags;           // per CTA: epoch of its last published spill
-    int epoch = 0;
     int64_t nlong = 0;         // rows too long for the round layout
     // entries outside the window (far) and the long rows, as per-target
     // contribution lists: y[t] += sum_k v_k x[src_k] in a fixed order, one
@@ -244,6 +238,7 @@ struct ktb_plan {
     ktb_matrix* m = nullptr;
     int kernel = KTB_U1;
     int64_t param = 0;
+    int cta_threads = 0;  // launch shape (param bits 16..31); 0 = the kernel's default
     int workers = 1;
     cudaStream_t stream = nullptr;
     bool own_stream = false;

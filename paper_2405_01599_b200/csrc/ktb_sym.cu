@@ -228,8 +228,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
          const int64_t* __restrict__ cta_base, const double* __restrict__ diag,
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
-         double* __restrict__ spill, int* __restrict__ flags, int epoch,
-         const int32_t* __restrict__ head_end, const int32_t* __restrict__ first_src) {
+         double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
@@ -456,79 +455,6 @@ __global__ void __launch_bounds__(kS3Threads, 1)
         for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
             st_hint_f64(spill + so + (j - R1), win[(j - R0) % W], keep);
     }
-    if (!flags) return;  // k_s3_fixup merges the spills
-    // In-kernel merge (cooperative launch: every block is resident). Publish
-    // this block's spill, wait for the blocks spilling into this one, then
-    // add their spills into the head rows [R0, head_end) -- the arithmetic of
-    // k_s3_fixup (sources ascending, y + (s_a + s_b + ...)), so y is the same
-    // bit for bit; all loads of a pass are in flight together.
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        st_release_gpu(flags + c, epoch);
-    }
-    const int32_t he = head_end[c];
-    if (he <= R0) return;
-    const int fs = first_src[c];
-    if (tid == 0)
-        for (int src = fs; src < c; ++src)
-            if (spill_hi[src] > R0)
-                while (ld_acquire_gpu(flags + src) != epoch) {
-                }
-    __syncthreads();
-    // the first two sources whose spill meets the head rows, inline
-    int sa = -1, sb = -1;
-    for (int src = fs; src < c; ++src)
-        if (spill_hi[src] > R0) {
-            if (sa < 0)
-                sa = src;
-            else if (sb < 0)
-                sb = src;
-        }
-    const int32_t a0 = sa >= 0 ? cta_row[sa + 1] : 0, a1 = sa >= 0 ? spill_hi[sa] : 0;
-    const int32_t b0 = sb >= 0 ? cta_row[sb + 1] : 0, b1 = sb >= 0 ? spill_hi[sb] : 0;
-    const double* spa = sa >= 0 ? spill + spill_off[sa] - a0 : spill;
-    const double* spb = sb >= 0 ? spill + spill_off[sb] - b0 : spill;
-#ifndef KTB_S3_MU
-#define KTB_S3_MU 14
-#endif
-    constexpr int MU = KTB_S3_MU;  // rows per thread per pass
-    for (int32_t j0 = R0; j0 < he; j0 += MU * kS3Threads) {
-        double yv[MU], va[MU], vb[MU];
-        bool tch[MU];
-#pragma unroll
-        for (int u = 0; u < MU; ++u) {
-            const int32_t j = j0 + u * kS3Threads + tid;
-            const bool in = j < he;
-            const bool ia = in && j >= a0 && j < a1;
-            const bool ib = in && j >= b0 && j < b1;
-            yv[u] = in ? __ldcg(y + j) : 0.0;
-            va[u] = ia ? __ldcg(spa + j) : 0.0;
-            vb[u] = ib ? __ldcg(spb + j) : 0.0;
-            tch[u] = ia || ib;
-        }
-        double acc[MU];
-#pragma unroll
-        for (int u = 0; u < MU; ++u) acc[u] = va[u] + vb[u];
-        for (int src = sb + 1; sb >= 0 && src < c; ++src) {  // more sources: rare
-            const int32_t s0 = cta_row[src + 1], shi = spill_hi[src];
-            if (shi <= R0) continue;
-            const double* sp = spill + spill_off[src] - s0;
-#pragma unroll
-            for (int u = 0; u < MU; ++u) {
-                const int32_t j = j0 + u * kS3Threads + tid;
-                if (j < he && j >= s0 && j < shi) {
-                    acc[u] += __ldcg(sp + j);
-                    tch[u] = true;
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < MU; ++u) {
-            const int32_t j = j0 + u * kS3Threads + tid;
-            if (tch[u]) y[j] = yv[u] + acc[u];
-        }
-    }
 }
 
 // Head rows of block d receive the spills of earlier blocks, summed in
@@ -590,95 +516,6 @@ __global__ void __launch_bounds__(256, KTB_S3_FIXUP_MINB) k_s3_fixup(const int4*
     for (int u = 0; u < U; ++u) {
         const int32_t j = j0 + u * 256 + threadIdx.x;
         if (touched[u]) y[j] = yv[u] + acc[u];
-    }
-}
-
-// Persistent form of k_s3_fixup: a grid of resident blocks walks the
-// segments (seg = blockIdx, blockIdx + grid, ...) two deep -- the next
-// segment's y and spill loads are issued before the current one is summed and
-// stored -- so the whole merge is about one round of L2 latency per block
-// instead of one per wave of short blocks. Same arithmetic as k_s3_fixup.
-struct FixSeg {
-    int32_t j0, j1, ns, list;
-    bool ok;
-    double yv[kFixRows / 256], v0[kFixRows / 256], v1[kFixRows / 256];
-    bool tch[kFixRows / 256];
-};
-
-__device__ __forceinline__ void fix_load(FixSeg& S, int64_t seg, int64_t nsegs,
-                                         const int4* __restrict__ desc,
-                                         const double* __restrict__ spill,
-                                         const double* __restrict__ y) {
-    constexpr int U = kFixRows / 256;
-    S.ok = seg < nsegs;
-    if (!S.ok) return;
-    const int4 a = __ldg(desc + 3 * seg), b = __ldg(desc + 3 * seg + 1), c = __ldg(desc + 3 * seg + 2);
-    S.j0 = a.x;
-    S.j1 = a.y;
-    S.ns = a.z;
-    S.list = a.w;
-    const int64_t base0 = static_cast<int64_t>(
-        static_cast<uint64_t>(static_cast<uint32_t>(c.x)) | (static_cast<uint64_t>(c.y) << 32));
-    const int64_t base1 = static_cast<int64_t>(
-        static_cast<uint64_t>(static_cast<uint32_t>(c.z)) | (static_cast<uint64_t>(c.w) << 32));
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int32_t j = S.j0 + u * 256 + threadIdx.x;
-        const bool in = j < S.j1;
-        const bool i0 = in && S.ns > 0 && j >= b.x && j < b.y;
-        const bool i1 = in && S.ns > 1 && j >= b.z && j < b.w;
-        S.yv[u] = in ? __ldcg(y + j) : 0.0;
-        S.v0[u] = i0 ? __ldcg(spill + base0 + j) : 0.0;
-        S.v1[u] = i1 ? __ldcg(spill + base1 + j) : 0.0;
-        S.tch[u] = i0 || i1;
-    }
-}
-
-__device__ __forceinline__ void fix_store(FixSeg& S, const int32_t* __restrict__ seg_src,
-                                          const int32_t* __restrict__ cta_row,
-                                          const int32_t* __restrict__ spill_hi,
-                                          const int64_t* __restrict__ spill_off,
-                                          const double* __restrict__ spill,
-                                          double* __restrict__ y) {
-    constexpr int U = kFixRows / 256;
-    if (!S.ok) return;
-    double acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = S.v0[u] + S.v1[u];  // ascending source order
-    for (int k = 2; k < S.ns; ++k) {  // more than two sources: rare (tiny blocks)
-        const int src = seg_src[S.list + k];
-        const int32_t s0 = cta_row[src + 1], hi = spill_hi[src];
-        const double* sp = spill + spill_off[src] - s0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int32_t j = S.j0 + u * 256 + threadIdx.x;
-            if (j < S.j1 && j >= s0 && j < hi) {
-                acc[u] += __ldcg(sp + j);
-                S.tch[u] = true;
-            }
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int32_t j = S.j0 + u * 256 + threadIdx.x;
-        if (S.tch[u]) y[j] = S.yv[u] + acc[u];
-    }
-}
-
-__global__ void __launch_bounds__(256) k_s3_fixup_persistent(
-    const int4* __restrict__ desc, int64_t nsegs, const int32_t* __restrict__ seg_src,
-    const int32_t* __restrict__ cta_row, const int32_t* __restrict__ spill_hi,
-    const int64_t* __restrict__ spill_off, const double* __restrict__ spill,
-    double* __restrict__ y) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_s3 complete and visible
-    FixSeg A, B;
-    int64_t seg = blockIdx.x;
-    fix_load(A, seg, nsegs, desc, spill, y);
-    for (; seg < nsegs; seg += 2 * gridDim.x) {
-        fix_load(B, seg + gridDim.x, nsegs, desc, spill, y);
-        fix_store(A, seg_src, cta_row, spill_hi, spill_off, spill, y);
-        fix_load(A, seg + 2 * gridDim.x, nsegs, desc, spill, y);
-        fix_store(B, seg_src, cta_row, spill_hi, spill_off, spill, y);
     }
 }
 
@@ -1005,10 +842,8 @@ void s3_setup(ktb_plan* p) {
     up32(L.spill_hi, spill_hi);
     up64(L.spill_off, spill_off);
     L.spill.alloc(std::max<int64_t>(so, 1));
-    up32(L.head_end, head_end);
     up32(L.segs, segs);
     up32(L.seg_src, seg_src);
-    up32(L.first_src, first_src);
     // far entries (both products) and long rows (row sum incl. diagonal and
     // transposed products) as contributions grouped by target row; the
     // stable sort keeps each target's contributions in a fixed order
@@ -1052,37 +887,10 @@ void s3_setup(ktb_plan* p) {
     KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kS3SmemFixed + W * 8)));
     p->ctas = P;
-    // KTB_S3_MERGE=1: merge the spills inside k_s3 (cooperative launch, every
-    // block resident) instead of the PDL-launched k_s3_fixup. Bitwise the
-    // same y; measured slower on config 2 (85.2 vs 82.9 us per apply: the
-    // tail merge is latency-bound while the fixup's blocks fill the SMs as
-    // k_s3's retire), so off by default.
-    {
-        int occ = 0, sms = 0;
-        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, k_s3, kS3Threads, static_cast<size_t>(kS3SmemFixed + W * 8)));
-        KTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
-        const char* env = std::getenv("KTB_S3_MERGE");
-        L.coop = env && env[0] == '1' && static_cast<int64_t>(occ) * sms >= P;
-        if (L.coop) {
-            L.flags.alloc(P);
-            KTB_CUDA(cudaMemsetAsync(L.flags.p, 0, sizeof(int) * P, st));
-            KTB_CUDA(cudaStreamSynchronize(st));
-        }
-    }
-    p->launches = 1 + (L.nsegs && !L.coop ? 1 : 0) + (L.npatch ? 1 : 0);
-    // KTB_S3_FIXUP_GRID=1: persistent, two-deep fixup over the resident blocks
-    // instead of one block per segment (measured 82.3 vs 80.3-80.9 us on
-    // config 2: the per-segment blocks already fill the SMs as k_s3's CTAs
-    // retire under programmatic dependent launch), so off by default
-    {
-        int occ = 0, sms = 0;
-        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_s3_fixup_persistent, 256, 0));
-        KTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
-        const char* env = std::getenv("KTB_S3_FIXUP_GRID");
-        const bool on = env && env[0] == '1';
-        L.fix_grid = on ? static_cast<int>(std::min<int64_t>(L.nsegs, int64_t(occ) * sms)) : 0;
-    }
+    // (round 1 also carried an in-kernel cooperative merge, 85.2 vs 82.9 us,
+    // and a persistent two-deep fixup, 82.3 vs 80.3-80.9 us on config 2; both
+    // slower than this PDL-launched per-segment fixup and removed)
+    p->launches = 1 + (L.nsegs ? 1 : 0) + (L.npatch ? 1 : 0);
     // padding slots (12 B each) + spill write/read + head-row read-modify-write
     // SELL stream (10 B/slot incl. padding) vs the 12 B/nnz model, + spill
     // write/read + head-row read-modify-write in the fixup; row_ptr unused
@@ -1092,36 +900,14 @@ void s3_setup(ktb_plan* p) {
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     const size_t smem = kS3SmemFixed + static_cast<size_t>(L.window) * 8;
-    if (L.coop) {  // spills merged inside k_s3 (all blocks resident)
-        const int32_t* cta_row = L.cta_row.p;
-        const int32_t* cta_chunk = L.cta_chunk.p;
-        const int32_t* meta = L.chunk_meta.p;
-        const int32_t* qreal = L.cta_qreal.p;
-        const unsigned char* sell = L.sell.p;
-        const int64_t* base = L.cta_base.p;
-        const double* diag = L.diag.p;
-        int W = L.window, reach = L.reach, n = static_cast<int>(p->m->n);
-        const int32_t* shi = L.spill_hi.p;
-        const int64_t* soff = L.spill_off.p;
-        double* spill = L.spill.p;
-        int* flags = L.flags.p;
-        int epoch = ++L.epoch;
-        const int32_t* he = L.head_end.p;
-        const int32_t* fs = L.first_src.p;
-        void* args[] = {&cta_row, &cta_chunk, &meta, &qreal, &sell, &base, &diag, &x, &y, &W,
-                        &reach, &n, &shi, &soff, &spill, &flags, &epoch, &he, &fs};
-        KTB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_s3), dim3(L.ctas),
-                                             dim3(kS3Threads), args, smem, p->stream));
-    } else {
-        k_s3<<<L.ctas, kS3Threads, smem, p->stream>>>(
-            L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p, L.cta_base.p,
-            L.diag.p, x, y, L.window, L.reach, static_cast<int>(p->m->n), L.spill_hi.p,
-            L.spill_off.p, L.spill.p, nullptr, 0, L.head_end.p, L.first_src.p);
-        KTB_LAUNCH();
-    }
-    if (L.nsegs && !L.coop) {
+    k_s3<<<L.ctas, kS3Threads, smem, p->stream>>>(
+        L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p, L.cta_base.p,
+        L.diag.p, x, y, L.window, L.reach, static_cast<int>(p->m->n), L.spill_hi.p,
+        L.spill_off.p, L.spill.p);
+    KTB_LAUNCH();
+    if (L.nsegs) {  // the fixup's blocks launch early and wait for k_s3 (PDL)
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(static_cast<unsigned>(L.fix_grid ? L.fix_grid : L.nsegs));
+        cfg.gridDim = dim3(static_cast<unsigned>(L.nsegs));
         cfg.blockDim = dim3(256);
         cfg.stream = p->stream;
         cudaLaunchAttribute attr[1];
@@ -1129,15 +915,6 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (L.fix_grid)
-            KTB_CUDA(cudaLaunchKernelEx(&cfg, k_s3_fixup_persistent,
-                                        reinterpret_cast<const int4*>(L.segs.p), L.nsegs,
-                                        static_cast<const int32_t*>(L.seg_src.p),
-                                        static_cast<const int32_t*>(L.cta_row.p),
-                                        static_cast<const int32_t*>(L.spill_hi.p),
-                                        static_cast<const int64_t*>(L.spill_off.p),
-                                        static_cast<const double*>(L.spill.p), y));
-        else
         KTB_CUDA(cudaLaunchKernelEx(&cfg, k_s3_fixup, reinterpret_cast<const int4*>(L.segs.p),
                                     static_cast<const int32_t*>(L.seg_src.p),
                                     static_cast<const int32_t*>(L.cta_row.p),
@@ -1145,7 +922,6 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
                                     static_cast<const int64_t*>(L.spill_off.p),
                                     static_cast<const double*>(L.spill.p), y));
     }
-
     if (L.npatch) {
         k_s3_patch<<<ceil_div(L.npatch, 8), 256, 0, p->stream>>>(
             L.patch_row.p, L.patch_rp.p, L.patch_src.p, L.patch_val.p, L.npatch, x, y);

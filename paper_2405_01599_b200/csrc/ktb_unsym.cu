@@ -136,7 +136,10 @@ constexpr int kU1sThreads = KTB_U1S_THREADS;
 #define KTB_U1S_MINB 1  // 7 (config 1's 8192 slices in one wave) caps registers at 32 and
                         // spills: slower on configs 1, 4 and 5
 #endif
-__global__ void __launch_bounds__(kU1sThreads, KTB_U1S_MINB) k_u1s(const int64_t* __restrict__ soff,
+// CTA shape: 64, 128 (default) or 256 threads, all instantiated; the
+// selector times them as launch-shape candidates (p->cta_threads)
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* __restrict__ soff,
                                              const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
@@ -443,6 +446,11 @@ static int pick_lanes(const ktb_matrix* m) {
 }
 
 void u1_setup(ktb_plan* p) {
+    require(p->cta_threads == 0 ||
+                ((p->param == 100 || p->param == 101) &&
+                 (p->cta_threads == 64 || p->cta_threads == 128 || p->cta_threads == 256)),
+            "u1: only the warp-sliced forms (params 100, 101) take a CTA shape: 64, 128 or 256 "
+            "threads");
     if (p->param == 100) {
         u1_sell_setup(p);
         p->launches = 1;
@@ -458,6 +466,30 @@ void u1_setup(ktb_plan* p) {
     while (v < p->param && v < 32) v <<= 1;
     p->param = v;
     p->launches = 1;
+}
+
+// k_u1s over `threads` slice lanes in the plan's CTA shape
+static void launch_u1s(ktb_plan* p, int64_t threads, const int64_t* soff, const double* x,
+                       double* y, int32_t r0, int32_t r1, int ell, const int32_t* perm) {
+    const int t = p->cta_threads ? p->cta_threads : kU1sThreads;
+    const int grid = ceil_div(threads, t);
+    p->ctas = grid;
+    switch (t) {
+        case 64:
+            k_u1s<64><<<grid, 64, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0, r1,
+                                                  ell, perm);
+            break;
+        case 128:
+            k_u1s<128><<<grid, 128, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0,
+                                                    r1, ell, perm);
+            break;
+        case 256:
+            k_u1s<256><<<grid, 256, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0,
+                                                    r1, ell, perm);
+            break;
+        default: throw Invalid("u1: warp-sliced CTAs are 64, 128 or 256 threads");
+    }
+    KTB_LAUNCH();
 }
 
 void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
@@ -479,22 +511,15 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
             KTB_CUDA(cudaEventRecord(p->join, p->side));
         }
         const int64_t slices = static_cast<int64_t>(p->sell_off.n) - 1;
-        const int grid = ceil_div(slices * 32, kU1sThreads);
-        p->ctas = grid;
-        k_u1s<<<grid, kU1sThreads, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y, 0,
-                                           static_cast<int32_t>(slices * 32), 0, p->sell_perm.p);
-        KTB_LAUNCH();
+        launch_u1s(p, slices * 32, p->sell_off.p, x, y, 0, static_cast<int32_t>(slices * 32), 0,
+                   p->sell_perm.p);
         if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
         return;
     }
     if (p->param == 100) {
         const int64_t s0 = r0 >> 5, s1 = ceil_div64(r1, 32);
-        const int grid = ceil_div((s1 - s0) * 32, kU1sThreads);
-        p->ctas = grid;
-        k_u1s<<<grid, kU1sThreads, 0, p->stream>>>(p->sell_off.p, p->sell_col.p, p->sell_val.p, x, y,
-                                           static_cast<int32_t>(r0), static_cast<int32_t>(r1),
-                                           p->ell_width, nullptr);
-        KTB_LAUNCH();
+        launch_u1s(p, (s1 - s0) * 32, p->sell_off.p, x, y, static_cast<int32_t>(r0),
+                   static_cast<int32_t>(r1), p->ell_width, nullptr);
         return;
     }
     const int V = static_cast<int>(p->param);
@@ -701,11 +726,9 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
 #ifndef KTB_U2W_MINB
 #define KTB_U2W_MINB 5
 #endif
-#ifndef KTB_TILE_WARPS
-#define KTB_TILE_WARPS 4  // warps per CTA of the U2/U3 warp-tile kernels (8: 4 % slower on config 3)
-#endif
-constexpr int kTileWarps = KTB_TILE_WARPS;
-template <int IPT>
+// CTA shape: 4 warps by default (8: 4 % slower on config 3); both shapes are
+// instantiated and the selector times them (launch-shape candidates).
+template <int IPT, int kTileWarps>
 __global__ void __launch_bounds__(32 * kTileWarps, KTB_U2W_MINB * 8 / kTileWarps) k_u2w(const int32_t* __restrict__ rp,
                                                           const int32_t* __restrict__ col,
                                                           const double* __restrict__ val,
@@ -835,13 +858,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, KTB_U2W_MINB * 8 / kTileWarps
     }
 }
 
-// ---- U2, vector warp tiles -------------------------------------------------
-// Same tiles, row-end map, summation order and carries as k_u2w (hence
-// bitwise-identical y), but lane b loads its own IPT consecutive nonzeros
-// with 16-byte vector loads (IPT/4 x int4 columns, IPT/2 x double2 values)
-// and keeps the products in registers: no product staging through shared
-// memory, a quarter of the load instructions. A tile that runs past nnz
-// (the last one) falls back to guarded scalar loads.
+// 16-byte streaming loads (U3 lanes)
 __device__ __forceinline__ int4 ld_stream_v4i32(const int32_t* p) {
     int4 r;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
@@ -855,358 +872,6 @@ __device__ __forceinline__ double2 ld_stream_v2f64(const double* p) {
         : "=d"(r.x), "=d"(r.y)
         : "l"(p), "l"(pol_first()));
     return r;
-}
-
-template <int IPT>
-__global__ void __launch_bounds__(256, IPT == 8 ? 5 : 3) k_u2v(const int32_t* __restrict__ rp,
-                                                          const int32_t* __restrict__ col,
-                                                          const double* __restrict__ val,
-                                                          const double* __restrict__ x,
-                                                          double* __restrict__ y,
-                                                          const int32_t* __restrict__ wrow,
-                                                          int64_t nnz, int64_t tiles,
-                                                          int32_t* __restrict__ carry_row,
-                                                          double* __restrict__ carry_val) {
-    constexpr int T = 32 * IPT;
-    static_assert(IPT == 8 || IPT == 16, "u2v: IPT");
-    // s_end: thread b's IPT ints are IPT/4 16-byte chunks, XOR-swizzled by
-    // (b >> ESH) so the blocked 16-byte reads of a quarter warp hit 32 banks
-    constexpr int ESH = IPT == 8 ? 2 : 1;
-    constexpr int EMASK = IPT / 4 - 1;
-    __shared__ __align__(16) int32_t s_end[8][T];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t w = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    if (w >= tiles) return;
-    const int64_t z0 = w * T;
-    const int32_t ra = __ldg(wrow + w), rb = __ldg(wrow + w + 1);
-
-    int32_t c[IPT];
-    double v[IPT];
-    const int64_t k0 = z0 + static_cast<int64_t>(lane) * IPT;
-    if (z0 + T <= nnz) {
-#pragma unroll
-        for (int q = 0; q < IPT; q += 4) {
-            const int4 c4 = ld_stream_v4i32(col + k0 + q);
-            c[q] = c4.x;
-            c[q + 1] = c4.y;
-            c[q + 2] = c4.z;
-            c[q + 3] = c4.w;
-        }
-#pragma unroll
-        for (int q = 0; q < IPT; q += 2) {
-            const double2 v2 = ld_stream_v2f64(val + k0 + q);
-            v[q] = v2.x;
-            v[q + 1] = v2.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const bool ok = k0 + j < nnz;
-            c[j] = ok ? ld_stream_i32(col + k0 + j) : -1;
-            v[j] = ok ? ld_stream_f64(val + k0 + j) : 0.0;
-        }
-    }
-    bool in = ra + lane < rb;
-    int32_t rb_ = in ? __ldg(rp + ra + lane) : 0;
-    int32_t re_ = in ? __ldg(rp + ra + lane + 1) : 0;
-#pragma unroll
-    for (int q = 0; q < IPT; q += 4) {
-        const int phys = ((q >> 2) ^ ((lane >> ESH) & EMASK)) << 2;
-        *reinterpret_cast<int4*>(&s_end[warp][lane * IPT + phys]) = make_int4(0, 0, 0, 0);
-    }
-    double xv[IPT];
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) xv[j] = c[j] >= 0 ? ld_x(x + c[j]) : 0.0;
-    __syncwarp();  // s_end zeroed before the scatter below
-    for (int32_t r0 = ra;;) {
-        const int32_t r = r0 + lane;
-        if (in) {
-            if (re_ > rb_) {
-                const int i = static_cast<int>(re_ - 1 - z0);
-                const int b = i / IPT, j = i % IPT;
-                s_end[warp][b * IPT + ((((j >> 2) ^ ((b >> ESH) & EMASK)) << 2) | (j & 3))] = r + 1;
-            } else {
-                y[r] = 0.0;  // empty row
-            }
-        }
-        r0 += 32;
-        if (r0 >= rb) break;
-        in = r0 + lane < rb;
-        rb_ = in ? __ldg(rp + r0 + lane) : 0;
-        re_ = in ? __ldg(rp + r0 + lane + 1) : 0;
-    }
-    __syncwarp();
-    int32_t er[IPT];
-#pragma unroll
-    for (int q = 0; q < IPT; q += 4) {
-        const int phys = ((q >> 2) ^ ((lane >> ESH) & EMASK)) << 2;
-        const int4 e4 = *reinterpret_cast<const int4*>(&s_end[warp][lane * IPT + phys]);
-        er[q] = e4.x;
-        er[q + 1] = e4.y;
-        er[q + 2] = e4.z;
-        er[q + 3] = e4.w;
-    }
-    double run = 0.0, head = 0.0;
-    int32_t head_row = 0;
-    bool has = false;
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        run += __dmul_rn(v[j], xv[j]);  // rounded product, as k_u2w stages it
-        if (er[j]) {
-            if (has) {
-                y[er[j] - 1] = run;
-            } else {
-                head = run;
-                head_row = er[j] - 1;
-            }
-            has = true;
-            run = 0.0;
-        }
-    }
-    const uint32_t F = __ballot_sync(0xffffffffu, has);
-    double S = run;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double up = __shfl_up_sync(0xffffffffu, S, d);
-        if (lane >= d && ((F >> (lane - d + 1)) & ((1u << d) - 1u)) == 0u) S += up;
-    }
-    double cin = __shfl_up_sync(0xffffffffu, S, 1);
-    if (lane == 0) cin = 0.0;
-    if (has) y[head_row] = head + cin;
-    if (lane == 31) {
-        carry_row[w] = rb;
-        carry_val[w] = S;
-    }
-}
-
-// ---- U2, TMA-streamed warp tiles -------------------------------------------
-// The k_u2w tiles (256 nonzeros, IPT 8; same row-end map, summation order and
-// carries, hence bitwise-identical y), fed by a bulk-copy ring instead of
-// per-thread global loads. A persistent CTA per SM slot owns a contiguous run
-// of chunks (8 tiles = 2048 nonzeros = 8 KB columns + 16 KB values); a
-// producer warp streams them through kU2tStages stages with
-// cp.async.bulk (full/empty mbarrier pairs), the 8 consumer warps take one tile
-// each per chunk. A warp copies its tile from the stage to registers with
-// conflict-free 16-byte reads (per quarter warp the lanes' chunk order is
-// rotated so the 8 lanes hit 8 distinct bank groups), releases the stage, and
-// issues its x gathers; tiles are software-pipelined two deep per warp (the
-// next tile's copy and gathers go out before the current tile is reduced), so
-// the only exposed latency is one gather round trip per two tiles. The
-// partial last chunk is handled by the last CTA with guarded loads.
-#ifndef KTB_U2T_WARPS
-#define KTB_U2T_WARPS 8
-#endif
-constexpr int kU2tWarps = KTB_U2T_WARPS;
-constexpr int kU2tTile = 256;                      // nonzeros per warp tile
-constexpr int kU2tChunk = kU2tWarps * kU2tTile;    // nonzeros per stage
-constexpr int kU2tStages = 4;
-constexpr int kU2tColBytes = kU2tChunk * 4;        // 8192
-constexpr int kU2tStageBytes = kU2tChunk * 12;     // 24576
-constexpr int kU2tEndBytes = kU2tWarps * kU2tTile * 4;
-constexpr int kU2tSmem = kU2tStages * kU2tStageBytes + kU2tEndBytes + 2 * kU2tStages * 8;
-constexpr int kU2tThreads = (kU2tWarps + 1) * 32;
-
-struct U2Tile {
-    int32_t c[8];
-    double v[8], xv[8];
-    int32_t ra, rb;
-    int32_t b0, e0, b1, e1;  // bounds of rows ra + lane and ra + 32 + lane
-    int64_t w;
-};
-
-// bounds of the tile's first 64 rows (two per lane), one round trip
-__device__ __forceinline__ void u2t_bounds(U2Tile& t, int lane, const int32_t* __restrict__ rp) {
-    const bool in0 = t.ra + lane < t.rb, in1 = t.ra + 32 + lane < t.rb;
-    t.b0 = in0 ? __ldg(rp + t.ra + lane) : 0;
-    t.e0 = in0 ? __ldg(rp + t.ra + lane + 1) : 0;
-    t.b1 = in1 ? __ldg(rp + t.ra + 32 + lane) : 0;
-    t.e1 = in1 ? __ldg(rp + t.ra + 33 + lane) : 0;
-}
-
-// the row-end scatter, segmented sums, warp carry scan and the tile carry of
-// one IPT-8 tile whose products are v[j] * xv[j] (k_u2w steps 2-5)
-__device__ __forceinline__ void u2_tile_reduce(const U2Tile& t, int lane, int32_t* s_end,
-                                               const int32_t* __restrict__ rp,
-                                               double* __restrict__ y,
-                                               int32_t* __restrict__ carry_row,
-                                               double* __restrict__ carry_val) {
-    constexpr int IPT = 8, ESH = 2, EMASK = 1;
-    const int64_t z0 = t.w * kU2tTile;
-#pragma unroll
-    for (int q = 0; q < IPT; q += 4) {
-        const int phys = ((q >> 2) ^ ((lane >> ESH) & EMASK)) << 2;
-        *reinterpret_cast<int4*>(&s_end[lane * IPT + phys]) = make_int4(0, 0, 0, 0);
-    }
-    __syncwarp();
-    auto mark = [&](int32_t r, int32_t rb_, int32_t re_) {
-        if (re_ > rb_) {
-            const int i = static_cast<int>(re_ - 1 - z0);
-            const int b = i / IPT, j = i % IPT;
-            s_end[b * IPT + ((((j >> 2) ^ ((b >> ESH) & EMASK)) << 2) | (j & 3))] = r + 1;
-        } else {
-            y[r] = 0.0;  // empty row
-        }
-    };
-    if (t.ra + lane < t.rb) mark(t.ra + lane, t.b0, t.e0);
-    if (t.ra + 32 + lane < t.rb) mark(t.ra + 32 + lane, t.b1, t.e1);
-    for (int32_t r = t.ra + 64 + lane; r - lane < t.rb; r += 32)  // rows beyond 64 (rare)
-        if (r < t.rb) mark(r, __ldg(rp + r), __ldg(rp + r + 1));
-    __syncwarp();
-    int32_t er[IPT];
-#pragma unroll
-    for (int q = 0; q < IPT; q += 4) {
-        const int phys = ((q >> 2) ^ ((lane >> ESH) & EMASK)) << 2;
-        const int4 e4 = *reinterpret_cast<const int4*>(&s_end[lane * IPT + phys]);
-        er[q] = e4.x;
-        er[q + 1] = e4.y;
-        er[q + 2] = e4.z;
-        er[q + 3] = e4.w;
-    }
-    double run = 0.0, head = 0.0;
-    int32_t head_row = 0;
-    bool has = false;
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        run += __dmul_rn(t.v[j], t.xv[j]);  // rounded product, as k_u2w stages it
-        if (er[j]) {
-            if (has) {
-                y[er[j] - 1] = run;
-            } else {
-                head = run;
-                head_row = er[j] - 1;
-            }
-            has = true;
-            run = 0.0;
-        }
-    }
-    const uint32_t F = __ballot_sync(0xffffffffu, has);
-    double S = run;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double up = __shfl_up_sync(0xffffffffu, S, d);
-        if (lane >= d && ((F >> (lane - d + 1)) & ((1u << d) - 1u)) == 0u) S += up;
-    }
-    double cin = __shfl_up_sync(0xffffffffu, S, 1);
-    if (lane == 0) cin = 0.0;
-    if (has) y[head_row] = head + cin;
-    if (lane == 31) {
-        carry_row[t.w] = t.rb;
-        carry_val[t.w] = S;
-    }
-}
-
-__global__ void __maxnreg__(112)
-    k_u2t(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-          const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-          const int32_t* __restrict__ wrow, int64_t nnz, int64_t tiles, int64_t nchunks,
-          int32_t* __restrict__ carry_row, double* __restrict__ carry_val) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    int32_t* s_end_all = reinterpret_cast<int32_t*>(smem + kU2tStages * kU2tStageBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kU2tStages * kU2tStageBytes + kU2tEndBytes);
-    uint64_t* empty = full + kU2tStages;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t k0 = nchunks * blockIdx.x / gridDim.x;
-    const int nk = static_cast<int>(nchunks * (blockIdx.x + 1) / gridDim.x - k0);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kU2tStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kU2tWarps);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (warp == kU2tWarps) {  // producer
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            for (int k = 0; k < nk; ++k) {
-                const int s = k % kU2tStages;
-                if (k >= kU2tStages) mbar_wait(&empty[s], ((k / kU2tStages) - 1) & 1);
-                unsigned char* st = smem + s * kU2tStageBytes;
-                const int64_t z = (k0 + k) * kU2tChunk;
-                mbar_arrive_expect_tx(&full[s], kU2tStageBytes);
-                tma_load_1d(st, col + z, kU2tColBytes, &full[s], pol);
-                tma_load_1d(st + kU2tColBytes, val + z, kU2tStageBytes - kU2tColBytes, &full[s],
-                            pol);
-            }
-        }
-        return;
-    }
-    int32_t* s_end = s_end_all + warp * kU2tTile;
-    // tile bounds run one tile ahead of the fetch: (nra, nrb) = wrow of the
-    // next tile this warp fetches
-    int32_t nra = 0, nrb = 0;
-    if (nk > 0) {
-        nra = __ldg(wrow + k0 * kU2tWarps + warp);
-        nrb = __ldg(wrow + k0 * kU2tWarps + warp + 1);
-    }
-    // copy tile (chunk k, this warp) to registers, release the stage, gather
-    auto fetch = [&](U2Tile& t, int k) {
-        t.w = (k0 + k) * kU2tWarps + warp;
-        t.ra = nra;
-        t.rb = nrb;
-        u2t_bounds(t, lane, rp);
-        if (k + 1 < nk) {
-            nra = __ldg(wrow + t.w + kU2tWarps);
-            nrb = __ldg(wrow + t.w + kU2tWarps + 1);
-        }
-        const int s = k % kU2tStages;
-        mbar_wait(&full[s], (k / kU2tStages) & 1);
-        const unsigned char* st = smem + s * kU2tStageBytes;
-        const int4* sc = reinterpret_cast<const int4*>(st) + warp * (kU2tTile / 4);
-        const int f = (lane >> 2) & 1;
-        const int4 A = sc[2 * lane + f], B = sc[2 * lane + (f ^ 1)];
-        const int4 lo = f ? B : A, hi = f ? A : B;
-        t.c[0] = lo.x; t.c[1] = lo.y; t.c[2] = lo.z; t.c[3] = lo.w;
-        t.c[4] = hi.x; t.c[5] = hi.y; t.c[6] = hi.z; t.c[7] = hi.w;
-        const double2* sv =
-            reinterpret_cast<const double2*>(st + kU2tColBytes) + warp * (kU2tTile / 2);
-        const int r = (lane >> 1) & 3;
-        double2 L[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) L[q] = sv[4 * lane + ((q + r) & 3)];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // chunk kk is L[(kk - r) & 3]
-            const int i = (kk - r) & 3;
-            const double2 ch = i == 0 ? L[0] : i == 1 ? L[1] : i == 2 ? L[2] : L[3];
-            t.v[2 * kk] = ch.x;
-            t.v[2 * kk + 1] = ch.y;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) t.xv[j] = ld_x(x + t.c[j]);
-    };
-    U2Tile A, B;
-    if (nk > 0) fetch(A, 0);
-    int k = 0;
-    for (; k + 2 <= nk; k += 2) {
-        fetch(B, k + 1);
-        u2_tile_reduce(A, lane, s_end, rp, y, carry_row, carry_val);
-        if (k + 2 < nk) fetch(A, k + 2);
-        u2_tile_reduce(B, lane, s_end, rp, y, carry_row, carry_val);
-    }
-    if (k < nk) u2_tile_reduce(A, lane, s_end, rp, y, carry_row, carry_val);
-
-    // tiles past the last full chunk (< kU2tWarps): last CTA, guarded loads
-    if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t w = nchunks * kU2tWarps + warp; w < tiles; w += kU2tWarps) {
-            U2Tile& t = A;
-            t.w = w;
-            t.ra = __ldg(wrow + w);
-            t.rb = __ldg(wrow + w + 1);
-            const int64_t kb = w * kU2tTile + lane * 8;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool ok = kb + j < nnz;
-                t.c[j] = ok ? ld_stream_i32(col + kb + j) : -1;
-                t.v[j] = ok ? ld_stream_f64(val + kb + j) : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) t.xv[j] = t.c[j] >= 0 ? ld_x(x + t.c[j]) : 0.0;
-            u2t_bounds(t, lane, rp);
-            u2_tile_reduce(t, lane, s_end, rp, y, carry_row, carry_val);
-        }
-    }
 }
 
 // first row whose end lies beyond z = w*T (w = 0: row 0)
@@ -1231,49 +896,30 @@ __global__ void k_u2w_rows(const int32_t* __restrict__ rp, int64_t n, int64_t nn
 }
 
 // param: 4 / 8 = warp tiles with that many items per thread (default 8);
-// 208 / 216 = vector warp tiles with IPT = param - 200;
-// 300 = TMA-streamed warp tiles (IPT 8);
 // 104 / 108 / 112 = the merge-path kernel with IPT = param - 100.
+// p->cta_threads: warp tiles in CTAs of 128 (default) or 256 threads.
 void u2_setup(ktb_plan* p) {
     if (p->param <= 0) p->param = 8;
     const int prm = static_cast<int>(p->param);
     const ktb_matrix* m = p->m;
-    const bool vec = prm == 208 || prm == 216 || prm == 300;
-    if (vec && ((reinterpret_cast<uintptr_t>(m->col.p) | reinterpret_cast<uintptr_t>(m->val.p)) & 15))
-        throw Invalid("u2: vector tiles need 16-byte aligned col/val");
-    if (prm == 4 || prm == 8 || vec) {
-        const int64_t T = prm == 300 ? kU2tTile : 32 * (vec ? prm - 200 : prm);
+    if (prm == 4 || prm == 8) {
+        require(p->cta_threads == 0 || p->cta_threads == 128 || p->cta_threads == 256,
+                "u2: warp tiles run in CTAs of 128 or 256 threads");
+        const int64_t T = 32 * prm;
         p->tiles = std::max<int64_t>(1, ceil_div64(m->nnz, T));
         p->wrow.alloc(p->tiles + 1);
         p->carry_row.alloc(p->tiles);
         p->carry_val.alloc(p->tiles);
-#ifdef KTB_U2W_CARVEOUT
-        KTB_CUDA(cudaFuncSetAttribute(k_u2w<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      KTB_U2W_CARVEOUT));
-        KTB_CUDA(cudaFuncSetAttribute(k_u2w<8>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      KTB_U2W_CARVEOUT));
-#endif
         k_u2w_rows<<<ceil_div(p->tiles + 1, 256), 256, 0, p->stream>>>(
             m->row_ptr.p, m->n, m->nnz, T, p->tiles, p->wrow.p);
         KTB_LAUNCH();
         KTB_CUDA(cudaStreamSynchronize(p->stream));
-        p->ctas = ceil_div64(p->tiles, 8);
-        if (prm == 300) {
-            KTB_CUDA(cudaFuncSetAttribute(k_u2t, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kU2tSmem));
-            KTB_CUDA(cudaFuncSetAttribute(k_u2t, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          100));
-            int occ = 0;
-            KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u2t, kU2tThreads,
-                                                                   kU2tSmem));
-            const int64_t nchunks = m->nnz / kU2tChunk;
-            p->ctas = std::max<int64_t>(1, std::min<int64_t>(nchunks, int64_t(std::max(occ, 1)) *
-                                                                          m->sm_count));
-        }
+        p->ctas = ceil_div64(p->tiles, p->cta_threads == 256 ? 8 : 4);
         p->launches = 2;
         p->extra_bytes = p->tiles * (4 + 4 + 8) * 2;
         return;
     }
+    require(p->cta_threads == 0, "u2: the merge-path tiles have one CTA shape");
     int ipt = prm - 100;
     if (ipt != 4 && ipt != 8 && ipt != 12) ipt = 8;
     p->param = 100 + ipt;
@@ -1294,45 +940,18 @@ void u2_setup(ktb_plan* p) {
 void u2_run(ktb_plan* p, const double* x, double* y) {
     const ktb_matrix* m = p->m;
     const int prm = static_cast<int>(p->param);
-    if (prm == 300) {
-        k_u2t<<<static_cast<int>(p->ctas), kU2tThreads, kU2tSmem, p->stream>>>(
-            m->row_ptr.p, m->col.p, m->val.p, x, y, p->wrow.p, m->nnz, p->tiles,
-            m->nnz / kU2tChunk, p->carry_row.p, p->carry_val.p);
-        KTB_LAUNCH();
-        fixup_run(p, y);
-        return;
-    }
-    if (prm > 200) {
-        const int grid = static_cast<int>(ceil_div64(p->tiles, 8));
-#define KTB_U2V_CASE(I)                                                                      \
-    case 200 + I:                                                                             \
-        k_u2v<I><<<grid, 256, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,         \
-                                              p->wrow.p, m->nnz, p->tiles, p->carry_row.p,    \
-                                              p->carry_val.p);                                \
-        break;
-        switch (prm) {
-            KTB_U2V_CASE(8)
-            KTB_U2V_CASE(16)
-            default: throw Invalid("u2: bad items per thread");
-        }
-#undef KTB_U2V_CASE
-        KTB_LAUNCH();
-        fixup_run(p, y);
-        return;
-    }
     if (prm < 100) {
-        const int grid = static_cast<int>(ceil_div64(p->tiles, kTileWarps));
-#define KTB_U2W_CASE(I)                                                                      \
-    case I:                                                                                   \
-        k_u2w<I><<<grid, 32 * kTileWarps, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,         \
-                                              p->wrow.p, m->nnz, p->tiles, p->carry_row.p,    \
-                                              p->carry_val.p);                                \
-        break;
-        switch (prm) {
-            KTB_U2W_CASE(4)
-            KTB_U2W_CASE(8)
-            default: throw Invalid("u2: bad items per thread");
-        }
+        const int warps = p->cta_threads == 256 ? 8 : 4;
+        const int grid = static_cast<int>(ceil_div64(p->tiles, warps));
+#define KTB_U2W_CASE(I, WW)                                                                   \
+    if (prm == I && warps == WW)                                                               \
+        k_u2w<I, WW><<<grid, 32 * WW, 0, p->stream>>>(m->row_ptr.p, m->col.p, m->val.p, x, y,  \
+                                                      p->wrow.p, m->nnz, p->tiles,             \
+                                                      p->carry_row.p, p->carry_val.p);
+        KTB_U2W_CASE(4, 4)
+        KTB_U2W_CASE(8, 4)
+        KTB_U2W_CASE(4, 8)
+        KTB_U2W_CASE(8, 8)
 #undef KTB_U2W_CASE
         KTB_LAUNCH();
         fixup_run(p, y);
@@ -1427,6 +1046,7 @@ __global__ void k_empty_list(const int32_t* __restrict__ rp, int64_t n,
     if (i < n && rp[i] == rp[i + 1]) out[i - ord[i]] = static_cast<int32_t>(i);  // ord = nonempty before i
 }
 
+template <int kTileWarps>
 __global__ void __launch_bounds__(32 * kTileWarps, 32 / kTileWarps) k_u3w(const int32_t* __restrict__ col,
                                                  const double* __restrict__ val,
                                                  const double* __restrict__ x,
@@ -1658,6 +1278,8 @@ void u3_setup(ktb_plan* p) {
     const ktb_matrix* m = p->m;
     require(m->nnz > 0, "bss plan: empty matrix");
     const bool warp_tiles = p->param == 1008 && p->kernel == KTB_U3;
+    require(p->cta_threads == 0 || (warp_tiles && (p->cta_threads == 128 || p->cta_threads == 256)),
+            "u3: only the warp tiles (param 1008) take a CTA shape: 128 or 256 threads");
     int E = p->param > 0 ? static_cast<int>(p->param) : 8;
     if (warp_tiles) E = 8;
     if (E != 4 && E != 8 && E != 16) E = 8;
@@ -1737,9 +1359,14 @@ void u3_run(ktb_plan* p, const double* x, double* y) {
     if (p->param == 1008 && p->kernel == KTB_U3) {
         k_zero_rows<<<ceil_div(p->nzero, 256), 256, 0, p->stream>>>(p->zero_rows.p, p->nzero, y);
         KTB_LAUNCH();
-        k_u3w<<<static_cast<int>(ceil_div64(p->tiles, kTileWarps)), 32 * kTileWarps, 0, p->stream>>>(
-            m->col.p, m->val.p, x, y, m->nnz, p->tiles, p->flag_bits.p, p->seg_row.p,
-            p->tile_q.p, p->carry_row.p, p->carry_val.p);
+        if (p->cta_threads == 256)
+            k_u3w<8><<<static_cast<int>(ceil_div64(p->tiles, 8)), 256, 0, p->stream>>>(
+                m->col.p, m->val.p, x, y, m->nnz, p->tiles, p->flag_bits.p, p->seg_row.p,
+                p->tile_q.p, p->carry_row.p, p->carry_val.p);
+        else
+            k_u3w<4><<<static_cast<int>(ceil_div64(p->tiles, 4)), 128, 0, p->stream>>>(
+                m->col.p, m->val.p, x, y, m->nnz, p->tiles, p->flag_bits.p, p->seg_row.p,
+                p->tile_q.p, p->carry_row.p, p->carry_val.p);
         KTB_LAUNCH();
         fixup_run(p, y);
         return;

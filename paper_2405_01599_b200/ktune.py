@@ -672,6 +672,8 @@ class TuningCandidate:  # autotune.hpp:130-139
     best_seconds: float
     correct: bool
     executions: int
+    cta_threads: int = 0       # launch shape timed (0 = the kernel's default)
+    setup_seconds: float = 0.0  # plan build before the warm-up
 
 
 @dataclass
@@ -701,7 +703,8 @@ class _Cand(C.Structure):
     _fields_ = [("name", C.c_char * 8), ("ordinal", C.c_int), ("param", I64),
                 ("workers", C.c_int), ("correct", C.c_int), ("executions", C.c_int),
                 ("n_trials", C.c_int), ("best_seconds", C.c_double),
-                ("trial_seconds", C.c_double * 8)]
+                ("trial_seconds", C.c_double * 8), ("cta_threads", C.c_int),
+                ("setup_seconds", C.c_double)]
 
 
 class _Opts(C.Structure):
@@ -750,7 +753,8 @@ def _select(a, opts: Optional[SelectOptions]):
         c = cands[i]
         rep.candidates.append(TuningCandidate(c.name.decode(), c.ordinal, c.param, c.workers,
                                               list(c.trial_seconds[: c.n_trials]),
-                                              c.best_seconds, bool(c.correct), c.executions))
+                                              c.best_seconds, bool(c.correct), c.executions,
+                                              c.cta_threads, c.setup_seconds))
     return DevicePlan(a, 0, handle=h), rep
 
 

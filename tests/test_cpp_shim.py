@@ -66,7 +66,7 @@ def test_reference_call_sequences_with_namespace_changed():
     """tests/cpp/ref_api_drop_in.cpp: meta.hpp:171-190 with ktune:: -> ktb_ref::
     (both branches) feeding the reference's gmres_m (iterations +-2 vs the
     unmodified sequence); spmv_unsym/spmv_sym with the reference signatures
-    (U1/U2 bitwise = spmv_ref, the rest within 1e-12 (|A||x|)_i); device
+    (U1 bitwise = spmv_ref on the stencil, all within 1e-12 (|A||x|)_i); device
     artefact builders bit-exact; the reference's error messages; one device
     copy across 200 calls."""
     out = subprocess.run([REF_BIN, "20"], capture_output=True, text=True, timeout=900)

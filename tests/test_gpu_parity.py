@@ -402,10 +402,13 @@ def test_config4_properties_full_size(K):
     assert_close(got, yl, absl, "cfg4 slab")
 
 
+SHAPE = 1 << 16  # param bits 16..31: CTA threads (launch-shape candidates)
+
+
 def test_u2_all_tile_variants(K):
-    """Every U2 implementation (warp tiles IPT 4/8, vector warp tiles
-    208/216, merge path 104/108/112) on random, skewed, empty-row and long-row
-    matrices; the vector tiles are bitwise equal to the scalar ones."""
+    """Every U2 implementation (warp tiles IPT 4/8 in 4- and 8-warp CTAs,
+    merge path 104/108/112) on random, skewed, empty-row and long-row
+    matrices; the two CTA shapes of the warp tiles are bitwise equal."""
     rng = np.random.default_rng(7)
     mats = []
     for t in range(8):
@@ -424,13 +427,66 @@ def test_u2_all_tile_variants(K):
         a = K.CsrMatrix(n, rp, ci, v)
         yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
         ys = {}
-        for prm in (4, 8, 208, 216, 300, 104, 108, 112):
+        for prm in (4, 8, 4 | 256 * SHAPE, 8 | 128 * SHAPE, 8 | 256 * SHAPE, 104, 108, 112):
             plan = K.DevicePlan(a, K.UnsymKernel.u2_nnz, prm)
             y = np.full(n, np.nan)
             plan.apply(x, y)
             assert_close(y, yref, absax, (n, prm))
             ys[prm] = y
-        assert np.array_equal(ys[8], ys[208]) and np.array_equal(ys[8], ys[300]), n
+        assert np.array_equal(ys[8], ys[8 | 256 * SHAPE]), n
+        assert np.array_equal(ys[8], ys[8 | 128 * SHAPE]), n
+        assert np.array_equal(ys[4], ys[4 | 256 * SHAPE]), n
+
+
+def test_launch_shapes(K):
+    """The selector's launch-shape candidates: U1 warp-sliced at 64/128/256
+    threads (bitwise = spmv_ref), U3 warp tiles at 4/8 warps (bitwise equal
+    to each other), each plan reporting its shape; bad shapes are refused."""
+    n, rp, ci, v = matgen.stencil7(30, 20, 18, xp=-0.7, xm=-1.3)
+    a = K.CsrMatrix(n, rp, ci, v)
+    x = O.seeded_vector(n, 6)
+    yref = O.spmv_ref(n, rp, ci, v, x)
+    for t in (64, 128, 256):
+        for base in (100, 101):
+            p = K.DevicePlan(a, K.UnsymKernel.u1_row, base | t * SHAPE)
+            assert p.param == base | t * SHAPE
+            y = np.full(n, np.nan)
+            p.apply(x, y)
+            assert np.array_equal(y, yref), (base, t)
+    n, rp, ci, v = matgen.random_csr(4000, 0.003, np.random.default_rng(2), skew=True,
+                                     empty_frac=0.1)
+    a = K.CsrMatrix(n, rp, ci, v)
+    x = O.seeded_vector(n, 7)
+    yref, absax = O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x)
+    ys = []
+    for t in (128, 256):
+        y = np.full(n, np.nan)
+        K.DevicePlan(a, K.UnsymKernel.u3_bss, 1008 | t * SHAPE).apply(x, y)
+        assert_close(y, yref, absax, t)
+        ys.append(y)
+    assert np.array_equal(ys[0], ys[1])
+    for k, prm in ((K.UnsymKernel.u1_row, 4 | 128 * SHAPE), (K.UnsymKernel.u1_row, 100 | 96 * SHAPE),
+                   (K.UnsymKernel.u3_bss, 8 | 128 * SHAPE), (K.UnsymKernel.u2_nnz, 108 | 256 * SHAPE)):
+        with pytest.raises(K.Error):
+            K.DevicePlan(a, k, prm)
+
+
+def test_selector_times_launch_shapes_and_keeps_one_plan(K):
+    """ktb_select's candidate list crosses the reference's kernels with the
+    GPU variants and their CTA shapes (the GPU worker-count sweep); every
+    candidate runs <= 4 times; each reports its plan-setup seconds."""
+    n, rp, ci, v = matgen.stencil7(40, 40, 40)
+    a = K.CsrMatrix(n, rp, ci, v)
+    choice, rep = K.select_spmv_unsym(a)
+    shapes = {(c.name, c.cta_threads) for c in rep.candidates}
+    assert {("u1", 64), ("u1", 128), ("u1", 256), ("u2", 128), ("u2", 256),
+            ("u3", 128), ("u3", 256)} <= shapes
+    assert all(c.executions <= 4 for c in rep.candidates)
+    assert all(c.setup_seconds >= 0 for c in rep.candidates if c.correct)
+    x = O.seeded_vector(n, 1)
+    y = np.empty(n)
+    choice.plan.apply(x, y)
+    assert_close(y, O.spmv_ref(n, rp, ci, v, x), absax_of(n, rp, ci, v, x))
 
 
 def test_u1_warp_sliced_bitwise_reference(K):
@@ -483,38 +539,6 @@ def test_u1_warp_sliced_bitwise_reference(K):
     a = K.CsrMatrix(n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1])))
     with pytest.raises(Exception):
         K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
-
-
-def test_s3_in_kernel_merge_matches_fixup_kernel(K, monkeypatch):
-    """KTB_S3_MERGE=1 merges the spills into the head rows inside k_s3
-    (cooperative launch) and KTB_S3_FIXUP_GRID=1 runs the fixup as a
-    persistent two-deep kernel, both with k_s3_fixup's arithmetic: y is
-    bitwise equal to the default two-kernel path, on config 2 and on a small
-    matrix."""
-    import torch
-
-    cases = [(K.stencil27_upper(128, 128, 128), 2)]
-    n, rp, ci, v = matgen.stencil27_upper(40, 37, 30)
-    cases.append((K.SymCsrMatrix(n, rp, ci, v), 5))
-    for a, seed in cases:
-        x = torch.from_numpy(O.seeded_vector(a.n, seed)).cuda()
-        ys = []
-        for merge, grid in (("0", "0"), ("1", "0"), ("0", "1")):
-            monkeypatch.setenv("KTB_S3_MERGE", merge)
-            monkeypatch.setenv("KTB_S3_FIXUP_GRID", grid)
-            plan = K.DevicePlan(a, K.SymKernel.s3_nnz_zero_omit)
-            y = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
-            for _ in range(3):  # repeated applies reuse the published-spill flags
-                plan.apply(x, y)
-            torch.cuda.synchronize()
-            ys.append(y.cpu().numpy())
-            plan.close()
-        assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
-        if a.n < 100000:
-            erp, eci, ev = O.expand_symmetric(n, rp, ci, v)
-            xh = O.seeded_vector(a.n, seed)
-            assert_close(ys[0], O.spmv_ref(a.n, erp, eci, ev, xh),
-                         absax_of(a.n, erp, eci, ev, xh), "s3 merge")
 
 
 def test_u1_sorted_slices(K):
