@@ -254,9 +254,14 @@ def nccl_init_lines() -> list[str]:
     path = path.replace("%h", socket.gethostname().split(".")[0]).replace("%p", str(os.getpid()))
     try:
         with open(path) as f:
-            return [ln.strip() for ln in f if "Init COMPLETE" in ln or " nRanks " in ln]
+            lines = [ln.strip() for ln in f if "Init COMPLETE" in ln or " nRanks " in ln]
     except OSError:
-        return []
+        lines = []
+    if not lines:
+        print(f"[bench] no NCCL init line in NCCL_DEBUG_FILE={path!r} (exists "
+              f"{os.path.exists(path)}); NCCL_DEBUG={os.environ.get('NCCL_DEBUG')!r} "
+              f"SUBSYS={os.environ.get('NCCL_DEBUG_SUBSYS')!r}", file=sys.stderr)
+    return lines
 
 
 # ----------------------------------------------------------------- clocks

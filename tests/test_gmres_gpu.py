@@ -83,3 +83,47 @@ def test_gmres_both_mgs_kernels_and_config5(monkeypatch):
     r = K.gmres_m(a, bd.cpu().numpy(), K.KrylovConfig(30, 30, 1e-8, 3000), plan=plan)
     assert r.converged and abs(r.iterations - 653) <= 2 and r.true_residual < 1e-8
     assert r.spmv_calls == r.iterations + r.restarts + 2
+
+
+@pytest.mark.parametrize("stream_mgs", ["0", "1"])
+@pytest.mark.parametrize("kernel,param", [(0, 100), (1, 8)])
+def test_gmres_odd_n_unaligned_columns(monkeypatch, stream_mgs, kernel, param):
+    """Odd n: basis column j starts at V + j*n, only 8-byte aligned for odd j
+    (the L2 bulk prefetch must widen to 16-byte bounds). Both MGS
+    kernels, two SpMV kernels; against the C restatement."""
+    from paper_2405_01599_b200 import ktune as K
+
+    if stream_mgs == "1":
+        monkeypatch.setenv("KTB_GMRES_STREAM_MGS", "1")
+    n, rp, ci, v = matgen.stencil7(15, 13, 11, xp=-0.7, xm=-1.3)
+    assert n % 2 == 1
+    b = O.spmv_ref(n, rp, ci, v, np.ones(n))
+    xo, ro = O.gmres_mgs(n, rp, ci, v, b)
+    a = K.CsrMatrix(n, rp, ci, v)
+    plan = K.DevicePlan(a, kernel, param)
+    r = K.gmres_m(a, b, K.KrylovConfig(30, 30, 1e-8, 3000), plan=plan)
+    assert r.converged and abs(r.iterations - ro["iterations"]) <= 2
+    assert r.true_residual < 1e-8
+
+
+def test_s3_odd_n_unaligned_x():
+    """S3's x front prefetch on an 8-byte-aligned x (a basis-column-like
+    offset view): same y as on an aligned copy."""
+    import torch
+
+    from paper_2405_01599_b200 import ktune as K
+
+    n, rp, ci, v = matgen.stencil27_upper(23, 19, 17)
+    s = K.SymCsrMatrix(n, rp, ci, v)
+    plan = K.DevicePlan(s, K.SymKernel.s3_nnz_zero_omit)
+    x = O.seeded_vector(n, 2)
+    buf = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(x).cuda()
+    xa = torch.from_numpy(x).cuda()
+    y0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    y1 = torch.empty_like(y0)
+    plan.apply(xa, y0)
+    plan.apply(buf[1:], y1)  # data_ptr % 16 == 8
+    torch.cuda.synchronize()
+    assert buf[1:].data_ptr() % 16 == 8
+    assert torch.equal(y0, y1)

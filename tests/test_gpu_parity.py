@@ -272,10 +272,13 @@ def test_selector_unsym_and_sym(K):
     assert rep.selected >= 0 and rep.selected_candidate().correct
     assert rep.max_executions() <= 4
     names = [c.name for c in rep.candidates]
-    assert names[:4] == ["u1", "u1", "u1", "u2"] and set(names[4:]) == {"u3"}
-    assert all(c.correct for c in rep.candidates[3:])  # U2 and every U3 form
+    # U1 (lanes, warp-sliced x 3 CTA shapes, row-sorted x 3), U2 (warp tiles x
+    # 2 shapes, merge path), U3 (lanes per E, warp tiles x 2 shapes)
+    assert names[:10] == ["u1"] * 7 + ["u2"] * 3 and set(names[10:]) == {"u3"}
+    assert all(c.correct for c in rep.candidates[7:])  # U2 and every U3 form
     # param slot (reference name jl): the warp-sliced U1 and its row-sorted form
-    assert rep.candidates[1].jl == 100 and rep.candidates[2].jl == 101
+    assert [c.jl for c in rep.candidates[1:7]] == [100] * 3 + [101] * 3
+    assert [c.cta_threads for c in rep.candidates[1:7]] == [128, 64, 256] * 2
     x = O.seeded_vector(n, 1)
     y = np.empty(n)
     choice.plan.apply(x, y)
