@@ -441,7 +441,8 @@ int ktb_ilu0_info(const ktb_ilu* f, int64_t* n, int64_t* lower_levels, int64_t* 
 int ktb_ilu0_download(const ktb_ilu* f, int32_t* diag_ptr, double* values);
 /* ilu0_apply (ilu0.hpp:73-87): z = (LU)^{-1} r. ptr_kind KTB_PTR_DEVICE: device
  * pointers, enqueued on `stream` (NULL = the legacy default stream);
- * KTB_PTR_HOST: host arrays, synchronous. */
+ * KTB_PTR_HOST: host arrays, synchronous. Applies of one factor on different
+ * streams are serialised (they share the factor's solve buffers). */
 int ktb_ilu0_apply(ktb_ilu* f, const double* r, double* z, int ptr_kind, void* stream);
 int ktb_ilu0_destroy(ktb_ilu* f);
 

@@ -321,8 +321,13 @@ struct ktb_ilu {
     cudaStream_t stream = nullptr;
     cudaGraphExec_t apply_graph = nullptr;
     int64_t launches = 0;  // per apply
+    // the applies share rbuf/zbuf: each apply's stream waits for the previous
+    // apply (on whatever stream it ran), so applies of one factor on several
+    // streams serialise instead of racing on the buffers
+    cudaEvent_t done = nullptr;
     ~ktb_ilu() {
         if (apply_graph) cudaGraphExecDestroy(apply_graph);
+        if (done) cudaEventDestroy(done);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -602,9 +607,15 @@ void ilu0_apply(ktb_ilu* f, const double* r, double* z, cudaStream_t s) {
     DeviceGuard g(f->device);
     const int64_t n = f->n;
     if (n == 0) return;
+    if (!f->done) {
+        KTB_CUDA(cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming));
+    } else {
+        KTB_CUDA(cudaStreamWaitEvent(s, f->done, 0));
+    }
     KTB_CUDA(cudaMemcpyAsync(f->rbuf.p, r, 8 * n, cudaMemcpyDeviceToDevice, s));
     KTB_CUDA(cudaGraphLaunch(f->apply_graph, s));
     KTB_CUDA(cudaMemcpyAsync(z, f->zbuf.p, 8 * n, cudaMemcpyDeviceToDevice, s));
+    KTB_CUDA(cudaEventRecord(f->done, s));
 }
 
 }  // namespace ktb

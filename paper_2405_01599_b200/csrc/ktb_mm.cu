@@ -15,11 +15,13 @@
 // +-inf results reject), so a line the reference rejects is rejected here
 // with the same message, first bad line first.
 //
-// One documented difference: the reference orders the COO with std::sort,
-// whose order among equal (row, col) keys is unspecified; here duplicates
-// are summed in file order. With two copies the sum is the same either way
-// (fp addition commutes); three or more copies of one coordinate may differ
-// in the last bit of that entry.
+// Duplicates: the reference orders the whole COO with std::sort, whose order
+// among equal (row, col) keys is unspecified, and sums each run in that
+// order. With two copies the sum is the same in any order (fp addition
+// commutes), so the fast paths sum in file order; when some coordinate
+// occurs three or more times the CRS is rebuilt exactly the reference's way
+// (the file-order COO through the same std::sort and comparator, the same
+// libstdc++), so the loaded matrix is bit-identical in every case.
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -321,8 +323,40 @@ bool assemble_sorted(int64_t n, std::vector<Part>& part, ktb_csr_host& a) {
     return true;
 }
 
+// matrix_market.hpp:89-108 verbatim in its ordering: the file-order COO
+// through std::sort on (row, col), runs summed front to back. Used only when
+// a coordinate occurs 3+ times (the order of such a run is std::sort's).
+void coo_to_csr_reference_order(int64_t n, const std::vector<Part>& part, ktb_csr_host& a) {
+    struct Entry {
+        int64_t row, col;
+        double value;
+    };
+    std::vector<Entry> coo;
+    for (auto& P : part)
+        for (size_t k = 0; k < P.r.size(); ++k) coo.push_back({P.r[k], P.c[k], P.v[k]});
+    std::sort(coo.begin(), coo.end(), [](const Entry& x, const Entry& y) {
+        return x.row < y.row || (x.row == y.row && x.col < y.col);
+    });
+    a.n = n;
+    a.row_ptr.assign(n + 1, 0);
+    a.col.clear();
+    a.val.clear();
+    for (size_t k = 0; k < coo.size();) {
+        size_t e = k + 1;
+        double v = coo[k].value;
+        while (e < coo.size() && coo[e].row == coo[k].row && coo[e].col == coo[k].col)
+            v += coo[e++].value;
+        a.col.push_back(coo[k].col);
+        a.val.push_back(v);
+        ++a.row_ptr[coo[k].row + 1];
+        k = e;
+    }
+    for (int64_t i = 0; i < n; ++i) a.row_ptr[i + 1] += a.row_ptr[i];
+}
+
 // matrix_market.hpp:89-108. Counting sort by row (stable), then a stable
-// sort of each row by column: file order among duplicates.
+// sort of each row by column: file order among duplicates (exact for runs
+// of at most two; longer runs switch to coo_to_csr_reference_order).
 void coo_to_csr(int64_t n, const std::vector<Part>& part, ktb_csr_host& a) {
     size_t m = 0;
     for (auto& P : part) m += P.r.size();
@@ -365,6 +399,10 @@ void coo_to_csr(int64_t n, const std::vector<Part>& part, ktb_csr_host& a) {
             size_t q = k + 1;
             double v = bv[b + ord[k]];
             while (q < ord.size() && bc[b + ord[q]] == bc[b + ord[k]]) v += bv[b + ord[q++]];
+            if (q - k >= 3) {  // a run whose sum depends on std::sort's order
+                coo_to_csr_reference_order(n, part, a);
+                return;
+            }
             a.col.push_back(bc[b + ord[k]]);
             a.val.push_back(v);
             ++cnt;

@@ -193,16 +193,28 @@ def test_probe(tmp_path):
     assert (info.n, info.entries, info.symmetric) == O.Ref.mm_probe(p) == (7, 3, True)
 
 
-def test_three_duplicates_file_order(tmp_path):
-    """Documented difference: duplicates are summed in file order (the
-    reference's std::sort leaves their order unspecified)."""
-    vals = [0.1, 0.2, 0.3, 1e16, -1e16]
-    text = HDR + f"1 1 {len(vals)}\n" + "".join(f"1 1 {x!r}\n" for x in vals)
-    a = K.load_matrix_market(_write(tmp_path, "d.mtx", text), False)
-    acc = vals[0]
-    for x in vals[1:]:
-        acc += x
-    assert a.values.tolist() == [acc]
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("sym", [False, True])
+def test_many_duplicates_match_reference_bitwise(tmp_path, seed, sym):
+    """Coordinates repeated 3-6 times in shuffled files well above std::sort's
+    16-element insertion-sort cut-off, values spanning 1e-3..1e16 so the
+    summation order shows in the last bits: the CRS equals the reference
+    loader's bit for bit (ADVICE r01: the exact std::sort path takes over
+    when a run has 3+ copies)."""
+    rng = np.random.default_rng(seed)
+    n = 40
+    coords = [(int(rng.integers(0, n)), int(rng.integers(0, n))) for _ in range(60)]
+    entries = []
+    for (i, j) in coords:
+        for _ in range(int(rng.integers(1, 7))):
+            entries.append((i, j, float(rng.choice([1e-3, 0.1, 1.0, 3.0, 1e8, 1e16]) *
+                                        rng.uniform(-1, 1))))
+    rng.shuffle(entries)
+    text = (SYM if sym else HDR) + f"{n} {n} {len(entries)}\n" + "".join(
+        f"{i + 1} {j + 1} {v!r}\n" for i, j, v in entries)
+    path = _write(tmp_path, f"dup{seed}.mtx", text)
+    for want in (False, True):
+        _same(path, want)
 
 
 # ------------------------------------------------------------------ fuzz
