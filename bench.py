@@ -36,7 +36,8 @@ os.environ.setdefault("OMP_PROC_BIND", "close")
 os.environ.setdefault("OMP_PLACES", "cores")
 # the NCCL communicator init line (nranks, devices) goes to a per-process log
 # that bench.py re-emits on stderr and in the JSON line
-os.environ.setdefault("NCCL_DEBUG", "INFO")
+if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+    os.environ["NCCL_DEBUG"] = "INFO"  # the image sets VERSION
 os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/ktb_bench_nccl.{os.getpid()}.log")
 import socket  # noqa: E402
