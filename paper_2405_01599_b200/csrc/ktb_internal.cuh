@@ -221,10 +221,6 @@ struct SymWindowLayout {
     DBuf<double> spill;
     DBuf<int32_t> segs;        // fixup block descriptors (3 int4 each, see s3_setup)
     DBuf<int32_t> seg_src;     // per fixup block: its spilling sources, ascending
-    DBuf<int32_t> seg_dst;     // per fixup block: the block whose head rows it finishes
-    DBuf<int> done;            // per block: epoch of its last completed apply
-    int epoch = 0;
-    bool use_flags = true;     // fixup waits per block (false: whole grid)
     int64_t nsegs = 0;
     int reach = 0;             // max(col - row), clipped to the window
     int64_t nlong = 0;         // rows too long for the round layout

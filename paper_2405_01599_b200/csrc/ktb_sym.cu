@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
          const int64_t* __restrict__ cta_base, const double* __restrict__ diag,
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
-         double* __restrict__ spill, int* __restrict__ done, int epoch) {
+         double* __restrict__ spill) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
@@ -455,12 +455,6 @@ __global__ void __launch_bounds__(kS3Threads, 1)
         for (int32_t j = R1 + tid; j < hi; j += kS3Threads)
             st_hint_f64(spill + so + (j - R1), win[(j - R0) % W], keep);
     }
-    if (done) {  // publish: this block's y rows and spill are written (the
-                 // fixup blocks that read them start as soon as they see it)
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release_gpu(done + c, epoch);
-    }
 }
 
 // Head rows of block d receive the spills of earlier blocks, summed in
@@ -477,30 +471,13 @@ __global__ void __launch_bounds__(256, KTB_S3_FIXUP_MINB) k_s3_fixup(const int4*
                                                   const int32_t* __restrict__ spill_hi,
                                                   const int64_t* __restrict__ spill_off,
                                                   const double* __restrict__ spill,
-                                                  double* __restrict__ y,
-                                                  const int32_t* __restrict__ seg_dst,
-                                                  const int* __restrict__ done, int epoch) {
+                                                  double* __restrict__ y) {
     constexpr int U = kFixRows / 256;
     // plan data, readable before the dependency resolves: rows [j0, j1), the
     // number of sources spilling into them (ascending), the first two
     // sources' ranges and spill bases inline
     const int4 a = desc[3 * blockIdx.x], b = desc[3 * blockIdx.x + 1], c = desc[3 * blockIdx.x + 2];
-    if (done) {
-        // wait only for the k_s3 blocks this segment reads -- its destination
-        // (head rows) and its sources (spills) -- not the whole grid: the
-        // segments of early-finishing blocks run beside k_s3's stragglers on
-        // the SMs their blocks vacated
-        if (threadIdx.x == 0) {
-            auto wait = [&](int blk) {
-                while (ld_acquire_gpu(done + blk) != epoch) __nanosleep(64);
-            };
-            wait(seg_dst[blockIdx.x]);
-            for (int k = 0; k < a.z; ++k) wait(seg_src[a.w + k]);
-        }
-        __syncthreads();
-    } else {
-        asm volatile("griddepcontrol.wait;" ::: "memory");  // k_s3 complete and visible
-    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_s3 complete and visible
     const int32_t j0 = a.x, j1 = a.y, ns = a.z;
     const int64_t base0 = static_cast<int64_t>(
         static_cast<uint64_t>(static_cast<uint32_t>(c.x)) | (static_cast<uint64_t>(c.y) << 32));
@@ -814,7 +791,7 @@ void s3_setup(ktb_plan* p) {
     // fixup blocks: <= kFixRows head rows of one destination each, with the
     // sources whose spill range meets them (ascending) -- 3 int4 per block:
     // (j0, j1, nsrc, list offset), (s0, hi) x 2, spill base (off - s0) x 2
-    std::vector<int32_t> segs, seg_src, seg_dst;
+    std::vector<int32_t> segs, seg_src;
     for (int d = 0; d < P; ++d)
         for (int32_t j = bnd[d]; j < head_end[d]; j += kFixRows) {
             const int32_t j1 = std::min<int32_t>(head_end[d], j + kFixRows);
@@ -836,7 +813,6 @@ void s3_setup(ktb_plan* p) {
                                    static_cast<int32_t>(base[1] & 0xffffffff),
                                    static_cast<int32_t>(base[1] >> 32)};
             segs.insert(segs.end(), v, v + 12);
-            seg_dst.push_back(d);
         }
     L.nsegs = static_cast<int64_t>(segs.size() / 12);
 
@@ -868,13 +844,6 @@ void s3_setup(ktb_plan* p) {
     L.spill.alloc(std::max<int64_t>(so, 1));
     up32(L.segs, segs);
     up32(L.seg_src, seg_src);
-    up32(L.seg_dst, seg_dst);
-    {  // KTB_S3_FLAGS=0: the fixup waits for the whole k_s3 grid (griddepcontrol)
-        const char* env = std::getenv("KTB_S3_FLAGS");
-        L.use_flags = !(env && env[0] == '0');
-        L.done.alloc(P);
-        KTB_CUDA(cudaMemsetAsync(L.done.p, 0, sizeof(int) * P, st));
-    }
     // far entries (both products) and long rows (row sum incl. diagonal and
     // transposed products) as contributions grouped by target row; the
     // stable sort keeps each target's contributions in a fixed order
@@ -931,12 +900,10 @@ void s3_setup(ktb_plan* p) {
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     const size_t smem = kS3SmemFixed + static_cast<size_t>(L.window) * 8;
-    const bool flags = L.use_flags && L.nsegs;
-    const int epoch = ++L.epoch;
     k_s3<<<L.ctas, kS3Threads, smem, p->stream>>>(
         L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p, L.cta_base.p,
         L.diag.p, x, y, L.window, L.reach, static_cast<int>(p->m->n), L.spill_hi.p,
-        L.spill_off.p, L.spill.p, flags ? L.done.p : nullptr, epoch);
+        L.spill_off.p, L.spill.p);
     KTB_LAUNCH();
     if (L.nsegs) {  // the fixup's blocks launch early and wait for k_s3 (PDL)
         cudaLaunchConfig_t cfg{};
@@ -953,9 +920,7 @@ void s3_run(ktb_plan* p, const double* x, double* y) {
                                     static_cast<const int32_t*>(L.cta_row.p),
                                     static_cast<const int32_t*>(L.spill_hi.p),
                                     static_cast<const int64_t*>(L.spill_off.p),
-                                    static_cast<const double*>(L.spill.p), y,
-                                    static_cast<const int32_t*>(L.seg_dst.p),
-                                    static_cast<const int*>(flags ? L.done.p : nullptr), epoch));
+                                    static_cast<const double*>(L.spill.p), y));
     }
     if (L.npatch) {
         k_s3_patch<<<ceil_div(L.npatch, 8), 256, 0, p->stream>>>(
