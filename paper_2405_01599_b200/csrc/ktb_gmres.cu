@@ -32,9 +32,9 @@ constexpr int kGThreads = 512;
 __device__ __forceinline__ double block_sum(double v, double* red) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
+    KTB_SYNC();
     if (l == 0) red[w] = v;
-    __syncthreads();
+    KTB_SYNC();
     double s = 0.0;
     if (threadIdx.x == 0)
         for (int k = 0; k < kGThreads / 32; ++k) s += red[k];
@@ -134,6 +134,7 @@ constexpr int kRThreads = KTB_MGS_THREADS;
 constexpr int kMaxPart = 8;  // nb <= 256
 
 __device__ __forceinline__ void publish(double2* slot, double v, long long tag) {
+    KTB_CHAOS_DELAY(0x7075);
     __stcg(slot, make_double2(v, __longlong_as_double(tag)));
 }
 
@@ -148,6 +149,7 @@ __device__ __forceinline__ double poll_total(const double2* slot, int nb, long l
         if (lane + 32 * m < nb) pending |= 1u << m;
     }
     while (pending) {
+        KTB_CHAOS_DELAY(0x706f);
 #pragma unroll
         for (int m = 0; m < kMaxPart; ++m) {
             if ((pending >> m) & 1u) {
@@ -178,7 +180,7 @@ __device__ __forceinline__ void block_sum_w0(double& a, double& b, double* red) 
         red[2 * w] = a;
         red[2 * w + 1] = b;
     }
-    __syncthreads();
+    KTB_SYNC();
     if (threadIdx.x < 32) {
         a = l < blockDim.x / 32 ? red[2 * l] : 0.0;
         b = l < blockDim.x / 32 ? red[2 * l + 1] : 0.0;
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
             bc[1] = t1;
         }
     }
-    __syncthreads();
+    KTB_SYNC();
     const double in2 = bc[0];
     double c = bc[1];
     for (int q = 0; q < k; ++q) {
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
             const double t = poll_total(sl, nb, tag0 + q + 2);
             if (tid == 0) bc[0] = t;
         }
-        __syncthreads();
+        KTB_SYNC();
         c = bc[0];
     }
     const double nrm = sqrt(c);

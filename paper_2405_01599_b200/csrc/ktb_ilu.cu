@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "ktb_internal.cuh"
+#include "ktb_ptx.cuh"
 
 namespace ktb {
 
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kRunThreads) k_ilu_run(const int32_t* __restri
         const int32_t b = lev_ptr[l], e = lev_ptr[l + 1];
         for (int32_t t = b + threadIdx.x; t < e; t += kRunThreads)
             ilu_row<OP>(rows[t], rp, col, val, diag, r, z, err);
-        __syncthreads();  // this level's rows are final for the next
+        KTB_SYNC();  // this level's rows are final for the next
     }
 }
 
@@ -250,10 +251,14 @@ __global__ void __launch_bounds__(kClThreads, 1)
 #if KTB_ILU_SPLIT_BARRIER
         // split-phase: the arrive releases this level's z stores, the next
         // record's loads go out between arrive and wait
+        KTB_CHAOS_DELAY(0x696c);
+        __syncwarp();
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 #else
+        KTB_CHAOS_DELAY(0x696d);
+        __syncwarp();
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
         if (l + 1 < nlev && nb + g < ne) load(nb + g, nxt);
         asm volatile("barrier.cluster.arrive.relaxed.aligned;\n"

@@ -6,6 +6,47 @@
 
 namespace ktb {
 
+// ---- race stress build (KTB_CHAOS, libktb_chaos.so) ------------------------
+// compute-sanitizer is unavailable on the GPU pool, so the hand-synchronised
+// kernels (S3's TMA/mbarrier ring and window rounds, the MGS tag exchange, the
+// ILU cluster sweep, the warp-tile carries) are stressed instead: every
+// barrier, mbarrier wait and cross-CTA publish/poll is preceded by a
+// pseudo-random per-thread sleep (0-2 us on 1 call in 4), which reorders
+// warps, lanes and CTAs far beyond normal jitter, and KTB_DCHECK bounds
+// checks trap. tests/test_chaos_gpu.py runs this build and requires results
+// bitwise equal to the normal build's (a missing barrier or fence shows up
+// as a wrong or non-reproducible y). Compiled out otherwise.
+#ifdef KTB_CHAOS
+__device__ __forceinline__ void chaos_delay(uint32_t salt) {
+    uint32_t h = static_cast<uint32_t>(clock64()) ^ (salt * 0x9e3779b9u) ^
+                 (blockIdx.x * 0x85ebca6bu) ^ (threadIdx.x * 0xc2b2ae35u);
+    h ^= h >> 16;
+    h *= 0x7feb352du;
+    h ^= h >> 15;
+    if ((h & 3) == 0) __nanosleep((h >> 16) & 2047);
+}
+#define KTB_CHAOS_DELAY(salt) ::ktb::chaos_delay(static_cast<uint32_t>(salt))
+#define KTB_DCHECK(c)        \
+    do {                     \
+        if (!(c)) __trap();  \
+    } while (0)
+// a block-wide barrier reached by every thread: delay, reconverge, sync
+#define KTB_SYNC()                     \
+    do {                               \
+        KTB_CHAOS_DELAY(__LINE__);     \
+        __syncwarp();                  \
+        __syncthreads();               \
+    } while (0)
+#else
+#define KTB_CHAOS_DELAY(salt) \
+    do {                      \
+    } while (0)
+#define KTB_DCHECK(c) \
+    do {              \
+    } while (0)
+#define KTB_SYNC() __syncthreads()
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -36,6 +77,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    KTB_CHAOS_DELAY(0x6d62);
     asm volatile(
         "{\n"
         ".reg .pred p;\n"

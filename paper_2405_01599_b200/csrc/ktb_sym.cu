@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
         }
     }
     for (int k = tid; k < W; k += kS3Threads) win[k] = 0.0;
-    __syncthreads();
+    KTB_SYNC();
     // let the fixup grid launch early (programmatic dependent launch): its
     // blocks take SMs as these retire and wait for this grid's completion
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -332,11 +332,11 @@ __global__ void __launch_bounds__(kS3Threads, 1)
         // prologue: chunks 0..kGD landed and visible; gather 0..kGD-1
         if (tid == 0)
             for (int k = 0; k <= kGD && k < Q; ++k) mbar_wait(&full[k], 0);
-        __syncthreads();
+        KTB_SYNC();
         static_assert(kGD >= 1 && kGD <= 2, "prologue gathers kGD chunks");
         gather(0, std::integral_constant<int, 0>{});
         if (kGD > 1) gather(1, std::integral_constant<int, 1>{});
-        __syncthreads();
+        KTB_SYNC();
         if (tid == 0)
             for (int k = 0; k < kGD && k + kStages < Q; ++k) {
                 fence_proxy_async_smem();
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
             gather(q + kGD, std::integral_constant<int, KG>{});  // padded meta: always valid
             const int m = mr[K];
             if (meta_empty(m)) {  // padding chunk: keep the barrier cadence only
-                __syncthreads();
+                KTB_SYNC();
                 return;
             }
             if (meta_round(m) == 0) {  // this sub-tile's diagonal, next one's x_i, the x front
@@ -385,6 +385,8 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                 sc[u] = cu >= 0;
                 rowsum[u] += sc[u] ? vr[K][u] * xr[K][u] : 0.0;
                 sl[u] = wrap(cu + off, W);
+                KTB_DCHECK(!sc[u] || (sl[u] >= 0 && sl[u] < W));
+                KTB_DCHECK(!sc[u] || a + cu < n);
 #if !(KTB_S3_ABL & 2)
                 if (sc[u]) wv[u] = win[sl[u]];
 #endif
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
 #if KTB_S3_ABL & 4
             if (q + kGD + 1 < Q) mbar_wait(&full[KW], wph ^ (KW <= K ? 1 : 0));  // ablation: no barrier
 #else
-            __syncthreads();
+            KTB_SYNC();
 #endif
             if (tid == 0) {
                 if (pend >= 0) {  // the refill deferred by the previous round
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(kS3Threads, 1)
                     rowsum[u] = 0.0;
                     xi[u] = xin[u];
                 }
-                __syncthreads();
+                KTB_SYNC();
                 off = wrap(off + kRows, W);
                 a += kRows;
             }

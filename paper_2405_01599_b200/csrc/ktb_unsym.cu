@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
         if (i < nrows) s_end[i] = ldg_i32(rp + c0.row + 1 + i);
     }
     if (tid == 0) s_end[nrows] = 0x7fffffff;  // the open row at tile end never closes here
-    __syncthreads();
+    KTB_SYNC();
 
     // this thread's merge-path start inside the tile
     const int diag = min(tid * IPT, nrows + nnzs);
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
     }
     SegPair agg;
     const SegPair pre = block_seg_scan_excl<kU2Threads>(SegPair{nemit > 0, run}, &agg);
-    __syncthreads();  // s_prod is reused for row outputs below
+    KTB_SYNC();  // s_prod is reused for row outputs below
     bool first = true;
 #pragma unroll
     for (int it = 0; it < IPT; ++it) {
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kU2Threads) k_u2(const int32_t* __restrict__ r
             first = false;
         }
     }
-    __syncthreads();
+    KTB_SYNC();
     for (int i = tid; i < nrows; i += kU2Threads) y[c0.row + i] = s_prod[i];
     if (tid == 0) {
         carry_row[blockIdx.x] = c1.row;
@@ -1216,7 +1216,7 @@ __global__ void __launch_bounds__(kU3Threads) k_u3(const int32_t* __restrict__ c
     __shared__ typename BS::TempStorage scan_tmp;
     int qpre = 0, qtot = 0;
     BS(scan_tmp).ExclusiveSum(nf, qpre, qtot);
-    __syncthreads();
+    KTB_SYNC();
     int64_t q = static_cast<int64_t>(tile_q[t]) + qpre;  // flags strictly before a
 
     // walk: close the open segment at each row start (flag), emit complete rows

@@ -8,6 +8,7 @@
 // ordered pass over the block partials. The multi-vector forms work on a
 // column-major basis V (column j at V + j*ldv).
 #include "ktb_internal.cuh"
+#include "ktb_ptx.cuh"
 
 namespace ktb {
 
@@ -20,9 +21,9 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();  // sh reused across calls
+    KTB_SYNC();  // sh reused across calls
     if (lane == 0) sh[warp] = v;
-    __syncthreads();
+    KTB_SYNC();
     double s = 0.0;
     if (threadIdx.x == 0)
         for (int k = 0; k < kVecThreads / 32; ++k) s += sh[k];
