@@ -267,6 +267,7 @@ ktb_matrix* matrix_slice(const ktb_matrix* m, int64_t r0, int64_t r1) {
         out->sm_count = m->sm_count;
         out->n = r1 - r0;
         out->ncols = m->ncols;
+        out->col_shift = m->col_shift + r0;
         out->nnz = z[1] - z[0];
         out->kind = KTB_GENERAL;
         out->row_ptr.alloc(out->n + 1);
@@ -660,6 +661,7 @@ ktb_matrix* gen_stencil7(int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t
     m->kind = KTB_GENERAL;
     const bool has_lo = slab && z0 > 0, has_hi = slab && z1 < nz;
     m->ncols = slab ? nrows + (has_lo ? plane : 0) + (has_hi ? plane : 0) : nrows;
+    m->col_shift = has_lo ? plane : 0;
     const int64_t col_base = slab ? z0 * plane - (has_lo ? plane : 0) : 0;
     cudaStream_t s = 0;
     DBuf<int32_t> len(nrows + 1);

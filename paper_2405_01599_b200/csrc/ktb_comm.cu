@@ -936,6 +936,7 @@ int ktb_halo_create_csr(int64_t n_global, int64_t row0, int64_t n_local, const i
         for (auto& c : loc) c -= lo;
         std::unique_ptr<ktb_matrix> m(
             matrix_create_rect(n_local, hi - lo, row_ptr, loc.data(), values, comm->device));
+        m->col_shift = row0 - lo;
         *out = halo_create(m.get(), row0 - lo, hi - row0 - n_local, comm, kernel, param);
     });
 }

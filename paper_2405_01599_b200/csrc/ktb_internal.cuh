@@ -108,6 +108,7 @@ struct ktb_matrix {
     int device = 0;
     int64_t n = 0, nnz = 0;
     int64_t ncols = 0;  // == n except for halo slabs (config 4 sharding)
+    int64_t col_shift = 0;  // x index of row r's own entry is r + col_shift (halo slabs, slices)
     int kind = KTB_GENERAL;
     int64_t max_row_nnz = 0;
     int64_t bandwidth = 0;  // max(col - row) over stored entries (>= 0 for sym upper)
@@ -239,6 +240,7 @@ struct ktb_plan {
     int kernel = KTB_U1;
     int64_t param = 0;
     int cta_threads = 0;  // launch shape (param bits 16..31); 0 = the kernel's default
+    bool x_prefetch = true;  // U1 warp-sliced: pull each CTA's own x rows into L2 first
     int workers = 1;
     cudaStream_t stream = nullptr;
     bool own_stream = false;

@@ -144,8 +144,18 @@ __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* _
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
                                              int32_t row_begin, int32_t row_end, int ell,
-                                             const int32_t* __restrict__ perm) {
+                                             const int32_t* __restrict__ perm, int64_t xpf,
+                                             int64_t xlen) {
     const int lane = threadIdx.x & 31;
+    if (xpf >= 0 && threadIdx.x == 0) {
+        // x entries of this CTA's own rows into L2 while the first column /
+        // value loads are in flight: the gathers (own rows and the rows of the
+        // CTAs running beside it) then find x in L2 instead of making a
+        // second DRAM round trip (xpf = the rows' column shift; -1 = off)
+        const int64_t r0 = static_cast<int64_t>(row_begin & ~31) + blockIdx.x * int64_t(kThreads);
+        const int64_t lo = max(r0 + xpf, int64_t(0)), hi = min(r0 + kThreads + xpf, xlen);
+        if (hi > lo) prefetch_l2_range(x + lo, x + hi);
+    }
     const int64_t s = (row_begin >> 5) + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
     int64_t row = s * 32 + lane;
     if (s * 32 >= row_end) return;
@@ -451,6 +461,10 @@ void u1_setup(ktb_plan* p) {
                  (p->cta_threads == 64 || p->cta_threads == 128 || p->cta_threads == 256)),
             "u1: only the warp-sliced forms (params 100, 101) take a CTA shape: 64, 128 or 256 "
             "threads");
+    {  // KTB_U1S_XPF=0 turns the x prefetch off (A/B measurements)
+        const char* e = std::getenv("KTB_U1S_XPF");
+        p->x_prefetch = !(e && e[0] == '0');
+    }
     if (p->param == 100) {
         u1_sell_setup(p);
         p->launches = 1;
@@ -472,20 +486,23 @@ void u1_setup(ktb_plan* p) {
 static void launch_u1s(ktb_plan* p, int64_t threads, const int64_t* soff, const double* x,
                        double* y, int32_t r0, int32_t r1, int ell, const int32_t* perm) {
     const int t = p->cta_threads ? p->cta_threads : kU1sThreads;
+    // x prefetch: row-ordered slices only (the sorted form permutes rows)
+    const int64_t xpf = (!perm && p->x_prefetch) ? p->m->col_shift : -1;
+    const int64_t xlen = p->m->ncols;
     const int grid = ceil_div(threads, t);
     p->ctas = grid;
     switch (t) {
         case 64:
             k_u1s<64><<<grid, 64, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0, r1,
-                                                  ell, perm);
+                                                  ell, perm, xpf, xlen);
             break;
         case 128:
             k_u1s<128><<<grid, 128, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0,
-                                                    r1, ell, perm);
+                                                    r1, ell, perm, xpf, xlen);
             break;
         case 256:
             k_u1s<256><<<grid, 256, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0,
-                                                    r1, ell, perm);
+                                                    r1, ell, perm, xpf, xlen);
             break;
         default: throw Invalid("u1: warp-sliced CTAs are 64, 128 or 256 threads");
     }
