@@ -881,7 +881,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
         if (m->kind == KTB_SYM_UPPER) {
             add(KTB_S1, 0, "s1", 0);
             add(KTB_S2, 0, "s2", 1);
-            add(KTB_S3, 0, "s3", 2);
+            for (int t : {256, 512}) add(KTB_S3, 0, "s3", 2, t);
         } else {
             add(KTB_U1, 0, "u1", 0);
             for (int t : {128, 64, 256}) add(KTB_U1, 100, "u1", 0, t);  // warp-sliced copy

@@ -153,12 +153,8 @@ void s12_run(ktb_plan* p, const double* x, double* y) {
 // by one block barrier. The part of each block's region beyond the block
 // (the spill) goes to a global buffer; k_s3_fixup adds it into the next
 // blocks' head rows in ascending source order (deterministic).
-#ifndef KTB_S3_THREADS
-#define KTB_S3_THREADS 256  // x 8 rows: measured 77.5-77.7 us vs 79.1-79.4 us for 512 x 4 (config 2)
-#endif
-constexpr int kS3Threads = KTB_S3_THREADS;  // threads per block (one block per SM)
-constexpr int kRPT = 2048 / kS3Threads;     // rows per thread: t + kS3Threads*u
-constexpr int kRows = kS3Threads * kRPT;  // rows per sub-tile (2048)
+constexpr int kRows = 2048;  // rows per sub-tile; CTA shape 256 x 8 (77.5-77.7 us on config
+                             // 2) or 512 x 4 (79.1-79.4 us), a template parameter of k_s3
 #ifndef KTB_S3_GD
 #define KTB_S3_GD 1
 #endif
@@ -177,13 +173,14 @@ constexpr int kS3SmemFixed = kStages * kStageBytes + kStages * 8 + 128;
 constexpr int kFixRows = KTB_S3_FIXROWS;  // rows per fixup block (kFixRows / 256 per thread)
 
 // host-side positions of sub-tile row t in a round's value / column arrays
-inline int64_t s3_val_pos(int t) {
-    const int th = t % kS3Threads, u = t / kS3Threads;
-    return (static_cast<int64_t>(u / 2) * kS3Threads + th) * 2 + (u % 2);
+// for a CTA of T threads (T rows per u, 2048 / T rows per thread)
+inline int64_t s3_val_pos(int t, int T) {
+    const int th = t % T, u = t / T;
+    return (static_cast<int64_t>(u / 2) * T + th) * 2 + (u % 2);
 }
-inline int64_t s3_col_pos(int t) {
-    const int th = t % kS3Threads, u = t / kS3Threads;
-    return static_cast<int64_t>(th) * kRPT + u;
+inline int64_t s3_col_pos(int t, int T) {
+    const int th = t % T, u = t / T;
+    return static_cast<int64_t>(th) * (kRows / T) + u;
 }
 
 // column u (sign-extended int16) from its packed word
@@ -221,7 +218,10 @@ __device__ __forceinline__ bool meta_empty(int m) { return m & kMetaEmpty; }
 // that follows the stage's copy into registers. Register ring slot and smem
 // stage of chunk q are both q % kStages, so every shared-memory offset below
 // is a compile-time constant of the unrolled loop.
-__global__ void __launch_bounds__(kS3Threads, 1)
+// Launch shapes: 256 threads x 8 rows (default) or 512 x 4 (the selector
+// times both; plan param bits 16.., the SELL positions follow the shape).
+template <int kS3T>
+__global__ void __launch_bounds__(kS3T, 1)
     k_s3(const int32_t* __restrict__ cta_row, const int32_t* __restrict__ cta_chunk,
          const int32_t* __restrict__ chunk_meta, const int32_t* __restrict__ cta_qreal,
          const unsigned char* __restrict__ sell,
@@ -229,6 +229,8 @@ __global__ void __launch_bounds__(kS3Threads, 1)
          const double* __restrict__ x, double* __restrict__ y, int W, int reach, int n,
          const int32_t* __restrict__ spill_hi, const int64_t* __restrict__ spill_off,
          double* __restrict__ spill) {
+    constexpr int kS3Threads = kS3T;           // this instantiation's shape
+    constexpr int kRPT = kRows / kS3T;         // rows per thread: t + kS3Threads*u
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     double* win = reinterpret_cast<double*>(smem + kS3SmemFixed);
@@ -552,6 +554,9 @@ void s3_setup(ktb_plan* p) {
     auto& L = p->sw;
     cudaStream_t st = p->stream;
     const int S = kRows;
+    require(p->cta_threads == 0 || p->cta_threads == 256 || p->cta_threads == 512,
+            "s3: CTAs of 256 or 512 threads");
+    const int T3 = p->cta_threads == 512 ? 512 : 256;
     const int64_t n = m->n, nnz = m->nnz;
     const int P = std::max(1, m->sm_count);
     L.ctas = P;
@@ -693,8 +698,8 @@ void s3_setup(ktb_plan* p) {
             for (int32_t t = 0; t < rows; ++t)
                 for (auto [r, k] : assign[t]) {
                     unsigned char* ch = &o.sell[(basei + pos_of[r]) * kStageBytes];
-                    reinterpret_cast<double*>(ch)[s3_val_pos(t)] = val[k];
-                    reinterpret_cast<int16_t*>(ch + kRows * 8)[s3_col_pos(t)] =
+                    reinterpret_cast<double*>(ch)[s3_val_pos(t, T3)] = val[k];
+                    reinterpret_cast<int16_t*>(ch + kRows * 8)[s3_col_pos(t, T3)] =
                         static_cast<int16_t>(col[k] - a);  // < W <= 32767
                 }
             o.slots += static_cast<int64_t>(R) * S;
@@ -886,7 +891,8 @@ void s3_setup(ktb_plan* p) {
     }
     upd(L.diag, sdiag);
     KTB_CUDA(cudaStreamSynchronize(st));
-    KTB_CUDA(cudaFuncSetAttribute(k_s3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KTB_CUDA(cudaFuncSetAttribute(T3 == 512 ? k_s3<512> : k_s3<256>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kS3SmemFixed + W * 8)));
     p->ctas = P;
     // (round 1 also carried an in-kernel cooperative merge, 85.2 vs 82.9 us,
@@ -902,7 +908,8 @@ void s3_setup(ktb_plan* p) {
 void s3_run(ktb_plan* p, const double* x, double* y) {
     auto& L = p->sw;
     const size_t smem = kS3SmemFixed + static_cast<size_t>(L.window) * 8;
-    k_s3<<<L.ctas, kS3Threads, smem, p->stream>>>(
+    auto kern = p->cta_threads == 512 ? k_s3<512> : k_s3<256>;
+    kern<<<L.ctas, p->cta_threads == 512 ? 512 : 256, smem, p->stream>>>(
         L.cta_row.p, L.cta_chunk.p, L.chunk_meta.p, L.cta_qreal.p, L.sell.p, L.cta_base.p,
         L.diag.p, x, y, L.window, L.reach, static_cast<int>(p->m->n), L.spill_hi.p,
         L.spill_off.p, L.spill.p);

@@ -149,6 +149,11 @@ def test_s3_is_deterministic(K):
     y0 = _run_sym(K, a, "s3_nnz_zero_omit", x)
     for _ in range(3):
         assert np.array_equal(_run_sym(K, a, "s3_nnz_zero_omit", x), y0)
+    # both CTA shapes (256 x 8, 512 x 4 rows): same rounds, same sums
+    for t in (256, 512):
+        y = np.full(n, np.nan)
+        K.DevicePlan(a, K.SymKernel.s3_nnz_zero_omit, t << 16).apply(x, y)
+        assert np.array_equal(y, y0), t
 
 
 def test_random_families_all_variants(K):
@@ -286,7 +291,8 @@ def test_selector_unsym_and_sym(K):
     n, rp, ci, v = matgen.stencil27_upper(16, 16, 16)
     s = K.SymCsrMatrix(n, rp, ci, v)
     choice, rep = K.select_spmv_sym(s)
-    assert [c.name for c in rep.candidates] == ["s1", "s2", "s3"]
+    assert [c.name for c in rep.candidates] == ["s1", "s2", "s3", "s3"]
+    assert [c.cta_threads for c in rep.candidates[2:]] == [256, 512]
     assert all(c.correct for c in rep.candidates)
 
 
