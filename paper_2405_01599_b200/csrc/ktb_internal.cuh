@@ -265,6 +265,9 @@ struct ktb_plan {
     ktb::DBuf<int32_t> sell_col;        // -1 = padding
     ktb::DBuf<double> sell_val;
     int ell_width = 0;                  // > 0: every slice has this width (offsets implicit)
+    // U1 param 102: column-delta dictionary (16 int32 per slice) and 4-bit codes
+    ktb::DBuf<uint32_t> sell_codes;
+    ktb::DBuf<int32_t> sell_dict;
     // U1 param 101: rows sorted by length into the slices (slot -> row), rows
     // longer than the slice cap in a compact sub-matrix run by U2 warp tiles
     ktb::DBuf<int32_t> sell_perm;

@@ -43,6 +43,12 @@ __device__ __forceinline__ double ld_stream_f64(const double* p) {
                  : "=d"(r) : "l"(p), "l"(pol_first()));
     return r;
 }
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(r) : "l"(p), "l"(pol_first()));
+    return r;
+}
 __device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p) {
     int32_t r;
     asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
@@ -138,14 +144,22 @@ constexpr int kU1sThreads = KTB_U1S_THREADS;
 #endif
 // CTA shape: 64, 128 (default) or 256 threads, all instantiated; the
 // selector times them as launch-shape candidates (p->cta_threads)
-template <int kThreads>
+//
+// kDict (U1 param 102): the same slices with the columns coded, not stored:
+// each slice keeps a dictionary of at most 15 column deltas (col - row; a
+// stencil row has 7) and every slot a 4-bit code (15 = padding), 8 codes per
+// 32-bit word, so a slot streams 8 B of value + 0.5 B of code instead of
+// 8 + 4 B; the column is row + dict[code] (one warp shuffle). Same entries,
+// same order, same arithmetic: y stays bitwise equal to spmv_ref.
+template <int kThreads, bool kDict>
 __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* __restrict__ soff,
                                              const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const double* __restrict__ x, double* __restrict__ y,
                                              int32_t row_begin, int32_t row_end, int ell,
                                              const int32_t* __restrict__ perm, int64_t xpf,
-                                             int64_t xlen) {
+                                             int64_t xlen, const uint32_t* __restrict__ codes,
+                                             const int32_t* __restrict__ dict) {
     const int lane = threadIdx.x & 31;
     if (xpf >= 0 && threadIdx.x == 0) {
         // x entries of this CTA's own rows into L2 while the first column /
@@ -171,6 +185,12 @@ __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* _
     }
     const int32_t* sc = scol + o + lane;
     const double* sv = sval + o + lane;
+    int32_t dv = 0;
+    const uint32_t* cw = nullptr;
+    if constexpr (kDict) {
+        dv = __ldg(dict + s * 16 + (lane & 15));  // lane j < 15 holds delta j
+        cw = codes + (o >> 3) + (lane >> 3);      // 4 words per 32 slots
+    }
     double sum = 0.0;
     for (int k0 = 0; k0 < W; k0 += kSellUnroll) {
         int32_t c[kSellUnroll];
@@ -178,7 +198,14 @@ __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* _
 #pragma unroll
         for (int u = 0; u < kSellUnroll; ++u) {
             const bool ok = k0 + u < W;  // warp-uniform
-            c[u] = ok ? ld_stream_i32(sc + (k0 + u) * 32) : -1;
+            if constexpr (kDict) {
+                const uint32_t wd = ok ? ld_stream_u32(cw + (k0 + u) * 4) : 0xffffffffu;
+                const int code = static_cast<int>((wd >> ((lane & 7) * 4)) & 15u);
+                const int32_t d = __shfl_sync(0xffffffffu, dv, code);
+                c[u] = code != 15 ? static_cast<int32_t>(row) + d : -1;
+            } else {
+                c[u] = ok ? ld_stream_i32(sc + (k0 + u) * 32) : -1;
+            }
             v[u] = ok ? ld_stream_f64(sv + (k0 + u) * 32) : 0.0;
         }
 #pragma unroll
@@ -349,6 +376,81 @@ static void u1_sell_setup(ktb_plan* p) {
     p->extra_bytes = (p->ell_width ? 0 : 8 * (slices + 1)) + 12 * (padded - m->nnz) - 4 * (m->n + 1);
 }
 
+// U1 param 102: per slice, the dictionary of column deltas and the 4-bit
+// codes, from the warp-sliced copy (one warp per slice). A slice needing more
+// than 15 distinct deltas refuses the whole layout (the selector then skips
+// the candidate; random-column matrices such as config 3).
+__global__ void k_dict_build(const int64_t* __restrict__ soff, const int32_t* __restrict__ scol,
+                             int64_t slices, int ell, uint32_t* __restrict__ codes,
+                             int32_t* __restrict__ dict, int* __restrict__ overflow) {
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= slices) return;  // whole warps
+    int64_t o;
+    int W;
+    if (ell) {
+        o = s * 32 * ell;
+        W = ell;
+    } else {
+        o = soff[s];
+        W = static_cast<int>((soff[s + 1] - o) >> 5);
+    }
+    const int32_t row = static_cast<int32_t>(s * 32 + lane);
+    int32_t dv = 0;  // lane j < count: delta j
+    int count = 0;
+    bool ok = true;
+    for (int k = 0; k < W; ++k) {
+        const int32_t c = scol[o + static_cast<int64_t>(k) * 32 + lane];
+        const int32_t d = c - row;
+        int code = 15;
+        unsigned pending = __ballot_sync(0xffffffffu, c >= 0);
+        while (pending) {
+            const int src = __ffs(pending) - 1;
+            const int32_t want = __shfl_sync(0xffffffffu, d, src);
+            const unsigned same = __ballot_sync(0xffffffffu, c >= 0 && d == want);
+            const unsigned hit = __ballot_sync(0xffffffffu, lane < count && dv == want);
+            int j;
+            if (hit) {
+                j = __ffs(hit) - 1;
+            } else if (count < 15) {
+                j = count++;
+                if (lane == j) dv = want;
+            } else {
+                j = 15;
+                ok = false;
+            }
+            if ((same >> lane) & 1u) code = j;
+            pending &= ~same;
+        }
+        // 8 codes per word: lane 8g+i contributes bits 4i..4i+3 of word g
+        uint32_t part = static_cast<uint32_t>(code & 15) << ((lane & 7) * 4);
+        for (int sh = 1; sh < 8; sh <<= 1) part |= __shfl_xor_sync(0xffffffffu, part, sh);
+        if ((lane & 7) == 0) codes[(o >> 3) + static_cast<int64_t>(k) * 4 + (lane >> 3)] = part;
+    }
+    if (lane < 16) dict[s * 16 + lane] = lane < count ? dv : 0;
+    if (!ok && lane == 0) atomicOr(overflow, 1);
+}
+
+static void u1_dict_setup(ktb_plan* p) {
+    const int64_t slices = ceil_div64(p->m->n, 32);
+    const int64_t padded = static_cast<int64_t>(p->sell_col.n);
+    p->sell_codes.alloc(std::max<int64_t>(padded / 8, 1));
+    p->sell_dict.alloc(std::max<int64_t>(slices * 16, 1));
+    DBuf<int> overflow(1);
+    KTB_CUDA(cudaMemsetAsync(overflow.p, 0, sizeof(int), p->stream));
+    k_dict_build<<<ceil_div(slices * 32, 256), 256, 0, p->stream>>>(
+        p->sell_off.p, p->sell_col.p, slices, p->ell_width, p->sell_codes.p, p->sell_dict.p,
+        overflow.p);
+    KTB_LAUNCH();
+    int ov = 0;
+    KTB_CUDA(cudaMemcpyAsync(&ov, overflow.p, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    KTB_CUDA(cudaStreamSynchronize(p->stream));
+    if (ov) throw Invalid("u1: a warp slice needs more than 15 distinct column deltas");
+    p->sell_col.release();  // the codes replace the columns
+    // 0.5 B of code per slot + 64 B of dictionary per slice instead of 4 B columns
+    p->extra_bytes += static_cast<int64_t>(padded / 2 + 64 * slices) - 4 * padded;
+}
+
 // U1 param 101: rows of length <= kSortedCap sorted by length (descending,
 // stable) into warp slices -- near-uniform slice widths for any row-length
 // distribution; longer rows go to a compact sub-matrix reduced by U2 warp
@@ -457,7 +559,7 @@ static int pick_lanes(const ktb_matrix* m) {
 
 void u1_setup(ktb_plan* p) {
     require(p->cta_threads == 0 ||
-                ((p->param == 100 || p->param == 101) &&
+                ((p->param == 100 || p->param == 101 || p->param == 102) &&
                  (p->cta_threads == 64 || p->cta_threads == 128 || p->cta_threads == 256)),
             "u1: only the warp-sliced forms (params 100, 101) take a CTA shape: 64, 128 or 256 "
             "threads");
@@ -467,6 +569,12 @@ void u1_setup(ktb_plan* p) {
     }
     if (p->param == 100) {
         u1_sell_setup(p);
+        p->launches = 1;
+        return;
+    }
+    if (p->param == 102) {
+        u1_sell_setup(p);
+        u1_dict_setup(p);
         p->launches = 1;
         return;
     }
@@ -491,21 +599,21 @@ static void launch_u1s(ktb_plan* p, int64_t threads, const int64_t* soff, const 
     const int64_t xlen = p->m->ncols;
     const int grid = ceil_div(threads, t);
     p->ctas = grid;
-    switch (t) {
-        case 64:
-            k_u1s<64><<<grid, 64, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0, r1,
-                                                  ell, perm, xpf, xlen);
-            break;
-        case 128:
-            k_u1s<128><<<grid, 128, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0,
-                                                    r1, ell, perm, xpf, xlen);
-            break;
-        case 256:
-            k_u1s<256><<<grid, 256, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0,
-                                                    r1, ell, perm, xpf, xlen);
-            break;
+    const bool dict = p->param == 102;
+#define KTB_U1S_LAUNCH(T, D)                                                                   \
+    k_u1s<T, D><<<grid, T, 0, p->stream>>>(soff, p->sell_col.p, p->sell_val.p, x, y, r0, r1,    \
+                                           ell, perm, xpf, xlen, p->sell_codes.p,             \
+                                           p->sell_dict.p)
+    switch (t * 2 + (dict ? 1 : 0)) {
+        case 128: KTB_U1S_LAUNCH(64, false); break;
+        case 129: KTB_U1S_LAUNCH(64, true); break;
+        case 256: KTB_U1S_LAUNCH(128, false); break;
+        case 257: KTB_U1S_LAUNCH(128, true); break;
+        case 512: KTB_U1S_LAUNCH(256, false); break;
+        case 513: KTB_U1S_LAUNCH(256, true); break;
         default: throw Invalid("u1: warp-sliced CTAs are 64, 128 or 256 threads");
     }
+#undef KTB_U1S_LAUNCH
     KTB_LAUNCH();
 }
 
@@ -533,7 +641,7 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
         return;
     }
-    if (p->param == 100) {
+    if (p->param == 100 || p->param == 102) {
         const int64_t s0 = r0 >> 5, s1 = ceil_div64(r1, 32);
         launch_u1s(p, (s1 - s0) * 32, p->sell_off.p, x, y, static_cast<int32_t>(r0),
                    static_cast<int32_t>(r1), p->ell_width, nullptr);

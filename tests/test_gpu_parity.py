@@ -279,11 +279,12 @@ def test_selector_unsym_and_sym(K):
     names = [c.name for c in rep.candidates]
     # U1 (lanes, warp-sliced x 3 CTA shapes, row-sorted x 3), U2 (warp tiles x
     # 2 shapes, merge path), U3 (lanes per E, warp tiles x 2 shapes)
-    assert names[:10] == ["u1"] * 7 + ["u2"] * 3 and set(names[10:]) == {"u3"}
-    assert all(c.correct for c in rep.candidates[7:])  # U2 and every U3 form
-    # param slot (reference name jl): the warp-sliced U1 and its row-sorted form
-    assert [c.jl for c in rep.candidates[1:7]] == [100] * 3 + [101] * 3
-    assert [c.cta_threads for c in rep.candidates[1:7]] == [128, 64, 256] * 2
+    assert names[:13] == ["u1"] * 10 + ["u2"] * 3 and set(names[13:]) == {"u3"}
+    assert all(c.correct for c in rep.candidates[10:])  # U2 and every U3 form
+    # param slot (reference name jl): the warp-sliced U1, its column-coded and
+    # its row-sorted forms
+    assert [c.jl for c in rep.candidates[1:10]] == [100] * 3 + [102] * 3 + [101] * 3
+    assert [c.cta_threads for c in rep.candidates[1:10]] == [128, 64, 256] * 3
     x = O.seeded_vector(n, 1)
     y = np.empty(n)
     choice.plan.apply(x, y)
@@ -456,7 +457,7 @@ def test_launch_shapes(K):
     x = O.seeded_vector(n, 6)
     yref = O.spmv_ref(n, rp, ci, v, x)
     for t in (64, 128, 256):
-        for base in (100, 101):
+        for base in (100, 101, 102):
             p = K.DevicePlan(a, K.UnsymKernel.u1_row, base | t * SHAPE)
             assert p.param == base | t * SHAPE
             y = np.full(n, np.nan)
@@ -548,6 +549,63 @@ def test_u1_warp_sliced_bitwise_reference(K):
     a = K.CsrMatrix(n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1])))
     with pytest.raises(Exception):
         K.DevicePlan(a, K.UnsymKernel.u1_row, 100)
+
+
+def test_u1_column_coded_slices(K):
+    """U1 param 102: the warp-sliced copy with each slice's columns coded as
+    4-bit indices into a <= 15-entry dictionary of column deltas (col - row).
+    Same entries, order and arithmetic: bitwise equal to spmv_ref on the
+    stencils (configs 1 and 5 at full size, row sub-ranges), on banded
+    matrices with exactly 15 distinct deltas per slice, and on empty rows;
+    16 distinct deltas in one slice and random columns are refused."""
+    import torch
+
+    for a, seed in ((K.stencil7(64, 64, 64), 1),
+                    (K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7), 5)):
+        rp, ci, v = a.to_host()
+        x = O.seeded_vector(a.n, seed)
+        yref = O.spmv_ref(a.n, rp, ci, v, x)
+        for t in (64, 128, 256):
+            plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 102 | t * SHAPE)
+            xd = torch.from_numpy(x).cuda()
+            yd = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
+            plan.apply(xd, yd)
+            torch.cuda.synchronize()
+            assert np.array_equal(yd.cpu().numpy(), yref), t
+        yd.fill_(float("nan"))
+        r0, r1 = 4133, a.n - 77
+        plan.apply_rows(r0, r1, xd, yd)
+        torch.cuda.synchronize()
+        got = yd.cpu().numpy()
+        assert np.array_equal(got[r0:r1], yref[r0:r1]) and np.isnan(got[:r0]).all()
+
+    def banded(n, deltas, rng, empty_every=0):
+        rows = []
+        for i in range(n):
+            if empty_every and i % empty_every == 3:
+                rows.append(np.zeros(0, np.int64))
+                continue
+            c = np.array([i + d for d in deltas if 0 <= i + d < n], np.int64)
+            keep = rng.random(len(c)) < 0.8
+            rows.append(np.unique(c[keep]))
+        rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+        ci = np.concatenate(rows).astype(np.int64)
+        return n, rp, ci, rng.uniform(-1, 1, len(ci))
+
+    rng = np.random.default_rng(21)
+    ok15 = [-700, -300, -64, -33, -5, -2, -1, 0, 1, 2, 7, 40, 129, 512, 999]
+    for n, rp, ci, v in (banded(5000, ok15, rng), banded(3000, ok15[:7], rng, empty_every=5)):
+        a = K.CsrMatrix(n, rp, ci, v)
+        x = O.seeded_vector(n, 4)
+        y = np.full(n, np.nan)
+        K.DevicePlan(a, K.UnsymKernel.u1_row, 102).apply(x, y)
+        assert np.array_equal(y, O.spmv_ref(n, rp, ci, v, x))
+    n, rp, ci, v = banded(4000, ok15 + [2000], rng)  # 16 deltas
+    with pytest.raises(K.Error, match="15 distinct column deltas"):
+        K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 102)
+    n, rp, ci, v = matgen.random_csr(3000, 0.01, rng)
+    with pytest.raises(K.Error):
+        K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 102)
 
 
 def test_u1_sorted_slices(K):
