@@ -195,18 +195,30 @@ __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* _
     for (int k0 = 0; k0 < W; k0 += kSellUnroll) {
         int32_t c[kSellUnroll];
         double v[kSellUnroll], xv[kSellUnroll];
+        if constexpr (kDict) {
+            // every code and value load of the batch first, the decode
+            // shuffles after them (a shuffle between loads would serialise
+            // the batch into one round trip per slot)
+            uint32_t wd[kSellUnroll];
 #pragma unroll
-        for (int u = 0; u < kSellUnroll; ++u) {
-            const bool ok = k0 + u < W;  // warp-uniform
-            if constexpr (kDict) {
-                const uint32_t wd = ok ? ld_stream_u32(cw + (k0 + u) * 4) : 0xffffffffu;
-                const int code = static_cast<int>((wd >> ((lane & 7) * 4)) & 15u);
+            for (int u = 0; u < kSellUnroll; ++u) {
+                const bool ok = k0 + u < W;  // warp-uniform
+                wd[u] = ok ? ld_stream_u32(cw + (k0 + u) * 4) : 0xffffffffu;
+                v[u] = ok ? ld_stream_f64(sv + (k0 + u) * 32) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kSellUnroll; ++u) {
+                const int code = static_cast<int>((wd[u] >> ((lane & 7) * 4)) & 15u);
                 const int32_t d = __shfl_sync(0xffffffffu, dv, code);
                 c[u] = code != 15 ? static_cast<int32_t>(row) + d : -1;
-            } else {
-                c[u] = ok ? ld_stream_i32(sc + (k0 + u) * 32) : -1;
             }
-            v[u] = ok ? ld_stream_f64(sv + (k0 + u) * 32) : 0.0;
+        } else {
+#pragma unroll
+            for (int u = 0; u < kSellUnroll; ++u) {
+                const bool ok = k0 + u < W;  // warp-uniform
+                c[u] = ok ? ld_stream_i32(sc + (k0 + u) * 32) : -1;
+                v[u] = ok ? ld_stream_f64(sv + (k0 + u) * 32) : 0.0;
+            }
         }
 #pragma unroll
         for (int u = 0; u < kSellUnroll; ++u) xv[u] = c[u] >= 0 ? ld_x(x + c[u]) : 0.0;
