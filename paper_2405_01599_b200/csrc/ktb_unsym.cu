@@ -229,6 +229,94 @@ __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* _
     if (perm ? row >= 0 : (row >= row_begin && row < row_end)) y[row] = sum;
 }
 
+// ---- U1 params 103 / 104: persistent, software-pipelined warp slices ---------
+// The warp-sliced kernel above runs one slice per warp and one wave of CTAs
+// after another: each warp's column/value loads and then its x gathers are
+// two serial round trips, and with ~31 resident warps per SM that is what
+// bounds it (ncu, config 4: 6.24 TB/s, eligible warps 0.75 per scheduler).
+// Here a grid of resident CTAs walks the slices (warp g takes g, g+G, ...)
+// two deep: the loads of the next slice are issued before the gathers of the
+// current one, so a warp always has one slice's stream and another's gathers
+// in flight. Uniform slice width W <= 8 (ELL; the stencils), int32 columns
+// (103) or the coded columns of 102 (104). Row sums unchanged: bitwise
+// spmv_ref.
+template <bool kDict>
+struct SliceRegs {
+    uint32_t cw[8];  // int32 column or code word per slot
+    double v[8];
+    int32_t dv;      // dictionary entry (kDict)
+};
+
+template <bool kDict>
+__device__ __forceinline__ void slice_load(SliceRegs<kDict>& R, int64_t s, int64_t s_end, int W,
+                                           const int32_t* __restrict__ scol,
+                                           const double* __restrict__ sval,
+                                           const uint32_t* __restrict__ codes,
+                                           const int32_t* __restrict__ dict, int lane) {
+    const bool live = s < s_end;  // warp-uniform
+    const int64_t o = s * 32 * W;
+    if (kDict) R.dv = live ? __ldg(dict + s * 16 + (lane & 15)) : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const bool ok = live && u < W;
+        if (kDict)
+            R.cw[u] = ok ? ld_stream_u32(codes + (o >> 3) + u * 4 + (lane >> 3)) : 0xffffffffu;
+        else
+            R.cw[u] = ok ? static_cast<uint32_t>(ld_stream_i32(scol + o + u * 32 + lane))
+                         : 0xffffffffu;
+        R.v[u] = ok ? ld_stream_f64(sval + o + u * 32 + lane) : 0.0;
+    }
+}
+
+template <bool kDict>
+__device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t s, int32_t r0,
+                                             int32_t r1, const double* __restrict__ x,
+                                             double* __restrict__ y, int lane) {
+    const int64_t row = s * 32 + lane;
+    int32_t c[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (kDict) {
+            const int code = static_cast<int>((R.cw[u] >> ((lane & 7) * 4)) & 15u);
+            const int32_t d = __shfl_sync(0xffffffffu, R.dv, code);
+            c[u] = code != 15 ? static_cast<int32_t>(row) + d : -1;
+        } else {
+            c[u] = static_cast<int32_t>(R.cw[u]);
+        }
+    }
+    double xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(x + c[u]) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        if (c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(R.v[u], xv[u]));
+    if (row >= r0 && row < r1) y[row] = sum;
+}
+
+template <bool kDict>
+__global__ void __launch_bounds__(256) k_u1p(const int32_t* __restrict__ scol,
+                                             const double* __restrict__ sval,
+                                             const uint32_t* __restrict__ codes,
+                                             const int32_t* __restrict__ dict,
+                                             const double* __restrict__ x, double* __restrict__ y,
+                                             int32_t row_begin, int32_t row_end, int W) {
+    const int lane = threadIdx.x & 31;
+    const int64_t G = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t s0 = row_begin >> 5, s_end = (static_cast<int64_t>(row_end) + 31) >> 5;
+    int64_t s = s0 + blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+    SliceRegs<kDict> A, B;
+    slice_load(A, s, s_end, W, scol, sval, codes, dict, lane);
+    // two slices per trip so that the register sets alternate without copies
+    for (; s < s_end; s += 2 * G) {
+        slice_load(B, s + G, s_end, W, scol, sval, codes, dict, lane);
+        slice_finish(A, s, row_begin, row_end, x, y, lane);
+        if (s + G >= s_end) break;
+        slice_load(A, s + 2 * G, s_end, W, scol, sval, codes, dict, lane);
+        slice_finish(B, s + G, row_begin, row_end, x, y, lane);
+    }
+}
+
 // ---- U1 param 101 setup helpers: rows sorted by length ----------------------
 __global__ void k_sort_keys(const int32_t* __restrict__ rp, int64_t n, int32_t cap,
                             int32_t* __restrict__ key, int32_t* __restrict__ row) {
@@ -590,6 +678,21 @@ void u1_setup(ktb_plan* p) {
         p->launches = 1;
         return;
     }
+    if (p->param == 103 || p->param == 104) {  // persistent pipelined slices (ELL, W <= 8)
+        require(p->cta_threads == 0, "u1: the persistent slices run 256-thread CTAs");
+        u1_sell_setup(p);
+        if (p->ell_width < 1 || p->ell_width > 8)
+            throw Invalid("u1: persistent slices need one slice width <= 8");
+        if (p->param == 104) u1_dict_setup(p);
+        int occ = 0;
+        if (p->param == 104)
+            KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u1p<true>, 256, 0));
+        else
+            KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u1p<false>, 256, 0));
+        p->ctas = static_cast<int64_t>(std::max(occ, 1)) * p->m->sm_count;
+        p->launches = 1;
+        return;
+    }
     if (p->param == 101) {
         u1_sorted_setup(p);
         p->launches = 1 + (p->long_plan ? p->long_plan->launches + 1 : 0);
@@ -651,6 +754,21 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         launch_u1s(p, slices * 32, p->sell_off.p, x, y, 0, static_cast<int32_t>(slices * 32), 0,
                    p->sell_perm.p);
         if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
+        return;
+    }
+    if (p->param == 103 || p->param == 104) {
+        const int64_t slices = ceil_div64(r1, 32) - (r0 >> 5);
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(p->ctas, ceil_div64(slices, 8))));
+        if (p->param == 104)
+            k_u1p<true><<<grid, 256, 0, p->stream>>>(nullptr, p->sell_val.p, p->sell_codes.p,
+                                                     p->sell_dict.p, x, y, static_cast<int32_t>(r0),
+                                                     static_cast<int32_t>(r1), p->ell_width);
+        else
+            k_u1p<false><<<grid, 256, 0, p->stream>>>(p->sell_col.p, p->sell_val.p, nullptr,
+                                                      nullptr, x, y, static_cast<int32_t>(r0),
+                                                      static_cast<int32_t>(r1), p->ell_width);
+        KTB_LAUNCH();
         return;
     }
     if (p->param == 100 || p->param == 102) {

@@ -30,8 +30,9 @@ def main():
         nnz = a.nnz()
         B = 12 * nnz + 4 * (a.n + 1) + 16 * a.n
         r = reps if a.n < 10 ** 8 else 30
-        for t in (128, 256):
-            plans = {p: K.DevicePlan(a, K.UnsymKernel.u1_row, p | (t << 16)) for p in params}
+        for t in (128,):
+            plans = {p: K.DevicePlan(a, K.UnsymKernel.u1_row, p | (t << 16 if p < 103 else 0))
+                     for p in params}
             res, ys = {p: [] for p in params}, {}
             for _ in range(5):
                 for p in params:
