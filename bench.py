@@ -655,8 +655,8 @@ def run_halo(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-            "config": dict(config_block(cfg, "u1 thread-per-row over the warp-sliced copy "
-                                             "(param 100), ktb_halo_spmv"),
+            "config": dict(config_block(cfg, "u1 persistent pipelined warp slices, coded "
+                                             "columns (param 104), ktb_halo_spmv"),
                            parallelism=f"row-block z-slabs x{ws}, one-plane halo, NCCL P2P"),
             "gflops": F / (ms / 1e3) / 1e9,
             "per_gpu_gbs": B / ws / (ms / 1e3) / 1e9,
@@ -671,12 +671,13 @@ def run_halo(args, cfg):
                          "frac": ach_min / peak,
                          "traffic": traffic_from_profile(cfg) if ws == 1 else None,
                          "peak_source": peak_src,
-                         "kernel": "k_u1s over the interior rows (1 launch per step)",
+                         "kernel": "k_u1p<coded> over the interior rows (1 launch per step)",
                          "bytes_per_launch": B_int,
-                         "note": "peak is the measured copy (read + write) bandwidth; a "
-                                 "read-dominated stream can exceed it (frac > 1); the "
-                                 "warp-sliced kernel does not read row_ptr (4 B/row of the "
-                                 "model); achieved = min over ranks"},
+                         "note": "achieved = the minimum-traffic model's bytes (12 B/nnz) over "
+                                 "the kernel time, min over ranks; the kernel moves fewer bytes "
+                                 "than the model (8 B value + 0.5 B column code per slot, no "
+                                 "row_ptr), so frac can exceed 1; traffic = its measured DRAM "
+                                 "bytes per launch (ncu)"},
             "e2e": {"value": B / (e2e16 / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
                     "ms_per_step": e2e16,

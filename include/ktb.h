@@ -155,7 +155,12 @@ int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
  *   param:   U1: lanes per row V in {0=auto,1,2,4,...,32}; 100 = one thread
  *                per row over a warp-sliced (SELL-32/ELL) copy, bitwise equal
  *                to spmv_ref; 101 = the same over rows sorted by length (rows
- *                > 256 through U2 tiles on a side stream);
+ *                > 256 through U2 tiles on a side stream); 102 = the warp
+ *                slices with each slice's columns coded as 4-bit indices into
+ *                a <= 15-entry dictionary of column deltas (8.5 B per slot
+ *                instead of 12); 103 / 104 = persistent, two-deep pipelined
+ *                warp slices (uniform width <= 8) with int32 / coded columns;
+ *                100-104 are all bitwise equal to spmv_ref;
  *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8);
  *                104/108/112 = merge-path tiles;
  *            U3/U4: nonzeros per segment lane E in {4,8,16} (0 = 8); U3 1008

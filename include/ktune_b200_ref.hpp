@@ -252,8 +252,9 @@ Entry& entry(const M& a, int kind) {
     return c.entries.emplace(k, std::move(e)).first->second;
 }
 
-// default device variant per kernel when none was selected
-inline int64_t default_param(int k) { return k == KTB_U1 ? 100 : 0; }
+// default device variant per kernel when none was selected: U1 tries the
+// persistent coded slices (104), then the plain warp slices (100), then lanes
+inline int64_t default_param(int k) { return k == KTB_U1 ? 104 : 0; }
 
 template <typename M>
 std::shared_ptr<ktb_cpp::Plan> plan_for(const M& a, int kind, int kernel) {
@@ -263,12 +264,15 @@ std::shared_ptr<ktb_cpp::Plan> plan_for(const M& a, int kind, int kernel) {
     auto it = e.plans.find(kernel);
     if (it != e.plans.end()) return it->second;
     std::shared_ptr<ktb_cpp::Plan> p;
-    try {
-        p = std::make_shared<ktb_cpp::Plan>(e.dm, kernel, default_param(kernel));
-    } catch (const Error&) {
-        if (kernel != KTB_U1) throw;
-        // the warp-sliced copy is refused for very irregular rows
-        p = std::make_shared<ktb_cpp::Plan>(e.dm, kernel, 0);
+    const int64_t tries[3] = {default_param(kernel), 100, 0};
+    for (int t = 0; t < (kernel == KTB_U1 ? 3 : 1) && !p; ++t) {
+        try {
+            p = std::make_shared<ktb_cpp::Plan>(e.dm, kernel, tries[t]);
+        } catch (const Error&) {
+            // refused layouts: uniform width / few column deltas (104), or
+            // padding beyond 3x (100) for very irregular rows
+            if (kernel != KTB_U1 || t == 2) throw;
+        }
     }
     e.plans[kernel] = p;
     return p;

@@ -476,7 +476,14 @@ ktb_halo* halo_create(ktb_matrix* local, int64_t halo_lo, int64_t halo_hi, ktb_c
         ktb_halo::Part q{r0, r1, nullptr, nullptr};
         q.m = matrix_slice(local, r0, r1);
         try {
-            q.p = plan_create_internal(q.m, kernel, param, 0, h->cs);
+            try {
+                q.p = plan_create_internal(q.m, kernel, param, 0, h->cs);
+            } catch (const Invalid&) {
+                // the persistent / coded slice forms need a uniform width and
+                // few column deltas (a thin boundary part may not have them)
+                if (kernel != KTB_U1 || param < 102 || param > 104) throw;
+                q.p = plan_create_internal(q.m, kernel, 100, 0, h->cs);
+            }
         } catch (...) {
             delete q.m;
             throw;

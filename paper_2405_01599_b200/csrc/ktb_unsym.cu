@@ -294,8 +294,11 @@ __device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t 
     if (row >= r0 && row < r1) y[row] = sum;
 }
 
+#ifndef KTB_U1P_MINB
+#define KTB_U1P_MINB 1
+#endif
 template <bool kDict>
-__global__ void __launch_bounds__(256) k_u1p(const int32_t* __restrict__ scol,
+__global__ void __launch_bounds__(256, KTB_U1P_MINB) k_u1p(const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const uint32_t* __restrict__ codes,
                                              const int32_t* __restrict__ dict,
