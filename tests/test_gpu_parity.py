@@ -566,7 +566,7 @@ def test_u1_column_coded_slices(K):
         x = O.seeded_vector(a.n, seed)
         yref = O.spmv_ref(a.n, rp, ci, v, x)
         for t in (64, 128, 256, 103, 104):
-            plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 102 | t * SHAPE if t > 104 else t)
+            plan = K.DevicePlan(a, K.UnsymKernel.u1_row, t if t in (103, 104) else 102 | t * SHAPE)
             xd = torch.from_numpy(x).cuda()
             yd = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
             plan.apply(xd, yd)
