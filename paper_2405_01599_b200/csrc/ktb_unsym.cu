@@ -242,9 +242,9 @@ __global__ void __launch_bounds__(kThreads, KTB_U1S_MINB) k_u1s(const int64_t* _
 // spmv_ref.
 template <bool kDict>
 struct SliceRegs {
-    uint32_t cw[kDict ? 1 : 8];  // int32 column per slot, or the row's code word
+    uint32_t cw[8];  // int32 column or code word per slot
     double v[8];
-    int32_t dv;                  // dictionary entry (kDict)
+    int32_t dv;      // dictionary entry (kDict)
 };
 
 template <bool kDict>
@@ -255,14 +255,13 @@ __device__ __forceinline__ void slice_load(SliceRegs<kDict>& R, int64_t s, int64
                                            const int32_t* __restrict__ dict, int lane) {
     const bool live = s < s_end;  // warp-uniform
     const int64_t o = s * 32 * W;
-    if (kDict) {
-        R.dv = live ? __ldg(dict + s * 16 + (lane & 15)) : 0;
-        R.cw[0] = live ? ld_stream_u32(codes + s * 32 + lane) : 0xffffffffu;  // lane-major
-    }
+    if (kDict) R.dv = live ? __ldg(dict + s * 16 + (lane & 15)) : 0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         const bool ok = live && u < W;
-        if (!kDict)
+        if (kDict)
+            R.cw[u] = ok ? ld_stream_u32(codes + (o >> 3) + u * 4 + (lane >> 3)) : 0xffffffffu;
+        else
             R.cw[u] = ok ? static_cast<uint32_t>(ld_stream_i32(scol + o + u * 32 + lane))
                          : 0xffffffffu;
         R.v[u] = ok ? ld_stream_f64(sval + o + u * 32 + lane) : 0.0;
@@ -278,7 +277,7 @@ __device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t 
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         if (kDict) {
-            const int code = static_cast<int>((R.cw[0] >> (4 * u)) & 15u);
+            const int code = static_cast<int>((R.cw[u] >> ((lane & 7) * 4)) & 15u);
             const int32_t d = __shfl_sync(0xffffffffu, R.dv, code);
             c[u] = code != 15 ? static_cast<int32_t>(row) + d : -1;
         } else {
@@ -295,12 +294,12 @@ __device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t 
     if (row >= r0 && row < r1) y[row] = sum;
 }
 
-#ifndef KTB_U1P_MINB
-#define KTB_U1P_MINB 3  // 80 registers, 24 warps/SM (1: 95 registers, 2 CTAs: half speed;
-                        // 4: 64 registers with spills)
-#endif
+// 80 registers = 3 CTAs (24 warps) per SM for both forms; the int32-column
+// form needs the 3-CTA bound to get there (82 registers otherwise: 2 CTAs,
+// 33 % slower), the coded form gets 80 unconstrained (an explicit bound of 1
+// gives 95 registers and half the speed)
 template <bool kDict>
-__global__ void __launch_bounds__(256, KTB_U1P_MINB) k_u1p(const int32_t* __restrict__ scol,
+__global__ void __launch_bounds__(256, kDict ? 0 : 3) k_u1p(const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const uint32_t* __restrict__ codes,
                                              const int32_t* __restrict__ dict,
@@ -487,8 +486,7 @@ static void u1_sell_setup(ktb_plan* p) {
 // the candidate; random-column matrices such as config 3).
 __global__ void k_dict_build(const int64_t* __restrict__ soff, const int32_t* __restrict__ scol,
                              int64_t slices, int ell, uint32_t* __restrict__ codes,
-                             int32_t* __restrict__ dict, int* __restrict__ overflow,
-                             uint32_t* __restrict__ lane_codes) {
+                             int32_t* __restrict__ dict, int* __restrict__ overflow) {
     const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (s >= slices) return;  // whole warps
@@ -505,7 +503,6 @@ __global__ void k_dict_build(const int64_t* __restrict__ soff, const int32_t* __
     int32_t dv = 0;  // lane j < count: delta j
     int count = 0;
     bool ok = true;
-    uint32_t lw = 0xffffffffu;  // lane-major: this row's codes, slot k in bits 4k..4k+3
     for (int k = 0; k < W; ++k) {
         const int32_t c = scol[o + static_cast<int64_t>(k) * 32 + lane];
         const int32_t d = c - row;
@@ -529,14 +526,12 @@ __global__ void k_dict_build(const int64_t* __restrict__ soff, const int32_t* __
             if ((same >> lane) & 1u) code = j;
             pending &= ~same;
         }
-        if (k < 8) lw = (lw & ~(15u << (4 * k))) | (static_cast<uint32_t>(code & 15) << (4 * k));
         // 8 codes per word: lane 8g+i contributes bits 4i..4i+3 of word g
         uint32_t part = static_cast<uint32_t>(code & 15) << ((lane & 7) * 4);
         for (int sh = 1; sh < 8; sh <<= 1) part |= __shfl_xor_sync(0xffffffffu, part, sh);
         if ((lane & 7) == 0) codes[(o >> 3) + static_cast<int64_t>(k) * 4 + (lane >> 3)] = part;
     }
     if (lane < 16) dict[s * 16 + lane] = lane < count ? dv : 0;
-    if (lane_codes) lane_codes[s * 32 + lane] = lw;
     if (!ok && lane == 0) atomicOr(overflow, 1);
 }
 
@@ -547,25 +542,17 @@ static void u1_dict_setup(ktb_plan* p) {
     p->sell_dict.alloc(std::max<int64_t>(slices * 16, 1));
     DBuf<int> overflow(1);
     KTB_CUDA(cudaMemsetAsync(overflow.p, 0, sizeof(int), p->stream));
-    const bool lane_major = p->param == 104;  // one code word per row (width <= 8)
-    if (lane_major) p->sell_lcodes.alloc(std::max<int64_t>(slices * 32, 1));
     k_dict_build<<<ceil_div(slices * 32, 256), 256, 0, p->stream>>>(
         p->sell_off.p, p->sell_col.p, slices, p->ell_width, p->sell_codes.p, p->sell_dict.p,
-        overflow.p, lane_major ? p->sell_lcodes.p : nullptr);
+        overflow.p);
     KTB_LAUNCH();
     int ov = 0;
     KTB_CUDA(cudaMemcpyAsync(&ov, overflow.p, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
     KTB_CUDA(cudaStreamSynchronize(p->stream));
     if (ov) throw Invalid("u1: a warp slice needs more than 15 distinct column deltas");
     p->sell_col.release();  // the codes replace the columns
-    if (lane_major) {
-        p->sell_codes.release();
-        // 4 B of codes per row + 64 B of dictionary per slice instead of 4 B columns
-        p->extra_bytes += static_cast<int64_t>(4 * 32 * slices + 64 * slices) - 4 * padded;
-    } else {
-        // 0.5 B of code per slot + 64 B of dictionary per slice instead of 4 B columns
-        p->extra_bytes += static_cast<int64_t>(padded / 2 + 64 * slices) - 4 * padded;
-    }
+    // 0.5 B of code per slot + 64 B of dictionary per slice instead of 4 B columns
+    p->extra_bytes += static_cast<int64_t>(padded / 2 + 64 * slices) - 4 * padded;
 }
 
 // U1 param 101: rows of length <= kSortedCap sorted by length (descending,
@@ -778,7 +765,7 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>(p->ctas, ceil_div64(slices, 8))));
         if (p->param == 104)
-            k_u1p<true><<<grid, 256, 0, p->stream>>>(nullptr, p->sell_val.p, p->sell_lcodes.p,
+            k_u1p<true><<<grid, 256, 0, p->stream>>>(nullptr, p->sell_val.p, p->sell_codes.p,
                                                      p->sell_dict.p, x, y, static_cast<int32_t>(r0),
                                                      static_cast<int32_t>(r1), p->ell_width);
         else
