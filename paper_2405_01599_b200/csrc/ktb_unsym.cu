@@ -244,60 +244,53 @@ template <bool kDict>
 struct SliceRegs {
     uint32_t cw[8];  // int32 column or code word per slot
     double v[8];
+    int32_t dv;      // dictionary entry (kDict)
 };
 
-// Every load below is unconditional from a clamped, valid address (a dead
-// slot reads a live one) and masked at use: inline-asm loads cannot be
-// predicated, so conditional ones cost a branch + reconvergence each.
 template <bool kDict>
 __device__ __forceinline__ void slice_load(SliceRegs<kDict>& R, int64_t s, int64_t s_end, int W,
                                            const int32_t* __restrict__ scol,
                                            const double* __restrict__ sval,
                                            const uint32_t* __restrict__ codes,
                                            const int32_t* __restrict__ dict, int lane) {
-    const int64_t sc = min(s, s_end - 1);  // dead slices (s >= s_end) are never finished
-    const int64_t o = sc * 32 * W;
-    (void)dict;
+    const bool live = s < s_end;  // warp-uniform
+    const int64_t o = s * 32 * W;
+    if (kDict) R.dv = live ? __ldg(dict + s * 16 + (lane & 15)) : 0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-        const int uu = min(u, W - 1);
+        const bool ok = live && u < W;
         if (kDict)
-            R.cw[u] = ld_stream_u32(codes + (o >> 3) + uu * 4 + (lane >> 3));
+            R.cw[u] = ok ? ld_stream_u32(codes + (o >> 3) + u * 4 + (lane >> 3)) : 0xffffffffu;
         else
-            R.cw[u] = static_cast<uint32_t>(ld_stream_i32(scol + o + uu * 32 + lane));
-        R.v[u] = ld_stream_f64(sval + o + uu * 32 + lane);
+            R.cw[u] = ok ? static_cast<uint32_t>(ld_stream_i32(scol + o + u * 32 + lane))
+                         : 0xffffffffu;
+        R.v[u] = ok ? ld_stream_f64(sval + o + u * 32 + lane) : 0.0;
     }
 }
 
 template <bool kDict>
-__device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t s, int W,
-                                             int32_t r0, int32_t r1,
-                                             const int32_t* __restrict__ dict,
-                                             const double* __restrict__ x,
+__device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t s, int32_t r0,
+                                             int32_t r1, const double* __restrict__ x,
                                              double* __restrict__ y, int lane) {
     const int64_t row = s * 32 + lane;
     int32_t c[8];
-    bool on[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         if (kDict) {
             const int code = static_cast<int>((R.cw[u] >> ((lane & 7) * 4)) & 15u);
-            on[u] = u < W && code != 15;
-            // the slice's dictionary (64 B, L1-resident after the first slot)
-            c[u] = static_cast<int32_t>(row) + __ldg(dict + s * 16 + code);
+            const int32_t d = __shfl_sync(0xffffffffu, R.dv, code);
+            c[u] = code != 15 ? static_cast<int32_t>(row) + d : -1;
         } else {
-            on[u] = u < W && static_cast<int32_t>(R.cw[u]) >= 0;
             c[u] = static_cast<int32_t>(R.cw[u]);
         }
-        if (!on[u]) c[u] = 0;  // a valid address; the product is dropped below
     }
     double xv[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) xv[u] = ld_x(x + c[u]);
+    for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(x + c[u]) : 0.0;
     double sum = 0.0;
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-        if (on[u]) sum = __dadd_rn(sum, __dmul_rn(R.v[u], xv[u]));
+        if (c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(R.v[u], xv[u]));
     if (row >= r0 && row < r1) y[row] = sum;
 }
 
@@ -306,7 +299,7 @@ __device__ __forceinline__ void slice_finish(const SliceRegs<kDict>& R, int64_t 
 // 33 % slower), the coded form gets 80 unconstrained (an explicit bound of 1
 // gives 95 registers and half the speed)
 template <bool kDict>
-__global__ void __launch_bounds__(256, 3) k_u1p(const int32_t* __restrict__ scol,
+__global__ void __launch_bounds__(256, kDict ? 0 : 3) k_u1p(const int32_t* __restrict__ scol,
                                              const double* __restrict__ sval,
                                              const uint32_t* __restrict__ codes,
                                              const int32_t* __restrict__ dict,
@@ -321,10 +314,10 @@ __global__ void __launch_bounds__(256, 3) k_u1p(const int32_t* __restrict__ scol
     // two slices per trip so that the register sets alternate without copies
     for (; s < s_end; s += 2 * G) {
         slice_load(B, s + G, s_end, W, scol, sval, codes, dict, lane);
-        slice_finish(A, s, W, row_begin, row_end, dict, x, y, lane);
+        slice_finish(A, s, row_begin, row_end, x, y, lane);
         if (s + G >= s_end) break;
         slice_load(A, s + 2 * G, s_end, W, scol, sval, codes, dict, lane);
-        slice_finish(B, s + G, W, row_begin, row_end, dict, x, y, lane);
+        slice_finish(B, s + G, row_begin, row_end, x, y, lane);
     }
 }
 
