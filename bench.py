@@ -485,6 +485,27 @@ def measure_plan(cfg, local, steps, warmup, warm_seconds, sampler=None):
             ev[k][1].record(stream)
         stream.synchronize()
     ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev]))
+    graph_us = None
+    if n <= (1 << 20):
+        # small matrices: launch + ramp dominate a cold single apply; the
+        # same applies captured back to back in one CUDA graph (warm L2: the
+        # whole matrix fits in it) show the amortised per-apply time
+        reps = 50
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                plan.apply(x, y)
+        plan.set_stream(stream.cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(5):
+            g.replay()
+        g1.record()
+        torch.cuda.synchronize()
+        graph_us = g0.elapsed_time(g1) * 1e3 / (5 * reps)
+        del g
     # e2e: the public host call, pipelined over steps (ktb_spmv_host_pipelined)
     xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     xh.copy_(x.cpu())
@@ -498,7 +519,7 @@ def measure_plan(cfg, local, steps, warmup, warm_seconds, sampler=None):
     e2e = (time.perf_counter() - t0) * 1e3 / kpipe
     clocks = sampler.stop() if sampler else None
     return dict(n=n, nnz=nnz, ms=ms, e2e_ms=e2e, plan=plan, sel=sel, rep=rep, clocks=clocks,
-                build_s=t_build, select_s=t_select)
+                build_s=t_build, select_s=t_select, graph_us=graph_us)
 
 
 def run_gpu(args, cfg):
@@ -542,9 +563,16 @@ def run_gpu(args, cfg):
             "gpu_launches": ws * args.steps * plan.launches,
             "clocks": r["clocks"],
             "setup_seconds": {"matrix": r["build_s"], "selection": r["select_s"]},
-            "selection": [{"name": c.name, "param": c.jl, "best_ms": c.best_seconds * 1e3,
+            "selection": [{"name": c.name, "param": c.jl, "cta_threads": c.cta_threads,
+                           "best_ms": c.best_seconds * 1e3, "setup_s": c.setup_seconds,
                            "correct": c.correct} for c in r["rep"].candidates],
         }
+        if r["graph_us"] is not None:
+            line["graph_amortised"] = {
+                "us_per_apply": r["graph_us"], "gbs": B / (r["graph_us"] * 1e-6) / 1e9,
+                "def": "50 applies captured back to back in one CUDA graph, replayed 5 times, "
+                       "warm L2 (the matrix fits in it): the amortised per-apply time next to "
+                       "the single cold-L2 apply of ms_per_step"}
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line))
