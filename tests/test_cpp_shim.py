@@ -77,3 +77,19 @@ def test_reference_call_sequences_with_namespace_changed():
         assert abs(info[k]["gpu_iterations"] - info[k]["ref_iterations"]) <= 2
     assert info["messages"]["same"] == info["messages"]["cases"]
     assert info["residency"]["after_200_calls"] == info["residency"]["device_matrices_before"]
+
+
+NATIVE_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "dist_native")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(NATIVE_BIN), reason="dist_native not built")
+def test_multi_gpu_data_plane_from_cpp():
+    """tests/cpp/dist_native.cpp: the halo operator and the general split
+    driven from C++ through ktb.h alone (NCCL at world 1; three loopback
+    ranks on threads), every row against a host product."""
+    out = subprocess.run([NATIVE_BIN], capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    info = {k: v for d in lines for k, v in d.items()}
+    assert out.returncode == 0 and info.get("ok") is True, out.stdout + out.stderr
+    assert info["nccl_world1"]["nccl"] == 1 and info["loopback_world3"]["ok"] is True
