@@ -217,6 +217,10 @@ typedef struct {
     int workers;           /* reference worker count for artefacts (0 = default) */
     ktb_now_fn now;        /* injected host timer (autotune.hpp:164); NULL = CUDA events */
     void* now_ctx;
+    int warm_trials;       /* 0 (default): before every timed trial L2 is flushed (2x its
+                              size written, then another 2x read), so each candidate is timed
+                              the way it runs on a matrix streamed from HBM; 1: back to back
+                              with a warm L2, the reference's protocol (autotune.hpp:216-240) */
 } ktb_select_opts;
 
 typedef struct {

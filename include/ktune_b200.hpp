@@ -177,6 +177,7 @@ struct SelectOptions {  // autotune.hpp:160-165
     std::vector<index_t> jl_candidates;  // GPU: nonzeros per BSS lane (jl = nnz / E)
     int timed_trials = 3;
     std::function<double()> now;  // injectable timer; empty = CUDA events
+    bool warm_trials = false;     // true: back-to-back trials (the reference's protocol)
 };
 
 struct Choice {  // UnsymChoice / SymChoice (autotune.hpp:168-183)
@@ -195,6 +196,7 @@ inline std::pair<Choice, TuningReport> select(std::shared_ptr<DeviceMatrix> m,
     o.params = opts.jl_candidates.empty() ? nullptr : opts.jl_candidates.data();
     o.n_params = static_cast<int>(opts.jl_candidates.size());
     o.timed_trials = opts.timed_trials;
+    o.warm_trials = opts.warm_trials ? 1 : 0;
     std::function<double()> now = opts.now;
     if (now) {
         o.now = &call_now;

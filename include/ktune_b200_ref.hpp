@@ -164,6 +164,7 @@ struct SelectOptions {
     int timed_trials = 3;
     bool sweep_workers = false;
     TimerFn now;
+    bool warm_trials = false;  // true: back-to-back trials as the reference (default: cold L2)
 };
 
 struct UnsymChoice {  // autotune.hpp:168-176
@@ -313,6 +314,7 @@ std::pair<int, TuningReport> select(const M& a, int kind, const SelectOptions& o
     auto dm = device_matrix(a, kind);
     ktb_select_opts o{};
     o.timed_trials = opts.timed_trials;
+    o.warm_trials = opts.warm_trials ? 1 : 0;
     TimerFn now = opts.now;
     if (now) {
         o.now = &call_now;

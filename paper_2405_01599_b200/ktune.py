@@ -697,6 +697,7 @@ class SelectOptions:  # autotune.hpp:160-165
     timed_trials: int = 3
     sweep_workers: bool = False
     now: Optional[Callable[[], float]] = None
+    warm_trials: bool = False  # True: back-to-back trials (the reference's protocol)
 
 
 class _Cand(C.Structure):
@@ -709,7 +710,8 @@ class _Cand(C.Structure):
 
 class _Opts(C.Structure):
     _fields_ = [("params", C.c_void_p), ("n_params", C.c_int), ("timed_trials", C.c_int),
-                ("workers", C.c_int), ("now", C.c_void_p), ("now_ctx", C.c_void_p)]
+                ("workers", C.c_int), ("now", C.c_void_p), ("now_ctx", C.c_void_p),
+                ("warm_trials", C.c_int)]
 
 
 _NOW = C.CFUNCTYPE(C.c_double, C.c_void_p)
@@ -739,6 +741,7 @@ def _select(a, opts: Optional[SelectOptions]):
         params = np.ascontiguousarray(opts.jl_candidates, np.int64)
         o.params, o.n_params = params.ctypes.data, len(params)
     o.timed_trials = opts.timed_trials
+    o.warm_trials = int(bool(opts.warm_trials))
     cb = None
     if opts.now is not None:
         cb = _NOW(lambda _ctx: float(opts.now()))
