@@ -321,6 +321,87 @@ __global__ void __launch_bounds__(256, kDict ? 0 : 3) k_u1p(const int32_t* __res
     }
 }
 
+// ---- U1 param 105: persistent coded slices staged by per-warp bulk copies ----
+// 104 keeps the next slice in registers, which caps it at two slices per warp
+// in flight and 24 warps per SM (80 registers). Here every warp owns a ring
+// of kU1tStages shared-memory stages; lane 0 fills a stage with one slice's
+// values (32 W doubles, contiguous in the ELL copy), its code words and its
+// dictionary by three bulk copies (cp.async.bulk, completion on the stage's
+// mbarrier) kU1tStages slices ahead, so a warp keeps that many slices of the
+// stream in flight without registers. Lanes read their values / codes from
+// the stage (conflict-free), decode through the staged dictionary, gather x,
+// sum left to right (bitwise spmv_ref) and hand the stage back.
+constexpr int kU1tStages = 4;
+constexpr int kU1tStageBytes = 32 * 8 * 8 + 8 * 16 + 64;  // values (W <= 8), codes, dict: 2240
+constexpr int kU1tWarps = 8;
+constexpr int kU1tSmem = kU1tWarps * (kU1tStages * kU1tStageBytes + kU1tStages * 8);
+
+__global__ void __launch_bounds__(kU1tWarps * 32) k_u1t(const double* __restrict__ sval,
+                                                         const uint32_t* __restrict__ codes,
+                                                         const int32_t* __restrict__ dict,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ y, int32_t row_begin,
+                                                         int32_t row_end, int W) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* ring = smem + warp * (kU1tStages * kU1tStageBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kU1tWarps * kU1tStages * kU1tStageBytes) +
+                     warp * kU1tStages;
+    const int64_t G = static_cast<int64_t>(gridDim.x) * kU1tWarps;
+    const int64_t s0 = (row_begin >> 5) + blockIdx.x * static_cast<int64_t>(kU1tWarps) + warp;
+    const int64_t s_end = (static_cast<int64_t>(row_end) + 31) >> 5;
+    const uint32_t vbytes = 32u * 8u * W, cbytes = 16u * W;
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int64_t s, int st) {  // lane 0
+        unsigned char* b = ring + st * kU1tStageBytes;
+        mbar_arrive_expect_tx(&bars[st], vbytes + cbytes + 64);
+        tma_load_1d(b, sval + s * 32 * W, vbytes, &bars[st], pol);
+        tma_load_1d(b + 32 * 8 * 8, codes + s * 4 * W, cbytes, &bars[st], pol);
+        tma_load_1d(b + 32 * 8 * 8 + 8 * 16, dict + s * 16, 64, &bars[st], pol);
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kU1tStages; ++st) mbar_init(&bars[st], 1);
+        fence_mbar_init();
+        for (int st = 0; st < kU1tStages; ++st)
+            if (s0 + st * G < s_end) issue(s0 + st * G, st);
+    }
+    __syncwarp();
+    int it = 0;
+    for (int64_t s = s0; s < s_end; s += G, ++it) {
+        const int st = it % kU1tStages;
+        const uint32_t ph = (it / kU1tStages) & 1;
+        mbar_wait(&bars[st], ph);
+        const unsigned char* b = ring + st * kU1tStageBytes;
+        const double* sv = reinterpret_cast<const double*>(b);
+        const uint32_t* sc = reinterpret_cast<const uint32_t*>(b + 32 * 8 * 8);
+        const int32_t* sd = reinterpret_cast<const int32_t*>(b + 32 * 8 * 8 + 8 * 16);
+        const int64_t row = s * 32 + lane;
+        int32_t c[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool ok = u < W;  // warp-uniform
+            const uint32_t wd = ok ? sc[u * 4 + (lane >> 3)] : 0xffffffffu;
+            const int code = static_cast<int>((wd >> ((lane & 7) * 4)) & 15u);
+            c[u] = code != 15 ? static_cast<int32_t>(row) + sd[code] : -1;
+            v[u] = ok ? sv[u * 32 + lane] : 0.0;
+        }
+        __syncwarp();  // every lane has its slots: the stage may be refilled
+        if (lane == 0 && s + kU1tStages * G < s_end) {
+            fence_proxy_async_smem();
+            issue(s + kU1tStages * G, st);
+        }
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? ld_x(x + c[u]) : 0.0;
+        double sum = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (c[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+        if (row >= row_begin && row < row_end) y[row] = sum;
+    }
+}
+
 // ---- U1 param 101 setup helpers: rows sorted by length ----------------------
 __global__ void k_sort_keys(const int32_t* __restrict__ rp, int64_t n, int32_t cap,
                             int32_t* __restrict__ key, int32_t* __restrict__ row) {
@@ -682,6 +763,23 @@ void u1_setup(ktb_plan* p) {
         p->launches = 1;
         return;
     }
+    if (p->param == 105) {  // persistent coded slices staged by per-warp bulk copies
+        require(p->cta_threads == 0, "u1: the staged slices run 256-thread CTAs");
+        u1_sell_setup(p);
+        if (p->ell_width < 1 || p->ell_width > 8)
+            throw Invalid("u1: staged slices need one slice width <= 8");
+        if ((reinterpret_cast<uintptr_t>(p->sell_val.p) & 15) != 0)
+            throw Invalid("u1: staged slices need 16-byte aligned values");
+        u1_dict_setup(p);
+        KTB_CUDA(cudaFuncSetAttribute(k_u1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kU1tSmem));
+        int occ = 0;
+        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u1t, kU1tWarps * 32,
+                                                               kU1tSmem));
+        p->ctas = static_cast<int64_t>(std::max(occ, 1)) * p->m->sm_count;
+        p->launches = 1;
+        return;
+    }
     if (p->param == 103 || p->param == 104) {  // persistent pipelined slices (ELL, W <= 8)
         require(p->cta_threads == 0, "u1: the persistent slices run 256-thread CTAs");
         u1_sell_setup(p);
@@ -758,6 +856,16 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         launch_u1s(p, slices * 32, p->sell_off.p, x, y, 0, static_cast<int32_t>(slices * 32), 0,
                    p->sell_perm.p);
         if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
+        return;
+    }
+    if (p->param == 105) {
+        const int64_t slices = ceil_div64(r1, 32) - (r0 >> 5);
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(p->ctas, ceil_div64(slices, kU1tWarps))));
+        k_u1t<<<grid, kU1tWarps * 32, kU1tSmem, p->stream>>>(
+            p->sell_val.p, p->sell_codes.p, p->sell_dict.p, x, y, static_cast<int32_t>(r0),
+            static_cast<int32_t>(r1), p->ell_width);
+        KTB_LAUNCH();
         return;
     }
     if (p->param == 103 || p->param == 104) {
