@@ -331,33 +331,44 @@ __global__ void __launch_bounds__(256, kDict ? 0 : 3) k_u1p(const int32_t* __res
 // stream in flight without registers. Lanes read their values / codes from
 // the stage (conflict-free), decode through the staged dictionary, gather x,
 // sum left to right (bitwise spmv_ref) and hand the stage back.
-constexpr int kU1tStages = 4;
-constexpr int kU1tStageBytes = 32 * 8 * 8 + 8 * 16 + 64;  // values (W <= 8), codes, dict: 2240
-constexpr int kU1tWarps = 8;
-constexpr int kU1tSmem = kU1tWarps * (kU1tStages * kU1tStageBytes + kU1tStages * 8);
+#ifndef KTB_U1T_STAGES
+#define KTB_U1T_STAGES 2
+#endif
+#ifndef KTB_U1T_WARPS
+#define KTB_U1T_WARPS 8
+#endif
+#ifndef KTB_U1T_MINB
+#define KTB_U1T_MINB 1
+#endif
+constexpr int kU1tStages = KTB_U1T_STAGES;
+constexpr int kU1tWarps = KTB_U1T_WARPS;
+// stage = one slice's values (32 W doubles), code words (4 W) and dictionary (16)
+inline int u1t_stage_bytes(int W) { return (32 * 8 * W + 16 * W + 64 + 15) & ~15; }
+inline int u1t_smem(int W) { return kU1tWarps * kU1tStages * (u1t_stage_bytes(W) + 8); }
 
-__global__ void __launch_bounds__(kU1tWarps * 32) k_u1t(const double* __restrict__ sval,
+__global__ void __launch_bounds__(kU1tWarps * 32, KTB_U1T_MINB) k_u1t(const double* __restrict__ sval,
                                                          const uint32_t* __restrict__ codes,
                                                          const int32_t* __restrict__ dict,
                                                          const double* __restrict__ x,
                                                          double* __restrict__ y, int32_t row_begin,
-                                                         int32_t row_end, int W) {
+                                                         int32_t row_end, int W, int stage_bytes) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* ring = smem + warp * (kU1tStages * kU1tStageBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kU1tWarps * kU1tStages * kU1tStageBytes) +
+    unsigned char* ring = smem + warp * (kU1tStages * stage_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kU1tWarps * kU1tStages * stage_bytes) +
                      warp * kU1tStages;
+    const int coff = 32 * 8 * W, doff = coff + 16 * W;  // codes, dictionary within a stage
     const int64_t G = static_cast<int64_t>(gridDim.x) * kU1tWarps;
     const int64_t s0 = (row_begin >> 5) + blockIdx.x * static_cast<int64_t>(kU1tWarps) + warp;
     const int64_t s_end = (static_cast<int64_t>(row_end) + 31) >> 5;
     const uint32_t vbytes = 32u * 8u * W, cbytes = 16u * W;
     const uint64_t pol = policy_evict_first();
     auto issue = [&](int64_t s, int st) {  // lane 0
-        unsigned char* b = ring + st * kU1tStageBytes;
+        unsigned char* b = ring + st * stage_bytes;
         mbar_arrive_expect_tx(&bars[st], vbytes + cbytes + 64);
         tma_load_1d(b, sval + s * 32 * W, vbytes, &bars[st], pol);
-        tma_load_1d(b + 32 * 8 * 8, codes + s * 4 * W, cbytes, &bars[st], pol);
-        tma_load_1d(b + 32 * 8 * 8 + 8 * 16, dict + s * 16, 64, &bars[st], pol);
+        tma_load_1d(b + coff, codes + s * 4 * W, cbytes, &bars[st], pol);
+        tma_load_1d(b + doff, dict + s * 16, 64, &bars[st], pol);
     };
     if (lane == 0) {
         for (int st = 0; st < kU1tStages; ++st) mbar_init(&bars[st], 1);
@@ -371,10 +382,10 @@ __global__ void __launch_bounds__(kU1tWarps * 32) k_u1t(const double* __restrict
         const int st = it % kU1tStages;
         const uint32_t ph = (it / kU1tStages) & 1;
         mbar_wait(&bars[st], ph);
-        const unsigned char* b = ring + st * kU1tStageBytes;
+        const unsigned char* b = ring + st * stage_bytes;
         const double* sv = reinterpret_cast<const double*>(b);
-        const uint32_t* sc = reinterpret_cast<const uint32_t*>(b + 32 * 8 * 8);
-        const int32_t* sd = reinterpret_cast<const int32_t*>(b + 32 * 8 * 8 + 8 * 16);
+        const uint32_t* sc = reinterpret_cast<const uint32_t*>(b + coff);
+        const int32_t* sd = reinterpret_cast<const int32_t*>(b + doff);
         const int64_t row = s * 32 + lane;
         int32_t c[8];
         double v[8];
@@ -771,11 +782,10 @@ void u1_setup(ktb_plan* p) {
         if ((reinterpret_cast<uintptr_t>(p->sell_val.p) & 15) != 0)
             throw Invalid("u1: staged slices need 16-byte aligned values");
         u1_dict_setup(p);
-        KTB_CUDA(cudaFuncSetAttribute(k_u1t, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kU1tSmem));
+        const int smem = u1t_smem(p->ell_width);
+        KTB_CUDA(cudaFuncSetAttribute(k_u1t, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int occ = 0;
-        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u1t, kU1tWarps * 32,
-                                                               kU1tSmem));
+        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u1t, kU1tWarps * 32, smem));
         p->ctas = static_cast<int64_t>(std::max(occ, 1)) * p->m->sm_count;
         p->launches = 1;
         return;
@@ -862,9 +872,9 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         const int64_t slices = ceil_div64(r1, 32) - (r0 >> 5);
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>(p->ctas, ceil_div64(slices, kU1tWarps))));
-        k_u1t<<<grid, kU1tWarps * 32, kU1tSmem, p->stream>>>(
+        k_u1t<<<grid, kU1tWarps * 32, u1t_smem(p->ell_width), p->stream>>>(
             p->sell_val.p, p->sell_codes.p, p->sell_dict.p, x, y, static_cast<int32_t>(r0),
-            static_cast<int32_t>(r1), p->ell_width);
+            static_cast<int32_t>(r1), p->ell_width, u1t_stage_bytes(p->ell_width));
         KTB_LAUNCH();
         return;
     }
