@@ -683,8 +683,8 @@ def run_halo(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-            "config": dict(config_block(cfg, "u1 persistent pipelined warp slices, coded "
-                                             "columns (param 104), ktb_halo_spmv"),
+            "config": dict(config_block(cfg, "u1 persistent warp slices, coded columns, "
+                                             "bulk-copy staged (param 105), ktb_halo_spmv"),
                            parallelism=f"row-block z-slabs x{ws}, one-plane halo, NCCL P2P"),
             "gflops": F / (ms / 1e3) / 1e9,
             "per_gpu_gbs": B / ws / (ms / 1e3) / 1e9,
@@ -699,7 +699,7 @@ def run_halo(args, cfg):
                          "frac": ach_min / peak,
                          "traffic": traffic_from_profile(cfg) if ws == 1 else None,
                          "peak_source": peak_src,
-                         "kernel": "k_u1p<coded> over the interior rows (1 launch per step)",
+                         "kernel": "k_u1t over the interior rows (1 launch per step)",
                          "bytes_per_launch": B_int,
                          "note": "achieved = the minimum-traffic model's bytes (12 B/nnz) over "
                                  "the kernel time, min over ranks; the kernel moves fewer bytes "

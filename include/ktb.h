@@ -160,7 +160,9 @@ int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
  *                a <= 15-entry dictionary of column deltas (8.5 B per slot
  *                instead of 12); 103 / 104 = persistent, two-deep pipelined
  *                warp slices (uniform width <= 8) with int32 / coded columns;
- *                100-104 are all bitwise equal to spmv_ref;
+ *                105 = persistent coded slices staged through per-warp
+ *                bulk-copy (TMA) rings (the halo operator's default);
+ *                100-105 are all bitwise equal to spmv_ref;
  *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8);
  *                104/108/112 = merge-path tiles;
  *            U3/U4: nonzeros per segment lane E in {4,8,16} (0 = 8); U3 1008

@@ -254,8 +254,8 @@ Entry& entry(const M& a, int kind) {
 }
 
 // default device variant per kernel when none was selected: U1 tries the
-// persistent coded slices (104), then the plain warp slices (100), then lanes
-inline int64_t default_param(int k) { return k == KTB_U1 ? 104 : 0; }
+// persistent coded slices (105), then the plain warp slices (100), then lanes
+inline int64_t default_param(int k) { return k == KTB_U1 ? 105 : 0; }
 
 template <typename M>
 std::shared_ptr<ktb_cpp::Plan> plan_for(const M& a, int kind, int kernel) {

@@ -476,13 +476,16 @@ ktb_halo* halo_create(ktb_matrix* local, int64_t halo_lo, int64_t halo_hi, ktb_c
         ktb_halo::Part q{r0, r1, nullptr, nullptr};
         q.m = matrix_slice(local, r0, r1);
         try {
-            try {
-                q.p = plan_create_internal(q.m, kernel, param, 0, h->cs);
-            } catch (const Invalid&) {
-                // the persistent / coded slice forms need a uniform width and
-                // few column deltas (a thin boundary part may not have them)
-                if (kernel != KTB_U1 || param < 102 || param > 104) throw;
-                q.p = plan_create_internal(q.m, kernel, 100, 0, h->cs);
+            // the persistent / coded slice forms need a uniform width and few
+            // column deltas (a thin boundary part may not have them): fall
+            // back 105 -> 104 -> 100
+            const int64_t tries[3] = {param, param == 105 ? 104 : 100, 100};
+            for (int t = 0; t < 3 && !q.p; ++t) {
+                try {
+                    q.p = plan_create_internal(q.m, kernel, tries[t], 0, h->cs);
+                } catch (const Invalid&) {
+                    if (kernel != KTB_U1 || param < 102 || param > 105 || t == 2) throw;
+                }
             }
         } catch (...) {
             delete q.m;
@@ -716,8 +719,8 @@ void dist_connect(ktb_dist* d, ktb_comm* comm, int kernel, int64_t param) {
         try {
             st->plan = plan_create_internal(d->local, kernel, param, 0, st->cs);
         } catch (const Invalid&) {
-            if (kernel != KTB_U1 || param != 100) throw;
-            // the warp-sliced copy refuses very irregular rows: nnz-balanced tiles
+            if (kernel != KTB_U1 || param < 100 || param > 105) throw;
+            // the warp-sliced / coded forms refuse irregular rows: nnz-balanced tiles
             st->plan = plan_create_internal(d->local, KTB_U2, 0, 0, st->cs);
         }
     }

@@ -310,7 +310,7 @@ class DistSpMV:
     halo group on a high-priority stream overlapped with the interior rows).
     Collective: every rank of ``comm`` constructs it together."""
 
-    def __init__(self, nx, ny, nz, comm: Comm, seed=4, diag=6.0, off=-1.0, kernel=0, param=104):
+    def __init__(self, nx, ny, nz, comm: Comm, seed=4, diag=6.0, off=-1.0, kernel=0, param=105):
         import ctypes as C
 
         import torch

@@ -279,11 +279,11 @@ def test_selector_unsym_and_sym(K):
     names = [c.name for c in rep.candidates]
     # U1 (lanes, warp-sliced x 3 CTA shapes, row-sorted x 3), U2 (warp tiles x
     # 2 shapes, merge path), U3 (lanes per E, warp tiles x 2 shapes)
-    assert names[:15] == ["u1"] * 12 + ["u2"] * 3 and set(names[15:]) == {"u3"}
-    assert all(c.correct for c in rep.candidates[12:])  # U2 and every U3 form
+    assert names[:16] == ["u1"] * 13 + ["u2"] * 3 and set(names[16:]) == {"u3"}
+    assert all(c.correct for c in rep.candidates[13:])  # U2 and every U3 form
     # param slot (reference name jl): the warp-sliced U1, its column-coded,
     # persistent and row-sorted forms
-    assert [c.jl for c in rep.candidates[1:12]] == [100] * 3 + [102] * 3 + [104, 103] + [101] * 3
+    assert [c.jl for c in rep.candidates[1:13]] == [100] * 3 + [102] * 3 + [105, 104, 103] + [101] * 3
     assert [c.cta_threads for c in rep.candidates[1:7]] == [128, 64, 256] * 2
     x = O.seeded_vector(n, 1)
     y = np.empty(n)
@@ -565,8 +565,8 @@ def test_u1_column_coded_slices(K):
         rp, ci, v = a.to_host()
         x = O.seeded_vector(a.n, seed)
         yref = O.spmv_ref(a.n, rp, ci, v, x)
-        for t in (64, 128, 256, 103, 104):
-            plan = K.DevicePlan(a, K.UnsymKernel.u1_row, t if t in (103, 104) else 102 | t * SHAPE)
+        for t in (64, 128, 256, 103, 104, 105):
+            plan = K.DevicePlan(a, K.UnsymKernel.u1_row, t if t in (103, 104, 105) else 102 | t * SHAPE)
             xd = torch.from_numpy(x).cuda()
             yd = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
             plan.apply(xd, yd)
