@@ -601,13 +601,14 @@ def run_halo(args, cfg):
             for ln in lines:
                 print(f"[rank {r}] {ln}", file=sys.stderr)
     t0 = time.perf_counter()
-    shard = D.DistSpMV(512, 512, 512, comm, seed=cfg["seed"])
+    shard = D.DistSpMV(512, 512, 512, comm, seed=cfg["seed"], param=args.u1_param)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     shard.set_timing(True)
     n_glob, nnz_glob = cfg["n"], cfg["nnz"]
     B, F = min_bytes(n_glob, nnz_glob), flops(n_glob, nnz_glob, False)
     ir, inz, br, bnz = shard.parts()
+    u1p = shard.plan_params()[0]
     B_int = min_bytes(ir, inz)
     stream = torch.cuda.Stream()
     flush = L2Flush(torch.cuda.get_device_properties(local).L2_cache_size)
@@ -683,8 +684,8 @@ def run_halo(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-            "config": dict(config_block(cfg, "u1 persistent warp slices, coded columns, "
-                                             "bulk-copy staged (param 105), ktb_halo_spmv"),
+            "config": dict(config_block(cfg, f"{U1_DESC.get(u1p, 'u1')} (param {u1p}), "
+                                             "ktb_halo_spmv"),
                            parallelism=f"row-block z-slabs x{ws}, one-plane halo, NCCL P2P"),
             "gflops": F / (ms / 1e3) / 1e9,
             "per_gpu_gbs": B / ws / (ms / 1e3) / 1e9,
@@ -699,13 +700,16 @@ def run_halo(args, cfg):
                          "frac": ach_min / peak,
                          "traffic": traffic_from_profile(cfg) if ws == 1 else None,
                          "peak_source": peak_src,
-                         "kernel": "k_u1t over the interior rows (1 launch per step)",
+                         "kernel": f"{U1_KERNEL.get(u1p, 'u1')} over the interior rows "
+                                   "(1 launch per step)",
                          "bytes_per_launch": B_int,
+                         "stream_bytes_per_launch": u1_stream_bytes(u1p, ir, inz),
                          "note": "achieved = the minimum-traffic model's bytes (12 B/nnz) over "
                                  "the kernel time, min over ranks; the kernel moves fewer bytes "
-                                 "than the model (8 B value + 0.5 B column code per slot, no "
-                                 "row_ptr), so frac can exceed 1; traffic = its measured DRAM "
-                                 "bytes per launch (ncu)"},
+                                 "than the model (" + U1_BYTES.get(u1p, "") + "), so frac can "
+                                 "exceed 1; stream_bytes_per_launch = the bytes of its own "
+                                 "layout + x + y; traffic = its measured DRAM bytes per launch "
+                                 "(ncu)"},
             "e2e": {"value": B / (e2e16 / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
                     "ms_per_step": e2e16,
@@ -1015,6 +1019,35 @@ def _gmres_cpu_baseline(a, B, full=False):
 
 
 
+U1_DESC = {
+    106: "u1 persistent warp slices, coded columns and coded values, bulk-copy staged",
+    105: "u1 persistent warp slices, coded columns, bulk-copy staged",
+    104: "u1 persistent pipelined warp slices, coded columns",
+    100: "u1 warp slices",
+}
+U1_KERNEL = {106: "k_u1v", 105: "k_u1t", 104: "k_u1p<coded>", 100: "k_u1s"}
+U1_BYTES = {
+    106: "one 448-byte record per 32 rows: 8 slot bytes per row (4-bit column code + 4-bit "
+         "value code) and the slice's two dictionaries; no row_ptr",
+    105: "8 B value + 0.5 B column code per slot, no row_ptr",
+    104: "8 B value + 0.5 B column code per slot, no row_ptr",
+    100: "no row_ptr",
+}
+
+
+def u1_stream_bytes(param, rows, nnz, width=7):
+    """Bytes the U1 variant's own layout streams per launch (+ x and y once)."""
+    slices = (rows + 31) // 32
+    xy = 16 * rows
+    if param == 106:
+        return slices * 448 + xy
+    if param in (104, 105):
+        return slices * (32 * width * 8 + 16 * width + 64) + xy
+    if param == 100:
+        return slices * 32 * width * 12 + xy
+    return None
+
+
 def traffic_from_profile(cfg):
     """dram bytes (read+write) per launch of the dominant kernel from the
     committed ncu --set full summary, if present (profiles/traffic.json)."""
@@ -1038,6 +1071,9 @@ def main():
                          "(oracle/Makefile): the reference's CMake Release (default), "
                          "+ -march=native, or the -ffp-contract=off parity build")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--u1-param", type=int, default=106,
+                    help="config 4: the halo operator's U1 variant (106 = coded columns and "
+                         "values, falls back to 105 = coded columns, 104, 100)")
     ap.add_argument("--ref-seconds", type=float, default=0.0,
                     help=argparse.SUPPRESS)  # cpu_baseline: time applies for this long
     ap.add_argument("--no-secondary", action="store_true",

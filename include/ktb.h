@@ -161,8 +161,11 @@ int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
  *                instead of 12); 103 / 104 = persistent, two-deep pipelined
  *                warp slices (uniform width <= 8) with int32 / coded columns;
  *                105 = persistent coded slices staged through per-warp
- *                bulk-copy (TMA) rings (the halo operator's default);
- *                100-105 are all bitwise equal to spmv_ref;
+ *                bulk-copy (TMA) rings; 106 = the same with the values coded
+ *                too (per slice <= 15 distinct fp64 bit patterns: one 448-byte
+ *                record per 32 rows, 14 B per row; refused otherwise) -- the
+ *                halo operator's default, falling back to 105;
+ *                100-106 are all bitwise equal to spmv_ref;
  *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8);
  *                104/108/112 = merge-path tiles;
  *            U3/U4: nonzeros per segment lane E in {4,8,16} (0 = 8); U3 1008
@@ -367,6 +370,9 @@ int ktb_halo_create_csr(int64_t n_global, int64_t row0, int64_t n_local, const i
 int ktb_halo_info(const ktb_halo* h, int64_t* n_local, int64_t* x_len, int64_t* owned_offset,
                   int64_t* interior_begin, int64_t* interior_end, int64_t* nnz, int* launches);
 /* Rows and stored entries of the interior and boundary parts. */
+/* The U1 variant (plan param) the interior / first boundary rows resolved to
+ * after the create call's fallbacks (106 -> 105 -> 104 -> 100); -1 = no rows. */
+int ktb_halo_plan_params(const ktb_halo* h, int64_t* interior_param, int64_t* boundary_param);
 int ktb_halo_parts(const ktb_halo* h, int64_t* interior_rows, int64_t* interior_nnz,
                    int64_t* boundary_rows, int64_t* boundary_nnz);
 /* y = A x (device pointers, asynchronous on stream). x has x_len entries with

@@ -254,8 +254,9 @@ Entry& entry(const M& a, int kind) {
 }
 
 // default device variant per kernel when none was selected: U1 tries the
-// persistent coded slices (105), then the plain warp slices (100), then lanes
-inline int64_t default_param(int k) { return k == KTB_U1 ? 105 : 0; }
+// persistent slices with coded columns and values (106), with coded columns
+// only (105), then the plain warp slices (100), then lanes
+inline int64_t default_param(int k) { return k == KTB_U1 ? 106 : 0; }
 
 template <typename M>
 std::shared_ptr<ktb_cpp::Plan> plan_for(const M& a, int kind, int kernel) {
@@ -265,14 +266,15 @@ std::shared_ptr<ktb_cpp::Plan> plan_for(const M& a, int kind, int kernel) {
     auto it = e.plans.find(kernel);
     if (it != e.plans.end()) return it->second;
     std::shared_ptr<ktb_cpp::Plan> p;
-    const int64_t tries[3] = {default_param(kernel), 100, 0};
-    for (int t = 0; t < (kernel == KTB_U1 ? 3 : 1) && !p; ++t) {
+    const int64_t tries[4] = {default_param(kernel), 105, 100, 0};
+    for (int t = 0; t < (kernel == KTB_U1 ? 4 : 1) && !p; ++t) {
         try {
             p = std::make_shared<ktb_cpp::Plan>(e.dm, kernel, tries[t]);
         } catch (const Error&) {
-            // refused layouts: uniform width / few column deltas (104), or
-            // padding beyond 3x (100) for very irregular rows
-            if (kernel != KTB_U1 || t == 2) throw;
+            // refused layouts: few distinct values (106), uniform width / few
+            // column deltas (105), or padding beyond 3x (100) for very
+            // irregular rows
+            if (kernel != KTB_U1 || t == 3) throw;
         }
     }
     e.plans[kernel] = p;

@@ -86,6 +86,7 @@ def load() -> C.CDLL:
                                 C.c_int),
         "ktb_halo_info": ([VP] + [C.POINTER(I64)] * 6 + [C.POINTER(C.c_int)], C.c_int),
         "ktb_halo_parts": ([VP] + [C.POINTER(I64)] * 4, C.c_int),
+        "ktb_halo_plan_params": ([VP] + [C.POINTER(I64)] * 2, C.c_int),
         "ktb_halo_spmv": ([VP, VP, VP, VP], C.c_int),
         "ktb_halo_exchange": ([VP, VP, VP], C.c_int),
         "ktb_halo_spmv_host": ([VP, VP, VP, C.c_int], C.c_int),

@@ -901,6 +901,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
             add(KTB_U1, 0, "u1", 0);
             for (int t : {128, 64, 256}) add(KTB_U1, 100, "u1", 0, t);  // warp-sliced copy
             for (int t : {128, 64, 256}) add(KTB_U1, 102, "u1", 0, t);  // + coded columns
+            add(KTB_U1, 106, "u1", 0);  // persistent slices, coded columns and values
             add(KTB_U1, 105, "u1", 0);  // persistent coded slices, bulk-copy staged
             add(KTB_U1, 104, "u1", 0);  // persistent pipelined slices, coded columns
             add(KTB_U1, 103, "u1", 0);  // the same with int32 columns

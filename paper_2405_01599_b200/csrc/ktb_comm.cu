@@ -478,13 +478,14 @@ ktb_halo* halo_create(ktb_matrix* local, int64_t halo_lo, int64_t halo_hi, ktb_c
         try {
             // the persistent / coded slice forms need a uniform width and few
             // column deltas (a thin boundary part may not have them): fall
-            // back 105 -> 104 -> 100
-            const int64_t tries[3] = {param, param == 105 ? 104 : 100, 100};
-            for (int t = 0; t < 3 && !q.p; ++t) {
+            // back 106 -> 105 -> 104 -> 100 (106 also needs few distinct values)
+            const int64_t tries[4] = {param, param == 106 ? 105 : param == 105 ? 104 : 100,
+                                      param == 106 ? 104 : 100, 100};
+            for (int t = 0; t < 4 && !q.p; ++t) {
                 try {
                     q.p = plan_create_internal(q.m, kernel, tries[t], 0, h->cs);
                 } catch (const Invalid&) {
-                    if (kernel != KTB_U1 || param < 102 || param > 105 || t == 2) throw;
+                    if (kernel != KTB_U1 || param < 102 || param > 106 || t == 3) throw;
                 }
             }
         } catch (...) {
@@ -719,7 +720,7 @@ void dist_connect(ktb_dist* d, ktb_comm* comm, int kernel, int64_t param) {
         try {
             st->plan = plan_create_internal(d->local, kernel, param, 0, st->cs);
         } catch (const Invalid&) {
-            if (kernel != KTB_U1 || param < 100 || param > 105) throw;
+            if (kernel != KTB_U1 || param < 100 || param > 106) throw;
             // the warp-sliced / coded forms refuse irregular rows: nnz-balanced tiles
             st->plan = plan_create_internal(d->local, KTB_U2, 0, 0, st->cs);
         }
@@ -967,6 +968,14 @@ int ktb_halo_info(const ktb_halo* h, int64_t* n_local, int64_t* x_len, int64_t* 
                 for (auto& q : *v) l += q.p->launches;
             *launches = l;
         }
+    });
+}
+
+int ktb_halo_plan_params(const ktb_halo* h, int64_t* interior_param, int64_t* boundary_param) {
+    return guarded_call([&] {
+        require(h != nullptr, "halo: null handle");
+        if (interior_param) *interior_param = h->interior.empty() ? -1 : h->interior[0].p->param;
+        if (boundary_param) *boundary_param = h->boundary.empty() ? -1 : h->boundary[0].p->param;
     });
 }
 

@@ -413,6 +413,201 @@ __global__ void __launch_bounds__(kU1tWarps * 32, KTB_U1T_MINB) k_u1t(const doub
     }
 }
 
+// ---- U1 param 106: persistent slices with coded (column, value) pairs ----
+// Many matrices (every constant-coefficient stencil, graph Laplacians,
+// adjacency matrices) hold only a handful of distinct (column - row, value)
+// pairs per 32 rows. 106 stores one 384-byte record per slice: a dictionary
+// of <= 15 pairs (16 bytes each: the fp64 bit pattern, the int32 column
+// delta, a "real" word; entry 15 = padding) and per row one 32-bit word of
+// eight 4-bit pair codes: 12 B per row whatever W <= 8 is, instead of 8.5 B
+// per slot. The values the kernel multiplies are the stored bit patterns and
+// the sum runs left to right with unfused multiply-add: bitwise spmv_ref. A
+// slice with more distinct pairs refuses the layout (the selector and the
+// halo operator fall back to 105). One bulk copy per slice fills a stage of
+// the warp's ring; a slot costs one 16-byte shared-memory lookup, one wide
+// multiply-add for the address, the gather and the two fp64 operations.
+constexpr int kU1vRec = 384;     // bytes per slice record: dictionary, then the code words
+constexpr int kU1vCodes = 256;   // offset of the code words
+constexpr int kU1vStage = 512;   // stage stride (dictionaries 256-byte aligned)
+#ifndef KTB_U1V_STAGES
+#define KTB_U1V_STAGES 4
+#endif
+#ifndef KTB_U1V_WARPS
+#define KTB_U1V_WARPS 8
+#endif
+#ifndef KTB_U1V_MINB
+#define KTB_U1V_MINB 4  // 64 registers, 32 warps per SM: 895 us on config 4 (72 registers / 24 warps: 1,001 us)
+#endif
+constexpr int kU1vStages = KTB_U1V_STAGES;
+constexpr int kU1vWarps = KTB_U1V_WARPS;
+inline int u1v_smem() { return kU1vWarps * kU1vStages * (kU1vStage + 8) + 256; }
+
+// one warp per slice of the ELL copy: the pair dictionary by ballot matching
+// (first-occurrence order, slot-major), then the code words
+__global__ void k_vrec_build(const int32_t* __restrict__ scol, const double* __restrict__ sval,
+                             int64_t slices, int W, unsigned char* __restrict__ rec,
+                             int* __restrict__ overflow) {
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= slices) return;  // whole warps
+    const int64_t o = s * 32 * W;
+    const int32_t row = static_cast<int32_t>(s * 32 + lane);
+    int32_t dc = 0;              // lane j < np: pair j
+    unsigned long long dv = 0;
+    int np = 0;
+    bool ok = true;
+    uint32_t word = 0xffffffffu;  // this lane's row: nibble 15 = padding
+    for (int k = 0; k < W; ++k) {
+        const int64_t at = o + static_cast<int64_t>(k) * 32 + lane;
+        const int32_t c = scol[at];
+        const unsigned long long vb =
+            static_cast<unsigned long long>(__double_as_longlong(sval[at]));
+        const int32_t d = c - row;
+        int code = 15;
+        unsigned pending = __ballot_sync(0xffffffffu, c >= 0);
+        while (pending) {
+            const int src = __ffs(pending) - 1;
+            const int32_t wd = __shfl_sync(0xffffffffu, d, src);
+            const unsigned long long wv = __shfl_sync(0xffffffffu, vb, src);
+            const unsigned same = __ballot_sync(0xffffffffu, c >= 0 && d == wd && vb == wv);
+            const unsigned hit = __ballot_sync(0xffffffffu, lane < np && dc == wd && dv == wv);
+            int j;
+            if (hit) {
+                j = __ffs(hit) - 1;
+            } else if (np < 15) {
+                j = np++;
+                if (lane == j) {
+                    dc = wd;
+                    dv = wv;
+                }
+            } else {
+                j = 14;
+                ok = false;
+            }
+            if ((same >> lane) & 1u) code = j;
+            pending &= ~same;
+        }
+        word = (word & ~(15u << (4 * k))) | (static_cast<uint32_t>(code) << (4 * k));
+    }
+    unsigned char* r = rec + s * kU1vRec;
+    if (lane < 16) {
+        const bool real = lane < np;
+        uint4 e;
+        e.x = real ? static_cast<uint32_t>(dv) : 0u;
+        e.y = real ? static_cast<uint32_t>(dv >> 32) : 0u;
+        e.z = real ? static_cast<uint32_t>(dc) : 0u;
+        e.w = real ? 1u : 0u;
+        reinterpret_cast<uint4*>(r)[lane] = e;
+    }
+    reinterpret_cast<uint32_t*>(r + kU1vCodes)[lane] = word;
+    if (!ok && lane == 0) atomicOr(overflow, 1);
+}
+
+// kW = the plan's slice width: slots kW..7 are padding in every row and cost
+// nothing (the L1TEX data pipe is this kernel's bound: 4 cycles per 16-byte
+// lookup, 2-3 per gather)
+template <int kW>
+__global__ void __launch_bounds__(kU1vWarps * 32, KTB_U1V_MINB)
+    k_u1v(const unsigned char* __restrict__ rec, const double* __restrict__ x,
+          double* __restrict__ y, int32_t row_begin, int32_t row_end, int32_t nrows) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // stages 256-byte aligned in the shared window: a dictionary entry's
+    // address is then (stage | code << 4), one logic operation
+    const uint32_t base = (smem_u32(smem_raw) + 255u) & ~255u;
+    const uint32_t ring = base + warp * (kU1vStages * kU1vStage);
+    const uint32_t bars = base + kU1vWarps * kU1vStages * kU1vStage + warp * kU1vStages * 8;
+    const int G = static_cast<int>(gridDim.x) * kU1vWarps;
+    const int first = (row_begin >> 5) + blockIdx.x * kU1vWarps + warp;
+    const int last = static_cast<int>((static_cast<int64_t>(row_end) + 31) >> 5);
+    const int nj = first < last ? (last - first + G - 1) / G : 0;  // this warp's slices
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int j, int st) {  // lane 0: one bulk copy per slice
+        const uint32_t bar = bars + st * 8;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(kU1vRec)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(ring + st * kU1vStage),
+            "l"(rec + (static_cast<int64_t>(first) + static_cast<int64_t>(j) * G) * kU1vRec),
+            "r"(kU1vRec), "r"(bar), "l"(pol)
+            : "memory");
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kU1vStages; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + st * 8), "r"(1)
+                         : "memory");
+        fence_mbar_init();
+        for (int st = 0; st < kU1vStages; ++st)
+            if (st < nj) issue(st, st);
+    }
+    __syncwarp();
+    for (int j = 0; j < nj; ++j) {
+        const int st = j % kU1vStages;
+        const uint32_t sb = ring + st * kU1vStage;
+        {
+            KTB_CHAOS_DELAY(0x7531);
+            const uint32_t ph = (j / kU1vStages) & 1, bar = bars + st * 8;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "WAITV_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra WAITV_%=;\n"
+                "}\n" ::"r"(bar),
+                "r"(ph)
+                : "memory");
+        }
+        uint32_t w;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(sb + kU1vCodes + lane * 4));
+        const int64_t row = (static_cast<int64_t>(first) + static_cast<int64_t>(j) * G) * 32 + lane;
+        // rows past the end of the matrix (last slice) hold padding only: their
+        // unconditional gathers read x at the last row instead
+        const double* xr = x + min(row, static_cast<int64_t>(nrows) - 1);
+        double v[kW], xv[kW];
+        uint32_t real[kW];
+#pragma unroll
+        for (int u = 0; u < kW; ++u) {
+            const uint32_t off = (u == 0 ? (w << 4) : (w >> (4 * u - 4))) & 0xf0u;
+            uint32_t e0, e1, e2, e3;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
+                         : "r"(sb | off));
+            v[u] = __hiloint2double(static_cast<int>(e1), static_cast<int>(e0));
+            real[u] = e3;
+            const double* px;
+            asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(px) : "r"(static_cast<int32_t>(e2)), "l"(xr));
+            xv[u] = ld_x(px);
+        }
+        __syncwarp();  // every lane has its slots: the stage may be refilled
+        if (lane == 0 && j + kU1vStages < nj) {
+            fence_proxy_async_smem();
+            issue(j + kU1vStages, st);
+        }
+        double sum = 0.0;
+#pragma unroll
+        for (int u = 0; u < kW; ++u)
+            if (real[u]) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+        if (row >= row_begin && row < row_end) y[row] = sum;
+    }
+}
+
+using U1vFn = void (*)(const unsigned char*, const double*, double*, int32_t, int32_t, int32_t);
+static U1vFn u1v_kernel(int W) {
+    switch (W) {
+        case 1: return k_u1v<1>;
+        case 2: return k_u1v<2>;
+        case 3: return k_u1v<3>;
+        case 4: return k_u1v<4>;
+        case 5: return k_u1v<5>;
+        case 6: return k_u1v<6>;
+        case 7: return k_u1v<7>;
+        case 8: return k_u1v<8>;
+        default: throw Invalid("u1: staged slices need one slice width <= 8");
+    }
+}
+
 // ---- U1 param 101 setup helpers: rows sorted by length ----------------------
 __global__ void k_sort_keys(const int32_t* __restrict__ rp, int64_t n, int32_t cap,
                             int32_t* __restrict__ key, int32_t* __restrict__ row) {
@@ -647,6 +842,28 @@ static void u1_dict_setup(ktb_plan* p) {
     p->extra_bytes += static_cast<int64_t>(padded / 2 + 64 * slices) - 4 * padded;
 }
 
+// U1 param 106: the slice records (pair dictionary + code words) from the
+// ELL copy; they replace both the columns and the values.
+static void u1_vrec_setup(ktb_plan* p) {
+    const int64_t slices = ceil_div64(p->m->n, 32);
+    p->sell_rec.alloc(std::max<int64_t>(slices, 1) * kU1vRec);
+    DBuf<int> overflow(1);
+    KTB_CUDA(cudaMemsetAsync(overflow.p, 0, sizeof(int), p->stream));
+    k_vrec_build<<<ceil_div(slices * 32, 256), 256, 0, p->stream>>>(
+        p->sell_col.p, p->sell_val.p, slices, p->ell_width, p->sell_rec.p, overflow.p);
+    KTB_LAUNCH();
+    int ov = 0;
+    KTB_CUDA(cudaMemcpyAsync(&ov, overflow.p, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    KTB_CUDA(cudaStreamSynchronize(p->stream));
+    if (ov)
+        throw Invalid("u1: a warp slice needs more than 15 distinct (column delta, value) pairs");
+    const int64_t padded = static_cast<int64_t>(p->sell_col.n);
+    p->sell_col.release();
+    p->sell_val.release();
+    // 384 B per slice instead of the warp-sliced copy's 12 B per slot
+    p->extra_bytes += slices * kU1vRec - 12 * padded;
+}
+
 // U1 param 101: rows of length <= kSortedCap sorted by length (descending,
 // stable) into warp slices -- near-uniform slice widths for any row-length
 // distribution; longer rows go to a compact sub-matrix reduced by U2 warp
@@ -774,6 +991,21 @@ void u1_setup(ktb_plan* p) {
         p->launches = 1;
         return;
     }
+    if (p->param == 106) {  // persistent slices, coded columns and coded values
+        require(p->cta_threads == 0, "u1: the staged slices run 256-thread CTAs");
+        u1_sell_setup(p);
+        if (p->ell_width < 1 || p->ell_width > 8)
+            throw Invalid("u1: staged slices need one slice width <= 8");
+        u1_vrec_setup(p);
+        const int smem = u1v_smem();
+        const U1vFn fn = u1v_kernel(p->ell_width);
+        KTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int occ = 0;
+        KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kU1vWarps * 32, smem));
+        p->ctas = static_cast<int64_t>(std::max(occ, 1)) * p->m->sm_count;
+        p->launches = 1;
+        return;
+    }
     if (p->param == 105) {  // persistent coded slices staged by per-warp bulk copies
         require(p->cta_threads == 0, "u1: the staged slices run 256-thread CTAs");
         u1_sell_setup(p);
@@ -866,6 +1098,16 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         launch_u1s(p, slices * 32, p->sell_off.p, x, y, 0, static_cast<int32_t>(slices * 32), 0,
                    p->sell_perm.p);
         if (p->long_plan) KTB_CUDA(cudaStreamWaitEvent(p->stream, p->join, 0));
+        return;
+    }
+    if (p->param == 106) {
+        const int64_t slices = ceil_div64(r1, 32) - (r0 >> 5);
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(p->ctas, ceil_div64(slices, kU1vWarps))));
+        u1v_kernel(p->ell_width)<<<grid, kU1vWarps * 32, u1v_smem(), p->stream>>>(
+            p->sell_rec.p, x, y, static_cast<int32_t>(r0), static_cast<int32_t>(r1),
+            static_cast<int32_t>(p->m->n));
+        KTB_LAUNCH();
         return;
     }
     if (p->param == 105) {

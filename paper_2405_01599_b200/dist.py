@@ -310,7 +310,7 @@ class DistSpMV:
     halo group on a high-priority stream overlapped with the interior rows).
     Collective: every rank of ``comm`` constructs it together."""
 
-    def __init__(self, nx, ny, nz, comm: Comm, seed=4, diag=6.0, off=-1.0, kernel=0, param=105):
+    def __init__(self, nx, ny, nz, comm: Comm, seed=4, diag=6.0, off=-1.0, kernel=0, param=106):
         import ctypes as C
 
         import torch
@@ -348,6 +348,15 @@ class DistSpMV:
 
         v = [C.c_int64() for _ in range(4)]
         self._check(self._L.ktb_halo_parts(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def plan_params(self):
+        """(interior, boundary) U1 variants the plans resolved to after the
+        create call's fallbacks (106 -> 105 -> 104 -> 100); -1 = no rows."""
+        import ctypes as C
+
+        v = [C.c_int64() for _ in range(2)]
+        self._check(self._L.ktb_halo_plan_params(self.h, *[C.byref(x) for x in v]))
         return tuple(x.value for x in v)
 
     def _s(self, stream=None):

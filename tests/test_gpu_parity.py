@@ -279,11 +279,12 @@ def test_selector_unsym_and_sym(K):
     names = [c.name for c in rep.candidates]
     # U1 (lanes, warp-sliced x 3 CTA shapes, row-sorted x 3), U2 (warp tiles x
     # 2 shapes, merge path), U3 (lanes per E, warp tiles x 2 shapes)
-    assert names[:16] == ["u1"] * 13 + ["u2"] * 3 and set(names[16:]) == {"u3"}
-    assert all(c.correct for c in rep.candidates[13:])  # U2 and every U3 form
+    assert names[:17] == ["u1"] * 14 + ["u2"] * 3 and set(names[17:]) == {"u3"}
+    assert all(c.correct for c in rep.candidates[14:])  # U2 and every U3 form
     # param slot (reference name jl): the warp-sliced U1, its column-coded,
     # persistent and row-sorted forms
-    assert [c.jl for c in rep.candidates[1:13]] == [100] * 3 + [102] * 3 + [105, 104, 103] + [101] * 3
+    assert [c.jl for c in rep.candidates[1:14]] == ([100] * 3 + [102] * 3 + [106, 105, 104, 103]
+                                                    + [101] * 3)
     assert [c.cta_threads for c in rep.candidates[1:7]] == [128, 64, 256] * 2
     x = O.seeded_vector(n, 1)
     y = np.empty(n)
@@ -565,8 +566,9 @@ def test_u1_column_coded_slices(K):
         rp, ci, v = a.to_host()
         x = O.seeded_vector(a.n, seed)
         yref = O.spmv_ref(a.n, rp, ci, v, x)
-        for t in (64, 128, 256, 103, 104, 105):
-            plan = K.DevicePlan(a, K.UnsymKernel.u1_row, t if t in (103, 104, 105) else 102 | t * SHAPE)
+        for t in (64, 128, 256, 103, 104, 106, 105):
+            plan = K.DevicePlan(a, K.UnsymKernel.u1_row,
+                                t if t in (103, 104, 105, 106) else 102 | t * SHAPE)
             xd = torch.from_numpy(x).cuda()
             yd = torch.full((a.n,), float("nan"), dtype=torch.float64, device="cuda")
             plan.apply(xd, yd)
@@ -606,6 +608,82 @@ def test_u1_column_coded_slices(K):
     n, rp, ci, v = matgen.random_csr(3000, 0.01, rng)
     with pytest.raises(K.Error):
         K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 102)
+
+
+def test_u1_value_coded_slices(K):
+    """U1 param 106: one 384-byte record per warp slice -- a dictionary of
+    <= 15 (column delta, fp64 bit pattern) pairs and eight 4-bit pair codes
+    per row. The multiplied values are the stored bit patterns and the sum
+    keeps spmv_ref's order: bitwise equal on banded matrices with exactly 15
+    distinct pairs per slice (incl. -0.0 next to 0.0, denormals, huge
+    values), with per-slice value sets that differ from slice to slice, empty
+    rows, row sub-ranges, n not a multiple of 32; 16 distinct pairs in one
+    slice, a row longer than 8 and random values are refused (the callers
+    fall back to 105)."""
+    import torch
+
+    rng = np.random.default_rng(106)
+    deltas = [-300, -33, -1, 0, 1, 40, 512]
+
+    def banded(n, vals_of, empty_every=0):
+        """vals_of(slice, delta index) -> the values that delta may take there."""
+        rows, vals = [], []
+        for i in range(n):
+            if empty_every and i % empty_every == 3:
+                rows.append(np.zeros(0, np.int64))
+                vals.append(np.zeros(0))
+                continue
+            keep = [k for k, d in enumerate(deltas) if 0 <= i + d < n and rng.random() < 0.85]
+            rows.append(np.array([i + deltas[k] for k in keep], np.int64))
+            vals.append(np.array([rng.choice(vals_of(i // 32, k)) for k in keep], np.float64))
+        rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+        return n, rp, np.concatenate(rows).astype(np.int64), np.concatenate(vals)
+
+    special = np.array([0.0, -0.0, 5e-324, -1.7e308, 1.0, -1.0, 6.0, 26.0, 1 / 3, -0.7, -1.3,
+                        2.0 ** -40, 3.5, 1e100, 7.25])
+    assert len(set(special.view(np.int64).tolist())) == 15
+    # 7 deltas x 2 values + a third value on the diagonal = 15 pairs per slice
+    two = lambda s, k: special[2 * k:2 * k + 2] if k != 3 else special[[6, 7, 14]]  # noqa: E731
+    own = lambda s, k: np.random.default_rng(1000 * s + k).uniform(-1, 1, 2)  # noqa: E731
+    cases = [banded(5003, two), banded(3000, lambda s, k: special[k:k + 1], empty_every=5),
+             banded(4001, own)]  # every slice its own values
+    for n, rp, ci, v in cases:
+        a = K.CsrMatrix(n, rp, ci, v)
+        x = O.seeded_vector(n, 4)
+        yref = O.spmv_ref(n, rp, ci, v, x)
+        plan = K.DevicePlan(a, K.UnsymKernel.u1_row, 106)
+        y = np.full(n, np.nan)
+        plan.apply(x, y)
+        assert np.array_equal(y.view(np.int64), yref.view(np.int64))  # incl. the sign of zero
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+        r0, r1 = 37, n - 45
+        plan.apply_rows(r0, r1, xd, yd)
+        torch.cuda.synchronize()
+        got = yd.cpu().numpy()
+        assert np.array_equal(got[r0:r1], yref[r0:r1]) and np.isnan(got[:r0]).all() \
+            and np.isnan(got[r1:]).all()
+    # an infinite x entry next to padding slots must not leak a NaN (0 * inf)
+    n, rp, ci, v = cases[1]
+    x = O.seeded_vector(n, 4)
+    x[[0, 77, n - 1]] = np.inf
+    y = np.full(n, np.nan)
+    K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106).apply(x, y)
+    with np.errstate(invalid="ignore"):
+        yref = O.spmv_ref(n, rp, ci, v, x)
+    # (NaN sign/payload differs between x86 and the GPU: compare as numbers)
+    assert np.array_equal(y, yref, equal_nan=True) and np.isnan(yref).sum() < 40
+    # 16 distinct pairs in one slice
+    n, rp, ci, v = banded(4000, lambda s, k: special[2 * k:2 * k + 2] if k != 3 else special[[6, 7, 14, 13]])
+    with pytest.raises(K.Error, match="15 distinct .column delta, value. pairs"):
+        K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106)
+    # random values (config 3's kind) and rows longer than 8
+    n, rp, ci, v = banded(3000, lambda s, k: rng.uniform(-1, 1, 64))
+    with pytest.raises(K.Error):
+        K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106)
+    n, rp, ci, v = matgen.stencil27_upper(12, 12, 12)
+    with pytest.raises(K.Error, match="width <= 8"):
+        K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106)
 
 
 def test_u1_sorted_slices(K):

@@ -56,10 +56,11 @@ def main():
     rp[1:] = np.cumsum([len(r) for r in rows])
     s = K.SymCsrMatrix(n, rp, np.concatenate(rows), rng.uniform(-1, 1, int(rp[-1])))
     rep_apply(K.DevicePlan(s, K.SymKernel.s3_nnz_zero_omit), O.seeded_vector(n, 3), n, "s3_far")
-    # persistent coded slices: register-pipelined (104) and bulk-copy staged (105)
+    # persistent coded slices: register-pipelined (104), bulk-copy staged (105),
+    # and with coded values (106)
     a5 = K.stencil7(96, 80, 64, c_xm=-1.3, c_xp=-0.7)
     x5 = O.seeded_vector(a5.n, 5)
-    for prm in (104, 105):
+    for prm in (104, 105, 106):
         rep_apply(K.DevicePlan(a5, 0, prm), x5, a5.n, f"u1_{prm}")
     # warp tiles (smem products, swizzled row-end maps, carries), both shapes
     n, rp, ci, v = matgen.powerlaw(300_000, 3, 3_000_000, 0.1, 65536)
