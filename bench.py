@@ -744,8 +744,11 @@ def secondary_cfg2(local, args):
         B = min_bytes(r["n"], r["nnz"])
         peak, _ = peak_hbm()
         a = B / (r["ms"] / 1e3) / 1e9
-        return {"cfg2_s3": {"workload": CONFIGS[2]["workload"],
+        s3 = [c.best_seconds * 1e3 for c in r["rep"].candidates
+              if c.name == "s3" and c.correct and c.best_seconds < float("inf")]
+        return {"cfg2_sym": {"workload": CONFIGS[2]["workload"],
                             "kernel": f"{r['sel'].name} (param {r['sel'].jl})",
+                            "s3_ms_in_selection": min(s3) if s3 else None,
                             "ms_per_step": r["ms"], "value": a, "unit": "GB/s",
                             "frac": a / peak, "launches": r["plan"].launches,
                             "gflops": flops(r["n"], r["nnz"], True) / (r["ms"] / 1e3) / 1e9,
@@ -753,7 +756,7 @@ def secondary_cfg2(local, args):
                             "setup_seconds": {"matrix": r["build_s"], "selection": r["select_s"]},
                             "l2": L2_NOTE}}
     except Exception as e:
-        return {"cfg2_s3": {"unavailable": str(e)}}
+        return {"cfg2_sym": {"unavailable": str(e)}}
 
 
 # ------------------------------------- configs 1/3 --shard: general row blocks
@@ -1020,15 +1023,15 @@ def _gmres_cpu_baseline(a, B, full=False):
 
 
 U1_DESC = {
-    106: "u1 persistent warp slices, coded columns and coded values, bulk-copy staged",
+    106: "u1 persistent warp slices, coded (column delta, value) pairs, bulk-copy staged",
     105: "u1 persistent warp slices, coded columns, bulk-copy staged",
     104: "u1 persistent pipelined warp slices, coded columns",
     100: "u1 warp slices",
 }
 U1_KERNEL = {106: "k_u1v", 105: "k_u1t", 104: "k_u1p<coded>", 100: "k_u1s"}
 U1_BYTES = {
-    106: "one 448-byte record per 32 rows: 8 slot bytes per row (4-bit column code + 4-bit "
-         "value code) and the slice's two dictionaries; no row_ptr",
+    106: "one 640-byte record per 64 rows: a dictionary of the record's (column delta, fp64 "
+         "value) pairs and one 8-bit pair code per slot; no row_ptr",
     105: "8 B value + 0.5 B column code per slot, no row_ptr",
     104: "8 B value + 0.5 B column code per slot, no row_ptr",
     100: "no row_ptr",
@@ -1040,7 +1043,7 @@ def u1_stream_bytes(param, rows, nnz, width=7):
     slices = (rows + 31) // 32
     xy = 16 * rows
     if param == 106:
-        return slices * 448 + xy
+        return (rows + 63) // 64 * (16 * (width + 1) + 256 * ((width + 3) // 4)) + xy
     if param in (104, 105):
         return slices * (32 * width * 8 + 16 * width + 64) + xy
     if param == 100:

@@ -895,6 +895,7 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
         // (autotune.hpp:163, 206-212): CTA threads instead of OpenMP threads
         if (m->kind == KTB_SYM_UPPER) {
             add(KTB_S1, 0, "s1", 0);
+            add(KTB_S1, 106, "s1", 0);  // transposed products gathered: expanded coded slices
             add(KTB_S2, 0, "s2", 1);
             for (int t : {256, 512}) add(KTB_S3, 0, "s3", 2, t);
         } else {

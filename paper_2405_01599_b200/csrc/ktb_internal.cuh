@@ -268,7 +268,8 @@ struct ktb_plan {
     // U1 param 102: column-delta dictionary (16 int32 per slice) and 4-bit codes
     ktb::DBuf<uint32_t> sell_codes;
     ktb::DBuf<int32_t> sell_dict;
-    ktb::DBuf<unsigned char> sell_rec;  // U1 106: 448-byte slice records (codes + dictionaries)
+    ktb::DBuf<unsigned char> sell_rec;  // U1 106: slice records (pair dictionary + code words)
+    int rec_dict = 0, rec_words = 0, rec_bytes = 0, rec_stride = 0, rec_stages = 0;
     // U1 param 101: rows sorted by length into the slices (slot -> row), rows
     // longer than the slice cap in a compact sub-matrix run by U2 warp tiles
     ktb::DBuf<int32_t> sell_perm;

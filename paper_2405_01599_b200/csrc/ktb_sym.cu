@@ -97,8 +97,25 @@ __global__ void __launch_bounds__(256) k_sym_atomic(const int32_t* __restrict__ 
 }
 
 void s12_setup(ktb_plan* p) {
-    const ktb_matrix* m = p->m;
+    ktb_matrix* m = p->m;
     require(m->kind == KTB_SYM_UPPER, "spmv: symmetric kernel on a general matrix");
+    if (p->kernel == KTB_S1 && p->param == 106) {
+        // S1 with gathered transposed products: row-based, and the "reduction"
+        // disappears -- every row reads its lower entries from the expanded
+        // matrix's pair-coded warp slices (U1 106: a 27-point stencil row is
+        // 27 one-byte codes + its share of a 28-pair dictionary, less than
+        // the upper triangle's CRS). Deterministic, bitwise equal to
+        // spmv_ref(expand_symmetric(A)); refused (Invalid) when a slice of the
+        // expanded matrix has too many distinct (column delta, value) pairs.
+        if (!m->expanded) m->expanded = expand_symmetric_dev(m, p->stream);
+        p->long_plan = plan_create_internal(m->expanded, KTB_U1, 106, 0, p->stream);
+        p->launches = 1;
+        p->ctas = p->long_plan->ctas;
+        // the records instead of the upper triangle's CRS
+        p->extra_bytes = static_cast<int64_t>(p->long_plan->sell_rec.n) - 12 * m->nnz -
+                         4 * (m->n + 1);
+        return;
+    }
     if (p->param <= 0) {
         const double mean = m->n ? double(m->nnz) / double(m->n) : 1.0;
         int v = 1;
@@ -123,6 +140,11 @@ void s12_setup(ktb_plan* p) {
 
 void s12_run(ktb_plan* p, const double* x, double* y) {
     const ktb_matrix* m = p->m;
+    if (p->long_plan) {  // S1 106: the expanded coded slices
+        p->long_plan->stream = p->stream;
+        plan_run(p->long_plan, x, y, 0, m->n);
+        return;
+    }
     KTB_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->n, p->stream));
     const int grid = static_cast<int>(p->ctas);
     const int32_t* blocks = p->kernel == KTB_S2 ? p->blocks.p : nullptr;

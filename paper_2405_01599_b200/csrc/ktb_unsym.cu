@@ -16,6 +16,8 @@
 //       flag branch left in (correctness reference, never a tuning candidate).
 #include <cub/cub.cuh>
 
+#include <utility>
+
 #include "ktb_internal.cuh"
 #include "ktb_ptx.cuh"
 #include "ktb_segscan.cuh"
@@ -416,139 +418,223 @@ __global__ void __launch_bounds__(kU1tWarps * 32, KTB_U1T_MINB) k_u1t(const doub
 // ---- U1 param 106: persistent slices with coded (column, value) pairs ----
 // Many matrices (every constant-coefficient stencil, graph Laplacians,
 // adjacency matrices) hold only a handful of distinct (column - row, value)
-// pairs per 32 rows. 106 stores one 384-byte record per slice: a dictionary
-// of <= 15 pairs (16 bytes each: the fp64 bit pattern, the int32 column
-// delta, a "real" word; entry 15 = padding) and per row one 32-bit word of
-// eight 4-bit pair codes: 12 B per row whatever W <= 8 is, instead of 8.5 B
-// per slot. The values the kernel multiplies are the stored bit patterns and
-// the sum runs left to right with unfused multiply-add: bitwise spmv_ref. A
-// slice with more distinct pairs refuses the layout (the selector and the
-// halo operator fall back to 105). One bulk copy per slice fills a stage of
-// the warp's ring; a slot costs one 16-byte shared-memory lookup, one wide
-// multiply-add for the address, the gather and the two fp64 operations.
-constexpr int kU1vRec = 384;     // bytes per slice record: dictionary, then the code words
-constexpr int kU1vCodes = 256;   // offset of the code words
-constexpr int kU1vStage = 512;   // stage stride (dictionaries 256-byte aligned)
-#ifndef KTB_U1V_STAGES
-#define KTB_U1V_STAGES 4
-#endif
+// pairs per block of rows. 106 stores one record per 64 rows: a dictionary of
+// the block's pairs (16 bytes each: the fp64 bit pattern, the int32 column
+// delta, a "real" word; the last entry is the padding pair) and per row
+// ceil(W/4) 32-bit words of 8-bit pair codes (word k of rows l and l + 32
+// side by side at 64 k + 2 l). With D dictionary entries (the plan's maximum
+// + padding, <= 64) and slice width W <= 32 a record is 16 D + 256 ceil(W/4)
+// bytes: 640 for the 7-point stencils (10 B per row instead of 8.5 B per
+// slot), 2,240 for a 27-point stencil. The values the kernel multiplies are
+// the stored bit patterns and the sum runs left to right with unfused
+// multiply-add: bitwise spmv_ref. More pairs or wider rows refuse the layout
+// (the selector and the halo operator fall back to 105). One bulk copy per
+// record fills a stage of the warp's ring. A lane owns rows l and l + 32; a
+// batch is two code words (8 slots) of both rows: the 4-byte delta lookups and
+// the 16 gathers go out first, the 8-byte value lookups follow when the
+// products are formed, so an in-flight slot holds its gathered x and nothing
+// else (64 registers, 32 warps per SM). When the two rows' code words are
+// equal in every lane (always, away from a boundary) one lookup serves both
+// rows. The kernel is bound by the L1TEX data pipe (ncu: ~3 wavefronts per
+// 256-byte gather, ~1 per lookup; 73 % busy), not by HBM. Measured and
+// dropped: an L2 prefetch of x at the sweep's front (+40 % time on config 4),
+// one code word per batch (+11 %), 80 registers / 24 warps (+28 %), CTAs of 4
+// warps (+12 %); 2, 4 or 6 stages make no difference on config 4.
+constexpr int kU1vMaxDict = 64;  // dictionary entries per record incl. padding
 #ifndef KTB_U1V_WARPS
 #define KTB_U1V_WARPS 8
 #endif
 #ifndef KTB_U1V_MINB
-#define KTB_U1V_MINB 4  // 64 registers, 32 warps per SM: 895 us on config 4 (72 registers / 24 warps: 1,001 us)
+#define KTB_U1V_MINB 4  // 64 registers, 32 warps per SM
 #endif
-constexpr int kU1vStages = KTB_U1V_STAGES;
 constexpr int kU1vWarps = KTB_U1V_WARPS;
-inline int u1v_smem() { return kU1vWarps * kU1vStages * (kU1vStage + 8) + 256; }
 
-// one warp per slice of the ELL copy: the pair dictionary by ballot matching
-// (first-occurrence order, slot-major), then the code words
+struct U1vLayout {
+    int dict = 0;    // dictionary entries incl. the padding pair
+    int words = 0;   // code words per row
+    int rec = 0;     // record bytes (global stride)
+    int stride = 0;  // stage stride in shared memory (dictionary aligned for the OR lookup)
+    int stages = 0;
+};
+static U1vLayout u1v_layout(int max_pairs, int W) {
+    U1vLayout L;
+    L.dict = max_pairs + 1;
+    L.words = (W + 3) / 4;
+    L.rec = 16 * L.dict + 256 * L.words;
+    int a = 256;
+    while (a < 16 * L.dict) a <<= 1;
+    L.stride = (L.rec + a - 1) / a * a;
+#ifdef KTB_U1V_STAGES
+    L.stages = KTB_U1V_STAGES;
+#else
+    L.stages = L.stride <= 1024 ? 4 : L.stride <= 1536 ? 3 : 2;
+#endif
+    return L;
+}
+static int u1v_smem(const U1vLayout& L) { return kU1vWarps * L.stages * (L.stride + 8) + 1024; }
+
+// One warp per 64-row record of the ELL copy (32-row slices 2 s and 2 s + 1).
+// Pass 1 (rec == nullptr): the record's pair count into the plan-wide
+// maximum. Pass 2: the record -- the pair dictionary by ballot matching
+// (first-occurrence order; lane j holds pairs j and 32 + j), then the code
+// bytes; the padding code is dict - 1.
 __global__ void k_vrec_build(const int32_t* __restrict__ scol, const double* __restrict__ sval,
-                             int64_t slices, int W, unsigned char* __restrict__ rec,
-                             int* __restrict__ overflow) {
+                             int64_t slices32, int64_t recs, int W, int dict, int rec_bytes,
+                             unsigned char* __restrict__ rec, int* __restrict__ max_pairs) {
     const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (s >= slices) return;  // whole warps
-    const int64_t o = s * 32 * W;
-    const int32_t row = static_cast<int32_t>(s * 32 + lane);
-    int32_t dc = 0;              // lane j < np: pair j
-    unsigned long long dv = 0;
+    if (s >= recs) return;  // whole warps
+    int32_t dc[2] = {0, 0};
+    unsigned long long dv[2] = {0, 0};
     int np = 0;
-    bool ok = true;
-    uint32_t word = 0xffffffffu;  // this lane's row: nibble 15 = padding
-    for (int k = 0; k < W; ++k) {
-        const int64_t at = o + static_cast<int64_t>(k) * 32 + lane;
-        const int32_t c = scol[at];
-        const unsigned long long vb =
-            static_cast<unsigned long long>(__double_as_longlong(sval[at]));
-        const int32_t d = c - row;
-        int code = 15;
-        unsigned pending = __ballot_sync(0xffffffffu, c >= 0);
-        while (pending) {
-            const int src = __ffs(pending) - 1;
-            const int32_t wd = __shfl_sync(0xffffffffu, d, src);
-            const unsigned long long wv = __shfl_sync(0xffffffffu, vb, src);
-            const unsigned same = __ballot_sync(0xffffffffu, c >= 0 && d == wd && vb == wv);
-            const unsigned hit = __ballot_sync(0xffffffffu, lane < np && dc == wd && dv == wv);
-            int j;
-            if (hit) {
-                j = __ffs(hit) - 1;
-            } else if (np < 15) {
-                j = np++;
-                if (lane == j) {
-                    dc = wd;
-                    dv = wv;
+    const int pad = dict - 1;
+    uint32_t word[2] = {0, 0};
+    unsigned char* r = rec ? rec + s * rec_bytes : nullptr;
+    for (int k = 0; k < 4 * ((W + 3) / 4); ++k) {
+        for (int h = 0; h < 2; ++h) {
+            int code = pad;
+            const int64_t s32 = 2 * s + h;
+            if (k < W && s32 < slices32) {
+                const int64_t at = (s32 * W + k) * 32 + lane;
+                const int32_t c = scol[at];
+                const unsigned long long vb =
+                    static_cast<unsigned long long>(__double_as_longlong(sval[at]));
+                const int32_t d = c - static_cast<int32_t>(s32 * 32 + lane);
+                unsigned pending = __ballot_sync(0xffffffffu, c >= 0);
+                while (pending) {
+                    const int src = __ffs(pending) - 1;
+                    const int32_t wd = __shfl_sync(0xffffffffu, d, src);
+                    const unsigned long long wv = __shfl_sync(0xffffffffu, vb, src);
+                    const unsigned same =
+                        __ballot_sync(0xffffffffu, c >= 0 && d == wd && vb == wv);
+                    const unsigned hit0 =
+                        __ballot_sync(0xffffffffu, lane < np && dc[0] == wd && dv[0] == wv);
+                    const unsigned hit1 =
+                        __ballot_sync(0xffffffffu, lane + 32 < np && dc[1] == wd && dv[1] == wv);
+                    int j;
+                    if (hit0) {
+                        j = __ffs(hit0) - 1;
+                    } else if (hit1) {
+                        j = 32 + __ffs(hit1) - 1;
+                    } else {
+                        j = np < 64 ? np : 63;  // past 63 pairs only the count matters (refused)
+                        if (np < 64 && lane == (j & 31)) {
+                            dc[j >> 5] = wd;
+                            dv[j >> 5] = wv;
+                        }
+                        ++np;
+                    }
+                    if ((same >> lane) & 1u) code = j;
+                    pending &= ~same;
                 }
-            } else {
-                j = 14;
-                ok = false;
             }
-            if ((same >> lane) & 1u) code = j;
-            pending &= ~same;
+            word[h] |= static_cast<uint32_t>(code & 255) << (8 * (k & 3));
         }
-        word = (word & ~(15u << (4 * k))) | (static_cast<uint32_t>(code) << (4 * k));
+        if ((k & 3) == 3) {
+            if (r)
+                reinterpret_cast<uint2*>(r + 16 * dict)[(k >> 2) * 32 + lane] =
+                    make_uint2(word[0], word[1]);
+            word[0] = word[1] = 0;
+        }
     }
-    unsigned char* r = rec + s * kU1vRec;
-    if (lane < 16) {
-        const bool real = lane < np;
-        uint4 e;
-        e.x = real ? static_cast<uint32_t>(dv) : 0u;
-        e.y = real ? static_cast<uint32_t>(dv >> 32) : 0u;
-        e.z = real ? static_cast<uint32_t>(dc) : 0u;
-        e.w = real ? 1u : 0u;
-        reinterpret_cast<uint4*>(r)[lane] = e;
+    if (!r) {
+        if (lane == 0) atomicMax(max_pairs, np);
+        return;
     }
-    reinterpret_cast<uint32_t*>(r + kU1vCodes)[lane] = word;
-    if (!ok && lane == 0) atomicOr(overflow, 1);
+    for (int h = 0; h < 2; ++h) {
+        const int j = 32 * h + lane;
+        if (j < dict) {
+            const bool real = j < np;
+            uint4 e;
+            e.x = real ? static_cast<uint32_t>(dv[h]) : 0u;
+            e.y = real ? static_cast<uint32_t>(dv[h] >> 32) : 0u;
+            e.z = real ? static_cast<uint32_t>(dc[h]) : 0u;
+            e.w = real ? 1u : 0u;
+            reinterpret_cast<uint4*>(r)[j] = e;
+        }
+    }
 }
 
-// kW = the plan's slice width: slots kW..7 are padding in every row and cost
-// nothing (the L1TEX data pipe is this kernel's bound: 4 cycles per 16-byte
-// lookup, 2-3 per gather)
+// dictionary entry at byte offset `off` of the stage: the fp64 bit pattern at
+// +0, the int32 column delta at +8. The delta is read when the gather is
+// issued and the value when its product is formed, so that an in-flight slot
+// holds two registers (the gathered x) and nothing else.
+__device__ __forceinline__ int32_t u1v_delta(uint32_t sb, uint32_t off) {
+    int32_t d;
+    asm volatile("ld.shared.s32 %0, [%1+8];" : "=r"(d) : "r"(sb | off));
+    return d;
+}
+__device__ __forceinline__ double u1v_value(uint32_t sb, uint32_t off) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(sb | off));
+    return v;
+}
+// byte offset (code << 4) of slot b of a code word
+__device__ __forceinline__ uint32_t u1v_off(uint32_t ww, int b) {
+    return (b == 0 ? (ww << 4) : (ww >> (8 * b - 4))) & 0xff0u;
+}
+__device__ __forceinline__ double u1v_gather(const double* xr, int32_t delta) {
+    const double* px;
+    asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(px) : "r"(delta), "l"(xr));
+    return ld_x(px);
+}
+
+#ifndef KTB_U1V_BATCH
+#define KTB_U1V_BATCH 2  // code words (4 slots each) per batch of gathers
+#endif
+
+// kW = the plan's slice width (slots kW.. of the last code word are padding in
+// every row and cost nothing). Per-warp state is kept small (the kernel runs
+// at 64 registers, 32 warps per SM): the current stage and barrier address,
+// the global address of the next record to fetch, the record's first row.
 template <int kW>
 __global__ void __launch_bounds__(kU1vWarps * 32, KTB_U1V_MINB)
     k_u1v(const unsigned char* __restrict__ rec, const double* __restrict__ x,
-          double* __restrict__ y, int32_t row_begin, int32_t row_end, int32_t nrows) {
+          double* __restrict__ y, int32_t row_begin, int32_t row_end, int32_t nrows,
+          int32_t xlen, int dict_bytes, int rec_bytes, int stride, int stages) {
+    constexpr int kWords = (kW + 3) / 4;
+    constexpr int kB = KTB_U1V_BATCH;
     extern __shared__ unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // stages 256-byte aligned in the shared window: a dictionary entry's
-    // address is then (stage | code << 4), one logic operation
-    const uint32_t base = (smem_u32(smem_raw) + 255u) & ~255u;
-    const uint32_t ring = base + warp * (kU1vStages * kU1vStage);
-    const uint32_t bars = base + kU1vWarps * kU1vStages * kU1vStage + warp * kU1vStages * 8;
+    // stages aligned to the dictionary's power-of-two size in the shared
+    // window: an entry's address is then (stage | code << 4), one logic op
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t ring = base + warp * (stages * stride);
+    const uint32_t bars = base + kU1vWarps * stages * stride + warp * stages * 8;
     const int G = static_cast<int>(gridDim.x) * kU1vWarps;
-    const int first = (row_begin >> 5) + blockIdx.x * kU1vWarps + warp;
-    const int last = static_cast<int>((static_cast<int64_t>(row_end) + 31) >> 5);
-    const int nj = first < last ? (last - first + G - 1) / G : 0;  // this warp's slices
+    const int first = (row_begin >> 6) + blockIdx.x * kU1vWarps + warp;
+    const int last = static_cast<int>((static_cast<int64_t>(row_end) + 63) >> 6);
+    int left = first < last ? (last - first + G - 1) / G : 0;  // this warp's records
     const uint64_t pol = policy_evict_first();
-    auto issue = [&](int j, int st) {  // lane 0: one bulk copy per slice
-        const uint32_t bar = bars + st * 8;
+    const int64_t gstep = static_cast<int64_t>(G) * rec_bytes;
+    const unsigned char* src = rec + static_cast<int64_t>(first) * rec_bytes;  // next record
+    const uint32_t pad = static_cast<uint32_t>(dict_bytes - 16);  // the padding pair's offset
+    auto issue = [&](uint32_t dst, uint32_t bar) {  // lane 0: one bulk copy per record
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(kU1vRec)
+                     "r"(rec_bytes)
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-            " [%0], [%1], %2, [%3], %4;" ::"r"(ring + st * kU1vStage),
-            "l"(rec + (static_cast<int64_t>(first) + static_cast<int64_t>(j) * G) * kU1vRec),
-            "r"(kU1vRec), "r"(bar), "l"(pol)
+            " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+            "l"(src), "r"(rec_bytes), "r"(bar), "l"(pol)
             : "memory");
+        src += gstep;
     };
+    const uint32_t rstep = static_cast<uint32_t>(G) * 64u;
     if (lane == 0) {
-        for (int st = 0; st < kU1vStages; ++st)
+        for (int st = 0; st < stages; ++st)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bars + st * 8), "r"(1)
                          : "memory");
         fence_mbar_init();
-        for (int st = 0; st < kU1vStages; ++st)
-            if (st < nj) issue(st, st);
+        for (int st = 0; st < stages && st < left; ++st) issue(ring + st * stride, bars + st * 8);
     }
     __syncwarp();
-    for (int j = 0; j < nj; ++j) {
-        const int st = j % kU1vStages;
-        const uint32_t sb = ring + st * kU1vStage;
+    int st = 0;
+    uint32_t ph = 0, sb = ring, bar = bars;
+    uint32_t row = static_cast<uint32_t>(first) * 64u + lane;  // rows row and row + 32
+    for (; left > 0; --left, row += rstep) {
         {
             KTB_CHAOS_DELAY(0x7531);
-            const uint32_t ph = (j / kU1vStages) & 1, bar = bars + st * 8;
             asm volatile(
                 "{\n"
                 ".reg .pred p;\n"
@@ -559,53 +645,106 @@ __global__ void __launch_bounds__(kU1vWarps * 32, KTB_U1V_MINB)
                 "r"(ph)
                 : "memory");
         }
-        uint32_t w;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(sb + kU1vCodes + lane * 4));
-        const int64_t row = (static_cast<int64_t>(first) + static_cast<int64_t>(j) * G) * 32 + lane;
-        // rows past the end of the matrix (last slice) hold padding only: their
+        // rows past the end of the matrix (last record) hold padding only: their
         // unconditional gathers read x at the last row instead
-        const double* xr = x + min(row, static_cast<int64_t>(nrows) - 1);
-        double v[kW], xv[kW];
-        uint32_t real[kW];
+        const double* xa = x + min(row, static_cast<uint32_t>(nrows - 1));
+        const double* xb = x + min(row + 32u, static_cast<uint32_t>(nrows - 1));
+        const uint32_t cb = sb + dict_bytes + lane * 8;
+        double sa = 0.0, sb2 = 0.0;
+        // kB code words (4 slots each) of both rows at a time: all their
+        // gathers in flight, then the products in slot order
 #pragma unroll
-        for (int u = 0; u < kW; ++u) {
-            const uint32_t off = (u == 0 ? (w << 4) : (w >> (4 * u - 4))) & 0xf0u;
-            uint32_t e0, e1, e2, e3;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
-                         : "r"(sb | off));
-            v[u] = __hiloint2double(static_cast<int>(e1), static_cast<int>(e0));
-            real[u] = e3;
-            const double* px;
-            asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(px) : "r"(static_cast<int32_t>(e2)), "l"(xr));
-            xv[u] = ld_x(px);
+        for (int g = 0; g < kWords; g += kB) {
+            uint32_t wa[kB], wb[kB];
+            bool same = true;
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (g + j < kWords) {
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                                 : "=r"(wa[j]), "=r"(wb[j])
+                                 : "r"(cb + (g + j) * 256));
+                    same = same && wa[j] == wb[j];
+                }
+            double xva[4 * kB], xvb[4 * kB];
+            if (__all_sync(0xffffffffu, same)) {  // one lookup serves both rows
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * (g + j) + u < kW) {
+                            const int32_t d = u1v_delta(sb, u1v_off(wa[j], u));
+                            xva[4 * j + u] = u1v_gather(xa, d);
+                            xvb[4 * j + u] = u1v_gather(xb, d);
+                        }
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * (g + j) + u < kW) {
+                            const uint32_t off = u1v_off(wa[j], u);
+                            const double v = u1v_value(sb, off);
+                            const double ta = __dadd_rn(sa, __dmul_rn(v, xva[4 * j + u]));
+                            const double tb = __dadd_rn(sb2, __dmul_rn(v, xvb[4 * j + u]));
+                            sa = off != pad ? ta : sa;
+                            sb2 = off != pad ? tb : sb2;
+                        }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * (g + j) + u < kW) {
+                            xva[4 * j + u] = u1v_gather(xa, u1v_delta(sb, u1v_off(wa[j], u)));
+                            xvb[4 * j + u] = u1v_gather(xb, u1v_delta(sb, u1v_off(wb[j], u)));
+                        }
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * (g + j) + u < kW) {
+                            const uint32_t oa = u1v_off(wa[j], u), ob = u1v_off(wb[j], u);
+                            const double ta =
+                                __dadd_rn(sa, __dmul_rn(u1v_value(sb, oa), xva[4 * j + u]));
+                            const double tb =
+                                __dadd_rn(sb2, __dmul_rn(u1v_value(sb, ob), xvb[4 * j + u]));
+                            sa = oa != pad ? ta : sa;
+                            sb2 = ob != pad ? tb : sb2;
+                        }
+            }
         }
-        __syncwarp();  // every lane has its slots: the stage may be refilled
-        if (lane == 0 && j + kU1vStages < nj) {
+        __syncwarp();  // every lane has read its last entries: the stage may be refilled
+        if (lane == 0 && left > stages) {
             fence_proxy_async_smem();
-            issue(j + kU1vStages, st);
+            issue(sb, bar);
         }
-        double sum = 0.0;
-#pragma unroll
-        for (int u = 0; u < kW; ++u)
-            if (real[u]) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
-        if (row >= row_begin && row < row_end) y[row] = sum;
+        if (row >= static_cast<uint32_t>(row_begin) && row < static_cast<uint32_t>(row_end))
+            y[row] = sa;
+        if (row + 32u >= static_cast<uint32_t>(row_begin) &&
+            row + 32u < static_cast<uint32_t>(row_end))
+            y[row + 32u] = sb2;
+        sb += stride;
+        bar += 8;
+        if (++st == stages) {
+            st = 0;
+            ph ^= 1u;
+            sb = ring;
+            bar = bars;
+        }
     }
 }
 
-using U1vFn = void (*)(const unsigned char*, const double*, double*, int32_t, int32_t, int32_t);
+using U1vFn = void (*)(const unsigned char*, const double*, double*, int32_t, int32_t, int32_t,
+                       int32_t, int, int, int, int);
+template <int... kWs>
+static U1vFn u1v_pick(int W, std::integer_sequence<int, kWs...>) {
+    U1vFn fn = nullptr;
+    ((W == kWs + 1 ? (fn = k_u1v<kWs + 1>, 0) : 0), ...);
+    return fn;
+}
 static U1vFn u1v_kernel(int W) {
-    switch (W) {
-        case 1: return k_u1v<1>;
-        case 2: return k_u1v<2>;
-        case 3: return k_u1v<3>;
-        case 4: return k_u1v<4>;
-        case 5: return k_u1v<5>;
-        case 6: return k_u1v<6>;
-        case 7: return k_u1v<7>;
-        case 8: return k_u1v<8>;
-        default: throw Invalid("u1: staged slices need one slice width <= 8");
-    }
+    U1vFn fn = u1v_pick(W, std::make_integer_sequence<int, 32>{});
+    if (!fn) throw Invalid("u1: coded slices need one slice width <= 32");
+    return fn;
 }
 
 // ---- U1 param 101 setup helpers: rows sorted by length ----------------------
@@ -722,7 +861,7 @@ __global__ void k_sell_fill(const int32_t* __restrict__ rp, const int32_t* __res
     }
 }
 
-static void u1_sell_setup(ktb_plan* p) {
+static void u1_sell_setup(ktb_plan* p, bool force_uniform = false) {
     const ktb_matrix* m = p->m;
     const int64_t slices = ceil_div64(m->n, 32);
     p->sell_off.alloc(slices + 1);
@@ -745,7 +884,11 @@ static void u1_sell_setup(ktb_plan* p) {
     KTB_CUDA(cudaMemcpyAsync(st, stats.p, sizeof(st), cudaMemcpyDeviceToHost, p->stream));
     KTB_CUDA(cudaStreamSynchronize(p->stream));
     p->ell_width = 0;
-    if (st[0] > 0 && st[0] * slices <= st[1] + st[1] / 16) {
+    if (force_uniform && st[0] > 32 * 32)
+        throw Invalid("u1: coded slices need one slice width <= 32");
+    // (the pair-coded records take one width whatever it costs: a padding
+    // slot is one byte there)
+    if (st[0] > 0 && (force_uniform || st[0] * slices <= st[1] + st[1] / 16)) {
         p->ell_width = static_cast<int>(st[0] / 32);
         k_fill_i64<<<ceil_div(slices, 256), 256, 0, p->stream>>>(p->sell_off.p, slices, st[0]);
         KTB_LAUNCH();
@@ -845,23 +988,35 @@ static void u1_dict_setup(ktb_plan* p) {
 // U1 param 106: the slice records (pair dictionary + code words) from the
 // ELL copy; they replace both the columns and the values.
 static void u1_vrec_setup(ktb_plan* p) {
-    const int64_t slices = ceil_div64(p->m->n, 32);
-    p->sell_rec.alloc(std::max<int64_t>(slices, 1) * kU1vRec);
-    DBuf<int> overflow(1);
-    KTB_CUDA(cudaMemsetAsync(overflow.p, 0, sizeof(int), p->stream));
-    k_vrec_build<<<ceil_div(slices * 32, 256), 256, 0, p->stream>>>(
-        p->sell_col.p, p->sell_val.p, slices, p->ell_width, p->sell_rec.p, overflow.p);
+    const int64_t slices32 = ceil_div64(p->m->n, 32), recs = ceil_div64(p->m->n, 64);
+    const int W = p->ell_width;
+    DBuf<int> maxp(1);
+    KTB_CUDA(cudaMemsetAsync(maxp.p, 0, sizeof(int), p->stream));
+    const int grid = ceil_div(recs * 32, 256);
+    k_vrec_build<<<grid, 256, 0, p->stream>>>(p->sell_col.p, p->sell_val.p, slices32, recs, W, 0,
+                                              0, nullptr, maxp.p);
     KTB_LAUNCH();
-    int ov = 0;
-    KTB_CUDA(cudaMemcpyAsync(&ov, overflow.p, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    int mp = 0;
+    KTB_CUDA(cudaMemcpyAsync(&mp, maxp.p, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
     KTB_CUDA(cudaStreamSynchronize(p->stream));
-    if (ov)
-        throw Invalid("u1: a warp slice needs more than 15 distinct (column delta, value) pairs");
+    if (mp + 1 > kU1vMaxDict)
+        throw Invalid("u1: 64 rows need more than 63 distinct (column delta, value) pairs");
+    const U1vLayout L = u1v_layout(mp, W);
+    p->rec_dict = L.dict;
+    p->rec_words = L.words;
+    p->rec_bytes = L.rec;
+    p->rec_stride = L.stride;
+    p->rec_stages = L.stages;
+    p->sell_rec.alloc(std::max<int64_t>(recs, 1) * L.rec);
+    k_vrec_build<<<grid, 256, 0, p->stream>>>(p->sell_col.p, p->sell_val.p, slices32, recs, W,
+                                              L.dict, L.rec, p->sell_rec.p, maxp.p);
+    KTB_LAUNCH();
+    KTB_CUDA(cudaStreamSynchronize(p->stream));
     const int64_t padded = static_cast<int64_t>(p->sell_col.n);
     p->sell_col.release();
     p->sell_val.release();
-    // 384 B per slice instead of the warp-sliced copy's 12 B per slot
-    p->extra_bytes += slices * kU1vRec - 12 * padded;
+    // one record per 64 rows instead of the warp-sliced copy's 12 B per slot
+    p->extra_bytes += recs * L.rec - 12 * padded;
 }
 
 // U1 param 101: rows of length <= kSortedCap sorted by length (descending,
@@ -991,13 +1146,14 @@ void u1_setup(ktb_plan* p) {
         p->launches = 1;
         return;
     }
-    if (p->param == 106) {  // persistent slices, coded columns and coded values
+    if (p->param == 106) {  // persistent slices, coded (column delta, value) pairs
         require(p->cta_threads == 0, "u1: the staged slices run 256-thread CTAs");
-        u1_sell_setup(p);
-        if (p->ell_width < 1 || p->ell_width > 8)
-            throw Invalid("u1: staged slices need one slice width <= 8");
+        u1_sell_setup(p, true);
+        if (p->ell_width < 1 || p->ell_width > 32)
+            throw Invalid("u1: coded slices need one slice width <= 32");
         u1_vrec_setup(p);
-        const int smem = u1v_smem();
+        const U1vLayout L = u1v_layout(p->rec_dict - 1, p->ell_width);
+        const int smem = u1v_smem(L);
         const U1vFn fn = u1v_kernel(p->ell_width);
         KTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int occ = 0;
@@ -1101,12 +1257,14 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
         return;
     }
     if (p->param == 106) {
-        const int64_t slices = ceil_div64(r1, 32) - (r0 >> 5);
+        const int64_t recs = ceil_div64(r1, 64) - (r0 >> 6);
         const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(p->ctas, ceil_div64(slices, kU1vWarps))));
-        u1v_kernel(p->ell_width)<<<grid, kU1vWarps * 32, u1v_smem(), p->stream>>>(
+            1, std::min<int64_t>(p->ctas, ceil_div64(recs, kU1vWarps))));
+        const U1vLayout L = u1v_layout(p->rec_dict - 1, p->ell_width);
+        u1v_kernel(p->ell_width)<<<grid, kU1vWarps * 32, u1v_smem(L), p->stream>>>(
             p->sell_rec.p, x, y, static_cast<int32_t>(r0), static_cast<int32_t>(r1),
-            static_cast<int32_t>(p->m->n));
+            static_cast<int32_t>(p->m->n), static_cast<int32_t>(p->m->ncols), 16 * L.dict, L.rec,
+            L.stride, L.stages);
         KTB_LAUNCH();
         return;
     }

@@ -293,9 +293,23 @@ def test_selector_unsym_and_sym(K):
     n, rp, ci, v = matgen.stencil27_upper(16, 16, 16)
     s = K.SymCsrMatrix(n, rp, ci, v)
     choice, rep = K.select_spmv_sym(s)
-    assert [c.name for c in rep.candidates] == ["s1", "s2", "s3", "s3"]
-    assert [c.cta_threads for c in rep.candidates[2:]] == [256, 512]
+    assert [c.name for c in rep.candidates] == ["s1", "s1", "s2", "s3", "s3"]
+    assert [c.jl for c in rep.candidates[:2]] == [rep.candidates[0].jl, 106]
+    assert [c.cta_threads for c in rep.candidates[3:]] == [256, 512]
     assert all(c.correct for c in rep.candidates)
+    # S1 106 (transposed products gathered from the expanded pair-coded slices):
+    # bitwise equal to spmv_ref(expand_symmetric(A))
+    x = O.seeded_vector(n, 2)
+    y = np.full(n, np.nan)
+    K.DevicePlan(s, K.SymKernel.s1_row, 106).apply(x, y)
+    erp, eci, ev = O.expand_symmetric(n, rp, ci, v)
+    assert np.array_equal(y, O.spmv_ref(n, erp, eci, ev, x))
+    # random symmetric values: too many pairs per slice -> refused, the selector skips it
+    rs = K.SymCsrMatrix(n, rp, ci, np.random.default_rng(5).uniform(-1, 1, len(ci)))
+    with pytest.raises(K.Error):
+        K.DevicePlan(rs, K.SymKernel.s1_row, 106)
+    _, rep = K.select_spmv_sym(rs)
+    assert not rep.candidates[1].correct and rep.selected_candidate().correct
 
 
 def test_selector_injected_timer_and_tie_break(K):
@@ -611,15 +625,14 @@ def test_u1_column_coded_slices(K):
 
 
 def test_u1_value_coded_slices(K):
-    """U1 param 106: one 384-byte record per warp slice -- a dictionary of
-    <= 15 (column delta, fp64 bit pattern) pairs and eight 4-bit pair codes
-    per row. The multiplied values are the stored bit patterns and the sum
+    """U1 param 106: one record per warp slice -- a dictionary of <= 63
+    (column delta, fp64 bit pattern) pairs and one 8-bit pair code per slot. The multiplied values are the stored bit patterns and the sum
     keeps spmv_ref's order: bitwise equal on banded matrices with exactly 15
     distinct pairs per slice (incl. -0.0 next to 0.0, denormals, huge
     values), with per-slice value sets that differ from slice to slice, empty
-    rows, row sub-ranges, n not a multiple of 32; 16 distinct pairs in one
-    slice, a row longer than 8 and random values are refused (the callers
-    fall back to 105)."""
+    rows, row sub-ranges, n not a multiple of 32, 27-slot rows, 63 pairs; 64
+    distinct pairs in one slice, random values and rows longer than 32 are
+    refused (the callers fall back to 105)."""
     import torch
 
     rng = np.random.default_rng(106)
@@ -673,16 +686,29 @@ def test_u1_value_coded_slices(K):
         yref = O.spmv_ref(n, rp, ci, v, x)
     # (NaN sign/payload differs between x86 and the GPU: compare as numbers)
     assert np.array_equal(y, yref, equal_nan=True) and np.isnan(yref).sum() < 40
-    # 16 distinct pairs in one slice
-    n, rp, ci, v = banded(4000, lambda s, k: special[2 * k:2 * k + 2] if k != 3 else special[[6, 7, 14, 13]])
-    with pytest.raises(K.Error, match="15 distinct .column delta, value. pairs"):
+    # wide rows and bigger dictionaries: the expanded 27-point stencil (27 slots, 27 pairs),
+    # 16 pairs, and 9 deltas x 7 values = 63 pairs
+    e27 = O.expand_symmetric(*matgen.stencil27_upper(20, 17, 13))
+    n27 = 20 * 17 * 13
+    deltas = [-300, -33, -7, -1, 0, 1, 40, 512, 1000]
+    wide = [(n27, *e27),
+            banded(4000, lambda s, k: (special[2 * k:2 * k + 2] if k < 7 else special[k:k + 1])
+                   if k != 3 else special[[6, 7, 14, 13]]),
+            banded(3000, lambda s, k: special[k:k + 7])]
+    for n, rp, ci, v in wide:
+        x = O.seeded_vector(n, 4)
+        y = np.full(n, np.nan)
+        K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106).apply(x, y)
+        assert np.array_equal(y.view(np.int64), O.spmv_ref(n, rp, ci, v, x).view(np.int64))
+    # 64 distinct pairs in one slice, random values (config 3's kind), rows longer than 32
+    n, rp, ci, v = banded(3000, lambda s, k: special[k:k + 7] if k else special[:8])
+    with pytest.raises(K.Error, match="63 distinct .column delta, value. pairs"):
         K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106)
-    # random values (config 3's kind) and rows longer than 8
     n, rp, ci, v = banded(3000, lambda s, k: rng.uniform(-1, 1, 64))
     with pytest.raises(K.Error):
         K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106)
-    n, rp, ci, v = matgen.stencil27_upper(12, 12, 12)
-    with pytest.raises(K.Error, match="width <= 8"):
+    n, rp, ci, v = matgen.random_csr(2000, 0.03, rng)
+    with pytest.raises(K.Error):
         K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, 106)
 
 
