@@ -309,6 +309,141 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
     }
 }
 
+// ---- MGS with w in registers and the basis columns fed by bulk copies --------
+// The same slices, element-to-thread mapping, update arithmetic, reduction
+// trees and exchange as k_mgs_res (bit-identical projections), but w's slice
+// stays in registers (E per thread) and the basis columns arrive in two
+// shared-memory buffers by one bulk copy each (cp.async.bulk + mbarrier):
+// column q+1 is requested as soon as the pass over column q-1's buffer is
+// done, i.e. before this CTA publishes projection q, so its HBM time overlaps
+// the cross-CTA exchange instead of following it, and a pass is two
+// shared-memory reads per element (update from column q, product with column
+// q+1) with no shared-memory stores. Needs even n (16-byte aligned column
+// slices) and 2 * E * kRThreads * 8 bytes of shared memory (E <= 14).
+template <int E>
+__global__ void __launch_bounds__(kRThreads, 1) k_mgs_dma(const double* __restrict__ V, int64_t n,
+                                                          int k, const double* __restrict__ w,
+                                                          double* __restrict__ vnext,
+                                                          double* __restrict__ h,
+                                                          double2* __restrict__ slots,
+                                                          int* __restrict__ breakdown,
+                                                          long long tag0) {
+    extern __shared__ __align__(128) double smem_d[];
+    constexpr int kSlice = E * kRThreads;
+    double* buf0 = smem_d;
+    double* buf1 = smem_d + kSlice;
+    __shared__ double red[2 * kRThreads / 32];
+    __shared__ double bc[2];
+    __shared__ __align__(8) uint64_t full[2];
+    const int nb = gridDim.x, tid = threadIdx.x;
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kSlice;
+    const int len = static_cast<int>(max(int64_t(0), min(n - s0, static_cast<int64_t>(kSlice))));
+    const int64_t base = s0 + tid;
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int col) {  // thread 0: column col's slice into buffer col & 1
+        if (len > 0) {
+            mbar_arrive_expect_tx(&full[col & 1], static_cast<uint32_t>(len) * 8u);
+            tma_load_1d((col & 1) ? buf1 : buf0, V + static_cast<int64_t>(col) * n + s0,
+                        static_cast<uint32_t>(len) * 8u, &full[col & 1], pol);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    // the slice's tail past n (last CTA) reads as zero in both buffers
+    for (int o = len + tid; o < kSlice; o += kRThreads) buf0[o] = buf1[o] = 0.0;
+    KTB_SYNC();
+    if (tid == 0) {
+        fence_proxy_async_smem();
+        issue(0);
+        if (k > 1) issue(1);
+    }
+    double wr[E];
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
+        wr[e] = i < n ? w[i] : 0.0;
+    }
+    if (len > 0) mbar_wait(&full[0], 0);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        a += wr[e] * wr[e];
+        b += buf0[e * kRThreads + tid] * wr[e];
+    }
+    block_sum_w0(a, b, red);
+    if (tid == 0) {
+        publish(slots + blockIdx.x, a, tag0);
+        publish(slots + nb + blockIdx.x, b, tag0 + 1);
+    }
+    if (tid < 32) {
+        const double t0 = poll_total(slots, nb, tag0);
+        const double t1 = poll_total(slots + nb, nb, tag0 + 1);
+        if (tid == 0) {
+            bc[0] = t0;
+            bc[1] = t1;
+        }
+    }
+    KTB_SYNC();
+    const double in2 = bc[0];
+    double c = bc[1];
+    for (int q = 0; q < k; ++q) {
+        if (blockIdx.x == 0 && tid == 0) h[q] = c;
+        const bool last = q + 1 == k;
+        const double mc = -c;
+        const double* cur = (q & 1) ? buf1 : buf0;
+        const double* nxt = (q & 1) ? buf0 : buf1;
+        // column q+1 is the ((q+1) >> 1)-th fill of its buffer
+        if (!last && len > 0) mbar_wait(&full[(q + 1) & 1], ((q + 1) >> 1) & 1);
+        double p = 0.0, dummy = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int o = e * kRThreads + tid;
+            const double wi = __dadd_rn(wr[e], __dmul_rn(mc, cur[o]));  // axpy(-c, q, v)
+            wr[e] = wi;
+            p += last ? wi * wi : nxt[o] * wi;
+        }
+        // block_sum_w0, split: after its barrier every thread has read column
+        // q's buffer, which thread 0 then refills with column q+2
+        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        if ((tid & 31) == 0) {
+            red[2 * (tid >> 5)] = p;
+            red[2 * (tid >> 5) + 1] = dummy;
+        }
+        KTB_SYNC();
+        if (tid == 0 && q + 2 < k) {
+            fence_proxy_async_smem();
+            issue(q + 2);
+        }
+        double2* sl = slots + static_cast<int64_t>(q + 2) * nb;
+        if (tid < 32) {
+            p = tid < kRThreads / 32 ? red[2 * tid] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+            if (tid == 0) publish(sl + blockIdx.x, p, tag0 + q + 2);
+            const double t = poll_total(sl, nb, tag0 + q + 2);
+            if (tid == 0) bc[0] = t;
+        }
+        KTB_SYNC();
+        c = bc[0];
+    }
+    const double nrm = sqrt(c);
+    const bool brk = nrm <= 1e-14 * sqrt(in2);
+    if (blockIdx.x == 0 && tid == 0) {
+        h[k] = nrm;
+        *breakdown = brk ? 1 : 0;
+    }
+    if (!brk) {
+        const double inv = 1.0 / nrm;  // scal(1.0 / r.norm, v)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int64_t i = base + static_cast<int64_t>(e) * kRThreads;
+            if (i < n) vnext[i] = __dmul_rn(wr[e], inv);
+        }
+    }
+}
+
 __global__ void k_sub_from(const double* __restrict__ b, double* __restrict__ r, int64_t n) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < n) r[i] = __dsub_rn(b[i], r[i]);
@@ -432,7 +567,19 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
             case 32: res_fn = reinterpret_cast<const void*>(&k_mgs_res<32>); break;
             default: break;
         }
-        const size_t res_smem = static_cast<size_t>(E) * kRThreads * 16;  // w and V slices
+        const size_t res_smem = static_cast<size_t>(E) * kRThreads * 16;  // two slices
+        // even n and E <= 14: w in registers, columns double-buffered by bulk copies
+        if ((n & 1) == 0 && !std::getenv("KTB_GMRES_NO_DMA_MGS")) {
+            switch (E) {
+                case 1: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<1>); break;
+                case 2: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<2>); break;
+                case 4: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<4>); break;
+                case 8: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<8>); break;
+                case 12: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<12>); break;
+                case 14: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<14>); break;
+                default: break;
+            }
+        }
         int res_nb = 0;
         if (res_fn && !std::getenv("KTB_GMRES_STREAM_MGS")) {
             KTB_CUDA(cudaFuncSetAttribute(res_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
