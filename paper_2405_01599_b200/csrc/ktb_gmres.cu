@@ -309,6 +309,44 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_res(const double* __restri
     }
 }
 
+// Exchange of k_mgs_dma (tools/exchange_bench.cu, 148 CTAs: 1.6 us per
+// exchange instead of 2.7 us for the layout above): one slot per 128-byte line
+// (stores of different SMs into one line serialise in L2), the <= 8 slot loads
+// of a lane's poll round in flight together, and three rows of slots reused
+// by every reduction of every launch -- row 2 for the input norm, rows 0 / 1
+// alternating for the projections (a CTA rewrites a row for reduction r + 2
+// only after its poll of r + 1 completed, i.e. after every CTA finished
+// reading r). Same summation order as poll_total.
+constexpr int kLineSlots = 8;  // double2 per 128-byte line
+constexpr int kPollParts = 5;  // nb <= 160 (one CTA per SM)
+__device__ __forceinline__ double2 ld_relaxed_pair(const double2* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+// warp 0 only; returns the total in every lane of warp 0
+__device__ __forceinline__ double poll_total_lines(const double2* row, int nb, long long tag) {
+    const int lane = threadIdx.x & 31;
+    double2 v[kPollParts];
+    bool ok;
+    do {
+        KTB_CHAOS_DELAY(0x706c);
+#pragma unroll
+        for (int m = 0; m < kPollParts; ++m)
+            if (32 * m < nb) v[m] = ld_relaxed_pair(row + min(lane + 32 * m, nb - 1) * kLineSlots);
+        ok = true;
+#pragma unroll
+        for (int m = 0; m < kPollParts; ++m)
+            if (32 * m < nb) ok = ok && __double_as_longlong(v[m].y) == tag;
+    } while (!__all_sync(0xffffffffu, ok));
+    double t = 0.0;
+#pragma unroll
+    for (int m = 0; m < kPollParts; ++m)
+        if (32 * m < nb) t += lane + 32 * m < nb ? v[m].x : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
 // ---- MGS with w in registers and the basis columns fed by bulk copies --------
 // The same slices, element-to-thread mapping, update arithmetic, reduction
 // trees and exchange as k_mgs_res (bit-identical projections), but w's slice
@@ -374,13 +412,14 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_dma(const double* __restri
         b += buf0[e * kRThreads + tid] * wr[e];
     }
     block_sum_w0(a, b, red);
+    const int rowlen = nb * kLineSlots;  // rows 0 / 1: projections, row 2: the input norm
     if (tid == 0) {
-        publish(slots + blockIdx.x, a, tag0);
-        publish(slots + nb + blockIdx.x, b, tag0 + 1);
+        publish(slots + 2 * rowlen + blockIdx.x * kLineSlots, a, tag0);
+        publish(slots + rowlen + blockIdx.x * kLineSlots, b, tag0 + 1);
     }
     if (tid < 32) {
-        const double t0 = poll_total(slots, nb, tag0);
-        const double t1 = poll_total(slots + nb, nb, tag0 + 1);
+        const double t0 = poll_total_lines(slots + 2 * rowlen, nb, tag0);
+        const double t1 = poll_total_lines(slots + rowlen, nb, tag0 + 1);
         if (tid == 0) {
             bc[0] = t0;
             bc[1] = t1;
@@ -417,12 +456,12 @@ __global__ void __launch_bounds__(kRThreads, 1) k_mgs_dma(const double* __restri
             fence_proxy_async_smem();
             issue(q + 2);
         }
-        double2* sl = slots + static_cast<int64_t>(q + 2) * nb;
+        double2* sl = slots + (q & 1) * rowlen;
         if (tid < 32) {
             p = tid < kRThreads / 32 ? red[2 * tid] : 0.0;
             for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-            if (tid == 0) publish(sl + blockIdx.x, p, tag0 + q + 2);
-            const double t = poll_total(sl, nb, tag0 + q + 2);
+            if (tid == 0) publish(sl + blockIdx.x * kLineSlots, p, tag0 + q + 2);
+            const double t = poll_total_lines(sl, nb, tag0 + q + 2);
             if (tid == 0) bc[0] = t;
         }
         KTB_SYNC();
@@ -503,7 +542,9 @@ struct GmresWork {
     GmresWork(int64_t n_, int64_t m_, bool prec_, int nb_, int res_nb_)
         : n(n_), m(m_), prec(prec_), nb(nb_), res_nb(res_nb_), b(n_), x(n_), r(n_), w(n_),
           V(static_cast<size_t>(n_) * (m_ + 1)), zp(prec_ ? n_ : 1), partials(4 * nb_),
-          dy(m_ + 1), slots(static_cast<size_t>(m_ + 3) * std::max(res_nb_, 1)),
+          dy(m_ + 1),
+          slots(std::max(static_cast<size_t>(m_ + 3), static_cast<size_t>(3 * kLineSlots)) *
+                std::max(res_nb_, 1)),
           h_pin(static_cast<size_t>(m_ + 1) * (m_ + 2)), brk_pin(m_ + 1), ev_s(m_ + 1),
           ev_e(m_ + 1), ev_step(m_ + 1) {
         KTB_CUDA(cudaEventCreate(&ev0));
@@ -569,7 +610,7 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         }
         const size_t res_smem = static_cast<size_t>(E) * kRThreads * 16;  // two slices
         // even n and E <= 14: w in registers, columns double-buffered by bulk copies
-        if ((n & 1) == 0 && !std::getenv("KTB_GMRES_NO_DMA_MGS")) {
+        if ((n & 1) == 0 && sms <= 32 * kPollParts && !std::getenv("KTB_GMRES_NO_DMA_MGS")) {
             switch (E) {
                 case 1: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<1>); break;
                 case 2: res_fn = reinterpret_cast<const void*>(&k_mgs_dma<2>); break;

@@ -1,0 +1,374 @@
+// Cost of one MGS projection's reduction chain (block sum -> cross-CTA
+// all-to-all -> broadcast) in isolation, one 1024-thread CTA per SM, for the
+// exchange variants considered for k_mgs_dma:
+//   0  block sum + barrier only (no cross-CTA step)
+//   1  pull: one tagged 16-byte slot per CTA, warp 0 polls all slots (ld.cv)      [k_mgs_res]
+//   2  pull, ld.relaxed.gpu polls
+//   3  push: thread t of every CTA stores its CTA's partial into CTA t's private
+//      inbox; warp 0 polls its own inbox only (one reader per line)
+//   4  push + all warps poll (warp w polls slots 32w..32w+31), sums via shared memory
+//   5  pull with 4 replicas of the slot array (CTA b polls replica b % 4): fewer readers per line
+//   6  pull with 8 replicas
+//   7  pull with 16 replicas
+//   8  one hop alone: CTA q % nb publishes, every CTA polls that one slot
+//   9  pull, two alternating slot rows (the lines stay in L2; a row is rewritten
+//      only after every CTA has finished reading it)
+//   10 pull, fresh rows, full 32-byte sector per slot (lanes 0 and 1 store the pair twice)
+//   11 = 9 + 10: two alternating rows of 32-byte slots
+//   12 pull, warp 0 polls with all its (<= 8) slot loads of a round in flight together
+//   13 pull, warps 0..4 poll one slot per lane, sums through shared memory
+//   14 two hops: every CTA stores its slot, CTA 0 alone polls the slots (warp 0, loads of a
+//      round in flight together), sums them and publishes the total; every CTA polls that one slot
+//   15 = 14 with one slot per 128-byte line; 16 = 12 with one slot per 128-byte line
+//   17 = 16 with st.relaxed.gpu; 18 = 16 with a 100 ns back-off between poll rounds;
+//   19 = 16 with slots 256 bytes apart
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/exchange_bench tools/exchange_bench.cu
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
+constexpr int kT = 1024;
+constexpr int kMaxPart = 8;
+
+__device__ __forceinline__ double2 ld_cv(const double2* p) {
+    double2 v;
+    asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_relaxed(const double2* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(double2* p, double2 v) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cg(double2* p, double2 v) {
+    asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+template <int kLoad>
+__device__ __forceinline__ double poll_total(const double2* slot, int nb, long long tag) {
+    const int lane = threadIdx.x & 31;
+    double acc[kMaxPart];
+    unsigned pending = 0;
+#pragma unroll
+    for (int m = 0; m < kMaxPart; ++m) {
+        acc[m] = 0.0;
+        if (lane + 32 * m < nb) pending |= 1u << m;
+    }
+    while (pending) {
+#pragma unroll
+        for (int m = 0; m < kMaxPart; ++m) {
+            if ((pending >> m) & 1u) {
+                const double2 v = kLoad == 0 ? ld_cv(slot + lane + 32 * m) : ld_relaxed(slot + lane + 32 * m);
+                if (__double_as_longlong(v.y) == tag) {
+                    acc[m] = v.x;
+                    pending &= ~(1u << m);
+                }
+            }
+        }
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int m = 0; m < kMaxPart; ++m) t += acc[m];
+    __syncwarp();
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
+__device__ __forceinline__ void block_sum_w0(double& a, double* red) {
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        a = l < blockDim.x / 32 ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    }
+}
+
+template <int kVar>
+__global__ void __launch_bounds__(kT, 1) k_chain(int k, double2* slots, double* out, long long tag0) {
+    __shared__ double red[kT / 32];
+    __shared__ double bc[2];
+    __shared__ double part[kT / 32];
+    const int nb = gridDim.x, tid = threadIdx.x;
+    double c = tid;
+    for (int q = 0; q < k; ++q) {
+        double p = c * 1e-9;
+        block_sum_w0(p, red);
+        const long long tag = tag0 + q;
+        if (kVar == 0) {
+            if (tid == 0) bc[0] = p;
+        } else if (kVar == 1 || kVar == 2) {
+            double2* sl = slots + static_cast<long long>(q) * nb;
+            if (tid == 0) st_cg(sl + blockIdx.x, make_double2(p, __longlong_as_double(tag)));
+            if (tid < 32) {
+                const double t = poll_total<kVar - 1>(sl, nb, tag);
+                if (tid == 0) bc[0] = t;
+            }
+        } else if (kVar >= 5 && kVar <= 7) {
+            constexpr int R = kVar == 5 ? 4 : kVar == 6 ? 8 : 16;
+            double2* sl = slots + static_cast<long long>(q) * nb * R;
+            if (tid < R)
+                st_cg(sl + tid * nb + blockIdx.x, make_double2(p, __longlong_as_double(tag)));
+            if (tid < 32) {
+                const double t = poll_total<1>(sl + (blockIdx.x % R) * nb, nb, tag);
+                if (tid == 0) bc[0] = t;
+            }
+        } else if (kVar == 9) {
+            double2* sl = slots + static_cast<long long>(q & 1) * nb;
+            if (tid == 0) st_cg(sl + blockIdx.x, make_double2(p, __longlong_as_double(tag)));
+            if (tid < 32) {
+                const double t = poll_total<1>(sl, nb, tag);
+                if (tid == 0) bc[0] = t;
+            }
+        } else if (kVar == 10 || kVar == 11) {
+            double2* sl = slots + static_cast<long long>(kVar == 10 ? q : (q & 1)) * nb * 2;
+            if (tid < 32) {
+                const double pv = __shfl_sync(0xffffffffu, p, 0);
+                if (tid < 2) st_cg(sl + 2 * blockIdx.x + tid, make_double2(pv, __longlong_as_double(tag)));
+                const int lane = tid;
+                double acc = 0.0;
+                for (int m = 0; m * 32 < nb; ++m) {
+                    if (lane + 32 * m < nb) {
+                        double2 r;
+                        do {
+                            r = ld_relaxed(sl + 2 * (lane + 32 * m));
+                        } while (__double_as_longlong(r.y) != tag);
+                        acc += r.x;
+                    }
+                }
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (tid == 0) bc[0] = acc;
+            }
+        } else if (kVar == 12) {
+            double2* sl = slots + static_cast<long long>(q & 1) * nb;
+            if (tid == 0) st_cg(sl + blockIdx.x, make_double2(p, __longlong_as_double(tag)));
+            if (tid < 32) {
+                double2 v[kMaxPart];
+                bool ok;
+                do {
+#pragma unroll
+                    for (int m = 0; m < kMaxPart; ++m)
+                        if (32 * m < nb) v[m] = ld_relaxed(sl + min(tid + 32 * m, nb - 1));
+                    ok = true;
+#pragma unroll
+                    for (int m = 0; m < kMaxPart; ++m)
+                        if (32 * m < nb) ok = ok && __double_as_longlong(v[m].y) == tag;
+                } while (!__all_sync(0xffffffffu, ok));
+                double t = 0.0;
+#pragma unroll
+                for (int m = 0; m < kMaxPart; ++m)
+                    if (32 * m < nb) t += tid + 32 * m < nb ? v[m].x : 0.0;
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (tid == 0) bc[0] = t;
+            }
+        } else if (kVar == 13) {
+            double2* sl = slots + static_cast<long long>(q & 1) * nb;
+            if (tid == 0) st_cg(sl + blockIdx.x, make_double2(p, __longlong_as_double(tag)));
+            const int w = tid >> 5, l = tid & 31;
+            if (w * 32 < nb) {
+                double v = 0.0;
+                if (tid < nb) {
+                    double2 r;
+                    do {
+                        r = ld_relaxed(sl + tid);
+                    } while (__double_as_longlong(r.y) != tag);
+                    v = r.x;
+                }
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (l == 0) part[w] = v;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int i = 0; i * 32 < nb; ++i) t += part[i];
+                bc[0] = t;
+            }
+        } else if (kVar == 14) {
+            double2* sl = slots + static_cast<long long>(q & 1) * (nb + 8);
+            double2* tot = sl + nb;
+            if (tid == 0) st_cg(sl + blockIdx.x, make_double2(p, __longlong_as_double(tag)));
+            if (blockIdx.x == 0 && tid < 32) {
+                double2 v[kMaxPart];
+                bool ok;
+                do {
+#pragma unroll
+                    for (int m = 0; m < kMaxPart; ++m)
+                        if (32 * m < nb) v[m] = ld_relaxed(sl + min(tid + 32 * m, nb - 1));
+                    ok = true;
+#pragma unroll
+                    for (int m = 0; m < kMaxPart; ++m)
+                        if (32 * m < nb) ok = ok && __double_as_longlong(v[m].y) == tag;
+                } while (!__all_sync(0xffffffffu, ok));
+                double t = 0.0;
+#pragma unroll
+                for (int m = 0; m < kMaxPart; ++m)
+                    if (32 * m < nb) t += tid + 32 * m < nb ? v[m].x : 0.0;
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (tid == 0) st_cg(tot, make_double2(t, __longlong_as_double(tag)));
+            }
+            if (tid == 0) {
+                double2 r;
+                do {
+                    r = ld_relaxed(tot);
+                } while (__double_as_longlong(r.y) != tag);
+                bc[0] = r.x;
+            }
+        } else if (kVar >= 15 && kVar <= 19) {
+            constexpr int S = kVar == 19 ? 16 : 8;  // slot stride in double2
+            double2* sl = slots + static_cast<long long>(q & 1) * (nb + 8) * S;
+            double2* tot = sl + nb * S;
+            if (tid == 0) {
+                if (kVar == 17)
+                    st_relaxed(sl + blockIdx.x * S, make_double2(p, __longlong_as_double(tag)));
+                else
+                    st_cg(sl + blockIdx.x * S, make_double2(p, __longlong_as_double(tag)));
+            }
+            if ((kVar >= 16 || blockIdx.x == 0) && tid < 32) {
+                double2 v[kMaxPart];
+                bool ok;
+                do {
+#pragma unroll
+                    for (int m = 0; m < kMaxPart; ++m)
+                        if (32 * m < nb) v[m] = ld_relaxed(sl + min(tid + 32 * m, nb - 1) * S);
+                    ok = true;
+#pragma unroll
+                    for (int m = 0; m < kMaxPart; ++m)
+                        if (32 * m < nb) ok = ok && __double_as_longlong(v[m].y) == tag;
+                    if (kVar == 18 && !ok) __nanosleep(100);
+                } while (!__all_sync(0xffffffffu, ok));
+                double t = 0.0;
+#pragma unroll
+                for (int m = 0; m < kMaxPart; ++m)
+                    if (32 * m < nb) t += tid + 32 * m < nb ? v[m].x : 0.0;
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (kVar >= 16) {
+                    if (tid == 0) bc[0] = t;
+                } else if (tid == 0) {
+                    st_cg(tot, make_double2(t, __longlong_as_double(tag)));
+                }
+            }
+            if (kVar == 15 && tid == 0) {
+                double2 r;
+                do {
+                    r = ld_relaxed(tot);
+                } while (__double_as_longlong(r.y) != tag);
+                bc[0] = r.x;
+            }
+        } else if (kVar == 8) {
+            double2* sl = slots + q;
+            if (tid == 0 && blockIdx.x == q % nb)
+                st_cg(sl, make_double2(p, __longlong_as_double(tag)));
+            if (tid == 0) {
+                double2 r;
+                do {
+                    r = ld_relaxed(sl);
+                } while (__double_as_longlong(r.y) != tag);
+                bc[0] = r.x;
+            }
+        } else if (kVar == 3) {
+            // inbox of CTA d for reduction q: slots[(q * nb + d) * nb + src]
+            double2* sl = slots + static_cast<long long>(q) * nb * nb;
+            if (tid == 0) bc[1] = p;
+            __syncthreads();
+            if (tid < nb)
+                st_cg(sl + static_cast<long long>(tid) * nb + blockIdx.x,
+                      make_double2(bc[1], __longlong_as_double(tag)));
+            if (tid < 32) {
+                const double t = poll_total<1>(sl + static_cast<long long>(blockIdx.x) * nb, nb, tag);
+                if (tid == 0) bc[0] = t;
+            }
+        } else if (kVar == 4) {
+            double2* sl = slots + static_cast<long long>(q) * nb * nb;
+            if (tid == 0) bc[1] = p;
+            __syncthreads();
+            if (tid < nb)
+                st_cg(sl + static_cast<long long>(tid) * nb + blockIdx.x,
+                      make_double2(bc[1], __longlong_as_double(tag)));
+            const int w = tid >> 5, l = tid & 31;
+            if (w * 32 < nb) {
+                const double2* in = sl + static_cast<long long>(blockIdx.x) * nb + w * 32;
+                double v = 0.0;
+                if (w * 32 + l < nb) {
+                    double2 r;
+                    do {
+                        r = ld_relaxed(in + l);
+                    } while (__double_as_longlong(r.y) != tag);
+                    v = r.x;
+                }
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (l == 0) part[w] = v;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int i = 0; i * 32 < nb; ++i) t += part[i];
+                bc[0] = t;
+            }
+        }
+        __syncthreads();
+        c = bc[0];
+    }
+    if (blockIdx.x == 0 && tid == 0) out[0] = c;
+}
+
+template <int kVar>
+static void run(int nb, int k, double2* slots, double* out, long long& tag) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        void* args[] = {&k, &slots, &out, &tag};
+        cudaEventRecord(a);
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_chain<kVar>), dim3(nb), dim3(kT),
+                                    args, 0, 0);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        tag += 4096;
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    const cudaError_t e = cudaGetLastError();
+    printf("variant %d: %8.3f us per reduction (k = %d, %d CTAs) %s\n", kVar, best * 1e3 / k, k, nb,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int k = 1000;
+    double2* slots;
+    double* out;
+    const size_t bytes = sizeof(double2) * static_cast<size_t>(k) * sms * sms;
+    cudaMalloc(&slots, bytes);
+    cudaMemset(slots, 0, bytes);
+    cudaMalloc(&out, 8);
+    long long tag = 64;
+    run<0>(sms, k, slots, out, tag);
+    run<1>(sms, k, slots, out, tag);
+    run<2>(sms, k, slots, out, tag);
+    run<3>(sms, k, slots, out, tag);
+    run<4>(sms, k, slots, out, tag);
+    run<5>(sms, k, slots, out, tag);
+    run<6>(sms, k, slots, out, tag);
+    run<7>(sms, k, slots, out, tag);
+    run<8>(sms, k, slots, out, tag);
+    run<9>(sms, k, slots, out, tag);
+    run<12>(sms, k, slots, out, tag);
+    run<14>(sms, k, slots, out, tag);
+    run<15>(sms, k, slots, out, tag);
+    run<16>(sms, k, slots, out, tag);
+    run<17>(sms, k, slots, out, tag);
+    run<18>(sms, k, slots, out, tag);
+    run<19>(sms, k, slots, out, tag);
+    run<13>(sms, k, slots, out, tag);
+    run<10>(sms, k, slots, out, tag);
+    run<11>(sms, k, slots, out, tag);
+    run<0>(sms, k, slots, out, tag);
+    return 0;
+}
