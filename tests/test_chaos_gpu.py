@@ -35,6 +35,6 @@ def test_race_stress_build_bitwise_equal(tmp_path):
     got = _run("libktb_chaos.so", tmp_path / "chaos.npz", 6)
     assert str(got["lib"]) == "libktb_chaos.so" and str(ref["lib"]) == "libktb.so"
     keys = sorted(k for k in ref.files if k != "lib")
-    assert len(keys) >= 14
+    assert len(keys) >= 16
     for k in keys:
         assert np.array_equal(ref[k], got[k]), k

@@ -85,6 +85,25 @@ def test_gmres_both_mgs_kernels_and_config5(monkeypatch):
     assert r.spmv_calls == r.iterations + r.restarts + 2
 
 
+@pytest.mark.parametrize("dims", [(24, 20, 16), (96, 64, 40), (130, 128, 126)])
+def test_mgs_bulk_copy_kernel_bitwise_equals_resident_kernel(monkeypatch, dims):
+    """k_mgs_dma (even n: w in registers, basis columns double-buffered in
+    shared memory by bulk copies, slots one per line) keeps k_mgs_res's
+    element-to-thread mapping, update arithmetic and reduction trees: the
+    two solves agree in every iteration and bit for bit in x, for slices of
+    1, 2 and 14 elements per thread (the last with a ragged final CTA)."""
+    n, rp, ci, v = matgen.stencil7(*dims, xp=-0.7, xm=-1.3)
+    assert n % 2 == 0
+    b = O.spmv_ref(n, rp, ci, v, np.ones(n))
+    r_dma = _solve(n, rp, ci, v, b)
+    monkeypatch.setenv("KTB_GMRES_NO_DMA_MGS", "1")
+    r_res = _solve(n, rp, ci, v, b)
+    monkeypatch.delenv("KTB_GMRES_NO_DMA_MGS")
+    assert r_dma.converged and r_dma.iterations == r_res.iterations
+    assert np.array_equal(r_dma.x, r_res.x)
+    assert np.array_equal(r_dma.residual_history, r_res.residual_history)
+
+
 @pytest.mark.parametrize("stream_mgs", ["0", "1"])
 @pytest.mark.parametrize("kernel,param", [(0, 100), (1, 8)])
 def test_gmres_odd_n_unaligned_columns(monkeypatch, stream_mgs, kernel, param):

@@ -62,6 +62,10 @@ def main():
     x5 = O.seeded_vector(a5.n, 5)
     for prm in (104, 105, 106):
         rep_apply(K.DevicePlan(a5, 0, prm), x5, a5.n, f"u1_{prm}")
+    # S1 106: the expanded 27-point stencil's pair-coded records (27 slots, 4 batches)
+    a27 = K.stencil27_upper(48, 40, 36)
+    rep_apply(K.DevicePlan(a27, K.SymKernel.s1_row, 106), O.seeded_vector(a27.n, 2), a27.n,
+              "s1_106")
     # warp tiles (smem products, swizzled row-end maps, carries), both shapes
     n, rp, ci, v = matgen.powerlaw(300_000, 3, 3_000_000, 0.1, 65536)
     a3 = K.CsrMatrix(n, rp, ci, v)
@@ -71,7 +75,9 @@ def main():
                         (0, 101, "u1sorted")):
         rep_apply(K.DevicePlan(a3, k, prm), x3, n, tag)
     # MGS tag exchange: GMRES on odd n and on a 48^3 convection-diffusion
-    for dims, tag in (((15, 13, 11), "gmres_odd"), ((48, 48, 48), "gmres_48")):
+    # (odd n: k_mgs_res; even n: k_mgs_dma with 1 and 8 elements per thread)
+    for dims, tag in (((15, 13, 11), "gmres_odd"), ((48, 48, 48), "gmres_48"),
+                      ((96, 96, 96), "gmres_96")):
         n, rp, ci, v = matgen.stencil7(*dims, xp=-0.7, xm=-1.3)
         b = O.spmv_ref(n, rp, ci, v, np.ones(n))
         a = K.CsrMatrix(n, rp, ci, v)
