@@ -1329,33 +1329,47 @@ void u1_run(ktb_plan* p, const double* x, double* y, int64_t r0, int64_t r1) {
 
 // =============================================================== carries
 // Tile carries (row, value) in tile order; the rows are non-decreasing, so
-// the tiles carrying one row form a run. One warp per tile: a tile that
-// starts a run sums the run 32 carries at a time (lane-strided partial sums,
-// then a fixed shuffle tree: deterministic) and adds it to y once; other
-// tiles exit. A run of L tiles costs L/32 dependent rounds (a 65,536-long
-// row spans 256 tiles: 8), where a serial walk cost L.
-__global__ void k_fixup_carries(const int32_t* __restrict__ crow,
-                                const double* __restrict__ cval, int64_t tiles, int64_t n,
-                                double* __restrict__ y) {
-    const int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+// the tiles carrying one row form a run. One thread per tile: the tile's row
+// and its neighbours' go out in one round trip; a tile that is a run by itself
+// (almost all of them: a run of L tiles needs a row of > 256 (L - 1)
+// nonzeros) adds its carry to y at once. The longer runs starting in a warp
+// are then summed by the whole warp one after the other, 32 carries at a time
+// (lane-strided partial sums, then a fixed shuffle tree: deterministic), and
+// added to y once: a run of L tiles costs L/32 dependent rounds (a
+// 65,536-long row spans 256 tiles: 8), where a serial walk cost L.
+__global__ void __launch_bounds__(256) k_fixup_carries(const int32_t* __restrict__ crow,
+                                                       const double* __restrict__ cval,
+                                                       int64_t tiles, int64_t n,
+                                                       double* __restrict__ y) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    if (t >= tiles) return;
-    const int32_t r = __ldg(crow + t);
-    if (r < 0 || r >= n) return;
-    if (t > 0 && __ldg(crow + t - 1) == r) return;  // not the run's first tile
-    double acc = 0.0;
-    for (int64_t u0 = t;; u0 += 32) {
-        const int64_t u = u0 + lane;
-        const bool same = u < tiles && __ldg(crow + u) == r;
-        if (same) acc += __ldg(cval + u);
-        if (__ballot_sync(0xffffffffu, same) != 0xffffffffu) break;
+    const bool in = t < tiles;
+    const int32_t r = in ? __ldg(crow + t) : -1;
+    const int32_t prev = in && t > 0 ? __ldg(crow + t - 1) : -1;
+    const int32_t next = in && t + 1 < tiles ? __ldg(crow + t + 1) : -1;
+    const double cv = in ? __ldg(cval + t) : 0.0;
+    const bool start = r >= 0 && r < n && prev != r;  // the run's first tile
+    if (start && next != r) y[r] += cv;
+    unsigned longer = __ballot_sync(0xffffffffu, start && next == r);
+    while (longer) {
+        const int src = __ffs(longer) - 1;
+        longer &= longer - 1;
+        const int64_t t0 = __shfl_sync(0xffffffffu, t, src);
+        const int32_t rr = __shfl_sync(0xffffffffu, r, src);
+        double acc = 0.0;
+        for (int64_t u0 = t0;; u0 += 32) {
+            const int64_t u = u0 + lane;
+            const bool same = u < tiles && __ldg(crow + u) == rr;
+            if (same) acc += __ldg(cval + u);
+            if (__ballot_sync(0xffffffffu, same) != 0xffffffffu) break;
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) y[rr] += acc;
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) y[r] += acc;
 }
 
 static void fixup_run(ktb_plan* p, double* y) {
-    k_fixup_carries<<<ceil_div(p->tiles * 32, 256), 256, 0, p->stream>>>(
+    k_fixup_carries<<<ceil_div(p->tiles, 256), 256, 0, p->stream>>>(
         p->carry_row.p, p->carry_val.p, p->tiles, p->m->n, y);
     KTB_LAUNCH();
 }
