@@ -1649,20 +1649,18 @@ __global__ void __launch_bounds__(32 * kTileWarps, KTB_U2W_MINB * 8 / kTileWarps
     }
 }
 
-// 16-byte streaming loads (U3 lanes)
-__device__ __forceinline__ int4 ld_stream_v4i32(const int32_t* p) {
-    int4 r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+// 32-byte streaming loads (sm_100 LDG.256): a lane's load is one whole sector,
+// where two 16-byte loads of a lane-blocked layout fetch every sector twice
+__device__ __forceinline__ void ld_stream_v8i32(const int32_t* p, int32_t* r) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
         : "l"(p), "l"(pol_first()));
-    return r;
 }
-__device__ __forceinline__ double2 ld_stream_v2f64(const double* p) {
-    double2 r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-        : "=d"(r.x), "=d"(r.y)
+__device__ __forceinline__ void ld_stream_v4f64(const double* p, double* r) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
         : "l"(p), "l"(pol_first()));
-    return r;
 }
 
 // first row whose end lies beyond z = w*T (w = 0: row 0)
@@ -1815,7 +1813,8 @@ __global__ void k_tile_q(const uint32_t* __restrict__ bits, int64_t nnz, int64_t
 // before a lane's first flag takes the carry of the lanes before it (one
 // flag-aware warp scan, as k_u2w), the run open at the tile end is the tile
 // carry (k_fixup_carries). Empty rows and the last nonempty row (never closed
-// by a flag) are zeroed first by k_zero_rows.
+// by a flag) are zeroed first by k_zero_rows (fused into the warps' work it
+// measured 2-10 us slower on config 3).
 __global__ void k_tile_pop(const uint32_t* __restrict__ bits, int64_t tiles,
                            int32_t* __restrict__ pop) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -1856,20 +1855,10 @@ __global__ void __launch_bounds__(32 * kTileWarps, 32 / kTileWarps) k_u3w(const 
     int32_t c[IPT];
     double v[IPT];
     if (z0 + 256 <= nnz) {
-#pragma unroll
-        for (int q = 0; q < IPT; q += 4) {
-            const int4 c4 = ld_stream_v4i32(col + k0 + q);
-            c[q] = c4.x;
-            c[q + 1] = c4.y;
-            c[q + 2] = c4.z;
-            c[q + 3] = c4.w;
-        }
-#pragma unroll
-        for (int q = 0; q < IPT; q += 2) {
-            const double2 v2 = ld_stream_v2f64(val + k0 + q);
-            v[q] = v2.x;
-            v[q + 1] = v2.y;
-        }
+        // 8 columns = one 32-byte sector, 8 values = two
+        ld_stream_v8i32(col + k0, c);
+        ld_stream_v4f64(val + k0, v);
+        ld_stream_v4f64(val + k0 + 4, v + 4);
     } else {
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
