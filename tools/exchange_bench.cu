@@ -22,6 +22,9 @@
 //   15 = 14 with one slot per 128-byte line; 16 = 12 with one slot per 128-byte line
 //   17 = 16 with st.relaxed.gpu; 18 = 16 with a 100 ns back-off between poll rounds;
 //   19 = 16 with slots 256 bytes apart
+//   20 = 16 while every CTA also streams 112 KB per reduction from HBM by one bulk copy
+//      (issued before the publish, awaited before the next block sum: k_mgs_dma's traffic)
+//   21 = 20 with the copy issued after the poll completed
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/exchange_bench tools/exchange_bench.cu
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -315,6 +318,113 @@ __global__ void __launch_bounds__(kT, 1) k_chain(int k, double2* slots, double* 
     if (blockIdx.x == 0 && tid == 0) out[0] = c;
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+constexpr int kLoadBytes = 112 * 1024;
+// variant 16's exchange with a concurrent HBM stream per CTA
+template <bool kAfter, int kChunks>
+__global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double* out, long long tag0,
+                                                  const char* src, long long src_bytes) {
+    extern __shared__ __align__(128) unsigned char buf[];
+    __shared__ double red[kT / 32];
+    __shared__ double bc[2];
+    __shared__ __align__(8) unsigned long long bar;
+    const int nb = gridDim.x, tid = threadIdx.x;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double c = tid;
+    long long off = static_cast<long long>(blockIdx.x) * kLoadBytes;
+    auto issue = [&]() {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                     "r"(kLoadBytes)
+                     : "memory");
+        constexpr int kChunk = kLoadBytes / kChunks;
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ++ch)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(buf) + ch * kChunk),
+                "l"(src + off + ch * kChunk), "r"(kChunk), "r"(smem_u32(&bar))
+                : "memory");
+        off += static_cast<long long>(nb) * kLoadBytes;
+        if (off + kLoadBytes > src_bytes) off = static_cast<long long>(blockIdx.x) * kLoadBytes;
+    };
+    for (int q = 0; q < k; ++q) {
+        if (q > 0) {  // the previous copy (every thread waits, as the pass would)
+            asm volatile(
+                "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra "
+                "W_%=;\n}\n" ::"r"(smem_u32(&bar)),
+                "r"((q - 1) & 1)
+                : "memory");
+        }
+        double p = c * 1e-9 + buf[tid];
+        block_sum_w0(p, red);
+        const long long tag = tag0 + q;
+        constexpr int S = 8;
+        double2* sl = slots + static_cast<long long>(q & 1) * (nb + 8) * S;
+        if (tid == 0) {
+            if (!kAfter) issue();
+            st_cg(sl + blockIdx.x * S, make_double2(p, __longlong_as_double(tag)));
+        }
+        if (tid < 32) {
+            double2 v[kMaxPart];
+            bool ok;
+            do {
+#pragma unroll
+                for (int m = 0; m < kMaxPart; ++m)
+                    if (32 * m < nb) v[m] = ld_relaxed(sl + min(tid + 32 * m, nb - 1) * S);
+                ok = true;
+#pragma unroll
+                for (int m = 0; m < kMaxPart; ++m)
+                    if (32 * m < nb) ok = ok && __double_as_longlong(v[m].y) == tag;
+            } while (!__all_sync(0xffffffffu, ok));
+            double t = 0.0;
+#pragma unroll
+            for (int m = 0; m < kMaxPart; ++m)
+                if (32 * m < nb) t += tid + 32 * m < nb ? v[m].x : 0.0;
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (tid == 0) {
+                bc[0] = t;
+                if (kAfter) issue();
+            }
+        }
+        __syncthreads();
+        c = bc[0];
+    }
+    if (blockIdx.x == 0 && tid == 0) out[0] = c;
+}
+
+template <bool kAfter, int kChunks>
+static void run_loaded(int nb, int k, double2* slots, double* out, long long& tag, const char* src,
+                       long long src_bytes) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaFuncSetAttribute(k_loaded<kAfter, kChunks>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLoadBytes);
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        void* args[] = {&k, &slots, &out, &tag, &src, &src_bytes};
+        cudaEventRecord(a);
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loaded<kAfter, kChunks>), dim3(nb),
+                                    dim3(kT), args, kLoadBytes, 0);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        tag += 4096;
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    const cudaError_t e = cudaGetLastError();
+    printf("variant %d (%d chunks): %8.3f us per reduction (k = %d, %d CTAs, %.1f TB/s streamed) %s\n",
+           kAfter ? 21 : 20, kChunks, best * 1e3 / k, k, nb,
+           double(kLoadBytes) * nb / (best * 1e-3 / k) / 1e12,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
 template <int kVar>
 static void run(int nb, int k, double2* slots, double* out, long long& tag) {
     cudaEvent_t a, b;
@@ -370,5 +480,15 @@ int main() {
     run<10>(sms, k, slots, out, tag);
     run<11>(sms, k, slots, out, tag);
     run<0>(sms, k, slots, out, tag);
+    char* src;
+    const long long src_bytes = 1ll << 30;
+    cudaMalloc(&src, src_bytes);
+    cudaMemset(src, 0, src_bytes);
+    run_loaded<false, 1>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 2>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 4>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 8>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 16>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<true, 1>(sms, k, slots, out, tag, src, src_bytes);
     return 0;
 }
