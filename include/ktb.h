@@ -161,16 +161,21 @@ int ktb_expand_symmetric(const ktb_matrix* m, ktb_matrix** out);
  *                instead of 12); 103 / 104 = persistent, two-deep pipelined
  *                warp slices (uniform width <= 8) with int32 / coded columns;
  *                105 = persistent coded slices staged through per-warp
- *                bulk-copy (TMA) rings; 106 = the same with the values coded
- *                too (per slice <= 15 distinct fp64 bit patterns: one 448-byte
- *                record per 32 rows, 14 B per row; refused otherwise) -- the
- *                halo operator's default, falling back to 105;
+ *                bulk-copy (TMA) rings; 106 = persistent warps over pair-coded
+ *                records (per 64 rows a dictionary of <= 63 distinct (column
+ *                delta, fp64 bit pattern) pairs and one 8-bit code per slot,
+ *                slice width <= 32: 10 B per 7-point row; refused otherwise)
+ *                -- the halo operator's default, falling back to 105;
  *                100-106 are all bitwise equal to spmv_ref;
  *            U2: 0/4/8 = warp tiles of 32*IPT nonzeros (0 = 8);
  *                104/108/112 = merge-path tiles;
  *            U3/U4: nonzeros per segment lane E in {4,8,16} (0 = 8); U3 1008
  *                = flag-driven warp-level BSS over 256-nonzero tiles;
- *            S1/S2: lanes per row (0 = auto); S3: 0 (2048-row sub-tiles).
+ *            S1/S2: lanes per row (0 = auto); S1 106 = the transposed products
+ *                gathered from the expanded matrix's pair-coded records (U1
+ *                106 over expand_symmetric(A); bitwise equal to
+ *                spmv_ref(expand_symmetric(A)); refused like U1 106);
+ *                S3: 0 (2048-row sub-tiles).
  *            The selector (ktb_select) sweeps these; see INTEGRATION.md.
  *            Bits 16..31 of param carry a launch shape (CTA threads; 0 =
  *            default): U1 100/101 take 64/128/256, U2 warp tiles and U3 1008
