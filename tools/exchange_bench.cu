@@ -25,6 +25,7 @@
 //   20 = 16 while every CTA also streams 112 KB per reduction from HBM by one bulk copy
 //      (issued before the publish, awaited before the next block sum: k_mgs_dma's traffic)
 //   21 = 20 with the copy issued after the poll completed
+//   20 with "L2 prefetch p ahead": thread 0 also pulls the slice p copies ahead into L2
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/exchange_bench tools/exchange_bench.cu
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -323,7 +324,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 constexpr int kLoadBytes = 112 * 1024;
 // variant 16's exchange with a concurrent HBM stream per CTA
-template <bool kAfter, int kChunks>
+template <bool kAfter, int kChunks, int kPf = 0>
 __global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double* out, long long tag0,
                                                   const char* src, long long src_bytes) {
     extern __shared__ __align__(128) unsigned char buf[];
@@ -352,6 +353,12 @@ __global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double*
                 : "memory");
         off += static_cast<long long>(nb) * kLoadBytes;
         if (off + kLoadBytes > src_bytes) off = static_cast<long long>(blockIdx.x) * kLoadBytes;
+        if (kPf) {  // the slice kPf copies ahead into L2
+            long long po = off + static_cast<long long>(kPf - 1) * nb * kLoadBytes;
+            if (po + kLoadBytes <= src_bytes)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + po), "r"(kLoadBytes)
+                             : "memory");
+        }
     };
     for (int q = 0; q < k; ++q) {
         if (q > 0) {  // the previous copy (every thread waits, as the pass would)
@@ -398,18 +405,18 @@ __global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double*
     if (blockIdx.x == 0 && tid == 0) out[0] = c;
 }
 
-template <bool kAfter, int kChunks>
+template <bool kAfter, int kChunks, int kPf = 0>
 static void run_loaded(int nb, int k, double2* slots, double* out, long long& tag, const char* src,
                        long long src_bytes) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    cudaFuncSetAttribute(k_loaded<kAfter, kChunks>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLoadBytes);
+    cudaFuncSetAttribute(k_loaded<kAfter, kChunks, kPf>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLoadBytes);
     float best = 1e30f;
     for (int rep = 0; rep < 6; ++rep) {
         void* args[] = {&k, &slots, &out, &tag, &src, &src_bytes};
         cudaEventRecord(a);
-        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loaded<kAfter, kChunks>), dim3(nb),
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loaded<kAfter, kChunks, kPf>), dim3(nb),
                                     dim3(kT), args, kLoadBytes, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
@@ -419,8 +426,8 @@ static void run_loaded(int nb, int k, double2* slots, double* out, long long& ta
         if (rep > 0 && ms < best) best = ms;
     }
     const cudaError_t e = cudaGetLastError();
-    printf("variant %d (%d chunks): %8.3f us per reduction (k = %d, %d CTAs, %.1f TB/s streamed) %s\n",
-           kAfter ? 21 : 20, kChunks, best * 1e3 / k, k, nb,
+    printf("variant %d (%d chunks, L2 prefetch %d ahead): %8.3f us per reduction (k = %d, %d CTAs, %.1f TB/s streamed) %s\n",
+           kAfter ? 21 : 20, kChunks, kPf, best * 1e3 / k, k, nb,
            double(kLoadBytes) * nb / (best * 1e-3 / k) / 1e12,
            e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
@@ -490,5 +497,8 @@ int main() {
     run_loaded<false, 8>(sms, k, slots, out, tag, src, src_bytes);
     run_loaded<false, 16>(sms, k, slots, out, tag, src, src_bytes);
     run_loaded<true, 1>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 1, 1>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 1, 2>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 1, 3>(sms, k, slots, out, tag, src, src_bytes);
     return 0;
 }
