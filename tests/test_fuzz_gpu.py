@@ -1,0 +1,20 @@
+"""Randomised bitwise parity of the pair-coded record kernels (U1 106, S1 106)
+against the oracle: tools/fuzz_u1v.py on a fixed seed (random banded
+matrices, 1-32 deltas, per-block value palettes, dropped entries, empty rows,
+n from 1 to 70,001; whole applies and random row sub-ranges; refused layouts
+must fail with the documented message)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def test_pair_coded_records_fuzz_bitwise():
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_u1v.py"), "160", "11"],
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "all built plans bitwise equal to the oracle" in p.stdout
