@@ -231,6 +231,18 @@ def test_config1_full_size_all_unsym(K):
     for kern in UNSYM:
         y = _run_unsym(K, a, kern, xd)
         assert_close(y.cpu().numpy(), yref, absax, kern)
+    # the bench's kernel for configs 1 and 5 (U1 106, pair-coded records): bitwise
+    for prm in (105, 106):
+        y = torch.full_like(xd, float("nan"))
+        K.DevicePlan(a, K.UnsymKernel.u1_row, prm).apply(xd, y)
+        assert np.array_equal(y.cpu().numpy(), yref), prm
+    a5 = K.stencil7(128, 128, 128, c_xm=-1.3, c_xp=-0.7)
+    rp, ci, v = a5.to_host()
+    x5 = O.seeded_vector(a5.n, 5)
+    xd5 = torch.from_numpy(x5).cuda()
+    y = torch.full_like(xd5, float("nan"))
+    K.DevicePlan(a5, K.UnsymKernel.u1_row, 106).apply(xd5, y)
+    assert np.array_equal(y.cpu().numpy(), O.spmv_ref(a5.n, rp, ci, v, x5))
 
 
 def test_config2_full_size_sym(K):
@@ -249,6 +261,11 @@ def test_config2_full_size_sym(K):
     for kern in SYM:
         y = _run_sym(K, a, kern, xd)
         assert_close(y.cpu().numpy(), yref, absax, kern)
+    # S1 106 (the bench's selected kernel: gathers over the expanded pair-coded
+    # records): bitwise equal to spmv_ref(expand_symmetric(A)) on every row
+    y = torch.full_like(xd, float("nan"))
+    K.DevicePlan(a, K.SymKernel.s1_row, 106).apply(xd, y)
+    assert np.array_equal(y.cpu().numpy(), yref)
 
 
 def test_seeded_vector_device_bitwise(K):
