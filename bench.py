@@ -660,7 +660,7 @@ def run_halo(args, cfg):
     yh = torch.empty(shard.n_local, dtype=torch.float64).pin_memory()
     xn, yn = xo.numpy(), yh.numpy()
     e2e = {}
-    for chunks in (16, 1):
+    for chunks in (64, 32, 16, 1):
         shard.apply_host(xn, yn, chunks=chunks)  # warm
         ts = []
         for k in range(max(3, min(args.steps, 10))):
@@ -674,8 +674,11 @@ def run_halo(args, cfg):
         e2e[chunks] = float(np.mean(ts))
     clocks = sampler.stop()
     ach_rank = B_int / (int_ms / 1e3) / 1e9 if int_ms > 0 else 0.0
-    ms, e2e16, e2e1, halo_max, int_max, bnd_max = ctl.max(
-        [ms, e2e[16], e2e[1], halo_ms, int_ms, bnd_ms])
+    ms, e2e64, e2e32, e2e16, e2e1, halo_max, int_max, bnd_max = ctl.max(
+        [ms, e2e[64], e2e[32], e2e[16], e2e[1], halo_ms, int_ms, bnd_ms])
+    by_chunks = {64: e2e64, 32: e2e32, 16: e2e16}
+    e2e_chunks = min(by_chunks, key=by_chunks.get)  # the chunk count a caller would pick
+    e2e_best = by_chunks[e2e_chunks]
     ach_min, = ctl.min([ach_rank])
     if rank == 0:
         peak, peak_src = peak_hbm()
@@ -710,12 +713,14 @@ def run_halo(args, cfg):
                                  "exceed 1; stream_bytes_per_launch = the bytes of its own "
                                  "layout + x + y; traffic = its measured DRAM bytes per launch "
                                  "(ncu)"},
-            "e2e": {"value": B / (e2e16 / 1e3) / 1e9, "unit": "GB/s",
+            "e2e": {"value": B / (e2e_best / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob,
-                    "ms_per_step": e2e16,
+                    "ms_per_step": e2e_best, "chunks": e2e_chunks,
                     "def": "ktb_halo_spmv_host on every rank: owned x from pinned host memory "
-                           "in, owned y out, copies overlapped with 16 row chunks inside the "
-                           "call; wall clock, max over ranks",
+                           "in, owned y out, copies overlapped with the row chunks inside the "
+                           "call (16, 32 and 64 chunks timed, the fastest reported); wall "
+                           "clock, max over ranks",
+                    "ms_by_chunks": {str(k): v for k, v in by_chunks.items()},
                     "unchunked": {"value": B / (e2e1 / 1e3) / 1e9, "ms_per_step": e2e1}},
             "gpu_launches": args.steps * shard.launches_per_apply() * ws,
             "clocks": clocks,
