@@ -18,3 +18,13 @@ def test_pair_coded_records_fuzz_bitwise():
                        capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
     assert "all built plans bitwise equal to the oracle" in p.stdout
+
+
+def test_every_plan_variant_fuzz():
+    """tools/fuzz_all.py on a fixed seed: every device plan variant (U1 lanes
+    and 100-106, U2 / U3 / U4 in both CTA shapes, S1 / S2 / S3, S1 106) on
+    random matrices of six families against the oracle."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_all.py"), "24", "5"],
+                       capture_output=True, text=True, timeout=1200)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "all reproducible" in p.stdout
