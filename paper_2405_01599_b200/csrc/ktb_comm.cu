@@ -1065,14 +1065,16 @@ int ktb_dist_set_plan(ktb_dist* d, ktb_plan* plan) {
 
 int ktb_dist_spmv(ktb_dist* d, const double* x_owned, double* y, void* stream) {
     return guarded_call([&] {
-        require(d != nullptr && x_owned != nullptr && y != nullptr, "spmv: dimension mismatch");
+        // (a rank that owns no rows has nothing to point at)
+        require(d != nullptr && ((x_owned != nullptr && y != nullptr) || d->n_loc == 0),
+                "spmv: dimension mismatch");
         dist_spmv(d, x_owned, y, static_cast<cudaStream_t>(stream));
     });
 }
 
 int ktb_dist_exchange(ktb_dist* d, const double* x_owned, void* stream) {
     return guarded_call([&] {
-        require(d != nullptr && x_owned != nullptr, "spmv: dimension mismatch");
+        require(d != nullptr && (x_owned != nullptr || d->n_loc == 0), "spmv: dimension mismatch");
         DeviceGuard g(d->device);
         auto s = static_cast<cudaStream_t>(stream);
         dist_exchange(d, x_owned, s);

@@ -623,8 +623,7 @@ void gmres_run(ktb_plan* A, ktb_ilu* P, const double* b_host, double* x_host, in
         }
         int res_nb = 0;
         if (res_fn && !std::getenv("KTB_GMRES_STREAM_MGS")) {
-            KTB_CUDA(cudaFuncSetAttribute(res_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(res_smem)));
+            allow_max_dynamic_smem(res_fn);
             int occ = 0;
             KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, res_fn, kRThreads,
                                                                    res_smem));

@@ -317,4 +317,22 @@ int guarded_call(const std::function<void()>& f);
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Opt a kernel into the device's full dynamic shared memory. The attribute is
+// per function, not per plan: setting it to one plan's need lets a later plan
+// with a smaller need lower it under an earlier plan's launches (seen as
+// "invalid argument" with two U1 105 plans of different widths, and with
+// ranks building plans concurrently). Every caller sets the same value, so
+// the order and concurrency of plan setups no longer matter.
+template <class F>
+inline void allow_max_dynamic_smem(F fn) {
+    int dev = 0, optin = 0;
+    KTB_CUDA(cudaGetDevice(&dev));
+    KTB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    KTB_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)));
+    KTB_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
+}
+
 }  // namespace ktb

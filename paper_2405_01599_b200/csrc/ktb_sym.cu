@@ -913,9 +913,10 @@ void s3_setup(ktb_plan* p) {
     }
     upd(L.diag, sdiag);
     KTB_CUDA(cudaStreamSynchronize(st));
-    KTB_CUDA(cudaFuncSetAttribute(T3 == 512 ? k_s3<512> : k_s3<256>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kS3SmemFixed + W * 8)));
+    if (T3 == 512)
+        allow_max_dynamic_smem(k_s3<512>);
+    else
+        allow_max_dynamic_smem(k_s3<256>);
     p->ctas = P;
     // (round 1 also carried an in-kernel cooperative merge, 85.2 vs 82.9 us,
     // and a persistent two-deep fixup, 82.3 vs 80.3-80.9 us on config 2; both

@@ -1155,7 +1155,7 @@ void u1_setup(ktb_plan* p) {
         const U1vLayout L = u1v_layout(p->rec_dict - 1, p->ell_width);
         const int smem = u1v_smem(L);
         const U1vFn fn = u1v_kernel(p->ell_width);
-        KTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        allow_max_dynamic_smem(fn);
         int occ = 0;
         KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kU1vWarps * 32, smem));
         p->ctas = static_cast<int64_t>(std::max(occ, 1)) * p->m->sm_count;
@@ -1171,7 +1171,7 @@ void u1_setup(ktb_plan* p) {
             throw Invalid("u1: staged slices need 16-byte aligned values");
         u1_dict_setup(p);
         const int smem = u1t_smem(p->ell_width);
-        KTB_CUDA(cudaFuncSetAttribute(k_u1t, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        allow_max_dynamic_smem(k_u1t);
         int occ = 0;
         KTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_u1t, kU1tWarps * 32, smem));
         p->ctas = static_cast<int64_t>(std::max(occ, 1)) * p->m->sm_count;

@@ -292,6 +292,12 @@ def run_ranks(world: int, fn):
             out[r] = fn(r)
         except BaseException as e:  # noqa: BLE001 (re-raised below)
             errs[r] = e
+            # the other ranks may now wait for this one forever: say why at once
+            import sys
+            import traceback
+
+            print(f"run_ranks: rank {r} failed:", file=sys.stderr)
+            traceback.print_exc()
 
     ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
     for t in ts:

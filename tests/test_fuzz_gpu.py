@@ -28,3 +28,15 @@ def test_every_plan_variant_fuzz():
                        capture_output=True, text=True, timeout=1200)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
     assert "all reproducible" in p.stdout
+
+
+def test_multi_gpu_data_plane_fuzz():
+    """tools/fuzz_dist.py on a fixed seed: the halo operator on random grids
+    (worlds 1-8 incl. one-plane slabs, every U1 form, the host-chunked call)
+    and the general split on random matrices (ranks without rows or ghosts),
+    loopback ranks running the native exchange code, against the oracle."""
+    env = dict(os.environ, FUZZ_WATCHDOG="600")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_dist.py"), "30", "4"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "of the oracle" in p.stdout

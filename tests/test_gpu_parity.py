@@ -842,3 +842,49 @@ def test_u3_warp_bss_tiles(K):
     torch.cuda.synchronize()
     assert_close(y.cpu().numpy(), O.spmv_ref(a.n, rp, ci, v, x), absax_of(a.n, rp, ci, v, x),
                  "cfg3 u3w")
+
+
+def test_plans_of_one_kernel_with_different_shared_memory_needs(K):
+    """The dynamic shared-memory opt-in is a per-kernel attribute, not a
+    per-plan one: a plan built later with a smaller need must not lower it
+    under an earlier plan's launches (U1 105 / 106 with different widths, S3
+    with different windows; found by tools/fuzz_dist.py as "invalid argument"
+    on loopback ranks)."""
+    rng = np.random.default_rng(8)
+
+    def banded(n, deltas):
+        rows = np.repeat(np.arange(n), len(deltas))
+        cols = rows + np.tile(deltas, n)
+        ok = (cols >= 0) & (cols < n)
+        rows, cols = rows[ok], cols[ok]
+        rp = np.zeros(n + 1, np.int64)
+        np.add.at(rp, rows + 1, 1)
+        return n, np.cumsum(rp), cols.astype(np.int64), np.where(rows == cols, 6.0, -1.0)
+
+    wide = banded(9000, [-600, -40, -3, -1, 0, 1, 3, 40])   # width 8
+    narrow = banded(9000, [-1, 0])                          # width 2
+    for prm in (105, 106):
+        plans, refs = [], []
+        for n, rp, ci, v in (wide, narrow):
+            plans.append((K.DevicePlan(K.CsrMatrix(n, rp, ci, v), K.UnsymKernel.u1_row, prm), n))
+            refs.append((n, rp, ci, v))
+        for (plan, n), (n_, rp, ci, v) in zip(plans, refs):  # the wide plan runs after the narrow setup
+            x = O.seeded_vector(n, 3)
+            y = np.full(n, np.nan)
+            plan.apply(x, y)
+            assert np.array_equal(y, O.spmv_ref(n, rp, ci, v, x)), prm
+    # S3: a wide-band symmetric matrix (large window), then a tridiagonal one
+    s_wide = matgen.stencil27_upper(20, 18, 16)
+    n2 = 7000
+    rp2 = np.arange(0, 2 * n2 + 1, 2, dtype=np.int64)
+    rp2[-1] = 2 * n2 - 1
+    ci2 = np.stack([np.arange(n2), np.arange(1, n2 + 1)], 1).ravel()[:2 * n2 - 1].astype(np.int64)
+    v2 = rng.uniform(-1, 1, len(ci2))
+    pa = K.DevicePlan(K.SymCsrMatrix(*s_wide), K.SymKernel.s3_nnz_zero_omit)
+    pb = K.DevicePlan(K.SymCsrMatrix(n2, rp2, ci2, v2), K.SymKernel.s3_nnz_zero_omit)
+    for plan, (n, rp, ci, v) in ((pa, s_wide), (pb, (n2, rp2, ci2, v2))):
+        x = O.seeded_vector(n, 5)
+        y = np.full(n, np.nan)
+        plan.apply(x, y)
+        erp, eci, ev = O.expand_symmetric(n, rp, ci, v)
+        assert_close(y, O.spmv_ref(n, erp, eci, ev, x), absax_of(n, erp, eci, ev, x), "s3")
