@@ -40,3 +40,15 @@ def test_multi_gpu_data_plane_fuzz():
                        capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
     assert "of the oracle" in p.stdout
+
+
+def test_gmres_and_ilu0_fuzz():
+    """tools/fuzz_krylov.py on a fixed seed: device GMRES(m) against the
+    oracle's restatement (+-2 iterations on solves of up to 200 iterations,
+    true residual < 1e-8 when converged) and ILU(0) factors and solves bitwise,
+    on random dominant matrices (n from 1 to 60,001, restart lengths 1-40)."""
+    env = dict(os.environ, FUZZ_WATCHDOG="600")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_krylov.py"), "30", "6"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "bitwise equal" in p.stdout
