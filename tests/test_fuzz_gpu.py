@@ -52,3 +52,16 @@ def test_gmres_and_ilu0_fuzz():
                        capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
     assert "bitwise equal" in p.stdout
+
+
+def test_integer_artefacts_and_selector_fuzz():
+    """tools/fuzz_artefacts.py on a fixed seed: row partitions (both schemes, P
+    up to 5,000 incl. P > n), BSS plans (jl up to 4,096 incl. jl > nnz),
+    reduction regions and expand_symmetric bit-exact against the oracle on
+    random matrices; the selector's report never holds a built candidate that
+    failed its check."""
+    env = dict(os.environ, FUZZ_WATCHDOG="600")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_artefacts.py"), "18", "7"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "bit-exact" in p.stdout
