@@ -868,7 +868,10 @@ int ktb_select(ktb_matrix* m, const ktb_select_opts* opts_in, void* stream, ktb_
         // the check: serial-order spmv_ref on the stored (GENERAL) or
         // expanded (SYM_UPPER, csr.hpp:88-123) matrix
         if (m->kind == KTB_SYM_UPPER) {
-            if (!m->expanded) m->expanded = expand_symmetric_dev(m, st);
+            {
+                std::lock_guard<std::mutex> lk(m->lazy_mu);
+                if (!m->expanded) m->expanded = expand_symmetric_dev(m, st);
+            }
             check_spmv_ref_order(m->expanded, x.p, ref.p, st);
         } else {
             check_spmv_ref_order(m, x.p, ref.p, st);

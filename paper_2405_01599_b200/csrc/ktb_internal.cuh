@@ -3,6 +3,7 @@
 
 #include <functional>
 #include <memory>
+#include <mutex>
 
 #include <cuda_runtime.h>
 
@@ -116,8 +117,11 @@ struct ktb_matrix {
     ktb::DBuf<int32_t> row_ptr;  // n+1
     ktb::DBuf<int32_t> col;      // nnz
     ktb::DBuf<double> val;       // nnz
-    // Lazily built: expanded full matrix (sym) for the selector's check.
+    // Lazily built (under lazy_mu: plans of one matrix may be set up from
+    // several host threads): expanded full matrix (sym) for the selector's
+    // check and S1 106.
     ktb_matrix* expanded = nullptr;
+    std::mutex lazy_mu;
     ~ktb_matrix();
 };
 

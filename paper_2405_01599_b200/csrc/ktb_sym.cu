@@ -107,7 +107,10 @@ void s12_setup(ktb_plan* p) {
         // the upper triangle's CRS). Deterministic, bitwise equal to
         // spmv_ref(expand_symmetric(A)); refused (Invalid) when a slice of the
         // expanded matrix has too many distinct (column delta, value) pairs.
-        if (!m->expanded) m->expanded = expand_symmetric_dev(m, p->stream);
+        {
+            std::lock_guard<std::mutex> lk(m->lazy_mu);
+            if (!m->expanded) m->expanded = expand_symmetric_dev(m, p->stream);
+        }
         p->long_plan = plan_create_internal(m->expanded, KTB_U1, 106, 0, p->stream);
         p->launches = 1;
         p->ctas = p->long_plan->ctas;

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -34,6 +35,8 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import _lib
+
+_DEV_LOCK = threading.Lock()  # lazy device uploads (CsrMatrix.dev)
 
 I64 = C.c_int64
 
@@ -151,7 +154,11 @@ class CsrMatrix:
 
     @property
     def dev(self) -> _DeviceMatrix:
-        if self._dev is None:
+        if self._dev is not None:
+            return self._dev
+        with _DEV_LOCK:  # one upload even when several threads ask at once
+            if self._dev is not None:
+                return self._dev
             # csr.hpp:39-43 length checks the C ABI cannot see
             require(self.n >= 0, "csr: negative dimension")
             require(len(self.row_ptr) == self.n + 1, "csr: row_ptr length != n+1")
@@ -164,7 +171,7 @@ class CsrMatrix:
                                                  self.values.ctypes.data, self._kind,
                                                  self.device, C.byref(h)))
             self._dev = _DeviceMatrix(h)
-        return self._dev
+            return self._dev
 
     def validate(self) -> None:
         _ = self.dev

@@ -65,3 +65,15 @@ def test_integer_artefacts_and_selector_fuzz():
                        capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
     assert "bit-exact" in p.stdout
+
+
+def test_concurrent_plan_setup_and_applies():
+    """tools/fuzz_threads.py: six host threads build plans of random variants
+    at the same time (on their own matrices and on one shared symmetric
+    matrix) and apply them on their own streams; every result equals the
+    oracle."""
+    env = dict(os.environ, FUZZ_WATCHDOG="600")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_threads.py"), "6", "3", "5"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "all equal to the oracle" in p.stdout
