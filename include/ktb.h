@@ -7,6 +7,12 @@
  * Every entry point names the reference interface it replaces
  * (paths relative to /root/reference/proj/include/ktune/).
  *
+ * Threading (the reference: one caller thread per WorkerPool, spmv.hpp:37-40):
+ * a matrix may be shared by plans set up and applied from several host
+ * threads at once (its lazily built members are created under a lock); one
+ * plan is used by one thread at a time (it owns scratch, staging buffers and
+ * a stream, like a WorkerPool). tools/fuzz_threads.py exercises both.
+ *
  * Index width: the reference's index_t is int64 (common.hpp:13); the host
  * side of this ABI takes int64 arrays unchanged and narrows to int32 on the
  * device, failing with KTB_ERR_INVALID if n or nnz >= 2^31.
