@@ -1,3 +1,9 @@
+"""Config 5 (GMRES(30), 128^3 convection-diffusion) solved 8 times on the selected
+SpMV plan: iterations, wall seconds and SpMV seconds per solve (host b in, host x
+out; the workspace is cached on the plan after the first solve).
+
+    python tools/gmres_repeat.py
+"""
 import time, sys
 sys.path.insert(0, '.')
 import numpy as np, torch
