@@ -4,7 +4,8 @@ runs of empty rows, one very long row; n from 1 to ~200,000): every U1 form
 (lanes, 100-106), the U2 / U3 / U4 variants in both CTA shapes, S1 / S2 / S3
 (both shapes) and S1 106. A plan either builds -- then |y - y_ref| <= 1e-12
 (|A||x|)_i on every row, bitwise for U1 100, 102-106 and S1 106, and bitwise
-reproducible on a second apply -- or is refused with a ktune error.
+reproducible on a second apply, U1 row sub-ranges leave the other rows
+untouched, the pipelined host batch agrees -- or is refused with a ktune error.
 
     python tools/fuzz_all.py [cases] [seed]
 """
@@ -79,7 +80,7 @@ def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     rng = np.random.default_rng(seed)
-    built = refused = 0
+    built = refused = subranges = batches = 0
     for c in range(cases):
         n, rp, ci, v = gen_unsym(rng, c)
         a = K.CsrMatrix(n, rp, ci, v)
@@ -100,6 +101,29 @@ def main():
             check((c, n, kern, prm), y, yref, absax, kern == 0 and (prm & (S - 1)) in BITWISE)
             assert np.array_equal(y, y2), (c, n, kern, prm, "not reproducible")
             built += 1
+            base = prm & (S - 1)
+            if kern == 0 and base != 101 and n > 1:  # row sub-range: rows outside stay untouched
+                import torch
+
+                r0 = int(rng.integers(0, n))
+                r1 = int(rng.integers(r0, n + 1))
+                xd = torch.from_numpy(x).cuda()
+                yd = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+                plan.apply_rows(r0, r1, xd, yd)
+                got = yd.cpu().numpy()
+                check((c, n, kern, prm, "rows", r0, r1), got[r0:r1], yref[r0:r1], absax[r0:r1],
+                      base in BITWISE)
+                assert np.isnan(got[:r0]).all() and np.isnan(got[r1:]).all(), (c, n, kern, prm, r0, r1)
+                subranges += 1
+            if (c + len(UNSYM_PLANS) + prm) % 7 == 0:  # the pipelined host batch: 3 vectors
+                X = np.stack([O.seeded_vector(n, 300 + c + k) for k in range(3)])
+                Y = np.full((3, n), np.nan)
+                plan.apply_host_pipelined(X, Y)
+                for k in range(3):
+                    yk = O.spmv_ref(n, rp, ci, v, X[k])
+                    ak = O.spmv_ref(n, rp, ci, np.abs(v), np.abs(X[k]))
+                    check((c, n, kern, prm, "batch", k), Y[k], yk, ak, kern == 0 and base in BITWISE)
+                batches += 1
         if c % 3 == 0:  # symmetric: the upper triangle of a random pattern, or a stencil
             if c % 2:
                 g = [int(q) for q in rng.integers(3, 30, 3)]
@@ -126,7 +150,8 @@ def main():
                 if kern == 18 or prm == 106:  # S3 and S1 106 are deterministic
                     assert np.array_equal(y, y2), (c, ns, kern, prm, "not reproducible")
                 built += 1
-    print(f"fuzz_all: {cases} cases, seed {seed}: {built} plans built and checked, {refused} refused; all within "
+    print(f"fuzz_all: {cases} cases, seed {seed}: {built} plans built and checked ({subranges} row sub-ranges, "
+          f"{batches} pipelined host batches), {refused} refused; all within "
           "1e-12 (|A||x|)_i of the oracle (U1 100, 102-106 and S1 106 bitwise), all reproducible")
 
 
