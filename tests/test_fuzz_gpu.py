@@ -77,3 +77,14 @@ def test_concurrent_plan_setup_and_applies():
                        capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
     assert "all equal to the oracle" in p.stdout
+
+
+def test_lanczos_fuzz():
+    """tools/fuzz_lanczos.py on a fixed seed: restarted Lanczos on an S3 plan
+    against numpy's dense eigendecomposition (random stencils and random
+    sparse symmetric matrices, the k largest-magnitude eigenvalues to 1e-8)."""
+    env = dict(os.environ, FUZZ_WATCHDOG="600")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_lanczos.py"), "10", "3"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    assert "eigenproblems" in p.stdout

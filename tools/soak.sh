@@ -11,6 +11,7 @@ for s in $(seq 101 112); do
   timeout 1000 python tools/fuzz_krylov.py 60 $s 2>&1 | tail -1 >> $O/soak.txt
   timeout 1000 python tools/fuzz_artefacts.py 30 $s 2>&1 | tail -1 >> $O/soak.txt
   timeout 1000 python tools/fuzz_threads.py 8 4 $s 2>&1 | tail -1 >> $O/soak.txt
+  timeout 1000 python tools/fuzz_lanczos.py 12 $s 2>&1 | tail -1 >> $O/soak.txt
 done
 for s in 201 202 203; do
   KTB_LIB_NAME=libktb_chaos.so timeout 1000 python tools/fuzz_all.py 36 $s 2>&1 | tail -1 >> $O/soak.txt
