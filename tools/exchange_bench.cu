@@ -324,7 +324,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 constexpr int kLoadBytes = 112 * 1024;
 // variant 16's exchange with a concurrent HBM stream per CTA
-template <bool kAfter, int kChunks, int kPf = 0>
+template <bool kAfter, int kChunks, int kPf = 0, int kPace = 0>
 __global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double* out, long long tag0,
                                                   const char* src, long long src_bytes) {
     extern __shared__ __align__(128) unsigned char buf[];
@@ -373,7 +373,27 @@ __global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double*
         const long long tag = tag0 + q;
         constexpr int S = 8;
         double2* sl = slots + static_cast<long long>(q & 1) * (nb + 8) * S;
-        if (tid == 0) {
+        if (kPace > 0) {
+            // warp 1 feeds the copy in paced chunks so that warp 0's poll loads never
+            // queue behind the whole slice's requests
+            if (tid == 32) {
+                constexpr int kChunk = kLoadBytes / kChunks;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                             "r"(kLoadBytes)
+                             : "memory");
+                for (int ch = 0; ch < kChunks; ++ch) {
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            smem_u32(buf) + ch * kChunk),
+                        "l"(src + off + ch * kChunk), "r"(kChunk), "r"(smem_u32(&bar))
+                        : "memory");
+                    __nanosleep(kPace);
+                }
+                off += static_cast<long long>(nb) * kLoadBytes;
+                if (off + kLoadBytes > src_bytes) off = static_cast<long long>(blockIdx.x) * kLoadBytes;
+            }
+            if (tid == 0) st_cg(sl + blockIdx.x * S, make_double2(p, __longlong_as_double(tag)));
+        } else if (tid == 0) {
             if (!kAfter) issue();
             st_cg(sl + blockIdx.x * S, make_double2(p, __longlong_as_double(tag)));
         }
@@ -405,18 +425,18 @@ __global__ void __launch_bounds__(kT, 1) k_loaded(int k, double2* slots, double*
     if (blockIdx.x == 0 && tid == 0) out[0] = c;
 }
 
-template <bool kAfter, int kChunks, int kPf = 0>
+template <bool kAfter, int kChunks, int kPf = 0, int kPace = 0>
 static void run_loaded(int nb, int k, double2* slots, double* out, long long& tag, const char* src,
                        long long src_bytes) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    cudaFuncSetAttribute(k_loaded<kAfter, kChunks, kPf>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLoadBytes);
+    cudaFuncSetAttribute(k_loaded<kAfter, kChunks, kPf, kPace>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLoadBytes);
     float best = 1e30f;
     for (int rep = 0; rep < 6; ++rep) {
         void* args[] = {&k, &slots, &out, &tag, &src, &src_bytes};
         cudaEventRecord(a);
-        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loaded<kAfter, kChunks, kPf>), dim3(nb),
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_loaded<kAfter, kChunks, kPf, kPace>), dim3(nb),
                                     dim3(kT), args, kLoadBytes, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
@@ -426,8 +446,8 @@ static void run_loaded(int nb, int k, double2* slots, double* out, long long& ta
         if (rep > 0 && ms < best) best = ms;
     }
     const cudaError_t e = cudaGetLastError();
-    printf("variant %d (%d chunks, L2 prefetch %d ahead): %8.3f us per reduction (k = %d, %d CTAs, %.1f TB/s streamed) %s\n",
-           kAfter ? 21 : 20, kChunks, kPf, best * 1e3 / k, k, nb,
+    printf("variant %d (%d chunks, L2 prefetch %d ahead, pace %d ns): %8.3f us per reduction (k = %d, %d CTAs, %.1f TB/s streamed) %s\n",
+           kAfter ? 21 : 20, kChunks, kPf, kPace, best * 1e3 / k, k, nb,
            double(kLoadBytes) * nb / (best * 1e-3 / k) / 1e12,
            e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
@@ -500,5 +520,9 @@ int main() {
     run_loaded<false, 1, 1>(sms, k, slots, out, tag, src, src_bytes);
     run_loaded<false, 1, 2>(sms, k, slots, out, tag, src, src_bytes);
     run_loaded<false, 1, 3>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 8, 0, 100>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 8, 0, 250>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 16, 0, 150>(sms, k, slots, out, tag, src, src_bytes);
+    run_loaded<false, 4, 0, 500>(sms, k, slots, out, tag, src, src_bytes);
     return 0;
 }
