@@ -8,8 +8,11 @@ Default workload = config 4 (BASELINE.json configs[3], the one quoted "at
 z-planes over the ranks with a one-plane x halo. One step = one y = A*x
 through libktb's native halo operator (ktb_halo_spmv: NCCL group on a
 high-priority stream overlapped with the interior rows, boundary planes after
-an event wait; U1 thread-per-row over the warp-sliced copy, bitwise equal to
-the reference's spmv_ref). The same code path runs at every N.
+an event wait; the rows by U1 param 106 -- persistent warps over pair-coded
+records, falling back to 105 / 104 / 100 when a layout is refused -- bitwise
+equal to the reference's spmv_ref). The same code path runs at every N.
+`e2e` = the public host call (host x in, host y out, copies inside the timed
+region), timed after 0.5 s of untimed calls of the same kind.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
                     [--config 1|2|3|4|5] [--shard] [--ref-build release|native|parity]
