@@ -122,6 +122,8 @@ class L2Flush:
 
 L2_NOTE = ("cold: before every timed step a 2x L2 buffer is written, then a second 2x L2 "
            "buffer is read (dirty lines written back outside the per-step event pairs)")
+# the same string in both arms' `config` (so the two lines name one config)
+L2_BOTH = ("GPU arm: " + L2_NOTE + "; CPU reference arm: n/a (inputs resident in host memory)")
 
 
 def min_bytes(n: int, nnz: int) -> int:
@@ -383,10 +385,12 @@ def cpu_baseline(args, seconds=10.0):
                 "sample": f"unavailable: {e}"}
 
 
-def config_block(cfg, kernel):
-    return {"workload": cfg["workload"], "kernel": kernel,
+def config_block(cfg):
+    """The workload, identical in both arms' lines; what an arm ran it with
+    (kernel, partitioning) goes into its `run` key."""
+    return {"workload": cfg["workload"],
             "x": f"seeded_vector(n, {cfg['seed']})",
-            "l2": L2_NOTE,
+            "l2": L2_BOTH,
             "bytes_model": "12*nnz + 4*(n+1) + 16*n (int32 idx, fp64 val, x read once, y written once)"}
 
 
@@ -426,8 +430,9 @@ def run_reference(args, cfg):
         "higher_is_better": True, "scaling": "strong" if args.config == 4 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-        "config": dict(config_block(cfg, f"reference {eng.selected['name']}"),
-                       l2="n/a (host CPU; inputs resident in host memory)"),
+        "config": config_block(cfg),
+        "run": {"kernel": f"reference {eng.selected['name']}",
+                "parallelism": f"{eng.selected['workers']} OpenMP workers, one host"},
         "impl": "reference",
         "gflops": flops(n, nnz, cfg["sym"]) / t / 1e9,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
@@ -553,8 +558,8 @@ def run_gpu(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded; replicas per rank)",
-            "config": dict(config_block(cfg, f"{sel.name} (param {sel.jl})"),
-                           parallelism=f"replicas x{ws}"),
+            "config": config_block(cfg),
+            "run": {"kernel": f"{sel.name} (param {sel.jl})", "parallelism": f"replicas x{ws}"},
             "gflops": ws * F / (ms / 1e3) / 1e9,
             "pct_hbm_peak": 100.0 * achieved / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -701,9 +706,9 @@ def run_halo(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-            "config": dict(config_block(cfg, f"{U1_DESC.get(u1p, 'u1')} (param {u1p}), "
-                                             "ktb_halo_spmv"),
-                           parallelism=f"row-block z-slabs x{ws}, one-plane halo, NCCL P2P"),
+            "config": config_block(cfg),
+            "run": {"kernel": f"{U1_DESC.get(u1p, 'u1')} (param {u1p}), ktb_halo_spmv",
+                    "parallelism": f"row-block z-slabs x{ws}, one-plane halo, NCCL P2P"},
             "gflops": F / (ms / 1e3) / 1e9,
             "per_gpu_gbs": B / ws / (ms / 1e3) / 1e9,
             "pct_hbm_peak_per_gpu": 100.0 * B / ws / (ms / 1e3) / 1e9 / peak,
@@ -845,9 +850,9 @@ def run_general_shard(args, cfg):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (SURVEY.md §8d recipe, seeded)",
-                "config": dict(config_block(cfg, f"{sp.kernel_name()} on A_d + k_ghost_acc "
-                                                 "(ktb_dist_spmv)"),
-                               parallelism=f"NNZ_BALANCED row blocks x{ws}, ghost exchange"),
+                "config": config_block(cfg),
+                "run": {"kernel": f"{sp.kernel_name()} on A_d + k_ghost_acc (ktb_dist_spmv)",
+                        "parallelism": f"NNZ_BALANCED row blocks x{ws}, ghost exchange"},
                 "gflops": F / (ms / 1e3) / 1e9, "exchange_ms": halo,
                 "roofline": {"bound": "hbm", "achieved": B / ws / (ms / 1e3) / 1e9,
                              "peak": peak, "unit": "GB/s",
@@ -990,9 +995,9 @@ def run_gmres(args, cfg):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8d recipe)",
                 "config": {"workload": "cfg5: GMRES(30)+MGS, 128^3 7-pt convection-diffusion, "
                                        "b = A*ones, tol 1e-8, max 3000 its",
-                           "kernel": kname, "parallelism": par,
                            "value_def": "algorithmic SpMV bytes x SpMV calls / SpMV device "
                                         "seconds inside the solve"},
+                "run": {"kernel": kname, "parallelism": par},
                 "gmres": info,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak,
